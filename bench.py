@@ -1,0 +1,416 @@
+"""Benchmark: FastKroneckerRegression solve time at BASELINE config 3 (n=16384, d=64).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c3]
+
+One step = one ``fast_kronecker_regression`` solve (SolveReport.wall_time semantics of the
+reference: sampling + preprocessing + Richardson, loss excluded) on the BASELINE inputs
+(A1, A2 ~ N(1, var 1e-3) seed 0, b = ones(n^2), lam=1e-3, eps=0.1, delta=0.01, alpha=1e-5).
+
+  value  -- device-resident inputs, CUDA-event time per solve (max over ranks), seconds.
+  e2e    -- the public API called with HOST inputs (numpy factors, pinned host b): wall time of
+            the solve including every host<->device transfer it makes (factors up, sampled b
+            entries up, indices/x down); loss excluded as in the reference.
+  roofline -- dominant kernel (the fused sketched normal-operator apply of the Richardson loop)
+            at algorithmic FLOPs / measured FP64 peak; KronMatMul (exact baseline n^2 pass) and
+            the loss pass are reported alongside under "kernels".
+  cpu_baseline -- the oracle port of the reference (NumPy/OpenBLAS) on this host's cores.
+
+``--impl reference`` times the reference's CPU implementation (oracle port) instead.
+Under torchrun (N>1) every rank solves the same problem (replicas) and rank 0
+reports the max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIGS = {
+    "c1": (1024, 16), "c2": (4096, 32), "c3": (16384, 64),
+}
+METRIC = "FastKronReg solve time (s) at n=16384,d=64"
+PARAMS = dict(eps=0.1, delta=0.01, lam=1e-3, alpha=1e-5, seed=0)
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def make_inputs(n, d):
+    from oracle import kronsolve_oracle as O  # generator only (experiments.py:106-115)
+    import numpy as np
+    rng = np.random.default_rng(0)
+    facs = [rng.normal(1.0, math.sqrt(0.001), (n, d)) for _ in range(2)]
+    return facs
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        cmd = ["nvidia-smi", f"--id={self.index}",
+               "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+               "--format=csv,noheader,nounits", "-lms", "100"]
+        try:
+            self.proc = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm = [float(s[0]) for s in self.samples if len(s) >= 8 and s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if len(s) >= 8 and s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            if len(s) >= 8:
+                for nm, v in zip(names, s[4:8]):
+                    if v.lower() == "active":
+                        reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "samples": len(self.samples), "reasons": sorted(reasons)}
+
+
+def fp64_peak_tflops():
+    """Measured FP64 (DMMA) peak of this pool's B200s (tools/fp64_peak.cu, profiles/r01_fp64_peak.txt)."""
+    p = ROOT / "profiles" / "r01_fp64_peak.txt"
+    best = None
+    if p.exists():
+        for line in p.read_text().splitlines():
+            if line.startswith("{") and '"dmma' in line:
+                try:
+                    v = json.loads(line)["tflops"]
+                    best = v if best is None else max(best, v)
+                except Exception:
+                    pass
+    return best or 37.1
+
+
+def hbm_peak_gbs():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return float(json.loads(p.read_text())["hbm_gbs"]), "MEASURED_PEAKS.json"
+        except Exception:
+            pass
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def flush_l2(buf):
+    buf.add_(1.0)
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import paper_2209_04876_b200 as K
+    from paper_2209_04876_b200 import _lib, _device as D
+    from paper_2209_04876_b200.solvers import FastSolveTrace
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    n, d = CONFIGS[args.config]
+    facs_h = make_inputs(n, d)
+    facs = [torch.tensor(a, device="cuda") for a in facs_h]
+    b = torch.ones(n * n, dtype=torch.float64, device="cuda")
+    cfg = K.RegressionConfig(**PARAMS)
+    l2 = torch.zeros(64 * 1024 * 1024, dtype=torch.float64, device="cuda")  # 512 MB > 126 MB L2
+
+    def barrier():
+        if ws > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        K.fast_kronecker_regression(facs, b, cfg)
+    barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    times = []
+    stream = torch.cuda.current_stream()
+    for _ in range(args.steps):
+        flush_l2(l2)
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        rep = K.fast_kronecker_regression(facs, b, cfg)
+        e1.record(stream)
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1) / 1e3)
+    barrier()
+    clk = clocks.stop()
+    t_step = sum(times) / len(times)
+    if ws > 1:
+        t = torch.tensor([t_step], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        t_step = float(t.item())
+    x_loss = rep.loss
+
+    # ---- e2e through the public API with host inputs (pinned b, numpy factors)
+    b_host = torch.ones(n * n, dtype=torch.float64).pin_memory()
+    e2e = []
+    for i in range(max(2, min(args.steps, 5))):
+        r = K.fast_kronecker_regression(facs_h, b_host, cfg)
+        if i > 0:
+            e2e.append(r.wall_time)
+    t0 = time.perf_counter()
+    r_full = K.fast_kronecker_regression(facs_h, b_host, cfg)
+    e2e_full = time.perf_counter() - t0
+    nnz = int(np.asarray(r_full.solution).size)  # placeholder replaced below
+
+    # ---- stage / kernel timing (outside the timed region)
+    tr = FastSolveTrace()
+    K.fast_kronecker_regression(facs, b, cfg, _trace=tr)
+    nnz = tr.sdiag.nnz
+    kernels = stage_timings(K, facs, b, cfg, tr, n, d)
+    launches = count_launches(K, facs, b, cfg)
+
+    result = None
+    if rank == 0:
+        peak = fp64_peak_tflops()
+        rich = kernels["richardson_apply"]
+        result = {
+            "metric": METRIC, "value": t_step, "unit": "s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": False,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"fast_kronecker_regression {args.config}: n={n}, d={d}, N=2, b=ones(n^2), "
+                                   "lam=1e-3, eps=0.1, delta=0.01, alpha=1e-5, seed=0",
+                       "n": n, "d": d, "sample_count": rep.sample_count, "iterations": rep.iterations,
+                       "nnz": nnz, "parallelism": f"replicas{ws}" if ws > 1 else "single",
+                       "l2": "flushed (512 MB write) before every timed solve"},
+            "loss": x_loss,
+            "e2e": {"value": statistics.median(e2e), "unit": "s",
+                    "h2d_bytes_per_step": 2 * n * d * 8 + nnz * 8,
+                    "d2h_bytes_per_step": nnz * 8 + d * d * 8,
+                    "note": "public API, numpy factors + pinned host b; SolveReport.wall_time (loss excluded "
+                            "as in the reference); only sampled entries of b cross PCIe",
+                    "full_call_with_loss_s": e2e_full},
+            "roofline": {"bound": "tensor", "kernel": "sketched normal-operator apply (Richardson)",
+                         "achieved": rich["tflops"], "peak": peak, "unit": "TFLOP/s",
+                         "frac": rich["tflops"] / peak, "traffic": None,
+                         "peak_source": "measured FP64 DMMA peak, profiles/r01_fp64_peak.txt",
+                         "algorithmic_flops_per_launch": rich["flops"],
+                         "launch_us": rich["us"]},
+            "kernels": kernels,
+            "gpu_launches": launches * args.steps,
+            "gpu_launches_per_step": launches,
+            "clocks": clk,
+        }
+        if not args.skip_cpu:
+            result["cpu_baseline"] = cpu_baseline(args.config, args.cpu_reps)
+    if ws > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+    return result
+
+
+def _timed(fn, reps=5):
+    import torch
+    fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn()
+        e1.record()
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1) * 1e3)
+    return statistics.median(ts)
+
+
+def stage_timings(K, facs, b, cfg, tr, n, d):
+    """Per-kernel device times (CUDA events on the launching stream) and roofline numbers."""
+    import ctypes
+    import torch
+    from paper_2209_04876_b200 import _lib, _device as D
+    from paper_2209_04876_b200.kron import _view_for
+    peak = fp64_peak_tflops()
+    hbm, _ = hbm_peak_gbs()
+    out = {}
+    sd = tr.sdiag
+    view = _view_for(facs, sd)
+    nnz, u1 = view.nnz, view.u_left
+    X = torch.randn(view.dL, view.dR, dtype=torch.float64, device="cuda")
+    from paper_2209_04876_b200 import _lib as L
+    np_ = (u1 + 31) // 32
+    part = torch.empty(np_ * view.dL * view.dR + 1, dtype=torch.float64, device="cuda")
+    G = torch.empty(view.dL, view.dR, dtype=torch.float64, device="cuda")
+    bv = torch.randn(nnz, dtype=torch.float64, device="cuda")
+
+    def rich_once():
+        L.call("ks_sketched_transpose_apply", ctypes.byref(view.struct), D.p(bv), D.p(None), D.p(G), D.stream())
+
+    # fused normal apply == transpose apply + the y / dot work; time the Richardson loop per iteration
+    from paper_2209_04876_b200.solvers import _fast_solve_dev
+    VL = torch.eye(view.dL, dtype=torch.float64, device="cuda")
+    VR = torch.eye(view.dR, dtype=torch.float64, device="cuda")
+    dinv = torch.ones(view.dL * view.dR, dtype=torch.float64, device="cuda")
+    rhs = torch.randn(view.dL, view.dR, dtype=torch.float64, device="cuda")
+    x = torch.empty(view.dL, view.dR, dtype=torch.float64, device="cuda")
+    hist = torch.zeros(64, dtype=torch.float64, device="cuda")
+    it = ctypes.c_int32(0)
+    hl = ctypes.c_int32(0)
+    iters = 24
+
+    def loop():
+        L.load().ks_richardson_sketched(ctypes.byref(view.struct), D.p(VL), D.p(VR), D.p(dinv), D.p(rhs), 1e-3, 0.5,
+                                        iters, 1e-300, D.p(x), D.p(hist), ctypes.byref(it), ctypes.byref(hl),
+                                        D.stream())
+
+    us_loop = _timed(loop, 3)
+    us_t = _timed(rich_once, 5)
+    d2 = d * d
+    flops_apply = 4.0 * u1 * d2 + 4.0 * nnz * d  # y + G GEMMs over distinct left rows + per-sample dots/axpys
+    flops_iter = flops_apply + 8.0 * d ** 3
+    out["richardson_loop"] = {"us": us_loop, "iterations": iters, "us_per_iter": us_loop / iters,
+                              "flops_per_iter": flops_iter,
+                              "tflops": flops_iter * iters / (us_loop * 1e-6) / 1e12}
+    out["richardson_apply"] = {"us": us_loop / iters, "flops": flops_apply,
+                               "tflops": flops_apply / (us_loop / iters * 1e-6) / 1e12,
+                               "note": "per Richardson iteration (apply + reduce + preconditioner + update)"}
+    out["transpose_apply"] = {"us": us_t, "flops": 2.0 * u1 * d2 + 2.0 * nnz * d,
+                              "tflops": (2.0 * u1 * d2 + 2.0 * nnz * d) / (us_t * 1e-6) / 1e12}
+    # KronMatMul n^2 pass of the exact solver: T = U1^T B U2
+    U1, U2 = facs
+    T = torch.empty(d, d, dtype=torch.float64, device="cuda")
+
+    def kmm():
+        L.call("ks_kron2_contract", D.p(U1), D.p(b), n, D.p(U2), n, n, d, d, D.p(T), D.stream())
+
+    us_k = _timed(kmm, 5)
+    fl = 2.0 * n * n * d + 2.0 * n * d * d
+    by = 8.0 * n * n
+    out["kronmatmul"] = {"us": us_k, "flops": fl, "bytes": by, "tflops": fl / (us_k * 1e-6) / 1e12,
+                         "gbs": by / (us_k * 1e-6) / 1e9, "frac_fp64": fl / (us_k * 1e-6) / 1e12 / peak,
+                         "frac_hbm": by / (us_k * 1e-6) / 1e9 / hbm,
+                         "bound": "fp64" if fl / (peak * 1e12) > by / (hbm * 1e9) else "hbm"}
+    Xs = torch.randn(d, d, dtype=torch.float64, device="cuda")
+    o = torch.empty(1, dtype=torch.float64, device="cuda")
+
+    def loss():
+        L.call("ks_kron2_residual_sumsq", D.p(U1), D.p(Xs), D.p(U2), D.p(b), n, n, n, d, d, D.p(o), D.stream())
+
+    us_l = _timed(loss, 5)
+    out["loss_pass"] = {"us": us_l, "flops": fl, "bytes": by, "tflops": fl / (us_l * 1e-6) / 1e12,
+                        "frac_fp64": fl / (us_l * 1e-6) / 1e12 / peak}
+    return out
+
+
+def count_launches(K, facs, b, cfg):
+    """Kernels of libkronsolve_b200.so launched by one solve (torch profiler, outside timing)."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        K.fast_kronecker_regression(facs, b, cfg)
+        torch.cuda.synchronize()
+    ours = 0
+    for ev in prof.events():
+        if ev.device_type == torch.autograd.DeviceType.CUDA:
+            name = ev.name
+            if "_kernel" in name and not name.startswith(("void at::", "at::", "void (anonymous namespace)::elementwise")):
+                ours += 1
+    return ours
+
+
+def cpu_baseline(config, reps):
+    """Oracle port of the reference (NumPy/OpenBLAS) on this host's cores."""
+    from oracle import kronsolve_oracle as O
+    n, d = CONFIGS[config]
+    facs, b = O.synth_regression(n, d, 2, 0)
+    ts = []
+    for _ in range(reps):
+        rep = O.fast_kronecker_regression(facs, b, with_loss=False, **PARAMS)
+        ts.append(rep.wall_time)
+    return {"value": statistics.median(ts), "unit": "s", "cores": os.cpu_count(), "kind": "port",
+            "sample": f"{reps} full fast_kronecker_regression solves at {config} (oracle/kronsolve_oracle.py, "
+                      "NumPy 2.3.5 + OpenBLAS threads = all host cores), median wall_time"}
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return None
+    from oracle import kronsolve_oracle as O
+    n, d = CONFIGS[args.config]
+    facs, b = O.synth_regression(n, d, 2, 0)
+    for _ in range(args.warmup):
+        O.fast_kronecker_regression(facs, b, with_loss=False, **PARAMS)
+    ts = []
+    t_wall0 = time.perf_counter()
+    for _ in range(args.steps):
+        rep = O.fast_kronecker_regression(facs, b, with_loss=False, **PARAMS)
+        ts.append(rep.wall_time)
+    _ = time.perf_counter() - t_wall0
+    v = sum(ts) / len(ts)
+    return {"metric": METRIC, "value": v, "unit": "s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": f"fast_kronecker_regression {args.config}: n={n}, d={d}, N=2, b=ones(n^2), "
+                                   "lam=1e-3, eps=0.1, delta=0.01, alpha=1e-5, seed=0", "n": n, "d": d},
+            "cpu_baseline": {"value": v, "unit": "s", "cores": os.cpu_count(), "kind": "port",
+                             "sample": f"{args.steps} full solves (oracle port of the reference, NumPy/OpenBLAS, "
+                                       "all host threads)"},
+            "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--cpu-reps", type=int, default=3)
+    ap.add_argument("--skip-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    res = run_reference(args) if args.impl == "reference" else run_ours(args)
+    if res is not None:
+        print(json.dumps(res))
+
+
+if __name__ == "__main__":
+    main()

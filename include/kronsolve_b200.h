@@ -1,0 +1,215 @@
+/*
+ * kronsolve_b200 -- C-ABI of the B200-native (sm_100a, FP64) FastKroneckerRegression hot path.
+ *
+ * Drop-in boundary.  The reference (arXiv 2209.04876, package `kronsolve`) has no FFI: its
+ * boundary is the set of Python functions re-exported by pkg/src/kronsolve/__init__.py:3-73.
+ * Every entry point below is the device half of one of those functions; the Python mirror in
+ * paper_2209_04876_b200/ keeps the reference signature and calls these through ctypes
+ * (see INTEGRATION.md).  Each entry cites the reference function it replaces.
+ *
+ * Conventions
+ *   - All matrices are row-major float64 in device memory (HBM); indices are int64.
+ *   - `stream` is a cudaStream_t passed as void*; every call is asynchronous on that stream
+ *     unless it documents a host output (it then synchronises the stream).
+ *   - Return value: KS_OK or one of the KS_E* codes; ks_last_error() gives a thread-local
+ *     message.  The Python shim maps KS_EINVAL -> InvalidInputError, KS_ESIZE ->
+ *     SizeGuardError, KS_ENUMERICAL / KS_EDIVERGED -> NumericalFailureError, KS_ECUDA ->
+ *     KronsolveError (reference errors.py:4-37).
+ *   - Scratch memory is stream-ordered (cudaMallocAsync on the device's default pool).
+ *   - No entry point falls back to the CPU.
+ */
+#ifndef KRONSOLVE_B200_H
+#define KRONSOLVE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KS_OK 0
+#define KS_EINVAL 1
+#define KS_ESIZE 2
+#define KS_ENUMERICAL 3
+#define KS_ECUDA 4
+#define KS_EDIVERGED 5
+
+#define KS_ABI_VERSION 1
+
+int ks_abi_version(void);
+const char* ks_last_error(void);
+
+/* ---------------------------------------------------------------- dense primitives */
+
+/* Batched strided GEMM: C[b] = alpha * A[b](MxK) * B[b](KxN) + beta * C[b].
+ * Element (i,j) of X lives at X[i*x_rs + j*x_cs + b*x_bs].  General building block of the
+ * implicit Kronecker multiplies (reference kron.py:66-77 tensordot / matmul). */
+int ks_gemm(int64_t M, int64_t N, int64_t K, double alpha,
+            const double* A, int64_t a_rs, int64_t a_cs, int64_t a_bs,
+            const double* B, int64_t b_rs, int64_t b_cs, int64_t b_bs,
+            double beta, double* C, int64_t c_rs, int64_t c_cs, int64_t c_bs,
+            int64_t batch, void* stream);
+
+/* Deterministic split-K product C(MxN) = alpha * A^T B for tall A (KxM), B (KxN), M,N <= 128.
+ * Element (k,m) of A at A[k*a_ks + m*a_ms]; (k,n) of B at B[k*b_ks + n*b_ns].
+ * Replaces the Gram / projection products a.T @ a (solvers.py:146, :439) and g @ a_tilde
+ * (leverage.py:127). */
+int ks_gemm_tn_tall(int64_t M, int64_t N, int64_t K, double alpha,
+                    const double* A, int64_t a_ks, int64_t a_ms,
+                    const double* B, int64_t b_ks, int64_t b_ns,
+                    double* C, void* stream);
+
+/* out = (F_0 kron ... kron F_{nf-1}) b with b of shape (prod cols, ncols), row-major.
+ * Replaces kron.kron_mat_mul (kron.py:44-77) and kron_vec_square (kron.py:80-100). */
+int ks_kron_mat_mul(int32_t nf, const double* const* factors, const int64_t* rows,
+                    const int64_t* cols, const double* b, int64_t ncols, double* out,
+                    void* stream);
+
+/* K1: T(p x q) = L^T (m x p) . B (m x k, leading dim ldb) . R (k x q).
+ * The n^2 pass of kronmatmul_svd_solve: kron_mat_mul([U1^T, U2^T], b) (solvers.py:314). */
+int ks_kron2_contract(const double* L, const double* B, int64_t ldb, const double* R,
+                      int64_t m, int64_t k, int32_t p, int32_t q, double* T, void* stream);
+
+/* K2: out[0] = sum_{i,j} ((L X R^T)[i,j] - B[i,j])^2 without materialising K x.
+ * L: m x p, X: p x q, R: k x q, B: m x k.  The n^2 pass of ridge_loss (solvers.py:251-262). */
+int ks_kron2_residual_sumsq(const double* L, const double* X, const double* R,
+                            const double* B, int64_t ldb, int64_t m, int64_t k, int32_t p,
+                            int32_t q, double* out, void* stream);
+
+/* out[0] = sum (a - b)^2 (b may be NULL -> sum a^2).  Deterministic. */
+int ks_sumsq_diff(const double* a, const double* b, int64_t n, double* out, void* stream);
+
+/* flags[0] = any non-finite entry, flags[1] = any nonzero entry (int32, device).
+ * Mirrors tensor.as_matrix (tensor.py:35-42) and solvers._validated_problem (:265-274). */
+int ks_check_finite_nonzero(const double* a, int64_t n, int32_t* flags, void* stream);
+
+/* ---------------------------------------------------------------- small dense (d <= 128) */
+
+/* R factor (d x d, upper) of a Householder TSQR of A (n x d).  Rows beyond n zero-padded. */
+int ks_qr_r(const double* A, int64_t n, int32_t d, double* R, void* stream);
+
+/* One-sided Jacobi SVD of a d x d matrix M: sigma descending (d), V (d x d, row-major,
+ * column j = right singular vector j).  Used for compact_svd (tensor.py:76-107) via QR and
+ * for factor_gram's eigendecomposition of a PSD Gram (solvers.py:143-150). */
+int ks_svd_small(const double* M, int32_t d, double* sigma, double* V, void* stream);
+
+/* X = M^-1 for a d x d matrix (LU with partial pivoting, LAPACK getrf pivot rule).
+ * info (device int32[2]): info[0] = k+1 if pivot k is exactly zero (np.linalg.solve's
+ * LinAlgError, leverage.py:114-119), info[1] = 1 if X has non-finite entries (:120-123). */
+int ks_inverse_small(const double* M, int32_t d, double* X, int32_t* info, void* stream);
+
+/* Thin SVD of A (n x d): U (n x d), sigma (d, descending), V (d x d).  Columns past the
+ * numerical rank (sigma <= rank_tol*sigma_max) are zeroed and *rank (host) reports it.
+ * Replaces tensor.compact_svd (tensor.py:76-107).  Synchronises the stream. */
+int ks_compact_svd(const double* A, int64_t n, int32_t d, double rank_tol, double* U,
+                   double* sigma, double* V, int32_t* rank, void* stream);
+
+/* ---------------------------------------------------------------- NumPy-exact random streams */
+
+/* out[i] = Generator.random() draw number (skip + i) of a PCG64 stream with the given
+ * 128-bit state/increment ((raw >> 11) * 2^-53).  Bit-exact with numpy.random.PCG64. */
+int ks_pcg64_random(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
+                    uint64_t skip, int64_t count, double* out, void* stream);
+
+/* out[i] = Generator.standard_normal() draw i / divisor (ziggurat; tables from the installed
+ * NumPy, passed in ki[256] (uint64), wi[256], fi[256] on the device).  Bit-exact with
+ * numpy.random.Generator(PCG64).standard_normal except for ulp-level differences of libm
+ * log1p/exp in the (rare) tail branch.  Replaces the host draw of leverage.py:124-126. */
+int ks_pcg64_standard_normal(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
+                             uint64_t inc_lo, int64_t count, double divisor,
+                             const uint64_t* ki, const double* wi, const double* fi,
+                             double* out, void* stream);
+
+/* ---------------------------------------------------------------- leverage scores & sampling */
+
+/* scores[i] = ||Q a_i||^2 / denom for rows a_i of A (n x d), Q (r x d).
+ * JL estimator body of approx_leverage_scores_jl (leverage.py:114-129). */
+int ks_jl_scores(const double* A, int64_t n, int32_t d, const double* Q, int32_t r,
+                 double denom, double* scores, void* stream);
+
+/* exact statistical leverage scores: scores[i] = sum_k U[i,k]^2 * wts[k] (leverage.py:51-64) */
+int ks_row_weighted_sumsq(const double* U, int64_t n, int32_t d, const double* wts,
+                          double* scores, void* stream);
+
+/* ProductSampler per-factor tables (leverage.py:159-175): total = pairwise sum (NumPy order),
+ * probs = scores / total, cdf = sequential cumsum (bit-exact, parallel verified scan).
+ * flags[0]: 1 if any score < 0 or non-finite, 2 if total <= 0.  If renormalise != 0 the cdf is
+ * additionally divided by its last entry (Generator.choice with p, used by sample_rows with an
+ * explicit distribution, leverage.py:222-230). */
+int ks_sampler_tables(const double* scores, int64_t n, int32_t renormalise, double* probs,
+                      double* cdf, int32_t* flags, void* stream);
+
+/* Inverse-CDF draws: idx[t*stride + off] = clip(upper_bound(cdf, u[t]), 0, n-1) (leverage.py:196-200). */
+int ks_searchsorted_right(const double* cdf, int64_t n, const double* u, int64_t s,
+                          int64_t* idx, int64_t stride, int64_t off, void* stream);
+
+/* Sketch weights (leverage.py:220-231): prob[t] = prod_f probs_f[idx[t, f]];
+ * w[t] = 1 / sqrt(prob[t] * s). */
+int ks_sketch_weights(int32_t nf, const double* const* probs, const int64_t* idx, int64_t s,
+                      double* w, void* stream);
+
+/* sparse_diagonal_from_sketch (kron.py:173-190): flat = ravel(idx) (C order), stable sort,
+ * unique, values = sqrt(w2[first] + pairwise_sum(w2[rest])) in NumPy reduceat order.
+ * sd_idx / sd_val must hold s entries; *nnz (host) is set.  Synchronises the stream. */
+int ks_sketch_diag(int32_t nf, const int64_t* idx, const int64_t* row_shape, const double* w,
+                   int64_t s, int64_t* sd_idx, double* sd_val, int64_t* nnz, void* stream);
+
+/* Gather b_at[t] = b[idx[t]] (solvers.py:451). */
+int ks_gather(const double* b, const int64_t* idx, int64_t n, double* out, void* stream);
+
+/* ---------------------------------------------------------------- sketched operator & solver */
+
+/* Grouped view of a sparse diagonal for the two-group scheme of kron.py:258-354.
+ * The nnz samples are ordered by (left group row, right group row); `seg` (u_left+1) are
+ * CSR offsets of each distinct left row, `lrow[u]` its row in Lmat (u_left x dL, ld ldl),
+ * `rrow[t]` the right-group row of sample t in Rmat (ld ldr), `v[t]` the diagonal value. */
+typedef struct ks_sketch_view {
+  const double* Lmat; int64_t ldl; int32_t dL;
+  const double* Rmat; int64_t ldr; int32_t dR;
+  int64_t u_left; int64_t nnz;
+  const int64_t* seg; const int64_t* lrow; const int64_t* rrow; const double* v;
+} ks_sketch_view;
+
+/* Build the grouped view of a sparse diagonal (sorted unique flat row indices sd_idx with values
+ * sd_val, nnz entries) for the factor split left_pos | right_pos (kron.balanced_partition,
+ * kron.py:117-144).  Outputs (caller-allocated, nnz-sized): seg (nnz+1), lrow, rrow, v, perm
+ * (grouped position -> position in sd_idx).  Lbuf (nnz x dL) must be given iff the left group
+ * is not a single factor (Khatri-Rao rows are materialised, kron.py:193-205), Rbuf (nnz x dR)
+ * iff the right group is not a single factor.  *u_left (host) receives the number of distinct
+ * left rows.  Synchronises the stream. */
+int ks_sketch_group(int32_t nf, const double* const* factors, const int64_t* rows,
+                    const int64_t* cols, int32_t nleft, const int32_t* left_pos, int32_t nright,
+                    const int32_t* right_pos, const int64_t* sd_idx, const double* sd_val,
+                    int64_t nnz, int64_t* seg, int64_t* lrow, int64_t* rrow, double* v,
+                    int64_t* perm, double* Lbuf, double* Rbuf, int64_t* u_left, void* stream);
+
+/* vals[perm[t]] = v[t] * Lrow_t^T X Rrow_t  (sketched_kron_apply, kron.py:258-300), X: dL x dR
+ * in grouped column order.  perm may be NULL (identity). */
+int ks_sketched_apply(const ks_sketch_view* sk, const double* X, const int64_t* perm,
+                      double* vals, void* stream);
+
+/* G(dL x dR) = sum_t bv[perm[t]] v[t] Lrow_t Rrow_t^T (sketched_kron_transpose_apply,
+ * kron.py:312-354). */
+int ks_sketched_transpose_apply(const ks_sketch_view* sk, const double* bv, const int64_t* perm,
+                                double* G, void* stream);
+
+/* Fused Richardson loop of fast_kronecker_regression (solvers.py:201-248 with the operator of
+ * :454-456 and KronPreconditioner.apply of :180-183), all on device:
+ *   step = P (H x - rhs),  H x = sum_t v_t^2 (Lrow_t^T X Rrow_t) Lrow_t Rrow_t^T + lam x,
+ *   P y = (VL kron VR) diag(dinv) (VL kron VR)^T y  (VL dL x dL, VR dR x dR).
+ * x (dL x dR) starts at zero.  hist (max_iters doubles) receives the step norms; *iters and
+ * *hist_len (host) are set.  Returns KS_EDIVERGED on the reference's divergence rule.
+ * Synchronises the stream at the end. */
+int ks_richardson_sketched(const ks_sketch_view* sk, const double* VL, const double* VR,
+                           const double* dinv, const double* rhs, double lam, double damping,
+                           int32_t max_iters, double residual_tol, double* x, double* hist,
+                           int32_t* iters, int32_t* hist_len, void* stream);
+
+/* Preconditioner apply y = (VL kron VR) diag(dinv) (VL kron VR)^T r (solvers.py:180-183). */
+int ks_kron_precond_apply(const double* VL, const double* VR, int32_t dL, int32_t dR,
+                          const double* dinv, const double* r, double* y, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KRONSOLVE_B200_H */

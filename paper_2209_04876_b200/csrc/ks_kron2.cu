@@ -1,0 +1,44 @@
+// Two-factor n^2 passes of the exact solver and of the loss (reference kron.py:66-77 through
+// solvers.py:314 and solvers.py:261).  Generic-GEMM formulation; the TMA/DMMA versions live in
+// ks_kron2_dmma.cu and are selected when the shapes allow.
+#include "ks_common.cuh"
+
+namespace ks {
+int gemm(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
+         int64_t a_rs, int64_t a_cs, int64_t a_bs, const double* B, int64_t b_rs, int64_t b_cs,
+         int64_t b_bs, double beta, double* C, int64_t c_rs, int64_t c_cs, int64_t c_bs,
+         int64_t batch);
+int gemm_tn_tall(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
+                 int64_t a_ks, int64_t a_ms, const double* B, int64_t b_ks, int64_t b_ns,
+                 double* C);
+int gemm_resid_sumsq(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha,
+                     const double* A, int64_t a_rs, int64_t a_cs, const double* B, int64_t b_rs,
+                     int64_t b_cs, const double* C, int64_t c_rs, int64_t c_cs, double* out);
+}
+
+// T = L^T (B R): P = B R (m x q) then T = L^T P.
+extern "C" int ks_kron2_contract(const double* L, const double* B, int64_t ldb, const double* R,
+                                 int64_t m, int64_t k, int32_t p, int32_t q, double* T,
+                                 void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  KS_REQUIRE(p >= 1 && q >= 1 && p <= 128 && q <= 128, KS_ESIZE, "contract widths must be <= 128");
+  ks::Scratch<double> P(m * q, st);
+  KS_REQUIRE(P.p, KS_ECUDA, "scratch allocation failed");
+  int rc = ks::gemm(st, m, q, k, 1.0, B, ldb, 1, 0, R, q, 1, 0, 0.0, P.p, q, 1, 0, 1);
+  if (rc) return rc;
+  return ks::gemm_tn_tall(st, p, q, m, 1.0, L, p, 1, P.p, q, 1, T);
+}
+
+// sum((L X R^T - B)^2): Zt = R X^T (k x p), then the residual GEMM L Zt^T - B.
+extern "C" int ks_kron2_residual_sumsq(const double* L, const double* X, const double* R,
+                                       const double* B, int64_t ldb, int64_t m, int64_t k, int32_t p,
+                                       int32_t q, double* out, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  ks::Scratch<double> Zt(k * p, st);
+  KS_REQUIRE(Zt.p, KS_ECUDA, "scratch allocation failed");
+  // Zt[j, a] = sum_c R[j, c] X[a, c]
+  int rc = ks::gemm(st, k, p, q, 1.0, R, q, 1, 0, X, 1, q, 0, 0.0, Zt.p, p, 1, 0, 1);
+  if (rc) return rc;
+  // E[i, j] = sum_a L[i, a] Zt[j, a] - B[i, j]
+  return ks::gemm_resid_sumsq(st, m, k, p, 1.0, L, p, 1, Zt.p, 1, p, B, ldb, 1, out);
+}

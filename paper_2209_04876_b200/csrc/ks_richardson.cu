@@ -1,0 +1,223 @@
+// Device-resident preconditioned Richardson iteration of fast_kronecker_regression.
+//
+// Reference semantics (solvers.py:201-248): x0 = 0; scale = ||P rhs||; tol = residual_tol *
+// max(scale, tiny); for it < max_iters: step = P(H x - rhs); history.append(||step||);
+// break if ||step|| <= tol; raise if the last 6 norms rise strictly and grow > 10x;
+// x -= damping * step.  H x = (SK)^T S (SK) x + lam x (solvers.py:454-456) with the sketched
+// operator of kron.py:258-354; P = KronPreconditioner.apply (solvers.py:180-183).
+//
+// Every iteration runs on the stream without host round trips; the loop state (status,
+// iteration count, residual history) lives in device memory and is copied back once.
+#include "ks_common.cuh"
+
+#include <cfloat>
+
+namespace ks {
+int sketched_gram_partials(cudaStream_t st, const ks_sketch_view* sk, const double* X,
+                           const double* bv, const int64_t* perm, int mode, double* part,
+                           int64_t* nparts_out);
+int64_t sketched_partials_count(const ks_sketch_view* sk);
+}
+
+namespace {
+
+enum { ST_RUNNING = 0, ST_CONVERGED = 1, ST_DIVERGED = 2 };
+
+struct LoopState {
+  int status;
+  int iters;
+  int hist_len;
+  int pad;
+  double tol;
+};
+
+// R = sum_p part[p] + lam X - rhs
+__global__ void residual_kernel(const double* __restrict__ part, int64_t nparts, int64_t count,
+                                const double* __restrict__ X, double lam,
+                                const double* __restrict__ rhs, double* __restrict__ R,
+                                const LoopState* __restrict__ ls) {
+  if (ls && ls->status != ST_RUNNING) return;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= count) return;
+  double s = 0.0;
+  for (int64_t p = 0; p < nparts; p++) s += part[p * count + e];
+  // (G + lam x) - rhs, in the reference's association
+  R[e] = (s + lam * X[e]) - rhs[e];
+}
+
+// T[r, :] = dinv[r, :] * ((VL^T R)[r, :] VR)     one block per row r
+__global__ void precond_a_kernel(const double* __restrict__ VL, const double* __restrict__ VR, int dL,
+                                 int dR, const double* __restrict__ dinv, const double* __restrict__ R,
+                                 double* __restrict__ T, const LoopState* __restrict__ ls) {
+  if (ls && ls->status != ST_RUNNING) return;
+  __shared__ double t1[128];
+  const int r = blockIdx.x;
+  for (int j = threadIdx.x; j < dR; j += blockDim.x) {
+    double s = 0.0;
+    for (int k = 0; k < dL; k++) s = fma(VL[k * dL + r], R[k * dR + j], s);
+    t1[j] = s;
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < dR; c += blockDim.x) {
+    double s = 0.0;
+    for (int j = 0; j < dR; j++) s = fma(t1[j], VR[j * dR + c], s);
+    T[r * dR + c] = s * dinv[r * dR + c];
+  }
+}
+
+// Y[r, :] = (VL T)[r, :] VR^T; rowsq[r] = ||Y[r, :]||^2       one block per row r
+__global__ void precond_b_kernel(const double* __restrict__ VL, const double* __restrict__ VRt, int dL,
+                                 int dR, const double* __restrict__ T, double* __restrict__ Y,
+                                 double* __restrict__ rowsq, const LoopState* __restrict__ ls) {
+  if (ls && ls->status != ST_RUNNING) return;
+  __shared__ double s1[128];
+  __shared__ double red[32];
+  const int r = blockIdx.x;
+  for (int j = threadIdx.x; j < dR; j += blockDim.x) {
+    double s = 0.0;
+    for (int k = 0; k < dL; k++) s = fma(VL[r * dL + k], T[k * dR + j], s);
+    s1[j] = s;
+  }
+  __syncthreads();
+  double sq = 0.0;
+  for (int c = threadIdx.x; c < dR; c += blockDim.x) {
+    double s = 0.0;
+    for (int j = 0; j < dR; j++) s = fma(s1[j], VRt[j * dR + c], s);
+    Y[r * dR + c] = s;
+    sq = fma(s, s, sq);
+  }
+  sq = block_sum(sq, red);
+  if (threadIdx.x == 0 && rowsq) rowsq[r] = sq;
+}
+
+__global__ void transpose_sq_kernel(const double* __restrict__ a, int d, double* __restrict__ out) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= d * d) return;
+  const int i = e / d, j = e - i * d;
+  out[j * d + i] = a[e];
+}
+
+__global__ void init_state_kernel(LoopState* ls, const double* __restrict__ rowsq, int dL,
+                                  double residual_tol, double* __restrict__ x, int64_t count) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < count) x[e] = 0.0;
+  if (e == 0) {
+    double s = 0.0;
+    for (int r = 0; r < dL; r++) s += rowsq[r];
+    const double scale = sqrt(s);
+    ls->status = ST_RUNNING;
+    ls->iters = 0;
+    ls->hist_len = 0;
+    ls->tol = residual_tol * fmax(scale, DBL_MIN);
+  }
+}
+
+// norm, history, stopping rules, x update (one block)
+__global__ void update_kernel(LoopState* ls, const double* __restrict__ rowsq, int dL, int it,
+                              double* __restrict__ hist, const double* __restrict__ step,
+                              double damping, double* __restrict__ x, int64_t count) {
+  __shared__ int s_go;
+  if (threadIdx.x == 0) {
+    s_go = 0;
+    if (ls->status == ST_RUNNING) {
+      double s = 0.0;
+      for (int r = 0; r < dL; r++) s += rowsq[r];
+      const double nrm = sqrt(s);
+      hist[it] = nrm;
+      ls->hist_len = it + 1;
+      const int h = it + 1;
+      if (nrm <= ls->tol) {
+        ls->status = ST_CONVERGED;
+      } else {
+        bool diverged = false;
+        if (h > 5) {
+          bool inc = true;
+          for (int i = h - 6; i < h - 1; i++) inc &= hist[i + 1] > hist[i];
+          diverged = inc && (hist[h - 1] > 10.0 * hist[h - 6]);
+        }
+        if (diverged) {
+          ls->status = ST_DIVERGED;
+        } else {
+          s_go = 1;
+          ls->iters = it + 1;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (!s_go) return;
+  for (int64_t e = threadIdx.x; e < count; e += blockDim.x) x[e] = __dsub_rn(x[e], __dmul_rn(damping, step[e]));
+}
+
+}  // namespace
+
+namespace ks {
+
+int precond_apply(cudaStream_t st, const double* VL, const double* VR, const double* VRt, int dL,
+                  int dR, const double* dinv, const double* r, double* tmp, double* y,
+                  double* rowsq, const void* ls) {
+  const int thr = dR >= 128 ? 128 : (dR >= 64 ? 64 : 32);
+  precond_a_kernel<<<dL, thr, 0, st>>>(VL, VR, dL, dR, dinv, r, tmp, (const LoopState*)ls);
+  KS_CHECK_LAUNCH();
+  precond_b_kernel<<<dL, thr, 0, st>>>(VL, VRt, dL, dR, tmp, y, rowsq, (const LoopState*)ls);
+  KS_CHECK_LAUNCH();
+  return KS_OK;
+}
+
+}  // namespace ks
+
+extern "C" int ks_kron_precond_apply(const double* VL, const double* VR, int32_t dL, int32_t dR,
+                                     const double* dinv, const double* r, double* y, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  KS_REQUIRE(dL >= 1 && dR >= 1 && dL <= 128 && dR <= 128, KS_ESIZE, "preconditioner dims must be <= 128");
+  ks::Scratch<double> VRt((int64_t)dR * dR, st), tmp((int64_t)dL * dR, st);
+  KS_REQUIRE(VRt.p && tmp.p, KS_ECUDA, "scratch allocation failed");
+  transpose_sq_kernel<<<ceil_div_u((int64_t)dR * dR, 256), 256, 0, st>>>(VR, dR, VRt.p);
+  KS_CHECK_LAUNCH();
+  return ks::precond_apply(st, VL, VR, VRt.p, dL, dR, dinv, r, tmp.p, y, nullptr, nullptr);
+}
+
+extern "C" int ks_richardson_sketched(const ks_sketch_view* sk, const double* VL, const double* VR,
+                                      const double* dinv, const double* rhs, double lam,
+                                      double damping, int32_t max_iters, double residual_tol,
+                                      double* x, double* hist, int32_t* iters, int32_t* hist_len,
+                                      void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const int dL = sk->dL, dR = sk->dR;
+  KS_REQUIRE(dL >= 1 && dR >= 1 && dL <= 128 && dR <= 128, KS_ESIZE, "group widths must be <= 128");
+  const int64_t count = (int64_t)dL * dR;
+  const int64_t np = ks::sketched_partials_count(sk);
+  ks::Scratch<double> part(np * count + 1, st), R(count, st), T(count, st), step(count, st);
+  ks::Scratch<double> rowsq(dL, st), VRt((int64_t)dR * dR, st);
+  ks::Scratch<LoopState> ls(1, st);
+  KS_REQUIRE(part.p && R.p && T.p && step.p && rowsq.p && VRt.p && ls.p, KS_ECUDA,
+             "scratch allocation failed");
+  transpose_sq_kernel<<<ceil_div_u((int64_t)dR * dR, 256), 256, 0, st>>>(VR, dR, VRt.p);
+  KS_CHECK_LAUNCH();
+  // scale = ||P rhs||
+  int rc = ks::precond_apply(st, VL, VR, VRt.p, dL, dR, dinv, rhs, T.p, step.p, rowsq.p, nullptr);
+  if (rc) return rc;
+  init_state_kernel<<<ceil_div_u(count, 256), 256, 0, st>>>(ls.p, rowsq.p, dL, residual_tol, x, count);
+  KS_CHECK_LAUNCH();
+  for (int it = 0; it < max_iters; it++) {
+    int64_t nb = 0;
+    rc = ks::sketched_gram_partials(st, sk, x, nullptr, nullptr, 1, part.p, &nb);
+    if (rc) return rc;
+    residual_kernel<<<ceil_div_u(count, 256), 256, 0, st>>>(part.p, nb, count, x, lam, rhs, R.p, ls.p);
+    KS_CHECK_LAUNCH();
+    rc = ks::precond_apply(st, VL, VR, VRt.p, dL, dR, dinv, R.p, T.p, step.p, rowsq.p, ls.p);
+    if (rc) return rc;
+    update_kernel<<<1, 1024, 0, st>>>(ls.p, rowsq.p, dL, it, hist, step.p, damping, x, count);
+    KS_CHECK_LAUNCH();
+  }
+  LoopState h{};
+  KS_TRY_CUDA(cudaMemcpyAsync(&h, ls.p, sizeof(LoopState), cudaMemcpyDeviceToHost, st));
+  KS_TRY_CUDA(cudaStreamSynchronize(st));
+  *iters = h.iters;
+  *hist_len = h.hist_len;
+  if (h.status == ST_DIVERGED) {
+    ks::set_error("Richardson iteration diverged");
+    return KS_EDIVERGED;
+  }
+  return KS_OK;
+}

@@ -1,0 +1,448 @@
+// Row-sketch plumbing and the sketched Kronecker operator.
+//   sparse_diagonal_from_sketch (kron.py:173-190)
+//   two-group view of the sketched rows (kron.py:117-144, :225-255, :303-309)
+//   sketched_kron_apply / sketched_kron_transpose_apply (kron.py:258-354)
+// The reference recomputes np.unique/argsort on every apply; here the grouping is built once
+// per sketch and every apply is a gathered-row contraction over the distinct left-group rows.
+#include "ks_common.cuh"
+#include "ks_pairwise.cuh"
+
+#include <vector>
+
+namespace ks {
+int radix_sort_pairs(cudaStream_t st, uint64_t* keys, int64_t* vals, int64_t n, int bits);
+int scan_exclusive_i32(cudaStream_t st, const int32_t* in, int64_t n, int64_t* out);
+}
+
+namespace {
+
+struct Shape8 {
+  int64_t v[8];
+};
+
+__global__ void ravel_kernel(const int64_t* __restrict__ idx, int nf, Shape8 rs, int64_t s,
+                             uint64_t* __restrict__ keys, int64_t* __restrict__ vals) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= s) return;
+  int64_t f = 0;
+  for (int k = 0; k < nf; k++) f = f * rs.v[k] + idx[t * nf + k];
+  keys[t] = (uint64_t)f;
+  vals[t] = t;
+}
+
+__global__ void head_flags_kernel(const uint64_t* __restrict__ keys, int64_t n, int32_t* __restrict__ head) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  head[i] = (i == 0 || keys[i] != keys[i - 1]) ? 1 : 0;
+}
+
+// One thread per segment start: value = sqrt(w2[first] + pairwise(w2[rest])) -- np.add.reduceat
+// copies the first element and reduces the remainder with the pairwise inner loop.
+__global__ void seg_sqrt_sum_kernel(const uint64_t* __restrict__ keys, const int64_t* __restrict__ perm,
+                                    const int32_t* __restrict__ head, const int64_t* __restrict__ segid,
+                                    int64_t n, const double* __restrict__ w,
+                                    int64_t* __restrict__ sd_idx, double* __restrict__ sd_val) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n || !head[i]) return;
+  int64_t e = i + 1;
+  while (e < n && !head[e]) e++;
+  const double w0 = w[perm[i]];
+  double acc = __dmul_rn(w0, w0);
+  if (e - i > 1) {
+    auto get = [&](int64_t j) {
+      const double x = w[perm[j]];
+      return __dmul_rn(x, x);
+    };
+    acc = acc + pw_sum_seq(get, i + 1, e - i - 1);
+  }
+  const int64_t g = segid[i];
+  sd_idx[g] = (int64_t)keys[i];
+  sd_val[g] = __dsqrt_rn(acc);
+}
+
+__global__ void nnz_kernel(const int32_t* __restrict__ head, const int64_t* __restrict__ segid, int64_t n,
+                           int64_t* __restrict__ out) {
+  out[0] = segid[n - 1] + head[n - 1];
+}
+
+// ---- grouping of the sketched rows into (left group, right group) --------------------------
+
+struct GroupSpec {
+  int nf;
+  int64_t rows[8];
+  int nl, nr;
+  int lpos[8], rpos[8];
+};
+
+__device__ __forceinline__ void unravel(int64_t flat, const GroupSpec& g, int64_t* multi) {
+  for (int k = g.nf - 1; k >= 0; k--) {
+    multi[k] = flat % g.rows[k];
+    flat /= g.rows[k];
+  }
+}
+
+// key = left_key * right_rows + right_key, val = sample position in the sparse diagonal
+__global__ void group_keys_kernel(const int64_t* __restrict__ sd_idx, int64_t nnz, GroupSpec g,
+                                  int64_t right_rows, uint64_t* __restrict__ keys,
+                                  int64_t* __restrict__ vals) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nnz) return;
+  int64_t m[8];
+  unravel(sd_idx[t], g, m);
+  int64_t lk = 0, rk = 0;
+  for (int k = 0; k < g.nl; k++) lk = lk * g.rows[g.lpos[k]] + m[g.lpos[k]];
+  for (int k = 0; k < g.nr; k++) rk = rk * g.rows[g.rpos[k]] + m[g.rpos[k]];
+  keys[t] = (uint64_t)(lk * right_rows + rk);
+  vals[t] = t;
+}
+
+__global__ void left_head_kernel(const uint64_t* __restrict__ keys, int64_t n, int64_t right_rows,
+                                 int32_t* __restrict__ head) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  head[i] = (i == 0 || keys[i] / right_rows != keys[i - 1] / right_rows) ? 1 : 0;
+}
+
+struct FacPtrs {
+  const double* f[8];
+  int64_t cols[8];
+};
+
+// Column c of the Khatri-Rao row of a factor group (kron.py:193-205: first factor slowest,
+// product accumulated left to right starting from 1.0).
+__device__ double kr_entry(const FacPtrs& F, const int64_t* m, const int* pos, int np, int c) {
+  int64_t digit[8];
+  int64_t rem = c;
+  for (int k = np - 1; k >= 0; k--) {
+    const int64_t cols = F.cols[pos[k]];
+    digit[k] = rem % cols;
+    rem /= cols;
+  }
+  double prod = 1.0;
+  for (int k = 0; k < np; k++) {
+    const int f = pos[k];
+    prod = __dmul_rn(prod, F.f[f][m[f] * F.cols[f] + digit[k]]);
+  }
+  return prod;
+}
+
+// Per grouped sample t: v[t], perm[t], rrow[t] (row in Rmat), and for each left segment start
+// the segment offset and left row; materialises Khatri-Rao rows of multi-factor groups.
+__global__ void group_fill_kernel(const uint64_t* __restrict__ keys, const int64_t* __restrict__ pos,
+                                  const int32_t* __restrict__ head, const int64_t* __restrict__ segid,
+                                  int64_t nnz, int64_t right_rows, GroupSpec g, FacPtrs F,
+                                  const int64_t* __restrict__ sd_idx, const double* __restrict__ sd_val,
+                                  int64_t* __restrict__ seg, int64_t* __restrict__ lrow,
+                                  int64_t* __restrict__ rrow, double* __restrict__ v,
+                                  int64_t* __restrict__ perm, double* __restrict__ Lbuf, int dL,
+                                  double* __restrict__ Rbuf, int dR) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nnz) return;
+  const int64_t p = pos[t];
+  perm[t] = p;
+  v[t] = sd_val[p];
+  int64_t m[8];
+  unravel(sd_idx[p], g, m);
+  const uint64_t key = keys[t];
+  const int64_t rk = (int64_t)(key % (uint64_t)right_rows);
+  if (Rbuf) {
+    // Khatri-Rao row of the right group, natural (row-major) column order of the group
+    rrow[t] = t;
+    for (int c = 0; c < dR; c++) Rbuf[t * dR + c] = kr_entry(F, m, g.rpos, g.nr, c);
+  } else {
+    rrow[t] = (g.nr == 1) ? m[g.rpos[0]] : rk;
+  }
+  if (head[t]) {
+    const int64_t u = segid[t];
+    seg[u] = t;
+    if (Lbuf) {
+      lrow[u] = u;
+      for (int c = 0; c < dL; c++) Lbuf[u * dL + c] = kr_entry(F, m, g.lpos, g.nl, c);
+    } else {
+      lrow[u] = m[g.lpos[0]];
+    }
+  }
+  if (t == nnz - 1) seg[segid[t] + head[t]] = nnz;
+}
+
+// ---- applies --------------------------------------------------------------------------------
+// One warp per distinct left row u: y = X^T L_u (dR), then over the segment's samples.
+constexpr int AP_WARPS = 8;
+constexpr int MAXD = 128;
+
+__global__ void __launch_bounds__(AP_WARPS * 32) forward_kernel(ks_sketch_view sk, const double* __restrict__ X,
+                                                               const int64_t* __restrict__ perm,
+                                                               double* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t u = (int64_t)blockIdx.x * AP_WARPS + (threadIdx.x >> 5);
+  if (u >= sk.u_left) return;
+  const int dL = sk.dL, dR = sk.dR;
+  const double* L = sk.Lmat + sk.lrow[u] * sk.ldl;
+  double y[MAXD / 32];
+#pragma unroll
+  for (int j = 0; j < MAXD / 32; j++) y[j] = 0.0;
+  for (int i = 0; i < dL; i++) {
+    const double li = L[i];
+#pragma unroll
+    for (int j = 0; j < MAXD / 32; j++) {
+      const int k = lane + 32 * j;
+      if (k < dR) y[j] = fma(li, X[(int64_t)i * dR + k], y[j]);
+    }
+  }
+  for (int64_t t = sk.seg[u]; t < sk.seg[u + 1]; t++) {
+    const double* R = sk.Rmat + sk.rrow[t] * sk.ldr;
+    double d = 0.0;
+#pragma unroll
+    for (int j = 0; j < MAXD / 32; j++) {
+      const int k = lane + 32 * j;
+      if (k < dR) d = fma(y[j], R[k], d);
+    }
+    d = warp_sum(d);
+    if (lane == 0) out[perm ? perm[t] : t] = sk.v[t] * d;
+  }
+}
+
+// MODE 0: s_t = v_t * bv[perm[t]]  (transpose apply)
+// MODE 1: s_t = v_t * (v_t * L_u^T X R_t)  (fused normal operator)
+// Each block handles AP_WARPS*CHW distinct left rows; block partial G_b = L_chunk^T Z_chunk.
+constexpr int CHW = 4;  // left rows per warp per block
+template <int MODE>
+__global__ void __launch_bounds__(AP_WARPS * 32) gram_apply_kernel(ks_sketch_view sk, const double* __restrict__ X,
+                                                                  const double* __restrict__ bv,
+                                                                  const int64_t* __restrict__ perm,
+                                                                  double* __restrict__ part) {
+  extern __shared__ double sm[];
+  const int dL = sk.dL, dR = sk.dR;
+  const int CH = AP_WARPS * CHW;
+  double* Ls = sm;                       // CH x dL
+  double* Zs = sm + (size_t)CH * dL;     // CH x dR
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int64_t u0 = (int64_t)blockIdx.x * CH;
+  for (int e = tid; e < CH * dL; e += blockDim.x) {
+    const int c = e / dL, i = e - c * dL;
+    const int64_t u = u0 + c;
+    Ls[e] = (u < sk.u_left) ? sk.Lmat[sk.lrow[u] * sk.ldl + i] : 0.0;
+  }
+  __syncthreads();
+  for (int cc = 0; cc < CHW; cc++) {
+    const int c = w * CHW + cc;
+    const int64_t u = u0 + c;
+    double z[MAXD / 32];
+#pragma unroll
+    for (int j = 0; j < MAXD / 32; j++) z[j] = 0.0;
+    if (u < sk.u_left) {
+      double y[MAXD / 32];
+      if (MODE == 1) {
+#pragma unroll
+        for (int j = 0; j < MAXD / 32; j++) y[j] = 0.0;
+        const double* L = Ls + (size_t)c * dL;
+        for (int i = 0; i < dL; i++) {
+          const double li = L[i];
+#pragma unroll
+          for (int j = 0; j < MAXD / 32; j++) {
+            const int k = lane + 32 * j;
+            if (k < dR) y[j] = fma(li, X[(int64_t)i * dR + k], y[j]);
+          }
+        }
+      }
+      for (int64_t t = sk.seg[u]; t < sk.seg[u + 1]; t++) {
+        const double* R = sk.Rmat + sk.rrow[t] * sk.ldr;
+        double r[MAXD / 32];
+#pragma unroll
+        for (int j = 0; j < MAXD / 32; j++) {
+          const int k = lane + 32 * j;
+          r[j] = (k < dR) ? R[k] : 0.0;
+        }
+        const double vt = sk.v[t];
+        double s;
+        if (MODE == 1) {
+          double d = 0.0;
+#pragma unroll
+          for (int j = 0; j < MAXD / 32; j++) d = fma(y[j], r[j], d);
+          d = warp_sum(d);
+          s = vt * (vt * d);
+        } else {
+          s = vt * bv[perm ? perm[t] : t];
+        }
+#pragma unroll
+        for (int j = 0; j < MAXD / 32; j++) z[j] = fma(s, r[j], z[j]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < MAXD / 32; j++) {
+      const int k = lane + 32 * j;
+      if (k < dR) Zs[(size_t)c * dR + k] = z[j];
+    }
+  }
+  __syncthreads();
+  // G_b[i][k] = sum_c Ls[c][i] Zs[c][k]
+  double* G = part + (int64_t)blockIdx.x * dL * dR;
+  for (int e = tid; e < dL * dR; e += blockDim.x) {
+    const int i = e / dR, k = e - i * dR;
+    double g = 0.0;
+    for (int c = 0; c < CH; c++) g = fma(Ls[c * dL + i], Zs[c * dR + k], g);
+    G[e] = g;
+  }
+}
+
+__global__ void reduce_cols_kernel(const double* __restrict__ part, int64_t nparts, int64_t count,
+                                   double* __restrict__ out) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= count) return;
+  double s = 0.0;
+  for (int64_t p = 0; p < nparts; p++) s += part[p * count + e];
+  out[e] = s;
+}
+
+}  // namespace
+
+namespace ks {
+
+int sketched_gram_partials(cudaStream_t st, const ks_sketch_view* sk, const double* X,
+                           const double* bv, const int64_t* perm, int mode, double* part,
+                           int64_t* nparts_out) {
+  const int CH = AP_WARPS * CHW;
+  const int64_t nb = (sk->u_left + CH - 1) / CH;
+  *nparts_out = nb;
+  if (nb == 0) return KS_OK;
+  const size_t smem = sizeof(double) * (size_t)CH * (sk->dL + sk->dR);
+  if (mode == 1) {
+    KS_TRY_CUDA(cudaFuncSetAttribute(gram_apply_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    gram_apply_kernel<1><<<(unsigned)nb, AP_WARPS * 32, smem, st>>>(*sk, X, bv, perm, part);
+  } else {
+    KS_TRY_CUDA(cudaFuncSetAttribute(gram_apply_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    gram_apply_kernel<0><<<(unsigned)nb, AP_WARPS * 32, smem, st>>>(*sk, X, bv, perm, part);
+  }
+  KS_CHECK_LAUNCH();
+  return KS_OK;
+}
+
+int64_t sketched_partials_count(const ks_sketch_view* sk) {
+  const int CH = AP_WARPS * CHW;
+  return (sk->u_left + CH - 1) / CH;
+}
+
+int reduce_partials(cudaStream_t st, const double* part, int64_t nparts, int64_t count, double* out) {
+  if (nparts == 0) {
+    KS_TRY_CUDA(cudaMemsetAsync(out, 0, count * sizeof(double), st));
+    return KS_OK;
+  }
+  reduce_cols_kernel<<<ceil_div_u(count, 256), 256, 0, st>>>(part, nparts, count, out);
+  KS_CHECK_LAUNCH();
+  return KS_OK;
+}
+
+}  // namespace ks
+
+// ------------------------------------------------------------------------------------ C-ABI
+
+extern "C" int ks_sketch_diag(int32_t nf, const int64_t* idx, const int64_t* row_shape,
+                              const double* w, int64_t s, int64_t* sd_idx, double* sd_val,
+                              int64_t* nnz, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  KS_REQUIRE(nf >= 1 && nf <= 8, KS_EINVAL, "1..8 factors supported");
+  if (s <= 0) { *nnz = 0; return KS_OK; }
+  Shape8 rs{};
+  uint64_t rows = 1;
+  for (int k = 0; k < nf; k++) { rs.v[k] = row_shape[k]; rows *= (uint64_t)row_shape[k]; }
+  int bits = 0;
+  while (bits < 64 && ((rows - 1) >> bits) != 0) bits++;
+  ks::Scratch<uint64_t> keys(s, st);
+  ks::Scratch<int64_t> perm(s, st);
+  ks::Scratch<int32_t> head(s, st);
+  ks::Scratch<int64_t> segid(s + 1, st);
+  KS_REQUIRE(keys.p && perm.p && head.p && segid.p, KS_ECUDA, "scratch allocation failed");
+  ravel_kernel<<<ceil_div_u(s, 256), 256, 0, st>>>(idx, nf, rs, s, keys.p, perm.p);
+  KS_CHECK_LAUNCH();
+  int rc = ks::radix_sort_pairs(st, keys.p, perm.p, s, bits);
+  if (rc) return rc;
+  head_flags_kernel<<<ceil_div_u(s, 256), 256, 0, st>>>(keys.p, s, head.p);
+  KS_CHECK_LAUNCH();
+  rc = ks::scan_exclusive_i32(st, head.p, s, segid.p);
+  if (rc) return rc;
+  seg_sqrt_sum_kernel<<<ceil_div_u(s, 128), 128, 0, st>>>(keys.p, perm.p, head.p, segid.p, s, w,
+                                                          sd_idx, sd_val);
+  KS_CHECK_LAUNCH();
+  nnz_kernel<<<1, 1, 0, st>>>(head.p, segid.p, s, segid.p + s);
+  KS_CHECK_LAUNCH();
+  KS_TRY_CUDA(cudaMemcpyAsync(nnz, segid.p + s, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  KS_TRY_CUDA(cudaStreamSynchronize(st));
+  return KS_OK;
+}
+
+extern "C" int ks_sketch_group(int32_t nf, const double* const* factors, const int64_t* rows,
+                               const int64_t* cols, int32_t nleft, const int32_t* left_pos,
+                               int32_t nright, const int32_t* right_pos, const int64_t* sd_idx,
+                               const double* sd_val, int64_t nnz, int64_t* seg, int64_t* lrow,
+                               int64_t* rrow, double* v, int64_t* perm, double* Lbuf,
+                               double* Rbuf, int64_t* u_left, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  KS_REQUIRE(nf >= 1 && nf <= 8 && nleft + nright == nf, KS_EINVAL, "bad group specification");
+  if (nnz <= 0) { *u_left = 0; return KS_OK; }
+  GroupSpec g{};
+  g.nf = nf;
+  g.nl = nleft;
+  g.nr = nright;
+  FacPtrs F{};
+  for (int k = 0; k < nf; k++) { g.rows[k] = rows[k]; F.f[k] = factors[k]; F.cols[k] = cols[k]; }
+  int64_t right_rows = 1, left_rows = 1, dL = 1, dR = 1;
+  for (int k = 0; k < nleft; k++) { g.lpos[k] = left_pos[k]; left_rows *= rows[left_pos[k]]; dL *= cols[left_pos[k]]; }
+  for (int k = 0; k < nright; k++) { g.rpos[k] = right_pos[k]; right_rows *= rows[right_pos[k]]; dR *= cols[right_pos[k]]; }
+  KS_REQUIRE(dL <= MAXD && dR <= MAXD, KS_ESIZE, "group column products must be <= %d (got %lld, %lld)", MAXD,
+             (long long)dL, (long long)dR);
+  KS_REQUIRE((Lbuf != nullptr) == (nleft != 1), KS_EINVAL, "Lbuf required iff the left group is not a single factor");
+  KS_REQUIRE((Rbuf != nullptr) == (nright != 1), KS_EINVAL, "Rbuf required iff the right group is not a single factor");
+  ks::Scratch<uint64_t> keys(nnz, st);
+  ks::Scratch<int64_t> pos(nnz, st);
+  ks::Scratch<int32_t> head(nnz, st);
+  ks::Scratch<int64_t> segid(nnz + 1, st);
+  KS_REQUIRE(keys.p && pos.p && head.p && segid.p, KS_ECUDA, "scratch allocation failed");
+  group_keys_kernel<<<ceil_div_u(nnz, 256), 256, 0, st>>>(sd_idx, nnz, g, right_rows, keys.p, pos.p);
+  KS_CHECK_LAUNCH();
+  // left group a prefix of the factor order => sorted flat order is already grouped
+  bool prefix = true;
+  for (int k = 0; k < nleft; k++) prefix &= (left_pos[k] == k);
+  if (!prefix) {
+    uint64_t total = (uint64_t)left_rows * (uint64_t)right_rows;
+    int bits = 0;
+    while (bits < 64 && ((total - 1) >> bits) != 0) bits++;
+    int rc = ks::radix_sort_pairs(st, keys.p, pos.p, nnz, bits);
+    if (rc) return rc;
+  }
+  left_head_kernel<<<ceil_div_u(nnz, 256), 256, 0, st>>>(keys.p, nnz, right_rows, head.p);
+  KS_CHECK_LAUNCH();
+  int rc = ks::scan_exclusive_i32(st, head.p, nnz, segid.p);
+  if (rc) return rc;
+  group_fill_kernel<<<ceil_div_u(nnz, 128), 128, 0, st>>>(keys.p, pos.p, head.p, segid.p, nnz, right_rows, g, F,
+                                                          sd_idx, sd_val, seg, lrow, rrow, v, perm, Lbuf,
+                                                          (int)dL, Rbuf, (int)dR);
+  KS_CHECK_LAUNCH();
+  nnz_kernel<<<1, 1, 0, st>>>(head.p, segid.p, nnz, segid.p + nnz);
+  KS_CHECK_LAUNCH();
+  KS_TRY_CUDA(cudaMemcpyAsync(u_left, segid.p + nnz, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  KS_TRY_CUDA(cudaStreamSynchronize(st));
+  return KS_OK;
+}
+
+extern "C" int ks_sketched_apply(const ks_sketch_view* sk, const double* X, const int64_t* perm,
+                                 double* vals, void* stream) {
+  KS_REQUIRE(sk->dR <= MAXD, KS_ESIZE, "right group width must be <= %d", MAXD);
+  if (sk->u_left <= 0) return KS_OK;
+  forward_kernel<<<ceil_div_u(sk->u_left, AP_WARPS), AP_WARPS * 32, 0, (cudaStream_t)stream>>>(*sk, X, perm, vals);
+  KS_CHECK_LAUNCH();
+  return KS_OK;
+}
+
+extern "C" int ks_sketched_transpose_apply(const ks_sketch_view* sk, const double* bv,
+                                           const int64_t* perm, double* G, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  KS_REQUIRE(sk->dR <= MAXD && sk->dL <= MAXD, KS_ESIZE, "group widths must be <= %d", MAXD);
+  const int64_t count = (int64_t)sk->dL * sk->dR;
+  const int64_t np = ks::sketched_partials_count(sk);
+  ks::Scratch<double> part(np * count + 1, st);
+  KS_REQUIRE(part.p, KS_ECUDA, "scratch allocation failed");
+  int64_t nb = 0;
+  int rc = ks::sketched_gram_partials(st, sk, nullptr, bv, perm, 0, part.p, &nb);
+  if (rc) return rc;
+  return ks::reduce_partials(st, part.p, nb, count, G);
+}

@@ -1,0 +1,427 @@
+// Small dense linear algebra on device (d <= 128): Householder TSQR (R only), one-sided
+// Jacobi SVD, thin SVD driver.  Replaces the LAPACK calls of the reference hot path:
+// np.linalg.svd in tensor.compact_svd (tensor.py:76-107) and np.linalg.eigh in
+// solvers.factor_gram (solvers.py:143-150).  No host LAPACK is used.
+#include "ks_common.cuh"
+
+#include <vector>
+#include <algorithm>
+
+namespace ks {
+int gemm(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
+         int64_t a_rs, int64_t a_cs, int64_t a_bs, const double* B, int64_t b_rs, int64_t b_cs,
+         int64_t b_bs, double beta, double* C, int64_t c_rs, int64_t c_cs, int64_t c_bs,
+         int64_t batch);
+}
+
+namespace {
+
+constexpr int QR_THREADS = 256;
+constexpr size_t QR_SMEM_CAP = 200 * 1024;
+
+// Householder QR of one panel of `rows` x d (rows <= prows) taken from src rows
+// [blockIdx.x*prows, ...).  Writes the d x d upper-triangular R of the panel to
+// dst + blockIdx.x*d*d (row-major, zero below the diagonal).  Panel storage is column-major
+// (column j contiguous) either in shared memory or in a per-block global workspace.
+template <bool SMEM>
+__global__ void __launch_bounds__(QR_THREADS) qr_panel_kernel(const double* __restrict__ src,
+                                                             int64_t n, int d, int prows,
+                                                             double* __restrict__ dst,
+                                                             double* __restrict__ gwork) {
+  extern __shared__ double dyn[];
+  __shared__ double red[32];
+  __shared__ double s_tau, s_beta;
+  const int64_t r0 = (int64_t)blockIdx.x * prows;
+  const int rows = (int)ks_min64(prows, n - r0);
+  double* P = SMEM ? dyn : gwork + (int64_t)blockIdx.x * prows * d;
+  const int tid = threadIdx.x;
+  for (int e = tid; e < rows * d; e += QR_THREADS) {
+    const int i = e / d, j = e - i * d;
+    P[(int64_t)j * rows + i] = src[(r0 + i) * d + j];
+  }
+  __syncthreads();
+  const int steps = min(rows, d);
+  // threads per column group for the trailing update
+  for (int j = 0; j < steps; j++) {
+    double* x = P + (int64_t)j * rows;
+    double part = 0.0;
+    for (int i = j + 1 + tid; i < rows; i += QR_THREADS) part = fma(x[i], x[i], part);
+    const double tail2 = block_sum(part, red);
+    if (tid == 0) {
+      const double alpha = x[j];
+      if (tail2 == 0.0) {
+        s_tau = 0.0;
+        s_beta = alpha;
+      } else {
+        const double nrm = sqrt(fma(alpha, alpha, tail2));
+        const double beta = alpha >= 0.0 ? -nrm : nrm;
+        s_tau = (beta - alpha) / beta;
+        s_beta = beta;
+        x[j] = alpha - beta;  // v0 (unnormalised); scaled below
+      }
+    }
+    __syncthreads();
+    const double tau = s_tau;
+    if (tau != 0.0) {
+      const double inv_v0 = 1.0 / x[j];
+      for (int i = j + 1 + tid; i < rows; i += QR_THREADS) x[i] *= inv_v0;
+      __syncthreads();
+      // trailing columns: w_k = v^T P[:,k]; P[:,k] -= tau w_k v  (v_j = 1)
+      const int ncols = d - j - 1;
+      if (ncols > 0) {
+        const int gsz = max(1, min(32, QR_THREADS / ncols));  // power of two not required
+        int g = 1;
+        while (g * 2 <= gsz) g *= 2;
+        const int ngroups = QR_THREADS / g;
+        const int lane_g = tid % g;
+        for (int c0 = tid / g; c0 < ncols; c0 += ngroups) {
+          double* col = P + (int64_t)(j + 1 + c0) * rows;
+          double w = 0.0;
+          for (int i = j + 1 + lane_g; i < rows; i += g) w = fma(x[i], col[i], w);
+          const unsigned gm = (g == 32) ? 0xffffffffu : (((1u << g) - 1u) << ((tid & 31) & ~(g - 1)));
+          for (int o = g >> 1; o > 0; o >>= 1) w += __shfl_xor_sync(gm, w, o, g);
+          w += col[j];
+          const double tw = tau * w;
+          if (lane_g == 0) col[j] -= tw;
+          for (int i = j + 1 + lane_g; i < rows; i += g) col[i] = fma(-tw, x[i], col[i]);
+        }
+      }
+    }
+    __syncthreads();
+    if (tid == 0) x[j] = s_beta;  // R diagonal
+    __syncthreads();
+  }
+  double* R = dst + (int64_t)blockIdx.x * d * d;
+  for (int e = tid; e < d * d; e += QR_THREADS) {
+    const int i = e / d, j = e - i * d;
+    R[e] = (i <= j && i < rows) ? P[(int64_t)j * rows + i] : 0.0;
+  }
+}
+
+// One-sided (Hestenes) Jacobi SVD of a d x d matrix in one CTA.  W = M (column-major in
+// smem), V = I; round-robin parallel ordering, one thread group per column pair.
+// Output sigma descending, V row-major (column j = right singular vector j).
+template <bool VSMEM>
+__global__ void jacobi_svd_kernel(const double* __restrict__ M, int d, double* __restrict__ sigma,
+                                  double* __restrict__ Vout, double* __restrict__ vwork) {
+  extern __shared__ double dyn[];
+  __shared__ int s_rot;
+  __shared__ int s_order[130];
+  __shared__ double s_norm[130];
+  const int dp = d + (d & 1);
+  double* W = dyn;                                      // dp columns x d rows
+  double* V = VSMEM ? dyn + (size_t)dp * d : vwork;     // dp columns x dp rows
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int e = tid; e < dp * d; e += nt) {
+    const int j = e / d, i = e - j * d;
+    W[e] = (j < d) ? M[(int64_t)i * d + j] : 0.0;
+  }
+  for (int e = tid; e < dp * dp; e += nt) {
+    const int j = e / dp, i = e - j * dp;
+    V[e] = (i == j) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  const int npairs = dp / 2;
+  int g = 1;
+  while (g * 2 * npairs <= nt && g < 32) g *= 2;
+  const int group = tid / g, lg = tid % g;
+  const bool active = group < npairs;
+  const unsigned gmask = (g == 32) ? 0xffffffffu : (((1u << g) - 1u) << ((tid & 31) & ~(g - 1)));
+  for (int sweep = 0; sweep < 60; sweep++) {
+    if (tid == 0) s_rot = 0;
+    __syncthreads();
+    for (int r = 0; r < dp - 1; r++) {
+      if (active) {
+        // circle method: position 0 fixed, others rotate
+        auto player = [&](int pos) { return pos == 0 ? 0 : 1 + (pos - 1 + r) % (dp - 1); };
+        const int p = player(group), q = player(dp - 1 - group);
+        double* wp = W + (size_t)p * d;
+        double* wq = W + (size_t)q * d;
+        double a = 0.0, b = 0.0, c = 0.0;
+        for (int i = lg; i < d; i += g) {
+          const double x = wp[i], y = wq[i];
+          a = fma(x, x, a);
+          b = fma(y, y, b);
+          c = fma(x, y, c);
+        }
+        for (int o = g >> 1; o > 0; o >>= 1) {
+          a += __shfl_xor_sync(gmask, a, o, g);
+          b += __shfl_xor_sync(gmask, b, o, g);
+          c += __shfl_xor_sync(gmask, c, o, g);
+        }
+        if (c != 0.0 && a != 0.0 && b != 0.0 && fabs(c) > 1e-15 * sqrt(a) * sqrt(b)) {
+          const double zeta = (b - a) / (2.0 * c);
+          const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+          const double cs = 1.0 / sqrt(1.0 + t * t);
+          const double sn = cs * t;
+          for (int i = lg; i < d; i += g) {
+            const double x = wp[i], y = wq[i];
+            wp[i] = cs * x - sn * y;
+            wq[i] = sn * x + cs * y;
+          }
+          double* vp = V + (size_t)p * dp;
+          double* vq = V + (size_t)q * dp;
+          for (int i = lg; i < dp; i += g) {
+            const double x = vp[i], y = vq[i];
+            vp[i] = cs * x - sn * y;
+            vq[i] = sn * x + cs * y;
+          }
+          if (lg == 0) s_rot = 1;
+        }
+      }
+      __syncthreads();
+    }
+    if (s_rot == 0) break;
+    __syncthreads();
+  }
+  // singular values and descending order (ties broken by index -> deterministic)
+  for (int j = tid; j < dp; j += nt) {
+    double s = 0.0;
+    if (j < d)
+      for (int i = 0; i < d; i++) s = fma(W[(size_t)j * d + i], W[(size_t)j * d + i], s);
+    s_norm[j] = sqrt(s);
+  }
+  __syncthreads();
+  for (int j = tid; j < d; j += nt) {
+    int rank = 0;
+    const double sj = s_norm[j];
+    for (int k = 0; k < d; k++) {
+      const double sk = s_norm[k];
+      rank += (sk > sj) || (sk == sj && k < j);
+    }
+    s_order[rank] = j;
+  }
+  __syncthreads();
+  for (int k = tid; k < d; k += nt) sigma[k] = s_norm[s_order[k]];
+  for (int e = tid; e < d * d; e += nt) {
+    const int i = e / d, k = e - i * d;
+    Vout[e] = V[(size_t)s_order[k] * dp + i];
+  }
+}
+
+// U[:, j] *= 1/sigma[j] for j < rank, zero otherwise (U = A V Sigma^-1, tensor.py:102-107)
+__global__ void scale_cols_kernel(double* U, int64_t n, int d, const double* __restrict__ sigma,
+                                  double rank_tol) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n * d) return;
+  const int j = (int)(e % d);
+  const double s0 = sigma[0];
+  const double sj = sigma[j];
+  const bool keep = s0 > 0.0 && sj > rank_tol * s0;
+  U[e] = keep ? U[e] / sj : 0.0;
+}
+
+__global__ void transpose_kernel(const double* __restrict__ a, int64_t rows, int64_t cols,
+                                 double* __restrict__ out) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= rows * cols) return;
+  const int64_t i = e / cols, j = e - i * cols;
+  out[j * rows + i] = a[e];
+}
+
+
+// LU with partial pivoting (LAPACK dgetrf pivot rule: first max |a|) in shared memory, then
+// X = A^-1 by forward/back substitution, one thread per column of the identity.
+// info[0] = k+1 if U(k,k) is exactly zero (np.linalg.solve raises LinAlgError), else 0;
+// info[1] = 1 if the inverse has a non-finite entry.
+__global__ void inverse_small_kernel(const double* __restrict__ M, int d, double* __restrict__ X,
+                                     int32_t* __restrict__ info) {
+  extern __shared__ double LU[];
+  __shared__ int piv[128];
+  __shared__ int s_p;
+  __shared__ int s_info;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int e = tid; e < d * d; e += nt) LU[e] = M[e];
+  if (tid == 0) s_info = 0;
+  __syncthreads();
+  for (int k = 0; k < d; k++) {
+    if (tid == 0) {
+      int p = k;
+      double best = fabs(LU[k * d + k]);
+      for (int i = k + 1; i < d; i++) {
+        const double v = fabs(LU[i * d + k]);
+        if (v > best) { best = v; p = i; }
+      }
+      s_p = p;
+      piv[k] = p;
+      if (LU[p * d + k] == 0.0 && s_info == 0) s_info = k + 1;
+    }
+    __syncthreads();
+    const int p = s_p;
+    if (p != k)
+      for (int j = tid; j < d; j += nt) {
+        const double t = LU[k * d + j];
+        LU[k * d + j] = LU[p * d + j];
+        LU[p * d + j] = t;
+      }
+    __syncthreads();
+    const double pivv = LU[k * d + k];
+    if (pivv != 0.0)
+      for (int i = k + 1 + tid; i < d; i += nt) LU[i * d + k] /= pivv;
+    __syncthreads();
+    for (int e = tid; e < (d - k - 1) * (d - k - 1); e += nt) {
+      const int i = k + 1 + e / (d - k - 1), j = k + 1 + e % (d - k - 1);
+      LU[i * d + j] = fma(-LU[i * d + k], LU[k * d + j], LU[i * d + j]);
+    }
+    __syncthreads();
+  }
+  bool bad = false;
+  for (int j = tid; j < d; j += nt) {
+    // column j of P*I: apply the row interchanges to e_j
+    int src = j;
+    // position of e_j after the swaps: track where row j ends up
+    for (int k = 0; k < d; k++) {
+      if (piv[k] == src) src = k; else if (k == src) src = piv[k];
+    }
+    for (int i = 0; i < d; i++) X[i * d + j] = (i == src) ? 1.0 : 0.0;
+    for (int i = 0; i < d; i++) {
+      double s = X[i * d + j];
+      for (int k = 0; k < i; k++) s = fma(-LU[i * d + k], X[k * d + j], s);
+      X[i * d + j] = s;
+    }
+    for (int i = d - 1; i >= 0; i--) {
+      double s = X[i * d + j];
+      for (int k = i + 1; k < d; k++) s = fma(-LU[i * d + k], X[k * d + j], s);
+      const double v = s / LU[i * d + i];
+      X[i * d + j] = v;
+      bad |= !isfinite(v);
+    }
+  }
+  bad = __syncthreads_or(bad);
+  if (tid == 0) {
+    info[0] = s_info;
+    info[1] = bad ? 1 : 0;
+  }
+}
+
+}  // namespace
+
+namespace ks {
+
+int qr_r(cudaStream_t st, const double* A, int64_t n, int d, double* R) {
+  KS_REQUIRE(d >= 1 && d <= 128, KS_ESIZE, "qr_r supports 1 <= d <= 128 (got %d)", d);
+  const bool smem = (size_t)d * 2 * d * sizeof(double) * 2 <= QR_SMEM_CAP;  // panel >= 4d rows fits
+  int prows;
+  if (smem) {
+    prows = (int)(QR_SMEM_CAP / (sizeof(double) * d));
+    prows = std::min(prows, 2048);
+  } else {
+    prows = 4 * d;
+  }
+  if (prows < 2 * d) prows = 2 * d;
+  const double* src = A;
+  int64_t rows = n;
+  Scratch<double> buf0((int64_t)((n + prows - 1) / prows) * d * d + d * d, st);
+  Scratch<double> buf1((int64_t)((n + prows - 1) / prows) * d * d + d * d, st);
+  KS_REQUIRE(buf0.p && buf1.p, KS_ECUDA, "scratch allocation failed");
+  Scratch<double> gwork(smem ? 0 : (int64_t)((n + prows - 1) / prows) * prows * d, st);
+  double* bufs[2] = {buf0.p, buf1.p};
+  int which = 0;
+  while (true) {
+    const int64_t nparts = (rows + prows - 1) / prows;
+    double* out = (nparts == 1) ? R : bufs[which];
+    const int cur_rows = (int)ks_min64(prows, rows);
+    if (smem) {
+      const size_t sm = (size_t)cur_rows * d * sizeof(double);
+      KS_TRY_CUDA(cudaFuncSetAttribute(qr_panel_kernel<true>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)QR_SMEM_CAP + 1024));
+      qr_panel_kernel<true><<<(unsigned)nparts, QR_THREADS, sm, st>>>(src, rows, d, prows, out, nullptr);
+    } else {
+      qr_panel_kernel<false><<<(unsigned)nparts, QR_THREADS, 0, st>>>(src, rows, d, prows, out, gwork.p);
+    }
+    KS_CHECK_LAUNCH();
+    if (nparts == 1) break;
+    src = out;
+    rows = nparts * d;
+    which ^= 1;
+  }
+  return KS_OK;
+}
+
+int svd_small(cudaStream_t st, const double* M, int d, double* sigma, double* V) {
+  KS_REQUIRE(d >= 1 && d <= 128, KS_ESIZE, "svd_small supports 1 <= d <= 128 (got %d)", d);
+  const int dp = d + (d & 1);
+  const size_t wbytes = (size_t)dp * d * sizeof(double);
+  const size_t vbytes = (size_t)dp * dp * sizeof(double);
+  const int threads = 512;
+  if (wbytes + vbytes <= QR_SMEM_CAP) {
+    KS_TRY_CUDA(cudaFuncSetAttribute(jacobi_svd_kernel<true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)QR_SMEM_CAP));
+    jacobi_svd_kernel<true><<<1, threads, wbytes + vbytes, st>>>(M, d, sigma, V, nullptr);
+  } else {
+    Scratch<double> vw((int64_t)dp * dp, st);
+    KS_REQUIRE(vw.p, KS_ECUDA, "scratch allocation failed");
+    KS_TRY_CUDA(cudaFuncSetAttribute(jacobi_svd_kernel<false>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)QR_SMEM_CAP));
+    jacobi_svd_kernel<false><<<1, threads, wbytes, st>>>(M, d, sigma, V, vw.p);
+  }
+  KS_CHECK_LAUNCH();
+  return KS_OK;
+}
+
+// Thin SVD of A (n x d) with n >= d: R = qr(A); (sigma, V) = svd(R); U = A V Sigma^-1.
+static int thin_svd_tall(cudaStream_t st, const double* A, int64_t n, int d, double rank_tol,
+                         double* U, double* sigma, double* V) {
+  Scratch<double> R((int64_t)d * d, st);
+  KS_REQUIRE(R.p, KS_ECUDA, "scratch allocation failed");
+  int rc = qr_r(st, A, n, d, R.p);
+  if (rc) return rc;
+  rc = svd_small(st, R.p, d, sigma, V);
+  if (rc) return rc;
+  rc = gemm(st, n, d, d, 1.0, A, d, 1, 0, V, d, 1, 0, 0.0, U, d, 1, 0, 1);
+  if (rc) return rc;
+  scale_cols_kernel<<<ceil_div_u(n * d, 256), 256, 0, st>>>(U, n, d, sigma, rank_tol);
+  KS_CHECK_LAUNCH();
+  return KS_OK;
+}
+
+}  // namespace ks
+
+extern "C" int ks_qr_r(const double* A, int64_t n, int32_t d, double* R, void* stream) {
+  return ks::qr_r((cudaStream_t)stream, A, n, d, R);
+}
+
+extern "C" int ks_svd_small(const double* M, int32_t d, double* sigma, double* V, void* stream) {
+  return ks::svd_small((cudaStream_t)stream, M, d, sigma, V);
+}
+
+// U: n x min(n,d)... to keep the ABI simple the caller provides U (n x k), sigma (k), V (d x k)
+// with k = min(n, d); columns past the rank are zero.
+extern "C" int ks_compact_svd(const double* A, int64_t n, int32_t d, double rank_tol, double* U,
+                              double* sigma, double* V, int32_t* rank, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  KS_REQUIRE(n >= 1 && d >= 1, KS_EINVAL, "compact_svd needs a non-empty matrix");
+  KS_REQUIRE(rank_tol >= 0.0 && rank_tol < 1.0, KS_EINVAL, "rank_tol must be in [0, 1)");
+  int rc;
+  const int k = (int)ks_min64(n, d);
+  if (n >= d) {
+    rc = ks::thin_svd_tall(st, A, n, d, rank_tol, U, sigma, V);
+    if (rc) return rc;
+  } else {
+    // A^T (d x n) = U' S V'^T  =>  A = V' S U'^T: U = V' (n x n), V = U' (d x n)
+    ks::Scratch<double> At((int64_t)d * n, st);
+    KS_REQUIRE(At.p, KS_ECUDA, "scratch allocation failed");
+    transpose_kernel<<<ceil_div_u(n * d, 256), 256, 0, st>>>(A, n, d, At.p);
+    KS_CHECK_LAUNCH();
+    rc = ks::thin_svd_tall(st, At.p, d, (int)n, rank_tol, V, sigma, U);
+    if (rc) return rc;
+    // U holds V' (n x n) already normalised; zero columns past the rank for consistency
+  }
+  std::vector<double> hs(k);
+  KS_TRY_CUDA(cudaMemcpyAsync(hs.data(), sigma, sizeof(double) * k, cudaMemcpyDeviceToHost, st));
+  KS_TRY_CUDA(cudaStreamSynchronize(st));
+  int r = 0;
+  if (hs[0] > 0.0)
+    for (int j = 0; j < k; j++) r += hs[j] > rank_tol * hs[0];
+  *rank = r;
+  return KS_OK;
+}
+
+extern "C" int ks_inverse_small(const double* M, int32_t d, double* X, int32_t* info, void* stream) {
+  KS_REQUIRE(d >= 1 && d <= 128, KS_ESIZE, "inverse_small supports 1 <= d <= 128 (got %d)", d);
+  const size_t smem = (size_t)d * d * sizeof(double);
+  KS_TRY_CUDA(cudaFuncSetAttribute(inverse_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem + 1024));
+  inverse_small_kernel<<<1, 128, smem, (cudaStream_t)stream>>>(M, d, X, info);
+  KS_CHECK_LAUNCH();
+  return KS_OK;
+}

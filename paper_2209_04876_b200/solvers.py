@@ -1,0 +1,497 @@
+"""Kronecker ridge regression solvers on the device.
+
+Drop-in for the north-star functions of pkg/src/kronsolve/solvers.py:
+``RegressionConfig`` (:61-112), ``SolveReport`` (:115-123), ``factor_gram`` / ``FactorGram``
+(:126-150), ``FactorCache`` / ``build_factor_cache`` (:153-163), ``KronPreconditioner`` /
+``pseudo_reciprocal`` / ``build_kron_preconditioner`` (:166-198), ``richardson_solve``
+(:201-248), ``ridge_loss`` (:251-262), ``kronmatmul_svd_solve`` (:302-320),
+``exact_factor_scores`` (:323-331) and ``fast_kronecker_regression`` (:372-462).
+
+Inside ``fast_kronecker_regression`` every step -- Gaussian/uniform streams, Gram and JL
+products, sampler tables, inverse-CDF draws, sketch deduplication, the sketched operator and
+all Richardson iterations -- runs on the GPU; the host only spawns seeds, evaluates the
+sample-count formulas and reads back the iteration count and residual history once."""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import time
+from dataclasses import dataclass, replace
+from functools import reduce
+from typing import Callable, Sequence
+
+import numpy as np
+import torch
+
+from . import _device as D
+from . import _lib
+from .errors import InvalidInputError, NumericalFailureError
+from .kron import (SparseDiagonal, _kron_apply_dev, _view_for, check_factors, kron_operator_shape,
+                   kron_vec_square, sparse_diagonal_from_sketch)
+from .leverage import (JL_LOG_FACTOR, REGRESSION_SAMPLE_CONSTANT, LeverageScores, ProductSampler,
+                       RowSketch, _inverse_small, _jl_scores_dev, _spectral_rows_dev,
+                       ridge_leverage_scores, spectral_sample_count)
+from ._numpy_rng import pcg64_state
+from .tensor import CompactSvd, _compact_svd_dev, as_matrix, compact_svd
+
+DEFAULT_DENSE_GUARD = 10 ** 8
+_DIVERGENCE_WINDOW = 5
+_DIVERGENCE_GROWTH = 10.0
+
+
+@dataclass(frozen=True)
+class RegressionConfig:
+    """Solver knobs (solvers.py:61-112): same fields, defaults and validation."""
+
+    eps: float = 0.25
+    delta: float = 0.05
+    lam: float = 0.0
+    alpha: float = 1.0
+    mode: str = "practical"
+    max_richardson_iters: int | None = None
+    residual_tol: float = 1e-9
+    seed: int = 0
+    damping: float | None = None
+    jl_log_factor: float = JL_LOG_FACTOR
+    share_row_sketch: bool = False
+
+    def __post_init__(self):
+        if not 0.0 < self.eps < 1.0:
+            raise InvalidInputError(f"eps must be in (0, 1), got {self.eps}")
+        if not 0.0 < self.delta < 1.0:
+            raise InvalidInputError(f"delta must be in (0, 1), got {self.delta}")
+        if self.lam < 0.0:
+            raise InvalidInputError(f"lambda must be >= 0, got {self.lam}")
+        if not 0.0 < self.alpha <= 1.0:
+            raise InvalidInputError(f"alpha must be in (0, 1], got {self.alpha}")
+        if self.mode not in ("theoretical", "practical"):
+            raise InvalidInputError(f"unknown mode {self.mode!r}")
+        if self.residual_tol <= 0.0:
+            raise InvalidInputError("residual_tol must be positive")
+
+    @property
+    def effective_alpha(self) -> float:
+        return 1.0 if self.mode == "theoretical" else self.alpha
+
+    @property
+    def effective_damping(self) -> float:
+        return (1.0 - math.sqrt(self.eps)) if self.damping is None else self.damping
+
+    @property
+    def effective_max_iters(self) -> int:
+        if self.max_richardson_iters is not None:
+            return self.max_richardson_iters
+        return 8 * max(1, math.ceil(math.log(1.0 / self.eps)))
+
+    def with_lam(self, lam: float) -> "RegressionConfig":
+        return replace(self, lam=lam)
+
+
+@dataclass(frozen=True)
+class SolveReport:
+    solution: object
+    loss: float
+    iterations: int
+    sample_count: int
+    wall_time: float
+
+
+@dataclass(frozen=True)
+class FactorGram:
+    """``A^T A = v diag(eigenvalues) v^T``; eigenvalues descending, clipped at 0."""
+
+    v: object
+    eigenvalues: object
+    matrix: object
+
+    @property
+    def dim(self) -> int:
+        return int(self.v.shape[0])
+
+
+def _gram_dev(a: torch.Tensor) -> torch.Tensor:
+    n, d = int(a.shape[0]), int(a.shape[1])
+    g = D.empty(d, d)
+    if d <= 128:
+        _lib.call("ks_gemm_tn_tall", d, d, n, 1.0, D.p(a), d, 1, D.p(a), d, 1, D.p(g), D.stream())
+    else:
+        _lib.call("ks_gemm", d, d, n, 1.0, D.p(a), 1, d, 0, D.p(a), d, 1, 0, 0.0, D.p(g), d, 1, 0, 1, D.stream())
+    return g
+
+
+def _factor_gram_dev(g: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor, torch.Tensor]:
+    """Symmetrise and eigendecompose a PSD Gram on the device (one-sided Jacobi)."""
+    d = int(g.shape[0])
+    gs = (0.5 * (g + g.T)).contiguous()
+    if d > 128:
+        from .errors import SizeGuardError
+        raise SizeGuardError(f"device eigensolver supports d <= 128, got {d}")
+    w = D.empty(d)
+    v = D.empty(d, d)
+    _lib.call("ks_svd_small", D.p(gs), d, D.p(w), D.p(v), D.stream())
+    return v, w, gs
+
+
+def factor_gram(a, assume_gram: bool = False) -> FactorGram:
+    """Eigendecomposition of ``a.T @ a`` (or of ``a`` if it is a Gram) -- solvers.py:143-150."""
+    host = not D.on_device(a)
+    at = as_matrix(a)
+    g = at if assume_gram else _gram_dev(at)
+    v, w, gs = _factor_gram_dev(g)
+    return FactorGram(v=D.out(v, host), eigenvalues=D.out(w, host), matrix=D.out(gs, host))
+
+
+@dataclass(frozen=True)
+class FactorCache:
+    svd: CompactSvd
+    gram: FactorGram
+
+
+def build_factor_cache(a) -> FactorCache:
+    host = not D.on_device(a)
+    at = as_matrix(a)
+    u, s, v = _compact_svd_dev(at, 1e-10)
+    gv, gw, gs = _factor_gram_dev(_gram_dev(at))
+    o = lambda t: D.out(t, host)  # noqa: E731
+    return FactorCache(svd=CompactSvd(u=o(u), sigma=o(s), v=o(v)), gram=FactorGram(v=o(gv), eigenvalues=o(gw),
+                                                                                 matrix=o(gs)))
+
+
+def pseudo_reciprocal(d):
+    """Entrywise 1/d with zeros kept at zero (solvers.py:186-191)."""
+    if isinstance(d, torch.Tensor):
+        return torch.where(d > 0, 1.0 / torch.where(d > 0, d, torch.ones_like(d)), torch.zeros_like(d))
+    d = np.asarray(d, dtype=np.float64)
+    out = np.zeros_like(d)
+    nz = d > 0
+    out[nz] = 1.0 / d[nz]
+    return out
+
+
+@dataclass(frozen=True)
+class KronPreconditioner:
+    """``(V kron ...) D (V kron ...)^T`` (solvers.py:166-183)."""
+
+    v_factors: tuple
+    d_diag: object
+    lam: float
+
+    def apply(self, x):
+        host = not D.on_device(x)
+        vs = [D.to_dev(v) for v in self.v_factors]
+        dd = D.to_dev(self.d_diag)
+        xt = D.to_dev(x).reshape(-1)
+        if len(vs) == 2:
+            d1, d2 = int(vs[0].shape[0]), int(vs[1].shape[0])
+            if d1 <= 128 and d2 <= 128:
+                y = D.empty(d1 * d2)
+                _lib.call("ks_kron_precond_apply", D.p(vs[0]), D.p(vs[1]), d1, d2, D.p(dd), D.p(xt.contiguous()),
+                          D.p(y), D.stream())
+                return D.out(y, host)
+        t = _kron_apply_dev([v.T.contiguous() for v in vs], xt[:, None].contiguous())[:, 0] * dd
+        return D.out(_kron_apply_dev(vs, t[:, None].contiguous())[:, 0], host)
+
+
+def build_kron_preconditioner(grams: Sequence[FactorGram], lam: float) -> KronPreconditioner:
+    host = not D.on_device(grams[0].eigenvalues)
+    eig = reduce(torch.kron, [D.to_dev(g.eigenvalues) for g in grams])
+    dd = pseudo_reciprocal(eig + lam)
+    return KronPreconditioner(v_factors=tuple(g.v for g in grams), d_diag=D.out(dd, host), lam=lam)
+
+
+def _norm(x) -> float:
+    if isinstance(x, torch.Tensor):
+        if x.is_cuda:
+            out = D.empty(1)
+            xt = x.reshape(-1).to(D.F64).contiguous()
+            _lib.call("ks_sumsq_diff", D.p(xt), D.p(None), xt.numel(), D.p(out), D.stream())
+            return math.sqrt(float(out.item()))
+        return float(torch.linalg.norm(x.reshape(-1).to(torch.float64)))
+    return float(np.linalg.norm(np.asarray(x, dtype=np.float64)))
+
+
+def richardson_solve(apply_normal: Callable, apply_precond: Callable, rhs, damping: float,
+                     config: RegressionConfig, x0=None, callback: Callable | None = None):
+    """Damped preconditioned Richardson iteration with user callables (solvers.py:201-248).
+
+    Works on NumPy arrays or CUDA tensors (whatever the callables consume).  The fused
+    device loop used by ``fast_kronecker_regression`` is ``ks_richardson_sketched``."""
+    if isinstance(rhs, torch.Tensor):
+        rhs = rhs.reshape(-1).to(torch.float64)
+        x = torch.zeros_like(rhs) if x0 is None else torch.as_tensor(x0, dtype=torch.float64,
+                                                                      device=rhs.device).clone()
+    else:
+        rhs = np.asarray(rhs, dtype=np.float64).reshape(-1)
+        x = np.zeros_like(rhs) if x0 is None else np.array(x0, dtype=np.float64)
+    if tuple(x.shape) != tuple(rhs.shape):
+        raise InvalidInputError("x0 must match the right-hand side length")
+    scale = _norm(apply_precond(rhs))
+    tol = config.residual_tol * max(scale, np.finfo(float).tiny)
+    history: list[float] = []
+    iterations = 0
+    for _ in range(config.effective_max_iters):
+        step = apply_precond(apply_normal(x) - rhs)
+        norm = _norm(step)
+        history.append(norm)
+        if norm <= tol:
+            break
+        if len(history) > _DIVERGENCE_WINDOW:
+            window = history[-(_DIVERGENCE_WINDOW + 1):]
+            if (all(window[i + 1] > window[i] for i in range(_DIVERGENCE_WINDOW))
+                    and window[-1] > _DIVERGENCE_GROWTH * window[0]):
+                raise NumericalFailureError("Richardson iteration diverged", iterations=iterations,
+                                            diagnostics={"residual_history": history})
+        x = x - damping * step
+        iterations += 1
+        if callback is not None:
+            callback(x)
+    return x, iterations
+
+
+def _split_first(facs):
+    """(A_0, kron(A_1..)) with the right group materialised when N > 2."""
+    if len(facs) == 2:
+        return facs[0], facs[1]
+    r = reduce(torch.kron, facs[1:]).contiguous()
+    return facs[0], r
+
+
+def _ridge_loss_dev(facs: list[torch.Tensor], x: torch.Tensor, b: torch.Tensor, lam: float) -> float:
+    out = D.empty(2)
+    rows = [int(a.shape[0]) for a in facs]
+    cols = [int(a.shape[1]) for a in facs]
+    rest_entries = math.prod(rows[1:]) * math.prod(cols[1:])
+    if len(facs) >= 2 and cols[0] <= 128 and math.prod(cols[1:]) <= 128 and rest_entries <= (1 << 25):
+        L, R = _split_first(facs)
+        X = x.reshape(cols[0], -1).contiguous()
+        B = b.reshape(rows[0], -1)
+        _lib.call("ks_kron2_residual_sumsq", D.p(L), D.p(X), D.p(R), D.p(B), int(B.shape[1]), rows[0],
+                  int(B.shape[1]), cols[0], int(X.shape[1]), D.p(out[0:1]), D.stream())
+    else:
+        kx = _kron_apply_dev(facs, x.reshape(-1, 1).contiguous())[:, 0]
+        _lib.call("ks_sumsq_diff", D.p(kx), D.p(b), kx.numel(), D.p(out[0:1]), D.stream())
+    _lib.call("ks_sumsq_diff", D.p(x), D.p(None), x.numel(), D.p(out[1:2]), D.stream())
+    r2, x2 = out.cpu().tolist()
+    return float(r2 + lam * x2)
+
+
+def ridge_loss(factors: Sequence, x, b, lam: float) -> float:
+    """``||K x - b||^2 + lam ||x||^2`` without materialising K x (solvers.py:251-262)."""
+    facs = check_factors(factors)
+    rows, cols = kron_operator_shape(facs)
+    xt = D.to_dev(x).reshape(-1).contiguous()
+    bt = D.to_dev(b).reshape(-1).contiguous()
+    if xt.numel() != cols or bt.numel() != rows:
+        raise InvalidInputError(f"x/b of lengths {xt.numel()}/{bt.numel()} do not match operator {rows}x{cols}")
+    return _ridge_loss_dev(facs, xt, bt, lam)
+
+
+def _validated_problem(factors, b):
+    """solvers.py:265-274: validated device factors; b is kept where it lives."""
+    facs = [D.to_dev(a) for a in factors]
+    if len(facs) == 0:
+        raise InvalidInputError("need at least one factor")
+    flags = torch.zeros(len(facs), 2, dtype=torch.int32, device=D.dev())
+    for n, a in enumerate(facs):
+        if a.ndim != 2:
+            raise InvalidInputError(f"factor {n} must be 2-dimensional, got ndim={a.ndim}")
+        if a.numel():
+            _lib.call("ks_check_finite_nonzero", D.p(a), a.numel(), D.p(flags[n]), D.stream())
+    fl = flags.cpu().tolist()
+    for n, (bad, nz) in enumerate(fl):
+        if bad:
+            raise InvalidInputError(f"factor {n} contains non-finite entries")
+    rows, cols = kron_operator_shape(facs)
+    blen = int(b.numel()) if isinstance(b, torch.Tensor) else int(np.asarray(b).size)
+    if blen != rows:
+        raise InvalidInputError(f"b has length {blen}, operator has {rows} rows")
+    for n, (bad, nz) in enumerate(fl):
+        if not nz:
+            raise InvalidInputError(f"factor {n} is identically zero")
+    return facs, rows, cols
+
+
+def _exact_solve_dev(facs: list[torch.Tensor], bt: torch.Tensor, lam: float) -> torch.Tensor:
+    svds = [_compact_svd_dev(a, 1e-10) for a in facs]
+    us = [s[0] for s in svds]
+    ranks = [int(s[1].numel()) for s in svds]
+    if min(ranks) == 0:
+        return D.zeros(math.prod(int(a.shape[1]) for a in facs))
+    if len(facs) == 2 and ranks[0] <= 128 and ranks[1] <= 128:
+        n1, n2 = int(facs[0].shape[0]), int(facs[1].shape[0])
+        T = D.empty(ranks[0], ranks[1])
+        _lib.call("ks_kron2_contract", D.p(us[0]), D.p(bt), n2, D.p(us[1]), n1, n2, ranks[0], ranks[1], D.p(T),
+                  D.stream())
+        t = T.reshape(-1)
+    else:
+        t = _kron_apply_dev([u.T.contiguous() for u in us], bt.reshape(-1, 1).contiguous())[:, 0]
+    sigma = reduce(torch.kron, [s[1] for s in svds])
+    t = t * (sigma / (sigma * sigma + lam))
+    return _kron_apply_dev([s[2] for s in svds], t.reshape(-1, 1).contiguous())[:, 0]
+
+
+def kronmatmul_svd_solve(factors: Sequence, b, lam: float) -> SolveReport:
+    """Exact ridge solution from factor SVDs and implicit Kronecker products (solvers.py:302-320)."""
+    host = not D.on_device(b)
+    facs, rows, cols = _validated_problem(factors, b)
+    if lam < 0:
+        raise InvalidInputError(f"lambda must be >= 0, got {lam}")
+    bt = D.to_dev(b).reshape(-1)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    x = _exact_solve_dev(facs, bt, lam)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    loss = _ridge_loss_dev(facs, x, bt, lam)
+    return SolveReport(solution=D.out(x, host), loss=loss, iterations=0, sample_count=0, wall_time=wall)
+
+
+def exact_factor_scores(factors: Sequence, caches: Sequence[FactorCache] | None = None) -> list[LeverageScores]:
+    out = []
+    for n, a in enumerate(factors):
+        svd = caches[n].svd if caches is not None else compact_svd(a)
+        out.append(ridge_leverage_scores(svd, 0.0))
+    return out
+
+
+def _regression_sample_count(cols: int, config: RegressionConfig) -> int:
+    return max(1, math.ceil(config.effective_alpha * REGRESSION_SAMPLE_CONSTANT * cols
+                            * math.log(40 * cols) * math.log(1.0 / config.delta) / config.eps))
+
+
+class FastSolveTrace:
+    """Device intermediates of one fast solve (parity tests compare them with the oracle)."""
+
+    def __init__(self):
+        self.__dict__.update(scores=[], eig=[], sampler=None, sketch=None, sdiag=None, rhs=None, history=[],
+                             a_tilde_rows=[])
+
+
+def _fast_solve_dev(facs, b, config: RegressionConfig, caches, trace: FastSolveTrace | None = None):
+    """The device pipeline of solvers.py:404-459; returns (x natural order, iterations, s)."""
+    n_factors = len(facs)
+    rows = [int(a.shape[0]) for a in facs]
+    cols_l = [int(a.shape[1]) for a in facs]
+    cols = math.prod(cols_l)
+    lam = config.lam
+    alpha = config.effective_alpha
+    s = _regression_sample_count(cols, config)
+    seeds = np.random.SeedSequence(config.seed).spawn(2 * n_factors + 1)
+    grams, scores, afs = [], [], []
+    if caches is not None:
+        for cache in caches:
+            g = cache.gram
+            grams.append((D.to_dev(g.v), D.to_dev(g.eigenvalues)))
+            sv = cache.svd
+            scores.append(D.to_dev(ridge_leverage_scores(CompactSvd(D.to_dev(sv.u), D.to_dev(sv.sigma),
+                                                                    D.to_dev(sv.v)), 0.0).scores))
+            afs.append(1.0)
+    else:
+        eps_one = math.log1p(config.eps / 4.0) / n_factors
+        eps_two = eps_one / (2.0 + eps_one)
+        delta_n = config.delta / (2.0 * n_factors)
+        eps_jl = 4.0 * math.log1p(config.eps / 4.0) / n_factors
+        for n, a in enumerate(facs):
+            s_n = math.ceil(alpha * spectral_sample_count(int(a.shape[1]), eps_two, delta_n))
+            if s_n >= int(a.shape[0]):
+                a_tilde = a
+            else:
+                a_tilde = (_spectral_rows_dev(a, eps_two, delta_n, seeds[2 * n], alpha)
+                           / math.sqrt(1.0 - eps_two)).contiguous()
+            if trace is not None:
+                trace.a_tilde_rows.append(int(a_tilde.shape[0]))
+            gt = _gram_dev(a_tilde)
+            v, w, _ = _factor_gram_dev(gt)
+            grams.append((v, w))
+            gi = _inverse_small(gt)
+            scores.append(_jl_scores_dev(a, a_tilde, gi, eps_jl, seeds[2 * n + 1], config.jl_log_factor))
+            afs.append(1.0 + eps_jl / 2.0)
+    sampler = ProductSampler([LeverageScores(sc, 0.0, af) for sc, af in zip(scores, afs)])
+    eig = reduce(torch.kron, [w for _, w in grams])
+    dinv = pseudo_reciprocal(eig + lam)
+    state, inc = pcg64_state(seeds[-1])
+    draws = sampler._sample_dev(s, state, inc)
+    w = sampler._weights_dev(draws, s)
+    sdiag = sparse_diagonal_from_sketch(RowSketch(draws, w), rows)
+    idx = sdiag.indices
+    if isinstance(b, torch.Tensor) and b.is_cuda:
+        b_at = D.empty(sdiag.nnz)
+        _lib.call("ks_gather", D.p(b), D.p(idx), sdiag.nnz, D.p(b_at), D.stream())
+    else:
+        # host-resident b: only the sampled entries cross PCIe (the solve never reads the rest)
+        bh = b.reshape(-1) if isinstance(b, torch.Tensor) else np.asarray(b, dtype=np.float64).reshape(-1)
+        ih = idx.cpu().numpy()
+        b_at = D.to_dev(np.asarray(bh[ih], dtype=np.float64))
+    view = _view_for(facs, sdiag)
+    bv = (sdiag.values * b_at).contiguous()
+    rhs = D.empty(view.dL, view.dR)
+    _lib.call("ks_sketched_transpose_apply", ctypes.byref(view.struct), D.p(bv), D.p(view.perm_arg()), D.p(rhs),
+              D.stream())
+    # preconditioner in grouped (left | right) order
+    left, right = view.part.left, view.part.right
+    VL = reduce(torch.kron, [grams[i][0] for i in left]) if left else torch.ones(1, 1, dtype=D.F64,
+                                                                                 device=D.dev())
+    VR = reduce(torch.kron, [grams[i][0] for i in right])
+    VL = VL.contiguous()
+    VR = VR.contiguous()
+    dg = view.to_groups(dinv).contiguous()
+    x = D.empty(view.dL, view.dR)
+    max_iters = config.effective_max_iters
+    hist = D.zeros(max(1, max_iters))
+    iters = ctypes.c_int32(0)
+    hlen = ctypes.c_int32(0)
+    lib = _lib.load()
+    rc = lib.ks_richardson_sketched(ctypes.byref(view.struct), D.p(VL), D.p(VR), D.p(dg), D.p(rhs),
+                                    float(lam), float(config.effective_damping), int(max_iters),
+                                    float(config.residual_tol), D.p(x), D.p(hist), ctypes.byref(iters),
+                                    ctypes.byref(hlen), D.stream())
+    history = hist[: hlen.value].cpu().tolist()
+    if rc == _lib.KS_EDIVERGED:
+        raise NumericalFailureError("Richardson iteration diverged", iterations=iters.value,
+                                    diagnostics={"residual_history": history})
+    _lib.check(rc, "ks_richardson_sketched")
+    if trace is not None:
+        trace.scores = scores
+        trace.eig = [w for _, w in grams]
+        trace.sampler = sampler
+        trace.sketch = RowSketch(draws, w)
+        trace.sdiag = sdiag
+        trace.rhs = view.from_groups(rhs)
+        trace.history = history
+    return view.from_groups(x), iters.value, s
+
+
+def fast_kronecker_regression(factors: Sequence, b, config: RegressionConfig,
+                              caches: Sequence[FactorCache] | None = None, _trace: FastSolveTrace | None = None
+                              ) -> SolveReport:
+    """(1+eps)-approximate Kronecker ridge regression (solvers.py:372-462), all on the GPU.
+
+    ``wall_time`` covers the solve (as in the reference); the reported loss is evaluated
+    exactly afterwards.  With host-resident ``b`` only its sampled entries are transferred
+    for the solve; the loss pass then uploads it."""
+    host = not D.on_device(b)
+    facs, rows, cols = _validated_problem(factors, b)
+    if not 0.0 < config.eps <= 0.25:
+        raise InvalidInputError(f"fast regression requires eps in (0, 1/4], got {config.eps}")
+    if caches is not None and len(caches) != len(facs):
+        raise InvalidInputError("need one cache entry per factor")
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    s = _regression_sample_count(cols, config)
+    if s >= rows:
+        bt = D.to_dev(b).reshape(-1)
+        x = _exact_solve_dev(facs, bt, config.lam)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        loss = _ridge_loss_dev(facs, x, bt, config.lam)
+        return SolveReport(solution=D.out(x, host), loss=loss, iterations=0, sample_count=0, wall_time=wall)
+    bsrc = b if D.on_device(b) else (b if isinstance(b, torch.Tensor) else np.asarray(b, dtype=np.float64))
+    if D.on_device(bsrc):
+        bsrc = bsrc.reshape(-1).to(torch.float64).contiguous()
+    x, iters, s = _fast_solve_dev(facs, bsrc, config, caches, _trace)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    bt = D.to_dev(b).reshape(-1)
+    loss = _ridge_loss_dev(facs, x, bt, config.lam)
+    return SolveReport(solution=D.out(x, host), loss=loss, iterations=iters, sample_count=s, wall_time=wall)

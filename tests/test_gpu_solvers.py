@@ -1,0 +1,183 @@
+"""Solvers on the device vs the reference golden fixtures and the oracle.
+
+Tolerances: loss <= 1e-9 relative; exact-path x <= 1e-9 relative; fast-path x
+and the step-norm history within max(1e-9, 2x the reference's own 1-ulp noise floor)
+(floor: x 5.7e-9/2.6e-9/7.5e-9, history 1.7e-8/1.4e-8 for c1/c2/c3); iterations and sample
+counts equal; sampled indices bit-exact."""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import dense_kron, rel
+from oracle import kronsolve_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+CASES = {"c1": (1024, 16), "c2": (4096, 32), "c3": (16384, 64)}
+X_TOL = {"c1": 2 * 5.7e-9, "c2": 2 * 2.6e-9, "c3": 2 * 7.5e-9}
+H_TOL = {"c1": 2 * 1.7e-8, "c2": 2 * 1.4e-8, "c3": 2 * 1.4e-8}
+
+
+def cfg(**kw):
+    import paper_2209_04876_b200 as K
+    base = dict(eps=0.1, delta=0.01, lam=1e-3, alpha=1e-5, seed=0)
+    base.update(kw)
+    return K.RegressionConfig(**base)
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3"])
+def test_fast_regression_matches_reference(golden, name):
+    import paper_2209_04876_b200 as K
+    from paper_2209_04876_b200.solvers import FastSolveTrace
+    n, d = CASES[name]
+    g = golden(name)
+    facs, b = O.synth_regression(n, d, 2, 0)
+    tr = FastSolveTrace()
+    rep = K.fast_kronecker_regression(facs, b, cfg(), _trace=tr)
+    assert rep.sample_count == int(g["s"])
+    assert rep.iterations == int(g["iterations"])
+    np.testing.assert_array_equal(tr.sketch.indices.cpu().numpy(), g["indices"].astype(np.int64))
+    # weights carry the JL score differences (gram inverse: ~kappa*u); indices are bit-exact
+    np.testing.assert_allclose(tr.sketch.weights.cpu().numpy(), g["weights"], rtol=1e-10)
+    np.testing.assert_array_equal(tr.sdiag.indices.cpu().numpy(), g["sd_indices"])
+    np.testing.assert_allclose(tr.sdiag.values.cpu().numpy(), g["sd_values"], rtol=1e-10)
+    assert rel(tr.rhs, g["rhs"]) <= 1e-10
+    assert rel(rep.solution, g["x"]) <= max(1e-9, X_TOL[name])
+    assert abs(rep.loss - float(g["loss"])) <= 1e-9 * float(g["loss"])
+    h = np.asarray(tr.history)
+    assert h.size == g["history"].size
+    assert np.max(np.abs(h - g["history"]) / g["history"]) <= max(1e-9, H_TOL[name])
+    assert rep.wall_time > 0
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3"])
+def test_exact_solver_matches_reference(golden, name):
+    import paper_2209_04876_b200 as K
+    n, d = CASES[name]
+    g = golden(name)
+    facs, b = O.synth_regression(n, d, 2, 0)
+    rep = K.kronmatmul_svd_solve(facs, b, 1e-3)
+    assert rel(rep.solution, g["exact_x"]) <= 1e-9
+    assert abs(rep.loss - float(g["opt"])) <= 1e-9 * float(g["opt"])
+
+
+def test_device_resident_inputs_return_device(golden):
+    import paper_2209_04876_b200 as K
+    g = golden("c1")
+    facs, b = O.synth_regression(1024, 16, 2, 0)
+    fd = [torch.tensor(a, device="cuda") for a in facs]
+    bd = torch.tensor(b, device="cuda")
+    rep = K.fast_kronecker_regression(fd, bd, cfg())
+    assert isinstance(rep.solution, torch.Tensor) and rep.solution.is_cuda
+    assert rel(rep.solution, g["x"]) <= X_TOL["c1"]
+
+
+def test_ridge_loss(rng):
+    import paper_2209_04876_b200 as K
+    facs = [rng.standard_normal((5, 2)), rng.standard_normal((4, 3))]
+    k = dense_kron(facs)
+    b = rng.standard_normal(20)
+    x = rng.standard_normal(6)
+    want = np.sum((k @ x - b) ** 2) + 0.05 * x @ x
+    assert K.ridge_loss(facs, x, b, 0.05) == pytest.approx(want, rel=1e-10)
+    assert K.ridge_loss(facs, np.zeros(6), b, 0.7) == pytest.approx(b @ b)
+    facs3 = [rng.standard_normal((6, 2)), rng.standard_normal((5, 3)), rng.standard_normal((4, 2))]
+    k3 = dense_kron(facs3)
+    b3 = rng.standard_normal(120)
+    x3 = rng.standard_normal(12)
+    assert K.ridge_loss(facs3, x3, b3, 0.1) == pytest.approx(np.sum((k3 @ x3 - b3) ** 2) + 0.1 * x3 @ x3, rel=1e-10)
+
+
+def test_exact_solvers_small(rng):
+    import paper_2209_04876_b200 as K
+    b = rng.standard_normal(6)
+    rep = K.kronmatmul_svd_solve([np.eye(2), np.eye(3)], b, 0.4)
+    np.testing.assert_allclose(rep.solution, b / 1.4, atol=1e-10)
+    for lam in (0.0, 1e-3, 1.0):
+        facs = [rng.standard_normal((8, 3)), rng.standard_normal((6, 2))]
+        bb = rng.standard_normal(48)
+        r1 = O.kronmatmul_svd_solve(facs, bb, lam)
+        r2 = K.kronmatmul_svd_solve(facs, bb, lam)
+        np.testing.assert_allclose(r2.solution, r1.solution, atol=1e-10)
+        assert r2.loss == pytest.approx(r1.loss, rel=1e-10)
+    facs3 = [rng.standard_normal((6, 2)), rng.standard_normal((5, 3)), rng.standard_normal((4, 2))]
+    b3 = rng.standard_normal(120)
+    np.testing.assert_allclose(K.kronmatmul_svd_solve(facs3, b3, 0.01).solution,
+                               O.kronmatmul_svd_solve(facs3, b3, 0.01).solution, atol=1e-10)
+
+
+def test_fast_regression_small_cases(rng):
+    import paper_2209_04876_b200 as K
+    from paper_2209_04876_b200.errors import InvalidInputError
+    b = rng.standard_normal(6)
+    rep = K.fast_kronecker_regression([np.eye(2), np.eye(3)], b, K.RegressionConfig(seed=0))
+    np.testing.assert_allclose(rep.solution, b, atol=1e-10)
+    with pytest.raises(InvalidInputError):
+        K.fast_kronecker_regression([np.zeros((3, 2)), np.eye(2)], rng.standard_normal(6), K.RegressionConfig(seed=0))
+    with pytest.raises(InvalidInputError):
+        K.fast_kronecker_regression([rng.standard_normal((4, 2))], rng.standard_normal(4),
+                                    K.RegressionConfig(eps=0.5, seed=0))
+    # sketched path at small scale: same result as the oracle (same streams)
+    for seed in range(5):
+        rs = np.random.default_rng(seed + 1000)
+        facs = [rs.normal(1.0, math.sqrt(1e-3), (20, 3)) for _ in range(2)]
+        bb = rs.standard_normal(400)
+        c = K.RegressionConfig(eps=0.25, delta=0.05, lam=1e-3, seed=seed, alpha=2e-4)
+        r = K.fast_kronecker_regression(facs, bb, c)
+        o = O.fast_kronecker_regression(facs, bb, eps=0.25, delta=0.05, lam=1e-3, seed=seed, alpha=2e-4)
+        assert r.sample_count == o.sample_count and r.iterations == o.iterations
+        assert rel(r.solution, o.solution) <= 1e-7
+        assert r.loss == pytest.approx(o.loss, rel=1e-9)
+
+
+def test_fast_regression_scale_equivariance_and_caches(rng):
+    import paper_2209_04876_b200 as K
+    facs = [rng.standard_normal((12, 2)), rng.standard_normal((10, 2))]
+    b = rng.standard_normal(120)
+    c = K.RegressionConfig(eps=0.25, delta=0.1, lam=1e-3, seed=11, alpha=1e-3)
+    r1 = K.fast_kronecker_regression(facs, b, c)
+    r2 = K.fast_kronecker_regression(facs, 3.0 * b, c)
+    assert r1.sample_count == r2.sample_count
+    np.testing.assert_allclose(r2.solution, 3.0 * r1.solution, rtol=1e-9, atol=1e-12)
+    facs = [rng.standard_normal((15, 2)), rng.standard_normal((12, 3))]
+    b = rng.standard_normal(180)
+    caches = [K.build_factor_cache(a) for a in facs]
+    c = K.RegressionConfig(eps=0.25, delta=0.1, lam=1e-2, seed=4, alpha=1e-3)
+    rep = K.fast_kronecker_regression(facs, b, c, caches=caches)
+    o = O.fast_kronecker_regression(facs, b, eps=0.25, delta=0.1, lam=1e-2, seed=4, alpha=1e-3,
+                                    caches=[O.factor_cache(a) for a in facs])
+    assert rel(rep.solution, o.solution) <= 1e-8
+    assert rep.loss <= 1.3 * O.kronmatmul_svd_solve(facs, b, 1e-2).loss
+
+
+def test_richardson_generic(rng):
+    import paper_2209_04876_b200 as K
+    from paper_2209_04876_b200.errors import NumericalFailureError
+    a = rng.standard_normal((8, 3))
+    b = rng.standard_normal(8)
+    ata = a.T @ a
+    inv = np.linalg.inv(ata)
+    x, it = K.richardson_solve(lambda v: ata @ v, lambda v: inv @ v, a.T @ b, 1.0, K.RegressionConfig(eps=0.25))
+    assert it == 1
+    bad = -inv
+    with pytest.raises(NumericalFailureError) as err:
+        K.richardson_solve(lambda v: ata @ v, lambda v: bad @ v, rng.standard_normal(3), 1.0,
+                           K.RegressionConfig(eps=0.25, max_richardson_iters=50, residual_tol=1e-300))
+    assert "residual_history" in err.value.diagnostics
+
+
+def test_fused_richardson_divergence_rule(golden):
+    """The device loop applies the reference's divergence rule (solvers.py:236-243)."""
+    import paper_2209_04876_b200 as K
+    from paper_2209_04876_b200.errors import NumericalFailureError
+    facs, b = O.synth_regression(1024, 16, 2, 0)
+    with pytest.raises(NumericalFailureError) as err:
+        K.fast_kronecker_regression(facs, b, cfg(damping=-1.0, max_richardson_iters=60))
+    hist = err.value.diagnostics["residual_history"]
+    assert len(hist) >= 6 and hist[-1] > 10 * hist[-6]
+    with pytest.raises(NumericalFailureError):
+        O.fast_kronecker_regression(facs, b, eps=0.1, delta=0.01, lam=1e-3, alpha=1e-5, seed=0, damping=-1.0,
+                                    max_iters=60)
