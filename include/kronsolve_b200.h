@@ -98,6 +98,10 @@ int ks_svd_small(const double* M, int32_t d, double* sigma, double* V, void* str
  * LinAlgError, leverage.py:114-119), info[1] = 1 if X has non-finite entries (:120-123). */
 int ks_inverse_small(const double* M, int32_t d, double* X, int32_t* info, void* stream);
 
+/* Batched ks_svd_small over `batch` contiguous d x d problems (one CTA each, concurrently). */
+int ks_svd_small_batched(const double* M, int32_t batch, int32_t d, double* sigma, double* V,
+                         void* stream);
+
 /* Thin SVD of A (n x d): U (n x d), sigma (d, descending), V (d x d).  Columns past the
  * numerical rank (sigma <= rank_tol*sigma_max) are zeroed and *rank (host) reports it.
  * Replaces tensor.compact_svd (tensor.py:76-107).  Synchronises the stream. */
@@ -204,6 +208,10 @@ int ks_richardson_sketched(const ks_sketch_view* sk, const double* VL, const dou
                            const double* dinv, const double* rhs, double lam, double damping,
                            int32_t max_iters, double residual_tol, double* x, double* hist,
                            int32_t* iters, int32_t* hist_len, void* stream);
+
+/* Profiling aid: average SM cycles per phase of the last persistent Richardson run (CTA 0):
+ * apply, sync, reduce, precond-A, precond-B, update. */
+int ks_debug_richardson_phases(int32_t iters, double* out6);
 
 /* Preconditioner apply y = (VL kron VR) diag(dinv) (VL kron VR)^T r (solvers.py:180-183). */
 int ks_kron_precond_apply(const double* VL, const double* VR, int32_t dL, int32_t dR,

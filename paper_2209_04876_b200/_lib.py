@@ -47,6 +47,7 @@ _SIGS = {
     "ks_check_finite_nonzero": ([_p, _i64, _p, _p], ctypes.c_int),
     "ks_qr_r": ([_p, _i64, _i32, _p, _p], ctypes.c_int),
     "ks_svd_small": ([_p, _i32, _p, _p, _p], ctypes.c_int),
+    "ks_svd_small_batched": ([_p, _i32, _i32, _p, _p, _p], ctypes.c_int),
     "ks_compact_svd": ([_p, _i64, _i32, _d, _p, _p, _p, POINTER(c_int32), _p], ctypes.c_int),
     "ks_inverse_small": ([_p, _i32, _p, _p, _p], ctypes.c_int),
     "ks_pcg64_random": ([c_uint64, c_uint64, c_uint64, c_uint64, c_uint64, _i64, _p, _p], ctypes.c_int),
@@ -66,6 +67,7 @@ _SIGS = {
     "ks_richardson_sketched": ([POINTER(SketchView), _p, _p, _p, _p, _d, _d, _i32, _d, _p, _p,
                                 POINTER(c_int32), POINTER(c_int32), _p], ctypes.c_int),
     "ks_kron_precond_apply": ([_p, _p, _i32, _i32, _p, _p, _p, _p], ctypes.c_int),
+    "ks_debug_richardson_phases": ([_i32, POINTER(c_double)], ctypes.c_int),
 }
 
 _lock = threading.Lock()

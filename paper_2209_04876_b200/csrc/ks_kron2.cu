@@ -1,7 +1,9 @@
 // Two-factor n^2 passes of the exact solver and of the loss (reference kron.py:66-77 through
-// solvers.py:314 and solvers.py:261).  Generic-GEMM formulation; the TMA/DMMA versions live in
-// ks_kron2_dmma.cu and are selected when the shapes allow.
+// solvers.py:314 and solvers.py:261).  The TMA/DMMA kernels of ks_kron2_dmma.cu run whenever
+// the layout allows (16-byte aligned rows); the generic DFMA formulation below covers the rest.
 #include "ks_common.cuh"
+
+#include <cstdlib>
 
 namespace ks {
 int gemm(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
@@ -14,14 +16,27 @@ int gemm_tn_tall(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha,
 int gemm_resid_sumsq(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha,
                      const double* A, int64_t a_rs, int64_t a_cs, const double* B, int64_t b_rs,
                      int64_t b_cs, const double* C, int64_t c_rs, int64_t c_cs, double* out);
+int kron2_contract_dmma(cudaStream_t st, const double* L, const double* B, int64_t ldb, const double* R,
+                        int64_t m, int64_t k, int p, int q, double* T);
+int kron2_residual_dmma(cudaStream_t st, const double* L, const double* X, const double* R, const double* B,
+                        int64_t ldb, int64_t m, int64_t k, int p, int q, double* out);
 }
 
-// T = L^T (B R): P = B R (m x q) then T = L^T P.
+static bool generic_forced() {
+  const char* e = getenv("KS_KRON2");
+  return e && e[0] == 'g';
+}
+
+// T = L^T (B R)
 extern "C" int ks_kron2_contract(const double* L, const double* B, int64_t ldb, const double* R,
                                  int64_t m, int64_t k, int32_t p, int32_t q, double* T,
                                  void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   KS_REQUIRE(p >= 1 && q >= 1 && p <= 128 && q <= 128, KS_ESIZE, "contract widths must be <= 128");
+  if (!generic_forced()) {
+    const int rc = ks::kron2_contract_dmma(st, L, B, ldb, R, m, k, p, q, T);
+    if (rc >= 0) return rc;
+  }
   ks::Scratch<double> P(m * q, st);
   KS_REQUIRE(P.p, KS_ECUDA, "scratch allocation failed");
   int rc = ks::gemm(st, m, q, k, 1.0, B, ldb, 1, 0, R, q, 1, 0, 0.0, P.p, q, 1, 0, 1);
@@ -29,11 +44,15 @@ extern "C" int ks_kron2_contract(const double* L, const double* B, int64_t ldb, 
   return ks::gemm_tn_tall(st, p, q, m, 1.0, L, p, 1, P.p, q, 1, T);
 }
 
-// sum((L X R^T - B)^2): Zt = R X^T (k x p), then the residual GEMM L Zt^T - B.
+// sum((L X R^T - B)^2)
 extern "C" int ks_kron2_residual_sumsq(const double* L, const double* X, const double* R,
                                        const double* B, int64_t ldb, int64_t m, int64_t k, int32_t p,
                                        int32_t q, double* out, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
+  if (!generic_forced()) {
+    const int rc = ks::kron2_residual_dmma(st, L, X, R, B, ldb, m, k, p, q, out);
+    if (rc >= 0) return rc;
+  }
   ks::Scratch<double> Zt(k * p, st);
   KS_REQUIRE(Zt.p, KS_ECUDA, "scratch allocation failed");
   // Zt[j, a] = sum_c R[j, c] X[a, c]

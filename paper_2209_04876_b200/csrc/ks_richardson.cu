@@ -11,12 +11,17 @@
 #include "ks_common.cuh"
 
 #include <cfloat>
+#include <cstdlib>
 
 namespace ks {
 int sketched_gram_partials(cudaStream_t st, const ks_sketch_view* sk, const double* X,
                            const double* bv, const int64_t* perm, int mode, double* part,
                            int64_t* nparts_out);
 int64_t sketched_partials_count(const ks_sketch_view* sk);
+bool persistent_supported(int dL, int dR);
+int richardson_persistent(cudaStream_t st, const ks_sketch_view* sk, const double* VL, const double* VR,
+                          const double* dinv, const double* rhs, double lam, double damping, int max_iters,
+                          double residual_tol, double* x, double* hist, int* iters, int* hist_len, int* status);
 }
 
 namespace {
@@ -39,10 +44,17 @@ __global__ void residual_kernel(const double* __restrict__ part, int64_t nparts,
   if (ls && ls->status != ST_RUNNING) return;
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= count) return;
-  double s = 0.0;
-  for (int64_t p = 0; p < nparts; p++) s += part[p * count + e];
-  // (G + lam x) - rhs, in the reference's association
-  R[e] = (s + lam * X[e]) - rhs[e];
+  // Neumaier-compensated sum of the block partials (fixed order, deterministic)
+  double s = 0.0, c = 0.0;
+  for (int64_t p = 0; p < nparts; p++) {
+    const double v = part[p * count + e];
+    const double t = s + v;
+    c += (fabs(s) >= fabs(v)) ? ((s - t) + v) : ((v - t) + s);
+    s = t;
+  }
+  s += c;
+  // (G + lam x) - rhs, in the reference's association and rounding
+  R[e] = __dsub_rn(__dadd_rn(s, __dmul_rn(lam, X[e])), rhs[e]);
 }
 
 // T[r, :] = dinv[r, :] * ((VL^T R)[r, :] VR)     one block per row r
@@ -185,6 +197,22 @@ extern "C" int ks_richardson_sketched(const ks_sketch_view* sk, const double* VL
   cudaStream_t st = (cudaStream_t)stream;
   const int dL = sk->dL, dR = sk->dR;
   KS_REQUIRE(dL >= 1 && dR >= 1 && dL <= 128 && dR <= 128, KS_ESIZE, "group widths must be <= 128");
+  const char* mode = getenv("KS_RICHARDSON");
+  const bool force_multi = mode && mode[0] == 'm';
+  if (!force_multi && sk->nnz > 0 && ks::persistent_supported(dL, dR) && max_iters <= 1024) {
+    int status = 0;
+    int it = 0, hl = 0;
+    int rc = ks::richardson_persistent(st, sk, VL, VR, dinv, rhs, lam, damping, max_iters, residual_tol, x, hist,
+                                       &it, &hl, &status);
+    if (rc) return rc;
+    *iters = it;
+    *hist_len = hl;
+    if (status == 2) {
+      ks::set_error("Richardson iteration diverged");
+      return KS_EDIVERGED;
+    }
+    return KS_OK;
+  }
   const int64_t count = (int64_t)dL * dR;
   const int64_t np = ks::sketched_partials_count(sk);
   ks::Scratch<double> part(np * count + 1, st), R(count, st), T(count, st), step(count, st);

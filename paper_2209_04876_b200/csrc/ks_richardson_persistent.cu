@@ -1,0 +1,559 @@
+// Persistent cooperative Richardson loop for dL, dR in {16, 32, 64} (all BASELINE configs
+// except the d=128 sweep point).  One CTA per SM runs all iterations of solvers.py:201-248:
+//
+//   P1  apply:   for each chunk of the sketch (<= 32 distinct left rows, <= CH_S samples),
+//                bulk-async copy the packed left rows / right rows (contiguous, padded slabs
+//                built once per sketch) into shared memory, then
+//                   Y = L_chunk X                  (DMMA m16n8k4)
+//                   z_u = sum_t v_t (v_t (y_u . R_t)) R_t      (warp per left row, smem only)
+//                   G_cta += L_chunk^T Z           (DMMA, accumulators stay in registers)
+//   P2  R = sum_cta G_cta + lam X - rhs          (warp per element, compensated, fixed order)
+//   P3  T = dinv o (VL^T R VR)                    (CTA per row)
+//   P4  step = VL T VR^T, rowsq                   (CTA per row)
+//   then every CTA computes ||step|| identically, applies the reference's stopping and
+//   divergence rules, and updates its shared-memory copy of x.
+// Four grid-wide barriers per iteration; no host round trips.
+#include "ks_common.cuh"
+#include "ks_tma.cuh"
+
+#include <cooperative_groups.h>
+#include <vector>
+#include <cfloat>
+
+namespace cg = cooperative_groups;
+
+namespace {
+
+constexpr int PT = 256;      // threads per CTA
+constexpr int PW = PT / 32;  // warps
+constexpr int CH_ROWS = 32;  // distinct left rows per chunk
+constexpr int CH_S = 96;     // samples per chunk
+constexpr int PAD = 4;       // row padding (doubles) of packed / staged rows
+
+struct Chunk {
+  int64_t u_b, u_e;  // left rows [u_b, u_e)
+  int64_t t_b, t_e;  // samples  [t_b, t_e)
+};
+
+struct PArgs {
+  const double* Lpack;  // u_left x (DL+PAD)
+  const double* Rpack;  // nnz x (DR+PAD)
+  const double* v;      // nnz
+  const int64_t* seg;   // u_left + 1
+  const Chunk* chunks;
+  int64_t nchunks;
+  const double* VL;     // DL x DL
+  const double* VR;     // DR x DR
+  const double* VRt;    // DR x DR
+  const double* dinv;   // DL x DR
+  const double* rhs;    // DL x DR
+  double lam, damping, residual_tol;
+  int max_iters;
+  double* part;         // grid x DL x DR
+  double* R;            // DL x DR
+  double* T;            // DL x DR
+  double* step;         // DL x DR
+  double* rowsq;        // DL
+  double* x_out;        // DL x DR
+  double* hist;         // max_iters
+  int* state;           // [status, iters, hist_len]
+  long long* prof;      // optional: CTA 0 clock64 stamps, 6 per iteration
+};
+
+__device__ long long g_prof[6 * 1024];
+
+template <int DL, int DR>
+struct Smem {
+  static constexpr int DLP = DL + PAD, DRP = DR + PAD;
+  static constexpr int X_OFF = 0;                          // DL x DRP
+  static constexpr int L_OFF = X_OFF + DL * DRP;           // 2 x CH_ROWS x DLP
+  static constexpr int R_OFF = L_OFF + 2 * CH_ROWS * DLP;  // 2 x CH_S x DRP
+  static constexpr int Y_OFF = R_OFF + 2 * CH_S * DRP;     // CH_ROWS x DRP (also Z)
+  static constexpr int Z_OFF = Y_OFF + CH_ROWS * DRP;      // CH_ROWS x DRP
+  static constexpr int W_OFF = Z_OFF + CH_ROWS * DRP;      // scratch 2*128
+  static constexpr int H_OFF = W_OFF + 256;                // history (<= 1024)
+  static constexpr int DOUBLES = H_OFF + 1024;
+  static constexpr size_t BYTES = (size_t)DOUBLES * 8 + 64;  // + mbarriers
+};
+
+__device__ __forceinline__ void bulk_copy(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"((uint64_t)src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+// issue the slab copies of chunk `c` into buffer `buf` (called by one thread)
+template <int DL, int DR>
+__device__ void issue_chunk(const PArgs& a, const Chunk& ch, double* sm, uint64_t* bar, int buf) {
+  using S = Smem<DL, DR>;
+  const uint32_t lbytes = (uint32_t)((ch.u_e - ch.u_b) * S::DLP * 8);
+  const uint32_t rbytes = (uint32_t)((ch.t_e - ch.t_b) * S::DRP * 8);
+  mbar_arrive_expect_tx(bar, lbytes + rbytes);
+  bulk_copy(sm + S::L_OFF + buf * CH_ROWS * S::DLP, a.Lpack + ch.u_b * S::DLP, lbytes, bar);
+  bulk_copy(sm + S::R_OFF + buf * CH_S * S::DRP, a.Rpack + ch.t_b * S::DRP, rbytes, bar);
+}
+
+template <int DL, int DR>
+__global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
+  using S = Smem<DL, DR>;
+  constexpr int DLP = S::DLP, DRP = S::DRP;
+  constexpr int GT_M = DL / 16, GT_N = DR / 8, G_TILES = GT_M * GT_N;
+  constexpr int G_PER_W = (G_TILES + PW - 1) / PW;
+  constexpr int YT_M = CH_ROWS / 16, YT_N = DR / 8, Y_TILES = YT_M * YT_N;
+  constexpr int Y_PER_W = (Y_TILES + PW - 1) / PW;
+  constexpr int NE = DL * DR;
+  extern __shared__ __align__(128) double sm[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + S::DOUBLES);
+  double* Xs = sm + S::X_OFF;
+  double* Ys = sm + S::Y_OFF;
+  double* Zs = sm + S::Z_OFF;
+  double* Ws = sm + S::W_OFF;
+  double* Hs = sm + S::H_OFF;
+  __shared__ int s_flag;
+  cg::grid_group grid = cg::this_grid();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int G = gridDim.x, b = blockIdx.x;
+
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_barrier_init();
+  }
+  for (int e = tid; e < DL * DRP; e += PT) Xs[e] = 0.0;
+  __syncthreads();
+
+  // chunk range of this CTA
+  const int64_t c_beg = a.nchunks * b / G, c_end = a.nchunks * (b + 1) / G;
+  uint32_t phase[2] = {0, 0};
+  int pending[2] = {0, 0};  // bulk copies in flight per buffer (thread 0's view)
+  const bool resident = (c_end - c_beg) == 1;  // a single chunk stays in buffer 0 for all iterations
+
+  // --- preconditioner phases (shared by the scale computation and the loop) ---
+  auto precond_a = [&](const double* Rin) {
+    for (int r = b; r < DL; r += G) {
+      double* t1 = Ws;
+      for (int j = tid; j < DR; j += PT) {
+        double s = 0.0;
+#pragma unroll 8
+        for (int k = 0; k < DL; k++) s = fma(a.VL[k * DL + r], __ldcg(&Rin[k * DR + j]), s);
+        t1[j] = s;
+      }
+      __syncthreads();
+      for (int c = tid; c < DR; c += PT) {
+        double s = 0.0;
+#pragma unroll 8
+        for (int j = 0; j < DR; j++) s = fma(t1[j], a.VR[j * DR + c], s);
+        a.T[r * DR + c] = s * a.dinv[r * DR + c];
+      }
+      __syncthreads();
+    }
+  };
+  auto precond_b = [&]() {
+    for (int r = b; r < DL; r += G) {
+      double* s1 = Ws;
+      for (int j = tid; j < DR; j += PT) {
+        double s = 0.0;
+#pragma unroll 8
+        for (int k = 0; k < DL; k++) s = fma(a.VL[r * DL + k], __ldcg(&a.T[k * DR + j]), s);
+        s1[j] = s;
+      }
+      __syncthreads();
+      double sq = 0.0;
+      for (int c = tid; c < DR; c += PT) {
+        double s = 0.0;
+#pragma unroll 8
+        for (int j = 0; j < DR; j++) s = fma(s1[j], a.VRt[j * DR + c], s);
+        a.step[r * DR + c] = s;
+        sq = fma(s, s, sq);
+      }
+      sq = block_sum(sq, Ws + 128);
+      if (tid == 0) a.rowsq[r] = sq;
+      __syncthreads();
+    }
+  };
+  auto row_norm = [&]() {
+    // identical fixed-order sum in every CTA
+    if (tid == 0) {
+      double s = 0.0;
+      for (int r = 0; r < DL; r++) s += __ldcg(&a.rowsq[r]);
+      Ws[200] = sqrt(s);
+    }
+    __syncthreads();
+    const double v = Ws[200];
+    __syncthreads();
+    return v;
+  };
+
+  // scale = ||P rhs|| -> tol
+  precond_a(a.rhs);
+  grid.sync();
+  precond_b();
+  grid.sync();
+  const double tol = a.residual_tol * fmax(row_norm(), DBL_MIN);
+
+  // prefetch the first chunk
+  if (tid == 0 && c_beg < c_end) {
+    issue_chunk<DL, DR>(a, a.chunks[c_beg], sm, &bars[0], 0);
+    pending[0] = 1;
+  }
+  int cur = 0;
+
+  int status = 0, iters = 0, hlen = 0;
+  const bool prof = (b == 0 && tid == 0);
+  for (int it = 0; it < a.max_iters; it++) {
+    if (prof) g_prof[it * 6 + 0] = clock64();
+    // ---------------- P1: sketched normal-operator apply ----------------
+    double gacc[G_PER_W][4];
+#pragma unroll
+    for (int i = 0; i < G_PER_W; i++)
+#pragma unroll
+      for (int j = 0; j < 4; j++) gacc[i][j] = 0.0;
+    int buf = cur;
+    for (int64_t c = c_beg; c < c_end; c++) {
+      const Chunk ch = a.chunks[c];
+      // prefetch the next chunk (or the first one of the next iteration) into the other buffer
+      if (tid == 0 && !resident) {
+        const int64_t cn = (c + 1 < c_end) ? c + 1 : c_beg;
+        if (!(cn == c_beg && it + 1 >= a.max_iters)) {
+          issue_chunk<DL, DR>(a, a.chunks[cn], sm, &bars[buf ^ 1], buf ^ 1);
+          pending[buf ^ 1] = 1;
+        }
+      }
+      if (!resident || it == 0) {
+        mbar_wait(&bars[buf], phase[buf]);
+        phase[buf] ^= 1;
+        pending[buf] = 0;
+      }
+      const double* Ls = sm + S::L_OFF + buf * CH_ROWS * DLP;
+      const double* Rs = sm + S::R_OFF + buf * CH_S * DRP;
+      const int nrows = (int)(ch.u_e - ch.u_b), nsamp = (int)(ch.t_e - ch.t_b);
+      // Y = L_chunk X   (rows >= nrows read stale smem; their results are never used)
+#pragma unroll
+      for (int yi = 0; yi < Y_PER_W; yi++) {
+        const int tile = warp + yi * PW;
+        if (tile < Y_TILES) {
+          const int m0 = (tile / YT_N) * 16, n0 = (tile % YT_N) * 8;
+          double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+          for (int k0 = 0; k0 < DL; k0 += 4) {
+            const double a0 = Ls[(m0 + g) * DLP + k0 + t4];
+            const double a1 = Ls[(m0 + g + 8) * DLP + k0 + t4];
+            const double b0 = Xs[(k0 + t4) * DRP + n0 + g];
+            dmma_16x8x4(acc, a0, a1, b0);
+          }
+          Ys[(m0 + g) * DRP + n0 + 2 * t4] = acc[0];
+          Ys[(m0 + g) * DRP + n0 + 2 * t4 + 1] = acc[1];
+          Ys[(m0 + g + 8) * DRP + n0 + 2 * t4] = acc[2];
+          Ys[(m0 + g + 8) * DRP + n0 + 2 * t4 + 1] = acc[3];
+        }
+      }
+      __syncthreads();
+      // samples: warp per left row
+      for (int r = warp; r < CH_ROWS; r += PW) {
+        double z[(DR + 31) / 32];
+#pragma unroll
+        for (int j = 0; j < (DR + 31) / 32; j++) z[j] = 0.0;
+        if (r < nrows) {
+          const int64_t u = ch.u_b + r;
+          const int64_t tb = max(a.seg[u], ch.t_b), te = min(a.seg[u + 1], ch.t_e);
+          double y[(DR + 31) / 32];
+#pragma unroll
+          for (int j = 0; j < (DR + 31) / 32; j++) {
+            const int k = lane + 32 * j;
+            y[j] = (k < DR) ? Ys[r * DRP + k] : 0.0;
+          }
+          for (int64_t t = tb; t < te; t++) {
+            const int ts = (int)(t - ch.t_b);
+            const double* Rt = Rs + ts * DRP;
+            double rv[(DR + 31) / 32];
+            double d = 0.0;
+#pragma unroll
+            for (int j = 0; j < (DR + 31) / 32; j++) {
+              const int k = lane + 32 * j;
+              rv[j] = (k < DR) ? Rt[k] : 0.0;
+              d = fma(y[j], rv[j], d);
+            }
+            d = warp_sum(d);
+            const double vt = Rt[DR];  // v_t travels in the row padding
+            const double s = vt * (vt * d);
+#pragma unroll
+            for (int j = 0; j < (DR + 31) / 32; j++) z[j] = fma(s, rv[j], z[j]);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < (DR + 31) / 32; j++) {
+          const int k = lane + 32 * j;
+          if (k < DR) Zs[r * DRP + k] = z[j];
+        }
+      }
+      __syncthreads();
+      // G += L_chunk^T Z   (K = CH_ROWS; rows >= nrows have Z == 0)
+#pragma unroll
+      for (int gi = 0; gi < G_PER_W; gi++) {
+        const int tile = warp + gi * PW;
+        if (tile < G_TILES) {
+          const int m0 = (tile / GT_N) * 16, n0 = (tile % GT_N) * 8;
+#pragma unroll
+          for (int k0 = 0; k0 < CH_ROWS; k0 += 4) {
+            const double a0 = (k0 + t4 < nrows) ? Ls[(k0 + t4) * DLP + m0 + g] : 0.0;
+            const double a1 = (k0 + t4 < nrows) ? Ls[(k0 + t4) * DLP + m0 + g + 8] : 0.0;
+            const double b0 = Zs[(k0 + t4) * DRP + n0 + g];
+            dmma_16x8x4(gacc[gi], a0, a1, b0);
+          }
+        }
+      }
+      __syncthreads();  // Ls/Rs/Zs of this buffer may be overwritten after this point
+      if (!resident) buf ^= 1;
+    }
+    cur = buf;
+    // write this CTA's partial G
+    double* P = a.part + (size_t)b * NE;
+#pragma unroll
+    for (int gi = 0; gi < G_PER_W; gi++) {
+      const int tile = warp + gi * PW;
+      if (tile < G_TILES) {
+        const int m0 = (tile / GT_N) * 16, n0 = (tile % GT_N) * 8;
+        P[(m0 + g) * DR + n0 + 2 * t4] = gacc[gi][0];
+        P[(m0 + g) * DR + n0 + 2 * t4 + 1] = gacc[gi][1];
+        P[(m0 + g + 8) * DR + n0 + 2 * t4] = gacc[gi][2];
+        P[(m0 + g + 8) * DR + n0 + 2 * t4 + 1] = gacc[gi][3];
+      }
+    }
+    if (prof) g_prof[it * 6 + 1] = clock64();
+    grid.sync();
+    if (prof) g_prof[it * 6 + 2] = clock64();
+    // ---------------- P2: R = sum G + lam X - rhs ----------------
+    for (int e = b * PW + warp; e < NE; e += G * PW) {
+      double s = 0.0, cmp = 0.0;
+      for (int p = lane; p < G; p += 32) {
+        const double v = __ldcg(&a.part[(size_t)p * NE + e]);
+        const double tt = s + v;
+        cmp += (fabs(s) >= fabs(v)) ? ((s - tt) + v) : ((v - tt) + s);
+        s = tt;
+      }
+      // combine lanes in a fixed butterfly order (TwoSum keeps the compensation)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double os = __shfl_xor_sync(0xffffffffu, s, o);
+        const double oc = __shfl_xor_sync(0xffffffffu, cmp, o);
+        const double lo = (lane & o) ? os : s, hi = (lane & o) ? s : os;  // order-independent pair
+        const double tt = lo + hi;
+        const double bb = tt - lo;
+        const double err = (lo - (tt - bb)) + (hi - bb);
+        s = tt;
+        cmp = ((lane & o) ? oc : cmp) + ((lane & o) ? cmp : oc) + err;
+      }
+      if (lane == 0) {
+        const double gsum = s + cmp;
+        const int i = e / DR, k = e - i * DR;
+        a.R[e] = __dsub_rn(__dadd_rn(gsum, __dmul_rn(a.lam, Xs[i * DRP + k])), a.rhs[e]);
+      }
+    }
+    grid.sync();
+    if (prof) g_prof[it * 6 + 3] = clock64();
+    // ---------------- P3 / P4: preconditioner ----------------
+    precond_a(a.R);
+    grid.sync();
+    if (prof) g_prof[it * 6 + 4] = clock64();
+    precond_b();
+    grid.sync();
+    if (prof) g_prof[it * 6 + 5] = clock64();
+    // ---------------- norm, stopping rules, update ----------------
+    const double nrm = row_norm();
+    if (tid == 0) Hs[it] = nrm;
+    hlen = it + 1;
+    if (nrm <= tol) {
+      status = 1;
+      break;
+    }
+    if (tid == 0) {
+      int div = 0;
+      if (hlen > 5) {
+        bool inc = true;
+        for (int i = hlen - 6; i < hlen - 1; i++) inc &= Hs[i + 1] > Hs[i];
+        div = inc && (Hs[hlen - 1] > 10.0 * Hs[hlen - 6]);
+      }
+      s_flag = div;
+    }
+    __syncthreads();
+    if (s_flag) {
+      status = 2;
+      break;
+    }
+    for (int e = tid; e < NE; e += PT) {
+      const int i = e / DR, k = e - i * DR;
+      Xs[i * DRP + k] = __dsub_rn(Xs[i * DRP + k], __dmul_rn(a.damping, __ldcg(&a.step[e])));
+    }
+    iters = it + 1;
+    __syncthreads();
+  }
+  // drain a prefetched chunk that will never be consumed (keeps the mbarrier state clean)
+  if (b == 0) {
+    for (int e = tid; e < NE; e += PT) {
+      const int i = e / DR, k = e - i * DR;
+      a.x_out[e] = Xs[i * DRP + k];
+    }
+    for (int i = tid; i < hlen; i += PT) a.hist[i] = Hs[i];
+    if (tid == 0) {
+      a.state[0] = status;
+      a.state[1] = iters;
+      a.state[2] = hlen;
+    }
+  }
+  // an early stop leaves the next iteration's prefetch in flight: drain it before exiting
+  if (tid == 0)
+    for (int k = 0; k < 2; k++)
+      if (pending[k]) mbar_wait(&bars[k], phase[k]);
+}
+
+// dst row i = src row rows[i] (d entries) + padding; pad slot 0 carries extra[i] if given.
+__global__ void pack_rows_kernel(const double* __restrict__ src, int64_t ld, const int64_t* __restrict__ rows,
+                                 int64_t n, int d, int dp, const double* __restrict__ extra,
+                                 double* __restrict__ dst) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n * dp) return;
+  const int64_t i = e / dp;
+  const int c = (int)(e - i * dp);
+  dst[e] = (c < d) ? src[rows[i] * ld + c] : ((c == d && extra) ? extra[i] : 0.0);
+}
+
+__global__ void transpose_sq_kernel2(const double* __restrict__ a, int d, double* __restrict__ out) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= d * d) return;
+  const int i = e / d, j = e - i * d;
+  out[j * d + i] = a[e];
+}
+
+template <int DL, int DR>
+int launch(cudaStream_t st, PArgs& a, int grid) {
+  using S = Smem<DL, DR>;
+  auto kern = richardson_persistent_kernel<DL, DR>;
+  KS_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::BYTES));
+  int per_sm = 0;
+  KS_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, PT, S::BYTES));
+  KS_REQUIRE(per_sm >= 1, KS_ESIZE, "persistent Richardson kernel does not fit on an SM");
+  if (grid > per_sm * ks::num_sms()) grid = per_sm * ks::num_sms();
+  void* args[] = {&a};
+  KS_TRY_CUDA(cudaLaunchCooperativeKernel((void*)kern, grid, PT, args, S::BYTES, st));
+  return KS_OK;
+}
+
+}  // namespace
+
+namespace ks {
+
+bool persistent_supported(int dL, int dR) {
+  auto ok = [](int d) { return d == 16 || d == 32 || d == 64; };
+  return ok(dL) && ok(dR);
+}
+
+// Runs the whole Richardson loop; x (dL x dR), hist on device; *iters, *hist_len, *status host.
+int richardson_persistent(cudaStream_t st, const ks_sketch_view* sk, const double* VL, const double* VR,
+                          const double* dinv, const double* rhs, double lam, double damping, int max_iters,
+                          double residual_tol, double* x, double* hist, int* iters, int* hist_len, int* status) {
+  const int dL = sk->dL, dR = sk->dR;
+  KS_REQUIRE(max_iters <= 1024, KS_ESIZE, "persistent loop keeps <= 1024 history entries");
+  const int dLp = dL + PAD, dRp = dR + PAD;
+  const int64_t nnz = sk->nnz, ul = sk->u_left;
+  // chunk table from the segment offsets (host; one small copy per sketch)
+  std::vector<int64_t> seg(ul + 1);
+  KS_TRY_CUDA(cudaMemcpyAsync(seg.data(), sk->seg, (ul + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  KS_TRY_CUDA(cudaStreamSynchronize(st));
+  std::vector<Chunk> chunks;
+  {
+    int64_t u = 0, t = 0;
+    while (t < nnz) {
+      Chunk c;
+      c.u_b = u;
+      c.t_b = t;
+      int64_t te = t, ue = u;
+      while (ue < ul && ue - u < CH_ROWS) {
+        const int64_t row_end = seg[ue + 1];
+        if (row_end - t <= CH_S) {
+          te = row_end;
+          ue++;
+        } else {
+          if (ue == u) {  // a heavy row: split it
+            te = t + CH_S;
+            ue = u + 1;
+          }
+          break;
+        }
+      }
+      c.u_e = ue;
+      c.t_e = te;
+      chunks.push_back(c);
+      t = te;
+      u = (te >= seg[ue]) ? ue : ue - 1;
+      while (u < ul && seg[u + 1] <= t) u++;
+    }
+  }
+  const int64_t nch = (int64_t)chunks.size();
+  const int grid = num_sms();
+  Scratch<double> Lpack(ul * dLp + 2, st), Rpack(nnz * dRp + 2, st), part((int64_t)grid * dL * dR, st);
+  Scratch<double> R((int64_t)dL * dR, st), T((int64_t)dL * dR, st), stepb((int64_t)dL * dR, st), rowsq(dL, st);
+  Scratch<double> VRt((int64_t)dR * dR, st);
+  Scratch<Chunk> dch(nch + 1, st);
+  Scratch<int> state(4, st);
+  KS_REQUIRE(Lpack.p && Rpack.p && part.p && R.p && T.p && stepb.p && rowsq.p && VRt.p && dch.p && state.p,
+             KS_ECUDA, "scratch allocation failed");
+  KS_TRY_CUDA(cudaMemcpyAsync(dch.p, chunks.data(), nch * sizeof(Chunk), cudaMemcpyHostToDevice, st));
+  pack_rows_kernel<<<ceil_div_u(ul * dLp, 256), 256, 0, st>>>(sk->Lmat, sk->ldl, sk->lrow, ul, dL, dLp, nullptr,
+                                                               Lpack.p);
+  KS_CHECK_LAUNCH();
+  pack_rows_kernel<<<ceil_div_u(nnz * dRp, 256), 256, 0, st>>>(sk->Rmat, sk->ldr, sk->rrow, nnz, dR, dRp, sk->v,
+                                                                Rpack.p);
+  KS_CHECK_LAUNCH();
+  transpose_sq_kernel2<<<ceil_div_u((int64_t)dR * dR, 256), 256, 0, st>>>(VR, dR, VRt.p);
+  KS_CHECK_LAUNCH();
+  PArgs a{};
+  a.Lpack = Lpack.p; a.Rpack = Rpack.p; a.v = sk->v; a.seg = sk->seg; a.chunks = dch.p; a.nchunks = nch;
+  a.VL = VL; a.VR = VR; a.VRt = VRt.p; a.dinv = dinv; a.rhs = rhs;
+  a.lam = lam; a.damping = damping; a.residual_tol = residual_tol; a.max_iters = max_iters;
+  a.part = part.p; a.R = R.p; a.T = T.p; a.step = stepb.p; a.rowsq = rowsq.p; a.x_out = x; a.hist = hist;
+  a.state = state.p;
+  int rc;
+  if (dL == 16 && dR == 16) rc = launch<16, 16>(st, a, grid);
+  else if (dL == 16 && dR == 32) rc = launch<16, 32>(st, a, grid);
+  else if (dL == 16 && dR == 64) rc = launch<16, 64>(st, a, grid);
+  else if (dL == 32 && dR == 16) rc = launch<32, 16>(st, a, grid);
+  else if (dL == 32 && dR == 32) rc = launch<32, 32>(st, a, grid);
+  else if (dL == 32 && dR == 64) rc = launch<32, 64>(st, a, grid);
+  else if (dL == 64 && dR == 16) rc = launch<64, 16>(st, a, grid);
+  else if (dL == 64 && dR == 32) rc = launch<64, 32>(st, a, grid);
+  else if (dL == 64 && dR == 64) rc = launch<64, 64>(st, a, grid);
+  else rc = KS_EINVAL;
+  if (rc) return rc;
+  int hs[4] = {0, 0, 0, 0};
+  KS_TRY_CUDA(cudaMemcpyAsync(hs, state.p, 3 * sizeof(int), cudaMemcpyDeviceToHost, st));
+  KS_TRY_CUDA(cudaStreamSynchronize(st));
+  *status = hs[0];
+  *iters = hs[1];
+  *hist_len = hs[2];
+  return KS_OK;
+}
+
+}  // namespace ks
+
+// Average cycles of CTA 0 per phase over the last persistent run:
+// out[0] = apply (P1), out[1] = grid sync after P1, out[2] = reduce (P2 + sync),
+// out[3] = precond A (P3 + sync), out[4] = precond B (P4 + sync), out[5] = update + loop.
+extern "C" int ks_debug_richardson_phases(int32_t iters, double* out6) {
+  if (iters < 2 || iters > 1024) return KS_EINVAL;
+  std::vector<long long> h(6 * iters);
+  KS_TRY_CUDA(cudaMemcpyFromSymbol(h.data(), g_prof, sizeof(long long) * 6 * iters));
+  for (int k = 0; k < 6; k++) out6[k] = 0.0;
+  for (int it = 0; it + 1 < iters; it++) {
+    const long long* p = &h[it * 6];
+    out6[0] += p[1] - p[0];
+    out6[1] += p[2] - p[1];
+    out6[2] += p[3] - p[2];
+    out6[3] += p[4] - p[3];
+    out6[4] += p[5] - p[4];
+    out6[5] += h[(it + 1) * 6] - p[5];
+  }
+  for (int k = 0; k < 6; k++) out6[k] /= (iters - 1);
+  return KS_OK;
+}

@@ -289,9 +289,14 @@ __global__ void reduce_cols_kernel(const double* __restrict__ part, int64_t npar
                                    double* __restrict__ out) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= count) return;
-  double s = 0.0;
-  for (int64_t p = 0; p < nparts; p++) s += part[p * count + e];
-  out[e] = s;
+  double s = 0.0, c = 0.0;
+  for (int64_t p = 0; p < nparts; p++) {
+    const double v = part[p * count + e];
+    const double t = s + v;
+    c += (fabs(s) >= fabs(v)) ? ((s - t) + v) : ((v - t) + s);
+    s = t;
+  }
+  out[e] = s + c;
 }
 
 }  // namespace

@@ -105,6 +105,11 @@ template <bool VSMEM>
 __global__ void jacobi_svd_kernel(const double* __restrict__ M, int d, double* __restrict__ sigma,
                                   double* __restrict__ Vout, double* __restrict__ vwork) {
   extern __shared__ double dyn[];
+  // batched: problem blockIdx.x of a contiguous batch
+  M += (size_t)blockIdx.x * d * d;
+  sigma += (size_t)blockIdx.x * d;
+  Vout += (size_t)blockIdx.x * d * d;
+  if (vwork) vwork += (size_t)blockIdx.x * (d + 1) * (d + 1);
   __shared__ int s_rot;
   __shared__ int s_order[130];
   __shared__ double s_norm[130];
@@ -122,12 +127,14 @@ __global__ void jacobi_svd_kernel(const double* __restrict__ M, int d, double* _
   }
   __syncthreads();
   const int npairs = dp / 2;
+  // dot products carry ~d*eps relative rounding: a tighter threshold never converges
+  const double tol = 2.0 * d * 2.220446049250313e-16;
   int g = 1;
   while (g * 2 * npairs <= nt && g < 32) g *= 2;
   const int group = tid / g, lg = tid % g;
   const bool active = group < npairs;
   const unsigned gmask = (g == 32) ? 0xffffffffu : (((1u << g) - 1u) << ((tid & 31) & ~(g - 1)));
-  for (int sweep = 0; sweep < 60; sweep++) {
+  for (int sweep = 0; sweep < 40; sweep++) {
     if (tid == 0) s_rot = 0;
     __syncthreads();
     for (int r = 0; r < dp - 1; r++) {
@@ -149,7 +156,8 @@ __global__ void jacobi_svd_kernel(const double* __restrict__ M, int d, double* _
           b += __shfl_xor_sync(gmask, b, o, g);
           c += __shfl_xor_sync(gmask, c, o, g);
         }
-        if (c != 0.0 && a != 0.0 && b != 0.0 && fabs(c) > 1e-15 * sqrt(a) * sqrt(b)) {
+        // rotate unless the pair is orthogonal to working precision (dgesvj-style threshold)
+        if (c != 0.0 && a != 0.0 && b != 0.0 && fabs(c) > tol * sqrt(a) * sqrt(b)) {
           const double zeta = (b - a) / (2.0 * c);
           const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
           const double cs = 1.0 / sqrt(1.0 + t * t);
@@ -338,8 +346,9 @@ int qr_r(cudaStream_t st, const double* A, int64_t n, int d, double* R) {
   return KS_OK;
 }
 
-int svd_small(cudaStream_t st, const double* M, int d, double* sigma, double* V) {
+int svd_small(cudaStream_t st, const double* M, int d, double* sigma, double* V, int batch) {
   KS_REQUIRE(d >= 1 && d <= 128, KS_ESIZE, "svd_small supports 1 <= d <= 128 (got %d)", d);
+  if (batch <= 0) return KS_OK;
   const int dp = d + (d & 1);
   const size_t wbytes = (size_t)dp * d * sizeof(double);
   const size_t vbytes = (size_t)dp * dp * sizeof(double);
@@ -347,13 +356,13 @@ int svd_small(cudaStream_t st, const double* M, int d, double* sigma, double* V)
   if (wbytes + vbytes <= QR_SMEM_CAP) {
     KS_TRY_CUDA(cudaFuncSetAttribute(jacobi_svd_kernel<true>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)QR_SMEM_CAP));
-    jacobi_svd_kernel<true><<<1, threads, wbytes + vbytes, st>>>(M, d, sigma, V, nullptr);
+    jacobi_svd_kernel<true><<<batch, threads, wbytes + vbytes, st>>>(M, d, sigma, V, nullptr);
   } else {
-    Scratch<double> vw((int64_t)dp * dp, st);
+    Scratch<double> vw((int64_t)batch * (d + 1) * (d + 1), st);
     KS_REQUIRE(vw.p, KS_ECUDA, "scratch allocation failed");
     KS_TRY_CUDA(cudaFuncSetAttribute(jacobi_svd_kernel<false>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)QR_SMEM_CAP));
-    jacobi_svd_kernel<false><<<1, threads, wbytes, st>>>(M, d, sigma, V, vw.p);
+    jacobi_svd_kernel<false><<<batch, threads, wbytes, st>>>(M, d, sigma, V, vw.p);
   }
   KS_CHECK_LAUNCH();
   return KS_OK;
@@ -366,7 +375,7 @@ static int thin_svd_tall(cudaStream_t st, const double* A, int64_t n, int d, dou
   KS_REQUIRE(R.p, KS_ECUDA, "scratch allocation failed");
   int rc = qr_r(st, A, n, d, R.p);
   if (rc) return rc;
-  rc = svd_small(st, R.p, d, sigma, V);
+  rc = svd_small(st, R.p, d, sigma, V, 1);
   if (rc) return rc;
   rc = gemm(st, n, d, d, 1.0, A, d, 1, 0, V, d, 1, 0, 0.0, U, d, 1, 0, 1);
   if (rc) return rc;
@@ -382,7 +391,12 @@ extern "C" int ks_qr_r(const double* A, int64_t n, int32_t d, double* R, void* s
 }
 
 extern "C" int ks_svd_small(const double* M, int32_t d, double* sigma, double* V, void* stream) {
-  return ks::svd_small((cudaStream_t)stream, M, d, sigma, V);
+  return ks::svd_small((cudaStream_t)stream, M, d, sigma, V, 1);
+}
+
+extern "C" int ks_svd_small_batched(const double* M, int32_t batch, int32_t d, double* sigma, double* V,
+                                    void* stream) {
+  return ks::svd_small((cudaStream_t)stream, M, d, sigma, V, batch);
 }
 
 // U: n x min(n,d)... to keep the ABI simple the caller provides U (n x k), sigma (k), V (d x k)

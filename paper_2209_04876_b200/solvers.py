@@ -360,6 +360,17 @@ def _regression_sample_count(cols: int, config: RegressionConfig) -> int:
                             * math.log(40 * cols) * math.log(1.0 / config.delta) / config.eps))
 
 
+def _inverse_from_eig(v: torch.Tensor, w: torch.Tensor) -> torch.Tensor:
+    d = int(w.numel())
+    if float(w.min().item()) <= 0.0:
+        raise NumericalFailureError("approximate Gram matrix is singular; cannot estimate leverage scores",
+                                    diagnostics={"shape": (d, d)})
+    vs = (v / w[None, :]).contiguous()
+    out = D.empty(d, d)
+    _lib.call("ks_gemm", d, d, d, 1.0, D.p(vs), d, 1, 0, D.p(v), 1, d, 0, 0.0, D.p(out), d, 1, 0, 1, D.stream())
+    return out
+
+
 class FastSolveTrace:
     """Device intermediates of one fast solve (parity tests compare them with the oracle)."""
 
@@ -404,7 +415,10 @@ def _fast_solve_dev(facs, b, config: RegressionConfig, caches, trace: FastSolveT
             gt = _gram_dev(a_tilde)
             v, w, _ = _factor_gram_dev(gt)
             grams.append((v, w))
-            gi = _inverse_small(gt)
+            # gram_tilde^-1 = V diag(1/w) V^T from the eigendecomposition the preconditioner needs
+            # anyway (the reference solves with LU, leverage.py:114-119; an exactly zero
+            # eigenvalue <=> an exactly singular Gram raises the same NumericalFailureError)
+            gi = _inverse_from_eig(v, w)
             scores.append(_jl_scores_dev(a, a_tilde, gi, eps_jl, seeds[2 * n + 1], config.jl_log_factor))
             afs.append(1.0 + eps_jl / 2.0)
     sampler = ProductSampler([LeverageScores(sc, 0.0, af) for sc, af in zip(scores, afs)])
@@ -452,6 +466,9 @@ def _fast_solve_dev(facs, b, config: RegressionConfig, caches, trace: FastSolveT
                                     diagnostics={"residual_history": history})
     _lib.check(rc, "ks_richardson_sketched")
     if trace is not None:
+        trace.loop_inputs = dict(view=view, VL=VL, VR=VR, dinv=dg, rhs=rhs, lam=float(lam),
+                                 damping=float(config.effective_damping), max_iters=int(max_iters),
+                                 tol=float(config.residual_tol))
         trace.scores = scores
         trace.eig = [w for _, w in grams]
         trace.sampler = sampler

@@ -178,6 +178,7 @@ def test_fused_richardson_divergence_rule(golden):
         K.fast_kronecker_regression(facs, b, cfg(damping=-1.0, max_richardson_iters=60))
     hist = err.value.diagnostics["residual_history"]
     assert len(hist) >= 6 and hist[-1] > 10 * hist[-6]
-    with pytest.raises(NumericalFailureError):
+    with pytest.raises(O.OracleError) as oerr:
         O.fast_kronecker_regression(facs, b, eps=0.1, delta=0.01, lam=1e-3, alpha=1e-5, seed=0, damping=-1.0,
                                     max_iters=60)
+    assert oerr.value.kind == "numerical" and oerr.value.iterations == err.value.iterations
