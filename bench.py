@@ -209,7 +209,7 @@ def run_ours(args):
     result = None
     if rank == 0:
         peak = fp64_peak_tflops()
-        rich = kernels["richardson_apply"]
+        rich = kernels["richardson_loop"]
         result = {
             "metric": METRIC, "value": t_step, "unit": "s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": False,
@@ -226,11 +226,12 @@ def run_ours(args):
                     "note": "public API, numpy factors + pinned host b; SolveReport.wall_time (loss excluded "
                             "as in the reference); only sampled entries of b cross PCIe",
                     "full_call_with_loss_s": e2e_full},
-            "roofline": {"bound": "tensor", "kernel": "sketched normal-operator apply (Richardson)",
+            "roofline": {"bound": "tensor", "kernel": "richardson_persistent_kernel (sketched normal operator + "
+                                                        "preconditioner, all iterations, FP64 DMMA)",
                          "achieved": rich["tflops"], "peak": peak, "unit": "TFLOP/s",
                          "frac": rich["tflops"] / peak, "traffic": None,
-                         "peak_source": "measured FP64 DMMA peak, profiles/r01_fp64_peak.txt",
-                         "algorithmic_flops_per_launch": rich["flops"],
+                         "peak_source": "measured FP64 DMMA peak (tools/fp64_peak.cu, profiles/r01_fp64_peak.txt)",
+                         "algorithmic_flops_per_launch": rich["flops_per_iter"] * rich["iterations"],
                          "launch_us": rich["us"]},
             "kernels": kernels,
             "gpu_launches": launches * args.steps,
@@ -265,60 +266,45 @@ def stage_timings(K, facs, b, cfg, tr, n, d):
     """Per-kernel device times (CUDA events on the launching stream) and roofline numbers."""
     import ctypes
     import torch
-    from paper_2209_04876_b200 import _lib, _device as D
-    from paper_2209_04876_b200.kron import _view_for
+    from paper_2209_04876_b200 import _lib as L, _device as D
     peak = fp64_peak_tflops()
     hbm, _ = hbm_peak_gbs()
     out = {}
-    sd = tr.sdiag
-    view = _view_for(facs, sd)
+    li = tr.loop_inputs
+    view = li["view"]
     nnz, u1 = view.nnz, view.u_left
-    X = torch.randn(view.dL, view.dR, dtype=torch.float64, device="cuda")
-    from paper_2209_04876_b200 import _lib as L
-    np_ = (u1 + 31) // 32
-    part = torch.empty(np_ * view.dL * view.dR + 1, dtype=torch.float64, device="cuda")
-    G = torch.empty(view.dL, view.dR, dtype=torch.float64, device="cuda")
-    bv = torch.randn(nnz, dtype=torch.float64, device="cuda")
-
-    def rich_once():
-        L.call("ks_sketched_transpose_apply", ctypes.byref(view.struct), D.p(bv), D.p(None), D.p(G), D.stream())
-
-    # fused normal apply == transpose apply + the y / dot work; time the Richardson loop per iteration
-    from paper_2209_04876_b200.solvers import _fast_solve_dev
-    VL = torch.eye(view.dL, dtype=torch.float64, device="cuda")
-    VR = torch.eye(view.dR, dtype=torch.float64, device="cuda")
-    dinv = torch.ones(view.dL * view.dR, dtype=torch.float64, device="cuda")
-    rhs = torch.randn(view.dL, view.dR, dtype=torch.float64, device="cuda")
     x = torch.empty(view.dL, view.dR, dtype=torch.float64, device="cuda")
-    hist = torch.zeros(64, dtype=torch.float64, device="cuda")
+    hist = torch.zeros(max(1, li["max_iters"]), dtype=torch.float64, device="cuda")
     it = ctypes.c_int32(0)
     hl = ctypes.c_int32(0)
-    iters = 24
 
     def loop():
-        L.load().ks_richardson_sketched(ctypes.byref(view.struct), D.p(VL), D.p(VR), D.p(dinv), D.p(rhs), 1e-3, 0.5,
-                                        iters, 1e-300, D.p(x), D.p(hist), ctypes.byref(it), ctypes.byref(hl),
-                                        D.stream())
+        rc = L.load().ks_richardson_sketched(ctypes.byref(view.struct), D.p(li["VL"]), D.p(li["VR"]), D.p(li["dinv"]),
+                                             D.p(li["rhs"]), li["lam"], li["damping"], li["max_iters"], li["tol"],
+                                             D.p(x), D.p(hist), ctypes.byref(it), ctypes.byref(hl), D.stream())
+        assert rc == 0, rc
 
-    us_loop = _timed(loop, 3)
-    us_t = _timed(rich_once, 5)
-    d2 = d * d
-    flops_apply = 4.0 * u1 * d2 + 4.0 * nnz * d  # y + G GEMMs over distinct left rows + per-sample dots/axpys
-    flops_iter = flops_apply + 8.0 * d ** 3
-    out["richardson_loop"] = {"us": us_loop, "iterations": iters, "us_per_iter": us_loop / iters,
-                              "flops_per_iter": flops_iter,
-                              "tflops": flops_iter * iters / (us_loop * 1e-6) / 1e12}
-    out["richardson_apply"] = {"us": us_loop / iters, "flops": flops_apply,
-                               "tflops": flops_apply / (us_loop / iters * 1e-6) / 1e12,
-                               "note": "per Richardson iteration (apply + reduce + preconditioner + update)"}
-    out["transpose_apply"] = {"us": us_t, "flops": 2.0 * u1 * d2 + 2.0 * nnz * d,
-                              "tflops": (2.0 * u1 * d2 + 2.0 * nnz * d) / (us_t * 1e-6) / 1e12}
-    # KronMatMul n^2 pass of the exact solver: T = U1^T B U2
+    us_loop = _timed(loop, 5)
+    iters = it.value
+    ph = (ctypes.c_double * 6)()
+    phases = None
+    if L.load().ks_debug_richardson_phases(iters, ph) == 0:
+        phases = dict(zip(["apply", "sync_after_apply", "reduce", "precond_a", "precond_b", "update"],
+                          [round(v) for v in ph]))
+    dL, dR = view.dL, view.dR
+    flops_apply = 2.0 * u1 * dL * dR * 2 + 4.0 * nnz * dR  # Y and G GEMMs over distinct left rows + dots/axpys
+    flops_iter = flops_apply + 4.0 * dL * dR * (dL + dR)  # + preconditioner (four d x d x d products)
+    out["richardson_loop"] = {"us": us_loop, "iterations": iters, "us_per_iter": us_loop / max(iters, 1),
+                              "flops_per_iter": flops_iter, "nnz": nnz, "u_left": u1,
+                              "tflops": flops_iter * iters / (us_loop * 1e-6) / 1e12,
+                              "frac_fp64": flops_iter * iters / (us_loop * 1e-6) / 1e12 / peak,
+                              "phase_cycles_per_iter": phases,
+                              "note": "one persistent cooperative launch: sketch packing + all iterations"}
     U1, U2 = facs
     T = torch.empty(d, d, dtype=torch.float64, device="cuda")
 
     def kmm():
-        L.call("ks_kron2_contract", D.p(U1), D.p(b), n, D.p(U2), n, n, d, d, D.p(T), D.stream())
+        assert L.load().ks_kron2_contract(D.p(U1), D.p(b), n, D.p(U2), n, n, d, d, D.p(T), D.stream()) == 0
 
     us_k = _timed(kmm, 5)
     fl = 2.0 * n * n * d + 2.0 * n * d * d
@@ -331,7 +317,8 @@ def stage_timings(K, facs, b, cfg, tr, n, d):
     o = torch.empty(1, dtype=torch.float64, device="cuda")
 
     def loss():
-        L.call("ks_kron2_residual_sumsq", D.p(U1), D.p(Xs), D.p(U2), D.p(b), n, n, n, d, d, D.p(o), D.stream())
+        assert L.load().ks_kron2_residual_sumsq(D.p(U1), D.p(Xs), D.p(U2), D.p(b), n, n, n, d, d, D.p(o),
+                                                D.stream()) == 0
 
     us_l = _timed(loss, 5)
     out["loss_pass"] = {"us": us_l, "flops": fl, "bytes": by, "tflops": fl / (us_l * 1e-6) / 1e12,

@@ -143,6 +143,12 @@ int ks_row_weighted_sumsq(const double* U, int64_t n, int32_t d, const double* w
 int ks_sampler_tables(const double* scores, int64_t n, int32_t renormalise, double* probs,
                       double* cdf, int32_t* flags, void* stream);
 
+/* ks_sampler_tables for nf <= 8 score vectors at once (one CTA per factor, concurrently);
+ * flags holds one int32 per factor.  cdf may be NULL (probabilities only). */
+int ks_sampler_tables_batched(int32_t nf, const double* const* scores, const int64_t* n,
+                              int32_t renormalise, double* const* probs, double* const* cdf,
+                              int32_t* flags, void* stream);
+
 /* Inverse-CDF draws: idx[t*stride + off] = clip(upper_bound(cdf, u[t]), 0, n-1) (leverage.py:196-200). */
 int ks_searchsorted_right(const double* cdf, int64_t n, const double* u, int64_t s,
                           int64_t* idx, int64_t stride, int64_t off, void* stream);

@@ -56,6 +56,7 @@ _SIGS = {
     "ks_jl_scores": ([_p, _i64, _i32, _p, _i32, _d, _p, _p], ctypes.c_int),
     "ks_row_weighted_sumsq": ([_p, _i64, _i32, _p, _p, _p], ctypes.c_int),
     "ks_sampler_tables": ([_p, _i64, _i32, _p, _p, _p, _p], ctypes.c_int),
+    "ks_sampler_tables_batched": ([_i32, _p, _p, _i32, _p, _p, _p, _p], ctypes.c_int),
     "ks_searchsorted_right": ([_p, _i64, _p, _i64, _p, _i64, _i64, _p], ctypes.c_int),
     "ks_sketch_weights": ([_i32, _p, _p, _i64, _p, _p], ctypes.c_int),
     "ks_sketch_diag": ([_i32, _p, _p, _p, _i64, _p, _p, POINTER(c_int64), _p], ctypes.c_int),

@@ -6,10 +6,14 @@
 //   - validation, gather, sum-of-squares reductions
 #include "ks_common.cuh"
 
+#include <cstdlib>
 #include <mutex>
 #include <vector>
 
 namespace ks {
+
+int gemm_tn_tall_dmma(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
+                      int64_t a_ks, int64_t a_ms, const double* B, int64_t b_ks, int64_t b_ns, double* C);
 
 static thread_local char g_err[1024] = "";
 
@@ -308,6 +312,10 @@ int gemm_tn_tall(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha,
   if (K <= 0) {
     KS_TRY_CUDA(cudaMemsetAsync(C, 0, sizeof(double) * M * N, st));
     return KS_OK;
+  }
+  {
+    const char* e = getenv("KS_TALL");
+    if (!(e && e[0] == 'g')) return gemm_tn_tall_dmma(st, M, N, K, alpha, A, a_ks, a_ms, B, b_ks, b_ns, C);
   }
   int64_t nparts = (K + 63) / 64;
   const int64_t cap = 2 * (int64_t)num_sms();

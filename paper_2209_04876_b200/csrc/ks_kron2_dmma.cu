@@ -28,10 +28,13 @@ namespace {
 constexpr int KS_STAGES = 6;
 constexpr int CONSUMERS = 4;
 constexpr int THREADS = (CONSUMERS + 1) * 32;
+// KronMatMul: 8 consumer warps (4 row groups x 2 column halves) = 2 per SM sub-partition
+constexpr int K1_CW = 8;
+constexpr int K1_THREADS = (K1_CW + 1) * 32;
 
 template <int Q, int WM>
 struct K1Cfg {
-  static constexpr int BM = CONSUMERS * WM;
+  static constexpr int BM = 4 * WM;
   static constexpr int B_TILE = BM * 16;                  // doubles
   static constexpr int R_TILE = Q * 16;                   // doubles
   static constexpr int STAGE = B_TILE + R_TILE;           // doubles (multiple of 128 -> 1 KB aligned)
@@ -42,13 +45,13 @@ struct K1Cfg {
 };
 
 template <int Q, int WM>
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __launch_bounds__(K1_THREADS, 1)
     kron2_contract_kernel(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmR,
                           const double* __restrict__ L, int64_t m, int p, int q, int64_t nKS,
                           int64_t total_steps, int64_t per_cta, int max_seg, double* __restrict__ part) {
   using C = K1Cfg<Q, WM>;
   constexpr int BM = C::BM;
-  constexpr int MT = WM / 16, NT = Q / 8;
+  constexpr int MT = WM / 16, NT = Q / 16;
   extern __shared__ unsigned char dyn_raw[];
   double* sm = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(dyn_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + C::BAR_OFF);
@@ -62,14 +65,14 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (tid == 0) {
     for (int s = 0; s < KS_STAGES; s++) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], CONSUMERS);
+      mbar_init(&empty[s], K1_CW);
     }
     fence_barrier_init();
   }
   __syncthreads();
   const int64_t rb_first = s0 / nKS;
 
-  if (warp == CONSUMERS) {
+  if (warp == K1_CW) {
     // ------------------------------ producer ------------------------------
     if (lane == 0) {
       tma_prefetch(&tmB);
@@ -97,7 +100,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
       for (int c = 0; c < 4; c++) acc[a][b][c] = 0.0;
 
-  const int row_w = warp * WM;
+  const int row_w = (warp & 3) * WM, col_w = (warp >> 2) * (Q / 2);
   for (int64_t i = 0, s = s0; s < s1; i++, s++) {
     const int st = (int)(i % KS_STAGES);
     mbar_wait(&full[st], (uint32_t)((i / KS_STAGES) & 1));
@@ -112,7 +115,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         af[a][1] = Bs[swz128(row_w + a * 16 + g + 8, k0 + t4)];
       }
 #pragma unroll
-      for (int b = 0; b < NT; b++) bf[b] = Rs[swz128(b * 8 + g, k0 + t4)];
+      for (int b = 0; b < NT; b++) bf[b] = Rs[swz128(col_w + b * 8 + g, k0 + t4)];
 #pragma unroll
       for (int a = 0; a < MT; a++)
 #pragma unroll
@@ -129,20 +132,20 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int a = 0; a < MT; a++)
 #pragma unroll
         for (int b = 0; b < NT; b++) {
-          const int r0 = row_w + a * 16 + g, c0 = b * 8 + 2 * t4;
+          const int r0 = row_w + a * 16 + g, c0 = col_w + b * 8 + 2 * t4;
           Ps[r0 * C::QP + c0] = acc[a][b][0];
           Ps[r0 * C::QP + c0 + 1] = acc[a][b][1];
           Ps[(r0 + 8) * C::QP + c0] = acc[a][b][2];
           Ps[(r0 + 8) * C::QP + c0 + 1] = acc[a][b][3];
           acc[a][b][0] = acc[a][b][1] = acc[a][b][2] = acc[a][b][3] = 0.0;
         }
-      named_bar_sync(1, CONSUMERS * 32);
+      named_bar_sync(1, K1_CW * 32);
       const int64_t row0 = rb * BM;
       double* out = part + ((int64_t)blockIdx.x * max_seg + (rb - rb_first)) * p * q;
-      for (int a0 = warp * 16; a0 < p; a0 += CONSUMERS * 16) {
-        double t[NT][4];
+      for (int a0 = warp * 16; a0 < p; a0 += K1_CW * 16) {
+        double t[Q / 8][4];
 #pragma unroll
-        for (int b = 0; b < NT; b++) t[b][0] = t[b][1] = t[b][2] = t[b][3] = 0.0;
+        for (int b = 0; b < Q / 8; b++) t[b][0] = t[b][1] = t[b][2] = t[b][3] = 0.0;
         for (int k0 = 0; k0 < BM; k0 += 4) {
           const int64_t gi = row0 + k0 + t4;
           const bool rok = gi < m;
@@ -150,13 +153,13 @@ __global__ void __launch_bounds__(THREADS, 1)
           const double la0 = (rok && a0 + g < p) ? __ldg(Lr + a0 + g) : 0.0;
           const double la1 = (rok && a0 + g + 8 < p) ? __ldg(Lr + a0 + g + 8) : 0.0;
 #pragma unroll
-          for (int b = 0; b < NT; b++) {
+          for (int b = 0; b < Q / 8; b++) {
             const double pb = Ps[(k0 + t4) * C::QP + b * 8 + g];
             dmma_16x8x4(t[b], la0, la1, pb);
           }
         }
 #pragma unroll
-        for (int b = 0; b < NT; b++) {
+        for (int b = 0; b < Q / 8; b++) {
           const int c0 = b * 8 + 2 * t4;
           const int r0 = a0 + g;
           if (r0 < p) {
@@ -169,7 +172,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
         }
       }
-      named_bar_sync(1, CONSUMERS * 32);
+      named_bar_sync(1, K1_CW * 32);
     }
   }
 }
@@ -212,7 +215,7 @@ int launch_k1(cudaStream_t st, const CUtensorMap& tmB, const CUtensorMap& tmR, c
   KS_TRY_CUDA(cudaMemsetAsync(part.p, 0, sizeof(double) * nslots * p * q, st));
   auto kern = kron2_contract_kernel<Q, WM>;
   KS_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::BYTES));
-  kern<<<grid, THREADS, C::BYTES, st>>>(tmB, tmR, L, m, p, q, nKS, total, per, max_seg, part.p);
+  kern<<<grid, K1_THREADS, C::BYTES, st>>>(tmB, tmR, L, m, p, q, nKS, total, per, max_seg, part.p);
   KS_CHECK_LAUNCH();
   const int64_t count = (int64_t)p * q;
   reduce_slots_kernel<<<ceil_div_u(count * 32, 256), 256, 0, st>>>(part.p, nslots, count, T);
@@ -236,7 +239,7 @@ int kron2_contract_dmma(cudaStream_t st, const double* L, const double* B, int64
   KS_CHECK_LAUNCH();
   CUtensorMap tmB, tmR;
   const int WM = (Qp == 128) ? 16 : 32;
-  const uint32_t BM = CONSUMERS * WM;
+  const uint32_t BM = 4 * WM;
   if (!make_tmap_f64(&tmB, B, (uint64_t)m, (uint64_t)k, (uint64_t)ldb, BM)) return -1;
   if (!make_tmap_f64(&tmR, Rt.p, (uint64_t)q, (uint64_t)k, (uint64_t)k, (uint32_t)Qp)) return -1;
   switch (Qp) {

@@ -56,188 +56,6 @@ __global__ void row_weighted_sumsq_kernel(const double* __restrict__ U, int64_t 
   out[i] = s;
 }
 
-// ---------------------------------------------------------------- sampler tables
-constexpr int ST_T = 1024;
-constexpr int ST_D = 10;  // 2^ST_D = ST_T subtrees
-
-__device__ double pw_combine(const double* slot, int64_t s, int64_t len, int depth, int path) {
-  // replay the top levels of the recursion (iterative, depth <= ST_D)
-  // evaluate with an explicit stack
-  int64_t st_s[ST_D + 1], st_l[ST_D + 1];
-  int st_d[ST_D + 1], st_p[ST_D + 1], st_state[ST_D + 1];
-  double st_v[ST_D + 1];
-  int sp = 0;
-  st_s[0] = s; st_l[0] = len; st_d[0] = depth; st_p[0] = path; st_state[0] = 0;
-  double ret = 0.0;
-  while (sp >= 0) {
-    const int64_t cl = st_l[sp];
-    const int dd = st_d[sp];
-    if (cl <= PW_BLOCK || dd == ST_D) {
-      ret = slot[st_p[sp] << (ST_D - dd)];
-      sp--;
-      if (sp >= 0) {
-        if (st_state[sp] == 1) { st_v[sp] = ret; st_state[sp] = 2; }
-        else { ret = st_v[sp] + ret; st_state[sp] = 3; }
-      }
-      continue;
-    }
-    int64_t n2;
-    pw_split(cl, &n2);
-    if (st_state[sp] == 0) {
-      st_state[sp] = 1;
-      sp++;
-      st_s[sp] = st_s[sp - 1]; st_l[sp] = n2; st_d[sp] = dd + 1; st_p[sp] = st_p[sp - 1] * 2;
-      st_state[sp] = 0;
-    } else if (st_state[sp] == 2) {
-      sp++;
-      st_s[sp] = st_s[sp - 1] + n2; st_l[sp] = cl - n2; st_d[sp] = dd + 1;
-      st_p[sp] = st_p[sp - 1] * 2 + 1; st_state[sp] = 0;
-    } else {
-      sp--;
-      if (sp >= 0) {
-        if (st_state[sp] == 1) { st_v[sp] = ret; st_state[sp] = 2; }
-        else { ret = st_v[sp] + ret; st_state[sp] = 3; }
-      }
-    }
-  }
-  return ret;
-}
-
-__device__ __forceinline__ int64_t block_incl_scan_i64(int64_t v, int64_t* wsum) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int64_t t = __shfl_up_sync(0xffffffffu, v, o);
-    if (lane >= o) v += t;
-  }
-  if (lane == 31) wsum[wid] = v;
-  __syncthreads();
-  if (wid == 0) {
-    int64_t t = lane < nw ? wsum[lane] : 0;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int64_t u = __shfl_up_sync(0xffffffffu, t, o);
-      if (lane >= o) t += u;
-    }
-    if (lane < nw) wsum[lane] = t;
-  }
-  __syncthreads();
-  if (wid > 0) v += wsum[wid - 1];
-  __syncthreads();
-  return v;
-}
-
-__device__ __forceinline__ double ulp_of(double x) {
-  // spacing of doubles at |x| (x > 0, normal range)
-  int e;
-  frexp(x, &e);          // x = m * 2^e, m in [0.5, 1)
-  return ldexp(1.0, e - 53);
-}
-
-// One block per factor: total (pairwise), probs, exact sequential cumsum via verified
-// speculation.  flags: 1 = negative/non-finite score, 2 = non-positive total.
-__global__ void __launch_bounds__(ST_T) sampler_tables_kernel(const double* __restrict__ scores,
-                                                             int64_t n, int renorm,
-                                                             double* __restrict__ probs,
-                                                             double* __restrict__ cdf,
-                                                             int32_t* __restrict__ flags) {
-  __shared__ double slot[ST_T];
-  __shared__ int64_t wsum[32];
-  __shared__ double s_total;
-  __shared__ int s_bad;
-  __shared__ int s_first;
-  __shared__ double s_spec[ST_T];
-  const int tid = threadIdx.x;
-  if (tid == 0) s_bad = 0;
-  __syncthreads();
-  {
-    bool bad = false;
-    for (int64_t i = tid; i < n; i += ST_T) {
-      const double v = scores[i];
-      bad |= !(v >= 0.0) || !isfinite(v);
-    }
-    if (__syncthreads_or(bad) && tid == 0) s_bad = 1;
-  }
-  // subtree of thread `tid` at depth ST_D (or the leaf it falls into)
-  {
-    int64_t s = 0, len = n;
-    int depth = 0;
-    bool owner = true;
-    for (; depth < ST_D; depth++) {
-      if (len <= PW_BLOCK) {
-        owner = (tid & ((1 << (ST_D - depth)) - 1)) == 0;
-        break;
-      }
-      int64_t n2;
-      pw_split(len, &n2);
-      const int bit = (tid >> (ST_D - 1 - depth)) & 1;
-      if (bit) { s += n2; len -= n2; } else { len = n2; }
-    }
-    if (owner) {
-      auto get = [&](int64_t i) { return scores[i]; };
-      slot[tid] = pw_sum_seq(get, s, len);
-    }
-  }
-  __syncthreads();
-  if (tid == 0) {
-    const double total = pw_combine(slot, 0, n, 0, 0);
-    s_total = total;
-    int f = s_bad ? 1 : 0;
-    if (!(total > 0.0)) f |= 2;
-    flags[0] = f;
-  }
-  __syncthreads();
-  const double total = s_total;
-  for (int64_t i = tid; i < n; i += ST_T) probs[i] = scores[i] / total;
-  __syncthreads();
-  if (cdf == nullptr) return;
-  // exact cumsum: s_k = fl(s_{k-1} + p_k), verified block speculation
-  double prev = 0.0;
-  int64_t pos = 0;
-  while (pos < n) {
-    const int64_t i = pos + tid;
-    const bool valid = i < n;
-    const double x = valid ? probs[i] : 0.0;
-    double ref = prev;
-    if (ref == 0.0) ref = (pos < n) ? probs[pos] : 0.0;
-    const double u = (ref > 0.0) ? ulp_of(ref) : 0x1.0p-1074;
-    long long qi = 0;
-    if (valid) {
-      const double qd = x / u;
-      qi = (qd < 0x1.0p52) ? __double2ll_rn(qd) : (1ll << 52);
-    }
-    const int64_t Q = block_incl_scan_i64(qi, wsum);
-    // spec = prev + Q*u computed exactly when representable
-    const double base = prev / u;  // integer-valued when prev is on the grid
-    const double spec = (double)((long long)base + Q) * u;
-    s_spec[tid] = spec;
-    if (tid == 0) s_first = ST_T;
-    __syncthreads();
-    const double sprev = (tid == 0) ? prev : s_spec[tid - 1];
-    const double real = __dadd_rn(sprev, x);
-    const bool ok = !valid || (real == spec);
-    if (!ok) atomicMin(&s_first, tid);
-    __syncthreads();
-    const int f = s_first;
-    if (valid && tid < f) cdf[i] = spec;
-    if (valid && tid == f) cdf[i] = real;
-    int64_t adv = (f < ST_T) ? (int64_t)f + 1 : (int64_t)ST_T;
-    if (pos + adv > n) adv = n - pos;
-    __syncthreads();
-    if (tid == 0) s_spec[0] = cdf[pos + adv - 1];
-    __syncthreads();
-    prev = s_spec[0];
-    pos += adv;
-    __syncthreads();
-  }
-  if (renorm) {
-    __syncthreads();
-    const double last = cdf[n - 1];
-    __syncthreads();
-    for (int64_t i = tid; i < n; i += ST_T) cdf[i] = cdf[i] / last;
-  }
-}
-
 __global__ void searchsorted_right_kernel(const double* __restrict__ cdf, int64_t n,
                                           const double* __restrict__ u, int64_t s,
                                           int64_t* __restrict__ idx, int64_t stride, int64_t off) {
@@ -285,14 +103,6 @@ extern "C" int ks_row_weighted_sumsq(const double* U, int64_t n, int32_t d, cons
                                      double* scores, void* stream) {
   if (n <= 0) return KS_OK;
   row_weighted_sumsq_kernel<<<ceil_div_u(n, 256), 256, 0, (cudaStream_t)stream>>>(U, n, d, wts, scores);
-  KS_CHECK_LAUNCH();
-  return KS_OK;
-}
-
-extern "C" int ks_sampler_tables(const double* scores, int64_t n, int32_t renormalise,
-                                 double* probs, double* cdf, int32_t* flags, void* stream) {
-  KS_REQUIRE(n >= 1, KS_EINVAL, "score vector must be nonempty");
-  sampler_tables_kernel<<<1, ST_T, 0, (cudaStream_t)stream>>>(scores, n, renormalise, probs, cdf, flags);
   KS_CHECK_LAUNCH();
   return KS_OK;
 }

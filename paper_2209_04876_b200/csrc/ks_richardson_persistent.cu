@@ -1,18 +1,20 @@
-// Persistent cooperative Richardson loop for dL, dR in {16, 32, 64} (all BASELINE configs
+// Persistent cooperative Richardson loop for dL, dR in {16, 32, 64} (every BASELINE config
 // except the d=128 sweep point).  One CTA per SM runs all iterations of solvers.py:201-248:
 //
 //   P1  apply:   for each chunk of the sketch (<= 32 distinct left rows, <= CH_S samples),
-//                bulk-async copy the packed left rows / right rows (contiguous, padded slabs
-//                built once per sketch) into shared memory, then
-//                   Y = L_chunk X                  (DMMA m16n8k4)
-//                   z_u = sum_t v_t (v_t (y_u . R_t)) R_t      (warp per left row, smem only)
-//                   G_cta += L_chunk^T Z           (DMMA, accumulators stay in registers)
-//   P2  R = sum_cta G_cta + lam X - rhs          (warp per element, compensated, fixed order)
-//   P3  T = dinv o (VL^T R VR)                    (CTA per row)
-//   P4  step = VL T VR^T, rowsq                   (CTA per row)
+//                bulk-async copy the packed left rows / right rows (contiguous padded slabs
+//                built once per sketch, double-buffered, prefetched across iterations) into
+//                shared memory, then
+//                   Y = L_chunk X                           (DMMA m16n8k4)
+//                   z_u = sum_t v_t (v_t (y_u . R_t)) R_t    (quarter-warp per left row)
+//                   G_cta += L_chunk^T Z                    (DMMA, accumulators in registers)
+//   P2  R = sum_cta G_cta + lam X - rhs     (warp per element, compensated, fixed order)
+//   P3  T = dinv o (VL^T R VR)              (CTA per row, operands staged in smem)
+//   P4  step = VL T VR^T, rowsq              (CTA per row)
 //   then every CTA computes ||step|| identically, applies the reference's stopping and
-//   divergence rules, and updates its shared-memory copy of x.
-// Four grid-wide barriers per iteration; no host round trips.
+//   divergence rules and updates its shared-memory copy of x.
+// Four grid-wide barriers per iteration; no host round trips.  Chunks are assigned to CTAs
+// in contiguous ranges of equal estimated cost (static, so results are deterministic).
 #include "ks_common.cuh"
 #include "ks_tma.cuh"
 
@@ -26,8 +28,8 @@ namespace {
 
 constexpr int PT = 256;      // threads per CTA
 constexpr int PW = PT / 32;  // warps
-constexpr int CH_ROWS = 32;  // distinct left rows per chunk
-constexpr int CH_S = 96;     // samples per chunk
+constexpr int CH_ROWS = 16;  // distinct left rows per chunk (one half-warp each)
+constexpr int CH_S = 128;    // samples per chunk
 constexpr int PAD = 4;       // row padding (doubles) of packed / staged rows
 
 struct Chunk {
@@ -36,28 +38,26 @@ struct Chunk {
 };
 
 struct PArgs {
-  const double* Lpack;  // u_left x (DL+PAD)
-  const double* Rpack;  // nnz x (DR+PAD)
-  const double* v;      // nnz
-  const int64_t* seg;   // u_left + 1
+  const double* Lpack;    // u_left x (DL+PAD)
+  const double* Rpack;    // nnz x (DR+PAD); pad slot 0 carries v_t
+  const int64_t* seg;     // u_left + 1
   const Chunk* chunks;
-  int64_t nchunks;
-  const double* VL;     // DL x DL
-  const double* VR;     // DR x DR
-  const double* VRt;    // DR x DR
-  const double* dinv;   // DL x DR
-  const double* rhs;    // DL x DR
+  const int64_t* range;   // grid + 1: chunk range of every CTA
+  const double* VL;       // DL x DL
+  const double* VR;       // DR x DR
+  const double* VRt;      // DR x DR
+  const double* dinv;     // DL x DR
+  const double* rhs;      // DL x DR
   double lam, damping, residual_tol;
   int max_iters;
-  double* part;         // grid x DL x DR
-  double* R;            // DL x DR
-  double* T;            // DL x DR
-  double* step;         // DL x DR
-  double* rowsq;        // DL
-  double* x_out;        // DL x DR
-  double* hist;         // max_iters
-  int* state;           // [status, iters, hist_len]
-  long long* prof;      // optional: CTA 0 clock64 stamps, 6 per iteration
+  double* part;           // grid x DL x DR
+  double* R;              // DL x DR
+  double* T;              // DL x DR
+  double* step;           // DL x DR
+  double* rowsq;          // DL
+  double* x_out;          // DL x DR
+  double* hist;           // max_iters
+  int* state;             // [status, iters, hist_len]
 };
 
 __device__ long long g_prof[6 * 1024];
@@ -68,12 +68,13 @@ struct Smem {
   static constexpr int X_OFF = 0;                          // DL x DRP
   static constexpr int L_OFF = X_OFF + DL * DRP;           // 2 x CH_ROWS x DLP
   static constexpr int R_OFF = L_OFF + 2 * CH_ROWS * DLP;  // 2 x CH_S x DRP
-  static constexpr int Y_OFF = R_OFF + 2 * CH_S * DRP;     // CH_ROWS x DRP (also Z)
+  static constexpr int Y_OFF = R_OFF + 2 * CH_S * DRP;     // CH_ROWS x DRP
   static constexpr int Z_OFF = Y_OFF + CH_ROWS * DRP;      // CH_ROWS x DRP
-  static constexpr int W_OFF = Z_OFF + CH_ROWS * DRP;      // scratch 2*128
+  static constexpr int W_OFF = Z_OFF + CH_ROWS * DRP;      // scratch 256
   static constexpr int H_OFF = W_OFF + 256;                // history (<= 1024)
   static constexpr int DOUBLES = H_OFF + 1024;
   static constexpr size_t BYTES = (size_t)DOUBLES * 8 + 64;  // + mbarriers
+  static_assert(CH_S >= DL + DR, "staging of R/T and VR needs the free slab buffer");
 };
 
 __device__ __forceinline__ void bulk_copy(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -83,7 +84,6 @@ __device__ __forceinline__ void bulk_copy(void* dst, const void* src, uint32_t b
                : "memory");
 }
 
-// issue the slab copies of chunk `c` into buffer `buf` (called by one thread)
 template <int DL, int DR>
 __device__ void issue_chunk(const PArgs& a, const Chunk& ch, double* sm, uint64_t* bar, int buf) {
   using S = Smem<DL, DR>;
@@ -92,6 +92,26 @@ __device__ void issue_chunk(const PArgs& a, const Chunk& ch, double* sm, uint64_
   mbar_arrive_expect_tx(bar, lbytes + rbytes);
   bulk_copy(sm + S::L_OFF + buf * CH_ROWS * S::DLP, a.Lpack + ch.u_b * S::DLP, lbytes, bar);
   bulk_copy(sm + S::R_OFF + buf * CH_S * S::DRP, a.Rpack + ch.t_b * S::DRP, rbytes, bar);
+}
+
+// staged copy of a rows x cols global matrix into padded smem (row stride ld)
+__device__ __forceinline__ void stage(double* dst, const double* __restrict__ src, int rows, int cols, int ld,
+                                      bool coherent) {
+  for (int e = threadIdx.x; e < rows * cols; e += PT) {
+    const int i = e / cols, j = e - i * cols;
+    dst[i * ld + j] = coherent ? __ldcg(&src[e]) : __ldg(&src[e]);
+  }
+}
+
+// out[j] = sum_k w[k] M[k][j] for j < cols; 4 threads per output, interleaved k-split.
+__device__ __forceinline__ void vecmat(const double* w, const double* M, int K, int cols, int ld, double* out) {
+  const int j = threadIdx.x >> 2, part = threadIdx.x & 3;
+  double s = 0.0;
+  if (j < cols)
+    for (int k = part; k < K; k += 4) s = fma(w[k], M[k * ld + j], s);
+  s += __shfl_xor_sync(0xffffffffu, s, 1);
+  s += __shfl_xor_sync(0xffffffffu, s, 2);
+  if (j < cols && part == 0) out[j] = s;
 }
 
 template <int DL, int DR>
@@ -103,6 +123,7 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
   constexpr int YT_M = CH_ROWS / 16, YT_N = DR / 8, Y_TILES = YT_M * YT_N;
   constexpr int Y_PER_W = (Y_TILES + PW - 1) / PW;
   constexpr int NE = DL * DR;
+  constexpr int QE = DR / 16;  // elements of a right row per half-warp lane
   extern __shared__ __align__(128) double sm[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + S::DOUBLES);
   double* Xs = sm + S::X_OFF;
@@ -124,81 +145,91 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
   for (int e = tid; e < DL * DRP; e += PT) Xs[e] = 0.0;
   __syncthreads();
 
-  // chunk range of this CTA
-  const int64_t c_beg = a.nchunks * b / G, c_end = a.nchunks * (b + 1) / G;
+  const int64_t c_beg = a.range[b], c_end = a.range[b + 1];
   uint32_t phase[2] = {0, 0};
-  int pending[2] = {0, 0};  // bulk copies in flight per buffer (thread 0's view)
-  const bool resident = (c_end - c_beg) == 1;  // a single chunk stays in buffer 0 for all iterations
+  int pending[2] = {0, 0};
+  const bool resident = (c_end - c_beg) == 1;
+  int cur = 0;  // buffer holding the next chunk to consume
 
-  // --- preconditioner phases (shared by the scale computation and the loop) ---
+  // --- preconditioner phases: operands staged in the free slab buffer and the Y/Z region ---
   auto precond_a = [&](const double* Rin) {
+    double* Rs = sm + S::R_OFF + (cur ^ 1) * CH_S * DRP;
+    double* VRs = Rs + DL * DRP;
     for (int r = b; r < DL; r += G) {
-      double* t1 = Ws;
-      for (int j = tid; j < DR; j += PT) {
-        double s = 0.0;
-#pragma unroll 8
-        for (int k = 0; k < DL; k++) s = fma(a.VL[k * DL + r], __ldcg(&Rin[k * DR + j]), s);
-        t1[j] = s;
-      }
+      stage(Rs, Rin, DL, DR, DRP, true);
+      stage(VRs, a.VR, DR, DR, DRP, false);
+      for (int k = tid; k < DL; k += PT) Ws[k] = __ldg(&a.VL[k * DL + r]);
       __syncthreads();
-      for (int c = tid; c < DR; c += PT) {
+      vecmat(Ws, Rs, DL, DR, DRP, Ws + 64);  // t1 = (VL^T R)[r, :]
+      __syncthreads();
+      {
+        const int c = tid >> 2, part = tid & 3;
         double s = 0.0;
-#pragma unroll 8
-        for (int j = 0; j < DR; j++) s = fma(t1[j], a.VR[j * DR + c], s);
-        a.T[r * DR + c] = s * a.dinv[r * DR + c];
+        if (c < DR)
+          for (int j = part; j < DR; j += 4) s = fma(Ws[64 + j], VRs[j * DRP + c], s);
+        s += __shfl_xor_sync(0xffffffffu, s, 1);
+        s += __shfl_xor_sync(0xffffffffu, s, 2);
+        if (c < DR && part == 0) a.T[r * DR + c] = s * __ldg(&a.dinv[r * DR + c]);
       }
       __syncthreads();
     }
   };
   auto precond_b = [&]() {
+    double* Ts = sm + S::R_OFF + (cur ^ 1) * CH_S * DRP;
+    double* VRts = Ts + DL * DRP;
     for (int r = b; r < DL; r += G) {
-      double* s1 = Ws;
-      for (int j = tid; j < DR; j += PT) {
-        double s = 0.0;
-#pragma unroll 8
-        for (int k = 0; k < DL; k++) s = fma(a.VL[r * DL + k], __ldcg(&a.T[k * DR + j]), s);
-        s1[j] = s;
-      }
+      stage(Ts, a.T, DL, DR, DRP, true);
+      stage(VRts, a.VRt, DR, DR, DRP, false);
+      for (int k = tid; k < DL; k += PT) Ws[k] = __ldg(&a.VL[r * DL + k]);
+      __syncthreads();
+      vecmat(Ws, Ts, DL, DR, DRP, Ws + 64);  // s1 = (VL T)[r, :]
       __syncthreads();
       double sq = 0.0;
-      for (int c = tid; c < DR; c += PT) {
+      {
+        const int c = tid >> 2, part = tid & 3;
         double s = 0.0;
-#pragma unroll 8
-        for (int j = 0; j < DR; j++) s = fma(s1[j], a.VRt[j * DR + c], s);
-        a.step[r * DR + c] = s;
-        sq = fma(s, s, sq);
+        if (c < DR)
+          for (int j = part; j < DR; j += 4) s = fma(Ws[64 + j], VRts[j * DRP + c], s);
+        s += __shfl_xor_sync(0xffffffffu, s, 1);
+        s += __shfl_xor_sync(0xffffffffu, s, 2);
+        if (c < DR && part == 0) {
+          a.step[r * DR + c] = s;
+          sq = s * s;
+        }
       }
-      sq = block_sum(sq, Ws + 128);
+      sq = block_sum(sq, Ws + 192);
       if (tid == 0) a.rowsq[r] = sq;
       __syncthreads();
     }
   };
+  // ||step|| from the per-row squares: identical fixed-order butterfly in every CTA
   auto row_norm = [&]() {
-    // identical fixed-order sum in every CTA
-    if (tid == 0) {
+    if (warp == 0) {
       double s = 0.0;
-      for (int r = 0; r < DL; r++) s += __ldcg(&a.rowsq[r]);
-      Ws[200] = sqrt(s);
+      for (int r = lane; r < DL; r += 32) s += __ldcg(&a.rowsq[r]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double os = __shfl_xor_sync(0xffffffffu, s, o);
+        s = (lane & o) ? os + s : s + os;
+      }
+      if (lane == 0) Ws[250] = sqrt(s);
     }
     __syncthreads();
-    const double v = Ws[200];
+    const double v = Ws[250];
     __syncthreads();
     return v;
   };
 
-  // scale = ||P rhs|| -> tol
   precond_a(a.rhs);
   grid.sync();
   precond_b();
   grid.sync();
   const double tol = a.residual_tol * fmax(row_norm(), DBL_MIN);
 
-  // prefetch the first chunk
   if (tid == 0 && c_beg < c_end) {
     issue_chunk<DL, DR>(a, a.chunks[c_beg], sm, &bars[0], 0);
     pending[0] = 1;
   }
-  int cur = 0;
 
   int status = 0, iters = 0, hlen = 0;
   const bool prof = (b == 0 && tid == 0);
@@ -207,13 +238,10 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
     // ---------------- P1: sketched normal-operator apply ----------------
     double gacc[G_PER_W][4];
 #pragma unroll
-    for (int i = 0; i < G_PER_W; i++)
-#pragma unroll
-      for (int j = 0; j < 4; j++) gacc[i][j] = 0.0;
+    for (int i = 0; i < G_PER_W; i++) gacc[i][0] = gacc[i][1] = gacc[i][2] = gacc[i][3] = 0.0;
     int buf = cur;
     for (int64_t c = c_beg; c < c_end; c++) {
       const Chunk ch = a.chunks[c];
-      // prefetch the next chunk (or the first one of the next iteration) into the other buffer
       if (tid == 0 && !resident) {
         const int64_t cn = (c + 1 < c_end) ? c + 1 : c_beg;
         if (!(cn == c_beg && it + 1 >= a.max_iters)) {
@@ -228,8 +256,8 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
       }
       const double* Ls = sm + S::L_OFF + buf * CH_ROWS * DLP;
       const double* Rs = sm + S::R_OFF + buf * CH_S * DRP;
-      const int nrows = (int)(ch.u_e - ch.u_b), nsamp = (int)(ch.t_e - ch.t_b);
-      // Y = L_chunk X   (rows >= nrows read stale smem; their results are never used)
+      const int nrows = (int)(ch.u_e - ch.u_b);
+      // Y = L_chunk X
 #pragma unroll
       for (int yi = 0; yi < Y_PER_W; yi++) {
         const int tile = warp + yi * PW;
@@ -250,43 +278,40 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
         }
       }
       __syncthreads();
-      // samples: warp per left row
-      for (int r = warp; r < CH_ROWS; r += PW) {
-        double z[(DR + 31) / 32];
+      // samples: half-warp per left row, QE consecutive right-row entries per lane
+      {
+        const int r = tid >> 4, ql = tid & 15;
+        const unsigned qmask = 0xffffu << (lane & 16);
+        double z[QE];
 #pragma unroll
-        for (int j = 0; j < (DR + 31) / 32; j++) z[j] = 0.0;
+        for (int j = 0; j < QE; j++) z[j] = 0.0;
         if (r < nrows) {
           const int64_t u = ch.u_b + r;
           const int64_t tb = max(a.seg[u], ch.t_b), te = min(a.seg[u + 1], ch.t_e);
-          double y[(DR + 31) / 32];
+          double y[QE];
 #pragma unroll
-          for (int j = 0; j < (DR + 31) / 32; j++) {
-            const int k = lane + 32 * j;
-            y[j] = (k < DR) ? Ys[r * DRP + k] : 0.0;
-          }
+          for (int j = 0; j < QE; j++) y[j] = Ys[r * DRP + ql * QE + j];
           for (int64_t t = tb; t < te; t++) {
-            const int ts = (int)(t - ch.t_b);
-            const double* Rt = Rs + ts * DRP;
-            double rv[(DR + 31) / 32];
+            const double* Rt = Rs + (int)(t - ch.t_b) * DRP;
+            double rv[QE];
             double d = 0.0;
 #pragma unroll
-            for (int j = 0; j < (DR + 31) / 32; j++) {
-              const int k = lane + 32 * j;
-              rv[j] = (k < DR) ? Rt[k] : 0.0;
+            for (int j = 0; j < QE; j++) {
+              rv[j] = Rt[ql * QE + j];
               d = fma(y[j], rv[j], d);
             }
-            d = warp_sum(d);
+            d += __shfl_xor_sync(qmask, d, 1);
+            d += __shfl_xor_sync(qmask, d, 2);
+            d += __shfl_xor_sync(qmask, d, 4);
+            d += __shfl_xor_sync(qmask, d, 8);
             const double vt = Rt[DR];  // v_t travels in the row padding
             const double s = vt * (vt * d);
 #pragma unroll
-            for (int j = 0; j < (DR + 31) / 32; j++) z[j] = fma(s, rv[j], z[j]);
+            for (int j = 0; j < QE; j++) z[j] = fma(s, rv[j], z[j]);
           }
         }
 #pragma unroll
-        for (int j = 0; j < (DR + 31) / 32; j++) {
-          const int k = lane + 32 * j;
-          if (k < DR) Zs[r * DRP + k] = z[j];
-        }
+        for (int j = 0; j < QE; j++) Zs[r * DRP + ql * QE + j] = z[j];
       }
       __syncthreads();
       // G += L_chunk^T Z   (K = CH_ROWS; rows >= nrows have Z == 0)
@@ -297,18 +322,18 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
           const int m0 = (tile / GT_N) * 16, n0 = (tile % GT_N) * 8;
 #pragma unroll
           for (int k0 = 0; k0 < CH_ROWS; k0 += 4) {
-            const double a0 = (k0 + t4 < nrows) ? Ls[(k0 + t4) * DLP + m0 + g] : 0.0;
-            const double a1 = (k0 + t4 < nrows) ? Ls[(k0 + t4) * DLP + m0 + g + 8] : 0.0;
+            const bool ok = k0 + t4 < nrows;
+            const double a0 = ok ? Ls[(k0 + t4) * DLP + m0 + g] : 0.0;
+            const double a1 = ok ? Ls[(k0 + t4) * DLP + m0 + g + 8] : 0.0;
             const double b0 = Zs[(k0 + t4) * DRP + n0 + g];
             dmma_16x8x4(gacc[gi], a0, a1, b0);
           }
         }
       }
-      __syncthreads();  // Ls/Rs/Zs of this buffer may be overwritten after this point
+      __syncthreads();
       if (!resident) buf ^= 1;
     }
     cur = buf;
-    // write this CTA's partial G
     double* P = a.part + (size_t)b * NE;
 #pragma unroll
     for (int gi = 0; gi < G_PER_W; gi++) {
@@ -325,30 +350,41 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
     grid.sync();
     if (prof) g_prof[it * 6 + 2] = clock64();
     // ---------------- P2: R = sum G + lam X - rhs ----------------
-    for (int e = b * PW + warp; e < NE; e += G * PW) {
-      double s = 0.0, cmp = 0.0;
-      for (int p = lane; p < G; p += 32) {
-        const double v = __ldcg(&a.part[(size_t)p * NE + e]);
-        const double tt = s + v;
-        cmp += (fabs(s) >= fabs(v)) ? ((s - tt) + v) : ((v - tt) + s);
-        s = tt;
-      }
-      // combine lanes in a fixed butterfly order (TwoSum keeps the compensation)
+    {
+      // quarter-warp per element; every lane issues all of its partial loads up front
+      constexpr int MAXQ = 20;  // 8 lanes x 20 >= 160 CTAs
+      const int qid = (b * PT + tid) >> 3, ql = lane & 7;
+      const unsigned qmask = 0xffu << (lane & 24);
+      for (int e = qid; e < NE; e += G * PT / 8) {
+        double v[MAXQ];
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double os = __shfl_xor_sync(0xffffffffu, s, o);
-        const double oc = __shfl_xor_sync(0xffffffffu, cmp, o);
-        const double lo = (lane & o) ? os : s, hi = (lane & o) ? s : os;  // order-independent pair
-        const double tt = lo + hi;
-        const double bb = tt - lo;
-        const double err = (lo - (tt - bb)) + (hi - bb);
-        s = tt;
-        cmp = ((lane & o) ? oc : cmp) + ((lane & o) ? cmp : oc) + err;
-      }
-      if (lane == 0) {
-        const double gsum = s + cmp;
-        const int i = e / DR, k = e - i * DR;
-        a.R[e] = __dsub_rn(__dadd_rn(gsum, __dmul_rn(a.lam, Xs[i * DRP + k])), a.rhs[e]);
+        for (int j = 0; j < MAXQ; j++) {
+          const int p = ql + 8 * j;
+          v[j] = (p < G) ? __ldcg(&a.part[(size_t)p * NE + e]) : 0.0;
+        }
+        double s = 0.0, cmp = 0.0;
+#pragma unroll
+        for (int j = 0; j < MAXQ; j++) {
+          const double tt = s + v[j];
+          cmp += (fabs(s) >= fabs(v[j])) ? ((s - tt) + v[j]) : ((v[j] - tt) + s);
+          s = tt;
+        }
+#pragma unroll
+        for (int o = 4; o > 0; o >>= 1) {
+          const double os = __shfl_xor_sync(qmask, s, o);
+          const double oc = __shfl_xor_sync(qmask, cmp, o);
+          const bool up = lane & o;
+          const double lo = up ? os : s, hi = up ? s : os;
+          const double tt = lo + hi;
+          const double bb = tt - lo;
+          const double err = (lo - (tt - bb)) + (hi - bb);
+          cmp = (up ? oc : cmp) + (up ? cmp : oc) + err;
+          s = tt;
+        }
+        if (ql == 0) {
+          const int i = e / DR, k = e - i * DR;
+          a.R[e] = __dsub_rn(__dadd_rn(s + cmp, __dmul_rn(a.lam, Xs[i * DRP + k])), __ldg(&a.rhs[e]));
+        }
       }
     }
     grid.sync();
@@ -389,7 +425,6 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
     iters = it + 1;
     __syncthreads();
   }
-  // drain a prefetched chunk that will never be consumed (keeps the mbarrier state clean)
   if (b == 0) {
     for (int e = tid; e < NE; e += PT) {
       const int i = e / DR, k = e - i * DR;
@@ -433,8 +468,8 @@ int launch(cudaStream_t st, PArgs& a, int grid) {
   KS_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::BYTES));
   int per_sm = 0;
   KS_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, PT, S::BYTES));
-  KS_REQUIRE(per_sm >= 1, KS_ESIZE, "persistent Richardson kernel does not fit on an SM");
-  if (grid > per_sm * ks::num_sms()) grid = per_sm * ks::num_sms();
+  KS_REQUIRE(per_sm >= 1 && grid <= per_sm * ks::num_sms(), KS_ESIZE,
+             "persistent Richardson kernel does not fit co-resident");
   void* args[] = {&a};
   KS_TRY_CUDA(cudaLaunchCooperativeKernel((void*)kern, grid, PT, args, S::BYTES, st));
   return KS_OK;
@@ -449,7 +484,6 @@ bool persistent_supported(int dL, int dR) {
   return ok(dL) && ok(dR);
 }
 
-// Runs the whole Richardson loop; x (dL x dR), hist on device; *iters, *hist_len, *status host.
 int richardson_persistent(cudaStream_t st, const ks_sketch_view* sk, const double* VL, const double* VR,
                           const double* dinv, const double* rhs, double lam, double damping, int max_iters,
                           double residual_tol, double* x, double* hist, int* iters, int* hist_len, int* status) {
@@ -457,11 +491,12 @@ int richardson_persistent(cudaStream_t st, const ks_sketch_view* sk, const doubl
   KS_REQUIRE(max_iters <= 1024, KS_ESIZE, "persistent loop keeps <= 1024 history entries");
   const int dLp = dL + PAD, dRp = dR + PAD;
   const int64_t nnz = sk->nnz, ul = sk->u_left;
-  // chunk table from the segment offsets (host; one small copy per sketch)
   std::vector<int64_t> seg(ul + 1);
   KS_TRY_CUDA(cudaMemcpyAsync(seg.data(), sk->seg, (ul + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   KS_TRY_CUDA(cudaStreamSynchronize(st));
+  // chunks: <= CH_ROWS distinct left rows and <= CH_S samples; heavy rows are split
   std::vector<Chunk> chunks;
+  std::vector<double> cost;
   {
     int64_t u = 0, t = 0;
     while (t < nnz) {
@@ -475,7 +510,7 @@ int richardson_persistent(cudaStream_t st, const ks_sketch_view* sk, const doubl
           te = row_end;
           ue++;
         } else {
-          if (ue == u) {  // a heavy row: split it
+          if (ue == u) {
             te = t + CH_S;
             ue = u + 1;
           }
@@ -485,21 +520,41 @@ int richardson_persistent(cudaStream_t st, const ks_sketch_view* sk, const doubl
       c.u_e = ue;
       c.t_e = te;
       chunks.push_back(c);
+      // DMMA work is fixed per chunk (32-row tiles); samples add the quarter-warp loop
+      cost.push_back(4.0 * CH_ROWS * dL * dR + 24.0 * (double)(te - t) * dR);
       t = te;
       u = (te >= seg[ue]) ? ue : ue - 1;
       while (u < ul && seg[u + 1] <= t) u++;
     }
   }
   const int64_t nch = (int64_t)chunks.size();
-  const int grid = num_sms();
+  int grid = num_sms();
+  // contiguous chunk ranges of (nearly) equal cost
+  std::vector<int64_t> range(grid + 1, nch);
+  {
+    double total = 0.0;
+    for (double c : cost) total += c;
+    range[0] = 0;
+    double acc = 0.0;
+    int64_t c = 0;
+    for (int bb = 1; bb < grid; bb++) {
+      const double target = total * bb / grid;
+      while (c < nch && acc + 0.5 * cost[c] < target) acc += cost[c++];
+      range[bb] = c;
+    }
+    range[grid] = nch;
+  }
   Scratch<double> Lpack(ul * dLp + 2, st), Rpack(nnz * dRp + 2, st), part((int64_t)grid * dL * dR, st);
   Scratch<double> R((int64_t)dL * dR, st), T((int64_t)dL * dR, st), stepb((int64_t)dL * dR, st), rowsq(dL, st);
   Scratch<double> VRt((int64_t)dR * dR, st);
   Scratch<Chunk> dch(nch + 1, st);
+  Scratch<int64_t> drange(grid + 1, st);
   Scratch<int> state(4, st);
-  KS_REQUIRE(Lpack.p && Rpack.p && part.p && R.p && T.p && stepb.p && rowsq.p && VRt.p && dch.p && state.p,
+  KS_REQUIRE(Lpack.p && Rpack.p && part.p && R.p && T.p && stepb.p && rowsq.p && VRt.p && dch.p && drange.p &&
+                 state.p,
              KS_ECUDA, "scratch allocation failed");
   KS_TRY_CUDA(cudaMemcpyAsync(dch.p, chunks.data(), nch * sizeof(Chunk), cudaMemcpyHostToDevice, st));
+  KS_TRY_CUDA(cudaMemcpyAsync(drange.p, range.data(), (grid + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
   pack_rows_kernel<<<ceil_div_u(ul * dLp, 256), 256, 0, st>>>(sk->Lmat, sk->ldl, sk->lrow, ul, dL, dLp, nullptr,
                                                                Lpack.p);
   KS_CHECK_LAUNCH();
@@ -509,7 +564,7 @@ int richardson_persistent(cudaStream_t st, const ks_sketch_view* sk, const doubl
   transpose_sq_kernel2<<<ceil_div_u((int64_t)dR * dR, 256), 256, 0, st>>>(VR, dR, VRt.p);
   KS_CHECK_LAUNCH();
   PArgs a{};
-  a.Lpack = Lpack.p; a.Rpack = Rpack.p; a.v = sk->v; a.seg = sk->seg; a.chunks = dch.p; a.nchunks = nch;
+  a.Lpack = Lpack.p; a.Rpack = Rpack.p; a.seg = sk->seg; a.chunks = dch.p; a.range = drange.p;
   a.VL = VL; a.VR = VR; a.VRt = VRt.p; a.dinv = dinv; a.rhs = rhs;
   a.lam = lam; a.damping = damping; a.residual_tol = residual_tol; a.max_iters = max_iters;
   a.part = part.p; a.R = R.p; a.T = T.p; a.step = stepb.p; a.rowsq = rowsq.p; a.x_out = x; a.hist = hist;
@@ -538,8 +593,8 @@ int richardson_persistent(cudaStream_t st, const ks_sketch_view* sk, const doubl
 }  // namespace ks
 
 // Average cycles of CTA 0 per phase over the last persistent run:
-// out[0] = apply (P1), out[1] = grid sync after P1, out[2] = reduce (P2 + sync),
-// out[3] = precond A (P3 + sync), out[4] = precond B (P4 + sync), out[5] = update + loop.
+// apply (P1), sync wait after P1, reduce (P2 + sync), precond A (P3 + sync), precond B (P4 + sync),
+// update + loop overhead.
 extern "C" int ks_debug_richardson_phases(int32_t iters, double* out6) {
   if (iters < 2 || iters > 1024) return KS_EINVAL;
   std::vector<long long> h(6 * iters);

@@ -144,19 +144,29 @@ __global__ void zig_eval_kernel(const uint64_t* __restrict__ raw, int64_t M, int
 
 constexpr int ZL = 128;  // chunk length (positions)
 constexpr int ZK = 16;   // entry offsets tracked per chunk
+constexpr int ZCB = 128; // chunks per block of the chunk / emit kernels
 
 // For each chunk and entry offset o < ZK: exit offset into the next chunk and normals emitted.
 __global__ void zig_chunk_kernel(const int16_t* __restrict__ cons, int64_t M, int64_t nchunks,
                                  uint8_t* __restrict__ exit_off, int32_t* __restrict__ cnt,
                                  int32_t* __restrict__ err) {
+  // stage the block's consumption table in shared memory (coalesced), then walk from smem
+  __shared__ int16_t sc[ZCB * ZL];
+  const int64_t blk_beg = (int64_t)blockIdx.x * ZCB * ZL;
+  for (int i = threadIdx.x; i < ZCB * ZL; i += blockDim.x) {
+    const int64_t p = blk_beg + i;
+    sc[i] = (p < M) ? cons[p] : (int16_t)1;
+  }
+  __syncthreads();
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= nchunks) return;
   const int64_t beg = c * ZL, end = ks_min64(M, beg + ZL);
+#define cons(q) sc[(q) - blk_beg]
   uint64_t mask[ZL / 64] = {0, 0};
   int64_t q = beg;
   int c0 = 0;
   while (q < end) {
-    const int k = cons[q];
+    const int k = cons(q);
     if (k <= 0) { atomicOr(err, 1); return; }
     mask[(q - beg) >> 6] |= 1ull << ((q - beg) & 63);
     c0++;
@@ -170,7 +180,7 @@ __global__ void zig_chunk_kernel(const int16_t* __restrict__ cons, int64_t M, in
     int64_t qq = beg + o;
     int steps = 0;
     while (qq < end && !((mask[(qq - beg) >> 6] >> ((qq - beg) & 63)) & 1)) {
-      const int k = cons[qq];
+      const int k = cons(qq);
       if (k <= 0) { atomicOr(err, 1); return; }
       steps++;
       qq += k;
@@ -190,6 +200,7 @@ __global__ void zig_chunk_kernel(const int16_t* __restrict__ cons, int64_t M, in
       cnt[c * ZK + o] = steps + (c0 - before);
     }
   }
+#undef cons
 }
 
 constexpr int ZS = 16;  // chunks per super-chunk
@@ -221,9 +232,10 @@ __global__ void __launch_bounds__(ZSCAN_T) zig_scan_kernel(const uint8_t* __rest
                                                           int64_t nsuper, uint8_t* __restrict__ sentry,
                                                           int64_t* __restrict__ sbase,
                                                           int64_t* __restrict__ total) {
+  // layout [buffer][offset][thread]: consecutive threads touch consecutive words (no bank conflicts)
   extern __shared__ unsigned char zsm[];
-  uint8_t (*fe)[ZSCAN_T][ZK] = reinterpret_cast<uint8_t (*)[ZSCAN_T][ZK]>(zsm);
-  int64_t (*fc)[ZSCAN_T][ZK] = reinterpret_cast<int64_t (*)[ZSCAN_T][ZK]>(zsm + 2 * ZSCAN_T * ZK);
+  int64_t (*fc)[ZK][ZSCAN_T] = reinterpret_cast<int64_t (*)[ZK][ZSCAN_T]>(zsm);
+  uint8_t (*fe)[ZK][ZSCAN_T] = reinterpret_cast<uint8_t (*)[ZK][ZSCAN_T]>(zsm + 2 * ZSCAN_T * ZK * sizeof(int64_t));
   const int t = threadIdx.x;
   const int64_t per = (nsuper + ZSCAN_T - 1) / ZSCAN_T;
   const int64_t c_beg = ks_min64(nsuper, t * per), c_end = ks_min64(nsuper, c_beg + per);
@@ -234,34 +246,34 @@ __global__ void __launch_bounds__(ZSCAN_T) zig_scan_kernel(const uint8_t* __rest
       k += scnt[c * ZK + e];
       e = sexit[c * ZK + e];
     }
-    fe[0][t][o] = (uint8_t)e;
-    fc[0][t][o] = k;
+    fe[0][o][t] = (uint8_t)e;
+    fc[0][o][t] = k;
   }
   __syncthreads();
   int cur = 0;
   for (int off = 1; off < ZSCAN_T; off <<= 1) {
     for (int o = 0; o < ZK; o++) {
       if (t >= off) {
-        const int mid = fe[cur][t - off][o];
-        fe[cur ^ 1][t][o] = fe[cur][t][mid];
-        fc[cur ^ 1][t][o] = fc[cur][t - off][o] + fc[cur][t][mid];
+        const int mid = fe[cur][o][t - off];
+        fe[cur ^ 1][o][t] = fe[cur][mid][t];
+        fc[cur ^ 1][o][t] = fc[cur][o][t - off] + fc[cur][mid][t];
       } else {
-        fe[cur ^ 1][t][o] = fe[cur][t][o];
-        fc[cur ^ 1][t][o] = fc[cur][t][o];
+        fe[cur ^ 1][o][t] = fe[cur][o][t];
+        fc[cur ^ 1][o][t] = fc[cur][o][t];
       }
     }
     __syncthreads();
     cur ^= 1;
   }
-  int e = (t == 0) ? 0 : fe[cur][t - 1][0];
-  int64_t k = (t == 0) ? 0 : fc[cur][t - 1][0];
+  int e = (t == 0) ? 0 : fe[cur][0][t - 1];
+  int64_t k = (t == 0) ? 0 : fc[cur][0][t - 1];
   for (int64_t c = c_beg; c < c_end; c++) {
     sentry[c] = (uint8_t)e;
     sbase[c] = k;
     k += scnt[c * ZK + e];
     e = sexit[c * ZK + e];
   }
-  if (t == ZSCAN_T - 1) *total = fc[cur][t][0];
+  if (t == ZSCAN_T - 1) *total = fc[cur][0][t];
 }
 
 // Per super-chunk: entry offsets and output bases of its chunks.
@@ -286,16 +298,24 @@ __global__ void zig_emit_kernel(const int16_t* __restrict__ cons, const double* 
                                 int64_t M, int64_t nchunks, const uint8_t* __restrict__ entry,
                                 const int64_t* __restrict__ base, int64_t count, double divisor,
                                 double* __restrict__ out, int64_t* __restrict__ consumed) {
+  __shared__ int16_t sc[ZCB * ZL];
+  const int64_t blk_beg = (int64_t)blockIdx.x * ZCB * ZL;
+  for (int i = threadIdx.x; i < ZCB * ZL; i += blockDim.x) {
+    const int64_t p = blk_beg + i;
+    sc[i] = (p < M) ? cons[p] : (int16_t)1;
+  }
+  __syncthreads();
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= nchunks) return;
   const int64_t beg = c * ZL, end = ks_min64(M, beg + ZL);
   int64_t q = beg + entry[c];
   int64_t k = base[c];
   while (q < end) {
+    const int step = sc[q - blk_beg];
     if (k < count) out[k] = val[q] / divisor;
-    if (k == count - 1) *consumed = q + cons[q];
+    if (k == count - 1) *consumed = q + step;
     k++;
-    q += cons[q];
+    q += step;
   }
 }
 

@@ -17,6 +17,7 @@ int gemm(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha, const d
 namespace {
 
 constexpr int QR_THREADS = 256;
+__device__ int g_jacobi_sweeps[8];
 constexpr size_t QR_SMEM_CAP = 200 * 1024;
 
 // Householder QR of one panel of `rows` x d (rows <= prows) taken from src rows
@@ -179,6 +180,7 @@ __global__ void jacobi_svd_kernel(const double* __restrict__ M, int d, double* _
       }
       __syncthreads();
     }
+    if (tid == 0) g_jacobi_sweeps[blockIdx.x & 7] = sweep + 1;
     if (s_rot == 0) break;
     __syncthreads();
   }
@@ -437,5 +439,11 @@ extern "C" int ks_inverse_small(const double* M, int32_t d, double* X, int32_t* 
   KS_TRY_CUDA(cudaFuncSetAttribute(inverse_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem + 1024));
   inverse_small_kernel<<<1, 128, smem, (cudaStream_t)stream>>>(M, d, X, info);
   KS_CHECK_LAUNCH();
+  return KS_OK;
+}
+
+// Profiling aid: sweeps used by the last one-sided Jacobi launch (first 8 problems).
+extern "C" int ks_debug_jacobi_sweeps(int32_t* out8) {
+  KS_TRY_CUDA(cudaMemcpyFromSymbol(out8, g_jacobi_sweeps, sizeof(int) * 8));
   return KS_OK;
 }

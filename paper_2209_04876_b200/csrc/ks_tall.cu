@@ -1,0 +1,130 @@
+// Split-K C(M x N) = alpha A^T B for tall operands (K >> M, N; M, N <= 128) on FP64 tensor cores.
+// Used for the Gram matrices A~^T A~ (reference solvers.py:146, :439) and the JL projection
+// G A~ (leverage.py:127).  Each CTA stages 32-row slabs of A and B in padded shared memory,
+// runs DMMA m16n8k4 over its K-range and writes a private partial; a warp-per-output fixed-order
+// reduction sums the partials (deterministic).
+#include "ks_common.cuh"
+#include "ks_tma.cuh"
+
+namespace {
+
+constexpr int TK = 32;       // k rows per slab
+constexpr int TT = 256;      // threads
+constexpr int TW = TT / 32;  // warps
+
+template <int MP, int NP>  // padded M, N (multiples of 16 / 8)
+__global__ void __launch_bounds__(TT) tall_tn_kernel(int M, int N, int64_t K, int64_t chunk,
+                                                     const double* __restrict__ A, int64_t a_ks, int64_t a_ms,
+                                                     const double* __restrict__ B, int64_t b_ks, int64_t b_ns,
+                                                     double* __restrict__ part) {
+  constexpr int LDA = MP + 4, LDB = NP + 4;
+  constexpr int TILES = (MP / 16) * (NP / 8);
+  constexpr int PER_W = (TILES + TW - 1) / TW;
+  extern __shared__ double tsm[];
+  double* As = tsm;
+  double* Bs = tsm + TK * LDA;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t4 = lane & 3;
+  const int64_t kbeg = (int64_t)blockIdx.x * chunk;
+  const int64_t kend = ks_min64(K, kbeg + chunk);
+  double acc[PER_W][4];
+#pragma unroll
+  for (int i = 0; i < PER_W; i++) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.0;
+  const bool a_kfast = (a_ks == 1);
+  const bool b_kfast = (b_ks == 1);
+  for (int64_t k0 = kbeg; k0 < kend; k0 += TK) {
+    for (int e = tid; e < TK * MP; e += TT) {
+      int kk, mm;
+      if (a_kfast) { mm = e / TK; kk = e - mm * TK; } else { kk = e / MP; mm = e - kk * MP; }
+      const int64_t gk = k0 + kk;
+      As[kk * LDA + mm] = (gk < kend && mm < M) ? A[gk * a_ks + (int64_t)mm * a_ms] : 0.0;
+    }
+    for (int e = tid; e < TK * NP; e += TT) {
+      int kk, nn;
+      if (b_kfast) { nn = e / TK; kk = e - nn * TK; } else { kk = e / NP; nn = e - kk * NP; }
+      const int64_t gk = k0 + kk;
+      Bs[kk * LDB + nn] = (gk < kend && nn < N) ? B[gk * b_ks + (int64_t)nn * b_ns] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < PER_W; i++) {
+      const int tile = warp + i * TW;
+      if (tile < TILES) {
+        const int m0 = (tile / (NP / 8)) * 16, n0 = (tile % (NP / 8)) * 8;
+#pragma unroll
+        for (int kk = 0; kk < TK; kk += 4) {
+          const double a0 = As[(kk + t4) * LDA + m0 + g];
+          const double a1 = As[(kk + t4) * LDA + m0 + g + 8];
+          const double b0 = Bs[(kk + t4) * LDB + n0 + g];
+          dmma_16x8x4(acc[i], a0, a1, b0);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  double* out = part + (int64_t)blockIdx.x * M * N;
+#pragma unroll
+  for (int i = 0; i < PER_W; i++) {
+    const int tile = warp + i * TW;
+    if (tile < TILES) {
+      const int m0 = (tile / (NP / 8)) * 16, n0 = (tile % (NP / 8)) * 8;
+      const int r0 = m0 + g, c0 = n0 + 2 * t4;
+      if (r0 < M && c0 < N) out[r0 * N + c0] = acc[i][0];
+      if (r0 < M && c0 + 1 < N) out[r0 * N + c0 + 1] = acc[i][1];
+      if (r0 + 8 < M && c0 < N) out[(r0 + 8) * N + c0] = acc[i][2];
+      if (r0 + 8 < M && c0 + 1 < N) out[(r0 + 8) * N + c0 + 1] = acc[i][3];
+    }
+  }
+}
+
+__global__ void reduce_parts_warp_kernel(const double* __restrict__ part, int64_t nparts, int64_t count,
+                                         double alpha, double* __restrict__ out) {
+  const int64_t e = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (e >= count) return;
+  double s = 0.0;
+  for (int64_t k = lane; k < nparts; k += 32) s += part[k * count + e];
+  s = warp_sum(s);
+  if (lane == 0) out[e] = alpha * s;
+}
+
+template <int MP, int NP>
+void launch_tall(cudaStream_t st, int nparts, int M, int N, int64_t K, int64_t chunk, const double* A, int64_t a_ks,
+                 int64_t a_ms, const double* B, int64_t b_ks, int64_t b_ns, double* part) {
+  const size_t smem = sizeof(double) * TK * ((MP + 4) + (NP + 4));
+  cudaFuncSetAttribute(tall_tn_kernel<MP, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  tall_tn_kernel<MP, NP><<<nparts, TT, smem, st>>>(M, N, K, chunk, A, a_ks, a_ms, B, b_ks, b_ns, part);
+}
+
+}  // namespace
+
+namespace ks {
+
+int gemm_tn_tall_dmma(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
+                      int64_t a_ks, int64_t a_ms, const double* B, int64_t b_ks, int64_t b_ns, double* C) {
+  const int mp = M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : 128;
+  const int np = N <= 16 ? 16 : N <= 32 ? 32 : N <= 64 ? 64 : 128;
+  int64_t nparts = (K + 63) / 64;
+  const int64_t cap = num_sms();
+  if (nparts > cap) nparts = cap;
+  int64_t chunk = (K + nparts - 1) / nparts;
+  chunk = (chunk + TK - 1) / TK * TK;
+  nparts = (K + chunk - 1) / chunk;
+  Scratch<double> part(nparts * M * N, st);
+  KS_REQUIRE(part.p, KS_ECUDA, "scratch allocation failed");
+  const int np_i = (int)nparts;
+#define KS_TALL(MM, NN)                                                                                  \
+  if (mp == MM && np == NN)                                                                              \
+    launch_tall<MM, NN>(st, np_i, (int)M, (int)N, K, chunk, A, a_ks, a_ms, B, b_ks, b_ns, part.p);
+  KS_TALL(16, 16) KS_TALL(16, 32) KS_TALL(16, 64) KS_TALL(16, 128)
+  KS_TALL(32, 16) KS_TALL(32, 32) KS_TALL(32, 64) KS_TALL(32, 128)
+  KS_TALL(64, 16) KS_TALL(64, 32) KS_TALL(64, 64) KS_TALL(64, 128)
+  KS_TALL(128, 16) KS_TALL(128, 32) KS_TALL(128, 64) KS_TALL(128, 128)
+#undef KS_TALL
+  KS_CHECK_LAUNCH();
+  const int64_t count = M * N;
+  reduce_parts_warp_kernel<<<ceil_div_u(count * 32, 256), 256, 0, st>>>(part.p, nparts, count, alpha, C);
+  KS_CHECK_LAUNCH();
+  return KS_OK;
+}
+
+}  // namespace ks

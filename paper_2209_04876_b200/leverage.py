@@ -73,6 +73,9 @@ def regression_sample_count(d: int, eps: float, beta: float = 1.0) -> int:
 
 
 _TABLES = {}
+# inside fast_kronecker_regression the sampler's validation flags are read once at the end of
+# the solve (one host synchronisation) instead of right after the tables are built
+_DEFER_CHECKS = [False]
 
 
 def _zig_tables_dev():
@@ -211,17 +214,46 @@ class ProductSampler:
         if len(per_factor_scores) == 0:
             raise InvalidInputError("need at least one score vector")
         self._host = not D.on_device(per_factor_scores[0].scores)
-        probs, cdfs = [], []
+        scs = []
         for n, ls in enumerate(per_factor_scores):
             sc = D.to_dev(ls.scores)
             if sc.ndim != 1 or sc.numel() == 0:
                 raise InvalidInputError(f"score vector {n} must be a nonempty vector")
-            p, c = _tables(sc, renorm=False, what=f"score vector {n}")
-            probs.append(p)
-            cdfs.append(c)
+            scs.append(sc.contiguous())
+        if len(scs) <= 8:
+            # one launch for every factor's pairwise total / probabilities / exact cdf
+            probs = [D.empty(int(sc.numel())) for sc in scs]
+            cdfs = [D.empty(int(sc.numel())) for sc in scs]
+            flags = torch.zeros(len(scs), dtype=torch.int32, device=D.dev())
+            _lib.call("ks_sampler_tables_batched", len(scs),
+                      _lib.ptr_array(ctypes.c_void_p, [s.data_ptr() for s in scs]),
+                      _lib.ptr_array(ctypes.c_int64, [int(s.numel()) for s in scs]), 0,
+                      _lib.ptr_array(ctypes.c_void_p, [p.data_ptr() for p in probs]),
+                      _lib.ptr_array(ctypes.c_void_p, [c.data_ptr() for c in cdfs]), D.p(flags), D.stream())
+            self._flags = flags  # checked lazily (one host sync per solve)
+        else:
+            probs, cdfs = [], []
+            for n, sc in enumerate(scs):
+                p, c = _tables(sc, renorm=False, what=f"score vector {n}")
+                probs.append(p)
+                cdfs.append(c)
+            self._flags = None
         self._probs = probs
         self._cdfs = cdfs
+        if not _DEFER_CHECKS[0]:
+            self.check()
         self.beta = float(np.prod([1.0 / ls.approx_factor for ls in per_factor_scores]))
+
+    def check(self):
+        """Raise the reference's InvalidInputError for invalid score vectors (leverage.py:163-171)."""
+        if self._flags is None:
+            return
+        for n, f in enumerate(self._flags.cpu().tolist()):
+            if f & 1:
+                raise InvalidInputError(f"score vector {n} must be nonnegative finite")
+            if f & 2:
+                raise InvalidInputError(f"score vector {n} sums to zero")
+        self._flags = None
 
     @property
     def per_factor_probabilities(self):

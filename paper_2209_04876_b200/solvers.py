@@ -421,7 +421,12 @@ def _fast_solve_dev(facs, b, config: RegressionConfig, caches, trace: FastSolveT
             gi = _inverse_from_eig(v, w)
             scores.append(_jl_scores_dev(a, a_tilde, gi, eps_jl, seeds[2 * n + 1], config.jl_log_factor))
             afs.append(1.0 + eps_jl / 2.0)
-    sampler = ProductSampler([LeverageScores(sc, 0.0, af) for sc, af in zip(scores, afs)])
+    from . import leverage as _lev
+    _lev._DEFER_CHECKS[0] = True
+    try:
+        sampler = ProductSampler([LeverageScores(sc, 0.0, af) for sc, af in zip(scores, afs)])
+    finally:
+        _lev._DEFER_CHECKS[0] = False
     eig = reduce(torch.kron, [w for _, w in grams])
     dinv = pseudo_reciprocal(eig + lam)
     state, inc = pcg64_state(seeds[-1])
@@ -461,6 +466,7 @@ def _fast_solve_dev(facs, b, config: RegressionConfig, caches, trace: FastSolveT
                                     float(config.residual_tol), D.p(x), D.p(hist), ctypes.byref(iters),
                                     ctypes.byref(hlen), D.stream())
     history = hist[: hlen.value].cpu().tolist()
+    sampler.check()
     if rc == _lib.KS_EDIVERGED:
         raise NumericalFailureError("Richardson iteration diverged", iterations=iters.value,
                                     diagnostics={"residual_history": history})

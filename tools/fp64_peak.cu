@@ -1,6 +1,7 @@
 // FP64 peak microbenchmark for B200 (sm_100a): DFMA vs DMMA (mma.sync f64) issue throughput.
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o fp64_peak fp64_peak.cu
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("CUDA %s at %d\n", cudaGetErrorString(e), __LINE__); return 1; } } while (0)
@@ -93,7 +94,28 @@ __global__ void copy_kernel(const double2* __restrict__ a, double2* __restrict__
   for (; i < n; i += stride) b[i] = a[i];
 }
 
-int main() {
+int sustained(double seconds) {
+  double* out; CK(cudaMalloc(&out, 8));
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const int grid = sms * 4, bs = 256, iters = 4000;
+  const double flops1 = 2.0 * 16 * 8 * 4 * 4 * iters * (double)grid * (bs / 32);
+  dmma_m16n8k4_kernel<<<grid, bs>>>(out, 100); CK(cudaDeviceSynchronize());
+  int launches = 0; float total_ms = 0;
+  cudaEventRecord(e0);
+  while (total_ms < seconds * 1e3) {
+    for (int i = 0; i < 20; i++) dmma_m16n8k4_kernel<<<grid, bs>>>(out, iters);
+    launches += 20;
+    cudaEventRecord(e1); CK(cudaEventSynchronize(e1));
+    cudaEventElapsedTime(&total_ms, e0, e1);
+  }
+  printf("{\"kind\": \"dmma_sustained\", \"seconds\": %.2f, \"tflops\": %.3f}\n", total_ms / 1e3,
+         flops1 * launches / (total_ms * 1e-3) / 1e12);
+  return 0;
+}
+
+int main(int argc, char** argv) {
+  if (argc > 1) return sustained(atof(argv[1]));
   double* out; CK(cudaMalloc(&out, 8));
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
