@@ -131,6 +131,12 @@ int ks_pcg64_standard_normal(uint64_t state_hi, uint64_t state_lo, uint64_t inc_
 int ks_jl_scores(const double* A, int64_t n, int32_t d, const double* Q, int32_t r,
                  double denom, double* scores, void* stream);
 
+/* Q (r x d) = scale * GA G^-1 for symmetric positive definite G (d x d) and GA (r x d) by a
+ * one-CTA Cholesky solve (the (1+eps/4) (g a_tilde) gram_tilde^-1 factor, leverage.py:114-127).
+ * info[0] (device int32) = k+1 if pivot k is not positive (the caller then uses LU). */
+int ks_jl_projection(const double* G, int32_t d, const double* GA, int32_t r, double scale,
+                     double* Q, int32_t* info, void* stream);
+
 /* exact statistical leverage scores: scores[i] = sum_k U[i,k]^2 * wts[k] (leverage.py:51-64) */
 int ks_row_weighted_sumsq(const double* U, int64_t n, int32_t d, const double* wts,
                           double* scores, void* stream);
@@ -214,6 +220,13 @@ int ks_richardson_sketched(const ks_sketch_view* sk, const double* VL, const dou
                            const double* dinv, const double* rhs, double lam, double damping,
                            int32_t max_iters, double residual_tol, double* x, double* hist,
                            int32_t* iters, int32_t* hist_len, void* stream);
+
+/* Profiling aid: per-CTA %globaltimer stamps (ns) of iteration 5 of the last persistent
+ * Richardson run, 9 per CTA (phase boundaries and grid-barrier exits). */
+int ks_debug_richardson_cta_stamps(int32_t nctas, uint64_t* out);
+
+/* Profiling aid: sweeps used by the last one-sided Jacobi launch (first 8 problems, host out8). */
+int ks_debug_jacobi_sweeps(int32_t* out8);
 
 /* Profiling aid: average SM cycles per phase of the last persistent Richardson run (CTA 0):
  * apply, sync, reduce, precond-A, precond-B, update. */

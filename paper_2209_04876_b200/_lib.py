@@ -54,6 +54,9 @@ _SIGS = {
     "ks_pcg64_standard_normal": ([c_uint64, c_uint64, c_uint64, c_uint64, _i64, _d, _p, _p, _p, _p,
                                   _p], ctypes.c_int),
     "ks_jl_scores": ([_p, _i64, _i32, _p, _i32, _d, _p, _p], ctypes.c_int),
+    "ks_jl_projection": ([_p, _i32, _p, _i32, _d, _p, _p, _p], ctypes.c_int),
+    "ks_debug_jacobi_sweeps": ([_p], ctypes.c_int),
+    "ks_debug_richardson_cta_stamps": ([_i32, _p], ctypes.c_int),
     "ks_row_weighted_sumsq": ([_p, _i64, _i32, _p, _p, _p], ctypes.c_int),
     "ks_sampler_tables": ([_p, _i64, _i32, _p, _p, _p, _p], ctypes.c_int),
     "ks_sampler_tables_batched": ([_i32, _p, _p, _i32, _p, _p, _p, _p], ctypes.c_int),

@@ -83,6 +83,16 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
   return t;
 }
 
+// Asynchronous global->shared copies (LDGSTS): issued back to back without touching registers,
+// so the L2/HBM latencies of a whole staging loop overlap.  (Plain load/store staging loops get
+// serialised by ptxas under register pressure.)  Zero-fill variant for out-of-range elements.
+__device__ __forceinline__ void ks_cp_async8(void* dst, const void* src, bool valid = true) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  const int n = valid ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(n) : "memory");
+}
+__device__ __forceinline__ void ks_cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 __host__ __device__ __forceinline__ int64_t ks_min64(int64_t a, int64_t b) { return a < b ? a : b; }
 __host__ __device__ __forceinline__ int64_t ks_max64(int64_t a, int64_t b) { return a > b ? a : b; }
 

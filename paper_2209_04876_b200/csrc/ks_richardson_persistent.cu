@@ -61,6 +61,15 @@ struct PArgs {
 };
 
 __device__ long long g_prof[6 * 1024];
+__device__ unsigned long long g_cta_ts[256 * 9];  // per-CTA globaltimer stamps of iteration 5
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define KS_STAMP(k) \
+  if (it == 5 && tid == 0 && b < 256) g_cta_ts[b * 9 + (k)] = gtimer();
 
 template <int DL, int DR>
 struct Smem {
@@ -95,11 +104,20 @@ __device__ void issue_chunk(const PArgs& a, const Chunk& ch, double* sm, uint64_
 }
 
 // staged copy of a rows x cols global matrix into padded smem (row stride ld)
+// 16-byte global->shared copies that bypass registers and L1 (all issued back to back, so their
+// L2 latencies overlap; ptxas would otherwise interleave loads with dependent arithmetic).
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// rows x cols (cols even) row-major global matrix -> padded smem (row stride ld, 16B aligned rows)
 __device__ __forceinline__ void stage(double* dst, const double* __restrict__ src, int rows, int cols, int ld,
-                                      bool coherent) {
-  for (int e = threadIdx.x; e < rows * cols; e += PT) {
-    const int i = e / cols, j = e - i * cols;
-    dst[i * ld + j] = coherent ? __ldcg(&src[e]) : __ldg(&src[e]);
+                                      bool /*coherent*/) {
+  const int pairs = rows * (cols / 2);
+  for (int e = threadIdx.x; e < pairs; e += PT) {
+    const int i = e / (cols / 2), j = 2 * (e - i * (cols / 2));
+    cp_async16(dst + i * ld + j, src + (size_t)i * cols + j);
   }
 }
 
@@ -159,6 +177,7 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
       stage(Rs, Rin, DL, DR, DRP, true);
       stage(VRs, a.VR, DR, DR, DRP, false);
       for (int k = tid; k < DL; k += PT) Ws[k] = __ldg(&a.VL[k * DL + r]);
+      cp_async_wait_all();
       __syncthreads();
       vecmat(Ws, Rs, DL, DR, DRP, Ws + 64);  // t1 = (VL^T R)[r, :]
       __syncthreads();
@@ -181,6 +200,7 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
       stage(Ts, a.T, DL, DR, DRP, true);
       stage(VRts, a.VRt, DR, DR, DRP, false);
       for (int k = tid; k < DL; k += PT) Ws[k] = __ldg(&a.VL[r * DL + k]);
+      cp_async_wait_all();
       __syncthreads();
       vecmat(Ws, Ts, DL, DR, DRP, Ws + 64);  // s1 = (VL T)[r, :]
       __syncthreads();
@@ -235,6 +255,7 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
   const bool prof = (b == 0 && tid == 0);
   for (int it = 0; it < a.max_iters; it++) {
     if (prof) g_prof[it * 6 + 0] = clock64();
+    KS_STAMP(0)
     // ---------------- P1: sketched normal-operator apply ----------------
     double gacc[G_PER_W][4];
 #pragma unroll
@@ -347,26 +368,36 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
       }
     }
     if (prof) g_prof[it * 6 + 1] = clock64();
+    KS_STAMP(1)
     grid.sync();
+    KS_STAMP(2)
     if (prof) g_prof[it * 6 + 2] = clock64();
     // ---------------- P2: R = sum G + lam X - rhs ----------------
     {
-      // quarter-warp per element; every lane issues all of its partial loads up front
-      constexpr int MAXQ = 20;  // 8 lanes x 20 >= 160 CTAs
-      const int qid = (b * PT + tid) >> 3, ql = lane & 7;
-      const unsigned qmask = 0xffu << (lane & 24);
-      for (int e = qid; e < NE; e += G * PT / 8) {
-        double v[MAXQ];
-#pragma unroll
-        for (int j = 0; j < MAXQ; j++) {
-          const int p = ql + 8 * j;
-          v[j] = (p < G) ? __ldcg(&a.part[(size_t)p * NE + e]) : 0.0;
+      // this CTA's slice of every partial is staged in shared memory with cp.async (all copies in
+      // flight at once), then 8 threads per element sum the G partials in a fixed order
+      const int epc = ((NE + G - 1) / G + 1) & ~1;
+      const int e0 = b * epc, e1 = min(NE, e0 + epc);
+      const int ne_cta = e1 > e0 ? e1 - e0 : 0;
+      double* P2s = sm + S::R_OFF + (cur ^ 1) * CH_S * DRP;  // G x epc
+      {
+        const int npair = ne_cta / 2;
+        for (int k = tid; k < G * npair; k += PT) {
+          const int p = k / npair, j = 2 * (k - p * npair);
+          cp_async16(P2s + p * epc + j, a.part + (size_t)p * NE + e0 + j);
         }
+        cp_async_wait_all();
+        __syncthreads();
+      }
+      const int ql = lane & 7;
+      const unsigned qmask = 0xffu << (lane & 24);
+      for (int eo = tid >> 3; eo < ne_cta; eo += PT / 8) {
+        const int e = e0 + eo;
         double s = 0.0, cmp = 0.0;
-#pragma unroll
-        for (int j = 0; j < MAXQ; j++) {
-          const double tt = s + v[j];
-          cmp += (fabs(s) >= fabs(v[j])) ? ((s - tt) + v[j]) : ((v[j] - tt) + s);
+        for (int p = ql; p < G; p += 8) {
+          const double vv = P2s[p * epc + eo];
+          const double tt = s + vv;
+          cmp += (fabs(s) >= fabs(vv)) ? ((s - tt) + vv) : ((vv - tt) + s);
           s = tt;
         }
 #pragma unroll
@@ -387,14 +418,20 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
         }
       }
     }
+    KS_STAMP(3)
     grid.sync();
+    KS_STAMP(4)
     if (prof) g_prof[it * 6 + 3] = clock64();
     // ---------------- P3 / P4: preconditioner ----------------
     precond_a(a.R);
+    KS_STAMP(5)
     grid.sync();
+    KS_STAMP(6)
     if (prof) g_prof[it * 6 + 4] = clock64();
     precond_b();
+    KS_STAMP(7)
     grid.sync();
+    KS_STAMP(8)
     if (prof) g_prof[it * 6 + 5] = clock64();
     // ---------------- norm, stopping rules, update ----------------
     const double nrm = row_norm();
@@ -610,5 +647,14 @@ extern "C" int ks_debug_richardson_phases(int32_t iters, double* out6) {
     out6[5] += h[(it + 1) * 6] - p[5];
   }
   for (int k = 0; k < 6; k++) out6[k] /= (iters - 1);
+  return KS_OK;
+}
+
+// Profiling aid: per-CTA globaltimer stamps (ns) of iteration 5: out[cta*9 + k], k = apply start,
+// apply end, after sync 1, reduce end, after sync 2, precond A end, after sync 3, precond B end,
+// after sync 4.
+extern "C" int ks_debug_richardson_cta_stamps(int32_t nctas, uint64_t* out) {
+  if (nctas < 1 || nctas > 256) return KS_EINVAL;
+  KS_TRY_CUDA(cudaMemcpyFromSymbol(out, g_cta_ts, sizeof(unsigned long long) * 9 * nctas));
   return KS_OK;
 }

@@ -141,7 +141,11 @@ __global__ void jacobi_svd_kernel(const double* __restrict__ M, int d, double* _
     for (int r = 0; r < dp - 1; r++) {
       if (active) {
         // circle method: position 0 fixed, others rotate
-        auto player = [&](int pos) { return pos == 0 ? 0 : 1 + (pos - 1 + r) % (dp - 1); };
+        auto player = [&](int pos) {
+          int x = pos - 1 + r;  // < 2 (dp - 1): one conditional subtraction instead of a modulo
+          if (x >= dp - 1) x -= dp - 1;
+          return pos == 0 ? 0 : 1 + x;
+        };
         const int p = player(group), q = player(dp - 1 - group);
         double* wp = W + (size_t)p * d;
         double* wq = W + (size_t)q * d;
@@ -158,10 +162,16 @@ __global__ void jacobi_svd_kernel(const double* __restrict__ M, int d, double* _
           c += __shfl_xor_sync(gmask, c, o, g);
         }
         // rotate unless the pair is orthogonal to working precision (dgesvj-style threshold)
-        if (c != 0.0 && a != 0.0 && b != 0.0 && fabs(c) > tol * sqrt(a) * sqrt(b)) {
-          const double zeta = (b - a) / (2.0 * c);
-          const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-          const double cs = 1.0 / sqrt(1.0 + t * t);
+        // (c^2 > tol^2 a b avoids two square roots on the serial path of every round)
+        if (c != 0.0 && a != 0.0 && b != 0.0 && c * c > tol * tol * a * b) {
+          // t only has to be close to tan(theta): any t gives an exact rotation as long as
+          // cs = 1/sqrt(1+t^2) and sn = t cs are consistent, so t uses fast reciprocals and the
+          // orthogonality-critical cs an accurate rsqrt.
+          const double zeta = (b - a) * __drcp_rn(2.0 * c);
+          const double az = fabs(zeta);
+          const double tt = __drcp_rn(az + sqrt(fma(az, az, 1.0)));
+          const double t = zeta >= 0.0 ? tt : -tt;
+          const double cs = rsqrt(fma(t, t, 1.0));
           const double sn = cs * t;
           for (int i = lg; i < d; i += g) {
             const double x = wp[i], y = wq[i];

@@ -36,14 +36,17 @@ __global__ void __launch_bounds__(TT) tall_tn_kernel(int M, int N, int64_t K, in
       int kk, mm;
       if (a_kfast) { mm = e / TK; kk = e - mm * TK; } else { kk = e / MP; mm = e - kk * MP; }
       const int64_t gk = k0 + kk;
-      As[kk * LDA + mm] = (gk < kend && mm < M) ? A[gk * a_ks + (int64_t)mm * a_ms] : 0.0;
+      const bool ok = gk < kend && mm < M;
+      ks_cp_async8(&As[kk * LDA + mm], ok ? A + gk * a_ks + (int64_t)mm * a_ms : A, ok);
     }
     for (int e = tid; e < TK * NP; e += TT) {
       int kk, nn;
       if (b_kfast) { nn = e / TK; kk = e - nn * TK; } else { kk = e / NP; nn = e - kk * NP; }
       const int64_t gk = k0 + kk;
-      Bs[kk * LDB + nn] = (gk < kend && nn < N) ? B[gk * b_ks + (int64_t)nn * b_ns] : 0.0;
+      const bool ok = gk < kend && nn < N;
+      ks_cp_async8(&Bs[kk * LDB + nn], ok ? B + gk * b_ks + (int64_t)nn * b_ns : B, ok);
     }
+    ks_cp_async_wait_all();
     __syncthreads();
 #pragma unroll
     for (int i = 0; i < PER_W; i++) {
@@ -128,3 +131,86 @@ int gemm_tn_tall_dmma(cudaStream_t st, int64_t M, int64_t N, int64_t K, double a
 }
 
 }  // namespace ks
+
+// =============================================================================================
+// Q (r x d) = scale * GA G^-1 for a symmetric positive definite Gram G (d x d), one CTA:
+// right-looking Cholesky G = L L^T in shared memory, then forward / backward substitution of
+// the r right-hand sides GA^T, all rows of a substitution step in parallel.  This is the
+// (1 + eps/4) (g a_tilde) gram_tilde^-1 factor of the JL estimator (leverage.py:114-127).
+// info[0] = k+1 if pivot k is not positive (caller falls back to LU).
+// =============================================================================================
+namespace {
+
+__global__ void __launch_bounds__(512) jl_projection_kernel(const double* __restrict__ G, int d,
+                                                            const double* __restrict__ GA, int r, double scale,
+                                                            double* __restrict__ Q, int32_t* __restrict__ info) {
+  extern __shared__ double sm[];
+  const int ld = d + 1;
+  double* L = sm;                   // d x ld (lower triangle used)
+  double* Y = sm + (size_t)d * ld;  // d x r  (right-hand sides, overwritten by the solution)
+  __shared__ int s_bad;
+  __shared__ double s_piv;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int e = tid; e < d * d; e += nt) L[(e / d) * ld + (e % d)] = G[e];
+  for (int e = tid; e < d * r; e += nt) {
+    const int k = e / r, c = e - k * r;
+    Y[e] = GA[(size_t)c * d + k];
+  }
+  if (tid == 0) s_bad = 0;
+  __syncthreads();
+  for (int k = 0; k < d; k++) {
+    if (tid == 0) {
+      const double p = L[k * ld + k];
+      if (!(p > 0.0) && !s_bad) s_bad = k + 1;
+      s_piv = p > 0.0 ? sqrt(p) : 1.0;
+      L[k * ld + k] = s_piv;
+    }
+    __syncthreads();
+    const double lkk = s_piv;
+    for (int i = k + 1 + tid; i < d; i += nt) L[i * ld + k] /= lkk;
+    __syncthreads();
+    const int m = d - k - 1;
+    for (int e = tid; e < m * m; e += nt) {
+      const int i = k + 1 + e / m, j = k + 1 + e % m;
+      if (j <= i) L[i * ld + j] = fma(-L[i * ld + k], L[j * ld + k], L[i * ld + j]);
+    }
+    __syncthreads();
+  }
+  // forward: L Z = Y
+  for (int k = 0; k < d; k++) {
+    for (int c = tid; c < r; c += nt) Y[k * r + c] /= L[k * ld + k];
+    __syncthreads();
+    for (int e = tid; e < (d - k - 1) * r; e += nt) {
+      const int i = k + 1 + e / r, c = e % r;
+      Y[i * r + c] = fma(-L[i * ld + k], Y[k * r + c], Y[i * r + c]);
+    }
+    __syncthreads();
+  }
+  // backward: L^T X = Z
+  for (int k = d - 1; k >= 0; k--) {
+    for (int c = tid; c < r; c += nt) Y[k * r + c] /= L[k * ld + k];
+    __syncthreads();
+    for (int e = tid; e < k * r; e += nt) {
+      const int i = e / r, c = e % r;
+      Y[i * r + c] = fma(-L[k * ld + i], Y[k * r + c], Y[i * r + c]);
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < r * d; e += nt) {
+    const int c = e / d, k = e - c * d;
+    Q[e] = scale * Y[k * r + c];
+  }
+  if (tid == 0) info[0] = s_bad;
+}
+
+}  // namespace
+
+extern "C" int ks_jl_projection(const double* G, int32_t d, const double* GA, int32_t r, double scale, double* Q,
+                                int32_t* info, void* stream) {
+  const size_t smem = sizeof(double) * ((size_t)d * (d + 1) + (size_t)d * r);
+  KS_REQUIRE(d >= 1 && r >= 1 && smem <= 220 * 1024, KS_ESIZE, "jl_projection: d=%d r=%d too large", d, r);
+  KS_TRY_CUDA(cudaFuncSetAttribute(jl_projection_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  jl_projection_kernel<<<1, 512, smem, (cudaStream_t)stream>>>(G, d, GA, r, scale, Q, info);
+  KS_CHECK_LAUNCH();
+  return KS_OK;
+}

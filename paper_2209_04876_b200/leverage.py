@@ -132,22 +132,36 @@ def jl_projection_rows(n: int, log_factor: float = JL_LOG_FACTOR) -> int:
     return max(1, math.ceil(log_factor * math.log(max(n, 2))))
 
 
-def _jl_scores_dev(a: torch.Tensor, a_tilde: torch.Tensor, gram_inv: torch.Tensor, eps: float, seed,
-                   log_factor: float) -> torch.Tensor:
+def _jl_ga(a: torch.Tensor, a_tilde: torch.Tensor, seed, log_factor: float):
+    """GA = g @ a_tilde with g = default_rng(seed).standard_normal((r, n_tilde)) / sqrt(r) drawn
+    on the device (leverage.py:124-127).  Returns (GA (r x d), r)."""
     n, d = int(a.shape[0]), int(a.shape[1])
     nt = int(a_tilde.shape[0])
     r = jl_projection_rows(n, log_factor)
     g = device_standard_normal(seed, r * nt, divisor=math.sqrt(r))
-    # GA = g @ a_tilde  (r x d), Q = (1 + eps/4) GA gram^-1
     ga = D.empty(r, d)
     if r <= 128 and d <= 128:
         _lib.call("ks_gemm_tn_tall", r, d, nt, 1.0, D.p(g), 1, nt, D.p(a_tilde), d, 1, D.p(ga), D.stream())
     else:
         _lib.call("ks_gemm", r, d, nt, 1.0, D.p(g), nt, 1, 0, D.p(a_tilde), d, 1, 0, 0.0, D.p(ga), d, 1, 0, 1,
                   D.stream())
+    return ga, r
+
+
+def _jl_scores_dev(a: torch.Tensor, a_tilde: torch.Tensor, gram_inv: torch.Tensor, eps: float, seed,
+                   log_factor: float) -> torch.Tensor:
+    d = int(a.shape[1])
+    ga, r = _jl_ga(a, a_tilde, seed, log_factor)
+    # Q = (1 + eps/4) GA gram^-1
     q = D.empty(r, d)
     _lib.call("ks_gemm", r, d, d, 1.0 + eps / 4.0, D.p(ga), d, 1, 0, D.p(gram_inv), d, 1, 0, 0.0, D.p(q), d, 1,
               0, 1, D.stream())
+    return _jl_scores_from_q(a, q, r, eps)
+
+
+def _jl_scores_from_q(a: torch.Tensor, q: torch.Tensor, r: int, eps: float) -> torch.Tensor:
+    """scores_i = ||Q a_i||^2 / ((1+eps/4)(1-eps/20)) (leverage.py:127-129)."""
+    n, d = int(a.shape[0]), int(a.shape[1])
     denom = (1.0 + eps / 4.0) * (1.0 - eps / 20.0)
     scores = D.empty(n)
     if r <= 256:

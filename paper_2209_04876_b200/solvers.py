@@ -360,6 +360,73 @@ def _regression_sample_count(cols: int, config: RegressionConfig) -> int:
                             * math.log(40 * cols) * math.log(1.0 / config.delta) / config.eps))
 
 
+_SIDE = {}
+
+
+def _side_stream() -> torch.cuda.Stream:
+    dev = torch.cuda.current_device()
+    s = _SIDE.get(dev)
+    if s is None:
+        s = torch.cuda.Stream(device=dev)
+        _SIDE[dev] = s
+    return s
+
+
+def _factor_grams_async(gts: list[torch.Tensor]):
+    """Launch the Gram eigendecompositions on a side stream; returns a handle for _join_grams."""
+    main = torch.cuda.current_stream()
+    side = _side_stream()
+    side.wait_stream(main)
+    outs = []
+    same = len({int(g.shape[0]) for g in gts}) == 1
+    with torch.cuda.stream(side):
+        if same and len(gts) > 1:
+            d = int(gts[0].shape[0])
+            gs = torch.stack([0.5 * (g + g.T) for g in gts]).contiguous()
+            w = D.empty(len(gts), d)
+            v = D.empty(len(gts), d, d)
+            _lib.call("ks_svd_small_batched", D.p(gs), len(gts), d, D.p(w), D.p(v), D.stream())
+            outs = [(v[i], w[i]) for i in range(len(gts))]
+            keep = [gs, w, v]
+        else:
+            for g in gts:
+                vv, ww, gs = _factor_gram_dev(g)
+                outs.append((vv, ww))
+            keep = []
+    for g in gts:
+        g.record_stream(side)
+    ev = torch.cuda.Event()
+    ev.record(side)
+    return (outs, ev, keep)
+
+
+def _join_grams(handle):
+    if isinstance(handle, list):
+        return handle
+    outs, ev, keep = handle
+    torch.cuda.current_stream().wait_event(ev)
+    for t in keep:
+        t.record_stream(torch.cuda.current_stream())
+    return outs
+
+
+def _jl_scores_chol(a: torch.Tensor, a_tilde: torch.Tensor, gram: torch.Tensor, eps: float, seed,
+                    log_factor: float) -> torch.Tensor:
+    """JL scores with (1+eps/4) (G a_tilde) gram^-1 from a device Cholesky solve (leverage.py:114-129);
+    falls back to the LU inverse when the Gram is not numerically positive definite."""
+    from .leverage import _jl_ga, _jl_scores_from_q
+    d = int(a.shape[1])
+    ga, r = _jl_ga(a, a_tilde, seed, log_factor)
+    q = D.empty(r, d)
+    info = torch.zeros(1, dtype=torch.int32, device=a.device)
+    _lib.call("ks_jl_projection", D.p(gram), d, D.p(ga), r, 1.0 + eps / 4.0, D.p(q), D.p(info), D.stream())
+    if int(info.item()) != 0:
+        gi = _inverse_small(gram)
+        _lib.call("ks_gemm", r, d, d, 1.0 + eps / 4.0, D.p(ga), d, 1, 0, D.p(gi), d, 1, 0, 0.0, D.p(q), d, 1, 0, 1,
+                  D.stream())
+    return _jl_scores_from_q(a, q, r, eps)
+
+
 def _inverse_from_eig(v: torch.Tensor, w: torch.Tensor) -> torch.Tensor:
     d = int(w.numel())
     if float(w.min().item()) <= 0.0:
@@ -403,6 +470,7 @@ def _fast_solve_dev(facs, b, config: RegressionConfig, caches, trace: FastSolveT
         eps_two = eps_one / (2.0 + eps_one)
         delta_n = config.delta / (2.0 * n_factors)
         eps_jl = 4.0 * math.log1p(config.eps / 4.0) / n_factors
+        tildes, gts = [], []
         for n, a in enumerate(facs):
             s_n = math.ceil(alpha * spectral_sample_count(int(a.shape[1]), eps_two, delta_n))
             if s_n >= int(a.shape[0]):
@@ -412,14 +480,14 @@ def _fast_solve_dev(facs, b, config: RegressionConfig, caches, trace: FastSolveT
                            / math.sqrt(1.0 - eps_two)).contiguous()
             if trace is not None:
                 trace.a_tilde_rows.append(int(a_tilde.shape[0]))
-            gt = _gram_dev(a_tilde)
-            v, w, _ = _factor_gram_dev(gt)
-            grams.append((v, w))
-            # gram_tilde^-1 = V diag(1/w) V^T from the eigendecomposition the preconditioner needs
-            # anyway (the reference solves with LU, leverage.py:114-119; an exactly zero
-            # eigenvalue <=> an exactly singular Gram raises the same NumericalFailureError)
-            gi = _inverse_from_eig(v, w)
-            scores.append(_jl_scores_dev(a, a_tilde, gi, eps_jl, seeds[2 * n + 1], config.jl_log_factor))
+            tildes.append(a_tilde)
+            gts.append(_gram_dev(a_tilde))
+        # The preconditioner's eigendecompositions (solvers.py:440, 446) run on a side stream,
+        # overlapped with the JL estimates, sampling and sketch construction; joined before the
+        # Richardson loop.
+        grams = _factor_grams_async(gts)
+        for n, a in enumerate(facs):
+            scores.append(_jl_scores_chol(a, tildes[n], gts[n], eps_jl, seeds[2 * n + 1], config.jl_log_factor))
             afs.append(1.0 + eps_jl / 2.0)
     from . import leverage as _lev
     _lev._DEFER_CHECKS[0] = True
@@ -427,8 +495,6 @@ def _fast_solve_dev(facs, b, config: RegressionConfig, caches, trace: FastSolveT
         sampler = ProductSampler([LeverageScores(sc, 0.0, af) for sc, af in zip(scores, afs)])
     finally:
         _lev._DEFER_CHECKS[0] = False
-    eig = reduce(torch.kron, [w for _, w in grams])
-    dinv = pseudo_reciprocal(eig + lam)
     state, inc = pcg64_state(seeds[-1])
     draws = sampler._sample_dev(s, state, inc)
     w = sampler._weights_dev(draws, s)
@@ -448,6 +514,9 @@ def _fast_solve_dev(facs, b, config: RegressionConfig, caches, trace: FastSolveT
     _lib.call("ks_sketched_transpose_apply", ctypes.byref(view.struct), D.p(bv), D.p(view.perm_arg()), D.p(rhs),
               D.stream())
     # preconditioner in grouped (left | right) order
+    grams = _join_grams(grams)
+    eig = reduce(torch.kron, [w for _, w in grams])
+    dinv = pseudo_reciprocal(eig + lam)
     left, right = view.part.left, view.part.right
     VL = reduce(torch.kron, [grams[i][0] for i in left]) if left else torch.ones(1, 1, dtype=D.F64,
                                                                                  device=D.dev())

@@ -73,3 +73,20 @@ if "--loop" in sys.argv:
     print("loop us (identity precond):", timed(eyeL, eyeR, ones, li["rhs"]), "iters", it.value)
     _lib.load().ks_debug_richardson_phases(it.value, ph)
     print("  phases:", [round(v) for v in ph])
+
+if "--cta" in sys.argv:
+    nct = torch.cuda.get_device_properties(0).multi_processor_count
+    buf = (ctypes.c_uint64 * (9 * nct))()
+    _lib.load().ks_debug_richardson_cta_stamps.argtypes = [ctypes.c_int32, ctypes.c_void_p]
+    assert _lib.load().ks_debug_richardson_cta_stamps(nct, buf) == 0
+    ts = np.array(list(buf), dtype=np.float64).reshape(nct, 9)
+    t0 = ts[:, 0].min()
+    ts = (ts - t0) / 1e3
+    names = ["apply_start", "apply_end", "sync1_out", "reduce_end", "sync2_out", "precA_end", "sync3_out",
+             "precB_end", "sync4_out"]
+    for k, nm in enumerate(names):
+        col = ts[:, k]
+        print(f"{nm:12s} min {col.min():8.2f} us  median {np.median(col):8.2f}  max {col.max():8.2f}  argmax {col.argmax()}")
+    dur = ts[:, 1] - ts[:, 0]
+    print("apply duration: min %.2f median %.2f max %.2f us" % (dur.min(), np.median(dur), dur.max()))
+    print("slowest CTAs:", np.argsort(-dur)[:8], dur[np.argsort(-dur)[:8]].round(2))
