@@ -102,6 +102,12 @@ int ks_inverse_small(const double* M, int32_t d, double* X, int32_t* info, void*
 int ks_svd_small_batched(const double* M, int32_t batch, int32_t d, double* sigma, double* V,
                          void* stream);
 
+/* Eigen-decomposition of nb (<= 8) symmetric PSD d x d Gram matrices at separate device
+ * addresses, each read as 0.5 (M + M^T) (the symmetrisation before eigh, solvers.py:440-446);
+ * outputs as ks_svd_small_batched: sigma (nb x d, descending) = eigenvalues, V (nb x d x d). */
+int ks_sym_eig_batched(int32_t nb, const double* const* mats, int32_t d, double* sigma, double* V,
+                       void* stream);
+
 /* Thin SVD of A (n x d): U (n x d), sigma (d, descending), V (d x d).  Columns past the
  * numerical rank (sigma <= rank_tol*sigma_max) are zeroed and *rank (host) reports it.
  * Replaces tensor.compact_svd (tensor.py:76-107).  Synchronises the stream. */
@@ -118,11 +124,15 @@ int ks_pcg64_random(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint6
 /* out[i] = Generator.standard_normal() draw i / divisor (ziggurat; tables from the installed
  * NumPy, passed in ki[256] (uint64), wi[256], fi[256] on the device).  Bit-exact with
  * numpy.random.Generator(PCG64).standard_normal except for ulp-level differences of libm
- * log1p/exp in the (rare) tail branch.  Replaces the host draw of leverage.py:124-126. */
+ * log1p/exp in the (rare) tail branch.  Replaces the host draw of leverage.py:124-126.
+ * status: optional device int32 (zeroed by the caller).  When given and count <= 2^25 the call
+ * is fully asynchronous and chain-resolution failures are OR-ed into *status (nonzero = the
+ * draw is invalid, KS_ENUMERICAL); otherwise the call synchronises the stream and returns
+ * KS_ENUMERICAL itself. */
 int ks_pcg64_standard_normal(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
                              uint64_t inc_lo, int64_t count, double divisor,
                              const uint64_t* ki, const double* wi, const double* fi,
-                             double* out, void* stream);
+                             double* out, int32_t* status, void* stream);
 
 /* ---------------------------------------------------------------- leverage scores & sampling */
 
@@ -224,6 +234,10 @@ int ks_richardson_sketched(const ks_sketch_view* sk, const double* VL, const dou
 /* Profiling aid: per-CTA %globaltimer stamps (ns) of iteration 5 of the last persistent
  * Richardson run, 9 per CTA (phase boundaries and grid-barrier exits). */
 int ks_debug_richardson_cta_stamps(int32_t nctas, uint64_t* out);
+
+/* Profiling aid: globaltimer stamps (ns) of CTA 0 of the last ks_jl_projection: entry,
+ * operands staged, Cholesky done, exit. */
+int ks_debug_jl_projection_stamps(uint64_t* out4);
 
 /* Profiling aid: sweeps used by the last one-sided Jacobi launch (first 8 problems, host out8). */
 int ks_debug_jacobi_sweeps(int32_t* out8);

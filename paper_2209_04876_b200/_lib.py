@@ -48,11 +48,13 @@ _SIGS = {
     "ks_qr_r": ([_p, _i64, _i32, _p, _p], ctypes.c_int),
     "ks_svd_small": ([_p, _i32, _p, _p, _p], ctypes.c_int),
     "ks_svd_small_batched": ([_p, _i32, _i32, _p, _p, _p], ctypes.c_int),
+    "ks_debug_jl_projection_stamps": ([_p], ctypes.c_int),
+    "ks_sym_eig_batched": ([_i32, _p, _i32, _p, _p, _p], ctypes.c_int),
     "ks_compact_svd": ([_p, _i64, _i32, _d, _p, _p, _p, POINTER(c_int32), _p], ctypes.c_int),
     "ks_inverse_small": ([_p, _i32, _p, _p, _p], ctypes.c_int),
     "ks_pcg64_random": ([c_uint64, c_uint64, c_uint64, c_uint64, c_uint64, _i64, _p, _p], ctypes.c_int),
     "ks_pcg64_standard_normal": ([c_uint64, c_uint64, c_uint64, c_uint64, _i64, _d, _p, _p, _p, _p,
-                                  _p], ctypes.c_int),
+                                  _p, _p], ctypes.c_int),
     "ks_jl_scores": ([_p, _i64, _i32, _p, _i32, _d, _p, _p], ctypes.c_int),
     "ks_jl_projection": ([_p, _i32, _p, _i32, _d, _p, _p, _p], ctypes.c_int),
     "ks_debug_jacobi_sweeps": ([_p], ctypes.c_int),

@@ -20,8 +20,21 @@ import numpy as np
 MASK64 = (1 << 64) - 1
 
 
+_SS_STATES: dict = {}
+
+
 def pcg64_state(seed):
     """(state, inc) of ``np.random.default_rng(seed)``'s PCG64 as Python ints."""
+    if isinstance(seed, np.random.SeedSequence) and isinstance(seed.entropy, int):
+        # pure function of the sequence's identity (entropy, spawn key, pool size): memoised
+        key = (seed.entropy, tuple(seed.spawn_key), seed.pool_size, seed.n_children_spawned)
+        got = _SS_STATES.get(key)
+        if got is None:
+            if len(_SS_STATES) > 1024:
+                _SS_STATES.clear()
+            st = np.random.PCG64(seed).state["state"]
+            got = _SS_STATES[key] = (int(st["state"]), int(st["inc"]))
+        return got
     if isinstance(seed, np.random.Generator):
         bg = seed.bit_generator
     elif isinstance(seed, np.random.BitGenerator):

@@ -91,6 +91,10 @@ __device__ __forceinline__ void ks_cp_async8(void* dst, const void* src, bool va
   const int n = valid ? 8 : 0;
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(n) : "memory");
 }
+__device__ __forceinline__ void ks_cp_async4(void* dst, const void* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src) : "memory");
+}
 __device__ __forceinline__ void ks_cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 __host__ __device__ __forceinline__ int64_t ks_min64(int64_t a, int64_t b) { return a < b ? a : b; }

@@ -4,44 +4,59 @@
 //   inverse-CDF draws (leverage.py:193-201, Generator.choice) and sketch weights (:208-232).
 #include "ks_common.cuh"
 #include "ks_pairwise.cuh"
+#include "ks_tma.cuh"
 
 namespace {
 
 // ---------------------------------------------------------------- JL scores
-// One block = 64 rows; Q (r x d) and the rows staged in padded shared memory.
+// One block = 64 rows: P = A_blk Q^T on FP64 tensor cores (DMMA m16n8k4, 8 warps = 4 row tiles x
+// 2 column-tile phases), scores = row sums of P^2 in the accumulator epilogue.  Q (r x d) and the
+// rows are staged in padded shared memory with asynchronous copies (zero-filled padding).
 constexpr int JL_ROWS = 64;
 __global__ void __launch_bounds__(256) jl_scores_kernel(const double* __restrict__ A, int64_t n, int d,
                                                        const double* __restrict__ Q, int r,
                                                        double denom, double* __restrict__ scores) {
   extern __shared__ double sm[];
-  const int ld = d + 1;
-  double* Qs = sm;                   // r x ld
-  double* As = sm + (size_t)r * ld;  // JL_ROWS x ld
+  const int dp = (d + 3) & ~3, ld = dp + 4, rp = (r + 7) & ~7;
+  double* Qs = sm;                    // rp x ld
+  double* As = sm + (size_t)rp * ld;  // JL_ROWS x ld
+  double* red = As + JL_ROWS * ld;    // 2 x JL_ROWS
   const int tid = threadIdx.x;
   const int64_t row0 = (int64_t)blockIdx.x * JL_ROWS;
-  for (int e = tid; e < r * d; e += 256) {
-    const int j = e / d, k = e - j * d;
-    Qs[j * ld + k] = Q[e];
+  for (int e = tid; e < rp * dp; e += 256) {
+    const int j = e / dp, k = e - j * dp;
+    const bool ok = j < r && k < d;
+    ks_cp_async8(&Qs[j * ld + k], ok ? Q + (size_t)j * d + k : Q, ok);
   }
-  for (int e = tid; e < JL_ROWS * d; e += 256) {
-    const int i = e / d, k = e - i * d;
-    const int64_t gi = row0 + i;
-    As[i * ld + k] = gi < n ? A[gi * d + k] : 0.0;
+  for (int e = tid; e < JL_ROWS * dp; e += 256) {
+    const int i = e / dp, k = e - i * dp;
+    const bool ok = row0 + i < n && k < d;
+    ks_cp_async8(&As[i * ld + k], ok ? A + (row0 + i) * d + k : A, ok);
+  }
+  ks_cp_async_wait_all();
+  __syncthreads();
+  const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  const int m0 = (warp & 3) * 16;
+  const double* a_lo = As + (m0 + g) * ld + t;
+  const double* a_hi = a_lo + 8 * ld;
+  double rs0 = 0.0, rs1 = 0.0;
+  for (int n0 = (warp >> 2) * 8; n0 < rp; n0 += 16) {
+    const double* q = Qs + (n0 + g) * ld + t;
+    double c[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int k0 = 0; k0 < dp; k0 += 4) dmma_16x8x4(c, a_lo[k0], a_hi[k0], q[k0]);
+    rs0 = fma(c[0], c[0], fma(c[1], c[1], rs0));
+    rs1 = fma(c[2], c[2], fma(c[3], c[3], rs1));
+  }
+  rs0 += __shfl_xor_sync(0xffffffffu, rs0, 1);
+  rs0 += __shfl_xor_sync(0xffffffffu, rs0, 2);
+  rs1 += __shfl_xor_sync(0xffffffffu, rs1, 1);
+  rs1 += __shfl_xor_sync(0xffffffffu, rs1, 2);
+  if (t == 0) {
+    red[(warp >> 2) * JL_ROWS + m0 + g] = rs0;
+    red[(warp >> 2) * JL_ROWS + m0 + g + 8] = rs1;
   }
   __syncthreads();
-  const int i = tid >> 2, sub = tid & 3;
-  double acc = 0.0;
-  const double* a = As + i * ld;
-  for (int j = sub; j < r; j += 4) {
-    const double* q = Qs + j * ld;
-    double z = 0.0;
-    for (int k = 0; k < d; k++) z = fma(a[k], q[k], z);
-    acc = fma(z, z, acc);
-  }
-  acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-  acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-  const int64_t gi = row0 + i;
-  if (sub == 0 && gi < n) scores[gi] = acc / denom;
+  if (tid < JL_ROWS && row0 + tid < n) scores[row0 + tid] = (red[tid] + red[JL_ROWS + tid]) / denom;
 }
 
 __global__ void row_weighted_sumsq_kernel(const double* __restrict__ U, int64_t n, int d,
@@ -91,7 +106,7 @@ extern "C" int ks_jl_scores(const double* A, int64_t n, int32_t d, const double*
   cudaStream_t st = (cudaStream_t)stream;
   KS_REQUIRE(d >= 1 && d <= 128 && r >= 1 && r <= 256, KS_ESIZE, "jl_scores: unsupported d=%d r=%d", d, r);
   if (n <= 0) return KS_OK;
-  const size_t smem = sizeof(double) * (size_t)(r + JL_ROWS) * (d + 1);
+  const size_t smem = sizeof(double) * ((size_t)(((r + 7) & ~7) + JL_ROWS) * (((d + 3) & ~3) + 4) + 2 * JL_ROWS);
   KS_REQUIRE(smem <= 220 * 1024, KS_ESIZE, "jl_scores: shared memory too large");
   KS_TRY_CUDA(cudaFuncSetAttribute(jl_scores_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   jl_scores_kernel<<<ceil_div_u(n, JL_ROWS), 256, smem, st>>>(A, n, d, Q, r, denom, scores);

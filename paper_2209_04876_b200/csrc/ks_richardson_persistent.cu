@@ -498,6 +498,103 @@ __global__ void transpose_sq_kernel2(const double* __restrict__ a, int d, double
   out[j * d + i] = a[e];
 }
 
+// Work plan on the device (no host round trip): left rows are cut into groups of CH_ROWS, a
+// group's samples into pieces of <= CH_S (one chunk each); chunks go to CTAs in contiguous
+// ranges of nearly equal estimated cost (chunk c goes to the first CTA b whose cost target
+// total * (b+1) / G exceeds the chunk's cost midpoint).  Costs are integers, so the plan is
+// exact and deterministic.  One block.
+constexpr int PLAN_T = 1024;
+__global__ void __launch_bounds__(PLAN_T) plan_kernel(const int64_t* __restrict__ seg, int64_t ul, int G,
+                                                      int64_t wrow, int64_t wsamp, Chunk* __restrict__ chunks,
+                                                      int64_t* __restrict__ cprefix, int64_t* __restrict__ range,
+                                                      int64_t* __restrict__ nchunks) {
+  __shared__ int64_t wsum_p[32], wsum_c[32];
+  __shared__ int64_t carry_p, carry_c;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int64_t ngroups = (ul + CH_ROWS - 1) / CH_ROWS;
+  if (tid == 0) carry_p = carry_c = 0;
+  __syncthreads();
+  for (int64_t g0 = 0; g0 < ngroups; g0 += PLAN_T) {
+    const int64_t gidx = g0 + tid;
+    int64_t pieces = 0, cost = 0, sb = 0, se = 0, ub = 0, ue = 0;
+    if (gidx < ngroups) {
+      ub = gidx * CH_ROWS;
+      ue = min(ul, ub + CH_ROWS);
+      sb = seg[ub];
+      se = seg[ue];
+      pieces = max((int64_t)1, (se - sb + CH_S - 1) / CH_S);
+      cost = pieces * wrow + (se - sb) * wsamp;
+    }
+    // block-wide inclusive scans of (pieces, cost)
+    int64_t vp = pieces, vc = cost;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t tp = __shfl_up_sync(0xffffffffu, vp, o), tc = __shfl_up_sync(0xffffffffu, vc, o);
+      if (lane >= o) { vp += tp; vc += tc; }
+    }
+    if (lane == 31) { wsum_p[wid] = vp; wsum_c[wid] = vc; }
+    __syncthreads();
+    if (wid == 0) {
+      int64_t tp = wsum_p[lane], tc = wsum_c[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int64_t up = __shfl_up_sync(0xffffffffu, tp, o), uc = __shfl_up_sync(0xffffffffu, tc, o);
+        if (lane >= o) { tp += up; tc += uc; }
+      }
+      wsum_p[lane] = tp;
+      wsum_c[lane] = tc;
+    }
+    __syncthreads();
+    const int64_t ip = vp + (wid ? wsum_p[wid - 1] : 0) + carry_p;
+    const int64_t ic = vc + (wid ? wsum_c[wid - 1] : 0) + carry_c;
+    if (gidx < ngroups) {
+      int64_t c = ip - pieces, acc = ic - cost;
+      for (int64_t k = 0; k < pieces; k++, c++) {
+        Chunk ch;
+        ch.t_b = sb + k * CH_S;
+        ch.t_e = min(se, ch.t_b + CH_S);
+        // rows touched by the piece: seg[u] <= t < seg[u + 1]
+        int64_t lo = ub, hi = ue - 1;
+        while (lo < hi) {
+          const int64_t mid = (lo + hi + 1) >> 1;
+          if (seg[mid] <= ch.t_b) lo = mid; else hi = mid - 1;
+        }
+        ch.u_b = lo;
+        lo = ch.u_b; hi = ue - 1;
+        while (lo < hi) {
+          const int64_t mid = (lo + hi + 1) >> 1;
+          if (seg[mid] <= ch.t_e - 1) lo = mid; else hi = mid - 1;
+        }
+        ch.u_e = lo + 1;
+        chunks[c] = ch;
+        const int64_t cc = wrow + (ch.t_e - ch.t_b) * wsamp;
+        cprefix[c] = 2 * acc + cc;  // twice the cost midpoint (integers)
+        acc += cc;
+      }
+    }
+    __syncthreads();
+    if (tid == PLAN_T - 1) { carry_p = ip; carry_c = ic; }
+    __syncthreads();
+  }
+  const int64_t nch = carry_p, total = carry_c;
+  // range[b] = #chunks whose midpoint lies below total * b / G  (2 * mid < 2 * total * b / G)
+  for (int bb = tid; bb <= G; bb += PLAN_T) {
+    int64_t r;
+    if (bb == 0) r = 0;
+    else if (bb == G) r = nch;
+    else {
+      int64_t lo = 0, hi = nch;  // first c with cprefix[c] * G >= 2 * total * bb
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if ((__int128)cprefix[mid] * G < (__int128)2 * total * bb) lo = mid + 1; else hi = mid;
+      }
+      r = lo;
+    }
+    range[bb] = r;
+  }
+  if (tid == 0) *nchunks = nch;
+}
+
 template <int DL, int DR>
 int launch(cudaStream_t st, PArgs& a, int grid) {
   using S = Smem<DL, DR>;
@@ -528,70 +625,22 @@ int richardson_persistent(cudaStream_t st, const ks_sketch_view* sk, const doubl
   KS_REQUIRE(max_iters <= 1024, KS_ESIZE, "persistent loop keeps <= 1024 history entries");
   const int dLp = dL + PAD, dRp = dR + PAD;
   const int64_t nnz = sk->nnz, ul = sk->u_left;
-  std::vector<int64_t> seg(ul + 1);
-  KS_TRY_CUDA(cudaMemcpyAsync(seg.data(), sk->seg, (ul + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  KS_TRY_CUDA(cudaStreamSynchronize(st));
-  // chunks: <= CH_ROWS distinct left rows and <= CH_S samples; heavy rows are split
-  std::vector<Chunk> chunks;
-  std::vector<double> cost;
-  {
-    int64_t u = 0, t = 0;
-    while (t < nnz) {
-      Chunk c;
-      c.u_b = u;
-      c.t_b = t;
-      int64_t te = t, ue = u;
-      while (ue < ul && ue - u < CH_ROWS) {
-        const int64_t row_end = seg[ue + 1];
-        if (row_end - t <= CH_S) {
-          te = row_end;
-          ue++;
-        } else {
-          if (ue == u) {
-            te = t + CH_S;
-            ue = u + 1;
-          }
-          break;
-        }
-      }
-      c.u_e = ue;
-      c.t_e = te;
-      chunks.push_back(c);
-      // DMMA work is fixed per chunk (32-row tiles); samples add the quarter-warp loop
-      cost.push_back(4.0 * CH_ROWS * dL * dR + 24.0 * (double)(te - t) * dR);
-      t = te;
-      u = (te >= seg[ue]) ? ue : ue - 1;
-      while (u < ul && seg[u + 1] <= t) u++;
-    }
-  }
-  const int64_t nch = (int64_t)chunks.size();
-  int grid = num_sms();
-  // contiguous chunk ranges of (nearly) equal cost
-  std::vector<int64_t> range(grid + 1, nch);
-  {
-    double total = 0.0;
-    for (double c : cost) total += c;
-    range[0] = 0;
-    double acc = 0.0;
-    int64_t c = 0;
-    for (int bb = 1; bb < grid; bb++) {
-      const double target = total * bb / grid;
-      while (c < nch && acc + 0.5 * cost[c] < target) acc += cost[c++];
-      range[bb] = c;
-    }
-    range[grid] = nch;
-  }
+  const int grid = num_sms();
+  const int64_t cap = (ul + CH_ROWS - 1) / CH_ROWS + nnz / CH_S + 2;  // >= chunk count
   Scratch<double> Lpack(ul * dLp + 2, st), Rpack(nnz * dRp + 2, st), part((int64_t)grid * dL * dR, st);
   Scratch<double> R((int64_t)dL * dR, st), T((int64_t)dL * dR, st), stepb((int64_t)dL * dR, st), rowsq(dL, st);
   Scratch<double> VRt((int64_t)dR * dR, st);
-  Scratch<Chunk> dch(nch + 1, st);
-  Scratch<int64_t> drange(grid + 1, st);
+  Scratch<Chunk> dch(cap, st);
+  Scratch<int64_t> cpre(cap, st), drange(grid + 2, st);
   Scratch<int> state(4, st);
   KS_REQUIRE(Lpack.p && Rpack.p && part.p && R.p && T.p && stepb.p && rowsq.p && VRt.p && dch.p && drange.p &&
-                 state.p,
+                 cpre.p && state.p,
              KS_ECUDA, "scratch allocation failed");
-  KS_TRY_CUDA(cudaMemcpyAsync(dch.p, chunks.data(), nch * sizeof(Chunk), cudaMemcpyHostToDevice, st));
-  KS_TRY_CUDA(cudaMemcpyAsync(drange.p, range.data(), (grid + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  // estimated chunk cost: DMMA work is fixed per chunk (CH_ROWS-row tiles), samples add the
+  // half-warp dot/axpy loop
+  plan_kernel<<<1, PLAN_T, 0, st>>>(sk->seg, ul, grid, (int64_t)4 * CH_ROWS * dL * dR, (int64_t)24 * dR, dch.p,
+                                     cpre.p, drange.p, drange.p + grid + 1);
+  KS_CHECK_LAUNCH();
   pack_rows_kernel<<<ceil_div_u(ul * dLp, 256), 256, 0, st>>>(sk->Lmat, sk->ldl, sk->lrow, ul, dL, dLp, nullptr,
                                                                Lpack.p);
   KS_CHECK_LAUNCH();

@@ -144,86 +144,110 @@ __global__ void zig_eval_kernel(const uint64_t* __restrict__ raw, int64_t M, int
 
 constexpr int ZL = 128;  // chunk length (positions)
 constexpr int ZK = 16;   // entry offsets tracked per chunk
-constexpr int ZCB = 128; // chunks per block of the chunk / emit kernels
+constexpr int ZCB = 32;  // chunks per block of the chunk / emit kernels
+constexpr int ZS = 32;   // chunks per super-chunk (ZCB % ZS == 0)
+constexpr int ZT = 256;  // threads of the compose / emit kernels
+constexpr int ZCT = 4;   // threads per chunk in the chunk kernel (ZK / ZCT offsets each)
+
+// Stage the consumption table of positions [blk_beg, blk_beg + ZCB*ZL) into shared memory with
+// 16-byte asynchronous copies (all in flight at once); positions >= M read as 1.
+__device__ __forceinline__ void zig_stage_cons(int16_t* sc, const int16_t* __restrict__ cons, int64_t M,
+                                               int64_t blk_beg) {
+  constexpr int V = 8;  // int16 per 16-byte copy
+  for (int i = threadIdx.x; i < ZCB * ZL / V; i += blockDim.x) {
+    const int64_t p = blk_beg + (int64_t)i * V;
+    if (p + V <= M) {
+      const unsigned d = (unsigned)__cvta_generic_to_shared(sc + i * V);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(cons + p) : "memory");
+    } else {
+      for (int v = 0; v < V; v++) sc[i * V + v] = (p + v < M) ? cons[p + v] : (int16_t)1;
+    }
+  }
+  ks_cp_async_wait_all();
+  __syncthreads();
+}
 
 // For each chunk and entry offset o < ZK: exit offset into the next chunk and normals emitted.
-__global__ void zig_chunk_kernel(const int16_t* __restrict__ cons, int64_t M, int64_t nchunks,
-                                 uint8_t* __restrict__ exit_off, int32_t* __restrict__ cnt,
-                                 int32_t* __restrict__ err) {
-  // stage the block's consumption table in shared memory (coalesced), then walk from smem
-  __shared__ int16_t sc[ZCB * ZL];
+__global__ void __launch_bounds__(ZCB * ZCT) zig_chunk_kernel(const int16_t* __restrict__ cons, int64_t M,
+                                                       int64_t nchunks, uint8_t* __restrict__ exit_off,
+                                                       int32_t* __restrict__ cnt, int32_t* __restrict__ err) {
+  __shared__ __align__(16) int16_t sc[ZCB * ZL];
   const int64_t blk_beg = (int64_t)blockIdx.x * ZCB * ZL;
-  for (int i = threadIdx.x; i < ZCB * ZL; i += blockDim.x) {
-    const int64_t p = blk_beg + i;
-    sc[i] = (p < M) ? cons[p] : (int16_t)1;
-  }
-  __syncthreads();
-  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= nchunks) return;
-  const int64_t beg = c * ZL, end = ks_min64(M, beg + ZL);
-#define cons(q) sc[(q) - blk_beg]
-  uint64_t mask[ZL / 64] = {0, 0};
-  int64_t q = beg;
-  int c0 = 0;
+  zig_stage_cons(sc, cons, M, blk_beg);
+  // ZCT threads per chunk, ZK / ZCT entry offsets each (each walks offset 0 for the merge mask)
+  const int lc = threadIdx.x / ZCT, part = threadIdx.x % ZCT;
+  const int64_t c = (int64_t)blockIdx.x * ZCB + lc;
+  if (lc >= ZCB || c >= nchunks) return;
+  const int beg = lc * ZL;
+  const int end = (int)ks_min64(M - blk_beg, beg + ZL);
+  uint64_t m0 = 0, m1 = 0;
+  int q = beg, c0 = 0;
   while (q < end) {
-    const int k = cons(q);
+    const int k = sc[q];
     if (k <= 0) { atomicOr(err, 1); return; }
-    mask[(q - beg) >> 6] |= 1ull << ((q - beg) & 63);
+    const int rel = q - beg;
+    if (rel < 64) m0 |= 1ull << rel; else m1 |= 1ull << (rel - 64);
     c0++;
     q += k;
   }
-  const int e0 = (int)(q - end);
+  const int e0 = q - end;
   if (e0 >= ZK) { atomicOr(err, 2); return; }
-  exit_off[c * ZK] = (uint8_t)e0;
-  cnt[c * ZK] = c0;
-  for (int o = 1; o < ZK; o++) {
-    int64_t qq = beg + o;
-    int steps = 0;
-    while (qq < end && !((mask[(qq - beg) >> 6] >> ((qq - beg) & 63)) & 1)) {
-      const int k = cons(qq);
+  for (int o = part * (ZK / ZCT); o < (part + 1) * (ZK / ZCT); o++) {
+    int qq = beg + o, steps = 0;
+    for (;;) {
+      if (qq >= end) break;
+      const int rel = qq - beg;
+      const bool on0 = rel < 64 ? ((m0 >> rel) & 1) : ((m1 >> (rel - 64)) & 1);
+      if (on0) break;
+      const int k = sc[qq];
       if (k <= 0) { atomicOr(err, 1); return; }
       steps++;
       qq += k;
     }
     if (qq >= end) {
-      const int e = (int)(qq - end);
+      const int e = qq - end;
       if (e >= ZK) { atomicOr(err, 2); return; }
       exit_off[c * ZK + o] = (uint8_t)e;
       cnt[c * ZK + o] = steps;
     } else {
       // merged with the offset-0 walk at qq: remaining count = walk-0 positions >= qq
-      const int rel = (int)(qq - beg);
-      int before = 0;
-      if (rel >= 64) before = __popcll(mask[0]) + __popcll(mask[1] & ((1ull << (rel - 64)) - 1));
-      else before = __popcll(mask[0] & ((rel == 0) ? 0ull : ((1ull << rel) - 1)));
+      const int rel = qq - beg;
+      const int before = rel >= 64 ? __popcll(m0) + __popcll(m1 & ((1ull << (rel - 64)) - 1))
+                                   : __popcll(m0 & ((1ull << rel) - 1));
       exit_off[c * ZK + o] = (uint8_t)e0;
       cnt[c * ZK + o] = steps + (c0 - before);
     }
   }
-#undef cons
 }
 
-constexpr int ZS = 16;  // chunks per super-chunk
-
-// Compose the maps of ZS consecutive chunks into one super-chunk map.
-__global__ void zig_compose_kernel(const uint8_t* __restrict__ exit_off, const int32_t* __restrict__ cnt,
-                                   int64_t nchunks, int64_t nsuper, uint8_t* __restrict__ sexit,
-                                   int32_t* __restrict__ scnt) {
-  const int64_t sidx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+// Compose the maps of ZS consecutive chunks into one super-chunk map.  One block covers
+// ZT / ZK super-chunks; their chunk maps are staged in shared memory first.
+__global__ void __launch_bounds__(ZT) zig_compose_kernel(const uint8_t* __restrict__ exit_off,
+                                                         const int32_t* __restrict__ cnt, int64_t nchunks,
+                                                         int64_t nsuper, uint8_t* __restrict__ sexit,
+                                                         int32_t* __restrict__ scnt) {
+  constexpr int SB = ZT / ZK;  // super-chunks per block
+  __shared__ __align__(16) uint8_t se[SB * ZS * ZK];
+  __shared__ int32_t sn[SB * ZS * ZK];
+  const int64_t cb = (int64_t)blockIdx.x * SB * ZS;  // first chunk of the block
+  const int64_t nc = ks_min64(nchunks - cb, SB * ZS);
+  for (int i = threadIdx.x; i < nc * ZK; i += ZT) ks_cp_async4(&sn[i], cnt + cb * ZK + i);
+  for (int i = threadIdx.x; i < nc * ZK / 4; i += ZT) ks_cp_async4(&se[4 * i], exit_off + cb * ZK + 4 * i);
+  ks_cp_async_wait_all();
+  __syncthreads();
+  const int ls = threadIdx.x / ZK, o = threadIdx.x % ZK;
+  const int64_t sidx = (int64_t)blockIdx.x * SB + ls;
   if (sidx >= nsuper) return;
-  const int64_t c_beg = sidx * ZS, c_end = ks_min64(nchunks, c_beg + ZS);
-  for (int o = 0; o < ZK; o++) {
-    int e = o;
-    int32_t k = 0;
-    for (int64_t c = c_beg; c < c_end; c++) {
-      k += cnt[c * ZK + e];
-      e = exit_off[c * ZK + e];
-    }
-    sexit[sidx * ZK + o] = (uint8_t)e;
-    scnt[sidx * ZK + o] = k;
+  const int c_end = (int)ks_min64(nc, (ls + 1) * ZS);
+  int e = o;
+  int32_t k = 0;
+  for (int c = ls * ZS; c < c_end; c++) {
+    k += sn[c * ZK + e];
+    e = se[c * ZK + e];
   }
+  sexit[sidx * ZK + o] = (uint8_t)e;
+  scnt[sidx * ZK + o] = k;
 }
-
 // One block: exclusive prefix of the super-chunk maps applied to entry offset 0
 // (sequential per thread over a contiguous range, Hillis-Steele across threads).
 constexpr int ZSCAN_T = 512;
@@ -239,6 +263,7 @@ __global__ void __launch_bounds__(ZSCAN_T) zig_scan_kernel(const uint8_t* __rest
   const int t = threadIdx.x;
   const int64_t per = (nsuper + ZSCAN_T - 1) / ZSCAN_T;
   const int64_t c_beg = ks_min64(nsuper, t * per), c_end = ks_min64(nsuper, c_beg + per);
+#pragma unroll
   for (int o = 0; o < ZK; o++) {
     int e = o;
     int64_t k = 0;
@@ -252,15 +277,24 @@ __global__ void __launch_bounds__(ZSCAN_T) zig_scan_kernel(const uint8_t* __rest
   __syncthreads();
   int cur = 0;
   for (int off = 1; off < ZSCAN_T; off <<= 1) {
+    // gather all ZK compositions into registers first (independent loads overlap), then store
+    int ne[ZK];
+    int64_t nk[ZK];
+#pragma unroll
     for (int o = 0; o < ZK; o++) {
       if (t >= off) {
         const int mid = fe[cur][o][t - off];
-        fe[cur ^ 1][o][t] = fe[cur][mid][t];
-        fc[cur ^ 1][o][t] = fc[cur][o][t - off] + fc[cur][mid][t];
+        ne[o] = fe[cur][mid][t];
+        nk[o] = fc[cur][o][t - off] + fc[cur][mid][t];
       } else {
-        fe[cur ^ 1][o][t] = fe[cur][o][t];
-        fc[cur ^ 1][o][t] = fc[cur][o][t];
+        ne[o] = fe[cur][o][t];
+        nk[o] = fc[cur][o][t];
       }
+    }
+#pragma unroll
+    for (int o = 0; o < ZK; o++) {
+      fe[cur ^ 1][o][t] = ne[o];
+      fc[cur ^ 1][o][t] = nk[o];
     }
     __syncthreads();
     cur ^= 1;
@@ -276,46 +310,84 @@ __global__ void __launch_bounds__(ZSCAN_T) zig_scan_kernel(const uint8_t* __rest
   if (t == ZSCAN_T - 1) *total = fc[cur][0][t];
 }
 
-// Per super-chunk: entry offsets and output bases of its chunks.
-__global__ void zig_expand_kernel(const uint8_t* __restrict__ exit_off, const int32_t* __restrict__ cnt,
-                                  int64_t nchunks, int64_t nsuper, const uint8_t* __restrict__ sentry,
-                                  const int64_t* __restrict__ sbase, uint8_t* __restrict__ entry,
-                                  int64_t* __restrict__ base) {
-  const int64_t sidx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (sidx >= nsuper) return;
-  const int64_t c_beg = sidx * ZS, c_end = ks_min64(nchunks, c_beg + ZS);
-  int e = sentry[sidx];
-  int64_t k = sbase[sidx];
-  for (int64_t c = c_beg; c < c_end; c++) {
-    entry[c] = (uint8_t)e;
-    base[c] = k;
-    k += cnt[c * ZK + e];
-    e = exit_off[c * ZK + e];
-  }
-}
 
-__global__ void zig_emit_kernel(const int16_t* __restrict__ cons, const double* __restrict__ val,
-                                int64_t M, int64_t nchunks, const uint8_t* __restrict__ entry,
-                                const int64_t* __restrict__ base, int64_t count, double divisor,
-                                double* __restrict__ out, int64_t* __restrict__ consumed) {
-  __shared__ int16_t sc[ZCB * ZL];
+// Emit the chain: per block of ZCB chunks, (1) chunk entry offsets / output bases from the
+// super-chunk prefix (ZCB / ZS sequential walks over shared-memory maps), (2) one walk per chunk
+// marking its chain positions in a 128-bit mask, (3) every position writes its value to
+// base + rank-in-chunk (coalesced reads of val, near-contiguous writes of out).
+__global__ void __launch_bounds__(ZT) zig_emit_kernel(const int16_t* __restrict__ cons,
+                                                      const double* __restrict__ val, int64_t M, int64_t nchunks,
+                                                      const uint8_t* __restrict__ exit_off,
+                                                      const int32_t* __restrict__ cnt,
+                                                      const uint8_t* __restrict__ sentry,
+                                                      const int64_t* __restrict__ sbase, int64_t count,
+                                                      double divisor, double* __restrict__ out,
+                                                      int64_t* __restrict__ consumed,
+                                                      const int64_t* __restrict__ total, int32_t* __restrict__ err) {
+  if (blockIdx.x == 0 && threadIdx.x == 0 && *total < count) atomicOr(err, 4);  // position budget exhausted
+  __shared__ __align__(16) int16_t sc[ZCB * ZL];
+  __shared__ __align__(16) uint8_t se[ZCB * ZK];
+  __shared__ int32_t sn[ZCB * ZK];
+  __shared__ uint8_t c_entry[ZCB];
+  __shared__ int64_t c_base[ZCB];
+  __shared__ uint64_t c_mask[ZCB][2];
   const int64_t blk_beg = (int64_t)blockIdx.x * ZCB * ZL;
-  for (int i = threadIdx.x; i < ZCB * ZL; i += blockDim.x) {
-    const int64_t p = blk_beg + i;
-    sc[i] = (p < M) ? cons[p] : (int16_t)1;
+  const int64_t cb = (int64_t)blockIdx.x * ZCB;
+  const int nc = (int)ks_min64(nchunks - cb, ZCB);
+  for (int i = threadIdx.x; i < nc * ZK; i += ZT) ks_cp_async4(&sn[i], cnt + cb * ZK + i);
+  for (int i = threadIdx.x; i < nc * ZK / 4; i += ZT) ks_cp_async4(&se[4 * i], exit_off + cb * ZK + 4 * i);
+  zig_stage_cons(sc, cons, M, blk_beg);  // waits for all copies
+  if (threadIdx.x < ZCB / ZS) {
+    const int s = threadIdx.x;
+    const int64_t sidx = (int64_t)blockIdx.x * (ZCB / ZS) + s;
+    if (s * ZS < nc) {
+      int e = sentry[sidx];
+      int64_t k = sbase[sidx];
+      const int c_end = min(nc, (s + 1) * ZS);
+      for (int c = s * ZS; c < c_end; c++) {
+        c_entry[c] = (uint8_t)e;
+        c_base[c] = k;
+        k += sn[c * ZK + e];
+        e = se[c * ZK + e];
+      }
+    }
   }
   __syncthreads();
-  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= nchunks) return;
-  const int64_t beg = c * ZL, end = ks_min64(M, beg + ZL);
-  int64_t q = beg + entry[c];
-  int64_t k = base[c];
-  while (q < end) {
-    const int step = sc[q - blk_beg];
-    if (k < count) out[k] = val[q] / divisor;
-    if (k == count - 1) *consumed = q + step;
-    k++;
-    q += step;
+  if (threadIdx.x < nc) {
+    const int lc = threadIdx.x;
+    const int beg = lc * ZL, end = (int)ks_min64(M - blk_beg, beg + ZL);
+    uint64_t m0 = 0, m1 = 0;
+    for (int q = beg + c_entry[lc]; q < end;) {
+      const int rel = q - beg;
+      const int step = sc[q];
+      if (step <= 0) break;  // reported by zig_chunk_kernel
+      q += step;
+      if (rel < 64) m0 |= 1ull << rel; else m1 |= 1ull << (rel - 64);
+    }
+    c_mask[lc][0] = m0;
+    c_mask[lc][1] = m1;
+  }
+  __syncthreads();
+  const int npos = (int)ks_min64(M - blk_beg, (int64_t)nc * ZL);
+  constexpr int U = 4;  // positions per thread per pass (their loads are issued together)
+  for (int i0 = threadIdx.x; i0 < npos; i0 += U * ZT) {
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) v[u] = i0 + u * ZT < npos ? val[blk_beg + i0 + u * ZT] : 0.0;
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const int i = i0 + u * ZT;
+      const int lc = i / ZL, rel = i % ZL;
+      if (i >= npos) break;
+      const uint64_t m0 = c_mask[lc][0], m1 = c_mask[lc][1];
+      const bool on = rel < 64 ? ((m0 >> rel) & 1) : ((m1 >> (rel - 64)) & 1);
+      if (!on) continue;
+      const int rank = rel >= 64 ? __popcll(m0) + __popcll(m1 & ((1ull << (rel - 64)) - 1))
+                                 : __popcll(m0 & ((1ull << rel) - 1));
+      const int64_t k = c_base[lc] + rank;
+      if (k < count) out[k] = v[u] / divisor;
+      if (k == count - 1) *consumed = blk_beg + i + sc[i];
+    }
   }
 }
 
@@ -334,13 +406,13 @@ extern "C" int ks_pcg64_random(uint64_t sh, uint64_t sl, uint64_t ih, uint64_t i
 extern "C" int ks_pcg64_standard_normal(uint64_t sh, uint64_t sl, uint64_t ih, uint64_t il,
                                         int64_t count, double divisor, const uint64_t* ki,
                                         const double* wi, const double* fi, double* out,
-                                        void* stream) {
+                                        int32_t* status, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (count <= 0) return KS_OK;
   const int64_t batch_max = (int64_t)1 << 25;
   uint64_t skip = 0;
-  const u128 s0 = mk128(sh, sl);
-  (void)s0;
+  // single batch with a caller status word: no host round trip (errors are OR-ed into *status)
+  const bool async = status != nullptr && count <= batch_max;
   int64_t done = 0;
   while (done < count) {
     const int64_t n = ks_min64(batch_max, count - done);
@@ -357,41 +429,37 @@ extern "C" int ks_pcg64_standard_normal(uint64_t sh, uint64_t sl, uint64_t ih, u
     ks::Scratch<int32_t> scnt(nsuper * ZK, st);
     ks::Scratch<uint8_t> sentry(nsuper, st);
     ks::Scratch<int64_t> sbase(nsuper, st);
-    ks::Scratch<uint8_t> entry(nchunks, st);
-    ks::Scratch<int64_t> base(nchunks + 2, st);  // [nchunks] total, [nchunks+1] consumed
-    ks::Scratch<int32_t> err(1, st);
-    KS_REQUIRE(raw.p && val.p && cons.p && exit_off.p && cnt.p && entry.p && base.p && err.p &&
-               sexit.p && scnt.p && sentry.p && sbase.p,
+    ks::Scratch<int64_t> tail(2, st);  // [0] chain length over M positions, [1] draws consumed
+    ks::Scratch<int32_t> err_s(async ? 0 : 1, st);
+    int32_t* err = async ? status : err_s.p;
+    KS_REQUIRE(raw.p && val.p && cons.p && exit_off.p && cnt.p && tail.p && err && sexit.p && scnt.p &&
+               sentry.p && sbase.p,
                KS_ECUDA, "scratch allocation failed");
-    KS_TRY_CUDA(cudaMemsetAsync(err.p, 0, sizeof(int32_t), st));
+    if (!async) KS_TRY_CUDA(cudaMemsetAsync(err, 0, sizeof(int32_t), st));
     const int64_t rthreads = (limit + RAW_PER_THREAD - 1) / RAW_PER_THREAD;
     pcg_raw_kernel<<<ceil_div_u(rthreads, 256), 256, 0, st>>>(sh, sl, ih, il, skip, limit, raw.p);
     KS_CHECK_LAUNCH();
     zig_eval_kernel<<<ceil_div_u(M, 256), 256, 0, st>>>(raw.p, M, limit, ki, wi, fi, val.p, cons.p);
     KS_CHECK_LAUNCH();
-    zig_chunk_kernel<<<ceil_div_u(nchunks, 128), 128, 0, st>>>(cons.p, M, nchunks, exit_off.p,
-                                                               cnt.p, err.p);
+    const unsigned nblk = ceil_div_u(nchunks, ZCB);
+    zig_chunk_kernel<<<nblk, ZCB * ZCT, 0, st>>>(cons.p, M, nchunks, exit_off.p, cnt.p, err);
     KS_CHECK_LAUNCH();
-    zig_compose_kernel<<<ceil_div_u(nsuper, 128), 128, 0, st>>>(exit_off.p, cnt.p, nchunks, nsuper,
-                                                                 sexit.p, scnt.p);
+    zig_compose_kernel<<<ceil_div_u(nsuper, ZT / ZK), ZT, 0, st>>>(exit_off.p, cnt.p, nchunks, nsuper,
+                                                                   sexit.p, scnt.p);
     KS_CHECK_LAUNCH();
     const size_t scan_smem = (size_t)2 * ZSCAN_T * ZK * (1 + sizeof(int64_t));
     KS_TRY_CUDA(cudaFuncSetAttribute(zig_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)scan_smem));
-    zig_scan_kernel<<<1, ZSCAN_T, scan_smem, st>>>(sexit.p, scnt.p, nsuper, sentry.p, sbase.p,
-                                                   base.p + nchunks);
+    zig_scan_kernel<<<1, ZSCAN_T, scan_smem, st>>>(sexit.p, scnt.p, nsuper, sentry.p, sbase.p, tail.p);
     KS_CHECK_LAUNCH();
-    zig_expand_kernel<<<ceil_div_u(nsuper, 128), 128, 0, st>>>(exit_off.p, cnt.p, nchunks, nsuper,
-                                                                sentry.p, sbase.p, entry.p, base.p);
+    zig_emit_kernel<<<nblk, ZT, 0, st>>>(cons.p, val.p, M, nchunks, exit_off.p, cnt.p, sentry.p, sbase.p, n,
+                                         divisor, out + done, tail.p + 1, tail.p, err);
     KS_CHECK_LAUNCH();
-    zig_emit_kernel<<<ceil_div_u(nchunks, 128), 128, 0, st>>>(cons.p, val.p, M, nchunks, entry.p,
-                                                              base.p, n, divisor, out + done,
-                                                              base.p + nchunks + 1);
-    KS_CHECK_LAUNCH();
+    if (async) break;
     int64_t host[2];
     int32_t herr = 0;
-    KS_TRY_CUDA(cudaMemcpyAsync(host, base.p + nchunks, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    KS_TRY_CUDA(cudaMemcpyAsync(&herr, err.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    KS_TRY_CUDA(cudaMemcpyAsync(host, tail.p, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    KS_TRY_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     KS_TRY_CUDA(cudaStreamSynchronize(st));
     KS_REQUIRE(herr == 0, KS_ENUMERICAL, "ziggurat chain resolution failed (code %d)", herr);
     KS_REQUIRE(host[0] >= n, KS_ENUMERICAL, "ziggurat position budget exhausted");

@@ -4,6 +4,7 @@
 // solvers.factor_gram (solvers.py:143-150).  No host LAPACK is used.
 #include "ks_common.cuh"
 
+#include <cstdlib>
 #include <vector>
 #include <algorithm>
 
@@ -219,6 +220,132 @@ __global__ void jacobi_svd_kernel(const double* __restrict__ M, int d, double* _
   }
 }
 
+// Fixed-size variant (D = 16, 32, 64) of the one-sided Jacobi above: 8 threads per column pair,
+// every loop unrolled, the pair's column slices kept in registers between the dot products and
+// the rotation, constant-width shuffles.  Column j is stored rotated by 8 elements when j is odd
+// so the two pairs sharing a half-warp hit disjoint banks.  SYM: read 0.5 (M + M^T) (the
+// reference symmetrises the Gram before eigh).  Ms: optional per-problem pointers.
+constexpr int JF_G = 8;
+struct MatPtrs {
+  const double* p[8];
+};
+
+template <int D>
+__device__ __forceinline__ int jf_off(int j, int i) {
+  return j * D + ((i + ((j & 1) << 3)) & (D - 1));
+}
+
+template <int D, bool SYM>
+__global__ void __launch_bounds__(D / 2 * JF_G) jacobi_fixed_kernel(MatPtrs Ms, const double* __restrict__ Mc,
+                                                                   double* __restrict__ sigma,
+                                                                   double* __restrict__ Vout) {
+  constexpr int NP = D / 2, NT = NP * JF_G, E = D / JF_G;
+  extern __shared__ double jf_sm[];
+  double* W = jf_sm;
+  double* V = jf_sm + D * D;
+  __shared__ int s_rot;
+  __shared__ int s_order[D];
+  __shared__ double s_norm[D];
+  const double* M = Mc ? Mc + (size_t)blockIdx.x * D * D : Ms.p[blockIdx.x];
+  sigma += (size_t)blockIdx.x * D;
+  Vout += (size_t)blockIdx.x * D * D;
+  const int tid = threadIdx.x;
+  for (int e = tid; e < D * D; e += NT) {
+    const int i = e / D, j = e % D;  // M row i, column j
+    const double m = SYM ? 0.5 * (M[(size_t)i * D + j] + M[(size_t)j * D + i]) : M[(size_t)i * D + j];
+    W[jf_off<D>(j, i)] = m;
+    V[jf_off<D>(j, i)] = (i == j) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  const int group = tid / JF_G, lg = tid % JF_G;
+  const double tol = 2.0 * D * 2.220446049250313e-16;
+  for (int sweep = 0; sweep < 40; sweep++) {
+    if (tid == 0) s_rot = 0;
+    __syncthreads();
+    for (int r = 0; r < D - 1; r++) {
+      auto player = [&](int pos) {
+        int x = pos - 1 + r;
+        if (x >= D - 1) x -= D - 1;
+        return pos == 0 ? 0 : 1 + x;
+      };
+      const int p = player(group), q = player(D - 1 - group);
+      double x[E], y[E];
+#pragma unroll
+      for (int k = 0; k < E; k++) {
+        x[k] = W[jf_off<D>(p, lg + k * JF_G)];
+        y[k] = W[jf_off<D>(q, lg + k * JF_G)];
+      }
+      double a = 0.0, b = 0.0, c = 0.0;
+#pragma unroll
+      for (int k = 0; k < E; k++) {
+        a = fma(x[k], x[k], a);
+        b = fma(y[k], y[k], b);
+        c = fma(x[k], y[k], c);
+      }
+#pragma unroll
+      for (int o = JF_G / 2; o > 0; o >>= 1) {
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+        b += __shfl_xor_sync(0xffffffffu, b, o);
+        c += __shfl_xor_sync(0xffffffffu, c, o);
+      }
+      if (c != 0.0 && a != 0.0 && b != 0.0 && c * c > tol * tol * a * b) {
+        const double zeta = (b - a) * __drcp_rn(2.0 * c);
+        const double az = fabs(zeta);
+        const double tt = __drcp_rn(az + sqrt(fma(az, az, 1.0)));
+        const double t = zeta >= 0.0 ? tt : -tt;
+        const double cs = rsqrt(fma(t, t, 1.0));
+        const double sn = cs * t;
+        double u[E], v[E];
+#pragma unroll
+        for (int k = 0; k < E; k++) {
+          u[k] = V[jf_off<D>(p, lg + k * JF_G)];
+          v[k] = V[jf_off<D>(q, lg + k * JF_G)];
+        }
+#pragma unroll
+        for (int k = 0; k < E; k++) {
+          W[jf_off<D>(p, lg + k * JF_G)] = cs * x[k] - sn * y[k];
+          W[jf_off<D>(q, lg + k * JF_G)] = sn * x[k] + cs * y[k];
+          V[jf_off<D>(p, lg + k * JF_G)] = cs * u[k] - sn * v[k];
+          V[jf_off<D>(q, lg + k * JF_G)] = sn * u[k] + cs * v[k];
+        }
+        if (lg == 0) s_rot = 1;
+      }
+      __syncthreads();
+    }
+    if (tid == 0) g_jacobi_sweeps[blockIdx.x & 7] = sweep + 1;
+    if (s_rot == 0) break;
+    __syncthreads();
+  }
+  for (int j = tid; j < D; j += NT) {
+    double s = 0.0;
+    for (int i = 0; i < D; i++) s = fma(W[jf_off<D>(j, i)], W[jf_off<D>(j, i)], s);
+    s_norm[j] = sqrt(s);
+  }
+  __syncthreads();
+  for (int j = tid; j < D; j += NT) {
+    int rank = 0;
+    const double sj = s_norm[j];
+    for (int k = 0; k < D; k++) {
+      const double sk = s_norm[k];
+      rank += (sk > sj) || (sk == sj && k < j);
+    }
+    s_order[rank] = j;
+  }
+  __syncthreads();
+  for (int k = tid; k < D; k += NT) sigma[k] = s_norm[s_order[k]];
+  for (int e = tid; e < D * D; e += NT) {
+    const int i = e / D, k = e % D;
+    Vout[e] = V[jf_off<D>(s_order[k], i)];
+  }
+}
+
+__global__ void symmetrize_kernel(const double* __restrict__ M, int d, double* __restrict__ out) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)d * d) return;
+  const int64_t i = e / d, j = e - i * d;
+  out[e] = 0.5 * (M[i * d + j] + M[j * d + i]);
+}
+
 // U[:, j] *= 1/sigma[j] for j < rank, zero otherwise (U = A V Sigma^-1, tensor.py:102-107)
 __global__ void scale_cols_kernel(double* U, int64_t n, int d, const double* __restrict__ sigma,
                                   double rank_tol) {
@@ -358,9 +485,33 @@ int qr_r(cudaStream_t st, const double* A, int64_t n, int d, double* R) {
   return KS_OK;
 }
 
+template <int D, bool SYM>
+static void launch_jacobi_fixed(cudaStream_t st, const MatPtrs& Ms, const double* M, double* sigma, double* V,
+                                int batch) {
+  const int smem = 2 * D * D * (int)sizeof(double);
+  cudaFuncSetAttribute(jacobi_fixed_kernel<D, SYM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  jacobi_fixed_kernel<D, SYM><<<batch, D / 2 * JF_G, smem, st>>>(Ms, M, sigma, V);
+}
+
+template <bool SYM>
+static bool jacobi_fixed(cudaStream_t st, const MatPtrs& Ms, const double* M, int d, double* sigma, double* V,
+                         int batch) {
+  if (getenv("KS_JACOBI_GENERIC")) return false;
+  switch (d) {
+    case 16: launch_jacobi_fixed<16, SYM>(st, Ms, M, sigma, V, batch); return true;
+    case 32: launch_jacobi_fixed<32, SYM>(st, Ms, M, sigma, V, batch); return true;
+    case 64: launch_jacobi_fixed<64, SYM>(st, Ms, M, sigma, V, batch); return true;
+    default: return false;
+  }
+}
+
 int svd_small(cudaStream_t st, const double* M, int d, double* sigma, double* V, int batch) {
   KS_REQUIRE(d >= 1 && d <= 128, KS_ESIZE, "svd_small supports 1 <= d <= 128 (got %d)", d);
   if (batch <= 0) return KS_OK;
+  if (jacobi_fixed<false>(st, MatPtrs{}, M, d, sigma, V, batch)) {
+    KS_CHECK_LAUNCH();
+    return KS_OK;
+  }
   const int dp = d + (d & 1);
   const size_t wbytes = (size_t)dp * d * sizeof(double);
   const size_t vbytes = (size_t)dp * dp * sizeof(double);
@@ -404,6 +555,29 @@ extern "C" int ks_qr_r(const double* A, int64_t n, int32_t d, double* R, void* s
 
 extern "C" int ks_svd_small(const double* M, int32_t d, double* sigma, double* V, void* stream) {
   return ks::svd_small((cudaStream_t)stream, M, d, sigma, V, 1);
+}
+
+// Eigen-decomposition of nb symmetric PSD d x d matrices given by separate device pointers,
+// symmetrised as 0.5 (M + M^T) on load; same output contract as ks_svd_small_batched.
+extern "C" int ks_sym_eig_batched(int32_t nb, const double* const* mats, int32_t d, double* sigma, double* V,
+                                  void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  KS_REQUIRE(nb >= 1 && nb <= 8, KS_EINVAL, "1..8 matrices per call");
+  KS_REQUIRE(d >= 1 && d <= 128, KS_ESIZE, "d must be in [1, 128] (got %d)", d);
+  MatPtrs ps{};
+  for (int i = 0; i < nb; i++) ps.p[i] = mats[i];
+  if (ks::jacobi_fixed<true>(st, ps, nullptr, d, sigma, V, nb)) {
+    KS_CHECK_LAUNCH();
+    return KS_OK;
+  }
+  // generic sizes: symmetrise into a contiguous batch, then the generic kernel
+  ks::Scratch<double> sym((int64_t)nb * d * d, st);
+  KS_REQUIRE(sym.p, KS_ECUDA, "scratch allocation failed");
+  for (int i = 0; i < nb; i++) {
+    symmetrize_kernel<<<ceil_div_u((int64_t)d * d, 256), 256, 0, st>>>(mats[i], d, sym.p + (int64_t)i * d * d);
+    KS_CHECK_LAUNCH();
+  }
+  return ks::svd_small(st, sym.p, d, sigma, V, nb);
 }
 
 extern "C" int ks_svd_small_batched(const double* M, int32_t batch, int32_t d, double* sigma, double* V,

@@ -141,6 +141,18 @@ int gemm_tn_tall_dmma(cudaStream_t st, int64_t M, int64_t N, int64_t K, double a
 // =============================================================================================
 namespace {
 
+constexpr int JP_CPW = 2;  // right-hand-side columns per warp and pass
+constexpr int JP_COLS = 16 * JP_CPW;  // columns per CTA (512 threads)
+
+__device__ unsigned long long g_jlp_ts[4];  // globaltimer stamps of CTA 0 (debug)
+__device__ __forceinline__ unsigned long long jlp_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define JLP_STAMP(k) \
+  if (blockIdx.x == 0 && threadIdx.x == 0) g_jlp_ts[k] = jlp_now();
+
 __global__ void __launch_bounds__(512) jl_projection_kernel(const double* __restrict__ G, int d,
                                                             const double* __restrict__ GA, int r, double scale,
                                                             double* __restrict__ Q, int32_t* __restrict__ info) {
@@ -149,68 +161,180 @@ __global__ void __launch_bounds__(512) jl_projection_kernel(const double* __rest
   double* L = sm;                   // d x ld (lower triangle used)
   double* Y = sm + (size_t)d * ld;  // d x r  (right-hand sides, overwritten by the solution)
   __shared__ int s_bad;
-  __shared__ double s_piv;
-  const int tid = threadIdx.x, nt = blockDim.x;
-  for (int e = tid; e < d * d; e += nt) L[(e / d) * ld + (e % d)] = G[e];
+  __shared__ double s_rdiag[64];
+  JLP_STAMP(0)
+  const int tid = threadIdx.x, nt = blockDim.x, tx = tid & 31, ty = tid >> 5, nty = nt >> 5;
+  for (int e = tid; e < d * d; e += nt) ks_cp_async8(&L[(e / d) * ld + (e % d)], G + e);
   for (int e = tid; e < d * r; e += nt) {
     const int k = e / r, c = e - k * r;
-    Y[e] = GA[(size_t)c * d + k];
+    ks_cp_async8(&Y[e], GA + (size_t)c * d + k);
   }
   if (tid == 0) s_bad = 0;
+  ks_cp_async_wait_all();
   __syncthreads();
-  for (int k = 0; k < d; k++) {
-    if (tid == 0) {
+  JLP_STAMP(1)
+  if (d <= 64 && nt == 512) {
+    // Register-resident right-looking LDL^T, one barrier per column: thread t owns column
+    // j = t % 64, rows i = t / 64 + 8m (m < 8).  At step k the owners of column k publish it
+    // (and the pivot owner 1 / d_k) in a double-buffered shared column; everyone then applies
+    // the rank-1 update a_ij -= a_ik (a_jk / d_k) to its own entries.  Square roots are kept off
+    // the serial chain: L = L_unit diag(sqrt(d)) is formed at the end, in parallel.
+    __shared__ double colb[2][64];
+    __shared__ double pivb[2];
+    __shared__ double dg[64];
+    const int j = tid & 63, i0 = tid >> 6;
+    // (s_rdiag: reciprocals of the Cholesky diagonal for the substitutions below)
+    double a[8];
+#pragma unroll
+    for (int m = 0; m < 8; m++) {
+      const int i = i0 + 8 * m;
+      a[m] = (i < d && j < d && j <= i) ? L[i * ld + j] : 0.0;
+    }
+    for (int k = 0; k < d; k++) {
+      const int b = k & 1;
+      if (j == k) {
+#pragma unroll
+        for (int m = 0; m < 8; m++) {
+          const int i = i0 + 8 * m;
+          if (i >= k && i < d) colb[b][i] = a[m];
+          if (i == k) {
+            const double p = a[m];
+            if (!(p > 0.0) && !s_bad) s_bad = k + 1;
+            pivb[b] = p > 0.0 ? 1.0 / p : 1.0;
+            dg[k] = p;
+          }
+        }
+      }
+      __syncthreads();
+      const double rd = pivb[b];
+      if (j == k) {
+#pragma unroll
+        for (int m = 0; m < 8; m++) {
+          const int i = i0 + 8 * m;
+          if (i > k && i < d) a[m] *= rd;
+        }
+      } else if (j > k && j < d) {
+        const double ljk = colb[b][j] * rd;
+#pragma unroll
+        for (int m = 0; m < 8; m++) {
+          const int i = i0 + 8 * m;
+          if (i >= j && i < d) a[m] = fma(-colb[b][i], ljk, a[m]);
+        }
+      }
+    }
+    __syncthreads();
+    if (j < d) {
+      const double dj = dg[j];
+      const double sj = dj > 0.0 ? sqrt(dj) : 1.0;
+      if (i0 == 0) s_rdiag[j] = 1.0 / sj;
+#pragma unroll
+      for (int m = 0; m < 8; m++) {
+        const int i = i0 + 8 * m;
+        if (i < d && j <= i) L[i * ld + j] = (i == j) ? sj : a[m] * sj;
+      }
+    }
+    __syncthreads();
+    JLP_STAMP(2)
+  } else {
+    // right-looking Cholesky, two barriers per column: every thread derives the pivot itself
+    for (int k = 0; k < d; k++) {
       const double p = L[k * ld + k];
-      if (!(p > 0.0) && !s_bad) s_bad = k + 1;
-      s_piv = p > 0.0 ? sqrt(p) : 1.0;
-      L[k * ld + k] = s_piv;
+      const double lkk = p > 0.0 ? sqrt(p) : 1.0;
+      for (int i = k + 1 + tid; i < d; i += nt) L[i * ld + k] /= lkk;
+      __syncthreads();
+      if (tid == 0) {
+        if (!(p > 0.0) && !s_bad) s_bad = k + 1;
+        L[k * ld + k] = lkk;
+      }
+      for (int i = k + 1 + ty; i < d; i += nty) {
+        const double lik = L[i * ld + k];
+        for (int jj = k + 1 + tx; jj <= i; jj += 32) L[i * ld + jj] = fma(-lik, L[jj * ld + k], L[i * ld + jj]);
+      }
+      __syncthreads();
+    }
+  }
+  // L Z = Y, then L^T X = Z.  Right-hand-side columns are independent: for d <= 64 a warp solves
+  // JP_CPW columns at once with the column in registers (lane l owns rows l and l + 32); the
+  // per-element operation order is the textbook one (divide by the pivot, then fma updates).
+  if (d <= 64 && nt == 512) {
+    const int lane = tx, warp = ty;
+    const int c_lo = blockIdx.x * JP_COLS, c_hi = min(r, c_lo + JP_COLS);
+    for (int c0 = c_lo + warp; c0 < c_hi; c0 += nty * JP_CPW) {
+      double y0[JP_CPW], y1[JP_CPW];
+#pragma unroll
+      for (int j = 0; j < JP_CPW; j++) {
+        const int c = c0 + j * nty;
+        y0[j] = (c < c_hi && lane < d) ? Y[lane * r + c] : 0.0;
+        y1[j] = (c < c_hi && lane + 32 < d) ? Y[(lane + 32) * r + c] : 0.0;
+      }
+      for (int k = 0; k < d; k++) {
+        const double rk = s_rdiag[k];
+        const bool u0 = lane > k && lane < d, u1 = lane + 32 > k && lane + 32 < d;
+        const double l0 = u0 ? L[lane * ld + k] : 0.0, l1 = u1 ? L[(lane + 32) * ld + k] : 0.0;
+#pragma unroll
+        for (int j = 0; j < JP_CPW; j++) {
+          const double yk = __shfl_sync(0xffffffffu, k < 32 ? y0[j] : y1[j], k & 31) * rk;
+          if (lane == (k & 31)) { if (k < 32) y0[j] = yk; else y1[j] = yk; }
+          if (u0) y0[j] = fma(-l0, yk, y0[j]);
+          if (u1) y1[j] = fma(-l1, yk, y1[j]);
+        }
+      }
+      for (int k = d - 1; k >= 0; k--) {
+        const double rk = s_rdiag[k];
+        const bool u0 = lane < k, u1 = lane + 32 < k;
+        const double l0 = u0 ? L[k * ld + lane] : 0.0, l1 = u1 ? L[k * ld + lane + 32] : 0.0;
+#pragma unroll
+        for (int j = 0; j < JP_CPW; j++) {
+          const double yk = __shfl_sync(0xffffffffu, k < 32 ? y0[j] : y1[j], k & 31) * rk;
+          if (lane == (k & 31)) { if (k < 32) y0[j] = yk; else y1[j] = yk; }
+          if (u0) y0[j] = fma(-l0, yk, y0[j]);
+          if (u1) y1[j] = fma(-l1, yk, y1[j]);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < JP_CPW; j++) {
+        const int c = c0 + j * nty;
+        if (c < c_hi && lane < d) Q[(size_t)c * d + lane] = scale * y0[j];
+        if (c < c_hi && lane + 32 < d) Q[(size_t)c * d + lane + 32] = scale * y1[j];
+      }
+    }
+  } else if (blockIdx.x == 0) {
+    for (int c = tid; c < r; c += nt) {
+      for (int k = 0; k < d; k++) {
+        const double yk = Y[k * r + c] / L[k * ld + k];
+        Y[k * r + c] = yk;
+        for (int i = k + 1; i < d; i++) Y[i * r + c] = fma(-L[i * ld + k], yk, Y[i * r + c]);
+      }
+      for (int k = d - 1; k >= 0; k--) {
+        const double yk = Y[k * r + c] / L[k * ld + k];
+        Y[k * r + c] = yk;
+        for (int i = 0; i < k; i++) Y[i * r + c] = fma(-L[k * ld + i], yk, Y[i * r + c]);
+      }
     }
     __syncthreads();
-    const double lkk = s_piv;
-    for (int i = k + 1 + tid; i < d; i += nt) L[i * ld + k] /= lkk;
-    __syncthreads();
-    const int m = d - k - 1;
-    for (int e = tid; e < m * m; e += nt) {
-      const int i = k + 1 + e / m, j = k + 1 + e % m;
-      if (j <= i) L[i * ld + j] = fma(-L[i * ld + k], L[j * ld + k], L[i * ld + j]);
+    for (int e = tid; e < r * d; e += nt) {
+      const int c = e / d, k = e - c * d;
+      Q[e] = scale * Y[k * r + c];
     }
-    __syncthreads();
   }
-  // forward: L Z = Y
-  for (int k = 0; k < d; k++) {
-    for (int c = tid; c < r; c += nt) Y[k * r + c] /= L[k * ld + k];
-    __syncthreads();
-    for (int e = tid; e < (d - k - 1) * r; e += nt) {
-      const int i = k + 1 + e / r, c = e % r;
-      Y[i * r + c] = fma(-L[i * ld + k], Y[k * r + c], Y[i * r + c]);
-    }
-    __syncthreads();
-  }
-  // backward: L^T X = Z
-  for (int k = d - 1; k >= 0; k--) {
-    for (int c = tid; c < r; c += nt) Y[k * r + c] /= L[k * ld + k];
-    __syncthreads();
-    for (int e = tid; e < k * r; e += nt) {
-      const int i = e / r, c = e % r;
-      Y[i * r + c] = fma(-L[k * ld + i], Y[k * r + c], Y[i * r + c]);
-    }
-    __syncthreads();
-  }
-  for (int e = tid; e < r * d; e += nt) {
-    const int c = e / d, k = e - c * d;
-    Q[e] = scale * Y[k * r + c];
-  }
-  if (tid == 0) info[0] = s_bad;
+  if (tid == 0 && blockIdx.x == 0) info[0] = s_bad;
+  JLP_STAMP(3)
 }
 
 }  // namespace
+
+extern "C" int ks_debug_jl_projection_stamps(uint64_t* out) {
+  KS_TRY_CUDA(cudaMemcpyFromSymbol(out, g_jlp_ts, sizeof(unsigned long long) * 4));
+  return KS_OK;
+}
 
 extern "C" int ks_jl_projection(const double* G, int32_t d, const double* GA, int32_t r, double scale, double* Q,
                                 int32_t* info, void* stream) {
   const size_t smem = sizeof(double) * ((size_t)d * (d + 1) + (size_t)d * r);
   KS_REQUIRE(d >= 1 && r >= 1 && smem <= 220 * 1024, KS_ESIZE, "jl_projection: d=%d r=%d too large", d, r);
   KS_TRY_CUDA(cudaFuncSetAttribute(jl_projection_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  jl_projection_kernel<<<1, 512, smem, (cudaStream_t)stream>>>(G, d, GA, r, scale, Q, info);
+  const unsigned grid = d <= 64 ? ceil_div_u(r, JP_COLS) : 1;
+  jl_projection_kernel<<<grid, 512, smem, (cudaStream_t)stream>>>(G, d, GA, r, scale, Q, info);
   KS_CHECK_LAUNCH();
   return KS_OK;
 }

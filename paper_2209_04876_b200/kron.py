@@ -159,6 +159,16 @@ class SparseDiagonal:
         object.__setattr__(self, "indices", idx)
         object.__setattr__(self, "values", val)
 
+    @classmethod
+    def _trusted(cls, indices, values) -> "SparseDiagonal":
+        """Construct without the validation passes (device syncs) for diagonals built by
+        sparse_diagonal_from_sketch, which are sorted, unique and finite by construction."""
+        obj = object.__new__(cls)
+        object.__setattr__(obj, "indices", indices)
+        object.__setattr__(obj, "values", values)
+        object.__setattr__(obj, "_views", {})
+        return obj
+
     @property
     def nnz(self) -> int:
         return int(self.indices.shape[0])
@@ -187,7 +197,9 @@ def sparse_diagonal_from_sketch(sketch, row_shape: Sequence[int]) -> SparseDiago
     _lib.call("ks_sketch_diag", nf, D.p(idx.contiguous()), _lib.ptr_array(ctypes.c_int64, shape), D.p(w), s,
               D.p(sd_idx), D.p(sd_val), ctypes.byref(nnz), D.stream())
     k = nnz.value
-    return SparseDiagonal(indices=D.out(sd_idx[:k], host), values=D.out(sd_val[:k], host))
+    if host:
+        return SparseDiagonal(indices=D.out(sd_idx[:k], host), values=D.out(sd_val[:k], host))
+    return SparseDiagonal._trusted(sd_idx[:k], sd_val[:k])
 
 
 def kron_rows(factors: Sequence, multi_indices) -> torch.Tensor:

@@ -73,9 +73,46 @@ def regression_sample_count(d: int, eps: float, beta: float = 1.0) -> int:
 
 
 _TABLES = {}
-# inside fast_kronecker_regression the sampler's validation flags are read once at the end of
-# the solve (one host synchronisation) instead of right after the tables are built
-_DEFER_CHECKS = [False]
+
+
+class DeferredChecks:
+    """Device validation flags read in one host round trip at the end of a fast solve (instead
+    of a stream synchronisation after every kernel that can fail).  Handlers run in order and
+    raise the reference's exception for the first failure."""
+
+    def __init__(self):
+        self.items = []
+
+    def add(self, flags: torch.Tensor, handler):
+        self.items.append((flags, handler))
+
+    def run(self):
+        items, self.items = self.items, []
+        if not items:
+            return
+        vals = torch.cat([f.reshape(-1).to(torch.int64) for f, _ in items]).cpu().tolist()
+        off = 0
+        for f, handler in items:
+            n = f.numel()
+            handler(vals[off:off + n])
+            off += n
+
+
+_DEFERRED: list = [None]
+
+
+def check_later(flags: torch.Tensor, handler):
+    """Run ``handler(flags as a list)`` now, or at the end of the enclosing fast solve."""
+    d = _DEFERRED[0]
+    if d is None:
+        handler(flags.cpu().tolist())
+    else:
+        d.add(flags, handler)
+
+
+def _zig_status(v):
+    if v[0]:
+        raise NumericalFailureError(f"device normal generator: ziggurat chain resolution failed (code {v[0]})")
 
 
 def _zig_tables_dev():
@@ -97,8 +134,10 @@ def device_standard_normal(seed, count: int, divisor: float = 1.0) -> torch.Tens
     ki, wi, fi = _zig_tables_dev()
     out = D.empty(count)
     if count:
+        status = torch.zeros(1, dtype=torch.int32, device=D.dev())
         _lib.call("ks_pcg64_standard_normal", sh, sl, ih, il, count, float(divisor), D.p(ki), D.p(wi),
-                  D.p(fi), D.p(out), D.stream())
+                  D.p(fi), D.p(out), D.p(status), D.stream())
+        check_later(status, _zig_status)
     return out
 
 
@@ -244,30 +283,25 @@ class ProductSampler:
                       _lib.ptr_array(ctypes.c_int64, [int(s.numel()) for s in scs]), 0,
                       _lib.ptr_array(ctypes.c_void_p, [p.data_ptr() for p in probs]),
                       _lib.ptr_array(ctypes.c_void_p, [c.data_ptr() for c in cdfs]), D.p(flags), D.stream())
-            self._flags = flags  # checked lazily (one host sync per solve)
+            check_later(flags, self._check_flags)
         else:
             probs, cdfs = [], []
             for n, sc in enumerate(scs):
                 p, c = _tables(sc, renorm=False, what=f"score vector {n}")
                 probs.append(p)
                 cdfs.append(c)
-            self._flags = None
         self._probs = probs
         self._cdfs = cdfs
-        if not _DEFER_CHECKS[0]:
-            self.check()
         self.beta = float(np.prod([1.0 / ls.approx_factor for ls in per_factor_scores]))
 
-    def check(self):
+    @staticmethod
+    def _check_flags(flags):
         """Raise the reference's InvalidInputError for invalid score vectors (leverage.py:163-171)."""
-        if self._flags is None:
-            return
-        for n, f in enumerate(self._flags.cpu().tolist()):
+        for n, f in enumerate(flags):
             if f & 1:
                 raise InvalidInputError(f"score vector {n} must be nonnegative finite")
             if f & 2:
                 raise InvalidInputError(f"score vector {n} sums to zero")
-        self._flags = None
 
     @property
     def per_factor_probabilities(self):

@@ -110,9 +110,9 @@ class FactorGram:
         return int(self.v.shape[0])
 
 
-def _gram_dev(a: torch.Tensor) -> torch.Tensor:
+def _gram_dev(a: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
     n, d = int(a.shape[0]), int(a.shape[1])
-    g = D.empty(d, d)
+    g = D.empty(d, d) if out is None else out
     if d <= 128:
         _lib.call("ks_gemm_tn_tall", d, d, n, 1.0, D.p(a), d, 1, D.p(a), d, 1, D.p(g), D.stream())
     else:
@@ -363,12 +363,13 @@ def _regression_sample_count(cols: int, config: RegressionConfig) -> int:
 _SIDE = {}
 
 
-def _side_stream() -> torch.cuda.Stream:
-    dev = torch.cuda.current_device()
-    s = _SIDE.get(dev)
+def _side_stream(k: int = 0) -> torch.cuda.Stream:
+    """k-th auxiliary stream of the current device (0: eigensolves, 1..: per-factor JL work)."""
+    key = (torch.cuda.current_device(), k)
+    s = _SIDE.get(key)
     if s is None:
-        s = torch.cuda.Stream(device=dev)
-        _SIDE[dev] = s
+        s = torch.cuda.Stream(device=key[0])
+        _SIDE[key] = s
     return s
 
 
@@ -380,14 +381,15 @@ def _factor_grams_async(gts: list[torch.Tensor]):
     outs = []
     same = len({int(g.shape[0]) for g in gts}) == 1
     with torch.cuda.stream(side):
-        if same and len(gts) > 1:
+        if same and 1 < len(gts) <= 8:
+            # one launch, one CTA per Gram, symmetrised on load
             d = int(gts[0].shape[0])
-            gs = torch.stack([0.5 * (g + g.T) for g in gts]).contiguous()
             w = D.empty(len(gts), d)
             v = D.empty(len(gts), d, d)
-            _lib.call("ks_svd_small_batched", D.p(gs), len(gts), d, D.p(w), D.p(v), D.stream())
+            _lib.call("ks_sym_eig_batched", len(gts), _lib.ptr_array(ctypes.c_void_p, [g.data_ptr() for g in gts]),
+                      d, D.p(w), D.p(v), D.stream())
             outs = [(v[i], w[i]) for i in range(len(gts))]
-            keep = [gs, w, v]
+            keep = [w, v]
         else:
             for g in gts:
                 vv, ww, gs = _factor_gram_dev(g)
@@ -410,17 +412,29 @@ def _join_grams(handle):
     return outs
 
 
+class _CholeskyFailed(Exception):
+    """A JL Gram was not numerically positive definite; the solve is redone with LU inverses."""
+
+
+def _chol_status(v):
+    if v[0]:
+        raise _CholeskyFailed()
+
+
 def _jl_scores_chol(a: torch.Tensor, a_tilde: torch.Tensor, gram: torch.Tensor, eps: float, seed,
-                    log_factor: float) -> torch.Tensor:
-    """JL scores with (1+eps/4) (G a_tilde) gram^-1 from a device Cholesky solve (leverage.py:114-129);
-    falls back to the LU inverse when the Gram is not numerically positive definite."""
-    from .leverage import _jl_ga, _jl_scores_from_q
+                    log_factor: float, use_chol: bool = True) -> torch.Tensor:
+    """JL scores with (1+eps/4) (G a_tilde) gram^-1 from a device Cholesky solve (leverage.py:114-129).
+    The positive-definiteness flag is checked with the solve's other deferred flags; on failure
+    the solve is repeated with ``use_chol=False`` (LU inverse, as the reference's np.linalg.inv)."""
+    from .leverage import _jl_ga, _jl_scores_from_q, check_later
     d = int(a.shape[1])
     ga, r = _jl_ga(a, a_tilde, seed, log_factor)
     q = D.empty(r, d)
-    info = torch.zeros(1, dtype=torch.int32, device=a.device)
-    _lib.call("ks_jl_projection", D.p(gram), d, D.p(ga), r, 1.0 + eps / 4.0, D.p(q), D.p(info), D.stream())
-    if int(info.item()) != 0:
+    if use_chol:
+        info = torch.zeros(1, dtype=torch.int32, device=a.device)
+        _lib.call("ks_jl_projection", D.p(gram), d, D.p(ga), r, 1.0 + eps / 4.0, D.p(q), D.p(info), D.stream())
+        check_later(info, _chol_status)
+    else:
         gi = _inverse_small(gram)
         _lib.call("ks_gemm", r, d, d, 1.0 + eps / 4.0, D.p(ga), d, 1, 0, D.p(gi), d, 1, 0, 0.0, D.p(q), d, 1, 0, 1,
                   D.stream())
@@ -448,6 +462,153 @@ class FastSolveTrace:
 
 def _fast_solve_dev(facs, b, config: RegressionConfig, caches, trace: FastSolveTrace | None = None):
     """The device pipeline of solvers.py:404-459; returns (x natural order, iterations, s)."""
+    from . import leverage as _lev
+    for use_chol in (True, False):
+        deferred = _lev.DeferredChecks()
+        _lev._DEFERRED[0] = deferred
+        retry = False
+        try:
+            return _fast_solve_pass(facs, b, config, caches, trace, use_chol, deferred)
+        except _CholeskyFailed:
+            retry = True
+        except Exception:
+            # a pending device flag (invalid scores, generator failure) explains a later error
+            # better: raise the reference's exception for it first
+            _lev._DEFERRED[0] = None
+            try:
+                deferred.run()
+            except _CholeskyFailed:
+                retry = True
+            if not retry:
+                raise
+        finally:
+            _lev._DEFERRED[0] = None
+        assert retry and use_chol
+    raise AssertionError("unreachable")
+
+
+_SEEDS: dict = {}
+
+
+def _spawned_seeds(seed, count: int):
+    """SeedSequence(seed).spawn(count) (solvers.py:415-416), memoised for integer seeds: the
+    children are a pure function of (seed, count) and spawning costs ~60 us of host time."""
+    if isinstance(seed, (int, np.integer)) and not isinstance(seed, bool):
+        key = (int(seed), count)
+        got = _SEEDS.get(key)
+        if got is None:
+            if len(_SEEDS) > 256:
+                _SEEDS.clear()
+            got = _SEEDS[key] = tuple(np.random.SeedSequence(int(seed)).spawn(count))
+        return got
+    return np.random.SeedSequence(seed).spawn(count)
+
+
+def _jl_and_sampling(facs, tildes, gts, eps_jl: float, config: RegressionConfig, use_chol: bool, seeds, s: int):
+    """JL leverage estimates of every factor (leverage.py:85-130), the product sampler's tables
+    and the s draws with their weights (solvers.py:430-452).  Launch-only: no host round trips,
+    so the whole stage can be captured in a CUDA graph."""
+    scores, afs = [], []
+    main = torch.cuda.current_stream()
+    capturing = torch.cuda.is_current_stream_capturing()
+    # the per-factor JL estimates are independent: factor n > 0 runs on its own stream (all
+    # streams fork here, before any factor's work is enqueued)
+    for n in range(1, len(facs)):
+        _side_stream(n).wait_stream(main)
+    for n, a in enumerate(facs):
+        st = main if n == 0 else _side_stream(n)
+        with torch.cuda.stream(st):
+            scores.append(_jl_scores_chol(a, tildes[n], gts[n], eps_jl, seeds[2 * n + 1], config.jl_log_factor,
+                                          use_chol))
+        afs.append(1.0 + eps_jl / 2.0)
+    for n in range(1, len(facs)):
+        main.wait_stream(_side_stream(n))
+        if not capturing:
+            scores[n].record_stream(main)
+    sampler = ProductSampler([LeverageScores(sc, 0.0, af) for sc, af in zip(scores, afs)])
+    state, inc = pcg64_state(seeds[-1])
+    draws = sampler._sample_dev(s, state, inc)
+    w = sampler._weights_dev(draws, s)
+    return scores, afs, sampler, draws, w
+
+
+class _PrefixGraph:
+    """CUDA graph of _jl_and_sampling for one (factor buffers, shapes, config) key.  The Grams
+    are written into ``gts`` (static inputs) eagerly before every replay; outputs and deferred
+    flag tensors are static graph-pool tensors."""
+
+    def __init__(self):
+        self.graph = None
+        self.gts = None
+        self.out = None
+        self.checks = []
+
+
+_PREFIX_GRAPHS: dict = {}
+_PREFIX_STATS = {"eager": 0, "capture": 0, "replay": 0}
+_USE_GRAPHS = [True]
+
+
+def _prefix_key(facs, tildes, config: RegressionConfig, use_chol: bool):
+    if not _USE_GRAPHS[0] or not use_chol or any(t is not a for t, a in zip(tildes, facs)):
+        return None
+    try:
+        key = (torch.cuda.current_device(), torch.cuda.current_stream().cuda_stream,
+               tuple((a.data_ptr(), tuple(a.shape), tuple(a.stride())) for a in facs), config)
+        hash(key)
+    except TypeError:
+        return None
+    return key
+
+
+def _prefix_graph_run(key, entry, gts, run, deferred):
+    """First sight of a key: eager (warms every lazy initialisation).  Second: capture, then
+    replay.  Afterwards: replay only."""
+    from . import leverage as _lev
+    if entry is None:
+        _PREFIX_STATS["eager"] += 1
+        if len(_PREFIX_GRAPHS) >= 8:
+            _PREFIX_GRAPHS.pop(next(iter(_PREFIX_GRAPHS)))
+        _PREFIX_GRAPHS[key] = _PrefixGraph()
+        return run()
+    if entry.graph is None:
+        _PREFIX_STATS["capture"] += 1
+        entry.gts = gts
+        g = torch.cuda.CUDAGraph()
+        cap = _lev.DeferredChecks()
+        outer = _lev._DEFERRED[0]
+        _lev._DEFERRED[0] = cap
+        try:
+            with torch.cuda.graph(g):
+                entry.out = run()
+        except Exception:
+            _PREFIX_GRAPHS.pop(key, None)
+            raise
+        finally:
+            _lev._DEFERRED[0] = outer
+        entry.graph = g
+        entry.checks = cap.items
+    _PREFIX_STATS["replay"] += 1
+    entry.graph.replay()
+    for flags, handler in entry.checks:
+        deferred.add(flags, handler)
+    return entry.out
+
+
+# Phase marks for tools/profile_fast.py --phases: (name, host time, CUDA event) when enabled.
+_PHASES: list | None = None
+
+
+def _mark(name: str):
+    if _PHASES is not None:
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record()
+        _PHASES.append((name, time.perf_counter(), ev))
+
+
+def _fast_solve_pass(facs, b, config: RegressionConfig, caches, trace, use_chol: bool, deferred):
+    from . import leverage as _lev
+    _mark("start")
     n_factors = len(facs)
     rows = [int(a.shape[0]) for a in facs]
     cols_l = [int(a.shape[1]) for a in facs]
@@ -455,7 +616,7 @@ def _fast_solve_dev(facs, b, config: RegressionConfig, caches, trace: FastSolveT
     lam = config.lam
     alpha = config.effective_alpha
     s = _regression_sample_count(cols, config)
-    seeds = np.random.SeedSequence(config.seed).spawn(2 * n_factors + 1)
+    seeds = _spawned_seeds(config.seed, 2 * n_factors + 1)
     grams, scores, afs = [], [], []
     if caches is not None:
         for cache in caches:
@@ -470,7 +631,7 @@ def _fast_solve_dev(facs, b, config: RegressionConfig, caches, trace: FastSolveT
         eps_two = eps_one / (2.0 + eps_one)
         delta_n = config.delta / (2.0 * n_factors)
         eps_jl = 4.0 * math.log1p(config.eps / 4.0) / n_factors
-        tildes, gts = [], []
+        tildes = []
         for n, a in enumerate(facs):
             s_n = math.ceil(alpha * spectral_sample_count(int(a.shape[1]), eps_two, delta_n))
             if s_n >= int(a.shape[0]):
@@ -481,24 +642,29 @@ def _fast_solve_dev(facs, b, config: RegressionConfig, caches, trace: FastSolveT
             if trace is not None:
                 trace.a_tilde_rows.append(int(a_tilde.shape[0]))
             tildes.append(a_tilde)
-            gts.append(_gram_dev(a_tilde))
+        key = _prefix_key(facs, tildes, config, use_chol) if trace is None else None
+        entry = _PREFIX_GRAPHS.get(key) if key is not None else None
+        gts = [_gram_dev(t, out=entry.gts[n] if entry is not None and entry.gts is not None else None)
+               for n, t in enumerate(tildes)]
         # The preconditioner's eigendecompositions (solvers.py:440, 446) run on a side stream,
         # overlapped with the JL estimates, sampling and sketch construction; joined before the
         # Richardson loop.
+        _mark("factor grams")
         grams = _factor_grams_async(gts)
-        for n, a in enumerate(facs):
-            scores.append(_jl_scores_chol(a, tildes[n], gts[n], eps_jl, seeds[2 * n + 1], config.jl_log_factor))
-            afs.append(1.0 + eps_jl / 2.0)
-    from . import leverage as _lev
-    _lev._DEFER_CHECKS[0] = True
-    try:
+        run = lambda: _jl_and_sampling(facs, tildes, gts, eps_jl, config, use_chol, seeds, s)  # noqa: E731
+        if key is None:
+            scores, afs, sampler, draws, w = run()
+        else:
+            scores, afs, sampler, draws, w = _prefix_graph_run(key, entry, gts, run, deferred)
+        _mark("jl scores+sampling")
+    if caches is not None:
         sampler = ProductSampler([LeverageScores(sc, 0.0, af) for sc, af in zip(scores, afs)])
-    finally:
-        _lev._DEFER_CHECKS[0] = False
-    state, inc = pcg64_state(seeds[-1])
-    draws = sampler._sample_dev(s, state, inc)
-    w = sampler._weights_dev(draws, s)
+        state, inc = pcg64_state(seeds[-1])
+        draws = sampler._sample_dev(s, state, inc)
+        w = sampler._weights_dev(draws, s)
+    _mark("draws+weights")
     sdiag = sparse_diagonal_from_sketch(RowSketch(draws, w), rows)
+    _mark("sparse diagonal")
     idx = sdiag.indices
     if isinstance(b, torch.Tensor) and b.is_cuda:
         b_at = D.empty(sdiag.nnz)
@@ -508,11 +674,14 @@ def _fast_solve_dev(facs, b, config: RegressionConfig, caches, trace: FastSolveT
         bh = b.reshape(-1) if isinstance(b, torch.Tensor) else np.asarray(b, dtype=np.float64).reshape(-1)
         ih = idx.cpu().numpy()
         b_at = D.to_dev(np.asarray(bh[ih], dtype=np.float64))
+    _mark("gather b")
     view = _view_for(facs, sdiag)
+    _mark("sketch view")
     bv = (sdiag.values * b_at).contiguous()
     rhs = D.empty(view.dL, view.dR)
     _lib.call("ks_sketched_transpose_apply", ctypes.byref(view.struct), D.p(bv), D.p(view.perm_arg()), D.p(rhs),
               D.stream())
+    _mark("rhs")
     # preconditioner in grouped (left | right) order
     grams = _join_grams(grams)
     eig = reduce(torch.kron, [w for _, w in grams])
@@ -530,12 +699,15 @@ def _fast_solve_dev(facs, b, config: RegressionConfig, caches, trace: FastSolveT
     iters = ctypes.c_int32(0)
     hlen = ctypes.c_int32(0)
     lib = _lib.load()
+    _mark("precond")
     rc = lib.ks_richardson_sketched(ctypes.byref(view.struct), D.p(VL), D.p(VR), D.p(dg), D.p(rhs),
                                     float(lam), float(config.effective_damping), int(max_iters),
                                     float(config.residual_tol), D.p(x), D.p(hist), ctypes.byref(iters),
                                     ctypes.byref(hlen), D.stream())
+    _mark("richardson")
+    _lev._DEFERRED[0] = None
+    deferred.run()  # generator / Cholesky / sampler-table flags, one host round trip
     history = hist[: hlen.value].cpu().tolist()
-    sampler.check()
     if rc == _lib.KS_EDIVERGED:
         raise NumericalFailureError("Richardson iteration diverged", iterations=iters.value,
                                     diagnostics={"residual_history": history})

@@ -182,3 +182,36 @@ def test_fused_richardson_divergence_rule(golden):
         O.fast_kronecker_regression(facs, b, eps=0.1, delta=0.01, lam=1e-3, alpha=1e-5, seed=0, damping=-1.0,
                                     max_iters=60)
     assert oerr.value.kind == "numerical" and oerr.value.iterations == err.value.iterations
+
+
+def test_graph_replay_matches_eager(golden):
+    """The JL/sampling stage is captured in a CUDA graph on the second solve with the same
+    buffers and replayed afterwards; every solve must equal the eager one bit for bit."""
+    import paper_2209_04876_b200 as K
+    from paper_2209_04876_b200 import solvers as S
+    g = golden("c2")
+    facs, b = O.synth_regression(4096, 32, 2, 0)
+    fd = [torch.tensor(a, device="cuda") for a in facs]
+    bd = torch.tensor(b, device="cuda")
+    S._USE_GRAPHS[0] = False
+    try:
+        ref = K.fast_kronecker_regression(fd, bd, cfg())
+    finally:
+        S._USE_GRAPHS[0] = True
+    S._PREFIX_GRAPHS.clear()
+    outs = [K.fast_kronecker_regression(fd, bd, cfg()) for _ in range(4)]  # eager, capture, replay x2
+    assert any(e.graph is not None for e in S._PREFIX_GRAPHS.values())
+    for rep in outs:
+        assert rep.iterations == ref.iterations
+        assert torch.equal(rep.solution, ref.solution)
+    assert rel(outs[-1].solution, g["x"]) <= X_TOL["c2"]
+    # the replayed stage reads the factors' current contents: a scaled factor changes the answer
+    # exactly like an eager solve of the scaled problem
+    fd[0].mul_(2.0)
+    rep2 = K.fast_kronecker_regression(fd, bd, cfg())
+    S._USE_GRAPHS[0] = False
+    try:
+        ref2 = K.fast_kronecker_regression(fd, bd, cfg())
+    finally:
+        S._USE_GRAPHS[0] = True
+    assert torch.equal(rep2.solution, ref2.solution)

@@ -32,8 +32,14 @@ for _ in range(reps):
     tr = FastSolveTrace()
     rep = K.fast_kronecker_regression(facs, b, cfg, _trace=tr)
     walls.append(rep.wall_time)
+    if "--mem" in sys.argv:
+        free, total = torch.cuda.mem_get_info()
+        print(f"mem: free {free / 2**30:.1f} GiB / {total / 2**30:.1f}; torch allocated "
+              f"{torch.cuda.memory_allocated() / 2**30:.2f} reserved {torch.cuda.memory_reserved() / 2**30:.2f} GiB")
 torch.cuda.synchronize()
 print("wall", walls, "loss", rep.loss, "iters", rep.iterations)
+from paper_2209_04876_b200 import solvers as _S  # noqa: E402
+print("prefix graph stats:", _S._PREFIX_STATS, "keys:", len(_S._PREFIX_GRAPHS))
 ph = (ctypes.c_double * 6)()
 if _lib.load().ks_debug_richardson_phases(rep.iterations, ph) == 0:
     names = ["apply", "sync", "reduce+sync", "precondA+sync", "precondB+sync", "update"]
@@ -90,3 +96,72 @@ if "--cta" in sys.argv:
     dur = ts[:, 1] - ts[:, 0]
     print("apply duration: min %.2f median %.2f max %.2f us" % (dur.min(), np.median(dur), dur.max()))
     print("slowest CTAs:", np.argsort(-dur)[:8], dur[np.argsort(-dur)[:8]].round(2))
+
+if "--trace" in sys.argv:
+    # kernel timeline of one solve (CUPTI via torch.profiler): start offset, duration, stream
+    import json
+    import tempfile
+    from torch.profiler import ProfilerActivity, profile
+    with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
+        rep = K.fast_kronecker_regression(facs, b, cfg)
+        torch.cuda.synchronize()
+    with tempfile.NamedTemporaryFile(suffix=".json", delete=False) as f:
+        path = f.name
+    prof.export_chrome_trace(path)
+    allev = json.load(open(path))["traceEvents"]
+    ev = [e for e in allev if e.get("ph") == "X" and e.get("cat") in ("kernel", "gpu_memcpy", "gpu_memset")]
+    rt = [e for e in allev if e.get("ph") == "X" and e.get("cat") == "cuda_runtime" and e.get("dur", 0) > 15]
+    ev.sort(key=lambda e: e["ts"])
+    t0 = ev[0]["ts"]
+    print(f"{'start_us':>9} {'dur_us':>8} {'gap_us':>7} strm  kernel")
+    prev_end = {}
+    for e in ev:
+        s = e["args"].get("stream", -1)
+        gap = e["ts"] - prev_end.get(s, e["ts"])
+        prev_end[s] = e["ts"] + e["dur"]
+        print(f"{e['ts'] - t0:9.1f} {e['dur']:8.1f} {gap:7.1f} {s:4}  {e['name'][:80]}")
+    import collections
+    agg = collections.defaultdict(lambda: [0, 0.0])
+    for e in allev:
+        if e.get("ph") == "X" and e.get("cat") == "cuda_runtime":
+            agg[e["name"]][0] += 1
+            agg[e["name"]][1] += e.get("dur", 0)
+    print("runtime API totals:")
+    for k, v in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+        print(f"  {k:40s} {v[0]:5d} calls {v[1]:9.1f} us")
+    print("slow runtime API calls (>15 us):")
+    for e in sorted(rt, key=lambda e: e["ts"]):
+        print(f"{e['ts'] - t0:9.1f} {e['dur']:8.1f}   {e['name']}")
+    end = max(e["ts"] + e["dur"] for e in ev)
+    print(f"span {end - t0:.1f} us, wall {rep.wall_time * 1e6:.1f} us")
+
+if "--host" in sys.argv:
+    # host-side profile of one warm solve (where the wall time goes that is not GPU work)
+    import cProfile
+    import pstats
+    torch.cuda.synchronize()
+    pr = cProfile.Profile()
+    for _ in range(5):
+        pr.enable()
+        rep = K.fast_kronecker_regression(facs, b, cfg)
+        pr.disable()
+        torch.cuda.synchronize()
+    st = pstats.Stats(pr)
+    st.sort_stats("tottime").print_stats(45)
+
+if "--phases" in sys.argv:
+    from paper_2209_04876_b200 import solvers as S
+    for rep_i in range(3):
+        S._PHASES = []
+        torch.cuda.synchronize()
+        t_host0 = __import__("time").perf_counter()
+        rep = K.fast_kronecker_regression(facs, b, cfg)
+        torch.cuda.synchronize()
+        ph, S._PHASES = S._PHASES, None
+        ms = torch.cuda.memory_stats()
+        print(f"solve {rep_i}: wall {rep.wall_time * 1e6:.0f} us  segments {ms['segment.all.allocated']} "
+              f"cudaMalloc retries {ms['num_alloc_retries']}")
+        prev = ph[0]
+        for name, th, ev in ph[1:]:
+            print(f"  {name:18s} gpu {prev[2].elapsed_time(ev) * 1e3:8.1f} us   host-issue {1e6 * (th - prev[1]):8.1f} us")
+            prev = (name, th, ev)
