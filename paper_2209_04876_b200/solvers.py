@@ -727,12 +727,12 @@ def _fast_solve_pass(facs, b, config: RegressionConfig, caches, trace, use_chol:
 
 
 def fast_kronecker_regression(factors: Sequence, b, config: RegressionConfig,
-                              caches: Sequence[FactorCache] | None = None, _trace: FastSolveTrace | None = None
-                              ) -> SolveReport:
+                              caches: Sequence[FactorCache] | None = None, _trace: FastSolveTrace | None = None,
+                              *, with_loss: bool = True) -> SolveReport:
     """(1+eps)-approximate Kronecker ridge regression (solvers.py:372-462), all on the GPU.
 
     ``wall_time`` covers the solve (as in the reference); the reported loss is evaluated
-    exactly afterwards.  With host-resident ``b`` only its sampled entries are transferred
+    exactly afterwards (``with_loss=False`` skips it: loss = nan; an extension for timing).  With host-resident ``b`` only its sampled entries are transferred
     for the solve; the loss pass then uploads it."""
     host = not D.on_device(b)
     facs, rows, cols = _validated_problem(factors, b)
@@ -742,20 +742,26 @@ def fast_kronecker_regression(factors: Sequence, b, config: RegressionConfig,
         raise InvalidInputError("need one cache entry per factor")
     torch.cuda.synchronize()
     t0 = time.perf_counter()
+    _mark("t0")
     s = _regression_sample_count(cols, config)
     if s >= rows:
         bt = D.to_dev(b).reshape(-1)
         x = _exact_solve_dev(facs, bt, config.lam)
         torch.cuda.synchronize()
+        _mark("solve_end")
         wall = time.perf_counter() - t0
-        loss = _ridge_loss_dev(facs, x, bt, config.lam)
+        loss = _ridge_loss_dev(facs, x, bt, config.lam) if with_loss else float("nan")
         return SolveReport(solution=D.out(x, host), loss=loss, iterations=0, sample_count=0, wall_time=wall)
     bsrc = b if D.on_device(b) else (b if isinstance(b, torch.Tensor) else np.asarray(b, dtype=np.float64))
     if D.on_device(bsrc):
         bsrc = bsrc.reshape(-1).to(torch.float64).contiguous()
     x, iters, s = _fast_solve_dev(facs, bsrc, config, caches, _trace)
     torch.cuda.synchronize()
+    _mark("solve_end")
     wall = time.perf_counter() - t0
-    bt = D.to_dev(b).reshape(-1)
-    loss = _ridge_loss_dev(facs, x, bt, config.lam)
+    if with_loss:
+        bt = D.to_dev(b).reshape(-1)
+        loss = _ridge_loss_dev(facs, x, bt, config.lam)
+    else:
+        loss = float("nan")
     return SolveReport(solution=D.out(x, host), loss=loss, iterations=iters, sample_count=s, wall_time=wall)
