@@ -231,6 +231,18 @@ int ks_richardson_sketched(const ks_sketch_view* sk, const double* VL, const dou
                            int32_t max_iters, double residual_tol, double* x, double* hist,
                            int32_t* iters, int32_t* hist_len, void* stream);
 
+/* Fused Richardson for single-factor groups (dL, dR in {16, 32, 64}) on the persistent path:
+ * additionally builds the right-hand side (SK)^T S b = sum_t v_t (v_t b_t) L_u R_t^T (solvers.py:455,
+ * kron.py:303-354) inside the loop kernel from b_at (b at the sparse-diagonal rows, in
+ * sparse-diagonal order; perm maps grouped -> sparse-diagonal position, NULL if identical) and
+ * returns it in rhs_out (dL x dR).  dinv may be NULL: then dinv = pseudo-reciprocal(wL (x) wR + lam)
+ * (solvers.py:186-198) with wL, wR the two Gram eigenvalue vectors.  Other arguments and
+ * returns as ks_richardson_sketched; KS_ESIZE when the shape is not supported. */
+int ks_richardson_fused(const ks_sketch_view* sk, const int64_t* perm, const double* b_at, const double* VL,
+                        const double* wL, const double* VR, const double* wR, const double* dinv, double lam,
+                        double damping, int32_t max_iters, double residual_tol, double* x, double* hist,
+                        double* rhs_out, int32_t* iters, int32_t* hist_len, void* stream);
+
 /* Profiling aid: per-CTA %globaltimer stamps (ns) of iteration 5 of the last persistent
  * Richardson run, 9 per CTA (phase boundaries and grid-barrier exits). */
 int ks_debug_richardson_cta_stamps(int32_t nctas, uint64_t* out);

@@ -20,7 +20,8 @@ int sketched_gram_partials(cudaStream_t st, const ks_sketch_view* sk, const doub
 int64_t sketched_partials_count(const ks_sketch_view* sk);
 bool persistent_supported(int dL, int dR);
 int richardson_persistent(cudaStream_t st, const ks_sketch_view* sk, const double* VL, const double* VR,
-                          const double* dinv, const double* rhs, double lam, double damping, int max_iters,
+                          const double* dinv, const double* wL, const double* wR, double* rhs, bool rhs_in_kernel,
+                          const double* b_at, const int64_t* perm, double lam, double damping, int max_iters,
                           double residual_tol, double* x, double* hist, int* iters, int* hist_len, int* status);
 }
 
@@ -202,8 +203,9 @@ extern "C" int ks_richardson_sketched(const ks_sketch_view* sk, const double* VL
   if (!force_multi && sk->nnz > 0 && ks::persistent_supported(dL, dR) && max_iters <= 1024) {
     int status = 0;
     int it = 0, hl = 0;
-    int rc = ks::richardson_persistent(st, sk, VL, VR, dinv, rhs, lam, damping, max_iters, residual_tol, x, hist,
-                                       &it, &hl, &status);
+    int rc = ks::richardson_persistent(st, sk, VL, VR, dinv, nullptr, nullptr, const_cast<double*>(rhs), false,
+                                       nullptr, nullptr, lam, damping, max_iters, residual_tol, x, hist, &it, &hl,
+                                       &status);
     if (rc) return rc;
     *iters = it;
     *hist_len = hl;
@@ -244,6 +246,32 @@ extern "C" int ks_richardson_sketched(const ks_sketch_view* sk, const double* VL
   *iters = h.iters;
   *hist_len = h.hist_len;
   if (h.status == ST_DIVERGED) {
+    ks::set_error("Richardson iteration diverged");
+    return KS_EDIVERGED;
+  }
+  return KS_OK;
+}
+
+// Fused form for single-factor groups on the persistent path: the right-hand side
+// (SK)^T S b (solvers.py:455) is built inside the loop kernel from b_at (b at the sparse-diagonal
+// rows) and returned in rhs_out; dinv (may be null) defaults to pseudo-reciprocal(wL x wR + lam).
+extern "C" int ks_richardson_fused(const ks_sketch_view* sk, const int64_t* perm, const double* b_at,
+                                   const double* VL, const double* wL, const double* VR, const double* wR,
+                                   const double* dinv, double lam, double damping, int32_t max_iters,
+                                   double residual_tol, double* x, double* hist, double* rhs_out, int32_t* iters,
+                                   int32_t* hist_len, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const int dL = sk->dL, dR = sk->dR;
+  KS_REQUIRE(sk->nnz > 0 && ks::persistent_supported(dL, dR) && max_iters <= 1024, KS_ESIZE,
+             "fused Richardson needs dL, dR in {16, 32, 64}, nnz > 0 and <= 1024 iterations");
+  KS_REQUIRE(dinv || (wL && wR), KS_EINVAL, "need dinv or both eigenvalue vectors");
+  int status = 0, it = 0, hl = 0;
+  int rc = ks::richardson_persistent(st, sk, VL, VR, dinv, wL, wR, rhs_out, true, b_at, perm, lam, damping,
+                                     max_iters, residual_tol, x, hist, &it, &hl, &status);
+  if (rc) return rc;
+  *iters = it;
+  *hist_len = hl;
+  if (status == 2) {
     ks::set_error("Richardson iteration diverged");
     return KS_EDIVERGED;
   }

@@ -46,8 +46,11 @@ struct PArgs {
   const double* VL;       // DL x DL
   const double* VR;       // DR x DR
   const double* VRt;      // DR x DR
-  const double* dinv;     // DL x DR
-  const double* rhs;      // DL x DR
+  const double* dinv;     // DL x DR, or null: dinv(i, j) = pseudo-reciprocal(wL[i] wR[j] + lam)
+  const double* wL;       // DL (eigenvalues of the left factor's Gram) when dinv is null
+  const double* wR;       // DR
+  double* rhs;            // DL x DR (input, or output when rhs_in_kernel)
+  int rhs_in_kernel;      // pass -1 builds rhs = sum_t v_t (v_t b_t) L_u R_t^T (Rpack pad slot 1 = v_t b_t)
   double lam, damping, residual_tol;
   int max_iters;
   double* part;           // grid x DL x DR
@@ -188,7 +191,16 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
           for (int j = part; j < DR; j += 4) s = fma(Ws[64 + j], VRs[j * DRP + c], s);
         s += __shfl_xor_sync(0xffffffffu, s, 1);
         s += __shfl_xor_sync(0xffffffffu, s, 2);
-        if (c < DR && part == 0) a.T[r * DR + c] = s * __ldg(&a.dinv[r * DR + c]);
+        if (c < DR && part == 0) {
+          double dv;
+          if (a.dinv) {
+            dv = __ldg(&a.dinv[r * DR + c]);
+          } else {  // solvers.py:186-191 on kron(wL, wR) + lam
+            const double e = __dadd_rn(__dmul_rn(__ldg(&a.wL[r]), __ldg(&a.wR[c])), a.lam);
+            dv = e > 0.0 ? __ddiv_rn(1.0, e) : 0.0;
+          }
+          a.T[r * DR + c] = s * dv;
+        }
       }
       __syncthreads();
     }
@@ -240,11 +252,15 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
     return v;
   };
 
-  precond_a(a.rhs);
-  grid.sync();
-  precond_b();
-  grid.sync();
-  const double tol = a.residual_tol * fmax(row_norm(), DBL_MIN);
+  // tol = residual_tol * ||P rhs|| (solvers.py:212-214)
+  auto init_tol = [&]() {
+    precond_a(a.rhs);
+    grid.sync();
+    precond_b();
+    grid.sync();
+    return a.residual_tol * fmax(row_norm(), DBL_MIN);
+  };
+  double tol = a.rhs_in_kernel ? 0.0 : init_tol();
 
   if (tid == 0 && c_beg < c_end) {
     issue_chunk<DL, DR>(a, a.chunks[c_beg], sm, &bars[0], 0);
@@ -253,8 +269,11 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
 
   int status = 0, iters = 0, hlen = 0;
   const bool prof = (b == 0 && tid == 0);
-  for (int it = 0; it < a.max_iters; it++) {
-    if (prof) g_prof[it * 6 + 0] = clock64();
+  // it == -1: the right-hand-side pass (same chunk pipeline, s_t = v_t (v_t b_t), no Y)
+  const int it0 = a.rhs_in_kernel ? -1 : 0;  // first pass: a CTA with a single (resident) chunk waits only here
+  for (int it = it0; it < a.max_iters; it++) {
+    const bool rp = it < 0;
+    if (prof && !rp) g_prof[it * 6 + 0] = clock64();
     KS_STAMP(0)
     // ---------------- P1: sketched normal-operator apply ----------------
     double gacc[G_PER_W][4];
@@ -270,7 +289,7 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
           pending[buf ^ 1] = 1;
         }
       }
-      if (!resident || it == 0) {
+      if (!resident || it == it0) {
         mbar_wait(&bars[buf], phase[buf]);
         phase[buf] ^= 1;
         pending[buf] = 0;
@@ -282,7 +301,7 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
 #pragma unroll
       for (int yi = 0; yi < Y_PER_W; yi++) {
         const int tile = warp + yi * PW;
-        if (tile < Y_TILES) {
+        if (!rp && tile < Y_TILES) {
           const int m0 = (tile / YT_N) * 16, n0 = (tile % YT_N) * 8;
           double acc[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
@@ -311,7 +330,7 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
           const int64_t tb = max(a.seg[u], ch.t_b), te = min(a.seg[u + 1], ch.t_e);
           double y[QE];
 #pragma unroll
-          for (int j = 0; j < QE; j++) y[j] = Ys[r * DRP + ql * QE + j];
+          for (int j = 0; j < QE; j++) y[j] = rp ? 0.0 : Ys[r * DRP + ql * QE + j];
           for (int64_t t = tb; t < te; t++) {
             const double* Rt = Rs + (int)(t - ch.t_b) * DRP;
             double rv[QE];
@@ -321,12 +340,17 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
               rv[j] = Rt[ql * QE + j];
               d = fma(y[j], rv[j], d);
             }
-            d += __shfl_xor_sync(qmask, d, 1);
-            d += __shfl_xor_sync(qmask, d, 2);
-            d += __shfl_xor_sync(qmask, d, 4);
-            d += __shfl_xor_sync(qmask, d, 8);
-            const double vt = Rt[DR];  // v_t travels in the row padding
-            const double s = vt * (vt * d);
+            const double vt = Rt[DR];  // v_t and v_t b_t travel in the row padding
+            double s;
+            if (rp) {
+              s = vt * Rt[DR + 1];
+            } else {
+              d += __shfl_xor_sync(qmask, d, 1);
+              d += __shfl_xor_sync(qmask, d, 2);
+              d += __shfl_xor_sync(qmask, d, 4);
+              d += __shfl_xor_sync(qmask, d, 8);
+              s = vt * (vt * d);
+            }
 #pragma unroll
             for (int j = 0; j < QE; j++) z[j] = fma(s, rv[j], z[j]);
           }
@@ -367,11 +391,11 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
         P[(m0 + g + 8) * DR + n0 + 2 * t4 + 1] = gacc[gi][3];
       }
     }
-    if (prof) g_prof[it * 6 + 1] = clock64();
+    if (prof && !rp) g_prof[it * 6 + 1] = clock64();
     KS_STAMP(1)
     grid.sync();
     KS_STAMP(2)
-    if (prof) g_prof[it * 6 + 2] = clock64();
+    if (prof && !rp) g_prof[it * 6 + 2] = clock64();
     // ---------------- P2: R = sum G + lam X - rhs ----------------
     {
       // this CTA's slice of every partial is staged in shared memory with cp.async (all copies in
@@ -414,13 +438,18 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
         }
         if (ql == 0) {
           const int i = e / DR, k = e - i * DR;
-          a.R[e] = __dsub_rn(__dadd_rn(s + cmp, __dmul_rn(a.lam, Xs[i * DRP + k])), __ldg(&a.rhs[e]));
+          if (rp) a.rhs[e] = s + cmp;
+          else a.R[e] = __dsub_rn(__dadd_rn(s + cmp, __dmul_rn(a.lam, Xs[i * DRP + k])), __ldcg(&a.rhs[e]));
         }
       }
     }
     KS_STAMP(3)
     grid.sync();
     KS_STAMP(4)
+    if (rp) {
+      tol = init_tol();
+      continue;
+    }
     if (prof) g_prof[it * 6 + 3] = clock64();
     // ---------------- P3 / P4: preconditioner ----------------
     precond_a(a.R);
@@ -480,15 +509,21 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
       if (pending[k]) mbar_wait(&bars[k], phase[k]);
 }
 
-// dst row i = src row rows[i] (d entries) + padding; pad slot 0 carries extra[i] if given.
+// dst row i = src row rows[i] (d entries) + padding; pad slot 0 carries extra[i] if given, pad
+// slot 1 carries extra[i] * b[perm[i]] if b is given (v_t b_t of the right-hand side).
 __global__ void pack_rows_kernel(const double* __restrict__ src, int64_t ld, const int64_t* __restrict__ rows,
                                  int64_t n, int d, int dp, const double* __restrict__ extra,
+                                 const double* __restrict__ b, const int64_t* __restrict__ perm,
                                  double* __restrict__ dst) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= n * dp) return;
   const int64_t i = e / dp;
   const int c = (int)(e - i * dp);
-  dst[e] = (c < d) ? src[rows[i] * ld + c] : ((c == d && extra) ? extra[i] : 0.0);
+  double v = 0.0;
+  if (c < d) v = src[rows[i] * ld + c];
+  else if (c == d && extra) v = extra[i];
+  else if (c == d + 1 && b) v = __dmul_rn(extra[i], b[perm ? perm[i] : i]);
+  dst[e] = v;
 }
 
 __global__ void transpose_sq_kernel2(const double* __restrict__ a, int d, double* __restrict__ out) {
@@ -618,8 +653,11 @@ bool persistent_supported(int dL, int dR) {
   return ok(dL) && ok(dR);
 }
 
+// rhs_in_kernel: rhs is an output, built from b_at (sparse-diagonal order) and perm (grouped ->
+// sparse-diagonal position, null when identical); dinv null: formed from wL, wR and lam.
 int richardson_persistent(cudaStream_t st, const ks_sketch_view* sk, const double* VL, const double* VR,
-                          const double* dinv, const double* rhs, double lam, double damping, int max_iters,
+                          const double* dinv, const double* wL, const double* wR, double* rhs, bool rhs_in_kernel,
+                          const double* b_at, const int64_t* perm, double lam, double damping, int max_iters,
                           double residual_tol, double* x, double* hist, int* iters, int* hist_len, int* status) {
   const int dL = sk->dL, dR = sk->dR;
   KS_REQUIRE(max_iters <= 1024, KS_ESIZE, "persistent loop keeps <= 1024 history entries");
@@ -642,16 +680,17 @@ int richardson_persistent(cudaStream_t st, const ks_sketch_view* sk, const doubl
                                      cpre.p, drange.p, drange.p + grid + 1);
   KS_CHECK_LAUNCH();
   pack_rows_kernel<<<ceil_div_u(ul * dLp, 256), 256, 0, st>>>(sk->Lmat, sk->ldl, sk->lrow, ul, dL, dLp, nullptr,
-                                                               Lpack.p);
+                                                               nullptr, nullptr, Lpack.p);
   KS_CHECK_LAUNCH();
   pack_rows_kernel<<<ceil_div_u(nnz * dRp, 256), 256, 0, st>>>(sk->Rmat, sk->ldr, sk->rrow, nnz, dR, dRp, sk->v,
-                                                                Rpack.p);
+                                                                rhs_in_kernel ? b_at : nullptr, perm, Rpack.p);
   KS_CHECK_LAUNCH();
   transpose_sq_kernel2<<<ceil_div_u((int64_t)dR * dR, 256), 256, 0, st>>>(VR, dR, VRt.p);
   KS_CHECK_LAUNCH();
   PArgs a{};
   a.Lpack = Lpack.p; a.Rpack = Rpack.p; a.seg = sk->seg; a.chunks = dch.p; a.range = drange.p;
-  a.VL = VL; a.VR = VR; a.VRt = VRt.p; a.dinv = dinv; a.rhs = rhs;
+  a.VL = VL; a.VR = VR; a.VRt = VRt.p; a.dinv = dinv; a.wL = wL; a.wR = wR; a.rhs = rhs;
+  a.rhs_in_kernel = rhs_in_kernel ? 1 : 0;
   a.lam = lam; a.damping = damping; a.residual_tol = residual_tol; a.max_iters = max_iters;
   a.part = part.p; a.R = R.p; a.T = T.p; a.step = stepb.p; a.rowsq = rowsq.p; a.x_out = x; a.hist = hist;
   a.state = state.p;

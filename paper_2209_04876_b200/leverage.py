@@ -82,20 +82,27 @@ class DeferredChecks:
 
     def __init__(self):
         self.items = []
+        self._host = None
 
     def add(self, flags: torch.Tensor, handler):
         self.items.append((flags, handler))
 
-    def run(self):
-        items, self.items = self.items, []
-        if not items:
-            return
-        vals = torch.cat([f.reshape(-1).to(torch.int64) for f, _ in items]).cpu().tolist()
-        off = 0
-        for f, handler in items:
-            n = f.numel()
-            handler(vals[off:off + n])
-            off += n
+    def stage(self):
+        """Queue the device->host copies of every flag on the current stream (no wait); a later
+        stream synchronisation (e.g. the Richardson launch's own) completes them."""
+        self._host = [(f.to("cpu", non_blocking=True), h) for f, h in self.items]
+        self.items = []
+
+    def run(self, synced: bool = False):
+        """Evaluate the handlers.  ``synced``: the stream was synchronised after stage()."""
+        if self._host is None:
+            self.stage()
+            synced = False
+        if not synced:
+            torch.cuda.current_stream().synchronize()
+        staged, self._host = self._host, None
+        for f, handler in staged:
+            handler(f.reshape(-1).tolist())
 
 
 _DEFERRED: list = [None]

@@ -545,6 +545,7 @@ class _PrefixGraph:
 
 
 _PREFIX_GRAPHS: dict = {}
+_USE_FUSED = [True]  # fused right-hand side + loop kernel for single-factor groups
 _PREFIX_STATS = {"eager": 0, "capture": 0, "replay": 0}
 _USE_GRAPHS = [True]
 
@@ -677,43 +678,64 @@ def _fast_solve_pass(facs, b, config: RegressionConfig, caches, trace, use_chol:
     _mark("gather b")
     view = _view_for(facs, sdiag)
     _mark("sketch view")
-    bv = (sdiag.values * b_at).contiguous()
-    rhs = D.empty(view.dL, view.dR)
-    _lib.call("ks_sketched_transpose_apply", ctypes.byref(view.struct), D.p(bv), D.p(view.perm_arg()), D.p(rhs),
-              D.stream())
-    _mark("rhs")
-    # preconditioner in grouped (left | right) order
-    grams = _join_grams(grams)
-    eig = reduce(torch.kron, [w for _, w in grams])
-    dinv = pseudo_reciprocal(eig + lam)
     left, right = view.part.left, view.part.right
-    VL = reduce(torch.kron, [grams[i][0] for i in left]) if left else torch.ones(1, 1, dtype=D.F64,
-                                                                                 device=D.dev())
-    VR = reduce(torch.kron, [grams[i][0] for i in right])
-    VL = VL.contiguous()
-    VR = VR.contiguous()
-    dg = view.to_groups(dinv).contiguous()
-    x = D.empty(view.dL, view.dR)
     max_iters = config.effective_max_iters
+    x = D.empty(view.dL, view.dR)
     hist = D.zeros(max(1, max_iters))
+    rhs = D.empty(view.dL, view.dR)
     iters = ctypes.c_int32(0)
     hlen = ctypes.c_int32(0)
     lib = _lib.load()
-    _mark("precond")
-    rc = lib.ks_richardson_sketched(ctypes.byref(view.struct), D.p(VL), D.p(VR), D.p(dg), D.p(rhs),
-                                    float(lam), float(config.effective_damping), int(max_iters),
-                                    float(config.residual_tol), D.p(x), D.p(hist), ctypes.byref(iters),
-                                    ctypes.byref(hlen), D.stream())
+    fused = (_USE_FUSED[0] and len(left) == 1 and len(right) == 1 and view.dL in (16, 32, 64)
+             and view.dR in (16, 32, 64) and view.nnz > 0 and max_iters <= 1024)
+    dg = VL = VR = None
+    if fused:
+        # right-hand side, preconditioner diagonal and the loop in one persistent launch
+        grams = _join_grams(grams)
+        VL, wL = grams[left[0]]
+        VR, wR = grams[right[0]]
+        _mark("precond")
+        deferred.stage()  # flag copies complete with the loop launch's own synchronisation
+        rc = lib.ks_richardson_fused(ctypes.byref(view.struct), D.p(view.perm_arg()), D.p(b_at.contiguous()),
+                                     D.p(VL), D.p(wL), D.p(VR), D.p(wR), None, float(lam),
+                                     float(config.effective_damping), int(max_iters), float(config.residual_tol),
+                                     D.p(x), D.p(hist), D.p(rhs), ctypes.byref(iters), ctypes.byref(hlen),
+                                     D.stream())
+        if trace is not None:
+            dg = view.to_groups(pseudo_reciprocal(torch.kron(wL, wR) + lam)).contiguous()
+    else:
+        bv = (sdiag.values * b_at).contiguous()
+        _lib.call("ks_sketched_transpose_apply", ctypes.byref(view.struct), D.p(bv), D.p(view.perm_arg()),
+                  D.p(rhs), D.stream())
+        _mark("rhs")
+        # preconditioner in grouped (left | right) order
+        grams = _join_grams(grams)
+        eig = reduce(torch.kron, [w for _, w in grams])
+        dinv = pseudo_reciprocal(eig + lam)
+        VL = reduce(torch.kron, [grams[i][0] for i in left]) if left else torch.ones(1, 1, dtype=D.F64,
+                                                                                     device=D.dev())
+        VR = reduce(torch.kron, [grams[i][0] for i in right])
+        VL = VL.contiguous()
+        VR = VR.contiguous()
+        dg = view.to_groups(dinv).contiguous()
+        _mark("precond")
+        deferred.stage()  # flag copies complete with the loop launch's own synchronisation
+        rc = lib.ks_richardson_sketched(ctypes.byref(view.struct), D.p(VL), D.p(VR), D.p(dg), D.p(rhs),
+                                        float(lam), float(config.effective_damping), int(max_iters),
+                                        float(config.residual_tol), D.p(x), D.p(hist), ctypes.byref(iters),
+                                        ctypes.byref(hlen), D.stream())
     _mark("richardson")
     _lev._DEFERRED[0] = None
-    deferred.run()  # generator / Cholesky / sampler-table flags, one host round trip
+    deferred.run(synced=True)  # generator / Cholesky / sampler-table flags, copied with the loop launch
     history = hist[: hlen.value].cpu().tolist()
     if rc == _lib.KS_EDIVERGED:
         raise NumericalFailureError("Richardson iteration diverged", iterations=iters.value,
                                     diagnostics={"residual_history": history})
     _lib.check(rc, "ks_richardson_sketched")
     if trace is not None:
-        trace.loop_inputs = dict(view=view, VL=VL, VR=VR, dinv=dg, rhs=rhs, lam=float(lam),
+        trace.loop_inputs = dict(view=view, VL=VL, VR=VR, dinv=dg, rhs=rhs, lam=float(lam), b_at=b_at,
+                                 wL=grams[left[0]][1] if len(left) == 1 else None,
+                                 wR=grams[right[0]][1] if len(right) == 1 else None,
                                  damping=float(config.effective_damping), max_iters=int(max_iters),
                                  tol=float(config.residual_tol))
         trace.scores = scores

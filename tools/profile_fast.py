@@ -71,6 +71,25 @@ if "--loop" in sys.argv:
         return statistics.median(ts)
 
     print("loop us (solve inputs):", timed(li["VL"], li["VR"], li["dinv"], li["rhs"]), "iters", it.value)
+    if li.get("wL") is not None:
+        rhs2 = D.empty(view.dL, view.dR)
+
+        def fused():
+            rc = _lib.load().ks_richardson_fused(ctypes.byref(view.struct), D.p(view.perm_arg()), D.p(li["b_at"]),
+                                                 D.p(li["VL"]), D.p(li["wL"]), D.p(li["VR"]), D.p(li["wR"]), None,
+                                                 li["lam"], li["damping"], li["max_iters"], li["tol"], D.p(x),
+                                                 D.p(hist), D.p(rhs2), ctypes.byref(it), ctypes.byref(hl), D.stream())
+            assert rc == 0, rc
+        fused()
+        ts = []
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fused()
+            e1.record()
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1) * 1e3)
+        print("fused rhs+loop us:", statistics.median(ts), "iters", it.value)
     _lib.load().ks_debug_richardson_phases(it.value, ph)
     print("  phases:", [round(v) for v in ph])
     eyeL = torch.eye(view.dL, dtype=torch.float64, device="cuda")
