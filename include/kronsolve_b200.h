@@ -258,6 +258,10 @@ int ks_debug_jacobi_sweeps(int32_t* out8);
  * apply, sync, reduce, precond-A, precond-B, update. */
 int ks_debug_richardson_phases(int32_t iters, double* out6);
 
+/* Profiling aid: CTA 0's apply phase of the last persistent run split into mbarrier wait, Y GEMM,
+ * sample loop and G GEMM (average SM cycles per iteration). */
+int ks_debug_richardson_apply_split(int32_t iters, double* out4);
+
 /* Preconditioner apply y = (VL kron VR) diag(dinv) (VL kron VR)^T r (solvers.py:180-183). */
 int ks_kron_precond_apply(const double* VL, const double* VR, int32_t dL, int32_t dR,
                           const double* dinv, const double* r, double* y, void* stream);

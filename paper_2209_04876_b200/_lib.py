@@ -76,6 +76,7 @@ _SIGS = {
                                 POINTER(c_int32), POINTER(c_int32), _p], ctypes.c_int),
     "ks_kron_precond_apply": ([_p, _p, _i32, _i32, _p, _p, _p, _p], ctypes.c_int),
     "ks_debug_richardson_phases": ([_i32, POINTER(c_double)], ctypes.c_int),
+    "ks_debug_richardson_apply_split": ([_i32, POINTER(c_double)], ctypes.c_int),
 }
 
 _lock = threading.Lock()

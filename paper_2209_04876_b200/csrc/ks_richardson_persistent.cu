@@ -29,7 +29,7 @@ namespace {
 constexpr int PT = 256;      // threads per CTA
 constexpr int PW = PT / 32;  // warps
 constexpr int CH_ROWS = 16;  // distinct left rows per chunk (one half-warp each)
-constexpr int CH_S = 128;    // samples per chunk
+constexpr int CH_S = 64;     // samples per chunk (>= DL: the free slab holds a DL x DRP matrix)
 constexpr int PAD = 4;       // row padding (doubles) of packed / staged rows
 
 struct Chunk {
@@ -64,6 +64,7 @@ struct PArgs {
 };
 
 __device__ long long g_prof[6 * 1024];
+__device__ long long g_p1split[4];  // CTA 0, summed over iterations: mbarrier wait, Y, samples, G
 __device__ unsigned long long g_cta_ts[256 * 9];  // per-CTA globaltimer stamps of iteration 5
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -78,7 +79,9 @@ template <int DL, int DR>
 struct Smem {
   static constexpr int DLP = DL + PAD, DRP = DR + PAD;
   static constexpr int X_OFF = 0;                          // DL x DRP
-  static constexpr int L_OFF = X_OFF + DL * DRP;           // 2 x CH_ROWS x DLP
+  static constexpr int VR_OFF = X_OFF + DL * DRP;          // DR x DRP (resident)
+  static constexpr int VRT_OFF = VR_OFF + DR * DRP;        // DR x DRP (resident, VR^T)
+  static constexpr int L_OFF = VRT_OFF + DR * DRP;         // 2 x CH_ROWS x DLP
   static constexpr int R_OFF = L_OFF + 2 * CH_ROWS * DLP;  // 2 x CH_S x DRP
   static constexpr int Y_OFF = R_OFF + 2 * CH_S * DRP;     // CH_ROWS x DRP
   static constexpr int Z_OFF = Y_OFF + CH_ROWS * DRP;      // CH_ROWS x DRP
@@ -86,7 +89,7 @@ struct Smem {
   static constexpr int H_OFF = W_OFF + 256;                // history (<= 1024)
   static constexpr int DOUBLES = H_OFF + 1024;
   static constexpr size_t BYTES = (size_t)DOUBLES * 8 + 64;  // + mbarriers
-  static_assert(CH_S >= DL + DR, "staging of R/T and VR needs the free slab buffer");
+  static_assert(CH_S >= DL, "staging of R / T needs the free slab buffer");
 };
 
 __device__ __forceinline__ void bulk_copy(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -175,10 +178,9 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
   // --- preconditioner phases: operands staged in the free slab buffer and the Y/Z region ---
   auto precond_a = [&](const double* Rin) {
     double* Rs = sm + S::R_OFF + (cur ^ 1) * CH_S * DRP;
-    double* VRs = Rs + DL * DRP;
+    const double* VRs = sm + S::VR_OFF;
     for (int r = b; r < DL; r += G) {
       stage(Rs, Rin, DL, DR, DRP, true);
-      stage(VRs, a.VR, DR, DR, DRP, false);
       for (int k = tid; k < DL; k += PT) Ws[k] = __ldg(&a.VL[k * DL + r]);
       cp_async_wait_all();
       __syncthreads();
@@ -207,10 +209,9 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
   };
   auto precond_b = [&]() {
     double* Ts = sm + S::R_OFF + (cur ^ 1) * CH_S * DRP;
-    double* VRts = Ts + DL * DRP;
+    const double* VRts = sm + S::VRT_OFF;
     for (int r = b; r < DL; r += G) {
       stage(Ts, a.T, DL, DR, DRP, true);
-      stage(VRts, a.VRt, DR, DR, DRP, false);
       for (int k = tid; k < DL; k += PT) Ws[k] = __ldg(&a.VL[r * DL + k]);
       cp_async_wait_all();
       __syncthreads();
@@ -252,6 +253,11 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
     return v;
   };
 
+  // VR and VR^T stay resident for the whole solve
+  stage(sm + S::VR_OFF, a.VR, DR, DR, DRP, false);
+  stage(sm + S::VRT_OFF, a.VRt, DR, DR, DRP, false);
+  cp_async_wait_all();
+  __syncthreads();
   // tol = residual_tol * ||P rhs|| (solvers.py:212-214)
   auto init_tol = [&]() {
     precond_a(a.rhs);
@@ -269,6 +275,7 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
 
   int status = 0, iters = 0, hlen = 0;
   const bool prof = (b == 0 && tid == 0);
+  long long p1acc[4] = {0, 0, 0, 0};
   // it == -1: the right-hand-side pass (same chunk pipeline, s_t = v_t (v_t b_t), no Y)
   const int it0 = a.rhs_in_kernel ? -1 : 0;  // first pass: a CTA with a single (resident) chunk waits only here
   for (int it = it0; it < a.max_iters; it++) {
@@ -289,11 +296,14 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
           pending[buf ^ 1] = 1;
         }
       }
+      long long pc0 = 0;
+      if (prof) pc0 = clock64();
       if (!resident || it == it0) {
         mbar_wait(&bars[buf], phase[buf]);
         phase[buf] ^= 1;
         pending[buf] = 0;
       }
+      if (prof && !rp) p1acc[0] += clock64() - pc0;
       const double* Ls = sm + S::L_OFF + buf * CH_ROWS * DLP;
       const double* Rs = sm + S::R_OFF + buf * CH_S * DRP;
       const int nrows = (int)(ch.u_e - ch.u_b);
@@ -318,6 +328,7 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
         }
       }
       __syncthreads();
+      if (prof && !rp) { const long long now = clock64(); p1acc[1] += now - pc0; pc0 = now; }
       // samples: half-warp per left row, QE consecutive right-row entries per lane
       {
         const int r = tid >> 4, ql = tid & 15;
@@ -331,7 +342,41 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
           double y[QE];
 #pragma unroll
           for (int j = 0; j < QE; j++) y[j] = rp ? 0.0 : Ys[r * DRP + ql * QE + j];
-          for (int64_t t = tb; t < te; t++) {
+          // two samples per step: their dot products and shuffle reductions are independent, so
+          // the latencies overlap; z accumulates in sample order as before
+          int64_t t = tb;
+          for (; t + 1 < te; t += 2) {
+            const double* Rt0 = Rs + (int)(t - ch.t_b) * DRP;
+            const double* Rt1 = Rt0 + DRP;
+            double rv0[QE], rv1[QE];
+            double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+            for (int j = 0; j < QE; j++) {
+              rv0[j] = Rt0[ql * QE + j];
+              rv1[j] = Rt1[ql * QE + j];
+              d0 = fma(y[j], rv0[j], d0);
+              d1 = fma(y[j], rv1[j], d1);
+            }
+            const double vt0 = Rt0[DR], vt1 = Rt1[DR];  // v_t and v_t b_t travel in the row padding
+            double s0, s1;
+            if (rp) {
+              s0 = vt0 * Rt0[DR + 1];
+              s1 = vt1 * Rt1[DR + 1];
+            } else {
+#pragma unroll
+              for (int o = 1; o < 16; o <<= 1) {
+                const double e0 = __shfl_xor_sync(qmask, d0, o);
+                const double e1 = __shfl_xor_sync(qmask, d1, o);
+                d0 += e0;
+                d1 += e1;
+              }
+              s0 = vt0 * (vt0 * d0);
+              s1 = vt1 * (vt1 * d1);
+            }
+#pragma unroll
+            for (int j = 0; j < QE; j++) z[j] = fma(s1, rv1[j], fma(s0, rv0[j], z[j]));
+          }
+          if (t < te) {
             const double* Rt = Rs + (int)(t - ch.t_b) * DRP;
             double rv[QE];
             double d = 0.0;
@@ -340,15 +385,13 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
               rv[j] = Rt[ql * QE + j];
               d = fma(y[j], rv[j], d);
             }
-            const double vt = Rt[DR];  // v_t and v_t b_t travel in the row padding
+            const double vt = Rt[DR];
             double s;
             if (rp) {
               s = vt * Rt[DR + 1];
             } else {
-              d += __shfl_xor_sync(qmask, d, 1);
-              d += __shfl_xor_sync(qmask, d, 2);
-              d += __shfl_xor_sync(qmask, d, 4);
-              d += __shfl_xor_sync(qmask, d, 8);
+#pragma unroll
+              for (int o = 1; o < 16; o <<= 1) d += __shfl_xor_sync(qmask, d, o);
               s = vt * (vt * d);
             }
 #pragma unroll
@@ -359,6 +402,7 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
         for (int j = 0; j < QE; j++) Zs[r * DRP + ql * QE + j] = z[j];
       }
       __syncthreads();
+      if (prof && !rp) { const long long now = clock64(); p1acc[2] += now - pc0; pc0 = now; }
       // G += L_chunk^T Z   (K = CH_ROWS; rows >= nrows have Z == 0)
 #pragma unroll
       for (int gi = 0; gi < G_PER_W; gi++) {
@@ -376,6 +420,7 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
         }
       }
       __syncthreads();
+      if (prof && !rp) p1acc[3] += clock64() - pc0;
       if (!resident) buf ^= 1;
     }
     cur = buf;
@@ -484,9 +529,16 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
       status = 2;
       break;
     }
-    for (int e = tid; e < NE; e += PT) {
-      const int i = e / DR, k = e - i * DR;
-      Xs[i * DRP + k] = __dsub_rn(Xs[i * DRP + k], __dmul_rn(a.damping, __ldcg(&a.step[e])));
+    {
+      // stage the step (written by other CTAs) with asynchronous copies, then update x
+      double* St = sm + S::R_OFF + (cur ^ 1) * CH_S * DRP;
+      stage(St, a.step, DL, DR, DRP, true);
+      cp_async_wait_all();
+      __syncthreads();
+      for (int e = tid; e < NE; e += PT) {
+        const int i = e / DR, k = e - i * DR;
+        Xs[i * DRP + k] = __dsub_rn(Xs[i * DRP + k], __dmul_rn(a.damping, St[i * DRP + k]));
+      }
     }
     iters = it + 1;
     __syncthreads();
@@ -498,6 +550,7 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
     }
     for (int i = tid; i < hlen; i += PT) a.hist[i] = Hs[i];
     if (tid == 0) {
+      for (int k = 0; k < 4; k++) g_p1split[k] = p1acc[k];
       a.state[0] = status;
       a.state[1] = iters;
       a.state[2] = hlen;
@@ -539,10 +592,37 @@ __global__ void transpose_sq_kernel2(const double* __restrict__ a, int d, double
 // total * (b+1) / G exceeds the chunk's cost midpoint).  Costs are integers, so the plan is
 // exact and deterministic.  One block.
 constexpr int PLAN_T = 1024;
+
+// Piece k of the group whose rows are [ub, ue) and samples [sb, se): its chunk and cost.
+__device__ __forceinline__ int64_t plan_piece(const int64_t* __restrict__ seg, int64_t ub, int64_t ue, int64_t sb,
+                                              int64_t se, int64_t k, int64_t wchunk, int64_t wsamp, int64_t wlong,
+                                              Chunk& ch) {
+  ch.t_b = sb + k * CH_S;
+  ch.t_e = min(se, ch.t_b + CH_S);
+  // rows touched by the piece: seg[u] <= t < seg[u + 1]
+  int64_t lo = ub, hi = ue - 1;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi + 1) >> 1;
+    if (seg[mid] <= ch.t_b) lo = mid; else hi = mid - 1;
+  }
+  ch.u_b = lo;
+  lo = ch.u_b;
+  hi = ue - 1;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi + 1) >> 1;
+    if (seg[mid] <= ch.t_e - 1) lo = mid; else hi = mid - 1;
+  }
+  ch.u_e = lo + 1;
+  // the sample phase runs the chunk's rows in parallel: its time follows the longest row
+  int64_t longest = 0;
+  for (int64_t u = ch.u_b; u < ch.u_e; u++) longest = max(longest, min(seg[u + 1], ch.t_e) - max(seg[u], ch.t_b));
+  return wchunk + (ch.t_e - ch.t_b) * wsamp + longest * wlong;
+}
+
 __global__ void __launch_bounds__(PLAN_T) plan_kernel(const int64_t* __restrict__ seg, int64_t ul, int G,
-                                                      int64_t wrow, int64_t wsamp, Chunk* __restrict__ chunks,
-                                                      int64_t* __restrict__ cprefix, int64_t* __restrict__ range,
-                                                      int64_t* __restrict__ nchunks) {
+                                                      int64_t wchunk, int64_t wsamp, int64_t wlong,
+                                                      Chunk* __restrict__ chunks, int64_t* __restrict__ cprefix,
+                                                      int64_t* __restrict__ range, int64_t* __restrict__ nchunks) {
   __shared__ int64_t wsum_p[32], wsum_c[32];
   __shared__ int64_t carry_p, carry_c;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -558,7 +638,10 @@ __global__ void __launch_bounds__(PLAN_T) plan_kernel(const int64_t* __restrict_
       sb = seg[ub];
       se = seg[ue];
       pieces = max((int64_t)1, (se - sb + CH_S - 1) / CH_S);
-      cost = pieces * wrow + (se - sb) * wsamp;
+      for (int64_t k = 0; k < pieces; k++) {
+        Chunk ch;
+        cost += plan_piece(seg, ub, ue, sb, se, k, wchunk, wsamp, wlong, ch);
+      }
     }
     // block-wide inclusive scans of (pieces, cost)
     int64_t vp = pieces, vc = cost;
@@ -586,23 +669,8 @@ __global__ void __launch_bounds__(PLAN_T) plan_kernel(const int64_t* __restrict_
       int64_t c = ip - pieces, acc = ic - cost;
       for (int64_t k = 0; k < pieces; k++, c++) {
         Chunk ch;
-        ch.t_b = sb + k * CH_S;
-        ch.t_e = min(se, ch.t_b + CH_S);
-        // rows touched by the piece: seg[u] <= t < seg[u + 1]
-        int64_t lo = ub, hi = ue - 1;
-        while (lo < hi) {
-          const int64_t mid = (lo + hi + 1) >> 1;
-          if (seg[mid] <= ch.t_b) lo = mid; else hi = mid - 1;
-        }
-        ch.u_b = lo;
-        lo = ch.u_b; hi = ue - 1;
-        while (lo < hi) {
-          const int64_t mid = (lo + hi + 1) >> 1;
-          if (seg[mid] <= ch.t_e - 1) lo = mid; else hi = mid - 1;
-        }
-        ch.u_e = lo + 1;
+        const int64_t cc = plan_piece(seg, ub, ue, sb, se, k, wchunk, wsamp, wlong, ch);
         chunks[c] = ch;
-        const int64_t cc = wrow + (ch.t_e - ch.t_b) * wsamp;
         cprefix[c] = 2 * acc + cc;  // twice the cost midpoint (integers)
         acc += cc;
       }
@@ -639,6 +707,9 @@ int launch(cudaStream_t st, PArgs& a, int grid) {
   KS_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, PT, S::BYTES));
   KS_REQUIRE(per_sm >= 1 && grid <= per_sm * ks::num_sms(), KS_ESIZE,
              "persistent Richardson kernel does not fit co-resident");
+  const int ne = DL * DR, epc = ((ne + grid - 1) / grid + 1) & ~1;
+  KS_REQUIRE((int64_t)grid * epc <= (int64_t)CH_S * S::DRP, KS_ESIZE,
+             "partial-sum staging exceeds the slab buffer for grid %d", grid);
   void* args[] = {&a};
   KS_TRY_CUDA(cudaLaunchCooperativeKernel((void*)kern, grid, PT, args, S::BYTES, st));
   return KS_OK;
@@ -674,9 +745,11 @@ int richardson_persistent(cudaStream_t st, const ks_sketch_view* sk, const doubl
   KS_REQUIRE(Lpack.p && Rpack.p && part.p && R.p && T.p && stepb.p && rowsq.p && VRt.p && dch.p && drange.p &&
                  cpre.p && state.p,
              KS_ECUDA, "scratch allocation failed");
-  // estimated chunk cost: DMMA work is fixed per chunk (CH_ROWS-row tiles), samples add the
-  // half-warp dot/axpy loop
-  plan_kernel<<<1, PLAN_T, 0, st>>>(sk->seg, ul, grid, (int64_t)4 * CH_ROWS * dL * dR, (int64_t)24 * dR, dch.p,
+  // estimated chunk cost (SM cycles): the Y and G DMMA tiles are fixed per chunk (the FP64 tensor
+  // pipe issues one m16n8k4 per ~8 cycles per SM), the sample phase follows the chunk's longest
+  // row (~120 cycles per sample pair-step), plus shared-memory traffic per sample
+  const int64_t dmma = (int64_t)(CH_ROWS / 16) * (dR / 8) * (dL / 4) + (int64_t)(dL / 16) * (dR / 8) * (CH_ROWS / 4);
+  plan_kernel<<<1, PLAN_T, 0, st>>>(sk->seg, ul, grid, 8 * dmma + 600, (int64_t)dR / 4, 120, dch.p,
                                      cpre.p, drange.p, drange.p + grid + 1);
   KS_CHECK_LAUNCH();
   pack_rows_kernel<<<ceil_div_u(ul * dLp, 256), 256, 0, st>>>(sk->Lmat, sk->ldl, sk->lrow, ul, dL, dLp, nullptr,
@@ -720,6 +793,14 @@ int richardson_persistent(cudaStream_t st, const ks_sketch_view* sk, const doubl
 // Average cycles of CTA 0 per phase over the last persistent run:
 // apply (P1), sync wait after P1, reduce (P2 + sync), precond A (P3 + sync), precond B (P4 + sync),
 // update + loop overhead.
+extern "C" int ks_debug_richardson_apply_split(int32_t iters, double* out4) {
+  if (iters < 1) return KS_EINVAL;
+  long long h[4];
+  KS_TRY_CUDA(cudaMemcpyFromSymbol(h, g_p1split, sizeof(h)));
+  for (int k = 0; k < 4; k++) out4[k] = (double)h[k] / iters;
+  return KS_OK;
+}
+
 extern "C" int ks_debug_richardson_phases(int32_t iters, double* out6) {
   if (iters < 2 || iters > 1024) return KS_EINVAL;
   std::vector<long long> h(6 * iters);

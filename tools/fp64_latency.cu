@@ -3,6 +3,29 @@
 #include <cstdio>
 #include <cuda_runtime.h>
 
+__device__ __forceinline__ void dmma(double* c, double a0, double a1, double b0) {
+  asm volatile("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
+               : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+               : "d"(a0), "d"(a1), "d"(b0));
+}
+
+// CHAINS independent accumulators per warp, WARPS warps per block
+template <int CHAINS>
+__global__ void dmma_kernel(int n, double* out, long long* cyc) {
+  double c[CHAINS][4] = {};
+  const double a0 = 1e-3 * threadIdx.x, a1 = 2e-3, b0 = 0.5;
+  long long t0 = clock64();
+  for (int i = 0; i < n; i++) {
+#pragma unroll
+    for (int k = 0; k < CHAINS; k++) dmma(c[k], a0, a1, b0);
+  }
+  long long t1 = clock64();
+  if (threadIdx.x == 0) *cyc = (t1 - t0);
+  double s = 0;
+  for (int k = 0; k < CHAINS; k++) s += c[k][0] + c[k][1] + c[k][2] + c[k][3];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 template <int OP>
 __global__ void lat_kernel(int n, double x0, double* out, long long* cyc) {
   double a = x0 + threadIdx.x * 1e-9, b = 1.0000001, c = 1e-7;
@@ -38,5 +61,13 @@ int main() {
   cudaDeviceSynchronize();                                           \
   printf("%-16s %6.1f cycles/op\n", names[OP], (double)*cyc / n);
   RUN(0) RUN(1) RUN(2) RUN(3) RUN(4) RUN(5) RUN(6) RUN(7) RUN(8)
+#define DM(CH, W)                                                              \
+  dmma_kernel<CH><<<1, 32 * W>>>(1024, out, cyc);                              \
+  cudaDeviceSynchronize();                                                     \
+  dmma_kernel<CH><<<1, 32 * W>>>(1024, out, cyc);                              \
+  cudaDeviceSynchronize();                                                     \
+  printf("dmma chains %d warps %2d: %6.1f cycles per dmma-step (per warp), %5.2f cycles/dmma/SM\n", CH, W, \
+         (double)*cyc / 1024, (double)*cyc / 1024 / (CH * W));
+  DM(1, 1) DM(2, 1) DM(4, 1) DM(8, 1) DM(1, 4) DM(4, 4) DM(1, 8) DM(4, 8) DM(8, 8) DM(4, 16)
   return 0;
 }

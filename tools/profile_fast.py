@@ -44,6 +44,9 @@ ph = (ctypes.c_double * 6)()
 if _lib.load().ks_debug_richardson_phases(rep.iterations, ph) == 0:
     names = ["apply", "sync", "reduce+sync", "precondA+sync", "precondB+sync", "update"]
     print("richardson phases (cycles/iter):", {k: round(v) for k, v in zip(names, ph)})
+    sp = (ctypes.c_double * 4)()
+    if _lib.load().ks_debug_richardson_apply_split(rep.iterations, sp) == 0:
+        print("  apply split (cycles/iter):", {k: round(v) for k, v in zip(["wait", "Y", "samples", "G"], sp)})
 
 if "--loop" in sys.argv:
     li = tr.loop_inputs
@@ -92,12 +95,7 @@ if "--loop" in sys.argv:
         print("fused rhs+loop us:", statistics.median(ts), "iters", it.value)
     _lib.load().ks_debug_richardson_phases(it.value, ph)
     print("  phases:", [round(v) for v in ph])
-    eyeL = torch.eye(view.dL, dtype=torch.float64, device="cuda")
-    eyeR = torch.eye(view.dR, dtype=torch.float64, device="cuda")
-    ones = torch.ones(view.dL * view.dR, dtype=torch.float64, device="cuda")
-    print("loop us (identity precond):", timed(eyeL, eyeR, ones, li["rhs"]), "iters", it.value)
-    _lib.load().ks_debug_richardson_phases(it.value, ph)
-    print("  phases:", [round(v) for v in ph])
+
 
 if "--cta" in sys.argv:
     nct = torch.cuda.get_device_properties(0).multi_processor_count
