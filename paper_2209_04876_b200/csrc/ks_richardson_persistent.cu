@@ -329,7 +329,7 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
       }
       __syncthreads();
       if (prof && !rp) { const long long now = clock64(); p1acc[1] += now - pc0; pc0 = now; }
-      // samples: half-warp per left row, QE consecutive right-row entries per lane
+      // samples: half-warp per left row, entries ql, ql + 16, ... per lane (conflict-free)
       {
         const int r = tid >> 4, ql = tid & 15;
         const unsigned qmask = 0xffffu << (lane & 16);
@@ -341,7 +341,7 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
           const int64_t tb = max(a.seg[u], ch.t_b), te = min(a.seg[u + 1], ch.t_e);
           double y[QE];
 #pragma unroll
-          for (int j = 0; j < QE; j++) y[j] = rp ? 0.0 : Ys[r * DRP + ql * QE + j];
+          for (int j = 0; j < QE; j++) y[j] = rp ? 0.0 : Ys[r * DRP + ql + 16 * j];
           // two samples per step: their dot products and shuffle reductions are independent, so
           // the latencies overlap; z accumulates in sample order as before
           int64_t t = tb;
@@ -352,8 +352,8 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
             double d0 = 0.0, d1 = 0.0;
 #pragma unroll
             for (int j = 0; j < QE; j++) {
-              rv0[j] = Rt0[ql * QE + j];
-              rv1[j] = Rt1[ql * QE + j];
+              rv0[j] = Rt0[ql + 16 * j];
+              rv1[j] = Rt1[ql + 16 * j];
               d0 = fma(y[j], rv0[j], d0);
               d1 = fma(y[j], rv1[j], d1);
             }
@@ -382,7 +382,7 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
             double d = 0.0;
 #pragma unroll
             for (int j = 0; j < QE; j++) {
-              rv[j] = Rt[ql * QE + j];
+              rv[j] = Rt[ql + 16 * j];
               d = fma(y[j], rv[j], d);
             }
             const double vt = Rt[DR];
@@ -399,7 +399,7 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
           }
         }
 #pragma unroll
-        for (int j = 0; j < QE; j++) Zs[r * DRP + ql * QE + j] = z[j];
+        for (int j = 0; j < QE; j++) Zs[r * DRP + ql + 16 * j] = z[j];
       }
       __syncthreads();
       if (prof && !rp) { const long long now = clock64(); p1acc[2] += now - pc0; pc0 = now; }
