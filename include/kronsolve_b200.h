@@ -196,6 +196,16 @@ typedef struct ks_sketch_view {
   const int64_t* seg; const int64_t* lrow; const int64_t* rrow; const double* v;
 } ks_sketch_view;
 
+/* Two-factor fused form of ks_sketch_diag + ks_sketch_group (left group {0}, right group {1}):
+ * from the s draws idx (s x 2) and weights w builds the sparse diagonal (sd_idx, sd_val, sorted
+ * and deduplicated exactly as ks_sketch_diag) and its grouped view in the same pass: rrow[t] = i1
+ * of entry t, seg (u_left + 1 segment starts over the entries), lrow (u_left first-factor rows);
+ * the grouped order is the sparse-diagonal order (perm = identity, v = sd_val).  counts (host,
+ * 2) receives nnz and u_left.  Buffers hold s (seg: s + 1) entries.  Synchronises the stream. */
+int ks_sketch_diag_grouped2(const int64_t* idx, const int64_t* row_shape, const double* w, int64_t s,
+                            int64_t* sd_idx, double* sd_val, int64_t* seg, int64_t* lrow, int64_t* rrow,
+                            int64_t* counts, void* stream);
+
 /* Build the grouped view of a sparse diagonal (sorted unique flat row indices sd_idx with values
  * sd_val, nnz entries) for the factor split left_pos | right_pos (kron.balanced_partition,
  * kron.py:117-144).  Outputs (caller-allocated, nnz-sized): seg (nnz+1), lrow, rrow, v, perm

@@ -65,6 +65,59 @@ __global__ void nnz_kernel(const int32_t* __restrict__ head, const int64_t* __re
   out[0] = segid[n - 1] + head[n - 1];
 }
 
+// Two-factor fused path: unique-key heads and left-row heads of the sorted keys in one pass
+// (a unique key starts a new left row when its first factor's index differs from the
+// previous element's).
+__global__ void heads2_kernel(const uint64_t* __restrict__ keys, int64_t n, uint64_t n1,
+                              int32_t* __restrict__ head, int32_t* __restrict__ lhead) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const bool h = i == 0 || keys[i] != keys[i - 1];
+  head[i] = h ? 1 : 0;
+  lhead[i] = (h && (i == 0 || keys[i] / n1 != keys[i - 1] / n1)) ? 1 : 0;
+}
+
+// Segment values (as seg_sqrt_sum_kernel) plus the two-group view of the sparse diagonal:
+// right row = i1, left rows / segment starts at the left heads.
+__global__ void seg_sqrt_group2_kernel(const uint64_t* __restrict__ keys, const int64_t* __restrict__ perm,
+                                       const int32_t* __restrict__ head, const int64_t* __restrict__ segid,
+                                       const int32_t* __restrict__ lhead, const int64_t* __restrict__ lsegid,
+                                       int64_t n, uint64_t n1, const double* __restrict__ w,
+                                       int64_t* __restrict__ sd_idx, double* __restrict__ sd_val,
+                                       int64_t* __restrict__ seg, int64_t* __restrict__ lrow,
+                                       int64_t* __restrict__ rrow, int64_t* __restrict__ counts) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (i == n - 1) {
+    const int64_t nnz = segid[i] + head[i], ul = lsegid[i] + lhead[i];
+    counts[0] = nnz;
+    counts[1] = ul;
+    seg[ul] = nnz;
+  }
+  if (!head[i]) return;
+  int64_t e = i + 1;
+  while (e < n && !head[e]) e++;
+  const double w0 = w[perm[i]];
+  double acc = __dmul_rn(w0, w0);
+  if (e - i > 1) {
+    auto get = [&](int64_t j) {
+      const double x = w[perm[j]];
+      return __dmul_rn(x, x);
+    };
+    acc = acc + pw_sum_seq(get, i + 1, e - i - 1);
+  }
+  const int64_t g = segid[i];
+  const uint64_t key = keys[i];
+  sd_idx[g] = (int64_t)key;
+  sd_val[g] = __dsqrt_rn(acc);
+  rrow[g] = (int64_t)(key % n1);
+  if (lhead[i]) {
+    const int64_t u = lsegid[i];
+    seg[u] = g;
+    lrow[u] = (int64_t)(key / n1);
+  }
+}
+
 // ---- grouping of the sketched rows into (left group, right group) --------------------------
 
 struct GroupSpec {
@@ -371,6 +424,47 @@ extern "C" int ks_sketch_diag(int32_t nf, const int64_t* idx, const int64_t* row
   nnz_kernel<<<1, 1, 0, st>>>(head.p, segid.p, s, segid.p + s);
   KS_CHECK_LAUNCH();
   KS_TRY_CUDA(cudaMemcpyAsync(nnz, segid.p + s, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  KS_TRY_CUDA(cudaStreamSynchronize(st));
+  return KS_OK;
+}
+
+extern "C" int ks_sketch_diag_grouped2(const int64_t* idx, const int64_t* row_shape, const double* w, int64_t s,
+                                       int64_t* sd_idx, double* sd_val, int64_t* seg, int64_t* lrow, int64_t* rrow,
+                                       int64_t* counts, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (s <= 0) {
+    counts[0] = counts[1] = 0;
+    return KS_OK;
+  }
+  Shape8 rs{};
+  rs.v[0] = row_shape[0];
+  rs.v[1] = row_shape[1];
+  const uint64_t n1 = (uint64_t)row_shape[1];
+  const uint64_t rows = (uint64_t)row_shape[0] * n1;
+  int bits = 0;
+  while (bits < 64 && ((rows - 1) >> bits) != 0) bits++;
+  ks::Scratch<uint64_t> keys(s, st);
+  ks::Scratch<int64_t> perm(s, st);
+  ks::Scratch<int32_t> head(2 * s, st);
+  ks::Scratch<int64_t> segid(2 * s, st);
+  ks::Scratch<int64_t> dcounts(2, st);
+  KS_REQUIRE(keys.p && perm.p && head.p && segid.p && dcounts.p, KS_ECUDA, "scratch allocation failed");
+  int32_t* lhead = head.p + s;
+  int64_t* lsegid = segid.p + s;
+  ravel_kernel<<<ceil_div_u(s, 256), 256, 0, st>>>(idx, 2, rs, s, keys.p, perm.p);
+  KS_CHECK_LAUNCH();
+  int rc = ks::radix_sort_pairs(st, keys.p, perm.p, s, bits);
+  if (rc) return rc;
+  heads2_kernel<<<ceil_div_u(s, 256), 256, 0, st>>>(keys.p, s, n1, head.p, lhead);
+  KS_CHECK_LAUNCH();
+  rc = ks::scan_exclusive_i32(st, head.p, s, segid.p);
+  if (rc) return rc;
+  rc = ks::scan_exclusive_i32(st, lhead, s, lsegid);
+  if (rc) return rc;
+  seg_sqrt_group2_kernel<<<ceil_div_u(s, 128), 128, 0, st>>>(keys.p, perm.p, head.p, segid.p, lhead, lsegid, s, n1, w,
+                                                             sd_idx, sd_val, seg, lrow, rrow, dcounts.p);
+  KS_CHECK_LAUNCH();
+  KS_TRY_CUDA(cudaMemcpyAsync(counts, dcounts.p, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   KS_TRY_CUDA(cudaStreamSynchronize(st));
   return KS_OK;
 }

@@ -116,9 +116,84 @@ __global__ void __launch_bounds__(RS_T) rs_scatter_kernel(const uint64_t* __rest
   }
 }
 
+// Two-kernel exclusive scan for larger n: per-tile totals, then every tile scans its own
+// elements after summing the totals of the tiles before it (fixed order, deterministic).
+constexpr int SC_T = 512, SC_PER = 4, SC_TILE = SC_T * SC_PER;
+
+__global__ void __launch_bounds__(SC_T) tile_sum_kernel(const int32_t* __restrict__ in, int64_t n,
+                                                       int64_t* __restrict__ tsum) {
+  __shared__ int64_t red[SC_T / 32];
+  const int64_t base = (int64_t)blockIdx.x * SC_TILE;
+  int64_t v = 0;
+#pragma unroll
+  for (int k = 0; k < SC_PER; k++) {
+    const int64_t i = base + k * SC_T + threadIdx.x;
+    if (i < n) v += in[i];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t t = 0;
+    for (int w = 0; w < SC_T / 32; w++) t += red[w];
+    tsum[blockIdx.x] = t;
+  }
+}
+
+__global__ void __launch_bounds__(SC_T) tile_scan_kernel(const int32_t* __restrict__ in, int64_t n,
+                                                        const int64_t* __restrict__ tsum,
+                                                        int64_t* __restrict__ out) {
+  __shared__ int64_t wsum[SC_T / 32];
+  __shared__ int64_t s_off;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (wid == 0) {  // offset = sum of the preceding tiles' totals
+    int64_t o = 0;
+    for (int b = lane; b < (int)blockIdx.x; b += 32) o += tsum[b];
+#pragma unroll
+    for (int k = 16; k > 0; k >>= 1) o += __shfl_xor_sync(0xffffffffu, o, k);
+    if (lane == 0) s_off = o;
+  }
+  // each thread owns SC_PER consecutive elements
+  const int64_t base = (int64_t)blockIdx.x * SC_TILE + (int64_t)threadIdx.x * SC_PER;
+  int32_t x[SC_PER];
+  int64_t loc = 0;
+#pragma unroll
+  for (int k = 0; k < SC_PER; k++) {
+    x[k] = (base + k < n) ? in[base + k] : 0;
+    loc += x[k];
+  }
+  int64_t incl = loc;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) wsum[wid] = incl;
+  __syncthreads();
+  if (wid == 0) {
+    int64_t t = lane < SC_T / 32 ? wsum[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t u = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += u;
+    }
+    if (lane < SC_T / 32) wsum[lane] = t;
+  }
+  __syncthreads();
+  int64_t run = s_off + (wid ? wsum[wid - 1] : 0) + incl - loc;
+#pragma unroll
+  for (int k = 0; k < SC_PER; k++) {
+    if (base + k < n) out[base + k] = run;
+    run += x[k];
+  }
+}
+
 }  // namespace
 
 namespace ks {
+
+int scan_exclusive_i32(cudaStream_t st, const int32_t* in, int64_t n, int64_t* out);
 
 // Stable sort of n (key, value) pairs on the low `bits` bits of the key.  Result in
 // (keys, vals) (the input buffers are overwritten).
@@ -137,8 +212,8 @@ int radix_sort_pairs(cudaStream_t st, uint64_t* keys, int64_t* vals, int64_t n, 
     const int shift = p * RS_BITS;
     rs_hist_kernel<<<(unsigned)ntiles, RS_T, 0, st>>>(ka, n, shift, ntiles, hist.p);
     KS_CHECK_LAUNCH();
-    scan_small_kernel<<<1, 1024, 0, st>>>(hist.p, ntiles * RS_DIG, offs.p);
-    KS_CHECK_LAUNCH();
+    int rc = scan_exclusive_i32(st, hist.p, ntiles * RS_DIG, offs.p);
+    if (rc) return rc;
     rs_scatter_kernel<<<(unsigned)ntiles, RS_T, 0, st>>>(ka, va, n, shift, ntiles, offs.p, kb, vb);
     KS_CHECK_LAUNCH();
     std::swap(ka, kb);
@@ -153,7 +228,17 @@ int radix_sort_pairs(cudaStream_t st, uint64_t* keys, int64_t* vals, int64_t n, 
 
 int scan_exclusive_i32(cudaStream_t st, const int32_t* in, int64_t n, int64_t* out) {
   if (n <= 0) return KS_OK;
-  scan_small_kernel<<<1, 1024, 0, st>>>(in, n, out);
+  if (n <= 4096) {
+    scan_small_kernel<<<1, 1024, 0, st>>>(in, n, out);
+    KS_CHECK_LAUNCH();
+    return KS_OK;
+  }
+  const int64_t tiles = (n + SC_TILE - 1) / SC_TILE;
+  Scratch<int64_t> tsum(tiles, st);
+  KS_REQUIRE(tsum.p, KS_ECUDA, "scratch allocation failed");
+  tile_sum_kernel<<<(unsigned)tiles, SC_T, 0, st>>>(in, n, tsum.p);
+  KS_CHECK_LAUNCH();
+  tile_scan_kernel<<<(unsigned)tiles, SC_T, 0, st>>>(in, n, tsum.p, out);
   KS_CHECK_LAUNCH();
   return KS_OK;
 }

@@ -258,6 +258,32 @@ class _View:
         self.col_shape = tuple(cols)
         self.order = tuple(left) + tuple(right)
 
+    @classmethod
+    def from_parts(cls, facs, sd: SparseDiagonal, seg, lrow, rrow, u_left: int):
+        """Two-factor view already built by ks_sketch_diag_grouped2 (left {0}, right {1}; grouped
+        order == sparse-diagonal order)."""
+        v = object.__new__(cls)
+        v.facs = facs
+        rows = [int(a.shape[0]) for a in facs]
+        cols = [int(a.shape[1]) for a in facs]
+        v.part = balanced_partition(cols)
+        v.dL, v.dR = cols[0], cols[1]
+        v.nnz = sd.nnz
+        v.sd_idx, v.sd_val = sd.indices, sd.values
+        v.seg, v.lrow, v.rrow = seg, lrow, rrow
+        v.v = sd.values
+        v.perm = None
+        v.Lbuf = v.Rbuf = None
+        v.u_left = int(u_left)
+        v.prefix = True
+        v.Lmat, v.Rmat = facs[0], facs[1]
+        v.struct = _lib.SketchView(facs[0].data_ptr(), cols[0], v.dL, facs[1].data_ptr(), cols[1], v.dR, v.u_left,
+                                   v.nnz, seg.data_ptr(), lrow.data_ptr(), rrow.data_ptr(), sd.values.data_ptr())
+        v.col_shape = tuple(cols)
+        v.order = (0, 1)
+        del rows
+        return v
+
     def perm_arg(self):
         # grouped order == sparse-diagonal order when the left group is a prefix
         return None if self.prefix else self.perm
@@ -275,6 +301,32 @@ class _View:
         inv = tuple(int(i) for i in np.argsort(np.asarray(self.order)))
         shape = tuple(self.col_shape[i] for i in self.order)
         return g.reshape(shape).permute(inv).reshape(-1).contiguous()
+
+
+def sketch_diag_and_view2(facs, sketch_indices: torch.Tensor, sketch_weights: torch.Tensor):
+    """Sparse diagonal of a two-factor row sketch together with its grouped view (one fused
+    device pass, one host round trip); None when the factors' balanced partition is not
+    (left {0}, right {1})."""
+    cols = [int(a.shape[1]) for a in facs]
+    part = balanced_partition(cols)
+    if len(facs) != 2 or part.left != (0,) or part.right != (1,):
+        return None
+    rows = [int(a.shape[0]) for a in facs]
+    s = int(sketch_indices.shape[0])
+    sd_idx = D.empty(max(s, 1), dtype=D.I64)
+    sd_val = D.empty(max(s, 1))
+    seg = D.empty(s + 1, dtype=D.I64)
+    lrow = D.empty(max(s, 1), dtype=D.I64)
+    rrow = D.empty(max(s, 1), dtype=D.I64)
+    counts = (ctypes.c_int64 * 2)()
+    _lib.call("ks_sketch_diag_grouped2", D.p(sketch_indices.contiguous()), _lib.ptr_array(ctypes.c_int64, rows),
+              D.p(sketch_weights.contiguous()), s, D.p(sd_idx), D.p(sd_val), D.p(seg), D.p(lrow), D.p(rrow), counts,
+              D.stream())
+    nnz, ul = int(counts[0]), int(counts[1])
+    sd = SparseDiagonal._trusted(sd_idx[:nnz], sd_val[:nnz])
+    view = _View.from_parts(facs, sd, seg, lrow, rrow, ul)
+    sd._views[tuple((a.data_ptr(), tuple(a.shape)) for a in facs)] = view
+    return sd, view
 
 
 def _view_for(facs, sd: SparseDiagonal) -> _View:

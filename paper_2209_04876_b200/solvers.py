@@ -28,6 +28,7 @@ from . import _device as D
 from . import _lib
 from .errors import InvalidInputError, NumericalFailureError
 from .kron import (SparseDiagonal, _kron_apply_dev, _view_for, check_factors, kron_operator_shape,
+                   sketch_diag_and_view2,
                    kron_vec_square, sparse_diagonal_from_sketch)
 from .leverage import (JL_LOG_FACTOR, REGRESSION_SAMPLE_CONSTANT, LeverageScores, ProductSampler,
                        RowSketch, _inverse_small, _jl_scores_dev, _spectral_rows_dev,
@@ -664,7 +665,11 @@ def _fast_solve_pass(facs, b, config: RegressionConfig, caches, trace, use_chol:
         draws = sampler._sample_dev(s, state, inc)
         w = sampler._weights_dev(draws, s)
     _mark("draws+weights")
-    sdiag = sparse_diagonal_from_sketch(RowSketch(draws, w), rows)
+    fused_sv = sketch_diag_and_view2(facs, draws, w) if _USE_FUSED[0] else None
+    if fused_sv is not None:
+        sdiag, _ = fused_sv
+    else:
+        sdiag = sparse_diagonal_from_sketch(RowSketch(draws, w), rows)
     _mark("sparse diagonal")
     idx = sdiag.indices
     if isinstance(b, torch.Tensor) and b.is_cuda:
