@@ -200,11 +200,13 @@ typedef struct ks_sketch_view {
  * from the s draws idx (s x 2) and weights w builds the sparse diagonal (sd_idx, sd_val, sorted
  * and deduplicated exactly as ks_sketch_diag) and its grouped view in the same pass: rrow[t] = i1
  * of entry t, seg (u_left + 1 segment starts over the entries), lrow (u_left first-factor rows);
- * the grouped order is the sparse-diagonal order (perm = identity, v = sd_val).  counts (host,
- * 2) receives nnz and u_left.  Buffers hold s (seg: s + 1) entries.  Synchronises the stream. */
+ * the grouped order is the sparse-diagonal order (perm = identity, v = sd_val).  nnz and u_left
+ * go to counts (host, 2; the call then synchronises the stream) and/or counts_dev (device, 2;
+ * with counts NULL the call is asynchronous and graph-capturable).  Buffers hold s (seg: s + 1)
+ * entries. */
 int ks_sketch_diag_grouped2(const int64_t* idx, const int64_t* row_shape, const double* w, int64_t s,
                             int64_t* sd_idx, double* sd_val, int64_t* seg, int64_t* lrow, int64_t* rrow,
-                            int64_t* counts, void* stream);
+                            int64_t* counts, int64_t* counts_dev, void* stream);
 
 /* Build the grouped view of a sparse diagonal (sorted unique flat row indices sd_idx with values
  * sd_val, nnz entries) for the factor split left_pos | right_pos (kron.balanced_partition,

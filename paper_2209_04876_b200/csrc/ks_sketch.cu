@@ -430,10 +430,12 @@ extern "C" int ks_sketch_diag(int32_t nf, const int64_t* idx, const int64_t* row
 
 extern "C" int ks_sketch_diag_grouped2(const int64_t* idx, const int64_t* row_shape, const double* w, int64_t s,
                                        int64_t* sd_idx, double* sd_val, int64_t* seg, int64_t* lrow, int64_t* rrow,
-                                       int64_t* counts, void* stream) {
+                                       int64_t* counts, int64_t* counts_dev, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
+  KS_REQUIRE(counts || counts_dev, KS_EINVAL, "need a host or a device counts buffer");
   if (s <= 0) {
-    counts[0] = counts[1] = 0;
+    if (counts) counts[0] = counts[1] = 0;
+    if (counts_dev) KS_TRY_CUDA(cudaMemsetAsync(counts_dev, 0, 2 * sizeof(int64_t), st));
     return KS_OK;
   }
   Shape8 rs{};
@@ -447,8 +449,9 @@ extern "C" int ks_sketch_diag_grouped2(const int64_t* idx, const int64_t* row_sh
   ks::Scratch<int64_t> perm(s, st);
   ks::Scratch<int32_t> head(2 * s, st);
   ks::Scratch<int64_t> segid(2 * s, st);
-  ks::Scratch<int64_t> dcounts(2, st);
-  KS_REQUIRE(keys.p && perm.p && head.p && segid.p && dcounts.p, KS_ECUDA, "scratch allocation failed");
+  ks::Scratch<int64_t> dcounts_s(counts_dev ? 0 : 2, st);
+  int64_t* dcounts = counts_dev ? counts_dev : dcounts_s.p;
+  KS_REQUIRE(keys.p && perm.p && head.p && segid.p && dcounts, KS_ECUDA, "scratch allocation failed");
   int32_t* lhead = head.p + s;
   int64_t* lsegid = segid.p + s;
   ravel_kernel<<<ceil_div_u(s, 256), 256, 0, st>>>(idx, 2, rs, s, keys.p, perm.p);
@@ -462,10 +465,12 @@ extern "C" int ks_sketch_diag_grouped2(const int64_t* idx, const int64_t* row_sh
   rc = ks::scan_exclusive_i32(st, lhead, s, lsegid);
   if (rc) return rc;
   seg_sqrt_group2_kernel<<<ceil_div_u(s, 128), 128, 0, st>>>(keys.p, perm.p, head.p, segid.p, lhead, lsegid, s, n1, w,
-                                                             sd_idx, sd_val, seg, lrow, rrow, dcounts.p);
+                                                             sd_idx, sd_val, seg, lrow, rrow, dcounts);
   KS_CHECK_LAUNCH();
-  KS_TRY_CUDA(cudaMemcpyAsync(counts, dcounts.p, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  KS_TRY_CUDA(cudaStreamSynchronize(st));
+  if (counts) {
+    KS_TRY_CUDA(cudaMemcpyAsync(counts, dcounts, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    KS_TRY_CUDA(cudaStreamSynchronize(st));
+  }
   return KS_OK;
 }
 

@@ -303,30 +303,45 @@ class _View:
         return g.reshape(shape).permute(inv).reshape(-1).contiguous()
 
 
-def sketch_diag_and_view2(facs, sketch_indices: torch.Tensor, sketch_weights: torch.Tensor):
-    """Sparse diagonal of a two-factor row sketch together with its grouped view (one fused
-    device pass, one host round trip); None when the factors' balanced partition is not
-    (left {0}, right {1})."""
-    cols = [int(a.shape[1]) for a in facs]
-    part = balanced_partition(cols)
-    if len(facs) != 2 or part.left != (0,) or part.right != (1,):
-        return None
+def grouped2_eligible(facs) -> bool:
+    """Two factors whose balanced partition is (left {0}, right {1})."""
+    if len(facs) != 2:
+        return False
+    part = balanced_partition([int(a.shape[1]) for a in facs])
+    return part.left == (0,) and part.right == (1,)
+
+
+def sketch_diag_grouped2_launch(facs, sketch_indices: torch.Tensor, sketch_weights: torch.Tensor):
+    """Launch-only half of sketch_diag_and_view2 (graph-capturable): returns the device buffers
+    (sd_idx, sd_val, seg, lrow, rrow, counts_dev)."""
     rows = [int(a.shape[0]) for a in facs]
     s = int(sketch_indices.shape[0])
-    sd_idx = D.empty(max(s, 1), dtype=D.I64)
-    sd_val = D.empty(max(s, 1))
-    seg = D.empty(s + 1, dtype=D.I64)
-    lrow = D.empty(max(s, 1), dtype=D.I64)
-    rrow = D.empty(max(s, 1), dtype=D.I64)
-    counts = (ctypes.c_int64 * 2)()
+    bufs = (D.empty(max(s, 1), dtype=D.I64), D.empty(max(s, 1)), D.empty(s + 1, dtype=D.I64),
+            D.empty(max(s, 1), dtype=D.I64), D.empty(max(s, 1), dtype=D.I64), D.empty(2, dtype=D.I64))
+    sd_idx, sd_val, seg, lrow, rrow, cdev = bufs
     _lib.call("ks_sketch_diag_grouped2", D.p(sketch_indices.contiguous()), _lib.ptr_array(ctypes.c_int64, rows),
-              D.p(sketch_weights.contiguous()), s, D.p(sd_idx), D.p(sd_val), D.p(seg), D.p(lrow), D.p(rrow), counts,
-              D.stream())
-    nnz, ul = int(counts[0]), int(counts[1])
+              D.p(sketch_weights.contiguous()), s, D.p(sd_idx), D.p(sd_val), D.p(seg), D.p(lrow), D.p(rrow), None,
+              D.p(cdev), D.stream())
+    return bufs
+
+
+def sketch_diag_grouped2_finish(facs, bufs):
+    """Read (nnz, u_left) and wrap the buffers as a SparseDiagonal and its cached view."""
+    sd_idx, sd_val, seg, lrow, rrow, cdev = bufs
+    nnz, ul = (int(v) for v in cdev.cpu().tolist())
     sd = SparseDiagonal._trusted(sd_idx[:nnz], sd_val[:nnz])
     view = _View.from_parts(facs, sd, seg, lrow, rrow, ul)
     sd._views[tuple((a.data_ptr(), tuple(a.shape)) for a in facs)] = view
     return sd, view
+
+
+def sketch_diag_and_view2(facs, sketch_indices: torch.Tensor, sketch_weights: torch.Tensor):
+    """Sparse diagonal of a two-factor row sketch together with its grouped view (one fused
+    device pass, one host round trip); None when the factors' balanced partition is not
+    (left {0}, right {1})."""
+    if not grouped2_eligible(facs):
+        return None
+    return sketch_diag_grouped2_finish(facs, sketch_diag_grouped2_launch(facs, sketch_indices, sketch_weights))
 
 
 def _view_for(facs, sd: SparseDiagonal) -> _View:

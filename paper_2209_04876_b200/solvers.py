@@ -27,8 +27,8 @@ import torch
 from . import _device as D
 from . import _lib
 from .errors import InvalidInputError, NumericalFailureError
-from .kron import (SparseDiagonal, _kron_apply_dev, _view_for, check_factors, kron_operator_shape,
-                   sketch_diag_and_view2,
+from .kron import (SparseDiagonal, _kron_apply_dev, _view_for, check_factors, grouped2_eligible,
+                   kron_operator_shape, sketch_diag_grouped2_finish, sketch_diag_grouped2_launch,
                    kron_vec_square, sparse_diagonal_from_sketch)
 from .leverage import (JL_LOG_FACTOR, REGRESSION_SAMPLE_CONSTANT, LeverageScores, ProductSampler,
                        RowSketch, _inverse_small, _jl_scores_dev, _spectral_rows_dev,
@@ -530,7 +530,9 @@ def _jl_and_sampling(facs, tildes, gts, eps_jl: float, config: RegressionConfig,
     state, inc = pcg64_state(seeds[-1])
     draws = sampler._sample_dev(s, state, inc)
     w = sampler._weights_dev(draws, s)
-    return scores, afs, sampler, draws, w
+    # two factors: the sparse diagonal and its grouped view are built here too (launch-only)
+    g2 = sketch_diag_grouped2_launch(facs, draws, w) if _USE_FUSED[0] and grouped2_eligible(facs) else None
+    return scores, afs, sampler, draws, w, g2
 
 
 class _PrefixGraph:
@@ -655,19 +657,19 @@ def _fast_solve_pass(facs, b, config: RegressionConfig, caches, trace, use_chol:
         grams = _factor_grams_async(gts)
         run = lambda: _jl_and_sampling(facs, tildes, gts, eps_jl, config, use_chol, seeds, s)  # noqa: E731
         if key is None:
-            scores, afs, sampler, draws, w = run()
+            scores, afs, sampler, draws, w, g2 = run()
         else:
-            scores, afs, sampler, draws, w = _prefix_graph_run(key, entry, gts, run, deferred)
+            scores, afs, sampler, draws, w, g2 = _prefix_graph_run(key, entry, gts, run, deferred)
         _mark("jl scores+sampling")
     if caches is not None:
         sampler = ProductSampler([LeverageScores(sc, 0.0, af) for sc, af in zip(scores, afs)])
         state, inc = pcg64_state(seeds[-1])
         draws = sampler._sample_dev(s, state, inc)
         w = sampler._weights_dev(draws, s)
+        g2 = sketch_diag_grouped2_launch(facs, draws, w) if _USE_FUSED[0] and grouped2_eligible(facs) else None
     _mark("draws+weights")
-    fused_sv = sketch_diag_and_view2(facs, draws, w) if _USE_FUSED[0] else None
-    if fused_sv is not None:
-        sdiag, _ = fused_sv
+    if g2 is not None:
+        sdiag, _ = sketch_diag_grouped2_finish(facs, g2)
     else:
         sdiag = sparse_diagonal_from_sketch(RowSketch(draws, w), rows)
     _mark("sparse diagonal")

@@ -167,18 +167,25 @@ if "--host" in sys.argv:
     st.sort_stats("tottime").print_stats(45)
 
 if "--phases" in sys.argv:
+    import collections
     from paper_2209_04876_b200 import solvers as S
-    for rep_i in range(3):
+    gpu_t, host_t, walls2 = collections.defaultdict(list), collections.defaultdict(list), []
+    order = []
+    for rep_i in range(8):
         S._PHASES = []
         torch.cuda.synchronize()
-        t_host0 = __import__("time").perf_counter()
         rep = K.fast_kronecker_regression(facs, b, cfg)
         torch.cuda.synchronize()
         ph, S._PHASES = S._PHASES, None
-        ms = torch.cuda.memory_stats()
-        print(f"solve {rep_i}: wall {rep.wall_time * 1e6:.0f} us  segments {ms['segment.all.allocated']} "
-              f"cudaMalloc retries {ms['num_alloc_retries']}")
+        walls2.append(rep.wall_time * 1e6)
         prev = ph[0]
         for name, th, ev in ph[1:]:
-            print(f"  {name:18s} gpu {prev[2].elapsed_time(ev) * 1e3:8.1f} us   host-issue {1e6 * (th - prev[1]):8.1f} us")
+            if name not in order:
+                order.append(name)
+            gpu_t[name].append(prev[2].elapsed_time(ev) * 1e3)
+            host_t[name].append(1e6 * (th - prev[1]))
             prev = (name, th, ev)
+    print(f"phases over 8 solves: wall median {statistics.median(walls2):.0f} us min {min(walls2):.0f} us")
+    for name in order:
+        print(f"  {name:20s} gpu median {statistics.median(gpu_t[name]):8.1f} us   host-issue median "
+              f"{statistics.median(host_t[name]):8.1f} us")
