@@ -147,6 +147,12 @@ int ks_jl_scores(const double* A, int64_t n, int32_t d, const double* Q, int32_t
 int ks_jl_projection(const double* G, int32_t d, const double* GA, int32_t r, double scale,
                      double* Q, int32_t* info, void* stream);
 
+/* The two halves of ks_jl_projection, so the factorization (which needs only the Gram) can run
+ * while GA is still being drawn: ks_jl_cholesky factors G into the workspace Lws
+ * (d (d + 1) + d doubles; info as above), ks_jl_solve forms Q from Lws and GA. */
+int ks_jl_cholesky(const double* G, int32_t d, double* Lws, int32_t* info, void* stream);
+int ks_jl_solve(const double* Lws, int32_t d, const double* GA, int32_t r, double scale, double* Q, void* stream);
+
 /* exact statistical leverage scores: scores[i] = sum_k U[i,k]^2 * wts[k] (leverage.py:51-64) */
 int ks_row_weighted_sumsq(const double* U, int64_t n, int32_t d, const double* wts,
                           double* scores, void* stream);

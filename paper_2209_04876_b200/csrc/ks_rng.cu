@@ -248,6 +248,67 @@ __global__ void __launch_bounds__(ZT) zig_compose_kernel(const uint8_t* __restri
   sexit[sidx * ZK + o] = (uint8_t)e;
   scnt[sidx * ZK + o] = k;
 }
+// Small-count variant (nsuper <= ZS2_MAX): the maps are staged in shared memory; the 32 lanes of
+// warp 0 compose contiguous blocks of super-chunks for all ZK entry offsets, lane 0 walks the 32
+// block maps from entry offset 0, and every lane then walks its block from its entry.  Only the
+// one path that matters is followed, instead of composing every map pair.
+constexpr int ZS2_MAX = 2048;
+constexpr int ZS2_T = 256;
+__global__ void __launch_bounds__(ZS2_T) zig_scan_small_kernel(const uint8_t* __restrict__ sexit,
+                                                              const int32_t* __restrict__ scnt, int64_t nsuper,
+                                                              uint8_t* __restrict__ sentry,
+                                                              int64_t* __restrict__ sbase,
+                                                              int64_t* __restrict__ total) {
+  extern __shared__ __align__(16) unsigned char zs2[];
+  int32_t* cn = reinterpret_cast<int32_t*>(zs2);                   // nsuper * ZK
+  uint8_t* ex = zs2 + (size_t)ZS2_MAX * ZK * sizeof(int32_t);       // nsuper * ZK
+  __shared__ int bexit[32][ZK];
+  __shared__ int64_t bcnt[32][ZK];
+  __shared__ int bentry[32];
+  __shared__ int64_t bbase[32];
+  const int nz = (int)nsuper * ZK;
+  for (int i = threadIdx.x; i < nz; i += ZS2_T) ks_cp_async4(&cn[i], scnt + i);
+  for (int i = threadIdx.x; i < nz / 4; i += ZS2_T) ks_cp_async4(&ex[4 * i], sexit + 4 * i);
+  ks_cp_async_wait_all();
+  __syncthreads();
+  if (threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
+  const int per = ((int)nsuper + 31) / 32;
+  const int c0 = min((int)nsuper, lane * per), c1 = min((int)nsuper, c0 + per);
+#pragma unroll
+  for (int o = 0; o < ZK; o++) {
+    int e = o;
+    int64_t k = 0;
+    for (int c = c0; c < c1; c++) {
+      k += cn[c * ZK + e];
+      e = ex[c * ZK + e];
+    }
+    bexit[lane][o] = e;
+    bcnt[lane][o] = k;
+  }
+  __syncwarp();
+  if (lane == 0) {
+    int e = 0;
+    int64_t k = 0;
+    for (int l = 0; l < 32; l++) {
+      bentry[l] = e;
+      bbase[l] = k;
+      k += bcnt[l][e];
+      e = bexit[l][e];
+    }
+    *total = k;
+  }
+  __syncwarp();
+  int e = bentry[lane];
+  int64_t k = bbase[lane];
+  for (int c = c0; c < c1; c++) {
+    sentry[c] = (uint8_t)e;
+    sbase[c] = k;
+    k += cn[c * ZK + e];
+    e = ex[c * ZK + e];
+  }
+}
+
 // One block: exclusive prefix of the super-chunk maps applied to entry offset 0
 // (sequential per thread over a contiguous range, Hillis-Steele across threads).
 constexpr int ZSCAN_T = 512;
@@ -447,10 +508,17 @@ extern "C" int ks_pcg64_standard_normal(uint64_t sh, uint64_t sl, uint64_t ih, u
     zig_compose_kernel<<<ceil_div_u(nsuper, ZT / ZK), ZT, 0, st>>>(exit_off.p, cnt.p, nchunks, nsuper,
                                                                    sexit.p, scnt.p);
     KS_CHECK_LAUNCH();
-    const size_t scan_smem = (size_t)2 * ZSCAN_T * ZK * (1 + sizeof(int64_t));
-    KS_TRY_CUDA(cudaFuncSetAttribute(zig_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)scan_smem));
-    zig_scan_kernel<<<1, ZSCAN_T, scan_smem, st>>>(sexit.p, scnt.p, nsuper, sentry.p, sbase.p, tail.p);
+    if (nsuper <= ZS2_MAX) {
+      const size_t smem2 = (size_t)ZS2_MAX * ZK * (sizeof(int32_t) + 1);
+      KS_TRY_CUDA(cudaFuncSetAttribute(zig_scan_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem2));
+      zig_scan_small_kernel<<<1, ZS2_T, smem2, st>>>(sexit.p, scnt.p, nsuper, sentry.p, sbase.p, tail.p);
+    } else {
+      const size_t scan_smem = (size_t)2 * ZSCAN_T * ZK * (1 + sizeof(int64_t));
+      KS_TRY_CUDA(cudaFuncSetAttribute(zig_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)scan_smem));
+      zig_scan_kernel<<<1, ZSCAN_T, scan_smem, st>>>(sexit.p, scnt.p, nsuper, sentry.p, sbase.p, tail.p);
+    }
     KS_CHECK_LAUNCH();
     zig_emit_kernel<<<nblk, ZT, 0, st>>>(cons.p, val.p, M, nchunks, exit_off.p, cnt.p, sentry.p, sbase.p, n,
                                          divisor, out + done, tail.p + 1, tail.p, err);

@@ -153,9 +153,12 @@ __device__ __forceinline__ unsigned long long jlp_now() {
 #define JLP_STAMP(k) \
   if (blockIdx.x == 0 && threadIdx.x == 0) g_jlp_ts[k] = jlp_now();
 
+// mode 0: factor + solve; 1: factor only (L and 1/diag(L) to Lg, d*(d+1) + d doubles); 2: solve
+// only with the factor from Lg (lets the factorization run before GA is ready).
 __global__ void __launch_bounds__(512) jl_projection_kernel(const double* __restrict__ G, int d,
                                                             const double* __restrict__ GA, int r, double scale,
-                                                            double* __restrict__ Q, int32_t* __restrict__ info) {
+                                                            double* __restrict__ Q, int32_t* __restrict__ info,
+                                                            double* __restrict__ Lg, int mode) {
   extern __shared__ double sm[];
   const int ld = d + 1;
   double* L = sm;                   // d x ld (lower triangle used)
@@ -164,16 +167,26 @@ __global__ void __launch_bounds__(512) jl_projection_kernel(const double* __rest
   __shared__ double s_rdiag[64];
   JLP_STAMP(0)
   const int tid = threadIdx.x, nt = blockDim.x, tx = tid & 31, ty = tid >> 5, nty = nt >> 5;
-  for (int e = tid; e < d * d; e += nt) ks_cp_async8(&L[(e / d) * ld + (e % d)], G + e);
-  for (int e = tid; e < d * r; e += nt) {
-    const int k = e / r, c = e - k * r;
-    ks_cp_async8(&Y[e], GA + (size_t)c * d + k);
+  if (mode != 2) {
+    for (int e = tid; e < d * d; e += nt) ks_cp_async8(&L[(e / d) * ld + (e % d)], G + e);
+  } else {
+    for (int e = tid; e < d * ld; e += nt) ks_cp_async8(&L[e], Lg + e);
+    if (d <= 64)
+      for (int e = tid; e < d; e += nt) ks_cp_async8(&s_rdiag[e], Lg + (size_t)d * ld + e);
+  }
+  if (mode != 1) {
+    for (int e = tid; e < d * r; e += nt) {
+      const int k = e / r, c = e - k * r;
+      ks_cp_async8(&Y[e], GA + (size_t)c * d + k);
+    }
   }
   if (tid == 0) s_bad = 0;
   ks_cp_async_wait_all();
   __syncthreads();
   JLP_STAMP(1)
-  if (d <= 64 && nt == 512) {
+  if (mode == 2) {
+    // factor already in shared memory
+  } else if (d <= 64 && nt == 512) {
     // Register-resident right-looking LDL^T, one barrier per column: thread t owns column
     // j = t % 64, rows i = t / 64 + 8m (m < 8).  At step k the owners of column k publish it
     // (and the pivot owner 1 / d_k) in a double-buffered shared column; everyone then applies
@@ -253,6 +266,15 @@ __global__ void __launch_bounds__(512) jl_projection_kernel(const double* __rest
       __syncthreads();
     }
   }
+  if (mode == 1) {
+    if (d > 64 || nt != 512)
+      for (int k = tid; k < d && k < 64; k += nt) s_rdiag[k] = 1.0 / L[k * ld + k];
+    __syncthreads();
+    for (int e = tid; e < d * ld; e += nt) Lg[e] = L[e];
+    for (int e = tid; e < d && e < 64; e += nt) Lg[(size_t)d * ld + e] = s_rdiag[e];
+    if (tid == 0 && blockIdx.x == 0) info[0] = s_bad;
+    return;
+  }
   // L Z = Y, then L^T X = Z.  Right-hand-side columns are independent: for d <= 64 a warp solves
   // JP_CPW columns at once with the column in registers (lane l owns rows l and l + 32); the
   // per-element operation order is the textbook one (divide by the pivot, then fma updates).
@@ -317,7 +339,7 @@ __global__ void __launch_bounds__(512) jl_projection_kernel(const double* __rest
       Q[e] = scale * Y[k * r + c];
     }
   }
-  if (tid == 0 && blockIdx.x == 0) info[0] = s_bad;
+  if (tid == 0 && blockIdx.x == 0 && mode == 0) info[0] = s_bad;
   JLP_STAMP(3)
 }
 
@@ -332,9 +354,30 @@ extern "C" int ks_jl_projection(const double* G, int32_t d, const double* GA, in
                                 int32_t* info, void* stream) {
   const size_t smem = sizeof(double) * ((size_t)d * (d + 1) + (size_t)d * r);
   KS_REQUIRE(d >= 1 && r >= 1 && smem <= 220 * 1024, KS_ESIZE, "jl_projection: d=%d r=%d too large", d, r);
-  KS_TRY_CUDA(cudaFuncSetAttribute(jl_projection_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  KS_TRY_CUDA(cudaFuncSetAttribute(jl_projection_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
   const unsigned grid = d <= 64 ? ceil_div_u(r, JP_COLS) : 1;
-  jl_projection_kernel<<<grid, 512, smem, (cudaStream_t)stream>>>(G, d, GA, r, scale, Q, info);
+  jl_projection_kernel<<<grid, 512, smem, (cudaStream_t)stream>>>(G, d, GA, r, scale, Q, info, nullptr, 0);
+  KS_CHECK_LAUNCH();
+  return KS_OK;
+}
+
+extern "C" int ks_jl_cholesky(const double* G, int32_t d, double* Lws, int32_t* info, void* stream) {
+  const size_t smem = sizeof(double) * ((size_t)d * (d + 1));
+  KS_REQUIRE(d >= 1 && smem <= 220 * 1024, KS_ESIZE, "jl_cholesky: d=%d too large", d);
+  KS_TRY_CUDA(cudaFuncSetAttribute(jl_projection_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+  jl_projection_kernel<<<1, 512, smem, (cudaStream_t)stream>>>(G, d, nullptr, 0, 1.0, nullptr, info, Lws, 1);
+  KS_CHECK_LAUNCH();
+  return KS_OK;
+}
+
+extern "C" int ks_jl_solve(const double* Lws, int32_t d, const double* GA, int32_t r, double scale, double* Q,
+                           void* stream) {
+  const size_t smem = sizeof(double) * ((size_t)d * (d + 1) + (size_t)d * r);
+  KS_REQUIRE(d >= 1 && r >= 1 && smem <= 220 * 1024, KS_ESIZE, "jl_solve: d=%d r=%d too large", d, r);
+  KS_TRY_CUDA(cudaFuncSetAttribute(jl_projection_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+  const unsigned grid = d <= 64 ? ceil_div_u(r, JP_COLS) : 1;
+  jl_projection_kernel<<<grid, 512, smem, (cudaStream_t)stream>>>(nullptr, d, GA, r, scale, Q, nullptr, (double*)Lws,
+                                                                   2);
   KS_CHECK_LAUNCH();
   return KS_OK;
 }

@@ -422,16 +422,33 @@ def _chol_status(v):
         raise _CholeskyFailed()
 
 
+def _jl_factor(gram: torch.Tensor) -> torch.Tensor:
+    """Device factorisation of a JL Gram (first half of ks_jl_projection) into a workspace."""
+    from .leverage import check_later
+    d = int(gram.shape[0])
+    ws = D.empty(d * (d + 1) + d)
+    info = torch.zeros(1, dtype=torch.int32, device=gram.device)
+    _lib.call("ks_jl_cholesky", D.p(gram), d, D.p(ws), D.p(info), D.stream())
+    check_later(info, _chol_status)
+    return ws
+
+
 def _jl_scores_chol(a: torch.Tensor, a_tilde: torch.Tensor, gram: torch.Tensor, eps: float, seed,
-                    log_factor: float, use_chol: bool = True) -> torch.Tensor:
+                    log_factor: float, use_chol: bool = True, factor: torch.Tensor | None = None,
+                    factor_stream=None) -> torch.Tensor:
     """JL scores with (1+eps/4) (G a_tilde) gram^-1 from a device Cholesky solve (leverage.py:114-129).
     The positive-definiteness flag is checked with the solve's other deferred flags; on failure
-    the solve is repeated with ``use_chol=False`` (LU inverse, as the reference's np.linalg.inv)."""
+    the solve is repeated with ``use_chol=False`` (LU inverse, as the reference's np.linalg.inv).
+    ``factor``: a workspace from _jl_factor (made on ``factor_stream``)."""
     from .leverage import _jl_ga, _jl_scores_from_q, check_later
     d = int(a.shape[1])
     ga, r = _jl_ga(a, a_tilde, seed, log_factor)
     q = D.empty(r, d)
-    if use_chol:
+    if use_chol and factor is not None:
+        if factor_stream is not None:
+            torch.cuda.current_stream().wait_stream(factor_stream)
+        _lib.call("ks_jl_solve", D.p(factor), d, D.p(ga), r, 1.0 + eps / 4.0, D.p(q), D.stream())
+    elif use_chol:
         info = torch.zeros(1, dtype=torch.int32, device=a.device)
         _lib.call("ks_jl_projection", D.p(gram), d, D.p(ga), r, 1.0 + eps / 4.0, D.p(q), D.p(info), D.stream())
         check_later(info, _chol_status)
@@ -512,20 +529,33 @@ def _jl_and_sampling(facs, tildes, gts, eps_jl: float, config: RegressionConfig,
     scores, afs = [], []
     main = torch.cuda.current_stream()
     capturing = torch.cuda.is_current_stream_capturing()
-    # the per-factor JL estimates are independent: factor n > 0 runs on its own stream (all
-    # streams fork here, before any factor's work is enqueued)
-    for n in range(1, len(facs)):
+    # the per-factor JL estimates are independent: factor n > 0 runs on its own stream, and every
+    # Gram factorisation (needs only the Gram) runs on its own stream while the Gaussian sketch is
+    # drawn (all streams fork here, before any work is enqueued)
+    nf = len(facs)
+    chol_st = [_side_stream(16 + n) for n in range(nf)] if use_chol else []
+    for n in range(1, nf):
         _side_stream(n).wait_stream(main)
+    for cs in chol_st:
+        cs.wait_stream(main)
+    factors = []
+    for n in range(nf):
+        if use_chol:
+            with torch.cuda.stream(chol_st[n]):
+                factors.append(_jl_factor(gts[n]))
     for n, a in enumerate(facs):
         st = main if n == 0 else _side_stream(n)
         with torch.cuda.stream(st):
             scores.append(_jl_scores_chol(a, tildes[n], gts[n], eps_jl, seeds[2 * n + 1], config.jl_log_factor,
-                                          use_chol))
+                                          use_chol, factors[n] if use_chol else None,
+                                          chol_st[n] if use_chol else None))
         afs.append(1.0 + eps_jl / 2.0)
-    for n in range(1, len(facs)):
+    for n in range(1, nf):
         main.wait_stream(_side_stream(n))
         if not capturing:
             scores[n].record_stream(main)
+    for cs in chol_st:
+        main.wait_stream(cs)
     sampler = ProductSampler([LeverageScores(sc, 0.0, af) for sc, af in zip(scores, afs)])
     state, inc = pcg64_state(seeds[-1])
     draws = sampler._sample_dev(s, state, inc)
