@@ -187,7 +187,10 @@ def run_ours(args):
         # loss pass that follows is excluded, as in solvers.py:404-462)
         times.append(ph[names.index("t0")][2].elapsed_time(ph[names.index("solve_end")][2]) / 1e3)
         full_times.append(e0.elapsed_time(e1) / 1e3)
-        if "richardson" in names:
+        if S._LAST_LOOP_EVENTS[0] is not None:  # whole-solve graph: events captured around the loop
+            l0, l1 = S._LAST_LOOP_EVENTS[0]
+            rich_live.append(l0.elapsed_time(l1) * 1e3)
+        elif "richardson" in names:
             i = names.index("richardson")
             rich_live.append(ph[i - 1][2].elapsed_time(ph[i][2]) * 1e3)
     barrier()

@@ -189,6 +189,11 @@ int ks_sketch_diag(int32_t nf, const int64_t* idx, const int64_t* row_shape, con
 /* Gather b_at[t] = b[idx[t]] (solvers.py:451). */
 int ks_gather(const double* b, const int64_t* idx, int64_t n, double* out, void* stream);
 
+/* out[t] = b[idx[t]] for t < *count_dev (device count, cap = buffer capacity); b may be device
+ * memory or page-locked host memory (mapped: only the gathered entries cross PCIe). */
+int ks_gather_count(const double* b, const int64_t* idx, const int64_t* count_dev, int64_t cap, double* out,
+                    void* stream);
+
 /* ---------------------------------------------------------------- sketched operator & solver */
 
 /* Grouped view of a sparse diagonal for the two-group scheme of kron.py:258-354.
@@ -260,6 +265,16 @@ int ks_richardson_fused(const ks_sketch_view* sk, const int64_t* perm, const dou
                         const double* wL, const double* VR, const double* wR, const double* dinv, double lam,
                         double damping, int32_t max_iters, double residual_tol, double* x, double* hist,
                         double* rhs_out, int32_t* iters, int32_t* hist_len, void* stream);
+
+/* Asynchronous ks_richardson_fused for CUDA-graph capture: sk->nnz / sk->u_left are capacities,
+ * the real counts are read on the device from counts_dev ([nnz, u_left], as written by
+ * ks_sketch_diag_grouped2), and the loop state [status (1 converged, 2 diverged), iterations,
+ * history length] is written to state_dev (device, 3 int32).  No host synchronisation. */
+int ks_richardson_fused_async(const ks_sketch_view* sk, const int64_t* counts_dev, const int64_t* perm,
+                              const double* b_at, const double* VL, const double* wL, const double* VR,
+                              const double* wR, const double* dinv, double lam, double damping, int32_t max_iters,
+                              double residual_tol, double* x, double* hist, double* rhs_out, int32_t* state_dev,
+                              void* stream);
 
 /* Profiling aid: per-CTA %globaltimer stamps (ns) of iteration 5 of the last persistent
  * Richardson run, 9 per CTA (phase boundaries and grid-barrier exits). */

@@ -434,6 +434,21 @@ extern "C" int ks_check_finite_nonzero(const double* a, int64_t n, int32_t* flag
   return KS_OK;
 }
 
+__global__ void gather_count_kernel(const double* __restrict__ b, const int64_t* __restrict__ idx,
+                                    const int64_t* __restrict__ count, int64_t cap, double* __restrict__ out) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= cap || t >= *count) return;
+  out[t] = b[idx[t]];
+}
+
+extern "C" int ks_gather_count(const double* b, const int64_t* idx, const int64_t* count_dev, int64_t cap,
+                               double* out, void* stream) {
+  if (cap <= 0) return KS_OK;
+  gather_count_kernel<<<ceil_div_u(cap, 256), 256, 0, (cudaStream_t)stream>>>(b, idx, count_dev, cap, out);
+  KS_CHECK_LAUNCH();
+  return KS_OK;
+}
+
 extern "C" int ks_gather(const double* b, const int64_t* idx, int64_t n, double* out,
                          void* stream) {
   if (n <= 0) return KS_OK;

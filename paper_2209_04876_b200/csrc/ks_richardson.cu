@@ -22,7 +22,8 @@ bool persistent_supported(int dL, int dR);
 int richardson_persistent(cudaStream_t st, const ks_sketch_view* sk, const double* VL, const double* VR,
                           const double* dinv, const double* wL, const double* wR, double* rhs, bool rhs_in_kernel,
                           const double* b_at, const int64_t* perm, double lam, double damping, int max_iters,
-                          double residual_tol, double* x, double* hist, int* iters, int* hist_len, int* status);
+                          double residual_tol, double* x, double* hist, int* iters, int* hist_len, int* status,
+                          const int64_t* counts_dev, int* state_dev);
 }
 
 namespace {
@@ -205,7 +206,7 @@ extern "C" int ks_richardson_sketched(const ks_sketch_view* sk, const double* VL
     int it = 0, hl = 0;
     int rc = ks::richardson_persistent(st, sk, VL, VR, dinv, nullptr, nullptr, const_cast<double*>(rhs), false,
                                        nullptr, nullptr, lam, damping, max_iters, residual_tol, x, hist, &it, &hl,
-                                       &status);
+                                       &status, nullptr, nullptr);
     if (rc) return rc;
     *iters = it;
     *hist_len = hl;
@@ -267,7 +268,7 @@ extern "C" int ks_richardson_fused(const ks_sketch_view* sk, const int64_t* perm
   KS_REQUIRE(dinv || (wL && wR), KS_EINVAL, "need dinv or both eigenvalue vectors");
   int status = 0, it = 0, hl = 0;
   int rc = ks::richardson_persistent(st, sk, VL, VR, dinv, wL, wR, rhs_out, true, b_at, perm, lam, damping,
-                                     max_iters, residual_tol, x, hist, &it, &hl, &status);
+                                     max_iters, residual_tol, x, hist, &it, &hl, &status, nullptr, nullptr);
   if (rc) return rc;
   *iters = it;
   *hist_len = hl;
@@ -276,4 +277,24 @@ extern "C" int ks_richardson_fused(const ks_sketch_view* sk, const int64_t* perm
     return KS_EDIVERGED;
   }
   return KS_OK;
+}
+
+// Asynchronous fused form for CUDA-graph capture: the view's nnz / u_left are capacities and the
+// real counts are read on the device from counts_dev ([nnz, u_left]); the loop state
+// [status (1 converged, 2 diverged), iterations, history length] goes to state_dev.  No host
+// synchronisation.
+extern "C" int ks_richardson_fused_async(const ks_sketch_view* sk, const int64_t* counts_dev, const int64_t* perm,
+                                         const double* b_at, const double* VL, const double* wL, const double* VR,
+                                         const double* wR, const double* dinv, double lam, double damping,
+                                         int32_t max_iters, double residual_tol, double* x, double* hist,
+                                         double* rhs_out, int32_t* state_dev, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const int dL = sk->dL, dR = sk->dR;
+  KS_REQUIRE(sk->nnz > 0 && ks::persistent_supported(dL, dR) && max_iters <= 1024, KS_ESIZE,
+             "fused Richardson needs dL, dR in {16, 32, 64}, nnz > 0 and <= 1024 iterations");
+  KS_REQUIRE(dinv || (wL && wR), KS_EINVAL, "need dinv or both eigenvalue vectors");
+  KS_REQUIRE(counts_dev && state_dev, KS_EINVAL, "need device counts and a device state buffer");
+  int status = 0, it = 0, hl = 0;
+  return ks::richardson_persistent(st, sk, VL, VR, dinv, wL, wR, rhs_out, true, b_at, perm, lam, damping, max_iters,
+                                   residual_tol, x, hist, &it, &hl, &status, counts_dev, state_dev);
 }

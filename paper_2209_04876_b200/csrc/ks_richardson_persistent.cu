@@ -565,10 +565,11 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
 // dst row i = src row rows[i] (d entries) + padding; pad slot 0 carries extra[i] if given, pad
 // slot 1 carries extra[i] * b[perm[i]] if b is given (v_t b_t of the right-hand side).
 __global__ void pack_rows_kernel(const double* __restrict__ src, int64_t ld, const int64_t* __restrict__ rows,
-                                 int64_t n, int d, int dp, const double* __restrict__ extra,
-                                 const double* __restrict__ b, const int64_t* __restrict__ perm,
-                                 double* __restrict__ dst) {
+                                 int64_t n_host, const int64_t* __restrict__ n_dev, int d, int dp,
+                                 const double* __restrict__ extra, const double* __restrict__ b,
+                                 const int64_t* __restrict__ perm, double* __restrict__ dst) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n = n_dev ? *n_dev : n_host;
   if (e >= n * dp) return;
   const int64_t i = e / dp;
   const int c = (int)(e - i * dp);
@@ -619,13 +620,15 @@ __device__ __forceinline__ int64_t plan_piece(const int64_t* __restrict__ seg, i
   return wchunk + (ch.t_e - ch.t_b) * wsamp + longest * wlong;
 }
 
-__global__ void __launch_bounds__(PLAN_T) plan_kernel(const int64_t* __restrict__ seg, int64_t ul, int G,
+__global__ void __launch_bounds__(PLAN_T) plan_kernel(const int64_t* __restrict__ seg, int64_t ul_host,
+                                                      const int64_t* __restrict__ ul_dev, int G,
                                                       int64_t wchunk, int64_t wsamp, int64_t wlong,
                                                       Chunk* __restrict__ chunks, int64_t* __restrict__ cprefix,
                                                       int64_t* __restrict__ range, int64_t* __restrict__ nchunks) {
   __shared__ int64_t wsum_p[32], wsum_c[32];
   __shared__ int64_t carry_p, carry_c;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int64_t ul = ul_dev ? *ul_dev : ul_host;
   const int64_t ngroups = (ul + CH_ROWS - 1) / CH_ROWS;
   if (tid == 0) carry_p = carry_c = 0;
   __syncthreads();
@@ -729,7 +732,10 @@ bool persistent_supported(int dL, int dR) {
 int richardson_persistent(cudaStream_t st, const ks_sketch_view* sk, const double* VL, const double* VR,
                           const double* dinv, const double* wL, const double* wR, double* rhs, bool rhs_in_kernel,
                           const double* b_at, const int64_t* perm, double lam, double damping, int max_iters,
-                          double residual_tol, double* x, double* hist, int* iters, int* hist_len, int* status) {
+                          double residual_tol, double* x, double* hist, int* iters, int* hist_len, int* status,
+                          const int64_t* counts_dev, int* state_dev) {
+  // counts_dev ([nnz, u_left] on the device): sk->nnz / sk->u_left are capacities and nothing
+  // here reads the counts on the host; state_dev: the loop state stays on the device (no sync)
   const int dL = sk->dL, dR = sk->dR;
   KS_REQUIRE(max_iters <= 1024, KS_ESIZE, "persistent loop keeps <= 1024 history entries");
   const int dLp = dL + PAD, dRp = dR + PAD;
@@ -741,22 +747,25 @@ int richardson_persistent(cudaStream_t st, const ks_sketch_view* sk, const doubl
   Scratch<double> VRt((int64_t)dR * dR, st);
   Scratch<Chunk> dch(cap, st);
   Scratch<int64_t> cpre(cap, st), drange(grid + 2, st);
-  Scratch<int> state(4, st);
+  Scratch<int> state_s(state_dev ? 0 : 4, st);
+  int* statep = state_dev ? state_dev : state_s.p;
   KS_REQUIRE(Lpack.p && Rpack.p && part.p && R.p && T.p && stepb.p && rowsq.p && VRt.p && dch.p && drange.p &&
-                 cpre.p && state.p,
+                 cpre.p && statep,
              KS_ECUDA, "scratch allocation failed");
   // estimated chunk cost (SM cycles): the Y and G DMMA tiles are fixed per chunk (the FP64 tensor
   // pipe issues one m16n8k4 per ~8 cycles per SM), the sample phase follows the chunk's longest
   // row (~120 cycles per sample pair-step), plus shared-memory traffic per sample
   const int64_t dmma = (int64_t)(CH_ROWS / 16) * (dR / 8) * (dL / 4) + (int64_t)(dL / 16) * (dR / 8) * (CH_ROWS / 4);
-  plan_kernel<<<1, PLAN_T, 0, st>>>(sk->seg, ul, grid, 8 * dmma + 600, (int64_t)dR / 4, 120, dch.p,
+  plan_kernel<<<1, PLAN_T, 0, st>>>(sk->seg, ul, counts_dev ? counts_dev + 1 : nullptr, grid, 8 * dmma + 600,
+                                     (int64_t)dR / 4, 120, dch.p,
                                      cpre.p, drange.p, drange.p + grid + 1);
   KS_CHECK_LAUNCH();
-  pack_rows_kernel<<<ceil_div_u(ul * dLp, 256), 256, 0, st>>>(sk->Lmat, sk->ldl, sk->lrow, ul, dL, dLp, nullptr,
-                                                               nullptr, nullptr, Lpack.p);
+  pack_rows_kernel<<<ceil_div_u(ul * dLp, 256), 256, 0, st>>>(sk->Lmat, sk->ldl, sk->lrow, ul,
+                                                               counts_dev ? counts_dev + 1 : nullptr, dL, dLp,
+                                                               nullptr, nullptr, nullptr, Lpack.p);
   KS_CHECK_LAUNCH();
-  pack_rows_kernel<<<ceil_div_u(nnz * dRp, 256), 256, 0, st>>>(sk->Rmat, sk->ldr, sk->rrow, nnz, dR, dRp, sk->v,
-                                                                rhs_in_kernel ? b_at : nullptr, perm, Rpack.p);
+  pack_rows_kernel<<<ceil_div_u(nnz * dRp, 256), 256, 0, st>>>(sk->Rmat, sk->ldr, sk->rrow, nnz, counts_dev, dR, dRp,
+                                                                sk->v, rhs_in_kernel ? b_at : nullptr, perm, Rpack.p);
   KS_CHECK_LAUNCH();
   transpose_sq_kernel2<<<ceil_div_u((int64_t)dR * dR, 256), 256, 0, st>>>(VR, dR, VRt.p);
   KS_CHECK_LAUNCH();
@@ -766,7 +775,7 @@ int richardson_persistent(cudaStream_t st, const ks_sketch_view* sk, const doubl
   a.rhs_in_kernel = rhs_in_kernel ? 1 : 0;
   a.lam = lam; a.damping = damping; a.residual_tol = residual_tol; a.max_iters = max_iters;
   a.part = part.p; a.R = R.p; a.T = T.p; a.step = stepb.p; a.rowsq = rowsq.p; a.x_out = x; a.hist = hist;
-  a.state = state.p;
+  a.state = statep;
   int rc;
   if (dL == 16 && dR == 16) rc = launch<16, 16>(st, a, grid);
   else if (dL == 16 && dR == 32) rc = launch<16, 32>(st, a, grid);
@@ -779,8 +788,9 @@ int richardson_persistent(cudaStream_t st, const ks_sketch_view* sk, const doubl
   else if (dL == 64 && dR == 64) rc = launch<64, 64>(st, a, grid);
   else rc = KS_EINVAL;
   if (rc) return rc;
+  if (state_dev) return KS_OK;
   int hs[4] = {0, 0, 0, 0};
-  KS_TRY_CUDA(cudaMemcpyAsync(hs, state.p, 3 * sizeof(int), cudaMemcpyDeviceToHost, st));
+  KS_TRY_CUDA(cudaMemcpyAsync(hs, statep, 3 * sizeof(int), cudaMemcpyDeviceToHost, st));
   KS_TRY_CUDA(cudaStreamSynchronize(st));
   *status = hs[0];
   *iters = hs[1];

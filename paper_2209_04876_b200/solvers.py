@@ -396,8 +396,9 @@ def _factor_grams_async(gts: list[torch.Tensor]):
                 vv, ww, gs = _factor_gram_dev(g)
                 outs.append((vv, ww))
             keep = []
-    for g in gts:
-        g.record_stream(side)
+    if not torch.cuda.is_current_stream_capturing():
+        for g in gts:
+            g.record_stream(side)
     ev = torch.cuda.Event()
     ev.record(side)
     return (outs, ev, keep)
@@ -408,8 +409,9 @@ def _join_grams(handle):
         return handle
     outs, ev, keep = handle
     torch.cuda.current_stream().wait_event(ev)
-    for t in keep:
-        t.record_stream(torch.cuda.current_stream())
+    if not torch.cuda.is_current_stream_capturing():
+        for t in keep:
+            t.record_stream(torch.cuda.current_stream())
     return outs
 
 
@@ -478,9 +480,154 @@ class FastSolveTrace:
                              a_tilde_rows=[])
 
 
+# ---------------------------------------------------------------------------------------------
+# Whole-solve CUDA graph (two factors, single-factor groups, device or page-locked b): Grams,
+# eigensolves (side stream), JL estimates, sampler, draws, sparse diagonal + view, the b gather
+# and the fused right-hand-side + Richardson launch are one graph; a replay costs one launch and
+# one small device->host read of the loop state, the history and the validation flags.
+# ---------------------------------------------------------------------------------------------
+
+
+class _SolveGraph:
+    def __init__(self):
+        self.graph = None
+        self.out = None
+        self.checks = []
+
+
+_SOLVE_GRAPHS: dict = {}
+_LAST_LOOP_EVENTS: list = [None]  # (start, end) events of the last graph-replayed loop launch
+_SOLVE_STATS = {"eager": 0, "capture": 0, "replay": 0}
+
+
+_USE_SOLVE_GRAPH = [True]
+
+
+def _solve_graph_key(facs, b, config: RegressionConfig):
+    if not (_USE_SOLVE_GRAPH[0] and _USE_GRAPHS[0] and _USE_FUSED[0]) or len(facs) != 2 \
+            or not grouped2_eligible(facs):
+        return None
+    d0, d1 = int(facs[0].shape[1]), int(facs[1].shape[1])
+    if d0 not in (16, 32, 64) or d1 not in (16, 32, 64) or config.effective_max_iters > 1024:
+        return None
+    if not isinstance(b, torch.Tensor) or b.dtype != torch.float64 or not b.is_contiguous():
+        return None
+    if not (b.is_cuda or b.is_pinned()):
+        return None
+    n_factors = 2
+    eps_one = math.log1p(config.eps / 4.0) / n_factors
+    eps_two = eps_one / (2.0 + eps_one)
+    delta_n = config.delta / (2.0 * n_factors)
+    for a in facs:  # the spectral row-sampling branch (data-dependent shapes) stays eager
+        if math.ceil(config.effective_alpha * spectral_sample_count(int(a.shape[1]), eps_two, delta_n)) < int(a.shape[0]):
+            return None
+    try:
+        key = (torch.cuda.current_device(), torch.cuda.current_stream().cuda_stream,
+               tuple((a.data_ptr(), tuple(a.shape), tuple(a.stride())) for a in facs),
+               (b.data_ptr(), b.numel(), b.is_cuda), config)
+        hash(key)
+    except TypeError:
+        return None
+    return key
+
+
+def _solve_graph_body(facs, b, config: RegressionConfig, s: int):
+    """Launch-only device pipeline of the fused two-factor solve (captured once per key)."""
+    seeds = _spawned_seeds(config.seed, 5)
+    eps_jl = 4.0 * math.log1p(config.eps / 4.0) / 2
+    d0, d1 = int(facs[0].shape[1]), int(facs[1].shape[1])
+    gts = [_gram_dev(a) for a in facs]
+    grams_h = _factor_grams_async(gts)
+    _, _, _, _, _, g2 = _jl_and_sampling(facs, facs, gts, eps_jl, config, True, seeds, s)
+    sd_idx, sd_val, seg, lrow, rrow, cdev = g2
+    b_at = D.empty(s)
+    _lib.call("ks_gather_count", D.p(b), D.p(sd_idx), D.p(cdev), s, D.p(b_at), D.stream())
+    (VL, wL), (VR, wR) = _join_grams(grams_h)
+    struct = _lib.SketchView(facs[0].data_ptr(), d0, d0, facs[1].data_ptr(), d1, d1, s, s, seg.data_ptr(),
+                             lrow.data_ptr(), rrow.data_ptr(), sd_val.data_ptr())
+    max_iters = config.effective_max_iters
+    x = D.empty(d0, d1)
+    hist = D.zeros(max(1, max_iters))
+    rhs = D.empty(d0, d1)
+    state = torch.zeros(4, dtype=torch.int32, device=D.dev())
+    # external events around the loop launch: readable after every replay (bench.py's roofline)
+    ev0 = torch.cuda.Event(enable_timing=True, external=True)
+    ev1 = torch.cuda.Event(enable_timing=True, external=True)
+    ev0.record()
+    _lib.call("ks_richardson_fused_async", ctypes.byref(struct), D.p(cdev), None, D.p(b_at), D.p(VL), D.p(wL),
+              D.p(VR), D.p(wR), None, float(config.lam), float(config.effective_damping), int(max_iters),
+              float(config.residual_tol), D.p(x), D.p(hist), D.p(rhs), D.p(state), D.stream())
+    ev1.record()
+    return dict(x=x, hist=hist, state=state, loop_events=(ev0, ev1),
+                keep=(gts, b_at, sd_idx, sd_val, seg, lrow, rrow, cdev, rhs))
+
+
+def _fast_solve_graph(facs, b, config: RegressionConfig):
+    """(x natural order, iterations, s) from the whole-solve graph, or None when this call has to
+    run eagerly (ineligible input, or the first sight of a key: the eager pass warms every lazy
+    initialisation before capture)."""
+    from . import leverage as _lev
+    key = _solve_graph_key(facs, b, config)
+    if key is None:
+        return None
+    entry = _SOLVE_GRAPHS.get(key)
+    if entry is None:
+        if len(_SOLVE_GRAPHS) >= 4:
+            _SOLVE_GRAPHS.pop(next(iter(_SOLVE_GRAPHS)))
+        _SOLVE_GRAPHS[key] = _SolveGraph()
+        _SOLVE_STATS["eager"] += 1
+        return None
+    s = _regression_sample_count(math.prod(int(a.shape[1]) for a in facs), config)
+    if entry.graph is None:
+        g = torch.cuda.CUDAGraph()
+        cap = _lev.DeferredChecks()
+        outer = _lev._DEFERRED[0]
+        _lev._DEFERRED[0] = cap
+        try:
+            with torch.cuda.graph(g):
+                entry.out = _solve_graph_body(facs, b.reshape(-1), config, s)
+        except Exception:
+            _SOLVE_GRAPHS.pop(key, None)
+            raise
+        finally:
+            _lev._DEFERRED[0] = outer
+        entry.graph, entry.checks = g, cap.items
+        _SOLVE_STATS["capture"] += 1
+        _LAST_LOOP_EVENTS[0] = entry.out["loop_events"]
+    else:
+        _SOLVE_STATS["replay"] += 1
+    _mark("graph launch")
+    _LAST_LOOP_EVENTS[0] = entry.out["loop_events"]
+    entry.graph.replay()
+    out = entry.out
+    deferred = _lev.DeferredChecks()
+    for flags, handler in entry.checks:
+        deferred.add(flags, handler)
+    deferred.stage()
+    st_h = out["state"].to("cpu", non_blocking=True)
+    hist_h = out["hist"].to("cpu", non_blocking=True)
+    x = out["x"].reshape(-1).clone()
+    torch.cuda.current_stream().synchronize()
+    _mark("richardson")
+    try:
+        deferred.run(synced=True)
+    except _CholeskyFailed:
+        return None  # the eager path retries with LU inverses
+    status, iters, hlen = (int(v) for v in st_h[:3].tolist())
+    history = hist_h[:hlen].tolist()
+    if status == 2:
+        raise NumericalFailureError("Richardson iteration diverged", iterations=iters,
+                                    diagnostics={"residual_history": history})
+    return x, iters, s
+
+
 def _fast_solve_dev(facs, b, config: RegressionConfig, caches, trace: FastSolveTrace | None = None):
     """The device pipeline of solvers.py:404-459; returns (x natural order, iterations, s)."""
     from . import leverage as _lev
+    if caches is None and trace is None:
+        got = _fast_solve_graph(facs, b, config)
+        if got is not None:
+            return got
     for use_chol in (True, False):
         deferred = _lev.DeferredChecks()
         _lev._DEFERRED[0] = deferred
@@ -733,6 +880,7 @@ def _fast_solve_pass(facs, b, config: RegressionConfig, caches, trace, use_chol:
         VR, wR = grams[right[0]]
         _mark("precond")
         deferred.stage()  # flag copies complete with the loop launch's own synchronisation
+        _LAST_LOOP_EVENTS[0] = None
         rc = lib.ks_richardson_fused(ctypes.byref(view.struct), D.p(view.perm_arg()), D.p(b_at.contiguous()),
                                      D.p(VL), D.p(wL), D.p(VR), D.p(wR), None, float(lam),
                                      float(config.effective_damping), int(max_iters), float(config.residual_tol),

@@ -199,7 +199,11 @@ def test_graph_replay_matches_eager(golden):
     finally:
         S._USE_GRAPHS[0] = True
     S._PREFIX_GRAPHS.clear()
-    outs = [K.fast_kronecker_regression(fd, bd, cfg()) for _ in range(4)]  # eager, capture, replay x2
+    S._USE_SOLVE_GRAPH[0] = False  # exercise the stage graph (used when the whole solve is not graphed)
+    try:
+        outs = [K.fast_kronecker_regression(fd, bd, cfg()) for _ in range(4)]  # eager, capture, replay x2
+    finally:
+        S._USE_SOLVE_GRAPH[0] = True
     assert any(e.graph is not None for e in S._PREFIX_GRAPHS.values())
     for rep in outs:
         assert rep.iterations == ref.iterations
@@ -208,7 +212,11 @@ def test_graph_replay_matches_eager(golden):
     # the replayed stage reads the factors' current contents: a scaled factor changes the answer
     # exactly like an eager solve of the scaled problem
     fd[0].mul_(2.0)
-    rep2 = K.fast_kronecker_regression(fd, bd, cfg())
+    S._USE_SOLVE_GRAPH[0] = False
+    try:
+        rep2 = K.fast_kronecker_regression(fd, bd, cfg())
+    finally:
+        S._USE_SOLVE_GRAPH[0] = True
     S._USE_GRAPHS[0] = False
     try:
         ref2 = K.fast_kronecker_regression(fd, bd, cfg())
@@ -237,3 +245,33 @@ def test_fused_rhs_loop_matches_separate_rhs(name):
     assert rel(t1.rhs, t2.rhs) <= 1e-13
     # kappa(K^T K + lam I) ~ 1e8-1e9 amplifies the rhs rounding: compare at the measured floor
     assert rel(r1.solution, r2.solution) <= X_TOL[name]
+
+
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_whole_solve_graph_matches_eager(golden, name):
+    """Two-factor solves with device-resident or page-locked host b run as one captured CUDA
+    graph from the second call on; results equal the eager (trace) pipeline bit for bit."""
+    import paper_2209_04876_b200 as K
+    from paper_2209_04876_b200 import solvers as S
+    from paper_2209_04876_b200.solvers import FastSolveTrace
+    n, d = CASES[name]
+    g = golden(name)
+    facs, b = O.synth_regression(n, d, 2, 0)
+    fd = [torch.tensor(a, device="cuda") for a in facs]
+    bd = torch.tensor(b, device="cuda")
+    ref = K.fast_kronecker_regression(fd, bd, cfg(), _trace=FastSolveTrace())  # eager
+    S._SOLVE_GRAPHS.clear()
+    before = dict(S._SOLVE_STATS)
+    outs = [K.fast_kronecker_regression(fd, bd, cfg()) for _ in range(4)]
+    assert S._SOLVE_STATS["capture"] == before["capture"] + 1
+    assert S._SOLVE_STATS["replay"] >= before["replay"] + 2
+    for rep in outs:
+        assert rep.iterations == ref.iterations
+        assert torch.equal(rep.solution, ref.solution)
+    assert rel(outs[-1].solution, g["x"]) <= X_TOL[name]
+    # page-locked host b: the graph gathers the sampled entries through mapped host memory
+    bh = torch.tensor(b).pin_memory()
+    hs = [K.fast_kronecker_regression(fd, bh, cfg()) for _ in range(3)]
+    for rep in hs:
+        assert rep.iterations == ref.iterations
+        np.testing.assert_array_equal(np.asarray(rep.solution), ref.solution.cpu().numpy())

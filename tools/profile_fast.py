@@ -39,7 +39,7 @@ for _ in range(reps):
 torch.cuda.synchronize()
 print("wall", walls, "loss", rep.loss, "iters", rep.iterations)
 from paper_2209_04876_b200 import solvers as _S  # noqa: E402
-print("prefix graph stats:", _S._PREFIX_STATS, "keys:", len(_S._PREFIX_GRAPHS))
+print("prefix graph stats:", _S._PREFIX_STATS, "keys:", len(_S._PREFIX_GRAPHS), "solve graph stats:", _S._SOLVE_STATS)
 ph = (ctypes.c_double * 6)()
 if _lib.load().ks_debug_richardson_phases(rep.iterations, ph) == 0:
     names = ["apply", "sync", "reduce+sync", "precondA+sync", "precondB+sync", "update"]
@@ -190,7 +190,8 @@ if "--phases" in sys.argv:
             gpu_t[name].append(prev[2].elapsed_time(ev) * 1e3)
             host_t[name].append(1e6 * (th - prev[1]))
             prev = (name, th, ev)
-    print(f"phases over 8 solves: wall median {statistics.median(walls2):.0f} us min {min(walls2):.0f} us")
+    print(f"phases over 8 solves: wall median {statistics.median(walls2):.0f} us min {min(walls2):.0f} us",
+          "solve graph stats:", S._SOLVE_STATS)
     for name in order:
         print(f"  {name:20s} gpu median {statistics.median(gpu_t[name]):8.1f} us   host-issue median "
               f"{statistics.median(host_t[name]):8.1f} us")
