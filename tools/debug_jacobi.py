@@ -40,3 +40,34 @@ for name, M in cases.items():
     ref = np.linalg.svd(M, compute_uv=False)
     err = np.max(np.abs(s.cpu().numpy() - ref) / ref.max())
     print(f"{name}: {statistics.median(ts):9.1f} us  sweeps {sw[0]}  sigma err {err:.2e}")
+
+print("two-sided symmetric (ks_sym_eig_batched):")
+lib.ks_sym_eig_batched.argtypes = [ctypes.c_int32, ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p,
+                                   ctypes.c_void_p]
+for name, M in cases.items():
+    d = M.shape[0]
+    if d not in (16, 32, 64) or name == "randn64":
+        continue
+    Mt = D.to_dev(M)
+    s = D.empty(d)
+    V = D.empty(d, d)
+    ptrs = (ctypes.c_void_p * 1)(Mt.data_ptr())
+    lib.ks_sym_eig_batched(1, ptrs, d, D.p(s), D.p(V), D.stream())
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        lib.ks_sym_eig_batched(1, ptrs, d, D.p(s), D.p(V), D.stream())
+        e1.record()
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1) * 1e3)
+    sw = (ctypes.c_int32 * 8)()
+    lib.ks_debug_jacobi_sweeps(sw)
+    w_ref, v_ref = np.linalg.eigh(M)
+    w = s.cpu().numpy()
+    err = np.max(np.abs(np.sort(w) - w_ref)) / np.max(np.abs(w_ref))
+    Vh = V.cpu().numpy()
+    resid = np.max(np.abs(M @ Vh - Vh * w[None, :])) / np.max(np.abs(w_ref))
+    orth = np.max(np.abs(Vh.T @ Vh - np.eye(d)))
+    print(f"{name}: {statistics.median(ts):9.1f} us  sweeps {sw[0]}  eig err {err:.2e}  resid {resid:.2e}  orth {orth:.2e}")
