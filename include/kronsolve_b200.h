@@ -287,6 +287,10 @@ int ks_debug_jl_projection_stamps(uint64_t* out4);
 /* Profiling aid: sweeps used by the last one-sided Jacobi launch (first 8 problems, host out8). */
 int ks_debug_jacobi_sweeps(int32_t* out8);
 
+/* Profiling aid: CTA 0 / thread 0 cycles of the last fixed-size one-sided Jacobi launch, summed
+ * over rounds: (load + dot products + reductions, rotation + update, barrier, rounds); reset on read. */
+int ks_debug_jacobi_stamps(long long* out4);
+
 /* Profiling aid: average SM cycles per phase of the last persistent Richardson run (CTA 0):
  * apply, sync, reduce, precond-A, precond-B, update. */
 int ks_debug_richardson_phases(int32_t iters, double* out6);

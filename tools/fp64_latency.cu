@@ -26,6 +26,26 @@ __global__ void dmma_kernel(int n, double* out, long long* cyc) {
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+// DFMA throughput: CH independent chains per thread, W warps
+template <int CH>
+__global__ void dfma_tp_kernel(int n, double* out, long long* cyc) {
+  double a[CH];
+#pragma unroll
+  for (int k = 0; k < CH; k++) a[k] = threadIdx.x * 1e-9 + k;
+  const double b = 1.0000001, c = 1e-7;
+  long long t0 = clock64();
+  for (int i = 0; i < n; i++) {
+#pragma unroll
+    for (int k = 0; k < CH; k++) a[k] = fma(a[k], b, c);
+  }
+  long long t1 = clock64();
+  if (threadIdx.x == 0) *cyc = (t1 - t0);
+  double s = 0;
+#pragma unroll
+  for (int k = 0; k < CH; k++) s += a[k];
+  out[threadIdx.x] = s;
+}
+
 template <int OP>
 __global__ void lat_kernel(int n, double x0, double* out, long long* cyc) {
   double a = x0 + threadIdx.x * 1e-9, b = 1.0000001, c = 1e-7;
@@ -69,5 +89,13 @@ int main() {
   printf("dmma chains %d warps %2d: %6.1f cycles per dmma-step (per warp), %5.2f cycles/dmma/SM\n", CH, W, \
          (double)*cyc / 1024, (double)*cyc / 1024 / (CH * W));
   DM(1, 1) DM(2, 1) DM(4, 1) DM(8, 1) DM(1, 4) DM(4, 4) DM(1, 8) DM(4, 8) DM(8, 8) DM(4, 16)
+#define TP(CH, W)                                                              \
+  dfma_tp_kernel<CH><<<1, 32 * W>>>(4096, out, cyc);                           \
+  cudaDeviceSynchronize();                                                     \
+  dfma_tp_kernel<CH><<<1, 32 * W>>>(4096, out, cyc);                           \
+  cudaDeviceSynchronize();                                                     \
+  printf("dfma chains %d warps %2d: %6.2f cycles per warp-dfma per SM (%.1f lanes/clk)\n", CH, W,   \
+         (double)*cyc / (4096.0 * CH * W), 32.0 * 4096.0 * CH * W / (double)*cyc);
+  TP(8, 1) TP(8, 4) TP(8, 8) TP(8, 16) TP(8, 32)
   return 0;
 }
