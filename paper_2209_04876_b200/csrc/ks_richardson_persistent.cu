@@ -167,6 +167,9 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
     fence_barrier_init();
   }
   for (int e = tid; e < DL * DRP; e += PT) Xs[e] = 0.0;
+  // slab L rows past a chunk's row count are read by the G tiles (multiplied by zero rows of Z):
+  // keep them finite
+  for (int e = tid; e < 2 * CH_ROWS * DLP; e += PT) sm[S::L_OFF + e] = 0.0;
   __syncthreads();
 
   const int64_t c_beg = a.range[b], c_end = a.range[b + 1];
@@ -283,52 +286,69 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
     if (prof && !rp) g_prof[it * 6 + 0] = clock64();
     KS_STAMP(0)
     // ---------------- P1: sketched normal-operator apply ----------------
+    // Software-pipelined over the CTA's chunks: phase A = samples(c) (CUDA cores), phase B =
+    // G(c) and Y(c+1) together (tensor cores, independent DMMA chains interleaved); two barriers
+    // per chunk.  Chunk c lives in slab buffer (c - c_beg + base) & 1.
     double gacc[G_PER_W][4];
 #pragma unroll
     for (int i = 0; i < G_PER_W; i++) gacc[i][0] = gacc[i][1] = gacc[i][2] = gacc[i][3] = 0.0;
-    int buf = cur;
-    for (int64_t c = c_beg; c < c_end; c++) {
-      const Chunk ch = a.chunks[c];
-      if (tid == 0 && !resident) {
-        const int64_t cn = (c + 1 < c_end) ? c + 1 : c_beg;
-        if (!(cn == c_beg && it + 1 >= a.max_iters)) {
-          issue_chunk<DL, DR>(a, a.chunks[cn], sm, &bars[buf ^ 1], buf ^ 1);
-          pending[buf ^ 1] = 1;
-        }
+    const int64_t nch = c_end - c_beg;
+    const int base = cur;
+    auto wait_buf = [&](int bb) {
+      long long pc0 = 0;
+      if (prof) pc0 = clock64();
+      mbar_wait(&bars[bb], phase[bb]);
+      phase[bb] ^= 1;
+      pending[bb] = 0;
+      if (prof && !rp) p1acc[0] += clock64() - pc0;
+    };
+    auto y_tile = [&](const double* Lsrc, int tile, double (&acc)[4], int k0) {
+      const int m0 = (tile / YT_N) * 16, n0 = (tile % YT_N) * 8;
+      const double a0 = Lsrc[(m0 + g) * DLP + k0 + t4];
+      const double a1 = Lsrc[(m0 + g + 8) * DLP + k0 + t4];
+      const double b0 = Xs[(k0 + t4) * DRP + n0 + g];
+      dmma_16x8x4(acc, a0, a1, b0);
+    };
+    auto y_store = [&](int tile, const double (&acc)[4]) {
+      const int m0 = (tile / YT_N) * 16, n0 = (tile % YT_N) * 8;
+      Ys[(m0 + g) * DRP + n0 + 2 * t4] = acc[0];
+      Ys[(m0 + g) * DRP + n0 + 2 * t4 + 1] = acc[1];
+      Ys[(m0 + g + 8) * DRP + n0 + 2 * t4] = acc[2];
+      Ys[(m0 + g + 8) * DRP + n0 + 2 * t4 + 1] = acc[3];
+    };
+    if (nch > 0) {
+      // prologue: chunk c_beg arrives; chunk c_beg + 1 is fetched; Y(c_beg)
+      if (!resident || it == it0) wait_buf(base);
+      if (tid == 0 && nch > 1) {
+        issue_chunk<DL, DR>(a, a.chunks[c_beg + 1], sm, &bars[base ^ 1], base ^ 1);
+        pending[base ^ 1] = 1;
       }
       long long pc0 = 0;
       if (prof) pc0 = clock64();
-      if (!resident || it == it0) {
-        mbar_wait(&bars[buf], phase[buf]);
-        phase[buf] ^= 1;
-        pending[buf] = 0;
-      }
-      if (prof && !rp) p1acc[0] += clock64() - pc0;
-      const double* Ls = sm + S::L_OFF + buf * CH_ROWS * DLP;
-      const double* Rs = sm + S::R_OFF + buf * CH_S * DRP;
-      const int nrows = (int)(ch.u_e - ch.u_b);
-      // Y = L_chunk X
+      if (!rp) {
+        const double* L0 = sm + S::L_OFF + base * CH_ROWS * DLP;
 #pragma unroll
-      for (int yi = 0; yi < Y_PER_W; yi++) {
-        const int tile = warp + yi * PW;
-        if (!rp && tile < Y_TILES) {
-          const int m0 = (tile / YT_N) * 16, n0 = (tile % YT_N) * 8;
-          double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int yi = 0; yi < Y_PER_W; yi++) {
+          const int tile = warp + yi * PW;
+          if (tile < Y_TILES) {
+            double acc[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-          for (int k0 = 0; k0 < DL; k0 += 4) {
-            const double a0 = Ls[(m0 + g) * DLP + k0 + t4];
-            const double a1 = Ls[(m0 + g + 8) * DLP + k0 + t4];
-            const double b0 = Xs[(k0 + t4) * DRP + n0 + g];
-            dmma_16x8x4(acc, a0, a1, b0);
+            for (int k0 = 0; k0 < DL; k0 += 4) y_tile(L0, tile, acc, k0);
+            y_store(tile, acc);
           }
-          Ys[(m0 + g) * DRP + n0 + 2 * t4] = acc[0];
-          Ys[(m0 + g) * DRP + n0 + 2 * t4 + 1] = acc[1];
-          Ys[(m0 + g + 8) * DRP + n0 + 2 * t4] = acc[2];
-          Ys[(m0 + g + 8) * DRP + n0 + 2 * t4 + 1] = acc[3];
         }
       }
       __syncthreads();
-      if (prof && !rp) { const long long now = clock64(); p1acc[1] += now - pc0; pc0 = now; }
+      if (prof && !rp) p1acc[1] += clock64() - pc0;
+    }
+    for (int64_t c = c_beg; c < c_end; c++) {
+      const Chunk ch = a.chunks[c];
+      const int bc = (int)((c - c_beg + base) & 1);
+      const double* Ls = sm + S::L_OFF + bc * CH_ROWS * DLP;
+      const double* Rs = sm + S::R_OFF + bc * CH_S * DRP;
+      const int nrows = (int)(ch.u_e - ch.u_b);
+      long long pc0 = 0;
+      if (prof) pc0 = clock64();
       // samples: half-warp per left row, entries ql, ql + 16, ... per lane (conflict-free)
       {
         const int r = tid >> 4, ql = tid & 15;
@@ -403,27 +423,61 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
       }
       __syncthreads();
       if (prof && !rp) { const long long now = clock64(); p1acc[2] += now - pc0; pc0 = now; }
-      // G += L_chunk^T Z   (K = CH_ROWS; rows >= nrows have Z == 0)
+      // phase B: G += L_c^T Z (K = CH_ROWS; rows >= nrows have Z == 0 and finite stale L) and
+      // Y(c+1) = L_{c+1} X, their DMMA chains interleaved
+      const bool next = c + 1 < c_end;
+      if (next) wait_buf(bc ^ 1);
+      const double* Ln = sm + S::L_OFF + (bc ^ 1) * CH_ROWS * DLP;
+      double yacc[Y_PER_W][4];
 #pragma unroll
-      for (int gi = 0; gi < G_PER_W; gi++) {
-        const int tile = warp + gi * PW;
-        if (tile < G_TILES) {
-          const int m0 = (tile / GT_N) * 16, n0 = (tile % GT_N) * 8;
+      for (int yi = 0; yi < Y_PER_W; yi++) yacc[yi][0] = yacc[yi][1] = yacc[yi][2] = yacc[yi][3] = 0.0;
+      const bool do_y = next && !rp;
 #pragma unroll
-          for (int k0 = 0; k0 < CH_ROWS; k0 += 4) {
-            const bool ok = k0 + t4 < nrows;
-            const double a0 = ok ? Ls[(k0 + t4) * DLP + m0 + g] : 0.0;
-            const double a1 = ok ? Ls[(k0 + t4) * DLP + m0 + g + 8] : 0.0;
-            const double b0 = Zs[(k0 + t4) * DRP + n0 + g];
-            dmma_16x8x4(gacc[gi], a0, a1, b0);
+      for (int k0 = 0; k0 < DL; k0 += 4) {
+        if (do_y) {
+#pragma unroll
+          for (int yi = 0; yi < Y_PER_W; yi++) {
+            const int tile = warp + yi * PW;
+            if (tile < Y_TILES) y_tile(Ln, tile, yacc[yi], k0);
+          }
+        }
+        if (k0 < CH_ROWS) {
+#pragma unroll
+          for (int gi = 0; gi < G_PER_W; gi++) {
+            const int tile = warp + gi * PW;
+            if (tile < G_TILES) {
+              const int m0 = (tile / GT_N) * 16, n0 = (tile % GT_N) * 8;
+              const double a0 = Ls[(k0 + t4) * DLP + m0 + g];
+              const double a1 = Ls[(k0 + t4) * DLP + m0 + g + 8];
+              const double b0 = Zs[(k0 + t4) * DRP + n0 + g];
+              dmma_16x8x4(gacc[gi], a0, a1, b0);
+            }
           }
         }
       }
-      __syncthreads();
+      (void)nrows;
+      if (do_y) {  // nobody reads Ys in phase B (the sample phase of chunk c is over)
+#pragma unroll
+        for (int yi = 0; yi < Y_PER_W; yi++) {
+          const int tile = warp + yi * PW;
+          if (tile < Y_TILES) y_store(tile, yacc[yi]);
+        }
+      }
+      __syncthreads();  // Y(c+1) visible; Zs and slab bc no longer read
       if (prof && !rp) p1acc[3] += clock64() - pc0;
-      if (!resident) buf ^= 1;
+      // slab bc is free: fetch chunk c + 2, or this CTA's first chunk of the next pass
+      if (tid == 0 && !resident) {
+        int64_t cn = -1;
+        if (c + 2 < c_end) cn = c + 2;
+        else if (c + 2 == c_end && it + 1 < a.max_iters) cn = c_beg;
+        if (cn >= 0) {
+          issue_chunk<DL, DR>(a, a.chunks[cn], sm, &bars[bc], bc);
+          pending[bc] = 1;
+        }
+      }
     }
-    cur = buf;
+    // the buffer holding the next pass's first chunk (in flight); the other one is free
+    if (!resident) cur = (int)((base + nch) & 1);
     double* P = a.part + (size_t)b * NE;
 #pragma unroll
     for (int gi = 0; gi < G_PER_W; gi++) {
