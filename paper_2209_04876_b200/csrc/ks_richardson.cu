@@ -23,7 +23,7 @@ int richardson_persistent(cudaStream_t st, const ks_sketch_view* sk, const doubl
                           const double* dinv, const double* wL, const double* wR, double* rhs, bool rhs_in_kernel,
                           const double* b_at, const int64_t* perm, double lam, double damping, int max_iters,
                           double residual_tol, double* x, double* hist, int* iters, int* hist_len, int* status,
-                          const int64_t* counts_dev, int* state_dev);
+                          const int64_t* counts_dev, int* state_dev, bool eig_mode);
 }
 
 namespace {
@@ -206,7 +206,7 @@ extern "C" int ks_richardson_sketched(const ks_sketch_view* sk, const double* VL
     int it = 0, hl = 0;
     int rc = ks::richardson_persistent(st, sk, VL, VR, dinv, nullptr, nullptr, const_cast<double*>(rhs), false,
                                        nullptr, nullptr, lam, damping, max_iters, residual_tol, x, hist, &it, &hl,
-                                       &status, nullptr, nullptr);
+                                       &status, nullptr, nullptr, false);
     if (rc) return rc;
     *iters = it;
     *hist_len = hl;
@@ -268,7 +268,8 @@ extern "C" int ks_richardson_fused(const ks_sketch_view* sk, const int64_t* perm
   KS_REQUIRE(dinv || (wL && wR), KS_EINVAL, "need dinv or both eigenvalue vectors");
   int status = 0, it = 0, hl = 0;
   int rc = ks::richardson_persistent(st, sk, VL, VR, dinv, wL, wR, rhs_out, true, b_at, perm, lam, damping,
-                                     max_iters, residual_tol, x, hist, &it, &hl, &status, nullptr, nullptr);
+                                     max_iters, residual_tol, x, hist, &it, &hl, &status, nullptr, nullptr,
+                                     !getenv("KS_NO_EIGBASIS"));
   if (rc) return rc;
   *iters = it;
   *hist_len = hl;
@@ -296,5 +297,6 @@ extern "C" int ks_richardson_fused_async(const ks_sketch_view* sk, const int64_t
   KS_REQUIRE(counts_dev && state_dev, KS_EINVAL, "need device counts and a device state buffer");
   int status = 0, it = 0, hl = 0;
   return ks::richardson_persistent(st, sk, VL, VR, dinv, wL, wR, rhs_out, true, b_at, perm, lam, damping, max_iters,
-                                   residual_tol, x, hist, &it, &hl, &status, counts_dev, state_dev);
+                                   residual_tol, x, hist, &it, &hl, &status, counts_dev, state_dev,
+                                   !getenv("KS_NO_EIGBASIS"));
 }

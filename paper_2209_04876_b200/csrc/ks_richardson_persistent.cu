@@ -51,6 +51,9 @@ struct PArgs {
   const double* wR;       // DR
   double* rhs;            // DL x DR (input, or output when rhs_in_kernel)
   int rhs_in_kernel;      // pass -1 builds rhs = sum_t v_t (v_t b_t) L_u R_t^T (Rpack pad slot 1 = v_t b_t)
+  int eig_mode;           // the packed rows are L VL / R VR: the loop runs in the preconditioner's
+                          // eigenbasis, where the preconditioner is the diagonal dinv (no P3/P4)
+  double* rhs_nat_out;    // eig_mode: VL rhs' VR^T (natural-order right-hand side), may be null
   double lam, damping, residual_tol;
   int max_iters;
   double* part;           // grid x DL x DR
@@ -496,6 +499,7 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
     KS_STAMP(2)
     if (prof && !rp) g_prof[it * 6 + 2] = clock64();
     // ---------------- P2: R = sum G + lam X - rhs ----------------
+    double eig_sq = 0.0;
     {
       // this CTA's slice of every partial is staged in shared memory with cp.async (all copies in
       // flight at once), then 8 threads per element sum the G partials in a fixed order
@@ -537,14 +541,98 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
         }
         if (ql == 0) {
           const int i = e / DR, k = e - i * DR;
-          if (rp) a.rhs[e] = s + cmp;
-          else a.R[e] = __dsub_rn(__dadd_rn(s + cmp, __dmul_rn(a.lam, Xs[i * DRP + k])), __ldcg(&a.rhs[e]));
+          if (a.eig_mode) {
+            // eigenbasis: step' = dinv o (G' + lam x' - rhs'), plus this CTA's share of ||step'||^2
+            double r;
+            if (rp) {
+              r = s + cmp;
+              a.rhs[e] = r;
+            } else {
+              r = __dsub_rn(__dadd_rn(s + cmp, __dmul_rn(a.lam, Xs[i * DRP + k])), __ldcg(&a.rhs[e]));
+            }
+            double dv;
+            if (a.dinv) {
+              dv = __ldg(&a.dinv[e]);
+            } else {
+              const double ev = __dadd_rn(__dmul_rn(__ldg(&a.wL[i]), __ldg(&a.wR[k])), a.lam);
+              dv = ev > 0.0 ? __ddiv_rn(1.0, ev) : 0.0;
+            }
+            const double st = r * dv;
+            if (!rp) a.step[e] = st;
+            eig_sq = fma(st, st, eig_sq);
+          } else if (rp) {
+            a.rhs[e] = s + cmp;
+          } else {
+            a.R[e] = __dsub_rn(__dadd_rn(s + cmp, __dmul_rn(a.lam, Xs[i * DRP + k])), __ldcg(&a.rhs[e]));
+          }
         }
+      }
+      if (a.eig_mode) {  // fixed-order CTA partial of ||step'||^2
+        eig_sq = block_sum(eig_sq, Ws + 192);
+        if (tid == 0) a.rowsq[b] = eig_sq;
       }
     }
     KS_STAMP(3)
     grid.sync();
     KS_STAMP(4)
+    if (a.eig_mode) {
+      // every CTA: ||step'|| from the G partials (fixed order) and, past the rhs pass, the step
+      double* St = sm + S::R_OFF + (cur ^ 1) * CH_S * DRP;
+      if (!rp) stage(St, a.step, DL, DR, DRP, true);
+      for (int q = tid; q < G; q += PT) Ws[q] = __ldcg(&a.rowsq[q]);  // G <= 148 < 192
+      cp_async_wait_all();
+      __syncthreads();
+      if (warp == 0) {
+        double t = 0.0;
+        for (int q = lane; q < G; q += 32) t += Ws[q];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double os = __shfl_xor_sync(0xffffffffu, t, o);
+          t = (lane & o) ? os + t : t + os;
+        }
+        if (lane == 0) Ws[250] = sqrt(t);
+      }
+      __syncthreads();
+      const double nrm = Ws[250];
+      __syncthreads();
+      if (rp) {
+        tol = a.residual_tol * fmax(nrm, DBL_MIN);
+        continue;
+      }
+      if (prof) g_prof[it * 6 + 3] = clock64();
+      KS_STAMP(5)
+      KS_STAMP(6)
+      if (tid == 0) Hs[it] = nrm;
+      hlen = it + 1;
+      if (nrm <= tol) {
+        status = 1;
+        break;
+      }
+      if (tid == 0) {
+        int div = 0;
+        if (hlen > 5) {
+          bool inc = true;
+          for (int i = hlen - 6; i < hlen - 1; i++) inc &= Hs[i + 1] > Hs[i];
+          div = inc && (Hs[hlen - 1] > 10.0 * Hs[hlen - 6]);
+        }
+        s_flag = div;
+      }
+      __syncthreads();
+      if (s_flag) {
+        status = 2;
+        break;
+      }
+      for (int e = tid; e < NE; e += PT) {
+        const int i = e / DR, k = e - i * DR;
+        Xs[i * DRP + k] = __dsub_rn(Xs[i * DRP + k], __dmul_rn(a.damping, St[i * DRP + k]));
+      }
+      iters = it + 1;
+      __syncthreads();
+      if (prof) g_prof[it * 6 + 4] = g_prof[it * 6 + 5] = clock64();
+      KS_STAMP(7)
+      KS_STAMP(8)
+      continue;
+    }
     if (rp) {
       tol = init_tol();
       continue;
@@ -597,11 +685,43 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
     iters = it + 1;
     __syncthreads();
   }
-  if (b == 0) {
-    for (int e = tid; e < NE; e += PT) {
-      const int i = e / DR, k = e - i * DR;
-      a.x_out[e] = Xs[i * DRP + k];
+  // an early stop leaves the next iteration's prefetch in flight: drain it
+  if (tid == 0)
+    for (int k = 0; k < 2; k++)
+      if (pending[k]) {
+        mbar_wait(&bars[k], phase[k]);
+        pending[k] = 0;
+      }
+  __syncthreads();
+  if (a.eig_mode) {
+    // back to the natural basis, one row per CTA: x = VL x' VR^T (CTAs 0..DL-1) and, when asked,
+    // rhs = VL rhs' VR^T (CTAs DL..2 DL-1); both slab buffers are free now
+    double* VRts = sm + S::R_OFF;
+    double* Ms = sm + S::R_OFF + CH_S * DRP;
+    const bool want_rhs = a.rhs_nat_out != nullptr;
+    for (int row = b; row < (want_rhs ? 2 * DL : DL); row += G) {
+      const bool is_rhs = row >= DL;
+      const int r = is_rhs ? row - DL : row;
+      stage(VRts, a.VRt, DR, DR, DRP, false);
+      if (is_rhs) stage(Ms, a.rhs, DL, DR, DRP, true);
+      for (int k = tid; k < DL; k += PT) Ws[k] = __ldg(&a.VL[r * DL + k]);
+      cp_async_wait_all();
+      __syncthreads();
+      vecmat(Ws, is_rhs ? Ms : Xs, DL, DR, DRP, Ws + 64);  // (VL M)[r, :]
+      __syncthreads();
+      vecmat(Ws + 64, VRts, DR, DR, DRP, Ws + 128);        // ((VL M) VR^T)[r, :]
+      __syncthreads();
+      double* dst = is_rhs ? a.rhs_nat_out : a.x_out;
+      for (int c = tid; c < DR; c += PT) dst[r * DR + c] = Ws[128 + c];
+      __syncthreads();
     }
+  }
+  if (b == 0) {
+    if (!a.eig_mode)
+      for (int e = tid; e < NE; e += PT) {
+        const int i = e / DR, k = e - i * DR;
+        a.x_out[e] = Xs[i * DRP + k];
+      }
     for (int i = tid; i < hlen; i += PT) a.hist[i] = Hs[i];
     if (tid == 0) {
       for (int k = 0; k < 4; k++) g_p1split[k] = p1acc[k];
@@ -610,10 +730,6 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
       a.state[2] = hlen;
     }
   }
-  // an early stop leaves the next iteration's prefetch in flight: drain it before exiting
-  if (tid == 0)
-    for (int k = 0; k < 2; k++)
-      if (pending[k]) mbar_wait(&bars[k], phase[k]);
 }
 
 // dst row i = src row rows[i] (d entries) + padding; pad slot 0 carries extra[i] if given, pad
@@ -632,6 +748,47 @@ __global__ void pack_rows_kernel(const double* __restrict__ src, int64_t ld, con
   else if (c == d && extra) v = extra[i];
   else if (c == d + 1 && b) v = __dmul_rn(extra[i], b[perm ? perm[i] : i]);
   dst[e] = v;
+}
+
+// Eigenbasis packing: dst row i = (src row rows[i]) V (d x d, row-major), padding as in
+// pack_rows_kernel.  XF_ROWS rows per block, V and the gathered rows staged in shared memory.
+constexpr int XF_ROWS = 32;
+__global__ void __launch_bounds__(256) pack_rows_xform_kernel(
+    const double* __restrict__ src, int64_t ld, const int64_t* __restrict__ rows, int64_t n_host,
+    const int64_t* __restrict__ n_dev, int d, int dp, const double* __restrict__ V,
+    const double* __restrict__ extra, const double* __restrict__ b, const int64_t* __restrict__ perm,
+    double* __restrict__ dst) {
+  extern __shared__ double xs[];
+  double* Vs = xs;               // d x d
+  double* Rw = xs + d * d;       // XF_ROWS x (d + 1)
+  const int64_t n = n_dev ? *n_dev : n_host;
+  const int64_t i0 = (int64_t)blockIdx.x * XF_ROWS;
+  if (i0 >= n) return;
+  const int tid = threadIdx.x;
+  for (int e = tid; e < d * d; e += blockDim.x) ks_cp_async8(&Vs[e], V + e);
+  for (int e = tid; e < XF_ROWS * d; e += blockDim.x) {
+    const int r = e / d, k = e - r * d;
+    const int64_t i = i0 + r;
+    const bool ok = i < n;
+    ks_cp_async8(&Rw[r * (d + 1) + k], ok ? src + rows[i] * ld + k : src, ok);
+  }
+  ks_cp_async_wait_all();
+  __syncthreads();
+  for (int e = tid; e < XF_ROWS * dp; e += blockDim.x) {
+    const int r = e / dp, c = e - r * dp;
+    const int64_t i = i0 + r;
+    if (i >= n) continue;
+    double v = 0.0;
+    if (c < d) {
+      const double* row = Rw + r * (d + 1);
+      for (int k = 0; k < d; k++) v = fma(row[k], Vs[k * d + c], v);
+    } else if (c == d && extra) {
+      v = extra[i];
+    } else if (c == d + 1 && b) {
+      v = __dmul_rn(extra[i], b[perm ? perm[i] : i]);
+    }
+    dst[i * dp + c] = v;
+  }
 }
 
 __global__ void transpose_sq_kernel2(const double* __restrict__ a, int d, double* __restrict__ out) {
@@ -787,7 +944,7 @@ int richardson_persistent(cudaStream_t st, const ks_sketch_view* sk, const doubl
                           const double* dinv, const double* wL, const double* wR, double* rhs, bool rhs_in_kernel,
                           const double* b_at, const int64_t* perm, double lam, double damping, int max_iters,
                           double residual_tol, double* x, double* hist, int* iters, int* hist_len, int* status,
-                          const int64_t* counts_dev, int* state_dev) {
+                          const int64_t* counts_dev, int* state_dev, bool eig_mode) {
   // counts_dev ([nnz, u_left] on the device): sk->nnz / sk->u_left are capacities and nothing
   // here reads the counts on the host; state_dev: the loop state stays on the device (no sync)
   const int dL = sk->dL, dR = sk->dR;
@@ -797,14 +954,16 @@ int richardson_persistent(cudaStream_t st, const ks_sketch_view* sk, const doubl
   const int grid = num_sms();
   const int64_t cap = (ul + CH_ROWS - 1) / CH_ROWS + nnz / CH_S + 2;  // >= chunk count
   Scratch<double> Lpack(ul * dLp + 2, st), Rpack(nnz * dRp + 2, st), part((int64_t)grid * dL * dR, st);
-  Scratch<double> R((int64_t)dL * dR, st), T((int64_t)dL * dR, st), stepb((int64_t)dL * dR, st), rowsq(dL, st);
+  Scratch<double> R((int64_t)dL * dR, st), T((int64_t)dL * dR, st), stepb((int64_t)dL * dR, st),
+      rowsq(dL > grid ? dL : grid, st), rhs_e(eig_mode ? (int64_t)dL * dR : 0, st);
   Scratch<double> VRt((int64_t)dR * dR, st);
   Scratch<Chunk> dch(cap, st);
   Scratch<int64_t> cpre(cap, st), drange(grid + 2, st);
   Scratch<int> state_s(state_dev ? 0 : 4, st);
   int* statep = state_dev ? state_dev : state_s.p;
+  KS_REQUIRE(eig_mode <= rhs_in_kernel, KS_EINVAL, "the eigenbasis loop builds its own right-hand side");
   KS_REQUIRE(Lpack.p && Rpack.p && part.p && R.p && T.p && stepb.p && rowsq.p && VRt.p && dch.p && drange.p &&
-                 cpre.p && statep,
+                 cpre.p && statep && (!eig_mode || rhs_e.p),
              KS_ECUDA, "scratch allocation failed");
   // estimated chunk cost (SM cycles): the Y and G DMMA tiles are fixed per chunk (the FP64 tensor
   // pipe issues one m16n8k4 per ~8 cycles per SM), the sample phase follows the chunk's longest
@@ -814,12 +973,29 @@ int richardson_persistent(cudaStream_t st, const ks_sketch_view* sk, const doubl
                                      (int64_t)dR / 4, 120, dch.p,
                                      cpre.p, drange.p, drange.p + grid + 1);
   KS_CHECK_LAUNCH();
-  pack_rows_kernel<<<ceil_div_u(ul * dLp, 256), 256, 0, st>>>(sk->Lmat, sk->ldl, sk->lrow, ul,
-                                                               counts_dev ? counts_dev + 1 : nullptr, dL, dLp,
-                                                               nullptr, nullptr, nullptr, Lpack.p);
-  KS_CHECK_LAUNCH();
-  pack_rows_kernel<<<ceil_div_u(nnz * dRp, 256), 256, 0, st>>>(sk->Rmat, sk->ldr, sk->rrow, nnz, counts_dev, dR, dRp,
-                                                                sk->v, rhs_in_kernel ? b_at : nullptr, perm, Rpack.p);
+  if (eig_mode) {
+    // rows pre-transformed into the preconditioner's eigenbasis: L VL and R VR
+    const size_t smL = sizeof(double) * ((size_t)dL * dL + (size_t)XF_ROWS * (dL + 1));
+    const size_t smR = sizeof(double) * ((size_t)dR * dR + (size_t)XF_ROWS * (dR + 1));
+    KS_TRY_CUDA(cudaFuncSetAttribute(pack_rows_xform_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)(smL > smR ? smL : smR)));
+    pack_rows_xform_kernel<<<ceil_div_u(ul, XF_ROWS), 256, smL, st>>>(sk->Lmat, sk->ldl, sk->lrow, ul,
+                                                                      counts_dev ? counts_dev + 1 : nullptr, dL,
+                                                                      dLp, VL, nullptr, nullptr, nullptr, Lpack.p);
+    KS_CHECK_LAUNCH();
+    pack_rows_xform_kernel<<<ceil_div_u(nnz, XF_ROWS), 256, smR, st>>>(sk->Rmat, sk->ldr, sk->rrow, nnz, counts_dev,
+                                                                       dR, dRp, VR, sk->v,
+                                                                       rhs_in_kernel ? b_at : nullptr, perm,
+                                                                       Rpack.p);
+  } else {
+    pack_rows_kernel<<<ceil_div_u(ul * dLp, 256), 256, 0, st>>>(sk->Lmat, sk->ldl, sk->lrow, ul,
+                                                                 counts_dev ? counts_dev + 1 : nullptr, dL, dLp,
+                                                                 nullptr, nullptr, nullptr, Lpack.p);
+    KS_CHECK_LAUNCH();
+    pack_rows_kernel<<<ceil_div_u(nnz * dRp, 256), 256, 0, st>>>(sk->Rmat, sk->ldr, sk->rrow, nnz, counts_dev, dR,
+                                                                  dRp, sk->v, rhs_in_kernel ? b_at : nullptr, perm,
+                                                                  Rpack.p);
+  }
   KS_CHECK_LAUNCH();
   transpose_sq_kernel2<<<ceil_div_u((int64_t)dR * dR, 256), 256, 0, st>>>(VR, dR, VRt.p);
   KS_CHECK_LAUNCH();
@@ -827,6 +1003,11 @@ int richardson_persistent(cudaStream_t st, const ks_sketch_view* sk, const doubl
   a.Lpack = Lpack.p; a.Rpack = Rpack.p; a.seg = sk->seg; a.chunks = dch.p; a.range = drange.p;
   a.VL = VL; a.VR = VR; a.VRt = VRt.p; a.dinv = dinv; a.wL = wL; a.wR = wR; a.rhs = rhs;
   a.rhs_in_kernel = rhs_in_kernel ? 1 : 0;
+  a.eig_mode = eig_mode ? 1 : 0;
+  if (eig_mode) {  // the loop keeps rhs' = VL^T rhs VR internally; the natural one goes to rhs
+    a.rhs = rhs_e.p;
+    a.rhs_nat_out = rhs;
+  }
   a.lam = lam; a.damping = damping; a.residual_tol = residual_tol; a.max_iters = max_iters;
   a.part = part.p; a.R = R.p; a.T = T.p; a.step = stepb.p; a.rowsq = rowsq.p; a.x_out = x; a.hist = hist;
   a.state = statep;
