@@ -750,45 +750,96 @@ __global__ void pack_rows_kernel(const double* __restrict__ src, int64_t ld, con
   dst[e] = v;
 }
 
-// Eigenbasis packing: dst row i = (src row rows[i]) V (d x d, row-major), padding as in
-// pack_rows_kernel.  XF_ROWS rows per block, V and the gathered rows staged in shared memory.
-constexpr int XF_ROWS = 32;
+// Eigenbasis packing: dst row i = (src row rows[i]) V (D x D, row-major), padding as in
+// pack_rows_kernel.  64 gathered rows per block on the FP64 tensor cores (4 x D/8 m16n8 tiles,
+// chains interleaved), rows and V staged in shared memory with asynchronous copies.
+constexpr int XF_ROWS = 64;
+template <int D>
 __global__ void __launch_bounds__(256) pack_rows_xform_kernel(
     const double* __restrict__ src, int64_t ld, const int64_t* __restrict__ rows, int64_t n_host,
-    const int64_t* __restrict__ n_dev, int d, int dp, const double* __restrict__ V,
-    const double* __restrict__ extra, const double* __restrict__ b, const int64_t* __restrict__ perm,
-    double* __restrict__ dst) {
-  extern __shared__ double xs[];
-  double* Vs = xs;               // d x d
-  double* Rw = xs + d * d;       // XF_ROWS x (d + 1)
+    const int64_t* __restrict__ n_dev, int dp, const double* __restrict__ V, const double* __restrict__ extra,
+    const double* __restrict__ b, const int64_t* __restrict__ perm, double* __restrict__ dst) {
+  constexpr int LDA = D + 4, LDV = D + 4;
+  constexpr int TILES = (XF_ROWS / 16) * (D / 8), PER_W = (TILES + 7) / 8;
+  extern __shared__ __align__(16) double xf_sm[];
+  double* As = xf_sm;                 // XF_ROWS x LDA
+  double* Vs = xf_sm + XF_ROWS * LDA; // D x LDV
   const int64_t n = n_dev ? *n_dev : n_host;
   const int64_t i0 = (int64_t)blockIdx.x * XF_ROWS;
   if (i0 >= n) return;
-  const int tid = threadIdx.x;
-  for (int e = tid; e < d * d; e += blockDim.x) ks_cp_async8(&Vs[e], V + e);
-  for (int e = tid; e < XF_ROWS * d; e += blockDim.x) {
-    const int r = e / d, k = e - r * d;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t4 = lane & 3;
+  for (int e = tid; e < D * D / 2; e += 256) {
+    const int r = (2 * e) / D, c = (2 * e) % D;
+    ks_cp_async8(&Vs[r * LDV + c], V + r * D + c);
+    ks_cp_async8(&Vs[r * LDV + c + 1], V + r * D + c + 1);
+  }
+  for (int e = tid; e < XF_ROWS * D; e += 256) {
+    const int r = e / D, k = e % D;
     const int64_t i = i0 + r;
     const bool ok = i < n;
-    ks_cp_async8(&Rw[r * (d + 1) + k], ok ? src + rows[i] * ld + k : src, ok);
+    ks_cp_async8(&As[r * LDA + k], ok ? src + rows[i] * ld + k : src, ok);
   }
   ks_cp_async_wait_all();
   __syncthreads();
-  for (int e = tid; e < XF_ROWS * dp; e += blockDim.x) {
-    const int r = e / dp, c = e - r * dp;
+  double acc[PER_W][4];
+#pragma unroll
+  for (int q = 0; q < PER_W; q++) acc[q][0] = acc[q][1] = acc[q][2] = acc[q][3] = 0.0;
+#pragma unroll
+  for (int k0 = 0; k0 < D; k0 += 4) {
+#pragma unroll
+    for (int q = 0; q < PER_W; q++) {
+      const int tile = warp + q * 8;
+      if (tile < TILES) {
+        const int m0 = (tile / (D / 8)) * 16, n0 = (tile % (D / 8)) * 8;
+        dmma_16x8x4(acc[q], As[(m0 + g) * LDA + k0 + t4], As[(m0 + g + 8) * LDA + k0 + t4],
+                    Vs[(k0 + t4) * LDV + n0 + g]);
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < PER_W; q++) {
+    const int tile = warp + q * 8;
+    if (tile < TILES) {
+      const int m0 = (tile / (D / 8)) * 16, n0 = (tile % (D / 8)) * 8;
+      const int64_t r0 = i0 + m0 + g, r1 = r0 + 8;
+      if (r0 < n) {
+        dst[r0 * dp + n0 + 2 * t4] = acc[q][0];
+        dst[r0 * dp + n0 + 2 * t4 + 1] = acc[q][1];
+      }
+      if (r1 < n) {
+        dst[r1 * dp + n0 + 2 * t4] = acc[q][2];
+        dst[r1 * dp + n0 + 2 * t4 + 1] = acc[q][3];
+      }
+    }
+  }
+  // padding: v_t, v_t b_t, zeros
+  for (int e = tid; e < XF_ROWS * (dp - D); e += 256) {
+    const int r = e / (dp - D), c = D + e % (dp - D);
     const int64_t i = i0 + r;
     if (i >= n) continue;
     double v = 0.0;
-    if (c < d) {
-      const double* row = Rw + r * (d + 1);
-      for (int k = 0; k < d; k++) v = fma(row[k], Vs[k * d + c], v);
-    } else if (c == d && extra) {
-      v = extra[i];
-    } else if (c == d + 1 && b) {
-      v = __dmul_rn(extra[i], b[perm ? perm[i] : i]);
-    }
+    if (c == D && extra) v = extra[i];
+    else if (c == D + 1 && b) v = __dmul_rn(extra[i], b[perm ? perm[i] : i]);
     dst[i * dp + c] = v;
   }
+}
+
+template <int D>
+static void launch_xform(cudaStream_t st, const double* src, int64_t ld, const int64_t* rows, int64_t n_host,
+                         const int64_t* n_dev, int dp, const double* V, const double* extra, const double* b,
+                         const int64_t* perm, double* dst) {
+  const int smem = (int)sizeof(double) * (XF_ROWS * (D + 4) + D * (D + 4));
+  cudaFuncSetAttribute(pack_rows_xform_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  pack_rows_xform_kernel<D><<<ceil_div_u(n_host, XF_ROWS), 256, smem, st>>>(src, ld, rows, n_host, n_dev, dp, V,
+                                                                           extra, b, perm, dst);
+}
+
+static void xform_rows(cudaStream_t st, int d, const double* src, int64_t ld, const int64_t* rows, int64_t n_host,
+                       const int64_t* n_dev, int dp, const double* V, const double* extra, const double* b,
+                       const int64_t* perm, double* dst) {
+  if (d == 16) launch_xform<16>(st, src, ld, rows, n_host, n_dev, dp, V, extra, b, perm, dst);
+  else if (d == 32) launch_xform<32>(st, src, ld, rows, n_host, n_dev, dp, V, extra, b, perm, dst);
+  else launch_xform<64>(st, src, ld, rows, n_host, n_dev, dp, V, extra, b, perm, dst);
 }
 
 __global__ void transpose_sq_kernel2(const double* __restrict__ a, int d, double* __restrict__ out) {
@@ -804,6 +855,7 @@ __global__ void transpose_sq_kernel2(const double* __restrict__ a, int d, double
 // total * (b+1) / G exceeds the chunk's cost midpoint).  Costs are integers, so the plan is
 // exact and deterministic.  One block.
 constexpr int PLAN_T = 1024;
+constexpr int PLAN_SM_SEG = 26000;  // segment offsets staged in shared memory up to this count
 
 // Piece k of the group whose rows are [ub, ue) and samples [sb, se): its chunk and cost.
 __device__ __forceinline__ int64_t plan_piece(const int64_t* __restrict__ seg, int64_t ub, int64_t ue, int64_t sb,
@@ -838,10 +890,16 @@ __global__ void __launch_bounds__(PLAN_T) plan_kernel(const int64_t* __restrict_
                                                       int64_t* __restrict__ range, int64_t* __restrict__ nchunks) {
   __shared__ int64_t wsum_p[32], wsum_c[32];
   __shared__ int64_t carry_p, carry_c;
+  extern __shared__ int64_t plan_sm[];  // segment offsets, when they fit (latency of the searches)
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t ul = ul_dev ? *ul_dev : ul_host;
   const int64_t ngroups = (ul + CH_ROWS - 1) / CH_ROWS;
   if (tid == 0) carry_p = carry_c = 0;
+  if (ul + 1 <= PLAN_SM_SEG) {
+    for (int64_t i = tid; i <= ul; i += PLAN_T) ks_cp_async8(&plan_sm[i], seg + i);
+    ks_cp_async_wait_all();
+    seg = plan_sm;
+  }
   __syncthreads();
   for (int64_t g0 = 0; g0 < ngroups; g0 += PLAN_T) {
     const int64_t gidx = g0 + tid;
@@ -969,24 +1027,20 @@ int richardson_persistent(cudaStream_t st, const ks_sketch_view* sk, const doubl
   // pipe issues one m16n8k4 per ~8 cycles per SM), the sample phase follows the chunk's longest
   // row (~120 cycles per sample pair-step), plus shared-memory traffic per sample
   const int64_t dmma = (int64_t)(CH_ROWS / 16) * (dR / 8) * (dL / 4) + (int64_t)(dL / 16) * (dR / 8) * (CH_ROWS / 4);
-  plan_kernel<<<1, PLAN_T, 0, st>>>(sk->seg, ul, counts_dev ? counts_dev + 1 : nullptr, grid, 8 * dmma + 600,
+  KS_TRY_CUDA(cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)(PLAN_SM_SEG * sizeof(int64_t))));
+  plan_kernel<<<1, PLAN_T, PLAN_SM_SEG * sizeof(int64_t), st>>>(sk->seg, ul, counts_dev ? counts_dev + 1 : nullptr,
+                                     grid, 8 * dmma + 600,
                                      (int64_t)dR / 4, 120, dch.p,
                                      cpre.p, drange.p, drange.p + grid + 1);
   KS_CHECK_LAUNCH();
   if (eig_mode) {
     // rows pre-transformed into the preconditioner's eigenbasis: L VL and R VR
-    const size_t smL = sizeof(double) * ((size_t)dL * dL + (size_t)XF_ROWS * (dL + 1));
-    const size_t smR = sizeof(double) * ((size_t)dR * dR + (size_t)XF_ROWS * (dR + 1));
-    KS_TRY_CUDA(cudaFuncSetAttribute(pack_rows_xform_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)(smL > smR ? smL : smR)));
-    pack_rows_xform_kernel<<<ceil_div_u(ul, XF_ROWS), 256, smL, st>>>(sk->Lmat, sk->ldl, sk->lrow, ul,
-                                                                      counts_dev ? counts_dev + 1 : nullptr, dL,
-                                                                      dLp, VL, nullptr, nullptr, nullptr, Lpack.p);
+    xform_rows(st, dL, sk->Lmat, sk->ldl, sk->lrow, ul, counts_dev ? counts_dev + 1 : nullptr, dLp, VL, nullptr,
+               nullptr, nullptr, Lpack.p);
     KS_CHECK_LAUNCH();
-    pack_rows_xform_kernel<<<ceil_div_u(nnz, XF_ROWS), 256, smR, st>>>(sk->Rmat, sk->ldr, sk->rrow, nnz, counts_dev,
-                                                                       dR, dRp, VR, sk->v,
-                                                                       rhs_in_kernel ? b_at : nullptr, perm,
-                                                                       Rpack.p);
+    xform_rows(st, dR, sk->Rmat, sk->ldr, sk->rrow, nnz, counts_dev, dRp, VR, sk->v, rhs_in_kernel ? b_at : nullptr,
+               perm, Rpack.p);
   } else {
     pack_rows_kernel<<<ceil_div_u(ul * dLp, 256), 256, 0, st>>>(sk->Lmat, sk->ldl, sk->lrow, ul,
                                                                  counts_dev ? counts_dev + 1 : nullptr, dL, dLp,
