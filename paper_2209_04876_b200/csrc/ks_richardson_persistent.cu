@@ -863,6 +863,17 @@ __device__ __forceinline__ int64_t plan_piece(const int64_t* __restrict__ seg, i
                                               Chunk& ch) {
   ch.t_b = sb + k * CH_S;
   ch.t_e = min(se, ch.t_b + CH_S);
+  if (ch.t_b == sb && ch.t_e == se) {  // the whole group in one piece (the common case)
+    ch.u_b = ub;
+    ch.u_e = ue;
+    int64_t longest = 0, prev = seg[ub];
+    for (int64_t u = ub; u < ue; u++) {
+      const int64_t nx = seg[u + 1];
+      longest = max(longest, nx - prev);
+      prev = nx;
+    }
+    return wchunk + (se - sb) * wsamp + longest * wlong;
+  }
   // rows touched by the piece: seg[u] <= t < seg[u + 1]
   int64_t lo = ub, hi = ue - 1;
   while (lo < hi) {
