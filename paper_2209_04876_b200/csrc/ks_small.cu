@@ -232,9 +232,11 @@ struct MatPtrs {
   const double* p[8];
 };
 
+// column j of W / V at stride D + 8: the two pairs sharing a half-warp (consecutive players,
+// opposite parity) land 16 banks apart, and element offsets are compile-time immediates
 template <int D>
 __device__ __forceinline__ int jf_off(int j, int i) {
-  return j * D + ((i + ((j & 1) << 3)) & (D - 1));
+  return j * (D + 8) + i;
 }
 
 template <int D, bool SYM>
@@ -244,7 +246,7 @@ __global__ void __launch_bounds__(D / 2 * JF_G) jacobi_fixed_kernel(MatPtrs Ms, 
   constexpr int NP = D / 2, NT = NP * JF_G, E = D / JF_G;
   extern __shared__ double jf_sm[];
   double* W = jf_sm;
-  double* V = jf_sm + D * D;
+  double* V = jf_sm + D * (D + 8);
   __shared__ int s_rot;
   __shared__ int s_order[D];
   __shared__ double s_norm[D];
@@ -274,11 +276,17 @@ __global__ void __launch_bounds__(D / 2 * JF_G) jacobi_fixed_kernel(MatPtrs Ms, 
       const int p = player(group), q = player(D - 1 - group);
       long long jt0 = 0;
       if (JSTAMP) jt0 = clock64();
-      double x[E], y[E];
+      double x[E], y[E], u[E], v[E];
 #pragma unroll
       for (int k = 0; k < E; k++) {
         x[k] = W[jf_off<D>(p, lg + k * JF_G)];
         y[k] = W[jf_off<D>(q, lg + k * JF_G)];
+      }
+      // V columns do not depend on the rotation: their loads overlap the dot products
+#pragma unroll
+      for (int k = 0; k < E; k++) {
+        u[k] = V[jf_off<D>(p, lg + k * JF_G)];
+        v[k] = V[jf_off<D>(q, lg + k * JF_G)];
       }
       double a = 0.0, b = 0.0, c = 0.0;
 #pragma unroll
@@ -295,18 +303,22 @@ __global__ void __launch_bounds__(D / 2 * JF_G) jacobi_fixed_kernel(MatPtrs Ms, 
       }
       if (JSTAMP) { const long long now = clock64(); js0 += now - jt0; jt0 = now; }
       if (c != 0.0 && a != 0.0 && b != 0.0 && c * c > tol * tol * a * b) {
-        const double zeta = (b - a) * __drcp_rn(2.0 * c);
-        const double az = fabs(zeta);
-        const double tt = __drcp_rn(az + sqrt(fma(az, az, 1.0)));
-        const double t = zeta >= 0.0 ? tt : -tt;
+        // t ~ tan(theta) = sign(x) y / (|x| + sqrt(x^2 + y^2)), x = b - a, y = 2c, from hardware
+        // approximations refined by one Newton step each (t only steers the rotation; cs, and so
+        // cs^2 + sn^2 = 1, is computed to full precision)
+        const double x2 = b - a, y2 = 2.0 * c;
+        const double qq = fma(x2, x2, y2 * y2);
+        double rq;
+        asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(rq) : "d"(qq));
+        rq = rq * fma(-0.5 * qq * rq, rq, 1.5);
+        const double den = fma(qq, rq, fabs(x2));
+        double ri;
+        asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(ri) : "d"(den));
+        ri = ri * fma(-den, ri, 2.0);
+        const double tt = y2 * ri;
+        const double t = x2 >= 0.0 ? tt : -tt;
         const double cs = rsqrt(fma(t, t, 1.0));
         const double sn = cs * t;
-        double u[E], v[E];
-#pragma unroll
-        for (int k = 0; k < E; k++) {
-          u[k] = V[jf_off<D>(p, lg + k * JF_G)];
-          v[k] = V[jf_off<D>(q, lg + k * JF_G)];
-        }
 #pragma unroll
         for (int k = 0; k < E; k++) {
           W[jf_off<D>(p, lg + k * JF_G)] = cs * x[k] - sn * y[k];
@@ -497,7 +509,7 @@ int qr_r(cudaStream_t st, const double* A, int64_t n, int d, double* R) {
 template <int D, bool SYM>
 static void launch_jacobi_fixed(cudaStream_t st, const MatPtrs& Ms, const double* M, double* sigma, double* V,
                                 int batch) {
-  const int smem = 2 * D * D * (int)sizeof(double);
+  const int smem = 2 * D * (D + 8) * (int)sizeof(double);
   cudaFuncSetAttribute(jacobi_fixed_kernel<D, SYM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   jacobi_fixed_kernel<D, SYM><<<batch, D / 2 * JF_G, smem, st>>>(Ms, M, sigma, V);
 }
