@@ -251,8 +251,9 @@ def run_ours(args):
                             "solution download; only the sampled entries of b cross PCIe; median of steps",
                     "full_call_with_loss_s": e2e_full},
             "full_call_device_s": statistics.median(full_times),
-            "roofline": {"bound": "tensor", "kernel": "richardson_persistent_kernel (sketched normal operator + "
-                                                        "preconditioner, all iterations, FP64 DMMA)",
+            "roofline": {"bound": "tensor", "kernel": "richardson_persistent_kernel (eigenbasis sketched normal "
+                                                        "operator, diagonal preconditioner, all iterations; FP64 "
+                                                        "DMMA) with its plan/packing launches",
                          "achieved": live_tf, "peak": peak, "unit": "TFLOP/s",
                          "frac": live_tf / peak, "traffic": traffic_bytes(),
                          "measured": "CUDA events on the solve stream around the Richardson stage of every "
@@ -305,10 +306,20 @@ def stage_timings(K, facs, b, cfg, tr, n, d):
     it = ctypes.c_int32(0)
     hl = ctypes.c_int32(0)
 
+    rhs2 = torch.empty(view.dL, view.dR, dtype=torch.float64, device="cuda")
+    fused = li.get("wL") is not None
+
     def loop():
-        rc = L.load().ks_richardson_sketched(ctypes.byref(view.struct), D.p(li["VL"]), D.p(li["VR"]), D.p(li["dinv"]),
-                                             D.p(li["rhs"]), li["lam"], li["damping"], li["max_iters"], li["tol"],
-                                             D.p(x), D.p(hist), ctypes.byref(it), ctypes.byref(hl), D.stream())
+        if fused:  # the product path: right-hand side + eigenbasis loop in one persistent launch
+            rc = L.load().ks_richardson_fused(ctypes.byref(view.struct), D.p(view.perm_arg()), D.p(li["b_at"]),
+                                              D.p(li["VL"]), D.p(li["wL"]), D.p(li["VR"]), D.p(li["wR"]), None,
+                                              li["lam"], li["damping"], li["max_iters"], li["tol"], D.p(x), D.p(hist),
+                                              D.p(rhs2), ctypes.byref(it), ctypes.byref(hl), D.stream())
+        else:
+            rc = L.load().ks_richardson_sketched(ctypes.byref(view.struct), D.p(li["VL"]), D.p(li["VR"]),
+                                                 D.p(li["dinv"]), D.p(li["rhs"]), li["lam"], li["damping"],
+                                                 li["max_iters"], li["tol"], D.p(x), D.p(hist), ctypes.byref(it),
+                                                 ctypes.byref(hl), D.stream())
         assert rc == 0, rc
 
     us_loop = _timed(loop, 5)
@@ -326,7 +337,9 @@ def stage_timings(K, facs, b, cfg, tr, n, d):
                               "tflops": flops_iter * iters / (us_loop * 1e-6) / 1e12,
                               "frac_fp64": flops_iter * iters / (us_loop * 1e-6) / 1e12 / peak,
                               "phase_cycles_per_iter": phases,
-                              "note": "one persistent cooperative launch: sketch packing + all iterations"}
+                              "note": "ks_richardson_fused: device work plan, eigenbasis packing of the sampled "
+                                      "rows, then one persistent cooperative launch (right-hand-side pass + all "
+                                      "iterations)"}
     U1, U2 = facs
     T = torch.empty(d, d, dtype=torch.float64, device="cuda")
 
