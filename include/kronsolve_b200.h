@@ -274,7 +274,14 @@ int ks_richardson_fused_async(const ks_sketch_view* sk, const int64_t* counts_de
                               const double* b_at, const double* VL, const double* wL, const double* VR,
                               const double* wR, const double* dinv, double lam, double damping, int32_t max_iters,
                               double residual_tol, double* x, double* hist, double* rhs_out, int32_t* state_dev,
-                              void* stream);
+                              const void* plan_ws, void* stream);
+
+/* The persistent loop's work plan (chunks of <= 16 left rows / <= 64 samples, balanced CTA
+ * ranges) built ahead of time, e.g. while the eigensolves still run: plan_ws (device,
+ * ks_richardson_plan_bytes(u_left capacity, nnz capacity) bytes) is then passed to
+ * ks_richardson_fused_async.  Asynchronous. */
+int64_t ks_richardson_plan_bytes(int64_t u_left_cap, int64_t nnz_cap);
+int ks_richardson_plan_async(const ks_sketch_view* sk, const int64_t* counts_dev, void* plan_ws, void* stream);
 
 /* Profiling aid: per-CTA %globaltimer stamps (ns) of iteration 5 of the last persistent
  * Richardson run, 9 per CTA (phase boundaries and grid-barrier exits). */

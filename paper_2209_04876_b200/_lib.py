@@ -50,7 +50,9 @@ _SIGS = {
     "ks_svd_small_batched": ([_p, _i32, _i32, _p, _p, _p], ctypes.c_int),
     "ks_debug_jl_projection_stamps": ([_p], ctypes.c_int),
     "ks_richardson_fused_async": ([POINTER(SketchView), _p, _p, _p, _p, _p, _p, _p, _p, _d, _d, _i32, _d, _p, _p,
-                                   _p, _p, _p], ctypes.c_int),
+                                   _p, _p, _p, _p], ctypes.c_int),
+    "ks_richardson_plan_bytes": ([_i64, _i64], ctypes.c_int64),
+    "ks_richardson_plan_async": ([POINTER(SketchView), _p, _p, _p], ctypes.c_int),
     "ks_gather_count": ([_p, _p, _p, _i64, _p, _p], ctypes.c_int),
     "ks_richardson_fused": ([POINTER(SketchView), _p, _p, _p, _p, _p, _p, _p, _d, _d, _i32, _d, _p, _p, _p,
                              POINTER(c_int32), POINTER(c_int32), _p], ctypes.c_int),

@@ -23,7 +23,9 @@ int richardson_persistent(cudaStream_t st, const ks_sketch_view* sk, const doubl
                           const double* dinv, const double* wL, const double* wR, double* rhs, bool rhs_in_kernel,
                           const double* b_at, const int64_t* perm, double lam, double damping, int max_iters,
                           double residual_tol, double* x, double* hist, int* iters, int* hist_len, int* status,
-                          const int64_t* counts_dev, int* state_dev, bool eig_mode);
+                          const int64_t* counts_dev, int* state_dev, bool eig_mode, const void* plan_ws);
+int64_t richardson_plan_bytes(int64_t ul_cap, int64_t nnz_cap);
+int richardson_plan(cudaStream_t st, const ks_sketch_view* sk, const int64_t* counts_dev, void* plan_ws);
 }
 
 namespace {
@@ -206,7 +208,7 @@ extern "C" int ks_richardson_sketched(const ks_sketch_view* sk, const double* VL
     int it = 0, hl = 0;
     int rc = ks::richardson_persistent(st, sk, VL, VR, dinv, nullptr, nullptr, const_cast<double*>(rhs), false,
                                        nullptr, nullptr, lam, damping, max_iters, residual_tol, x, hist, &it, &hl,
-                                       &status, nullptr, nullptr, false);
+                                       &status, nullptr, nullptr, false, nullptr);
     if (rc) return rc;
     *iters = it;
     *hist_len = hl;
@@ -269,7 +271,7 @@ extern "C" int ks_richardson_fused(const ks_sketch_view* sk, const int64_t* perm
   int status = 0, it = 0, hl = 0;
   int rc = ks::richardson_persistent(st, sk, VL, VR, dinv, wL, wR, rhs_out, true, b_at, perm, lam, damping,
                                      max_iters, residual_tol, x, hist, &it, &hl, &status, nullptr, nullptr,
-                                     !getenv("KS_NO_EIGBASIS"));
+                                     !getenv("KS_NO_EIGBASIS"), nullptr);
   if (rc) return rc;
   *iters = it;
   *hist_len = hl;
@@ -284,11 +286,21 @@ extern "C" int ks_richardson_fused(const ks_sketch_view* sk, const int64_t* perm
 // real counts are read on the device from counts_dev ([nnz, u_left]); the loop state
 // [status (1 converged, 2 diverged), iterations, history length] goes to state_dev.  No host
 // synchronisation.
+extern "C" int64_t ks_richardson_plan_bytes(int64_t u_left_cap, int64_t nnz_cap) {
+  return ks::richardson_plan_bytes(u_left_cap, nnz_cap);
+}
+
+extern "C" int ks_richardson_plan_async(const ks_sketch_view* sk, const int64_t* counts_dev, void* plan_ws,
+                                        void* stream) {
+  KS_REQUIRE(plan_ws && sk->nnz > 0, KS_EINVAL, "need a plan workspace and a nonempty sketch");
+  return ks::richardson_plan((cudaStream_t)stream, sk, counts_dev, plan_ws);
+}
+
 extern "C" int ks_richardson_fused_async(const ks_sketch_view* sk, const int64_t* counts_dev, const int64_t* perm,
                                          const double* b_at, const double* VL, const double* wL, const double* VR,
                                          const double* wR, const double* dinv, double lam, double damping,
                                          int32_t max_iters, double residual_tol, double* x, double* hist,
-                                         double* rhs_out, int32_t* state_dev, void* stream) {
+                                         double* rhs_out, int32_t* state_dev, const void* plan_ws, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   const int dL = sk->dL, dR = sk->dR;
   KS_REQUIRE(sk->nnz > 0 && ks::persistent_supported(dL, dR) && max_iters <= 1024, KS_ESIZE,
@@ -298,5 +310,5 @@ extern "C" int ks_richardson_fused_async(const ks_sketch_view* sk, const int64_t
   int status = 0, it = 0, hl = 0;
   return ks::richardson_persistent(st, sk, VL, VR, dinv, wL, wR, rhs_out, true, b_at, perm, lam, damping, max_iters,
                                    residual_tol, x, hist, &it, &hl, &status, counts_dev, state_dev,
-                                   !getenv("KS_NO_EIGBASIS"));
+                                   !getenv("KS_NO_EIGBASIS"), plan_ws);
 }

@@ -755,7 +755,7 @@ __global__ void pack_rows_kernel(const double* __restrict__ src, int64_t ld, con
 // chains interleaved), rows and V staged in shared memory with asynchronous copies.
 constexpr int XF_ROWS = 64;
 template <int D>
-__global__ void __launch_bounds__(256) pack_rows_xform_kernel(
+__device__ __forceinline__ void pack_rows_xform_body(
     const double* __restrict__ src, int64_t ld, const int64_t* __restrict__ rows, int64_t n_host,
     const int64_t* __restrict__ n_dev, int dp, const double* __restrict__ V, const double* __restrict__ extra,
     const double* __restrict__ b, const int64_t* __restrict__ perm, double* __restrict__ dst) {
@@ -822,6 +822,47 @@ __global__ void __launch_bounds__(256) pack_rows_xform_kernel(
     else if (c == D + 1 && b) v = __dmul_rn(extra[i], b[perm ? perm[i] : i]);
     dst[i * dp + c] = v;
   }
+}
+
+template <int D>
+__global__ void __launch_bounds__(256) pack_rows_xform_kernel(
+    const double* __restrict__ src, int64_t ld, const int64_t* __restrict__ rows, int64_t n_host,
+    const int64_t* __restrict__ n_dev, int dp, const double* __restrict__ V, const double* __restrict__ extra,
+    const double* __restrict__ b, const int64_t* __restrict__ perm, double* __restrict__ dst) {
+  pack_rows_xform_body<D>(src, ld, rows, n_host, n_dev, dp, V, extra, b, perm, dst);
+}
+
+struct XfJob {
+  const double* src;
+  int64_t ld;
+  const int64_t* rows;
+  int64_t n_host;
+  const int64_t* n_dev;
+  int dp;
+  const double* V;
+  const double* extra;
+  const double* b;
+  const int64_t* perm;
+  double* dst;
+};
+
+template <int D>
+__global__ void __launch_bounds__(256) pack_rows_xform_pair_kernel(XfJob j0, XfJob j1) {
+  const XfJob& j = blockIdx.y == 0 ? j0 : j1;
+  pack_rows_xform_body<D>(j.src, j.ld, j.rows, j.n_host, j.n_dev, j.dp, j.V, j.extra, j.b, j.perm, j.dst);
+}
+
+static void xform_pair(cudaStream_t st, int d, const XfJob& j0, const XfJob& j1) {
+  const int64_t nmax = j0.n_host > j1.n_host ? j0.n_host : j1.n_host;
+  const dim3 grid(ceil_div_u(nmax, XF_ROWS), 2);
+  auto go = [&](auto kern, int D) {
+    const int smem = (int)sizeof(double) * (XF_ROWS * (D + 4) + D * (D + 4));
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    kern<<<grid, 256, smem, st>>>(j0, j1);
+  };
+  if (d == 16) go(pack_rows_xform_pair_kernel<16>, 16);
+  else if (d == 32) go(pack_rows_xform_pair_kernel<32>, 32);
+  else go(pack_rows_xform_pair_kernel<64>, 64);
 }
 
 template <int D>
@@ -1002,6 +1043,36 @@ int launch(cudaStream_t st, PArgs& a, int grid) {
 
 namespace ks {
 
+static int64_t plan_cap(int64_t ul, int64_t nnz) { return (ul + CH_ROWS - 1) / CH_ROWS + nnz / CH_S + 2; }
+static size_t plan_range_offset(int64_t cap) { return (size_t)cap * (sizeof(Chunk) + sizeof(int64_t)); }
+
+static int launch_plan(cudaStream_t st, const ks_sketch_view* sk, int64_t ul, const int64_t* counts_dev, int dL,
+                       int dR, int grid, Chunk* chunks, int64_t* cpre, int64_t* range) {
+  // estimated chunk cost (SM cycles): the Y and G DMMA tiles are fixed per chunk (the FP64 tensor
+  // pipe issues one m16n8k4 per ~8 cycles per SM), the sample phase follows the chunk's longest
+  // row (~120 cycles per sample pair-step), plus shared-memory traffic per sample
+  const int64_t dmma = (int64_t)(CH_ROWS / 16) * (dR / 8) * (dL / 4) + (int64_t)(dL / 16) * (dR / 8) * (CH_ROWS / 4);
+  KS_TRY_CUDA(cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)(PLAN_SM_SEG * sizeof(int64_t))));
+  plan_kernel<<<1, PLAN_T, PLAN_SM_SEG * sizeof(int64_t), st>>>(sk->seg, ul, counts_dev ? counts_dev + 1 : nullptr,
+                                                                grid, 8 * dmma + 600, (int64_t)dR / 4, 120, chunks,
+                                                                cpre, range, range + grid + 1);
+  KS_CHECK_LAUNCH();
+  return KS_OK;
+}
+
+int64_t richardson_plan_bytes(int64_t ul_cap, int64_t nnz_cap) {
+  const int64_t cap = plan_cap(ul_cap, nnz_cap);
+  return (int64_t)plan_range_offset(cap) + (int64_t)(num_sms() + 2) * (int64_t)sizeof(int64_t);
+}
+
+int richardson_plan(cudaStream_t st, const ks_sketch_view* sk, const int64_t* counts_dev, void* plan_ws) {
+  const int64_t cap = plan_cap(sk->u_left, sk->nnz);
+  char* base = (char*)plan_ws;
+  return launch_plan(st, sk, sk->u_left, counts_dev, sk->dL, sk->dR, num_sms(), (Chunk*)base,
+                     (int64_t*)(base + (size_t)cap * sizeof(Chunk)), (int64_t*)(base + plan_range_offset(cap)));
+}
+
 bool persistent_supported(int dL, int dR) {
   auto ok = [](int d) { return d == 16 || d == 32 || d == 64; };
   return ok(dL) && ok(dR);
@@ -1013,7 +1084,7 @@ int richardson_persistent(cudaStream_t st, const ks_sketch_view* sk, const doubl
                           const double* dinv, const double* wL, const double* wR, double* rhs, bool rhs_in_kernel,
                           const double* b_at, const int64_t* perm, double lam, double damping, int max_iters,
                           double residual_tol, double* x, double* hist, int* iters, int* hist_len, int* status,
-                          const int64_t* counts_dev, int* state_dev, bool eig_mode) {
+                          const int64_t* counts_dev, int* state_dev, bool eig_mode, const void* plan_ws) {
   // counts_dev ([nnz, u_left] on the device): sk->nnz / sk->u_left are capacities and nothing
   // here reads the counts on the host; state_dev: the loop state stays on the device (no sync)
   const int dL = sk->dL, dR = sk->dR;
@@ -1021,37 +1092,42 @@ int richardson_persistent(cudaStream_t st, const ks_sketch_view* sk, const doubl
   const int dLp = dL + PAD, dRp = dR + PAD;
   const int64_t nnz = sk->nnz, ul = sk->u_left;
   const int grid = num_sms();
-  const int64_t cap = (ul + CH_ROWS - 1) / CH_ROWS + nnz / CH_S + 2;  // >= chunk count
+  const int64_t cap = plan_cap(ul, nnz);  // >= chunk count
   Scratch<double> Lpack(ul * dLp + 2, st), Rpack(nnz * dRp + 2, st), part((int64_t)grid * dL * dR, st);
   Scratch<double> R((int64_t)dL * dR, st), T((int64_t)dL * dR, st), stepb((int64_t)dL * dR, st),
       rowsq(dL > grid ? dL : grid, st), rhs_e(eig_mode ? (int64_t)dL * dR : 0, st);
   Scratch<double> VRt((int64_t)dR * dR, st);
-  Scratch<Chunk> dch(cap, st);
-  Scratch<int64_t> cpre(cap, st), drange(grid + 2, st);
+  Scratch<Chunk> dch(plan_ws ? 0 : cap, st);
+  Scratch<int64_t> cpre(plan_ws ? 0 : cap, st), drange(plan_ws ? 0 : grid + 2, st);
+  Chunk* chunks_p = plan_ws ? (Chunk*)plan_ws : dch.p;
+  int64_t* range_p = plan_ws ? (int64_t*)((char*)plan_ws + plan_range_offset(cap)) : drange.p;
   Scratch<int> state_s(state_dev ? 0 : 4, st);
   int* statep = state_dev ? state_dev : state_s.p;
   KS_REQUIRE(eig_mode <= rhs_in_kernel, KS_EINVAL, "the eigenbasis loop builds its own right-hand side");
-  KS_REQUIRE(Lpack.p && Rpack.p && part.p && R.p && T.p && stepb.p && rowsq.p && VRt.p && dch.p && drange.p &&
-                 cpre.p && statep && (!eig_mode || rhs_e.p),
+  KS_REQUIRE(Lpack.p && Rpack.p && part.p && R.p && T.p && stepb.p && rowsq.p && VRt.p && chunks_p && range_p &&
+                 (plan_ws || cpre.p) && statep && (!eig_mode || rhs_e.p),
              KS_ECUDA, "scratch allocation failed");
   // estimated chunk cost (SM cycles): the Y and G DMMA tiles are fixed per chunk (the FP64 tensor
   // pipe issues one m16n8k4 per ~8 cycles per SM), the sample phase follows the chunk's longest
   // row (~120 cycles per sample pair-step), plus shared-memory traffic per sample
   const int64_t dmma = (int64_t)(CH_ROWS / 16) * (dR / 8) * (dL / 4) + (int64_t)(dL / 16) * (dR / 8) * (CH_ROWS / 4);
-  KS_TRY_CUDA(cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)(PLAN_SM_SEG * sizeof(int64_t))));
-  plan_kernel<<<1, PLAN_T, PLAN_SM_SEG * sizeof(int64_t), st>>>(sk->seg, ul, counts_dev ? counts_dev + 1 : nullptr,
-                                     grid, 8 * dmma + 600,
-                                     (int64_t)dR / 4, 120, dch.p,
-                                     cpre.p, drange.p, drange.p + grid + 1);
-  KS_CHECK_LAUNCH();
+  if (!plan_ws) {
+    int rc0 = launch_plan(st, sk, ul, counts_dev, dL, dR, grid, dch.p, cpre.p, drange.p);
+    if (rc0) return rc0;
+  }
   if (eig_mode) {
     // rows pre-transformed into the preconditioner's eigenbasis: L VL and R VR
-    xform_rows(st, dL, sk->Lmat, sk->ldl, sk->lrow, ul, counts_dev ? counts_dev + 1 : nullptr, dLp, VL, nullptr,
-               nullptr, nullptr, Lpack.p);
-    KS_CHECK_LAUNCH();
-    xform_rows(st, dR, sk->Rmat, sk->ldr, sk->rrow, nnz, counts_dev, dRp, VR, sk->v, rhs_in_kernel ? b_at : nullptr,
-               perm, Rpack.p);
+    XfJob jl{sk->Lmat, sk->ldl, sk->lrow, ul, counts_dev ? counts_dev + 1 : nullptr, dLp, VL, nullptr, nullptr,
+             nullptr, Lpack.p};
+    XfJob jr{sk->Rmat, sk->ldr, sk->rrow, nnz, counts_dev, dRp, VR, sk->v, rhs_in_kernel ? b_at : nullptr, perm,
+             Rpack.p};
+    if (dL == dR) {
+      xform_pair(st, dL, jl, jr);  // one launch for both sides
+    } else {
+      xform_rows(st, dL, jl.src, jl.ld, jl.rows, jl.n_host, jl.n_dev, jl.dp, jl.V, jl.extra, jl.b, jl.perm, jl.dst);
+      KS_CHECK_LAUNCH();
+      xform_rows(st, dR, jr.src, jr.ld, jr.rows, jr.n_host, jr.n_dev, jr.dp, jr.V, jr.extra, jr.b, jr.perm, jr.dst);
+    }
   } else {
     pack_rows_kernel<<<ceil_div_u(ul * dLp, 256), 256, 0, st>>>(sk->Lmat, sk->ldl, sk->lrow, ul,
                                                                  counts_dev ? counts_dev + 1 : nullptr, dL, dLp,
@@ -1065,7 +1141,7 @@ int richardson_persistent(cudaStream_t st, const ks_sketch_view* sk, const doubl
   transpose_sq_kernel2<<<ceil_div_u((int64_t)dR * dR, 256), 256, 0, st>>>(VR, dR, VRt.p);
   KS_CHECK_LAUNCH();
   PArgs a{};
-  a.Lpack = Lpack.p; a.Rpack = Rpack.p; a.seg = sk->seg; a.chunks = dch.p; a.range = drange.p;
+  a.Lpack = Lpack.p; a.Rpack = Rpack.p; a.seg = sk->seg; a.chunks = chunks_p; a.range = range_p;
   a.VL = VL; a.VR = VR; a.VRt = VRt.p; a.dinv = dinv; a.wL = wL; a.wR = wR; a.rhs = rhs;
   a.rhs_in_kernel = rhs_in_kernel ? 1 : 0;
   a.eig_mode = eig_mode ? 1 : 0;

@@ -536,15 +536,25 @@ def _solve_graph_body(facs, b, config: RegressionConfig, s: int):
     seeds = _spawned_seeds(config.seed, 5)
     eps_jl = 4.0 * math.log1p(config.eps / 4.0) / 2
     d0, d1 = int(facs[0].shape[1]), int(facs[1].shape[1])
-    gts = [_gram_dev(a) for a in facs]
+    main = torch.cuda.current_stream()
+    gside = _side_stream(8)
+    gside.wait_stream(main)
+    g0 = _gram_dev(facs[0])
+    with torch.cuda.stream(gside):  # the two Grams concurrently
+        g1 = _gram_dev(facs[1])
+    main.wait_stream(gside)
+    gts = [g0, g1]
     grams_h = _factor_grams_async(gts)
     _, _, _, _, _, g2 = _jl_and_sampling(facs, facs, gts, eps_jl, config, True, seeds, s)
     sd_idx, sd_val, seg, lrow, rrow, cdev = g2
     b_at = D.empty(s)
     _lib.call("ks_gather_count", D.p(b), D.p(sd_idx), D.p(cdev), s, D.p(b_at), D.stream())
-    (VL, wL), (VR, wR) = _join_grams(grams_h)
     struct = _lib.SketchView(facs[0].data_ptr(), d0, d0, facs[1].data_ptr(), d1, d1, s, s, seg.data_ptr(),
                              lrow.data_ptr(), rrow.data_ptr(), sd_val.data_ptr())
+    # the loop's work plan needs only the sketch: built while the eigensolves still run
+    plan_ws = torch.empty(int(_lib.load().ks_richardson_plan_bytes(s, s)), dtype=torch.uint8, device=D.dev())
+    _lib.call("ks_richardson_plan_async", ctypes.byref(struct), D.p(cdev), D.p(plan_ws), D.stream())
+    (VL, wL), (VR, wR) = _join_grams(grams_h)
     max_iters = config.effective_max_iters
     x = D.empty(d0, d1)
     hist = D.zeros(max(1, max_iters))
@@ -556,10 +566,10 @@ def _solve_graph_body(facs, b, config: RegressionConfig, s: int):
     ev0.record()
     _lib.call("ks_richardson_fused_async", ctypes.byref(struct), D.p(cdev), None, D.p(b_at), D.p(VL), D.p(wL),
               D.p(VR), D.p(wR), None, float(config.lam), float(config.effective_damping), int(max_iters),
-              float(config.residual_tol), D.p(x), D.p(hist), D.p(rhs), D.p(state), D.stream())
+              float(config.residual_tol), D.p(x), D.p(hist), D.p(rhs), D.p(state), D.p(plan_ws), D.stream())
     ev1.record()
     return dict(x=x, hist=hist, state=state, loop_events=(ev0, ev1),
-                keep=(gts, b_at, sd_idx, sd_val, seg, lrow, rrow, cdev, rhs))
+                keep=(gts, b_at, sd_idx, sd_val, seg, lrow, rrow, cdev, rhs, plan_ws))
 
 
 def _fast_solve_graph(facs, b, config: RegressionConfig):

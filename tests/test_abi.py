@@ -14,7 +14,7 @@ LIB = ROOT / "paper_2209_04876_b200" / "libkronsolve_b200.so"
 
 def declared():
     text = HEADER.read_text()
-    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(ks_[a-z0-9_]+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|const char\*)\s+(ks_[a-z0-9_]+)\s*\(", text, re.M)))
 
 
 def test_header_declares_entry_points():
