@@ -1048,14 +1048,15 @@ static size_t plan_range_offset(int64_t cap) { return (size_t)cap * (sizeof(Chun
 
 static int launch_plan(cudaStream_t st, const ks_sketch_view* sk, int64_t ul, const int64_t* counts_dev, int dL,
                        int dR, int grid, Chunk* chunks, int64_t* cpre, int64_t* range) {
-  // estimated chunk cost (SM cycles): the Y and G DMMA tiles are fixed per chunk (the FP64 tensor
-  // pipe issues one m16n8k4 per ~8 cycles per SM), the sample phase follows the chunk's longest
-  // row (~120 cycles per sample pair-step), plus shared-memory traffic per sample
+  // estimated chunk cost (SM cycles), fitted to measured per-CTA apply times at c3
+  // (tools/fit_plan_costs.py: rms error 0.23 us): ~13.3 cycles per DMMA tile-step of the Y and G
+  // GEMMs (fixed per chunk), ~139 cycles per sample of the chunk's longest row (the rows' sample
+  // loops run in parallel), ~4 cycles per sample of shared-memory traffic
   const int64_t dmma = (int64_t)(CH_ROWS / 16) * (dR / 8) * (dL / 4) + (int64_t)(dL / 16) * (dR / 8) * (CH_ROWS / 4);
   KS_TRY_CUDA(cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)(PLAN_SM_SEG * sizeof(int64_t))));
   plan_kernel<<<1, PLAN_T, PLAN_SM_SEG * sizeof(int64_t), st>>>(sk->seg, ul, counts_dev ? counts_dev + 1 : nullptr,
-                                                                grid, 8 * dmma + 600, (int64_t)dR / 4, 120, chunks,
+                                                                grid, (int64_t)(13.3 * dmma), (int64_t)dR / 16, 139, chunks,
                                                                 cpre, range, range + grid + 1);
   KS_CHECK_LAUNCH();
   return KS_OK;
@@ -1107,9 +1108,10 @@ int richardson_persistent(cudaStream_t st, const ks_sketch_view* sk, const doubl
   KS_REQUIRE(Lpack.p && Rpack.p && part.p && R.p && T.p && stepb.p && rowsq.p && VRt.p && chunks_p && range_p &&
                  (plan_ws || cpre.p) && statep && (!eig_mode || rhs_e.p),
              KS_ECUDA, "scratch allocation failed");
-  // estimated chunk cost (SM cycles): the Y and G DMMA tiles are fixed per chunk (the FP64 tensor
-  // pipe issues one m16n8k4 per ~8 cycles per SM), the sample phase follows the chunk's longest
-  // row (~120 cycles per sample pair-step), plus shared-memory traffic per sample
+  // estimated chunk cost (SM cycles), fitted to measured per-CTA apply times at c3
+  // (tools/fit_plan_costs.py: rms error 0.23 us): ~13.3 cycles per DMMA tile-step of the Y and G
+  // GEMMs (fixed per chunk), ~139 cycles per sample of the chunk's longest row (the rows' sample
+  // loops run in parallel), ~4 cycles per sample of shared-memory traffic
   const int64_t dmma = (int64_t)(CH_ROWS / 16) * (dR / 8) * (dL / 4) + (int64_t)(dL / 16) * (dR / 8) * (CH_ROWS / 4);
   if (!plan_ws) {
     int rc0 = launch_plan(st, sk, ul, counts_dev, dL, dR, grid, dch.p, cpre.p, drange.p);
