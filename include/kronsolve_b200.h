@@ -310,6 +310,75 @@ int ks_debug_richardson_apply_split(int32_t iters, double* out4);
 int ks_kron_precond_apply(const double* VL, const double* VR, int32_t dL, int32_t dR,
                           const double* dinv, const double* r, double* y, void* stream);
 
+
+/* ---------------------------------------------------------------- Tucker factor-matrix updates
+ * (reference tucker.py).  The "other" factors of a mode-n update are
+ * M (1..4) matrices A_m (I_m x R_m, row-major); leftover Kronecker vectors (length
+ * R_rest = prod R_m <= 4096) are indexed C-order by (r_0, ..., r_{M-1}).  V_m / G_m / E_m are the
+ * eigenvectors (R_m x R_m, column j = vector j), Gram matrices and eigenvalues of each A_m^T A_m
+ * (FactorGram, solvers.py:126-150).  gn = G (R_n x R_rest, core unfolding), gnp = G^+ (R_rest x R_n),
+ * R_n <= 64. */
+
+/* PCG64 draws of many streams: out[m*rows*s + row*s + t] = random() draw (m*s + t) of stream row;
+ * states holds 4 words per stream (state hi, state lo, inc hi, inc lo).  The per-row sampler
+ * streams of fast_factor_matrix_update (tucker.py:361-369). */
+int ks_pcg64_random_streams(const uint64_t* states, int64_t rows, int32_t nf, int64_t s, double* out,
+                            void* stream);
+
+/* Product-sampler draws of `rows` independent sketches of s samples each (leverage.py:196-231 per
+ * row): idx ((rows*s) x (M+1), column 0 = row, then clip(upper_bound(cdf_m, u)) per factor) and
+ * w = 1/sqrt(prod_m prob_m[idx_m] * s), from uniforms laid out as ks_pcg64_random_streams. */
+int ks_factor_draws_rows(int32_t M, const double* const* cdf, const double* const* prob, const int64_t* n,
+                         const double* u, int64_t rows, int64_t s, int64_t* idx, double* w, void* stream);
+
+/* build_factor_workspace (tucker.py:217-280) minus the R_n x R_n inverse: power iteration
+ * (_power_iteration, :283-313, start vector v0 = default_rng(0).standard_normal(R_rest)) on the
+ * constrained Gram, wout[0] = w = (1 + 12/eps) * estimate * 1.05, wout[1] = estimate,
+ * bdiag = pseudo_reciprocal(kron(E) + w), right = lam (G^T)^+ - w G and
+ * cm = I + right (V diag(bdiag) V^T) G^+ (the Woodbury core matrix; its inverse = correction_mid,
+ * via ks_inverse_small).  flags[0] |= 1 if a power iterate is non-finite. */
+int ks_factor_workspace(int32_t M, const int32_t* R, const double* const* V, const double* const* G,
+                        const double* const* E, int32_t Rn, const double* gn, const double* gnp,
+                        double lam, double eps, const double* v0, double* wout, double* bdiag,
+                        double* right, double* cm, int32_t* flags, void* stream);
+
+/* FactorUpdateWorkspace.apply (which = 0), .apply_base (1), .apply_penalized_normal (2) of one
+ * vector z (tucker.py:185-214). */
+int ks_factor_ws_apply(int32_t M, const int32_t* R, const double* const* V, const double* const* G,
+                       int32_t Rn, const double* gn, const double* gnp, const double* mid,
+                       const double* right, const double* bdiag, const double* wdev, double lam,
+                       const double* z, int32_t which, double* out, void* stream);
+
+/* Dynamic shared memory bytes of one factor-row solve (ks_factor_rows_richardson). */
+int64_t ks_factor_rows_smem(int32_t Rrest, int32_t Rright, int32_t Rn, int32_t max_iters, int32_t cap,
+                            int32_t ucap);
+
+/* The per-row loop of fast_factor_matrix_update (tucker.py:361-379), one CTA per row: the row's
+ * segment of the sparse diagonal (sd_idx = row * I_rest + flat index, sorted, or plain flat
+ * indices when shared != 0 and every row uses the same sketch), b_at gathered in place from the
+ * tensor x (stride xs_n of mode n, xs[m] of the other modes), rhs, damped Richardson with the
+ * Woodbury preconditioner and the exact stopping / divergence rules of richardson_solve
+ * (solvers.py:201-248), projection and out[row] = (G^T)^+ G^T (G^T)^+ z.  iters[row] = completed
+ * updates; flags[row] = 1 if the row diverged, 2 if it holds more than cap samples.  kr:
+ * nnz x prod_{m>=1} R_m scratch (required when M >= 3).  hist (rows x max_iters) optional. */
+int ks_factor_rows_richardson(int32_t M, const double* const* A, const int64_t* I, const int32_t* R,
+                              const double* const* V, int32_t Rn, const double* gn, const double* gnp,
+                              const double* mid, const double* right, const double* bdiag,
+                              const double* wdev, double lam, const int64_t* sd_idx, const double* sd_val,
+                              int64_t nnz, int32_t shared, int64_t rows, const double* x, int64_t xs_n,
+                              const int64_t* xs, double* kr, double damping, int32_t max_iters,
+                              double residual_tol, int32_t cap, double* out, int32_t* iters,
+                              int32_t* flags, double* hist, void* stream);
+
+/* Q (n x k) of np.linalg.qr(A) (reduced): Householder QR with LAPACK's dgeqrf / dorg2r
+ * conventions, one CTA.  initial_model (tucker.py:400-409). */
+int ks_qr_explicit(const double* A, int64_t n, int32_t k, double* Q, void* stream);
+
+/* X (d x n) = (V / sigma) U^T for a compact SVD (U: n x k, sigma: k, V: d x k): pseudo_inverse
+ * (tensor.py:110-115) and np.linalg.pinv of naive_factor_update (tucker.py:157). */
+int ks_pinv_compose(const double* U, int64_t n, const double* sigma, const double* V, int64_t d,
+                    int32_t k, double* X, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

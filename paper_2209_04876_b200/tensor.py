@@ -106,3 +106,97 @@ def devectorize(v, shape: Sequence[int]):
     if a.size != size:
         raise InvalidInputError(f"vector of length {a.size} cannot fill shape {tuple(shape)}")
     return a.reshape(tuple(shape))
+
+
+# ---------------------------------------------------------------------------
+# Unfoldings and mode products (tensor.py:110-183) -- used by the Tucker factor updates
+# ---------------------------------------------------------------------------
+
+def unfold(x, mode: int):
+    """Mode-``mode`` unfolding: (I_mode, prod of the other dims), other indices lexicographic
+    (tensor.py:133-143).  A layout copy on the device."""
+    host = not D.on_device(x)
+    t = as_tensor(x)
+    if not 0 <= mode < t.ndim:
+        raise InvalidInputError(f"mode {mode} out of range for order-{t.ndim} tensor")
+    return D.out(t.movedim(mode, 0).reshape(int(t.shape[mode]), -1).contiguous(), host)
+
+
+def fold(m, shape: Sequence[int], mode: int):
+    """Inverse of :func:`unfold` (tensor.py:146-156)."""
+    host = not D.on_device(m)
+    t = D.to_dev(m)
+    shape = tuple(int(s) for s in shape)
+    if not 0 <= mode < len(shape):
+        raise InvalidInputError(f"mode {mode} out of range for shape {shape}")
+    rest = shape[:mode] + shape[mode + 1:]
+    if tuple(t.shape) != (shape[mode], math.prod(rest)):
+        raise InvalidInputError(f"matrix of shape {tuple(t.shape)} does not unfold to {shape} at mode {mode}")
+    return D.out(t.reshape((shape[mode],) + rest).movedim(0, mode).contiguous(), host)
+
+
+def _mode_mul_dev(x: torch.Tensor, a: torch.Tensor, mode: int, transpose: bool = False) -> torch.Tensor:
+    """x x_mode A (A: J x I_mode) or, with ``transpose``, x x_mode A^T (A: I_mode x J), as one
+    batched strided ks_gemm over the fibres of ``mode``."""
+    shape = tuple(int(s) for s in x.shape)
+    k = shape[mode]
+    j = int(a.shape[1] if transpose else a.shape[0])
+    p = math.prod(shape[:mode])
+    q = math.prod(shape[mode + 1:])
+    out = D.empty(*(shape[:mode] + (j,) + shape[mode + 1:]))
+    if out.numel() == 0:
+        return out.zero_()
+    a_rs, a_cs = (1, j) if transpose else (k, 1)  # element (row i of the output fibre, k)
+    if q == 1:
+        # last mode: out (p x j) = x (p x k) . op(A)^T in one GEMM
+        _lib.call("ks_gemm", p, j, k, 1.0, D.p(x), k, 1, 0, D.p(a), a_cs, a_rs, 0, 0.0, D.p(out), j, 1, 0, 1,
+                  D.stream())
+    else:
+        _lib.call("ks_gemm", j, q, k, 1.0, D.p(a), a_rs, a_cs, 0, D.p(x), q, 1, k * q, 0.0, D.p(out), q, 1, j * q,
+                  p, D.stream())
+    return out
+
+
+def n_mode_product(x, a, mode: int):
+    """Multiply every mode-``mode`` fibre of ``x`` by ``a`` (tensor.py:159-172)."""
+    host = not D.on_device(x)
+    t = as_tensor(x)
+    m = as_matrix(a)
+    if not 0 <= mode < t.ndim:
+        raise InvalidInputError(f"mode {mode} out of range for order-{t.ndim} tensor")
+    if int(m.shape[1]) != int(t.shape[mode]):
+        raise InvalidInputError(f"matrix with {int(m.shape[1])} columns cannot multiply mode {mode} of size "
+                                f"{int(t.shape[mode])}")
+    return D.out(_mode_mul_dev(t.contiguous(), m, mode), host)
+
+
+def multi_mode_product(x, factors: Sequence):
+    """``x x_1 A1 x_2 ... x_N AN`` (tensor.py:175-183)."""
+    host = not D.on_device(x)
+    t = as_tensor(x)
+    if len(factors) != t.ndim:
+        raise InvalidInputError(f"need {t.ndim} factors for an order-{t.ndim} tensor, got {len(factors)}")
+    for mode, a in enumerate(factors):
+        m = as_matrix(a)
+        if int(m.shape[1]) != int(t.shape[mode]):
+            raise InvalidInputError(f"factor {mode} does not match mode size {int(t.shape[mode])}")
+        t = _mode_mul_dev(t, m, mode)
+    return D.out(t, host)
+
+
+def _pinv_dev(t: torch.Tensor, rank_tol: float) -> torch.Tensor:
+    """(V / sigma) U^T from the compact SVD, zero matrix at rank 0 (tensor.py:110-115)."""
+    n, d = int(t.shape[0]), int(t.shape[1])
+    u, s, v = _compact_svd_dev(t, rank_tol)
+    k = int(s.numel())
+    out = D.zeros(d, n)
+    if k:
+        _lib.call("ks_pinv_compose", D.p(u.contiguous()), n, D.p(s), D.p(v.contiguous()), d, k, D.p(out),
+                  D.stream())
+    return out
+
+
+def pseudo_inverse(a, rank_tol: float = DEFAULT_RANK_TOL):
+    """Moore-Penrose inverse via the compact SVD (tensor.py:110-115)."""
+    host = not D.on_device(a)
+    return D.out(_pinv_dev(as_matrix(a), rank_tol), host)
