@@ -320,10 +320,12 @@ int ks_kron_precond_apply(const double* VL, const double* VR, int32_t dL, int32_
  * R_n <= 64. */
 
 /* PCG64 draws of many streams: out[m*rows*s + row*s + t] = random() draw (m*s + t) of stream row;
- * states holds 4 words per stream (state hi, state lo, inc hi, inc lo).  The per-row sampler
- * streams of fast_factor_matrix_update (tucker.py:361-369). */
-int ks_pcg64_random_streams(const uint64_t* states, int64_t rows, int32_t nf, int64_t s, double* out,
-                            void* stream);
+ * states holds 4 words per stream: (state hi, state lo, inc hi, inc lo) when seeded == 0, or the
+ * pcg64_set_seed inputs (initstate hi, lo, initseq hi, lo) when seeded != 0 (the kernel then
+ * seeds the stream as PCG64(SeedSequence) does).  The per-row sampler streams of
+ * fast_factor_matrix_update (tucker.py:361-369). */
+int ks_pcg64_random_streams(const uint64_t* states, int32_t seeded, int64_t rows, int32_t nf, int64_t s,
+                            double* out, void* stream);
 
 /* Product-sampler draws of `rows` independent sketches of s samples each (leverage.py:196-231 per
  * row): idx ((rows*s) x (M+1), column 0 = row, then clip(upper_bound(cdf_m, u)) per factor) and
@@ -349,9 +351,10 @@ int ks_factor_ws_apply(int32_t M, const int32_t* R, const double* const* V, cons
                        const double* right, const double* bdiag, const double* wdev, double lam,
                        const double* z, int32_t which, double* out, void* stream);
 
-/* Dynamic shared memory bytes of one factor-row solve (ks_factor_rows_richardson). */
+/* Dynamic shared memory bytes of one factor-row solve (ks_factor_rows_richardson) with `threads`
+ * threads per row. */
 int64_t ks_factor_rows_smem(int32_t Rrest, int32_t Rright, int32_t Rn, int32_t max_iters, int32_t cap,
-                            int32_t ucap);
+                            int32_t ucap, int32_t threads);
 
 /* The per-row loop of fast_factor_matrix_update (tucker.py:361-379), one CTA per row: the row's
  * segment of the sparse diagonal (sd_idx = row * I_rest + flat index, sorted, or plain flat

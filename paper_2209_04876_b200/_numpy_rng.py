@@ -118,3 +118,63 @@ def ziggurat_tables():
     if ki.size != 256 or wi.size != 256 or fi.size != 256 or fi[0] != 1.0:
         raise RuntimeError("unexpected ziggurat table layout in libnpyrandom.a")
     return ki, wi, fi
+
+
+_SS_INIT_A, _SS_MULT_A, _SS_INIT_B, _SS_MULT_B = 0x43b0d7e5, 0x931e8875, 0x8b51f9dd, 0x58f38ded
+_SS_MIX_L, _SS_MIX_R = 0xca01f9dd, 0x4973f715
+
+
+def seedseq_children_seed_words(entropy: int, count: int) -> np.ndarray:
+    """PCG64 seeding words of ``np.random.SeedSequence(entropy).spawn(count)``, vectorised.
+
+    Row i holds (initstate hi, initstate lo, initseq hi, initseq lo) = the four uint64 words of
+    child i's ``generate_state(4, np.uint64)`` that ``PCG64(child)`` feeds to pcg64_set_seed; the
+    device finishes the seeding (ks_pcg64_random_streams, seeded = 1).  Restates NumPy's
+    published SeedSequence algorithm (entropy and spawn key as little-endian uint32 words, the
+    run entropy zero-padded to the pool size, hashmix / mix over a 4-word pool, then the
+    generate_state hash); checked bit for bit against NumPy in tests/test_rng_oracle.py."""
+    if entropy < 0 or count >= 2 ** 32:
+        raise ValueError("unsupported SeedSequence parameters")
+    run = []
+    e = int(entropy)
+    while e > 0:
+        run.append(e & 0xFFFFFFFF)
+        e >>= 32
+    run = run or [0]
+    run += [0] * max(0, 4 - len(run))
+    m32 = np.uint64(0xFFFFFFFF)
+    sh16 = np.uint64(16)
+    ent = np.zeros((count, len(run) + 1), dtype=np.uint64)
+    ent[:, :len(run)] = np.asarray(run, dtype=np.uint64)
+    ent[:, len(run)] = np.arange(count, dtype=np.uint64)
+    hc = [_SS_INIT_A]
+
+    def hashmix(v):
+        v = (v ^ np.uint64(hc[0])) & m32
+        hc[0] = (hc[0] * _SS_MULT_A) & 0xFFFFFFFF
+        v = (v * np.uint64(hc[0])) & m32
+        return v ^ (v >> sh16)
+
+    def mix(x, y):
+        r = (np.uint64(_SS_MIX_L) * x - np.uint64(_SS_MIX_R) * y) & m32
+        return r ^ (r >> sh16)
+
+    pool = [hashmix(ent[:, i]) for i in range(4)]
+    for src in range(4):
+        for dst in range(4):
+            if src != dst:
+                pool[dst] = mix(pool[dst], hashmix(pool[src]))
+    for src in range(4, ent.shape[1]):
+        for dst in range(4):
+            pool[dst] = mix(pool[dst], hashmix(ent[:, src]))
+    h = _SS_INIT_B
+    w32 = []
+    for i in range(8):
+        v = pool[i % 4] ^ np.uint64(h)
+        h = (h * _SS_MULT_B) & 0xFFFFFFFF
+        v = (v * np.uint64(h)) & m32
+        w32.append(v ^ (v >> sh16))
+    out = np.empty((count, 4), dtype=np.uint64)
+    for k in range(4):
+        out[:, k] = (w32[2 * k + 1] << np.uint64(32)) | w32[2 * k]
+    return out

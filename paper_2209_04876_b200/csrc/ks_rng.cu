@@ -457,13 +457,18 @@ __global__ void __launch_bounds__(ZT) zig_emit_kernel(const int16_t* __restrict_
 // `row` (states: 4 words per stream, state hi/lo then increment hi/lo).  The per-row sampler
 // draws of fast_factor_matrix_update (tucker.py:361-369, one SeedSequence child per row).
 __global__ void pcg_uniform_streams_kernel(const uint64_t* __restrict__ states, int64_t rows, int64_t per,
-                                           int64_t s, double* __restrict__ out) {
+                                           int64_t s, int seeded, double* __restrict__ out) {
   const int64_t chunks = (per + RAW_PER_THREAD - 1) / RAW_PER_THREAD;
   const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= rows * chunks) return;
   const int64_t row = q / chunks, k0 = (q - row * chunks) * RAW_PER_THREAD;
-  const u128 inc = mk128(states[4 * row + 2], states[4 * row + 3]);
-  u128 st = pcg_advance(mk128(states[4 * row], states[4 * row + 1]), inc, (uint64_t)k0 + 1);
+  u128 inc = mk128(states[4 * row + 2], states[4 * row + 3]);
+  u128 st0 = mk128(states[4 * row], states[4 * row + 1]);
+  if (seeded) {  // pcg64_set_seed: inc = 2 initseq + 1; state = ((0 M + inc) + initstate) M + inc
+    inc = (inc << 1) | 1;
+    st0 = (inc + st0) * PCG_MULT + inc;
+  }
+  u128 st = pcg_advance(st0, inc, (uint64_t)k0 + 1);
   const int n = (int)ks_min64(RAW_PER_THREAD, per - k0);
   for (int j = 0; j < n; j++) {
     const int64_t k = k0 + j, m = k / s, t = k - m * s;
@@ -557,12 +562,13 @@ extern "C" int ks_pcg64_standard_normal(uint64_t sh, uint64_t sl, uint64_t ih, u
   return KS_OK;
 }
 
-extern "C" int ks_pcg64_random_streams(const uint64_t* states, int64_t rows, int32_t nf, int64_t s, double* out,
-                                       void* stream) {
+extern "C" int ks_pcg64_random_streams(const uint64_t* states, int32_t seeded, int64_t rows, int32_t nf, int64_t s,
+                                       double* out, void* stream) {
   if (rows <= 0 || s <= 0 || nf <= 0) return KS_OK;
   const int64_t per = (int64_t)nf * s;
   const int64_t threads = rows * ((per + RAW_PER_THREAD - 1) / RAW_PER_THREAD);
-  pcg_uniform_streams_kernel<<<ceil_div_u(threads, 256), 256, 0, (cudaStream_t)stream>>>(states, rows, per, s, out);
+  pcg_uniform_streams_kernel<<<ceil_div_u(threads, 256), 256, 0, (cudaStream_t)stream>>>(states, rows, per, s, seeded,
+                                                                                          out);
   KS_CHECK_LAUNCH();
   return KS_OK;
 }

@@ -47,18 +47,30 @@ __device__ __forceinline__ int64_t mode_stride(const Others& o, int m) {
   return st;
 }
 
+// Sum over k < n of f(k, acc) with 8 independent accumulators (memory-level parallelism for the
+// L2-latency-bound gathers), combined in a fixed order.
+template <class F>
+__device__ __forceinline__ double sum8(int n, F f) {
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0, s4 = 0.0, s5 = 0.0, s6 = 0.0, s7 = 0.0;
+  int k = 0;
+  for (; k + 8 <= n; k += 8) {
+    s0 = f(k, s0); s1 = f(k + 1, s1); s2 = f(k + 2, s2); s3 = f(k + 3, s3);
+    s4 = f(k + 4, s4); s5 = f(k + 5, s5); s6 = f(k + 6, s6); s7 = f(k + 7, s7);
+  }
+  for (; k < n; k++) s0 = f(k, s0);
+  return ((s0 + s1) + (s2 + s3)) + ((s4 + s5) + (s6 + s7));
+}
+
 // dst = (I (x) .. (x) F (x) .. (x) I) src along mode m; F(i,k) = trans ? F[k*R+i] : F[i*R+k].
 __device__ void mode_product(const double* __restrict__ F, int R, int64_t st, bool trans,
                              const double* src, double* dst, int n) {
   for (int r = threadIdx.x; r < n; r += blockDim.x) {
     const int im = (int)((r / st) % R);
     const int64_t base = r - (int64_t)im * st;
-    double acc = 0.0;
-    for (int k = 0; k < R; k++) {
+    dst[r] = sum8(R, [&](int k, double acc) {
       const double f = trans ? __ldg(F + (int64_t)k * R + im) : __ldg(F + (int64_t)im * R + k);
-      acc = fma(f, src[base + (int64_t)k * st], acc);
-    }
-    dst[r] = acc;
+      return fma(f, src[base + (int64_t)k * st], acc);
+    });
   }
 }
 
@@ -90,9 +102,7 @@ __device__ void warp_dots(int K, int L, const double* __restrict__ P, int64_t sk
 }
 
 __device__ __forceinline__ double thread_dot(int L, const double* __restrict__ P, int64_t sl, const double* x) {
-  double acc = 0.0;
-  for (int l = 0; l < L; l++) acc = fma(__ldg(P + (int64_t)l * sl), x[l], acc);
-  return acc;
+  return sum8(L, [&](int l, double acc) { return fma(__ldg(P + (int64_t)l * sl), x[l], acc); });
 }
 
 __device__ double block_sumsq(const double* v, int n, double* red) {
@@ -302,71 +312,85 @@ struct RowArgs {
   double* hist;           // I_n x max_iters (may be null)
 };
 
-__device__ __forceinline__ double rrow(const RowArgs& a, const int32_t* jr, int64_t lo, int t, int rr) {
+// Right-group row element rr of sample t: A_1[j_t] (M = 2), a Khatri-Rao row (M >= 3), 1 (M = 1).
+struct RightRows {
+  const double* base;  // A_1 (M = 2) or kr + lo * R_right (M >= 3)
+  int M, RR, R1;
+  __device__ __forceinline__ double at(const int32_t* jr, int t, int rr) const {
+    if (M == 1) return 1.0;
+    if (M == 2) return __ldg(base + (int64_t)jr[t] * R1 + rr);
+    return base[(int64_t)t * RR + rr];
+  }
+};
+
+__device__ __forceinline__ RightRows right_rows(const RowArgs& a, int64_t lo) {
   const Others& o = a.o;
-  if (o.M == 1) return 1.0;
-  if (o.M == 2) return __ldg(o.A[1] + (int64_t)jr[t] * o.R[1] + rr);
-  return a.kr[(lo + t) * o.Rright + rr];
+  RightRows r;
+  r.M = o.M;
+  r.RR = o.Rright;
+  r.R1 = o.M >= 2 ? o.R[1] : 1;
+  r.base = o.M == 2 ? o.A[1] : (o.M >= 3 ? a.kr + lo * o.Rright : nullptr);
+  return r;
 }
 
 // c -> dst = K_S^T c (grouped); Z: u x R_right scratch, part: partial sums.
-__device__ void sk_transpose(const RowArgs& a, int64_t lo, int nt, int u, const int32_t* jr, const int32_t* gstart,
-                             const int32_t* gj, const double* c, double* Z, double* part, double* dst) {
-  const Others& o = a.o;
-  const int RR = o.Rright, R0 = o.R[0], n = o.Rrest;
+__device__ void sk_transpose(const RowArgs& a, const RightRows& rw, int u, const int32_t* jr,
+                             const int32_t* gstart, const int32_t* gj, const double* c, double* Z, double* part,
+                             double* dst) {
+  const int RR = a.o.Rright, R0 = a.o.R[0], n = a.o.Rrest;
+  const double* A0 = a.o.A[0];
   for (int task = threadIdx.x; task < u * RR; task += blockDim.x) {
     const int g = task / RR, rr = task - g * RR;
-    double acc = 0.0;
-    for (int t = gstart[g]; t < gstart[g + 1]; t++) acc = fma(c[t], rrow(a, jr, lo, t, rr), acc);
-    Z[task] = acc;
+    const int t0 = gstart[g];
+    Z[task] = sum8(gstart[g + 1] - t0, [&](int k, double acc) { return fma(c[t0 + k], rw.at(jr, t0 + k, rr), acc); });
   }
   __syncthreads();
   const int P = n >= (int)blockDim.x ? 1 : (int)blockDim.x / n;
   for (int task = threadIdx.x; task < n * P; task += blockDim.x) {
     const int pp = task / n, oo = task - pp * n;
     const int r0 = oo / RR, rr = oo - r0 * RR;
-    double acc = 0.0;
-    for (int g = pp; g < u; g += P) acc = fma(__ldg(o.A[0] + (int64_t)gj[g] * R0 + r0), Z[g * RR + rr], acc);
-    part[task] = acc;
+    const int cnt = u > pp ? (u - pp + P - 1) / P : 0;
+    part[task] = sum8(cnt, [&](int k, double acc) {
+      const int g = pp + k * P;
+      return fma(__ldg(A0 + (int64_t)gj[g] * R0 + r0), Z[g * RR + rr], acc);
+    });
   }
   __syncthreads();
   for (int oo = threadIdx.x; oo < n; oo += blockDim.x) {
-    double s = part[oo];
-    for (int pp = 1; pp < P; pp++) s += part[pp * n + oo];
-    dst[oo] = s;
+    double sacc = part[oo];
+    for (int pp = 1; pp < P; pp++) sacc += part[pp * n + oo];
+    dst[oo] = sacc;
   }
   __syncthreads();
-  (void)nt;
 }
 
 // c_t = v_t (v_t (K x)_t) for the row's samples (kron.py:258-300 then the scaling of :345).
-__device__ void sk_forward(const RowArgs& a, int64_t lo, int nt, int u, const int32_t* jr, const int32_t* gid,
-                           const int32_t* gj, const double* v, const double* xv, double* Y, double* c) {
-  const Others& o = a.o;
-  const int RR = o.Rright, R0 = o.R[0];
+__device__ void sk_forward(const RowArgs& a, const RightRows& rw, int nt, int u, const int32_t* jr,
+                           const int32_t* gid, const int32_t* gj, const double* v, const double* xv, double* Y,
+                           double* c) {
+  const int RR = a.o.Rright, R0 = a.o.R[0];
+  const double* A0 = a.o.A[0];
   for (int task = threadIdx.x; task < u * RR; task += blockDim.x) {
     const int g = task / RR, rr = task - g * RR;
-    const double* arow = o.A[0] + (int64_t)gj[g] * R0;
-    double acc = 0.0;
-    for (int r0 = 0; r0 < R0; r0++) acc = fma(__ldg(arow + r0), xv[r0 * RR + rr], acc);
-    Y[task] = acc;
+    const double* arow = A0 + (int64_t)gj[g] * R0;
+    Y[task] = sum8(R0, [&](int r0, double acc) { return fma(__ldg(arow + r0), xv[r0 * RR + rr], acc); });
   }
   __syncthreads();
   for (int t = threadIdx.x; t < nt; t += blockDim.x) {
     const double* y = Y + (int64_t)gid[t] * RR;
-    double acc = 0.0;
-    for (int rr = 0; rr < RR; rr++) acc = fma(y[rr], rrow(a, jr, lo, t, rr), acc);
-    c[t] = v[t] * (v[t] * acc);
+    const double val = sum8(RR, [&](int rr, double acc) { return fma(y[rr], rw.at(jr, t, rr), acc); });
+    c[t] = v[t] * (v[t] * val);
   }
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(FT) factor_rows_kernel(RowArgs a) {
+__global__ void __launch_bounds__(1024) factor_rows_kernel(RowArgs a) {
+  const int NT = blockDim.x;
   extern __shared__ double sm[];
   const Others& o = a.o;
   const int n = o.Rrest, Rn = a.ws.Rn, cap = a.cap, ucap = a.ucap;
   const int row = blockIdx.x;
-  const int P = n >= FT ? 1 : FT / n;
+  const int P = n >= NT ? 1 : NT / n;
   double* xv = sm;
   double* rhs = xv + n;
   double* tv = rhs + n;
@@ -389,7 +413,7 @@ __global__ void __launch_bounds__(FT) factor_rows_kernel(RowArgs a) {
   int32_t* gj = gid + cap;                    // ucap
   int32_t* gstart = gj + ucap;                // ucap + 1
   __shared__ int64_t s_lo, s_hi;
-  __shared__ int s_stop, s_wtot[FT / 32];
+  __shared__ int s_stop, s_wtot[32];
 
   // ---- this row's segment of the (sorted) sparse diagonal
   if (threadIdx.x == 0) {
@@ -416,7 +440,7 @@ __global__ void __launch_bounds__(FT) factor_rows_kernel(RowArgs a) {
   const int64_t kbase = a.shared ? 0 : (int64_t)row * o.Irest;
   // ---- samples: right-group flat index, value, v * b_at, first-factor groups
   int running = 0;
-  for (int base = 0; base < nt; base += FT) {
+  for (int base = 0; base < nt; base += NT) {
     const int t = base + threadIdx.x;
     int head = 0;
     int64_t j0 = 0;
@@ -462,7 +486,7 @@ __global__ void __launch_bounds__(FT) factor_rows_kernel(RowArgs a) {
     int before = running;
     for (int w = 0; w < wid; w++) before += s_wtot[w];
     int tot = 0;
-    for (int w = 0; w < FT / 32; w++) tot += s_wtot[w];
+    for (int w = 0; w < NT / 32; w++) tot += s_wtot[w];
     const int incl = before + __popc(bal & ((2u << lane) - 1u));  // heads up to and including t
     if (t < nt) {
       const int g = incl - 1;
@@ -483,24 +507,25 @@ __global__ void __launch_bounds__(FT) factor_rows_kernel(RowArgs a) {
     return;
   }
   if (threadIdx.x == 0) gstart[u] = nt;
-  for (int t = threadIdx.x; t < nt; t += FT) cc[t] = vv[t] * vb[t];
+  for (int t = threadIdx.x; t < nt; t += NT) cc[t] = vv[t] * vb[t];
   __syncthreads();
   const double w = a.ws.wdev[0];
 
   // ---- rhs = K_S^T (v * (v * b_at))
-  sk_transpose(a, lo, nt, u, jr, gstart, gj, cc, YZ, part, rhs);
+  const RightRows rw = right_rows(a, lo);
+  sk_transpose(a, rw, u, jr, gstart, gj, cc, YZ, part, rhs);
   // ---- Richardson (solvers.py:201-248)
-  for (int r = threadIdx.x; r < n; r += FT) xv[r] = 0.0;
+  for (int r = threadIdx.x; r < n; r += NT) xv[r] = 0.0;
   ws_apply(o, a.ws, rhs, bv, tmp, p0, p1, s0, s1, sv);
   const double scale = sqrt(block_sumsq(sv, n, red));
   const double tol = a.residual_tol * fmax(scale, 2.2250738585072014e-308);
   int done = 0, nh = 0, diverged = 0;
   for (int it = 0; it < a.max_iters; it++) {
     // tv = normal(x) - rhs
-    sk_forward(a, lo, nt, u, jr, gid, gj, vv, xv, YZ, cc);
-    sk_transpose(a, lo, nt, u, jr, gstart, gj, cc, YZ, part, tv);
+    sk_forward(a, rw, nt, u, jr, gid, gj, vv, xv, YZ, cc);
+    sk_transpose(a, rw, u, jr, gstart, gj, cc, YZ, part, tv);
     penalty_terms(o, a.ws, w, xv, tv, s0, s1);
-    for (int r = threadIdx.x; r < n; r += FT) tv[r] = tv[r] - rhs[r];
+    for (int r = threadIdx.x; r < n; r += NT) tv[r] = tv[r] - rhs[r];
     __syncthreads();
     ws_apply(o, a.ws, tv, bv, tmp, p0, p1, s0, s1, sv);
     const double nrm = sqrt(block_sumsq(sv, n, red));
@@ -517,7 +542,7 @@ __global__ void __launch_bounds__(FT) factor_rows_kernel(RowArgs a) {
         break;
       }
     }
-    for (int r = threadIdx.x; r < n; r += FT) xv[r] = xv[r] - a.damping * sv[r];
+    for (int r = threadIdx.x; r < n; r += NT) xv[r] = xv[r] - a.damping * sv[r];
     __syncthreads();
     done++;
   }
@@ -527,11 +552,11 @@ __global__ void __launch_bounds__(FT) factor_rows_kernel(RowArgs a) {
     a.flags[row] = diverged;
   }
   if (a.hist)
-    for (int k = threadIdx.x; k < a.max_iters; k += FT) a.hist[(int64_t)row * a.max_iters + k] = k < nh ? hs[k] : 0.0;
+    for (int k = threadIdx.x; k < a.max_iters; k += NT) a.hist[(int64_t)row * a.max_iters + k] = k < nh ? hs[k] : 0.0;
   // ---- z = G^T ((G^T)^+ x); new row = (G^T)^+ z  (tucker.py:377-378)
   warp_dots(Rn, n, a.ws.gnp, 1, Rn, xv, s0);
   __syncthreads();
-  for (int r = threadIdx.x; r < n; r += FT) tv[r] = thread_dot(Rn, a.ws.gn + r, n, s0);
+  for (int r = threadIdx.x; r < n; r += NT) tv[r] = thread_dot(Rn, a.ws.gn + r, n, s0);
   __syncthreads();
   warp_dots(Rn, n, a.ws.gnp, 1, Rn, tv, s1);
   __syncthreads();
@@ -758,8 +783,8 @@ extern "C" int ks_factor_draws_rows(int32_t M, const double* const* cdf, const d
 }
 
 extern "C" int64_t ks_factor_rows_smem(int32_t Rrest, int32_t Rright, int32_t Rn, int32_t max_iters, int32_t cap,
-                                       int32_t ucap) {
-  const int P = Rrest >= FT ? 1 : FT / Rrest;
+                                       int32_t ucap, int32_t threads) {
+  const int P = Rrest >= threads ? 1 : threads / Rrest;
   return (int64_t)sizeof(double) * ((int64_t)8 * Rrest + (int64_t)P * Rrest + 2 * Rn + 32 + max_iters + 3LL * cap +
                                     (int64_t)ucap * Rright) +
          (int64_t)sizeof(int32_t) * (2LL * cap + 2LL * ucap + 1);
@@ -782,7 +807,10 @@ extern "C" int ks_factor_rows_richardson(int32_t M, const double* const* A, cons
   if (rows <= 0) return KS_OK;
   cap = (int32_t)ks_max64(1, cap);
   const int32_t ucap = (int32_t)ks_min64(cap, o.I[0]);
-  const int64_t smem = ks_factor_rows_smem(o.Rrest, o.Rright, Rn, max_iters, cap, ucap);
+  // few heavy rows: 32 warps per row to hide the L2 latency of the factor-row gathers
+  // (measured at c5: 1024 threads for the 64 mode-2 rows, 256 for the 512 rows of modes 0/1)
+  const int threads = rows <= 2 * (int64_t)ks::num_sms() ? 1024 : 256;
+  const int64_t smem = ks_factor_rows_smem(o.Rrest, o.Rright, Rn, max_iters, cap, ucap, threads);
   KS_REQUIRE(smem <= 227 * 1024, KS_ESIZE, "factor row solve needs %lld bytes of shared memory (> 227 KB)",
              (long long)smem);
   RowArgs a{};
@@ -806,7 +834,7 @@ extern "C" int ks_factor_rows_richardson(int32_t M, const double* const* A, cons
   a.flags = flags;
   a.hist = hist;
   KS_TRY_CUDA(cudaFuncSetAttribute(factor_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  factor_rows_kernel<<<(unsigned)rows, FT, (size_t)smem, (cudaStream_t)stream>>>(a);
+  factor_rows_kernel<<<(unsigned)rows, threads, (size_t)smem, (cudaStream_t)stream>>>(a);
   KS_CHECK_LAUNCH();
   return KS_OK;
 }

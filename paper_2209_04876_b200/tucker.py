@@ -30,7 +30,7 @@ import torch
 
 from . import _device as D
 from . import _lib
-from ._numpy_rng import pcg64_state, split128
+from ._numpy_rng import pcg64_state, seedseq_children_seed_words, split128
 from .errors import InvalidInputError, NumericalFailureError, SizeGuardError
 from .kron import _kron_apply_dev
 from .leverage import REGRESSION_SAMPLE_CONSTANT, ProductSampler, device_standard_normal, ridge_leverage_scores
@@ -387,14 +387,19 @@ def _factor_sample_count(config: RegressionConfig, r_rest: int, i_n: int) -> int
                             * math.log(i_n / config.delta) / config.eps))
 
 
-def _row_states(seed, rows: int, share: bool) -> torch.Tensor:
-    seeds = np.random.SeedSequence(seed).spawn(rows)
-    use = seeds[:1] if share else seeds
-    words = np.empty((len(use), 4), dtype=np.uint64)
-    for i, ss in enumerate(use):
+def _row_states(seed, rows: int, share: bool):
+    """Seeding words of SeedSequence(seed).spawn(rows) (only the first child when shared) and
+    whether they are pcg64_set_seed inputs (1) or final PCG64 states (0)."""
+    use = 1 if share else rows
+    if isinstance(seed, (int, np.integer)) and int(seed) >= 0:
+        words = seedseq_children_seed_words(int(seed), use)
+        return torch.from_numpy(words.view(np.int64)).to(D.dev()), 1
+    seeds = np.random.SeedSequence(seed).spawn(rows)[:use]
+    words = np.empty((use, 4), dtype=np.uint64)
+    for i, ss in enumerate(seeds):
         st, inc = pcg64_state(ss)
         words[i] = (*split128(st), *split128(inc))
-    return torch.from_numpy(words.view(np.int64)).to(D.dev())
+    return torch.from_numpy(words.view(np.int64)).to(D.dev()), 0
 
 
 def fast_factor_matrix_update(model: TuckerModel, x, n: int, config: RegressionConfig,
@@ -437,9 +442,9 @@ def _fast_factor_update_dev(core, facs, lam, xt, n, config, caches, trace=None):
     M = len(others)
     share = bool(config.share_row_sketch)
     nstreams = 1 if share else i_n
-    states = _row_states(config.seed, i_n, share)
+    states, seeded = _row_states(config.seed, i_n, share)
     u = D.empty(M * nstreams * s)
-    _lib.call("ks_pcg64_random_streams", D.p(states), nstreams, M, s, D.p(u), D.stream())
+    _lib.call("ks_pcg64_random_streams", D.p(states), seeded, nstreams, M, s, D.p(u), D.stream())
     idx = D.empty(nstreams * s, M + 1, dtype=D.I64)
     w = D.empty(nstreams * s)
     _lib.call("ks_factor_draws_rows", M, _ptrs(sampler._cdfs), _ptrs(sampler._probs),

@@ -179,3 +179,19 @@ def test_c5_fast_factor_update_mode2_matches_oracle():
     naive = K().naive_factor_update(model_of(core, facs, 1e-3), x, 2)
     assert rel(naive, T.naive_factor_update(core, facs, 1e-3, x, 2)) <= 1e-10
     assert math.isfinite(float(np.sum(got)))
+
+
+@pytest.mark.parametrize("mode", ["fast", "exact"])
+def test_c5_als_sweep_matches_reference_fixture(golden, mode):
+    """One ALS sweep at BASELINE config 5 against the reference's own run (tests/golden/c5_als.npz,
+    make_golden.py c5als): step losses, final core, factor 2 and rre."""
+    g = golden("c5_als")
+    x = O.synth_tucker((512, 512, 64), (16, 16, 4), 0.01, seed=0)
+    cfg = (K().RegressionConfig(eps=0.1, delta=0.01, alpha=1e-5, seed=0) if mode == "fast"
+           else K().RegressionConfig(seed=0))
+    model, rep = K().tucker_als(x, (16, 16, 4), lam=1e-3, sweeps=1, solver_mode=mode, config=cfg)
+    tol = 1e-9 if mode == "exact" else 1e-7
+    np.testing.assert_allclose(rep.step_losses, g[f"{mode}_losses"], rtol=tol)
+    assert rep.rre == pytest.approx(float(g[f"{mode}_rre"]), rel=tol)
+    assert rel(model.core, g[f"{mode}_core"]) <= 100 * tol
+    assert rel(model.factors[2], g[f"{mode}_factor2"]) <= 100 * tol

@@ -33,3 +33,20 @@ def test_ziggurat_restatement_bit_exact(seed):
     g = np.random.default_rng(seed)
     g.standard_normal(n)
     assert g.bit_generator.random_raw(1)[0] == raw[used]
+
+
+@pytest.mark.parametrize("seed", [0, 7, 12345, 2 ** 40 + 3, 4294967295, 2 ** 70 + 11])
+def test_seedseq_children_words_match_numpy(seed):
+    """The vectorised SeedSequence children seeding (fast_factor_matrix_update's per-row streams)
+    is bit-exact with NumPy: finishing pcg64_set_seed on the words gives PCG64(child).state."""
+    from paper_2209_04876_b200._numpy_rng import seedseq_children_seed_words
+    words = seedseq_children_seed_words(seed, 300)
+    mult = 0x2360ED051FC65DA44385DF649FCCF645
+    m128 = (1 << 128) - 1
+    for i, child in enumerate(np.random.SeedSequence(seed).spawn(300)):
+        initstate = (int(words[i, 0]) << 64) | int(words[i, 1])
+        initseq = (int(words[i, 2]) << 64) | int(words[i, 3])
+        inc = ((initseq << 1) | 1) & m128
+        state = (((inc + initstate) & m128) * mult + inc) & m128
+        st = np.random.PCG64(child).state["state"]
+        assert (state, inc) == (int(st["state"]), int(st["inc"]))
