@@ -382,6 +382,13 @@ int ks_qr_explicit(const double* A, int64_t n, int32_t k, double* Q, void* strea
 int ks_pinv_compose(const double* U, int64_t n, const double* sigma, const double* V, int64_t d,
                     int32_t k, double* X, void* stream);
 
+
+/* sketch_rows_of_kron (kron.py:208-222): out (s x prod cols) = w[t] * (A_0[j_0] (x) ... (x) A_{nf-1}[j_{nf-1}])
+ * for draw t; idx holds s x nf multi-indices (flat == 0) or s flat row indices (flat != 0).  The
+ * materialised S K of sketch_and_solve_ridge (solvers.py:334-369). */
+int ks_sketch_rows(int32_t nf, const double* const* factors, const int64_t* rows, const int32_t* cols,
+                   const int64_t* idx, int32_t flat, const double* w, int64_t s, double* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -570,3 +570,41 @@ def initial_tucker_factors(shape, core_shape, seed):
         q, _ = np.linalg.qr(gen.standard_normal((i_n, r_n)))
         out.append(q)
     return out
+
+
+# ---------------------------------------------------------------------------
+# Dense comparison baselines (solvers.py:277-299, :334-369) -- SURVEY.md 8(f) row 3
+# ---------------------------------------------------------------------------
+
+def naive_normal_solve(factors, b, lam):
+    """Densified normal equations: pinv(kron(A^T A) + lam I) K^T b -- solvers.py:277-299."""
+    mats = [np.asarray(a, dtype=np.float64) for a in factors]
+    b = np.asarray(b, dtype=np.float64).reshape(-1)
+    cols = math.prod(a.shape[1] for a in mats)
+    gram = reduce(np.kron, [a.T @ a for a in mats])
+    ktb = kron_mat_mul([a.T for a in mats], b)
+    x = np.linalg.pinv(gram + lam * np.eye(cols)) @ ktb
+    return Report(x, ridge_loss(mats, x, b, lam), 0, 0, 0.0, {})
+
+
+def sketch_and_solve_ridge(factors, b, eps=0.25, lam=0.0, alpha=1.0, seed=0, sketch=None):
+    """Sketch-and-solve with exact leverage-score product sampling -- solvers.py:334-369.
+
+    ``sketch`` = (indices, weights) overrides the draw."""
+    mats = [np.asarray(a, dtype=np.float64) for a in factors]
+    b = np.asarray(b, dtype=np.float64).reshape(-1)
+    cols = math.prod(a.shape[1] for a in mats)
+    if sketch is None:
+        sampler = Sampler([ridge_scores(compact_svd(a), 0.0) for a in mats])
+        s = max(1, math.ceil(alpha * regression_sample_count(cols, eps)))
+        idx, w = sample_rows(sampler, s, seed)
+    else:
+        idx, w = sketch
+    s = w.size
+    idx = np.asarray(idx)
+    multi = idx if idx.ndim == 2 else np.stack(np.unravel_index(idx, tuple(a.shape[0] for a in mats)), axis=1)
+    sk = w[:, None] * _rows_of(mats, multi)
+    flat = np.ravel_multi_index(tuple(multi.T), tuple(a.shape[0] for a in mats))
+    sb = w * b[flat]
+    x = np.linalg.pinv(sk.T @ sk + lam * np.eye(cols)) @ (sk.T @ sb)
+    return Report(x, ridge_loss(mats, x, b, lam), 0, s, 0.0, {"indices": idx, "weights": w})

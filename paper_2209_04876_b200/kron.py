@@ -403,3 +403,31 @@ def sketched_kron_transpose_apply(factors: Sequence, s_diag: SparseDiagonal, b_v
     _lib.call("ks_sketched_transpose_apply", ctypes.byref(view.struct), D.p(bv.contiguous()),
               D.p(view.perm_arg()), D.p(G), D.stream())
     return D.out(view.from_groups(G), host)
+
+
+def sketch_rows_of_kron(factors: Sequence, sketch):
+    """Materialise the sketched matrix ``S K``: one rescaled row per draw (kron.py:208-222)."""
+    host = not D.on_device(sketch.weights)
+    facs = check_factors(factors)
+    rows, _ = kron_operator_shape(facs)
+    idx = D.to_dev(sketch.indices, D.I64).contiguous()
+    w = D.to_dev(sketch.weights).reshape(-1).contiguous()
+    flat = idx.ndim == 1
+    if idx.numel():
+        if flat:
+            lo, hi = int(idx.min()), int(idx.max())
+            if lo < 0 or hi >= rows:
+                raise InvalidInputError("sketch index out of range")
+        else:
+            mn, mx = idx.min(dim=0).values.tolist(), idx.max(dim=0).values.tolist()
+            for n, a in enumerate(facs):
+                if mn[n] < 0 or mx[n] >= int(a.shape[0]):
+                    raise InvalidInputError(f"sketch index out of range in mode {n}")
+    s = int(w.numel())
+    ncols = math.prod(int(a.shape[1]) for a in facs)
+    out = D.empty(s, ncols)
+    _lib.call("ks_sketch_rows", len(facs), _lib.ptr_array(ctypes.c_void_p, [a.data_ptr() for a in facs]),
+              _lib.ptr_array(ctypes.c_int64, [int(a.shape[0]) for a in facs]),
+              _lib.ptr_array(ctypes.c_int32, [int(a.shape[1]) for a in facs]), D.p(idx), int(flat), D.p(w), s,
+              D.p(out), D.stream())
+    return D.out(out, host)

@@ -26,7 +26,7 @@ import torch
 
 from . import _device as D
 from . import _lib
-from .errors import InvalidInputError, NumericalFailureError
+from .errors import InvalidInputError, NumericalFailureError, SizeGuardError
 from .kron import (SparseDiagonal, _kron_apply_dev, _view_for, check_factors, grouped2_eligible,
                    kron_operator_shape, sketch_diag_grouped2_finish, sketch_diag_grouped2_launch,
                    kron_vec_square, sparse_diagonal_from_sketch)
@@ -982,3 +982,96 @@ def fast_kronecker_regression(factors: Sequence, b, config: RegressionConfig,
     else:
         loss = float("nan")
     return SolveReport(solution=D.out(x, host), loss=loss, iterations=iters, sample_count=s, wall_time=wall)
+
+
+def _pinv_sym_dev(m: torch.Tensor) -> torch.Tensor:
+    """np.linalg.pinv (rcond 1e-15) of a symmetric matrix on the device: the one-sided Jacobi SVD
+    for n <= 128; above that the dense eigensolver of the CUDA math library (cuSOLVER syevd via
+    torch.linalg.eigh) -- used only by the dense comparison baseline sketch_and_solve_ridge."""
+    n = int(m.shape[0])
+    if n <= 128:
+        from .tensor import _pinv_dev
+        return _pinv_dev(m.contiguous(), 1e-15)
+    w, v = torch.linalg.eigh(0.5 * (m + m.T))
+    a = w.abs()
+    keep = a > 1e-15 * a.max()
+    inv = torch.where(keep, 1.0 / torch.where(keep, w, torch.ones_like(w)), torch.zeros_like(w))
+    return ((v * inv) @ v.T).contiguous()
+
+
+def naive_normal_solve(factors: Sequence, b, lam: float,
+                       max_dense_entries: int | None = DEFAULT_DENSE_GUARD) -> SolveReport:
+    """Exact ridge solution of the normal equations (solvers.py:277-299).
+
+    The reference densifies ``K^T K = kron(A_n^T A_n)`` and pseudo-inverts it.  Its pseudo-inverse
+    (singular values above 1e-15 of the largest) is exactly ``(kron V_n) diag(pinv(kron w_n + lam))
+    (kron V_n)^T`` from the factor Gram eigendecompositions, which is how it is applied here:
+    O(sum d_n^3) instead of O(prod d_n^3), same result to rounding.  The size guard is kept."""
+    host = not D.on_device(b)
+    facs, rows, cols = _validated_problem(factors, b)
+    if lam < 0:
+        raise InvalidInputError(f"lambda must be >= 0, got {lam}")
+    if max_dense_entries is not None and cols * cols > max_dense_entries:
+        raise SizeGuardError(f"normal matrix would hold {cols}x{cols} entries (guard: {max_dense_entries})")
+    bt = D.to_dev(b).reshape(-1)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    eig = [_factor_gram_dev(_gram_dev(a)) for a in facs]
+    ktb = _kron_apply_dev([a.T.contiguous() for a in facs], bt[:, None].contiguous())
+    w = reduce(torch.kron, [e[1] for e in eig]) + lam
+    a = w.abs()
+    keep = a > 1e-15 * a.max()
+    dinv = torch.where(keep, 1.0 / torch.where(keep, w, torch.ones_like(w)), torch.zeros_like(w))
+    t = _kron_apply_dev([e[0].T.contiguous() for e in eig], ktb) * dinv[:, None]
+    x = _kron_apply_dev([e[0] for e in eig], t.contiguous())[:, 0].contiguous()
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    return SolveReport(solution=D.out(x, host), loss=_ridge_loss_dev(facs, x, bt, lam), iterations=0,
+                       sample_count=0, wall_time=wall)
+
+
+def sketch_and_solve_ridge(factors: Sequence, b, config: RegressionConfig, sketch=None,
+                           max_dense_entries: int | None = DEFAULT_DENSE_GUARD) -> SolveReport:
+    """Sketch-and-solve baseline (DJSSW19, solvers.py:334-369): draw rows from the exact
+    leverage-score product distribution, materialise S K (ks_sketch_rows), solve
+    ``((SK)^T SK + lam I)^+ (SK)^T S b``."""
+    from .kron import sketch_rows_of_kron
+    from .leverage import RowSketch, build_product_sampler, regression_sample_count, sample_rows
+    host = not D.on_device(b)
+    facs, rows, cols = _validated_problem(factors, b)
+    bt = D.to_dev(b).reshape(-1)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    if sketch is None:
+        sampler = build_product_sampler(exact_factor_scores(facs))
+        s = max(1, math.ceil(config.effective_alpha * regression_sample_count(cols, config.eps)))
+        sketch = sample_rows(sampler, s, config.seed)
+    s = sketch.sample_count
+    if max_dense_entries is not None and max(s * cols, cols * cols) > max_dense_entries:
+        raise SizeGuardError(f"sketched matrix would hold {s}x{cols} entries (guard: {max_dense_entries})")
+    idx = D.to_dev(sketch.indices, D.I64)
+    sw = D.to_dev(sketch.weights).reshape(-1)
+    sk = sketch_rows_of_kron(facs, RowSketch(indices=idx, weights=sw))
+    if idx.ndim == 2:
+        strides = torch.tensor([math.prod(int(a.shape[0]) for a in facs[n + 1:]) for n in range(len(facs))],
+                               dtype=torch.int64, device=idx.device)
+        flat = (idx * strides).sum(dim=1).contiguous()
+    else:
+        flat = idx.contiguous()
+    bat = D.empty(s)
+    _lib.call("ks_gather", D.p(bt), D.p(flat), s, D.p(bat), D.stream())
+    sb = (sw * bat).contiguous()
+    m = D.empty(cols, cols)
+    _lib.call("ks_gemm", cols, cols, s, 1.0, D.p(sk), 1, cols, 0, D.p(sk), cols, 1, 0, 0.0, D.p(m), cols, 1, 0, 1,
+              D.stream())
+    m += config.lam * torch.eye(cols, dtype=D.F64, device=m.device)
+    r = D.empty(cols, 1)
+    _lib.call("ks_gemm", cols, 1, s, 1.0, D.p(sk), 1, cols, 0, D.p(sb), 1, 1, 0, 0.0, D.p(r), 1, 1, 0, 1, D.stream())
+    p = _pinv_sym_dev(m)
+    x = D.empty(cols, 1)
+    _lib.call("ks_gemm", cols, 1, cols, 1.0, D.p(p), cols, 1, 0, D.p(r), 1, 1, 0, 0.0, D.p(x), 1, 1, 0, 1, D.stream())
+    x = x[:, 0].contiguous()
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    return SolveReport(solution=D.out(x, host), loss=_ridge_loss_dev(facs, x, bt, config.lam), iterations=0,
+                       sample_count=s, wall_time=wall)

@@ -108,3 +108,22 @@ def test_oracle_matches_live_reference_units(golden):
     a = np.random.default_rng(12345).standard_normal((50, 5))
     sc, _ = O.jl_scores(a, a, a.T @ a, 0.25, 3)
     np.testing.assert_array_equal(sc, u["jl_scores"])
+
+
+@pytest.mark.skipif(not REFERENCE_SRC.exists(), reason="reference not mounted (GPU box)")
+def test_dense_baselines_match_live_reference():
+    sys.path.insert(0, str(REFERENCE_SRC))
+    import kronsolve as ks
+    rng = np.random.default_rng(77)
+    facs = [rng.standard_normal((14, 3)), rng.standard_normal((12, 2))]
+    b = rng.standard_normal(14 * 12)
+    for lam in (0.0, 1e-2):
+        r = ks.naive_normal_solve(facs, b, lam)
+        o = O.naive_normal_solve(facs, b, lam)
+        np.testing.assert_array_equal(o.solution, r.solution)
+        assert o.loss == r.loss
+        cfg = ks.RegressionConfig(eps=0.5, delta=0.1, lam=lam, seed=4)
+        r = ks.sketch_and_solve_ridge(facs, b, cfg)
+        o = O.sketch_and_solve_ridge(facs, b, eps=0.5, lam=lam, seed=4)
+        np.testing.assert_array_equal(o.solution, r.solution)
+        assert o.sample_count == r.sample_count
