@@ -389,6 +389,18 @@ int ks_pinv_compose(const double* U, int64_t n, const double* sigma, const doubl
 int ks_sketch_rows(int32_t nf, const double* const* factors, const int64_t* rows, const int32_t* cols,
                    const int64_t* idx, int32_t flat, const double* w, int64_t s, double* out, void* stream);
 
+
+/* CholeskyQR2 of a tall A (n x d, n >= d, d <= 128): R (d x d upper) with R^T R = A^T A; *ok (host)
+ * = 0 when A is too ill-conditioned (kappa^2 > ~1e13) and R is undefined.  ks_qr_r uses it for
+ * n >= 4d before falling back to Householder TSQR.  Synchronises the stream. */
+int ks_chol_qr2_r(const double* A, int64_t n, int32_t d, double* R, int32_t* ok, void* stream);
+
+/* Statistical leverage scores of a numerically full-rank tall A: scores[i] = ||(A R^-1)_i||^2 with
+ * R from CholeskyQR2 (= ridge_leverage_scores(compact_svd(a), 0), leverage.py:51-64, for
+ * kappa(A) < ~3e6).  *ok = 0 when A is too ill-conditioned (scores undefined; use the compact SVD).
+ * Synchronises the stream.  spectral_approx_rows' scores (leverage.py:235-252). */
+int ks_leverage_scores_tall(const double* A, int64_t n, int32_t d, double* scores, int32_t* ok, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

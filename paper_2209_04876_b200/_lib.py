@@ -97,6 +97,8 @@ _SIGS = {
     "ks_qr_explicit": ([_p, _i64, _i32, _p, _p], ctypes.c_int),
     "ks_pinv_compose": ([_p, _i64, _p, _p, _i64, _i32, _p, _p], ctypes.c_int),
     "ks_sketch_rows": ([_i32, _p, _p, _p, _p, _i32, _p, _i64, _p, _p], ctypes.c_int),
+    "ks_chol_qr2_r": ([_p, _i64, _i32, _p, POINTER(c_int32), _p], ctypes.c_int),
+    "ks_leverage_scores_tall": ([_p, _i64, _i32, _p, POINTER(c_int32), _p], ctypes.c_int),
 }
 
 _lock = threading.Lock()

@@ -390,9 +390,21 @@ def sample_rows(sampler, s: int, seed) -> RowSketch:
     return RowSketch(indices=D.out(idx, host), weights=D.out(w, host))
 
 
+def _statistical_scores_dev(a: torch.Tensor) -> torch.Tensor:
+    """ridge_leverage_scores(compact_svd(a), 0).scores: for a tall, numerically full-rank a the
+    squared row norms of a R^-1 (CholeskyQR2 R, one fused pass); otherwise the compact SVD."""
+    n, d = int(a.shape[0]), int(a.shape[1])
+    if n >= 4 * d and d <= 128:
+        sc = D.empty(n)
+        ok = ctypes.c_int32(0)
+        _lib.call("ks_leverage_scores_tall", D.p(a.contiguous()), n, d, D.p(sc), ctypes.byref(ok), D.stream())
+        if ok.value:
+            return sc
+    return ridge_leverage_scores(compact_svd(a), 0.0).scores
+
+
 def _spectral_rows_dev(a: torch.Tensor, eps: float, delta: float, seed, alpha: float) -> torch.Tensor:
-    svd = compact_svd(a)
-    sc = ridge_leverage_scores(svd, 0.0).scores
+    sc = _statistical_scores_dev(a)
     p1, _ = _tables(D.to_dev(sc), renorm=False, want_cdf=False, what="score vector")
     s = max(1, math.ceil(alpha * spectral_sample_count(int(a.shape[1]), eps, delta)))
     sk = sample_rows(p1, s, seed)
