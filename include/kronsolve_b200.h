@@ -401,6 +401,11 @@ int ks_chol_qr2_r(const double* A, int64_t n, int32_t d, double* R, int32_t* ok,
  * Synchronises the stream.  spectral_approx_rows' scores (leverage.py:235-252). */
 int ks_leverage_scores_tall(const double* A, int64_t n, int32_t d, double* scores, int32_t* ok, void* stream);
 
+/* ks_leverage_scores_tall without a host round trip: info_dev (device, 2 x int32) is written with
+ * the two Cholesky status words (nonzero = declined, scores undefined).  Graph-capturable. */
+int ks_leverage_scores_tall_async(const double* A, int64_t n, int32_t d, double* scores, int32_t* info_dev,
+                                  void* stream);
+
 #ifdef __cplusplus
 }
 #endif

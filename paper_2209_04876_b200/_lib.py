@@ -99,6 +99,7 @@ _SIGS = {
     "ks_sketch_rows": ([_i32, _p, _p, _p, _p, _i32, _p, _i64, _p, _p], ctypes.c_int),
     "ks_chol_qr2_r": ([_p, _i64, _i32, _p, POINTER(c_int32), _p], ctypes.c_int),
     "ks_leverage_scores_tall": ([_p, _i64, _i32, _p, POINTER(c_int32), _p], ctypes.c_int),
+    "ks_leverage_scores_tall_async": ([_p, _i64, _i32, _p, _p, _p], ctypes.c_int),
 }
 
 _lock = threading.Lock()

@@ -2,16 +2,16 @@
 //
 // The R factor of A (reference: the QR inside tensor.compact_svd, tensor.py:76-107, LAPACK
 // Householder) is computed as R = R2 R1 with R1 = chol(A^T A), Q1 = A R1^-1, R2 = chol(Q1^T Q1):
-// two Gram passes on the FP64 tensor pipe (ks_gemm_tn_tall) and one streaming triangular solve,
+// two Gram passes on the FP64 tensor pipe (ks_gemm_tn_tall) and one streaming product with R1^-1,
 // instead of a latency-bound Householder TSQR.  R is unique up to row signs; every consumer (the
 // one-sided Jacobi SVD of R, U = A V Sigma^-1, scores) is invariant to them.  CholeskyQR2 is
-// backward stable like Householder for kappa(A) below ~1e7; a Cholesky pivot that is not
+// backward stable like Householder for kappa(A) below ~1e6; a Cholesky pivot that is not
 // comfortably positive (ill-conditioned or rank-deficient A) reports failure and the caller falls
 // back to Householder TSQR (ks_qr_r).
 //
 // Statistical leverage scores (ridge_leverage_scores(compact_svd(a), 0), leverage.py:51-64) of a
 // numerically full-rank A are the squared row norms of A R^-1; ks_leverage_scores_tall fuses the
-// triangular solve and the row norms in one pass.
+// product and the row norms in one pass.
 #include "ks_common.cuh"
 
 namespace ks {
@@ -27,12 +27,15 @@ namespace {
 constexpr int CT = 256;
 
 // Upper Cholesky factor R (R^T R = 0.5 (G + G^T)) of a d x d Gram in one CTA (right-looking, in
-// shared memory).  info[slot] = k + 1 if pivot k is below tol * max diag (not comfortably PD).
+// shared memory) and, if asked, its inverse (upper) by column-parallel back substitution.
+// info[slot] = k + 1 if pivot k is below tol * max diag (not comfortably positive definite).
 __global__ void __launch_bounds__(CT) chol_upper_kernel(const double* __restrict__ G, int d, double* __restrict__ R,
-                                                       int32_t* __restrict__ info, int slot) {
-  extern __shared__ double S[];  // d x d, row-major, upper triangle used
-  __shared__ double s_piv, s_dmax;
+                                                       double* __restrict__ Rinv, int32_t* __restrict__ info,
+                                                       int slot) {
+  extern __shared__ double S[];      // d x d (row-major, upper triangle used), then row k
+  double* W = S + (size_t)d * d;
   __shared__ int s_bad;
+  __shared__ double s_dmax;
   for (int e = threadIdx.x; e < d * d; e += CT) {
     const int i = e / d, j = e - i * d;
     S[e] = i <= j ? 0.5 * (G[i * d + j] + G[j * d + i]) : 0.0;
@@ -40,102 +43,113 @@ __global__ void __launch_bounds__(CT) chol_upper_kernel(const double* __restrict
   if (threadIdx.x == 0) {
     s_bad = 0;
     double m = 0.0;
-    for (int i = 0; i < d; i++) m = fmax(m, 0.5 * (G[i * d + i] + G[i * d + i]));
+    for (int i = 0; i < d; i++) m = fmax(m, G[i * d + i]);
     s_dmax = m;
   }
   __syncthreads();
-  const double tol = 1e-13 * s_dmax;  // kappa(A)^2 below ~1e13: CholeskyQR2 regime
+  const double tol = 1e-12 * s_dmax;  // kappa(A)^2 below ~1e12: the CholeskyQR2 regime
   for (int k = 0; k < d; k++) {
-    if (threadIdx.x == 0) {
-      const double p = S[k * d + k];
-      if (!(p > tol) || !isfinite(p)) {
-        s_bad = k + 1;
-        s_piv = 1.0;
-      } else {
-        s_piv = sqrt(p);
-      }
-      S[k * d + k] = s_piv;
+    const double p = S[k * d + k];    // every thread reads the pivot: no broadcast step
+    if (!(p > tol) || !isfinite(p)) {
+      if (threadIdx.x == 0) s_bad = k + 1;
+      break;
     }
+    const double r = sqrt(p);
+    for (int j = k + threadIdx.x; j < d; j += CT) W[j] = (j == k) ? r : S[k * d + j] / r;
     __syncthreads();
-    if (s_bad) break;
-    const double r = s_piv;
-    for (int j = k + 1 + threadIdx.x; j < d; j += CT) S[k * d + j] /= r;
-    __syncthreads();
+    for (int j = k + threadIdx.x; j < d; j += CT) S[k * d + j] = W[j];
     const int m = d - k - 1;
     for (int e = threadIdx.x; e < m * m; e += CT) {
       const int i = k + 1 + e / m, j = k + 1 + e % m;
-      if (i <= j) S[i * d + j] = fma(-S[k * d + i], S[k * d + j], S[i * d + j]);
+      if (i <= j) S[i * d + j] = fma(-W[i], W[j], S[i * d + j]);
     }
     __syncthreads();
   }
-  if (threadIdx.x == 0 && info) info[slot] = s_bad;
+  __syncthreads();
+  const int bad = s_bad;
+  if (threadIdx.x == 0 && info) info[slot] = bad;
   for (int e = threadIdx.x; e < d * d; e += CT) {
     const int i = e / d, j = e - i * d;
     R[e] = i <= j ? S[e] : 0.0;
   }
+  if (!Rinv || bad) return;
+  // column j of R^-1 (one thread per column, written straight to global memory):
+  // X_jj = 1 / R_jj, X_ij = -(sum_{k=i+1..j} R_ik X_kj) / R_ii for i < j
+  for (int j = threadIdx.x; j < d; j += CT) {
+    double* X = Rinv + j;
+    for (int i = j + 1; i < d; i++) X[(size_t)i * d] = 0.0;
+    X[(size_t)j * d] = 1.0 / S[j * d + j];
+    for (int i = j - 1; i >= 0; i--) {
+      double a0 = 0.0, a1 = 0.0;
+      int k = i + 1;
+      for (; k + 2 <= j + 1; k += 2) {
+        a0 = fma(S[i * d + k], X[(size_t)k * d], a0);
+        a1 = fma(S[i * d + k + 1], X[(size_t)(k + 1) * d], a1);
+      }
+      for (; k <= j; k++) a0 = fma(S[i * d + k], X[(size_t)k * d], a0);
+      X[(size_t)i * d] = -(a0 + a1) / S[i * d + i];
+    }
+  }
 }
 
-// Row-wise triangular solve X = A R^-1 (R upper, d x d) for a tall A (n x d): 64 rows per CTA
-// staged through shared memory, one thread per row (forward substitution x_j = (a_j -
-// sum_{k<j} x_k R_kj) / R_jj).  Writes X (if given) and/or the squared row norms of X (scores).
-constexpr int TR_ROWS = 64;
-__global__ void __launch_bounds__(TR_ROWS) trsm_rows_kernel(const double* __restrict__ A, int64_t n, int d,
-                                                           const double* __restrict__ R, double* __restrict__ X,
-                                                           double* __restrict__ sq) {
+// X = A B for a tall A (n x d) and a small B (d x d): tm rows of A and all of B staged in shared
+// memory, every thread computes independent dot products.  Writes X (if given) and/or the
+// squared row norms of X (sq).
+__global__ void __launch_bounds__(CT) tallmm_kernel(const double* __restrict__ A, int64_t n, int d, int tm,
+                                                   const double* __restrict__ B, double* __restrict__ X,
+                                                   double* __restrict__ sq) {
   extern __shared__ double S[];
-  double* Rs = S;                          // d x d
-  double* As = Rs + (size_t)d * d;         // TR_ROWS x (d + 1)
+  double* Bs = S;                           // d x d
+  double* As = Bs + (size_t)d * d;          // tm x (d + 1)
+  double* Xs = As + (size_t)tm * (d + 1);   // tm x (d + 1)
   const int ld = d + 1;
-  const int64_t r0 = (int64_t)blockIdx.x * TR_ROWS;
-  const int rows = (int)ks_min64(TR_ROWS, n - r0);
-  for (int e = threadIdx.x; e < d * d; e += TR_ROWS) Rs[e] = R[e];
-  for (int e = threadIdx.x; e < rows * d; e += TR_ROWS) {
+  const int64_t r0 = (int64_t)blockIdx.x * tm;
+  const int rows = (int)ks_min64(tm, n - r0);
+  for (int e = threadIdx.x; e < d * d; e += CT) Bs[e] = B[e];
+  for (int e = threadIdx.x; e < rows * d; e += CT) {
     const int i = e / d, j = e - i * d;
     As[i * ld + j] = A[(r0 + i) * d + j];
   }
   __syncthreads();
-  if (threadIdx.x < rows) {
-    double* x = As + threadIdx.x * ld;  // solved in place
-    double s2 = 0.0;
-    for (int j = 0; j < d; j++) {
-      // four independent partial sums (the chain over k is latency-bound otherwise)
-      double a0 = x[j], a1 = 0.0, a2 = 0.0, a3 = 0.0;
-      int k = 0;
-      for (; k + 4 <= j; k += 4) {
-        a0 = fma(-x[k], Rs[k * d + j], a0);
-        a1 = fma(-x[k + 1], Rs[(k + 1) * d + j], a1);
-        a2 = fma(-x[k + 2], Rs[(k + 2) * d + j], a2);
-        a3 = fma(-x[k + 3], Rs[(k + 3) * d + j], a3);
-      }
-      for (; k < j; k++) a0 = fma(-x[k], Rs[k * d + j], a0);
-      const double acc = (a0 + a1) + (a2 + a3);
-      const double v = acc / Rs[j * d + j];
-      x[j] = v;
-      s2 = fma(v, v, s2);
+  for (int e = threadIdx.x; e < rows * d; e += CT) {
+    const int i = e / d, j = e - i * d;
+    const double* a = As + i * ld;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int k = 0;
+    for (; k + 4 <= d; k += 4) {
+      a0 = fma(a[k], Bs[k * d + j], a0);
+      a1 = fma(a[k + 1], Bs[(k + 1) * d + j], a1);
+      a2 = fma(a[k + 2], Bs[(k + 2) * d + j], a2);
+      a3 = fma(a[k + 3], Bs[(k + 3) * d + j], a3);
     }
-    if (sq) sq[r0 + threadIdx.x] = s2;
+    for (; k < d; k++) a0 = fma(a[k], Bs[k * d + j], a0);
+    const double v = (a0 + a1) + (a2 + a3);
+    if (X) X[(r0 + i) * d + j] = v;
+    Xs[i * ld + j] = v;
   }
+  if (!sq) return;
   __syncthreads();
-  if (X)
-    for (int e = threadIdx.x; e < rows * d; e += TR_ROWS) {
-      const int i = e / d, j = e - i * d;
-      X[(r0 + i) * d + j] = As[i * ld + j];
-    }
+  for (int i = threadIdx.x; i < rows; i += CT) {
+    double s2 = 0.0;
+    for (int j = 0; j < d; j++) s2 = fma(Xs[i * ld + j], Xs[i * ld + j], s2);
+    sq[r0 + i] = s2;
+  }
 }
 
-int chol_upper(cudaStream_t st, const double* G, int d, double* R, int32_t* info, int slot) {
-  const size_t smem = (size_t)d * d * sizeof(double);
+int chol_upper(cudaStream_t st, const double* G, int d, double* R, double* Rinv, int32_t* info, int slot) {
+  const size_t smem = (size_t)d * (d + 1) * sizeof(double);
   KS_TRY_CUDA(cudaFuncSetAttribute(chol_upper_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  chol_upper_kernel<<<1, CT, smem, st>>>(G, d, R, info, slot);
+  chol_upper_kernel<<<1, CT, smem, st>>>(G, d, R, Rinv, info, slot);
   KS_CHECK_LAUNCH();
   return KS_OK;
 }
 
-int trsm_rows(cudaStream_t st, const double* A, int64_t n, int d, const double* R, double* X, double* sq) {
-  const size_t smem = sizeof(double) * ((size_t)d * d + (size_t)TR_ROWS * (d + 1));
-  KS_REQUIRE(smem <= 227 * 1024, KS_ESIZE, "trsm_rows: d = %d too large", d);
-  KS_TRY_CUDA(cudaFuncSetAttribute(trsm_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  trsm_rows_kernel<<<ceil_div_u(n, TR_ROWS), TR_ROWS, smem, st>>>(A, n, d, R, X, sq);
+int tallmm(cudaStream_t st, const double* A, int64_t n, int d, const double* B, double* X, double* sq) {
+  const int tm = d > 64 ? 32 : 64;
+  const size_t smem = sizeof(double) * ((size_t)d * d + 2 * (size_t)tm * (d + 1));
+  KS_REQUIRE(smem <= 227 * 1024, KS_ESIZE, "tallmm: d = %d too large", d);
+  KS_TRY_CUDA(cudaFuncSetAttribute(tallmm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  tallmm_kernel<<<ceil_div_u(n, tm), CT, smem, st>>>(A, n, d, tm, B, X, sq);
   KS_CHECK_LAUNCH();
   return KS_OK;
 }
@@ -144,21 +158,42 @@ int trsm_rows(cudaStream_t st, const double* A, int64_t n, int d, const double* 
 
 namespace ks {
 
-// R (d x d, upper) of A (n x d) by CholeskyQR2.  *ok (host) = 1 on success, 0 if A is too
-// ill-conditioned for it (R is then undefined; use Householder).  Synchronises the stream.
-int chol_qr2_r(cudaStream_t st, const double* A, int64_t n, int d, double* R, int* ok) {
+// R (d x d, upper) of A (n x d) by CholeskyQR2, and R^-1 if Rinv is given.  *ok (host) = 1 on
+// success, 0 if A is too ill-conditioned (R undefined; use Householder).  Synchronises the stream.
+// Asynchronous form: info_dev (device, 2 x int32) receives the two factorisations' status words
+// (nonzero = CholeskyQR2 declined; R / Rinv are then undefined).
+int chol_qr2_r_async(cudaStream_t st, const double* A, int64_t n, int d, double* R, double* Rinv,
+                     int32_t* info_dev) {
   KS_REQUIRE(d >= 1 && d <= 128 && n >= d, KS_ESIZE, "chol_qr2 needs n >= d, d <= 128");
-  Scratch<double> G((int64_t)d * d, st), R1((int64_t)d * d, st), R2((int64_t)d * d, st), Q((int64_t)n * d, st);
-  Scratch<int32_t> info(2, st);
-  KS_REQUIRE(G.p && R1.p && R2.p && Q.p && info.p, KS_ECUDA, "scratch allocation failed");
+  Scratch<double> G((int64_t)d * d, st), R1((int64_t)d * d, st), R1i((int64_t)d * d, st), R2((int64_t)d * d, st),
+      R2i((int64_t)d * d, st), Q((int64_t)n * d, st);
+  KS_REQUIRE(G.p && R1.p && R1i.p && R2.p && R2i.p && Q.p, KS_ECUDA, "scratch allocation failed");
   int rc = gemm_tn_tall(st, d, d, n, 1.0, A, d, 1, A, d, 1, G.p);
   if (rc) return rc;
-  if ((rc = chol_upper(st, G.p, d, R1.p, info.p, 0))) return rc;
-  if ((rc = trsm_rows(st, A, n, d, R1.p, Q.p, nullptr))) return rc;
+  if ((rc = chol_upper(st, G.p, d, R1.p, R1i.p, info_dev, 0))) return rc;
+  if ((rc = tallmm(st, A, n, d, R1i.p, Q.p, nullptr))) return rc;  // Q1 = A R1^-1
   if ((rc = gemm_tn_tall(st, d, d, n, 1.0, Q.p, d, 1, Q.p, d, 1, G.p))) return rc;
-  if ((rc = chol_upper(st, G.p, d, R2.p, info.p, 1))) return rc;
-  // R = R2 R1 (both upper)
+  if ((rc = chol_upper(st, G.p, d, R2.p, Rinv ? R2i.p : nullptr, info_dev, 1))) return rc;
   if ((rc = gemm(st, d, d, d, 1.0, R2.p, d, 1, 0, R1.p, d, 1, 0, 0.0, R, d, 1, 0, 1))) return rc;
+  if (Rinv && (rc = gemm(st, d, d, d, 1.0, R1i.p, d, 1, 0, R2i.p, d, 1, 0, 0.0, Rinv, d, 1, 0, 1))) return rc;
+  return KS_OK;
+}
+
+int chol_qr2_r(cudaStream_t st, const double* A, int64_t n, int d, double* R, int* ok, double* Rinv) {
+  KS_REQUIRE(d >= 1 && d <= 128 && n >= d, KS_ESIZE, "chol_qr2 needs n >= d, d <= 128");
+  Scratch<double> G((int64_t)d * d, st), R1((int64_t)d * d, st), R1i((int64_t)d * d, st), R2((int64_t)d * d, st),
+      R2i((int64_t)d * d, st), Q((int64_t)n * d, st);
+  Scratch<int32_t> info(2, st);
+  KS_REQUIRE(G.p && R1.p && R1i.p && R2.p && R2i.p && Q.p && info.p, KS_ECUDA, "scratch allocation failed");
+  int rc = gemm_tn_tall(st, d, d, n, 1.0, A, d, 1, A, d, 1, G.p);
+  if (rc) return rc;
+  if ((rc = chol_upper(st, G.p, d, R1.p, R1i.p, info.p, 0))) return rc;
+  if ((rc = tallmm(st, A, n, d, R1i.p, Q.p, nullptr))) return rc;  // Q1 = A R1^-1
+  if ((rc = gemm_tn_tall(st, d, d, n, 1.0, Q.p, d, 1, Q.p, d, 1, G.p))) return rc;
+  if ((rc = chol_upper(st, G.p, d, R2.p, Rinv ? R2i.p : nullptr, info.p, 1))) return rc;
+  // R = R2 R1 and R^-1 = R1^-1 R2^-1 (all upper triangular)
+  if ((rc = gemm(st, d, d, d, 1.0, R2.p, d, 1, 0, R1.p, d, 1, 0, 0.0, R, d, 1, 0, 1))) return rc;
+  if (Rinv && (rc = gemm(st, d, d, d, 1.0, R1i.p, d, 1, 0, R2i.p, d, 1, 0, 0.0, Rinv, d, 1, 0, 1))) return rc;
   int32_t h[2];
   KS_TRY_CUDA(cudaMemcpyAsync(h, info.p, sizeof(h), cudaMemcpyDeviceToHost, st));
   KS_TRY_CUDA(cudaStreamSynchronize(st));
@@ -176,20 +211,34 @@ extern "C" int ks_leverage_scores_tall(const double* A, int64_t n, int32_t d, do
                                        void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   KS_REQUIRE(d >= 1 && d <= 128 && n >= d, KS_ESIZE, "leverage_scores_tall needs n >= d, 1 <= d <= 128");
-  ks::Scratch<double> R((int64_t)d * d, st);
-  KS_REQUIRE(R.p, KS_ECUDA, "scratch allocation failed");
+  ks::Scratch<double> R((int64_t)d * d, st), Ri((int64_t)d * d, st);
+  KS_REQUIRE(R.p && Ri.p, KS_ECUDA, "scratch allocation failed");
   int good = 0;
-  int rc = ks::chol_qr2_r(st, A, n, d, R.p, &good);
+  int rc = ks::chol_qr2_r(st, A, n, d, R.p, &good, Ri.p);
   if (rc) return rc;
   *ok = good;
   if (!good) return KS_OK;
-  return trsm_rows(st, A, n, d, R.p, nullptr, scores);
+  return tallmm(st, A, n, d, Ri.p, nullptr, scores);
 }
 
-// R factor by CholeskyQR2 (ok = 1) -- exported for tests and the compact SVD.
+// Asynchronous ks_leverage_scores_tall: no host round trip; info_dev (device, 2 x int32, zeroed by
+// the caller or not -- both words are written) nonzero = declined, scores undefined.
+extern "C" int ks_leverage_scores_tall_async(const double* A, int64_t n, int32_t d, double* scores, int32_t* info_dev,
+                                             void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  KS_REQUIRE(d >= 1 && d <= 128 && n >= d, KS_ESIZE, "leverage_scores_tall needs n >= d, 1 <= d <= 128");
+  ks::Scratch<double> R((int64_t)d * d, st), Ri((int64_t)d * d, st);
+  KS_REQUIRE(R.p && Ri.p, KS_ECUDA, "scratch allocation failed");
+  KS_TRY_CUDA(cudaMemsetAsync(Ri.p, 0, sizeof(double) * d * d, st));  // defined input if declined
+  int rc = ks::chol_qr2_r_async(st, A, n, d, R.p, Ri.p, info_dev);
+  if (rc) return rc;
+  return tallmm(st, A, n, d, Ri.p, nullptr, scores);
+}
+
+// R factor by CholeskyQR2 (ok = 1) -- exported for tests; ks_qr_r uses it internally.
 extern "C" int ks_chol_qr2_r(const double* A, int64_t n, int32_t d, double* R, int32_t* ok, void* stream) {
   int good = 0;
-  int rc = ks::chol_qr2_r((cudaStream_t)stream, A, n, d, R, &good);
+  int rc = ks::chol_qr2_r((cudaStream_t)stream, A, n, d, R, &good, nullptr);
   *ok = good;
   return rc;
 }

@@ -466,7 +466,7 @@ __global__ void inverse_small_kernel(const double* __restrict__ M, int d, double
 
 namespace ks {
 
-int chol_qr2_r(cudaStream_t st, const double* A, int64_t n, int d, double* R, int* ok);
+int chol_qr2_r(cudaStream_t st, const double* A, int64_t n, int d, double* R, int* ok, double* Rinv);
 
 int qr_r(cudaStream_t st, const double* A, int64_t n, int d, double* R) {
   KS_REQUIRE(d >= 1 && d <= 128, KS_ESIZE, "qr_r supports 1 <= d <= 128 (got %d)", d);
@@ -474,7 +474,7 @@ int qr_r(cudaStream_t st, const double* A, int64_t n, int d, double* R) {
   // ks_cholqr.cu); otherwise Householder TSQR below
   if (n >= 4 * (int64_t)d && !getenv("KS_TSQR")) {
     int ok = 0;
-    int rc = chol_qr2_r(st, A, n, d, R, &ok);
+    int rc = chol_qr2_r(st, A, n, d, R, &ok, nullptr);
     if (rc) return rc;
     if (ok) return KS_OK;
   }

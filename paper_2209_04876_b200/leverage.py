@@ -256,11 +256,14 @@ def _tables(scores: torch.Tensor, renorm: bool, want_cdf: bool = True, what: str
     flags = torch.zeros(1, dtype=torch.int32, device=scores.device)
     _lib.call("ks_sampler_tables", D.p(scores), n, 1 if renorm else 0, D.p(probs), D.p(cdf), D.p(flags),
               D.stream())
-    f = int(flags.item())
-    if f & 1:
-        raise InvalidInputError(f"{what} must be nonnegative finite")
-    if f & 2:
-        raise InvalidInputError(f"{what} sums to zero")
+
+    def handler(v):
+        if v[0] & 1:
+            raise InvalidInputError(f"{what} must be nonnegative finite")
+        if v[0] & 2:
+            raise InvalidInputError(f"{what} sums to zero")
+
+    check_later(flags, handler)  # immediate outside a fast solve, deferred inside one
     return probs, cdf
 
 
@@ -390,12 +393,29 @@ def sample_rows(sampler, s: int, seed) -> RowSketch:
     return RowSketch(indices=D.out(idx, host), weights=D.out(w, host))
 
 
-def _statistical_scores_dev(a: torch.Tensor) -> torch.Tensor:
+class ScoresFallback(Exception):
+    """CholeskyQR2 declined (ill-conditioned factor): redo the solve with the compact-SVD scores."""
+
+
+def _scores_status(v):
+    if v[0] or v[1]:
+        raise ScoresFallback()
+
+
+def _statistical_scores_dev(a: torch.Tensor, fast: bool = True) -> torch.Tensor:
     """ridge_leverage_scores(compact_svd(a), 0).scores: for a tall, numerically full-rank a the
-    squared row norms of a R^-1 (CholeskyQR2 R, one fused pass); otherwise the compact SVD."""
+    squared row norms of a R^-1 (CholeskyQR2 R, one fused pass); otherwise the compact SVD.
+    Inside a fast solve (deferred checks active) the CholeskyQR2 path is asynchronous and a
+    declined factorisation raises ScoresFallback at the end of the solve (which is then redone with
+    fast=False)."""
     n, d = int(a.shape[0]), int(a.shape[1])
-    if n >= 4 * d and d <= 128:
+    if fast and n >= 4 * d and d <= 128:
         sc = D.empty(n)
+        if _DEFERRED[0] is not None:
+            info = torch.zeros(2, dtype=torch.int32, device=a.device)
+            _lib.call("ks_leverage_scores_tall_async", D.p(a.contiguous()), n, d, D.p(sc), D.p(info), D.stream())
+            check_later(info, _scores_status)
+            return sc
         ok = ctypes.c_int32(0)
         _lib.call("ks_leverage_scores_tall", D.p(a.contiguous()), n, d, D.p(sc), ctypes.byref(ok), D.stream())
         if ok.value:
@@ -403,8 +423,9 @@ def _statistical_scores_dev(a: torch.Tensor) -> torch.Tensor:
     return ridge_leverage_scores(compact_svd(a), 0.0).scores
 
 
-def _spectral_rows_dev(a: torch.Tensor, eps: float, delta: float, seed, alpha: float) -> torch.Tensor:
-    sc = _statistical_scores_dev(a)
+def _spectral_rows_dev(a: torch.Tensor, eps: float, delta: float, seed, alpha: float,
+                       fast_scores: bool = True) -> torch.Tensor:
+    sc = _statistical_scores_dev(a, fast_scores)
     p1, _ = _tables(D.to_dev(sc), renorm=False, want_cdf=False, what="score vector")
     s = max(1, math.ceil(alpha * spectral_sample_count(int(a.shape[1]), eps, delta)))
     sk = sample_rows(p1, s, seed)

@@ -638,27 +638,33 @@ def _fast_solve_dev(facs, b, config: RegressionConfig, caches, trace: FastSolveT
         got = _fast_solve_graph(facs, b, config)
         if got is not None:
             return got
-    for use_chol in (True, False):
+    use_chol, fast_scores = True, True
+    for _attempt in range(3):
         deferred = _lev.DeferredChecks()
         _lev._DEFERRED[0] = deferred
-        retry = False
+        failure = None
         try:
-            return _fast_solve_pass(facs, b, config, caches, trace, use_chol, deferred)
-        except _CholeskyFailed:
-            retry = True
+            return _fast_solve_pass(facs, b, config, caches, trace, use_chol, deferred, fast_scores)
+        except (_CholeskyFailed, _lev.ScoresFallback) as exc:
+            failure = exc
         except Exception:
             # a pending device flag (invalid scores, generator failure) explains a later error
             # better: raise the reference's exception for it first
             _lev._DEFERRED[0] = None
             try:
                 deferred.run()
-            except _CholeskyFailed:
-                retry = True
-            if not retry:
+            except (_CholeskyFailed, _lev.ScoresFallback) as exc:
+                failure = exc
+            if failure is None:
                 raise
         finally:
             _lev._DEFERRED[0] = None
-        assert retry and use_chol
+        if isinstance(failure, _CholeskyFailed):
+            assert use_chol
+            use_chol = False
+        else:
+            assert fast_scores
+            fast_scores = False
     raise AssertionError("unreachable")
 
 
@@ -797,7 +803,8 @@ def _mark(name: str):
         _PHASES.append((name, time.perf_counter(), ev))
 
 
-def _fast_solve_pass(facs, b, config: RegressionConfig, caches, trace, use_chol: bool, deferred):
+def _fast_solve_pass(facs, b, config: RegressionConfig, caches, trace, use_chol: bool, deferred,
+                     fast_scores: bool = True):
     from . import leverage as _lev
     _mark("start")
     n_factors = len(facs)
@@ -823,16 +830,29 @@ def _fast_solve_pass(facs, b, config: RegressionConfig, caches, trace, use_chol:
         delta_n = config.delta / (2.0 * n_factors)
         eps_jl = 4.0 * math.log1p(config.eps / 4.0) / n_factors
         tildes = []
+        # per-factor spectral row sampling (leverage.py:235-252) is independent across factors:
+        # factor n > 0 runs on its own stream (no host round trip inside; joined below)
+        main = torch.cuda.current_stream()
+        spectral = [math.ceil(alpha * spectral_sample_count(int(a.shape[1]), eps_two, delta_n)) < int(a.shape[0])
+                    for a in facs]
+        for n in range(1, n_factors):
+            if spectral[n]:
+                _side_stream(n).wait_stream(main)
         for n, a in enumerate(facs):
-            s_n = math.ceil(alpha * spectral_sample_count(int(a.shape[1]), eps_two, delta_n))
-            if s_n >= int(a.shape[0]):
+            if not spectral[n]:
                 a_tilde = a
             else:
-                a_tilde = (_spectral_rows_dev(a, eps_two, delta_n, seeds[2 * n], alpha)
-                           / math.sqrt(1.0 - eps_two)).contiguous()
+                with torch.cuda.stream(main if n == 0 else _side_stream(n)):
+                    a_tilde = (_spectral_rows_dev(a, eps_two, delta_n, seeds[2 * n], alpha, fast_scores)
+                               / math.sqrt(1.0 - eps_two)).contiguous()
+                if n > 0:
+                    a_tilde.record_stream(main)
             if trace is not None:
                 trace.a_tilde_rows.append(int(a_tilde.shape[0]))
             tildes.append(a_tilde)
+        for n in range(1, n_factors):
+            if spectral[n]:
+                main.wait_stream(_side_stream(n))
         key = _prefix_key(facs, tildes, config, use_chol) if trace is None else None
         entry = _PREFIX_GRAPHS.get(key) if key is not None else None
         gts = [_gram_dev(t, out=entry.gts[n] if entry is not None and entry.gts is not None else None)

@@ -139,3 +139,34 @@ def test_inverse_small(rng):
         np.testing.assert_allclose(x @ m, np.eye(d), atol=1e-11)
     with pytest.raises(NumericalFailureError):
         _inverse_small(D.to_dev(np.zeros((2, 2))))
+
+
+@pytest.mark.parametrize("n,d", [(4096, 16), (65536, 64), (20000, 128)])
+def test_cholqr2_and_leverage_scores_tall(n, d):
+    """CholeskyQR2 R (R^T R = A^T A, up to row signs the Householder R) and the fused leverage
+    scores ||(A R^-1)_i||^2 against NumPy's QR / the oracle's compact-SVD scores."""
+    import ctypes
+    import torch
+    from paper_2209_04876_b200 import _device as D, _lib
+    from oracle import kronsolve_oracle as O
+    rng = np.random.default_rng(n + d)
+    a = rng.normal(1.0, np.sqrt(1e-3), (n, d))
+    at = torch.tensor(a, device="cuda")
+    r = D.empty(d, d)
+    ok = ctypes.c_int32(0)
+    _lib.call("ks_chol_qr2_r", D.p(at), n, d, D.p(r), ctypes.byref(ok), D.stream())
+    assert ok.value == 1
+    rr = r.cpu().numpy()
+    _, rq = np.linalg.qr(a)
+    signs = np.sign(np.diag(rq))
+    np.testing.assert_allclose(rr, signs[:, None] * rq, rtol=1e-10, atol=1e-10 * np.abs(rq).max())
+    sc = D.empty(n)
+    _lib.call("ks_leverage_scores_tall", D.p(at), n, d, D.p(sc), ctypes.byref(ok), D.stream())
+    assert ok.value == 1
+    want = O.ridge_scores(O.compact_svd(a), 0.0)
+    np.testing.assert_allclose(sc.cpu().numpy(), want, rtol=1e-10)
+    # rank-deficient input: CholeskyQR2 declines, callers fall back to Householder / the SVD
+    a[:, 1] = a[:, 0]
+    _lib.call("ks_leverage_scores_tall", D.p(torch.tensor(a, device="cuda")), n, d, D.p(sc), ctypes.byref(ok),
+              D.stream())
+    assert ok.value == 0

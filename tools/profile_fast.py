@@ -22,10 +22,14 @@ from paper_2209_04876_b200.solvers import FastSolveTrace  # noqa: E402
 args = [a for a in sys.argv[1:] if not a.startswith("--")]
 name = args[0] if args else "c3"
 reps = int(args[1]) if len(args) > 1 else 1
-n, d = {"c1": (1024, 16), "c2": (4096, 32), "c3": (16384, 64)}[name]
+n, d = {"c1": (1024, 16), "c2": (4096, 32), "c3": (16384, 64), "c4": (65536, 64), "c4d32": (65536, 32)}[name]
 rng = np.random.default_rng(0)
 facs = [torch.tensor(rng.normal(1.0, math.sqrt(1e-3), (n, d)), device="cuda") for _ in range(2)]
-b = torch.ones(n * n, dtype=torch.float64, device="cuda")
+if name.startswith("c4"):
+    from paper_2209_04876_b200.leverage import device_standard_normal
+    b = device_standard_normal(0, n * n)
+else:
+    b = torch.ones(n * n, dtype=torch.float64, device="cuda")
 cfg = K.RegressionConfig(eps=0.1, delta=0.01, lam=1e-3, alpha=1e-5, seed=0)
 walls = []
 for _ in range(reps):
