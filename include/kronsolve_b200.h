@@ -297,6 +297,8 @@ int ks_debug_jacobi_sweeps(int32_t* out8);
 /* Profiling aid: CTA 0 / thread 0 cycles of the last fixed-size one-sided Jacobi launch, summed
  * over rounds: (load + dot products + reductions, rotation + update, barrier, rounds); reset on read. */
 int ks_debug_jacobi_stamps(long long* out4);
+/* Profiling aid: cycles of the FP32 prelude, its FP64 transition and the FP64 rounds (CTA 0). */
+int ks_debug_jacobi_mix(long long* out3);
 
 /* Profiling aid: average SM cycles per phase of the last persistent Richardson run (CTA 0):
  * apply, sync, reduce, precond-A, precond-B, update. */
