@@ -142,3 +142,69 @@ def expected_allreduce_bytes(d1: int, d2: int, iterations: int) -> int:
     """Bytes each rank contributes to collectives in one sharded fast solve (rhs + one Gram partial
     per iteration), for reporting."""
     return 8 * d1 * d2 * (iterations + 1) + 8 * math.prod((1,))
+
+
+# ---------------------------------------------------------------------------
+# Device execution (NCCL): the exact solve and the loss on row-sharded b
+# ---------------------------------------------------------------------------
+
+class DeviceKron2Ops:
+    """Local compute of ShardedKron2 on the GPU: the K1 contraction (ks_kron2_contract) and the K2
+    residual pass (ks_kron2_residual_sumsq) on this rank's row block."""
+
+    def __init__(self):
+        import torch
+        from . import _device as D
+        self.torch, self.D = torch, D
+        self.device = D.dev()
+
+    def contract(self, L_rows, B_rows, R):
+        from . import _lib
+        D = self.D
+        m, p = int(L_rows.shape[0]), int(L_rows.shape[1])
+        k, q = int(R.shape[0]), int(R.shape[1])
+        T = D.empty(p, q)
+        if m == 0:
+            return T.zero_()
+        _lib.call("ks_kron2_contract", D.p(L_rows.contiguous()), D.p(B_rows), int(B_rows.stride(0)), D.p(R), m, k, p,
+                  q, D.p(T), D.stream())
+        return T
+
+    def resid(self, L_rows, X, R, B_rows):
+        from . import _lib
+        D = self.D
+        out = D.zeros(1)
+        m = int(L_rows.shape[0])
+        if m:
+            _lib.call("ks_kron2_residual_sumsq", D.p(L_rows.contiguous()), D.p(X.contiguous()), D.p(R), D.p(B_rows),
+                      int(B_rows.stride(0)), m, int(R.shape[0]), int(L_rows.shape[1]), int(R.shape[1]), D.p(out),
+                      D.stream())
+        return float(out.item())
+
+
+def sharded_kronmatmul_svd_solve(factors, b_rows, lam: float, plan: ShardPlan, dist=None):
+    """kronmatmul_svd_solve (solvers.py:302-320) with b row-sharded over the ranks:
+    every rank holds both (small) factors and its rows [lo, hi) of the n1 x n2 reshape of b
+    (``b_rows``, device, (hi - lo) x n2).  The compact SVDs are replicated, the n^2 contraction
+    U1[lo:hi]^T B_rows U2 runs locally on the FP64 tensor pipe, one d1*d2 all-reduce combines it,
+    and x = (V1 (x) V2) (sigma / (sigma^2 + lam)) t is replicated.  Returns (x, loss): the loss is
+    the sharded K2 pass plus one scalar all-reduce."""
+    import torch
+    from functools import reduce as _reduce
+    from . import _device as D
+    from .kron import _kron_apply_dev
+    from .tensor import _compact_svd_dev
+    facs = [D.to_dev(a) for a in factors]
+    if len(facs) != 2:
+        raise ValueError("the row-sharded exact solve covers the two-factor problem")
+    lo, hi = plan.rows
+    svds = [_compact_svd_dev(a, 1e-10) for a in facs]
+    ops = DeviceKron2Ops()
+    sk = ShardedKron2(plan, ops, torch)
+    T = sk.contract(svds[0][0], b_rows, svds[1][0].contiguous())
+    sigma = _reduce(torch.kron, [s[1] for s in svds])
+    t = T.reshape(-1) * (sigma / (sigma * sigma + lam))
+    x = _kron_apply_dev([s[2] for s in svds], t.reshape(-1, 1).contiguous())[:, 0].contiguous()
+    X = x.reshape(int(facs[0].shape[1]), int(facs[1].shape[1]))
+    r2 = sk.residual_sumsq(facs[0], X, facs[1], b_rows)
+    return x, r2 + lam * float((x * x).sum().item())
