@@ -32,7 +32,7 @@ constexpr int CT = 256;
 __global__ void __launch_bounds__(CT) chol_upper_kernel(const double* __restrict__ G, int d, double* __restrict__ R,
                                                        double* __restrict__ Rinv, int32_t* __restrict__ info,
                                                        int slot) {
-  extern __shared__ double S[];      // d x d (row-major, upper triangle used), then row k
+  extern __shared__ double S[];      // d x d (row-major, upper triangle used), then row k / packed R^-1
   double* W = S + (size_t)d * d;
   __shared__ int s_bad;
   __shared__ double s_dmax;
@@ -73,22 +73,27 @@ __global__ void __launch_bounds__(CT) chol_upper_kernel(const double* __restrict
     R[e] = i <= j ? S[e] : 0.0;
   }
   if (!Rinv || bad) return;
-  // column j of R^-1 (one thread per column, written straight to global memory):
-  // X_jj = 1 / R_jj, X_ij = -(sum_{k=i+1..j} R_ik X_kj) / R_ii for i < j
+  // column j of R^-1 (one thread per column) in packed upper-triangular shared memory after S:
+  // X_jj = 1 / R_jj, X_ij = -(sum_{k=i+1..j} R_ik X_kj) / R_ii for i < j; X(k, j) at P[k d - k(k-1)/2 + j - k]
+  double* P = S + (size_t)d * d;
+  auto po = [d](int k, int j) { return k * d - (k * (k - 1)) / 2 + (j - k); };
   for (int j = threadIdx.x; j < d; j += CT) {
-    double* X = Rinv + j;
-    for (int i = j + 1; i < d; i++) X[(size_t)i * d] = 0.0;
-    X[(size_t)j * d] = 1.0 / S[j * d + j];
+    P[po(j, j)] = 1.0 / S[j * d + j];
     for (int i = j - 1; i >= 0; i--) {
       double a0 = 0.0, a1 = 0.0;
       int k = i + 1;
       for (; k + 2 <= j + 1; k += 2) {
-        a0 = fma(S[i * d + k], X[(size_t)k * d], a0);
-        a1 = fma(S[i * d + k + 1], X[(size_t)(k + 1) * d], a1);
+        a0 = fma(S[i * d + k], P[po(k, j)], a0);
+        a1 = fma(S[i * d + k + 1], P[po(k + 1, j)], a1);
       }
-      for (; k <= j; k++) a0 = fma(S[i * d + k], X[(size_t)k * d], a0);
-      X[(size_t)i * d] = -(a0 + a1) / S[i * d + i];
+      for (; k <= j; k++) a0 = fma(S[i * d + k], P[po(k, j)], a0);
+      P[po(i, j)] = -(a0 + a1) / S[i * d + i];
     }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < d * d; e += CT) {
+    const int i = e / d, j = e - i * d;
+    Rinv[e] = i <= j ? P[po(i, j)] : 0.0;
   }
 }
 
@@ -137,7 +142,7 @@ __global__ void __launch_bounds__(CT) tallmm_kernel(const double* __restrict__ A
 }
 
 int chol_upper(cudaStream_t st, const double* G, int d, double* R, double* Rinv, int32_t* info, int slot) {
-  const size_t smem = (size_t)d * (d + 1) * sizeof(double);
+  const size_t smem = ((size_t)d * d + (size_t)d * (d + 1) / 2 + d) * sizeof(double);
   KS_TRY_CUDA(cudaFuncSetAttribute(chol_upper_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   chol_upper_kernel<<<1, CT, smem, st>>>(G, d, R, Rinv, info, slot);
   KS_CHECK_LAUNCH();

@@ -40,6 +40,26 @@ struct LoopState {
   double tol;
 };
 
+// Two-level fixed-order reduction of the block partials (deterministic): split s of gridDim.y sums
+// partials [s*per, (s+1)*per) with Neumaier compensation into part2[s]; residual_kernel then sums
+// the splits in order.  (One level over ~2000 partials of d^2 = 16384 doubles is a latency-bound
+// chain per thread.)
+__global__ void partial_split_kernel(const double* __restrict__ part, int64_t nparts, int64_t per, int64_t count,
+                                     double* __restrict__ part2, const LoopState* __restrict__ ls) {
+  if (ls && ls->status != ST_RUNNING) return;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= count) return;
+  const int64_t p0 = (int64_t)blockIdx.y * per, p1 = ks_min64(nparts, p0 + per);
+  double s = 0.0, c = 0.0;
+  for (int64_t p = p0; p < p1; p++) {
+    const double v = part[p * count + e];
+    const double t = s + v;
+    c += (fabs(s) >= fabs(v)) ? ((s - t) + v) : ((v - t) + s);
+    s = t;
+  }
+  part2[(int64_t)blockIdx.y * count + e] = s + c;
+}
+
 // R = sum_p part[p] + lam X - rhs
 __global__ void residual_kernel(const double* __restrict__ part, int64_t nparts, int64_t count,
                                 const double* __restrict__ X, double lam,
@@ -220,10 +240,10 @@ extern "C" int ks_richardson_sketched(const ks_sketch_view* sk, const double* VL
   }
   const int64_t count = (int64_t)dL * dR;
   const int64_t np = ks::sketched_partials_count(sk);
-  ks::Scratch<double> part(np * count + 1, st), R(count, st), T(count, st), step(count, st);
+  ks::Scratch<double> part(np * count + 1, st), part2(32 * count, st), R(count, st), T(count, st), step(count, st);
   ks::Scratch<double> rowsq(dL, st), VRt((int64_t)dR * dR, st);
   ks::Scratch<LoopState> ls(1, st);
-  KS_REQUIRE(part.p && R.p && T.p && step.p && rowsq.p && VRt.p && ls.p, KS_ECUDA,
+  KS_REQUIRE(part.p && part2.p && R.p && T.p && step.p && rowsq.p && VRt.p && ls.p, KS_ECUDA,
              "scratch allocation failed");
   transpose_sq_kernel<<<ceil_div_u((int64_t)dR * dR, 256), 256, 0, st>>>(VR, dR, VRt.p);
   KS_CHECK_LAUNCH();
@@ -236,7 +256,15 @@ extern "C" int ks_richardson_sketched(const ks_sketch_view* sk, const double* VL
     int64_t nb = 0;
     rc = ks::sketched_gram_partials(st, sk, x, nullptr, nullptr, 1, part.p, &nb);
     if (rc) return rc;
-    residual_kernel<<<ceil_div_u(count, 256), 256, 0, st>>>(part.p, nb, count, x, lam, rhs, R.p, ls.p);
+    if (nb > 64) {  // two levels: 32 splits, then the splits in order
+      const int64_t per = (nb + 31) / 32, ns = (nb + per - 1) / per;
+      partial_split_kernel<<<dim3(ceil_div_u(count, 256), (unsigned)ns), 256, 0, st>>>(part.p, nb, per, count,
+                                                                                       part2.p, ls.p);
+      KS_CHECK_LAUNCH();
+      residual_kernel<<<ceil_div_u(count, 256), 256, 0, st>>>(part2.p, ns, count, x, lam, rhs, R.p, ls.p);
+    } else {
+      residual_kernel<<<ceil_div_u(count, 256), 256, 0, st>>>(part.p, nb, count, x, lam, rhs, R.p, ls.p);
+    }
     KS_CHECK_LAUNCH();
     rc = ks::precond_apply(st, VL, VR, VRt.p, dL, dR, dinv, R.p, T.p, step.p, rowsq.p, ls.p);
     if (rc) return rc;
