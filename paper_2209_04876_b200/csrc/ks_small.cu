@@ -205,9 +205,10 @@ __global__ void jacobi_svd_kernel(const double* __restrict__ M, int d, double* _
   __syncthreads();
   for (int j = tid; j < d; j += nt) {
     int rank = 0;
-    const double sj = s_norm[j];
+    // total order even for non-finite input (NaN ranks last): every rank is assigned exactly once
+    const double sj = isnan(s_norm[j]) ? -1.0 : s_norm[j];
     for (int k = 0; k < d; k++) {
-      const double sk = s_norm[k];
+      const double sk = isnan(s_norm[k]) ? -1.0 : s_norm[k];
       rank += (sk > sj) || (sk == sj && k < j);
     }
     s_order[rank] = j;
@@ -492,9 +493,10 @@ __global__ void __launch_bounds__(D / 2 * JF_G) jacobi_fixed_kernel(MatPtrs Ms, 
   __syncthreads();
   for (int j = tid; j < D; j += NT) {
     int rank = 0;
-    const double sj = s_norm[j];
+    // total order even for non-finite input (NaN ranks last): every rank is assigned exactly once
+    const double sj = isnan(s_norm[j]) ? -1.0 : s_norm[j];
     for (int k = 0; k < D; k++) {
-      const double sk = s_norm[k];
+      const double sk = isnan(s_norm[k]) ? -1.0 : s_norm[k];
       rank += (sk > sj) || (sk == sj && k < j);
     }
     s_order[rank] = j;

@@ -407,6 +407,11 @@ def _factor_grams_async(gts: list[torch.Tensor]):
 def _join_grams(handle):
     if isinstance(handle, list):
         return handle
+    if handle[0] == "per-factor":
+        _, outs, evs = handle
+        for ev in evs:
+            torch.cuda.current_stream().wait_event(ev)
+        return outs
     outs, ev, keep = handle
     torch.cuda.current_stream().wait_event(ev)
     if not torch.cuda.is_current_stream_capturing():
@@ -531,21 +536,54 @@ def _solve_graph_key(facs, b, config: RegressionConfig):
     return key
 
 
-def _solve_graph_body(facs, b, config: RegressionConfig, s: int):
-    """Launch-only device pipeline of the fused two-factor solve (captured once per key)."""
+def _eig_on(stream, g):
+    d = int(g.shape[0])
+    w = D.empty(1, d)
+    v = D.empty(1, d, d)
+    with torch.cuda.stream(stream):
+        _lib.call("ks_sym_eig_batched", 1, _lib.ptr_array(ctypes.c_void_p, [g.data_ptr()]), d, D.p(w), D.p(v),
+                  D.stream())
+    ev = torch.cuda.Event()
+    ev.record(stream)
+    return (v[0], w[0]), ev
+
+
+def _solve_graph_body(facs, b, config: RegressionConfig, s: int, factor1_stream=None):
+    """Launch-only device pipeline of the fused two-factor solve (captured once per key).
+
+    ``factor1_stream``: the stream on which facs[1] becomes ready (its upload, when the graph also
+    holds the host-to-device copies); then factor 1's Gram, eigensolve and JL chain start as soon
+    as it lands, while factor 0's already run (per-factor eigensolve launches instead of the batched
+    one)."""
     seeds = _spawned_seeds(config.seed, 5)
     eps_jl = 4.0 * math.log1p(config.eps / 4.0) / 2
     d0, d1 = int(facs[0].shape[1]), int(facs[1].shape[1])
     main = torch.cuda.current_stream()
-    gside = _side_stream(8)
-    gside.wait_stream(main)
-    g0 = _gram_dev(facs[0])
-    with torch.cuda.stream(gside):  # the two Grams concurrently
-        g1 = _gram_dev(facs[1])
-    main.wait_stream(gside)
-    gts = [g0, g1]
-    grams_h = _factor_grams_async(gts)
-    _, _, _, _, _, g2 = _jl_and_sampling(facs, facs, gts, eps_jl, config, True, seeds, s)
+    ready = None
+    if factor1_stream is None:
+        gside = _side_stream(8)
+        gside.wait_stream(main)
+        g0 = _gram_dev(facs[0])
+        with torch.cuda.stream(gside):  # the two Grams concurrently
+            g1 = _gram_dev(facs[1])
+        main.wait_stream(gside)
+        gts = [g0, g1]
+        grams_h = _factor_grams_async(gts)
+    else:
+        g0 = _gram_dev(facs[0])
+        with torch.cuda.stream(factor1_stream):
+            g1 = _gram_dev(facs[1])
+        ev1 = torch.cuda.Event()
+        ev1.record(factor1_stream)
+        gts = [g0, g1]
+        e0s, e1s = _side_stream(0), _side_stream(10)
+        e0s.wait_stream(main)
+        e1s.wait_event(ev1)
+        r0, ev_e0 = _eig_on(e0s, g0)
+        r1, ev_e1 = _eig_on(e1s, g1)
+        grams_h = ("per-factor", [r0, r1], [ev_e0, ev_e1])
+        ready = [None, ev1]
+    _, _, _, _, _, g2 = _jl_and_sampling(facs, facs, gts, eps_jl, config, True, seeds, s, ready)
     sd_idx, sd_val, seg, lrow, rrow, cdev = g2
     b_at = D.empty(s)
     _lib.call("ks_gather_count", D.p(b), D.p(sd_idx), D.p(cdev), s, D.p(b_at), D.stream())
@@ -631,6 +669,145 @@ def _fast_solve_graph(facs, b, config: RegressionConfig):
     return x, iters, s
 
 
+class _HostFacsGraph:
+    """Whole-solve graph for page-locked HOST factors: the factor uploads and their validation are
+    graph nodes too, so the upload of factor 1 overlaps factor 0's Gram / eigensolve / JL chain."""
+
+    def __init__(self):
+        self.graph = None
+        self.dev = None
+        self.flags = None
+        self.out = None
+        self.checks = []
+
+
+_HOST_GRAPHS: dict = {}
+
+
+def _host_graph_key(factors, b, config: RegressionConfig):
+    if not (_USE_SOLVE_GRAPH[0] and _USE_GRAPHS[0] and _USE_FUSED[0]) or len(factors) != 2:
+        return None
+    for a in factors:
+        if not (isinstance(a, torch.Tensor) and not a.is_cuda and a.dtype == torch.float64 and a.ndim == 2
+                and a.is_contiguous() and a.is_pinned()):
+            return None
+    if not (isinstance(b, torch.Tensor) and b.dtype == torch.float64 and b.is_contiguous()
+            and (b.is_cuda or b.is_pinned())):
+        return None
+    rows = math.prod(int(a.shape[0]) for a in factors)
+    if int(b.numel()) != rows:
+        return None  # the regular path raises the reference's error
+    eps_one = math.log1p(config.eps / 4.0) / 2
+    eps_two = eps_one / (2.0 + eps_one)
+    delta_n = config.delta / 4.0
+    for a in factors:
+        n, d = int(a.shape[0]), int(a.shape[1])
+        if d not in (16, 32, 64) or n < 16 or \
+                math.ceil(config.effective_alpha * spectral_sample_count(d, eps_two, delta_n)) < n:
+            return None
+    if config.effective_max_iters > 1024:
+        return None
+    s = _regression_sample_count(math.prod(int(a.shape[1]) for a in factors), config)
+    if s >= rows:
+        return None
+    try:
+        key = ("host", torch.cuda.current_device(), torch.cuda.current_stream().cuda_stream,
+               tuple((a.data_ptr(), tuple(a.shape)) for a in factors), (b.data_ptr(), b.numel(), b.is_cuda), config)
+        hash(key)
+    except TypeError:
+        return None
+    return key
+
+
+def _validation_handler(nf: int):
+    def handler(v):
+        for n in range(nf):
+            if v[2 * n]:
+                raise InvalidInputError(f"factor {n} contains non-finite entries")
+        for n in range(nf):
+            if not v[2 * n + 1]:
+                raise InvalidInputError(f"factor {n} is identically zero")
+    return handler
+
+
+def _fast_solve_host_graph(factors, b, config: RegressionConfig, with_loss: bool):
+    """fast_kronecker_regression for page-locked host factors from one graph replay (uploads,
+    validation, the whole solve), or None (first sight of the key / ineligible / LU retry needed)."""
+    from . import leverage as _lev
+    if not 0.0 < config.eps <= 0.25:
+        return None
+    key = _host_graph_key(factors, b, config)
+    if key is None:
+        return None
+    entry = _HOST_GRAPHS.get(key)
+    if entry is None:
+        if len(_HOST_GRAPHS) >= 4:
+            _HOST_GRAPHS.pop(next(iter(_HOST_GRAPHS)))
+        _HOST_GRAPHS[key] = _HostFacsGraph()
+        return None
+    s = _regression_sample_count(math.prod(int(a.shape[1]) for a in factors), config)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    _mark("t0")
+    if entry.graph is None:
+        entry.dev = [D.empty(*a.shape) for a in factors]
+        entry.flags = torch.zeros(len(factors), 2, dtype=torch.int32, device=D.dev())
+        g = torch.cuda.CUDAGraph()
+        cap = _lev.DeferredChecks()
+        outer = _lev._DEFERRED[0]
+        _lev._DEFERRED[0] = cap
+        try:
+            with torch.cuda.graph(g):
+                main = torch.cuda.current_stream()
+                side = _side_stream(9)
+                entry.dev[0].copy_(factors[0], non_blocking=True)
+                side.wait_stream(main)  # after factor 0's upload: the PCIe link serves one copy at a time
+                with torch.cuda.stream(side):
+                    entry.dev[1].copy_(factors[1], non_blocking=True)
+                    _lib.call("ks_check_finite_nonzero", D.p(entry.dev[1]), entry.dev[1].numel(),
+                              D.p(entry.flags[1]), D.stream())
+                _lib.call("ks_check_finite_nonzero", D.p(entry.dev[0]), entry.dev[0].numel(), D.p(entry.flags[0]),
+                          D.stream())
+                entry.out = _solve_graph_body(entry.dev, b.reshape(-1), config, s, factor1_stream=side)
+                main.wait_stream(side)
+        except Exception:
+            _HOST_GRAPHS.pop(key, None)
+            raise
+        finally:
+            _lev._DEFERRED[0] = outer
+        entry.graph, entry.checks = g, cap.items
+    _mark("graph launch")
+    _LAST_LOOP_EVENTS[0] = entry.out["loop_events"]
+    entry.graph.replay()
+    out = entry.out
+    deferred = _lev.DeferredChecks()
+    deferred.add(entry.flags.reshape(-1), _validation_handler(len(factors)))  # the reference validates first
+    for flags, handler in entry.checks:
+        deferred.add(flags, handler)
+    deferred.stage()
+    st_h = out["state"].to("cpu", non_blocking=True)
+    hist_h = out["hist"].to("cpu", non_blocking=True)
+    x_h = out["x"].reshape(-1).to("cpu", non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    _mark("richardson")
+    try:
+        deferred.run(synced=True)
+    except _CholeskyFailed:
+        return None  # the regular path retries with LU inverses
+    status, iters, hlen = (int(v) for v in st_h[:3].tolist())
+    if status == 2:
+        raise NumericalFailureError("Richardson iteration diverged", iterations=iters,
+                                    diagnostics={"residual_history": hist_h[:hlen].tolist()})
+    _mark("solve_end")
+    wall = time.perf_counter() - t0
+    if with_loss:
+        x = out["x"].reshape(-1).clone()
+        loss = _ridge_loss_dev(entry.dev, x, D.to_dev(b).reshape(-1), config.lam)
+    else:
+        loss = float("nan")
+    return SolveReport(solution=x_h.numpy().copy(), loss=loss, iterations=iters, sample_count=s, wall_time=wall)
+
+
 def _fast_solve_dev(facs, b, config: RegressionConfig, caches, trace: FastSolveTrace | None = None):
     """The device pipeline of solvers.py:404-459; returns (x natural order, iterations, s)."""
     from . import leverage as _lev
@@ -685,7 +862,8 @@ def _spawned_seeds(seed, count: int):
     return np.random.SeedSequence(seed).spawn(count)
 
 
-def _jl_and_sampling(facs, tildes, gts, eps_jl: float, config: RegressionConfig, use_chol: bool, seeds, s: int):
+def _jl_and_sampling(facs, tildes, gts, eps_jl: float, config: RegressionConfig, use_chol: bool, seeds, s: int,
+                     ready=None):
     """JL leverage estimates of every factor (leverage.py:85-130), the product sampler's tables
     and the s draws with their weights (solvers.py:430-452).  Launch-only: no host round trips,
     so the whole stage can be captured in a CUDA graph."""
@@ -697,10 +875,17 @@ def _jl_and_sampling(facs, tildes, gts, eps_jl: float, config: RegressionConfig,
     # drawn (all streams fork here, before any work is enqueued)
     nf = len(facs)
     chol_st = [_side_stream(16 + n) for n in range(nf)] if use_chol else []
+
+    def fork(st, n):  # ready[n]: event after which factor n's inputs exist (else: main's progress)
+        if ready is not None and ready[n] is not None:
+            st.wait_event(ready[n])
+        else:
+            st.wait_stream(main)
+
     for n in range(1, nf):
-        _side_stream(n).wait_stream(main)
-    for cs in chol_st:
-        cs.wait_stream(main)
+        fork(_side_stream(n), n)
+    for n, cs in enumerate(chol_st):
+        fork(cs, n)
     factors = []
     for n in range(nf):
         if use_chol:
@@ -972,6 +1157,10 @@ def fast_kronecker_regression(factors: Sequence, b, config: RegressionConfig,
     exactly afterwards (``with_loss=False`` skips it: loss = nan; an extension for timing).  With host-resident ``b`` only its sampled entries are transferred
     for the solve; the loss pass then uploads it."""
     host = not D.on_device(b)
+    if caches is None and _trace is None and host:
+        got = _fast_solve_host_graph(factors, b, config, with_loss)
+        if got is not None:
+            return got
     facs, rows, cols = _validated_problem(factors, b)
     if not 0.0 < config.eps <= 0.25:
         raise InvalidInputError(f"fast regression requires eps in (0, 1/4], got {config.eps}")

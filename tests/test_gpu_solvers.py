@@ -275,3 +275,41 @@ def test_whole_solve_graph_matches_eager(golden, name):
     for rep in hs:
         assert rep.iterations == ref.iterations
         np.testing.assert_array_equal(np.asarray(rep.solution), ref.solution.cpu().numpy())
+
+
+def test_host_pinned_factor_graph_matches_device_path():
+    """Page-locked host factors and b: the third and later calls replay one graph that also holds
+    the factor uploads and their validation; the result equals the device-resident path bit for bit,
+    and invalid factors still raise the reference's error."""
+    import torch
+    import paper_2209_04876_b200 as K
+    from paper_2209_04876_b200 import solvers as S
+    from paper_2209_04876_b200.errors import InvalidInputError
+    n, d = 4096, 32
+    rng = np.random.default_rng(0)
+    facs_h = [rng.normal(1.0, np.sqrt(1e-3), (n, d)) for _ in range(2)]
+    cfg = K.RegressionConfig(eps=0.1, delta=0.01, lam=1e-3, alpha=1e-5, seed=0)
+    facs_pin = [torch.from_numpy(a).pin_memory() for a in facs_h]
+    b_pin = torch.ones(n * n, dtype=torch.float64).pin_memory()
+    dev = K.fast_kronecker_regression([torch.tensor(a, device="cuda") for a in facs_h],
+                                      torch.ones(n * n, dtype=torch.float64, device="cuda"), cfg)
+    outs = [K.fast_kronecker_regression(facs_pin, b_pin, cfg) for _ in range(3)]
+    assert any(k[0] == "host" for k in S._HOST_GRAPHS) and any(e.graph is not None for e in S._HOST_GRAPHS.values())
+    for r in outs:
+        np.testing.assert_array_equal(np.asarray(r.solution), dev.solution.cpu().numpy())
+        assert r.iterations == dev.iterations and r.loss == pytest.approx(dev.loss, rel=1e-12)
+    facs_pin[1][5, 3] = float("nan")
+    with pytest.raises(InvalidInputError, match="factor 1 contains non-finite"):
+        K.fast_kronecker_regression(facs_pin, b_pin, cfg)
+    facs_pin[1][5, 3] = float("inf")
+    with pytest.raises(InvalidInputError, match="factor 1 contains non-finite"):
+        K.fast_kronecker_regression(facs_pin, b_pin, cfg)
+    facs_pin[1][5, 3] = 1.0
+    keep = facs_pin[0].clone()
+    facs_pin[0].zero_()
+    with pytest.raises(InvalidInputError, match="factor 0 is identically zero"):
+        K.fast_kronecker_regression(facs_pin, b_pin, cfg)
+    facs_pin[0].copy_(keep)
+    facs_pin[1][5, 3] = 1.0
+    r = K.fast_kronecker_regression(facs_pin, b_pin, cfg)  # the graph is still usable afterwards
+    assert np.all(np.isfinite(np.asarray(r.solution)))
