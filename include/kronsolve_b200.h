@@ -219,6 +219,17 @@ int ks_sketch_diag_grouped2(const int64_t* idx, const int64_t* row_shape, const 
                             int64_t* sd_idx, double* sd_val, int64_t* seg, int64_t* lrow, int64_t* rrow,
                             int64_t* counts, int64_t* counts_dev, void* stream);
 
+/* ks_sketch_diag_grouped2 that also writes first_raw[t] (s entries) = the index, in draw order, of
+ * the first draw of sparse-diagonal entry t, so b can be gathered at the raw draws (ks_gather_draws2)
+ * while the sketch is sorted, and then permuted on the device (ks_gather_count). */
+int ks_sketch_diag_grouped2_ex(const int64_t* idx, const int64_t* row_shape, const double* w, int64_t s,
+                               int64_t* sd_idx, double* sd_val, int64_t* seg, int64_t* lrow, int64_t* rrow,
+                               int64_t* counts, int64_t* counts_dev, int64_t* first_raw, void* stream);
+
+/* out[q] = b[draws[q,0] * n1 + draws[q,1]] for the s two-factor draws (b device or page-locked
+ * host memory): the right-hand side's b entries read at the raw draws (solvers.py:451). */
+int ks_gather_draws2(const double* b, const int64_t* draws, int64_t n1, int64_t s, double* out, void* stream);
+
 /* Build the grouped view of a sparse diagonal (sorted unique flat row indices sd_idx with values
  * sd_val, nnz entries) for the factor split left_pos | right_pos (kron.balanced_partition,
  * kron.py:117-144).  Outputs (caller-allocated, nnz-sized): seg (nnz+1), lrow, rrow, v, perm

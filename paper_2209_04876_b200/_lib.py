@@ -78,6 +78,8 @@ _SIGS = {
     "ks_sketch_diag": ([_i32, _p, _p, _p, _i64, _p, _p, POINTER(c_int64), _p], ctypes.c_int),
     "ks_gather": ([_p, _p, _i64, _p, _p], ctypes.c_int),
     "ks_sketch_diag_grouped2": ([_p, _p, _p, _i64, _p, _p, _p, _p, _p, _p, _p, _p], ctypes.c_int),
+    "ks_sketch_diag_grouped2_ex": ([_p, _p, _p, _i64, _p, _p, _p, _p, _p, _p, _p, _p, _p], ctypes.c_int),
+    "ks_gather_draws2": ([_p, _p, _i64, _i64, _p, _p], ctypes.c_int),
     "ks_sketch_group": ([_i32, _p, _p, _p, _i32, _p, _i32, _p, _p, _p, _i64, _p, _p, _p, _p, _p, _p,
                          _p, POINTER(c_int64), _p], ctypes.c_int),
     "ks_sketched_apply": ([POINTER(SketchView), _p, _p, _p, _p], ctypes.c_int),

@@ -85,7 +85,8 @@ __global__ void seg_sqrt_group2_kernel(const uint64_t* __restrict__ keys, const 
                                        int64_t n, uint64_t n1, const double* __restrict__ w,
                                        int64_t* __restrict__ sd_idx, double* __restrict__ sd_val,
                                        int64_t* __restrict__ seg, int64_t* __restrict__ lrow,
-                                       int64_t* __restrict__ rrow, int64_t* __restrict__ counts) {
+                                       int64_t* __restrict__ rrow, int64_t* __restrict__ counts,
+                                       int64_t* __restrict__ first_raw) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   if (i == n - 1) {
@@ -111,6 +112,7 @@ __global__ void seg_sqrt_group2_kernel(const uint64_t* __restrict__ keys, const 
   sd_idx[g] = (int64_t)key;
   sd_val[g] = __dsqrt_rn(acc);
   rrow[g] = (int64_t)(key % n1);
+  if (first_raw) first_raw[g] = perm[i];  // the first draw (in draw order) of this entry
   if (lhead[i]) {
     const int64_t u = lsegid[i];
     seg[u] = g;
@@ -428,9 +430,9 @@ extern "C" int ks_sketch_diag(int32_t nf, const int64_t* idx, const int64_t* row
   return KS_OK;
 }
 
-extern "C" int ks_sketch_diag_grouped2(const int64_t* idx, const int64_t* row_shape, const double* w, int64_t s,
-                                       int64_t* sd_idx, double* sd_val, int64_t* seg, int64_t* lrow, int64_t* rrow,
-                                       int64_t* counts, int64_t* counts_dev, void* stream) {
+extern "C" int ks_sketch_diag_grouped2_ex(const int64_t* idx, const int64_t* row_shape, const double* w, int64_t s,
+                                          int64_t* sd_idx, double* sd_val, int64_t* seg, int64_t* lrow, int64_t* rrow,
+                                          int64_t* counts, int64_t* counts_dev, int64_t* first_raw, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   KS_REQUIRE(counts || counts_dev, KS_EINVAL, "need a host or a device counts buffer");
   if (s <= 0) {
@@ -465,7 +467,7 @@ extern "C" int ks_sketch_diag_grouped2(const int64_t* idx, const int64_t* row_sh
   rc = ks::scan_exclusive_i32(st, lhead, s, lsegid);
   if (rc) return rc;
   seg_sqrt_group2_kernel<<<ceil_div_u(s, 128), 128, 0, st>>>(keys.p, perm.p, head.p, segid.p, lhead, lsegid, s, n1, w,
-                                                             sd_idx, sd_val, seg, lrow, rrow, dcounts);
+                                                             sd_idx, sd_val, seg, lrow, rrow, dcounts, first_raw);
   KS_CHECK_LAUNCH();
   if (counts) {
     KS_TRY_CUDA(cudaMemcpyAsync(counts, dcounts, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
@@ -549,4 +551,28 @@ extern "C" int ks_sketched_transpose_apply(const ks_sketch_view* sk, const doubl
   int rc = ks::sketched_gram_partials(st, sk, nullptr, bv, perm, 0, part.p, &nb);
   if (rc) return rc;
   return ks::reduce_partials(st, part.p, nb, count, G);
+}
+
+extern "C" int ks_sketch_diag_grouped2(const int64_t* idx, const int64_t* row_shape, const double* w, int64_t s,
+                                       int64_t* sd_idx, double* sd_val, int64_t* seg, int64_t* lrow, int64_t* rrow,
+                                       int64_t* counts, int64_t* counts_dev, void* stream) {
+  return ks_sketch_diag_grouped2_ex(idx, row_shape, w, s, sd_idx, sd_val, seg, lrow, rrow, counts, counts_dev, nullptr,
+                                    stream);
+}
+
+namespace {
+__global__ void gather_draws2_kernel(const double* __restrict__ b, const int64_t* __restrict__ draws, int64_t n1,
+                                     int64_t s, double* __restrict__ out) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= s) return;
+  out[q] = b[draws[2 * q] * n1 + draws[2 * q + 1]];
+}
+}  // namespace
+
+extern "C" int ks_gather_draws2(const double* b, const int64_t* draws, int64_t n1, int64_t s, double* out,
+                                void* stream) {
+  if (s <= 0) return KS_OK;
+  gather_draws2_kernel<<<ceil_div_u(s, 128), 128, 0, (cudaStream_t)stream>>>(b, draws, n1, s, out);
+  KS_CHECK_LAUNCH();
+  return KS_OK;
 }

@@ -311,17 +311,19 @@ def grouped2_eligible(facs) -> bool:
     return part.left == (0,) and part.right == (1,)
 
 
-def sketch_diag_grouped2_launch(facs, sketch_indices: torch.Tensor, sketch_weights: torch.Tensor):
+def sketch_diag_grouped2_launch(facs, sketch_indices: torch.Tensor, sketch_weights: torch.Tensor,
+                                first_raw: torch.Tensor | None = None):
     """Launch-only half of sketch_diag_and_view2 (graph-capturable): returns the device buffers
-    (sd_idx, sd_val, seg, lrow, rrow, counts_dev)."""
+    (sd_idx, sd_val, seg, lrow, rrow, counts_dev); ``first_raw`` (optional, s int64) receives each
+    entry's first draw index."""
     rows = [int(a.shape[0]) for a in facs]
     s = int(sketch_indices.shape[0])
     bufs = (D.empty(max(s, 1), dtype=D.I64), D.empty(max(s, 1)), D.empty(s + 1, dtype=D.I64),
             D.empty(max(s, 1), dtype=D.I64), D.empty(max(s, 1), dtype=D.I64), D.empty(2, dtype=D.I64))
     sd_idx, sd_val, seg, lrow, rrow, cdev = bufs
-    _lib.call("ks_sketch_diag_grouped2", D.p(sketch_indices.contiguous()), _lib.ptr_array(ctypes.c_int64, rows),
+    _lib.call("ks_sketch_diag_grouped2_ex", D.p(sketch_indices.contiguous()), _lib.ptr_array(ctypes.c_int64, rows),
               D.p(sketch_weights.contiguous()), s, D.p(sd_idx), D.p(sd_val), D.p(seg), D.p(lrow), D.p(rrow), None,
-              D.p(cdev), D.stream())
+              D.p(cdev), D.p(first_raw), D.stream())
     return bufs
 
 

@@ -583,10 +583,13 @@ def _solve_graph_body(facs, b, config: RegressionConfig, s: int, factor1_stream=
         r1, ev_e1 = _eig_on(e1s, g1)
         grams_h = ("per-factor", [r0, r1], [ev_e0, ev_e1])
         ready = [None, ev1]
-    _, _, _, _, _, g2 = _jl_and_sampling(facs, facs, gts, eps_jl, config, True, seeds, s, ready)
-    sd_idx, sd_val, seg, lrow, rrow, cdev = g2
-    b_at = D.empty(s)
-    _lib.call("ks_gather_count", D.p(b), D.p(sd_idx), D.p(cdev), s, D.p(b_at), D.stream())
+    b_raw = D.empty(max(s, 1))
+    gst = _side_stream(11)
+    _, _, _, _, _, g2 = _jl_and_sampling(facs, facs, gts, eps_jl, config, True, seeds, s, ready, (b, b_raw, gst))
+    sd_idx, sd_val, seg, lrow, rrow, cdev, first_raw = g2
+    main.wait_stream(gst)
+    b_at = D.empty(s)  # b at the sparse-diagonal rows = b_raw at each entry's first draw
+    _lib.call("ks_gather_count", D.p(b_raw), D.p(first_raw), D.p(cdev), s, D.p(b_at), D.stream())
     struct = _lib.SketchView(facs[0].data_ptr(), d0, d0, facs[1].data_ptr(), d1, d1, s, s, seg.data_ptr(),
                              lrow.data_ptr(), rrow.data_ptr(), sd_val.data_ptr())
     # the loop's work plan needs only the sketch: built while the eigensolves still run
@@ -607,7 +610,7 @@ def _solve_graph_body(facs, b, config: RegressionConfig, s: int, factor1_stream=
               float(config.residual_tol), D.p(x), D.p(hist), D.p(rhs), D.p(state), D.p(plan_ws), D.stream())
     ev1.record()
     return dict(x=x, hist=hist, state=state, loop_events=(ev0, ev1),
-                keep=(gts, b_at, sd_idx, sd_val, seg, lrow, rrow, cdev, rhs, plan_ws))
+                keep=(gts, b_at, b_raw, first_raw, sd_idx, sd_val, seg, lrow, rrow, cdev, rhs, plan_ws))
 
 
 def _fast_solve_graph(facs, b, config: RegressionConfig):
@@ -863,7 +866,7 @@ def _spawned_seeds(seed, count: int):
 
 
 def _jl_and_sampling(facs, tildes, gts, eps_jl: float, config: RegressionConfig, use_chol: bool, seeds, s: int,
-                     ready=None):
+                     ready=None, raw_b=None):
     """JL leverage estimates of every factor (leverage.py:85-130), the product sampler's tables
     and the s draws with their weights (solvers.py:430-452).  Launch-only: no host round trips,
     so the whole stage can be captured in a CUDA graph."""
@@ -909,6 +912,16 @@ def _jl_and_sampling(facs, tildes, gts, eps_jl: float, config: RegressionConfig,
     draws = sampler._sample_dev(s, state, inc)
     w = sampler._weights_dev(draws, s)
     # two factors: the sparse diagonal and its grouped view are built here too (launch-only)
+    if raw_b is not None and _USE_FUSED[0] and grouped2_eligible(facs):
+        # raw_b = (b, out): b read at the raw draws on a side stream while the sketch is sorted and
+        # deduplicated (the read may cross PCIe: page-locked host b); joined by the caller
+        b, b_raw, gst = raw_b
+        gst.wait_stream(main)
+        with torch.cuda.stream(gst):
+            _lib.call("ks_gather_draws2", D.p(b), D.p(draws), int(facs[1].shape[0]), s, D.p(b_raw), D.stream())
+        first_raw = D.empty(max(s, 1), dtype=D.I64)
+        g2 = sketch_diag_grouped2_launch(facs, draws, w, first_raw) + (first_raw,)
+        return scores, afs, sampler, draws, w, g2
     g2 = sketch_diag_grouped2_launch(facs, draws, w) if _USE_FUSED[0] and grouped2_eligible(facs) else None
     return scores, afs, sampler, draws, w, g2
 
