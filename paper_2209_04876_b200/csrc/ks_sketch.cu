@@ -4,7 +4,10 @@
 //   sketched_kron_apply / sketched_kron_transpose_apply (kron.py:258-354)
 // The reference recomputes np.unique/argsort on every apply; here the grouping is built once
 // per sketch and every apply is a gathered-row contraction over the distinct left-group rows.
+#include <cstdlib>
+
 #include "ks_common.cuh"
+#include "ks_tma.cuh"
 #include "ks_pairwise.cuh"
 
 #include <vector>
@@ -340,6 +343,109 @@ __global__ void __launch_bounds__(AP_WARPS * 32) gram_apply_kernel(ks_sketch_vie
   }
 }
 
+
+// Fused normal-operator partials for d_L = d_R = 128 on the FP64 tensor cores (the generic path's
+// widest case: the persistent loop kernel's X does not fit shared memory at 128 x 128).  Grid-stride
+// over chunks of 32 left rows; per chunk Y = L_c X (DMMA, X resident in shared memory), the
+// samples' values and Z_c = sum_t c_t R_t (one warp per left row), then G_b += L_c^T Z_c (DMMA) into
+// register accumulators (warp w owns rows 16w..16w+15 of G_b).  One d^2 partial per block.
+constexpr int G128_CH = 32, G128_LDX = 136, G128_LDL = 132, G128_LDZ = 136;
+__global__ void __launch_bounds__(256) gram_apply_dmma128_kernel(ks_sketch_view sk, const double* __restrict__ X,
+                                                                 double* __restrict__ part) {
+  extern __shared__ double sm[];
+  double* Xs = sm;                             // 128 x LDX
+  double* Ls = Xs + 128 * G128_LDX;            // CH x LDL
+  double* Ys = Ls + G128_CH * G128_LDL;        // CH x LDZ: Y, then Z
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, g = lane >> 2, t = lane & 3;
+  for (int e = tid; e < 128 * 128; e += 256) Xs[(e >> 7) * G128_LDX + (e & 127)] = X[e];
+  double acc[16][4];
+#pragma unroll
+  for (int q = 0; q < 16; q++)
+#pragma unroll
+    for (int j = 0; j < 4; j++) acc[q][j] = 0.0;
+  const int64_t nchunks = (sk.u_left + G128_CH - 1) / G128_CH;
+  for (int64_t chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x) {
+    const int64_t u0 = chunk * G128_CH;
+    const int rows = (int)ks_min64(G128_CH, sk.u_left - u0);
+    __syncthreads();  // the previous chunk's G phase is done with Ls / Ys
+    for (int e = tid; e < G128_CH * 128; e += 256) {
+      const int r = e >> 7, k = e & 127;
+      Ls[r * G128_LDL + k] = (r < rows) ? sk.Lmat[sk.lrow[u0 + r] * sk.ldl + k] : 0.0;
+    }
+    __syncthreads();
+    {  // Y = L_c X: 2 m-tiles x 16 n-tiles; warp w: m-tile w & 1, n-tiles 4 (w >> 1) .. + 3
+      const int mt = w & 1, nt0 = (w >> 1) * 4;
+      double c[4][4];
+#pragma unroll
+      for (int q = 0; q < 4; q++)
+#pragma unroll
+        for (int j = 0; j < 4; j++) c[q][j] = 0.0;
+#pragma unroll 4
+      for (int k0 = 0; k0 < 128; k0 += 4) {
+        const double a0 = Ls[(mt * 16 + g) * G128_LDL + k0 + t];
+        const double a1 = Ls[(mt * 16 + g + 8) * G128_LDL + k0 + t];
+#pragma unroll
+        for (int q = 0; q < 4; q++) dmma_16x8x4(c[q], a0, a1, Xs[(k0 + t) * G128_LDX + (nt0 + q) * 8 + g]);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        double* y0 = Ys + (mt * 16 + g) * G128_LDZ + (nt0 + q) * 8 + 2 * t;
+        double* y1 = y0 + 8 * G128_LDZ;
+        y0[0] = c[q][0];
+        y0[1] = c[q][1];
+        y1[0] = c[q][2];
+        y1[1] = c[q][3];
+      }
+    }
+    __syncthreads();
+    // samples of each left row (warp per row): c_t = v_t (v_t Y_u . R_t), Z_u = sum c_t R_t
+    for (int rr = w; rr < G128_CH; rr += 8) {
+      double z[4] = {0.0, 0.0, 0.0, 0.0};
+      if (rr < rows) {
+        const int64_t u = u0 + rr;
+        double y[4];
+#pragma unroll
+        for (int j = 0; j < 4; j++) y[j] = Ys[rr * G128_LDZ + lane + 32 * j];
+        for (int64_t tt = sk.seg[u]; tt < sk.seg[u + 1]; tt++) {
+          const double* R = sk.Rmat + sk.rrow[tt] * sk.ldr;
+          double r[4];
+#pragma unroll
+          for (int j = 0; j < 4; j++) r[j] = R[lane + 32 * j];
+          double d = 0.0;
+#pragma unroll
+          for (int j = 0; j < 4; j++) d = fma(y[j], r[j], d);
+          d = warp_sum(d);
+          const double vt = sk.v[tt];
+          const double cf = vt * (vt * d);
+#pragma unroll
+          for (int j = 0; j < 4; j++) z[j] = fma(cf, r[j], z[j]);
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < 4; j++) Ys[rr * G128_LDZ + lane + 32 * j] = z[j];
+    }
+    __syncthreads();
+    // G_b += L_c^T Z_c: warp w owns m-tile w (rows 16w..), all 16 n-tiles; k over the chunk rows
+#pragma unroll 2
+    for (int k0 = 0; k0 < G128_CH; k0 += 4) {
+      const double a0 = Ls[(k0 + t) * G128_LDL + w * 16 + g];
+      const double a1 = Ls[(k0 + t) * G128_LDL + w * 16 + g + 8];
+#pragma unroll
+      for (int q = 0; q < 16; q++) dmma_16x8x4(acc[q], a0, a1, Ys[(k0 + t) * G128_LDZ + q * 8 + g]);
+    }
+  }
+  double* G = part + (int64_t)blockIdx.x * 128 * 128;
+#pragma unroll
+  for (int q = 0; q < 16; q++) {
+    const int row = w * 16 + g, col = q * 8 + 2 * t;
+    G[row * 128 + col] = acc[q][0];
+    G[row * 128 + col + 1] = acc[q][1];
+    G[(row + 8) * 128 + col] = acc[q][2];
+    G[(row + 8) * 128 + col + 1] = acc[q][3];
+  }
+}
+
 __global__ void reduce_cols_kernel(const double* __restrict__ part, int64_t nparts, int64_t count,
                                    double* __restrict__ out) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -366,6 +472,16 @@ int sketched_gram_partials(cudaStream_t st, const ks_sketch_view* sk, const doub
   *nparts_out = nb;
   if (nb == 0) return KS_OK;
   const size_t smem = sizeof(double) * (size_t)CH * (sk->dL + sk->dR);
+  if (mode == 1 && sk->dL == 128 && sk->dR == 128 && !getenv("KS_GRAM_SCALAR")) {
+    const int64_t nchunks = (sk->u_left + G128_CH - 1) / G128_CH;
+    const int64_t nb128 = ks_min64(nchunks, (int64_t)num_sms());
+    *nparts_out = nb128;
+    const size_t sm128 = sizeof(double) * (size_t)(128 * G128_LDX + G128_CH * G128_LDL + G128_CH * G128_LDZ);
+    KS_TRY_CUDA(cudaFuncSetAttribute(gram_apply_dmma128_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm128));
+    gram_apply_dmma128_kernel<<<(unsigned)nb128, 256, sm128, st>>>(*sk, X, part);
+    KS_CHECK_LAUNCH();
+    return KS_OK;
+  }
   if (mode == 1) {
     KS_TRY_CUDA(cudaFuncSetAttribute(gram_apply_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     gram_apply_kernel<1><<<(unsigned)nb, AP_WARPS * 32, smem, st>>>(*sk, X, bv, perm, part);
