@@ -679,6 +679,151 @@ static void launch_jacobi_fixed(cudaStream_t st, const MatPtrs& Ms, const double
   jacobi_fixed_kernel<D, SYM><<<batch, D / 2 * JF_G, smem, st>>>(Ms, M, sigma, V, sweeps32);
 }
 
+
+// d = 128: the fixed-size one-sided Jacobi with W (128 x 136 doubles, 139 KB) in shared memory; the
+// accumulated rotations V keep rows 0..63 in shared memory (70 KB) and rows 64..127 in a
+// per-problem global scratch (L2-resident).  Both halves of a pair's V columns are loaded at the
+// start of the round (their latency hides behind the dot products) and written after the
+// rotation; the block barrier publishes them to the next round.  512 threads: 64 column pairs x 8
+// threads, 16 elements per thread.  Same rotation formulas, convergence rule and output contract
+// as jacobi_fixed_kernel.
+template <bool SYM>
+__global__ void __launch_bounds__(512) jacobi128_kernel(MatPtrs Ms, const double* __restrict__ Mc,
+                                                        double* __restrict__ sigma, double* __restrict__ Vout,
+                                                        double* __restrict__ Vg_all) {
+  constexpr int D = 128, NT = 512, E = D / JF_G, EH = E / 2, LV = 72;
+  extern __shared__ double jf_sm[];
+  double* W = jf_sm;
+  double* Vs = jf_sm + D * (D + 8);                  // rows 0..63:   Vs[j * LV + i]
+  double* Vg = Vg_all + (size_t)blockIdx.x * D * LV;  // rows 64..127: Vg[j * LV + i - 64]
+  __shared__ int s_rot;
+  __shared__ int s_order[D];
+  __shared__ double s_norm[D];
+  const double* M = Mc ? Mc + (size_t)blockIdx.x * D * D : Ms.p[blockIdx.x];
+  sigma += (size_t)blockIdx.x * D;
+  Vout += (size_t)blockIdx.x * D * D;
+  const int tid = threadIdx.x;
+  for (int e = tid; e < D * D; e += NT) {
+    const int i = e / D, j = e % D;
+    const double m = SYM ? 0.5 * (M[(size_t)i * D + j] + M[(size_t)j * D + i]) : M[(size_t)i * D + j];
+    W[jf_off<D>(j, i)] = m;
+    const double id = (i == j) ? 1.0 : 0.0;
+    if (i < 64) Vs[j * LV + i] = id; else Vg[j * LV + i - 64] = id;
+  }
+  __syncthreads();
+  const int group = tid / JF_G, lg = tid % JF_G;
+  const double tol = 2.0 * D * 2.220446049250313e-16;
+  for (int sweep = 0; sweep < 40; sweep++) {
+    if (tid == 0) s_rot = 0;
+    __syncthreads();
+    for (int r = 0; r < D - 1; r++) {
+      auto player = [&](int pos) {
+        int x = pos - 1 + r;
+        if (x >= D - 1) x -= D - 1;
+        return pos == 0 ? 0 : 1 + x;
+      };
+      const int p = player(group), q = player(D - 1 - group);
+      double x[E], y[E], ug[EH], vg[EH];
+      // global half of V first: the longest latency, consumed last
+#pragma unroll
+      for (int k = 0; k < EH; k++) {
+        ug[k] = Vg[p * LV + lg + k * JF_G];
+        vg[k] = Vg[q * LV + lg + k * JF_G];
+      }
+#pragma unroll
+      for (int k = 0; k < E; k++) {
+        x[k] = W[jf_off<D>(p, lg + k * JF_G)];
+        y[k] = W[jf_off<D>(q, lg + k * JF_G)];
+      }
+      double a = 0.0, b = 0.0, c = 0.0;
+#pragma unroll
+      for (int k = 0; k < E; k++) {
+        a = fma(x[k], x[k], a);
+        b = fma(y[k], y[k], b);
+        c = fma(x[k], y[k], c);
+      }
+#pragma unroll
+      for (int o = JF_G / 2; o > 0; o >>= 1) {
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+        b += __shfl_xor_sync(0xffffffffu, b, o);
+        c += __shfl_xor_sync(0xffffffffu, c, o);
+      }
+      if (c != 0.0 && a != 0.0 && b != 0.0 && c * c > tol * tol * a * b) {
+        const double x2 = b - a, y2 = 2.0 * c;
+        const double qq = fma(x2, x2, y2 * y2);
+        double rq;
+        asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(rq) : "d"(qq));
+        rq = rq * fma(-0.5 * qq * rq, rq, 1.5);
+        const double den = fma(qq, rq, fabs(x2));
+        double ri;
+        asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(ri) : "d"(den));
+        ri = ri * fma(-den, ri, 2.0);
+        const double tt = y2 * ri;
+        const double t = x2 >= 0.0 ? tt : -tt;
+        const double cs = rsqrt(fma(t, t, 1.0));
+        const double sn = cs * t;
+#pragma unroll
+        for (int k = 0; k < E; k++) {
+          W[jf_off<D>(p, lg + k * JF_G)] = cs * x[k] - sn * y[k];
+          W[jf_off<D>(q, lg + k * JF_G)] = sn * x[k] + cs * y[k];
+        }
+#pragma unroll
+        for (int k = 0; k < EH; k++) {
+          const int i = lg + k * JF_G;
+          const double u = Vs[p * LV + i], v = Vs[q * LV + i];
+          Vs[p * LV + i] = cs * u - sn * v;
+          Vs[q * LV + i] = sn * u + cs * v;
+        }
+#pragma unroll
+        for (int k = 0; k < EH; k++) {
+          const int i = lg + k * JF_G;
+          Vg[p * LV + i] = cs * ug[k] - sn * vg[k];
+          Vg[q * LV + i] = sn * ug[k] + cs * vg[k];
+        }
+        if (lg == 0) s_rot = 1;
+      }
+      __syncthreads();
+    }
+    if (tid == 0) g_jacobi_sweeps[blockIdx.x & 7] = sweep + 1;
+    if (s_rot == 0) break;
+    __syncthreads();
+  }
+  for (int j = tid; j < D; j += NT) {
+    double s2 = 0.0;
+    for (int i = 0; i < D; i++) s2 = fma(W[jf_off<D>(j, i)], W[jf_off<D>(j, i)], s2);
+    s_norm[j] = sqrt(s2);
+  }
+  __syncthreads();
+  for (int j = tid; j < D; j += NT) {
+    int rank = 0;
+    // total order even for non-finite input (NaN ranks last): every rank is assigned exactly once
+    const double sj = isnan(s_norm[j]) ? -1.0 : s_norm[j];
+    for (int k = 0; k < D; k++) {
+      const double sk = isnan(s_norm[k]) ? -1.0 : s_norm[k];
+      rank += (sk > sj) || (sk == sj && k < j);
+    }
+    s_order[rank] = j;
+  }
+  __syncthreads();
+  for (int k = tid; k < D; k += NT) sigma[k] = s_norm[s_order[k]];
+  for (int e = tid; e < D * D; e += NT) {
+    const int i = e / D, k = e % D;
+    const int j = s_order[k];
+    Vout[e] = i < 64 ? Vs[j * LV + i] : Vg[j * LV + i - 64];
+  }
+}
+
+template <bool SYM>
+static int launch_jacobi128(cudaStream_t st, const MatPtrs& Ms, const double* M, double* sigma, double* V, int batch) {
+  Scratch<double> vg((int64_t)batch * 128 * 72, st);
+  KS_REQUIRE(vg.p, KS_ECUDA, "scratch allocation failed");
+  const int smem = (128 * 136 + 128 * 72) * (int)sizeof(double);
+  KS_TRY_CUDA(cudaFuncSetAttribute(jacobi128_kernel<SYM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  jacobi128_kernel<SYM><<<batch, 512, smem, st>>>(Ms, M, sigma, V, vg.p);
+  KS_CHECK_LAUNCH();
+  return KS_OK;
+}
+
 template <bool SYM>
 static bool jacobi_fixed(cudaStream_t st, const MatPtrs& Ms, const double* M, int d, double* sigma, double* V,
                          int batch) {
@@ -687,6 +832,7 @@ static bool jacobi_fixed(cudaStream_t st, const MatPtrs& Ms, const double* M, in
     case 16: launch_jacobi_fixed<16, SYM>(st, Ms, M, sigma, V, batch); return true;
     case 32: launch_jacobi_fixed<32, SYM>(st, Ms, M, sigma, V, batch); return true;
     case 64: launch_jacobi_fixed<64, SYM>(st, Ms, M, sigma, V, batch); return true;
+    case 128: return launch_jacobi128<SYM>(st, Ms, M, sigma, V, batch) == KS_OK;
     default: return false;
   }
 }

@@ -16,7 +16,7 @@ from paper_2209_04876_b200 import _device as D, _lib  # noqa: E402
 
 lib = _lib.load()
 rng = np.random.default_rng(0)
-for n, d in [(16384, 64), (4096, 32), (1024, 16)]:
+for n, d in [(16384, 64), (4096, 32), (1024, 16), (65536, 128)]:
     a = rng.normal(1.0, np.sqrt(1e-3), (n, d))
     g = a.T @ a
     gt = D.to_dev(g)
