@@ -59,53 +59,70 @@ def make_inputs(n, d):
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """SM clocks and clock-event (throttle) reasons sampled DURING the timed region: NVML every
+    2 ms in a thread (nvidia-smi as the fallback); one sample is taken at start() and one at stop(),
+    so even a short timed region has samples."""
+
+    _REASONS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40}
 
     def __init__(self, index=0):
         self.index = index
-        self.samples = []
-        self.proc = None
+        self.samples = []  # (sm_mhz, max_mhz, reason_mask)
         self.thread = None
+        self.stop_flag = threading.Event()
+        self.nvml = None
+
+    def _sample(self):
+        nv, h = self.nvml
+        try:
+            get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                nv.nvmlDeviceGetCurrentClocksThrottleReasons
+            self.samples.append((float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)),
+                                 float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)), int(get_reasons(h))))
+        except Exception:
+            pass
+
+    def _loop(self):
+        while not self.stop_flag.wait(0.002):
+            self._sample()
 
     def start(self):
-        cmd = ["nvidia-smi", f"--id={self.index}",
-               "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-               "--format=csv,noheader,nounits", "-lms", "100"]
         try:
-            self.proc = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-        except OSError:
-            self.proc = None
+            import pynvml as nv
+            nv.nvmlInit()
+            self.nvml = (nv, nv.nvmlDeviceGetHandleByIndex(self.index))
+        except Exception:
+            self.nvml = None
             return
-        self.thread = threading.Thread(target=self._read, daemon=True)
+        self._sample()
+        self.thread = threading.Thread(target=self._loop, daemon=True)
         self.thread.start()
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.samples.append([x.strip() for x in line.split(",")])
-
     def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except Exception:
-            self.proc.kill()
+        if self.nvml is None:
+            return self._smi_once()
+        self._sample()
+        self.stop_flag.set()
         if self.thread:
             self.thread.join(timeout=2)
-        sm = [float(s[0]) for s in self.samples if len(s) >= 8 and s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if len(s) >= 8 and s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = set()
-        for s in self.samples:
-            if len(s) >= 8:
-                for nm, v in zip(names, s[4:8]):
-                    if v.lower() == "active":
-                        reasons.add(nm)
+        sm = [x[0] for x in self.samples]
+        mx = [x[1] for x in self.samples]
+        reasons = sorted({nm for x in self.samples for nm, bit in self._REASONS.items() if x[2] & bit})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "samples": len(self.samples), "reasons": sorted(reasons)}
+                "samples": len(self.samples), "source": "nvml, 2 ms", "reasons": reasons}
+
+    def _smi_once(self):
+        cmd = ["nvidia-smi", f"--id={self.index}", "--query-gpu=clocks.sm,clocks.max.sm,"
+               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+               "--format=csv,noheader,nounits"]
+        try:
+            out = subprocess.run(cmd, capture_output=True, text=True, timeout=10).stdout.strip().split(",")
+            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            return {"sm_mhz": float(out[0]), "sm_max_mhz": float(out[1]), "samples": 1, "source": "nvidia-smi",
+                    "reasons": sorted(nm for nm, v in zip(names, out[2:6]) if v.strip().lower() == "active")}
+        except Exception:
+            return {"sm_mhz": None, "sm_max_mhz": None, "samples": 0, "reasons": ["clock query unavailable"]}
 
 
 def fp64_peak_tflops():
@@ -251,6 +268,8 @@ def run_ours(args):
         e2e_t = time.perf_counter() - t0
         if i >= e2e_warm:
             e2e.append(e2e_t)
+        if os.environ.get("KS_BENCH_DEBUG"):
+            print(f"e2e {i} {e2e_t * 1e3:.3f} ms", file=sys.stderr)
     t0 = time.perf_counter()
     r_full = K.fast_kronecker_regression(facs_h, b_host, cfg)
     e2e_full = time.perf_counter() - t0
