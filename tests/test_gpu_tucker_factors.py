@@ -195,3 +195,21 @@ def test_c5_als_sweep_matches_reference_fixture(golden, mode):
     assert rep.rre == pytest.approx(float(g[f"{mode}_rre"]), rel=tol)
     assert rel(model.core, g[f"{mode}_core"]) <= 100 * tol
     assert rel(model.factors[2], g[f"{mode}_factor2"]) <= 100 * tol
+
+
+@pytest.mark.parametrize("shape,rank,n", [((200, 150), (3, 2), 0), ((200, 150), (3, 2), 1),
+                                          ((10, 9, 8, 7), (2, 3, 2, 2), 0), ((10, 9, 8, 7), (2, 3, 2, 2), 3)])
+def test_fast_update_other_orders_match_oracle(shape, rank, n):
+    """Order-2 models (one other factor: no right group) and order-4 models (three other factors:
+    Khatri-Rao right rows) through the same row kernel, against the oracle."""
+    rng = np.random.default_rng(len(shape) * 10 + n)
+    core = rng.standard_normal(rank)
+    facs = [np.linalg.qr(rng.standard_normal((i, r)))[0] for i, r in zip(shape, rank)]
+    x = T.reconstruct(core, facs) + 0.05 * rng.standard_normal(shape)
+    i_rest = x.size // x.shape[n]
+    cfg = dict(eps=0.25, delta=0.05, alpha=1e-4, seed=5)
+    s = T.factor_sample_count(int(np.prod([r for k, r in enumerate(rank) if k != n])), shape[n], T.Cfg(**cfg))
+    assert s < i_rest  # the sketched path, not the exact shortcut
+    want = T.fast_factor_matrix_update(core, facs, 0.02, x, n, T.Cfg(lam=0.02, **cfg))
+    got = K().fast_factor_matrix_update(model_of(core, facs, 0.02), x, n, K().RegressionConfig(lam=0.02, **cfg))
+    assert rel(got, want) <= 1e-8
