@@ -178,13 +178,18 @@ def jl_projection_rows(n: int, log_factor: float = JL_LOG_FACTOR) -> int:
     return max(1, math.ceil(log_factor * math.log(max(n, 2))))
 
 
-def _jl_ga(a: torch.Tensor, a_tilde: torch.Tensor, seed, log_factor: float):
+def _jl_ga(a: torch.Tensor, a_tilde: torch.Tensor, seed, log_factor: float, pre=None):
     """GA = g @ a_tilde with g = default_rng(seed).standard_normal((r, n_tilde)) / sqrt(r) drawn
-    on the device (leverage.py:124-127).  Returns (GA (r x d), r)."""
+    on the device (leverage.py:124-127).  Returns (GA (r x d), r).  ``pre``: (g, event) drawn
+    earlier (the sketch depends only on the seed), waited for here."""
     n, d = int(a.shape[0]), int(a.shape[1])
     nt = int(a_tilde.shape[0])
     r = jl_projection_rows(n, log_factor)
-    g = device_standard_normal(seed, r * nt, divisor=math.sqrt(r))
+    if pre is not None:
+        g, ev = pre
+        torch.cuda.current_stream().wait_event(ev)
+    else:
+        g = device_standard_normal(seed, r * nt, divisor=math.sqrt(r))
     ga = D.empty(r, d)
     if r <= 128 and d <= 128:
         _lib.call("ks_gemm_tn_tall", r, d, nt, 1.0, D.p(g), 1, nt, D.p(a_tilde), d, 1, D.p(ga), D.stream())

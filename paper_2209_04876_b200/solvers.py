@@ -442,14 +442,14 @@ def _jl_factor(gram: torch.Tensor) -> torch.Tensor:
 
 def _jl_scores_chol(a: torch.Tensor, a_tilde: torch.Tensor, gram: torch.Tensor, eps: float, seed,
                     log_factor: float, use_chol: bool = True, factor: torch.Tensor | None = None,
-                    factor_stream=None) -> torch.Tensor:
+                    factor_stream=None, pre_g=None) -> torch.Tensor:
     """JL scores with (1+eps/4) (G a_tilde) gram^-1 from a device Cholesky solve (leverage.py:114-129).
     The positive-definiteness flag is checked with the solve's other deferred flags; on failure
     the solve is repeated with ``use_chol=False`` (LU inverse, as the reference's np.linalg.inv).
     ``factor``: a workspace from _jl_factor (made on ``factor_stream``)."""
     from .leverage import _jl_ga, _jl_scores_from_q, check_later
     d = int(a.shape[1])
-    ga, r = _jl_ga(a, a_tilde, seed, log_factor)
+    ga, r = _jl_ga(a, a_tilde, seed, log_factor, pre_g)
     q = D.empty(r, d)
     if use_chol and factor is not None:
         if factor_stream is not None:
@@ -548,7 +548,29 @@ def _eig_on(stream, g):
     return (v[0], w[0]), ev
 
 
-def _solve_graph_body(facs, b, config: RegressionConfig, s: int, factor1_stream=None):
+_NO_PREDRAW = [bool(__import__("os").environ.get("KS_NO_PREDRAW"))]
+
+
+def _predraw_jl_sketches(facs, config: RegressionConfig, seeds):
+    """The JL Gaussian sketches (leverage.py:124-126) depend only on the seeds and the shapes: draw
+    them first, each on its own stream (off the Gram / upload critical path).  Returns per factor
+    (g, event)."""
+    from .leverage import device_standard_normal, jl_projection_rows
+    main = torch.cuda.current_stream()
+    out = []
+    for n, a in enumerate(facs):
+        r = jl_projection_rows(int(a.shape[0]), config.jl_log_factor)
+        st = _side_stream(12 + n)
+        st.wait_stream(main)
+        with torch.cuda.stream(st):
+            g = device_standard_normal(seeds[2 * n + 1], r * int(a.shape[0]), divisor=math.sqrt(r))
+        ev = torch.cuda.Event()
+        ev.record(st)
+        out.append((g, ev))
+    return out
+
+
+def _solve_graph_body(facs, b, config: RegressionConfig, s: int, factor1_stream=None, pre_g=None):
     """Launch-only device pipeline of the fused two-factor solve (captured once per key).
 
     ``factor1_stream``: the stream on which facs[1] becomes ready (its upload, when the graph also
@@ -559,6 +581,8 @@ def _solve_graph_body(facs, b, config: RegressionConfig, s: int, factor1_stream=
     eps_jl = 4.0 * math.log1p(config.eps / 4.0) / 2
     d0, d1 = int(facs[0].shape[1]), int(facs[1].shape[1])
     main = torch.cuda.current_stream()
+    if pre_g is None and not _NO_PREDRAW[0]:
+        pre_g = _predraw_jl_sketches(facs, config, seeds)
     ready = None
     if factor1_stream is None:
         gside = _side_stream(8)
@@ -585,7 +609,8 @@ def _solve_graph_body(facs, b, config: RegressionConfig, s: int, factor1_stream=
         ready = [None, ev1]
     b_raw = D.empty(max(s, 1))
     gst = _side_stream(11)
-    _, _, _, _, _, g2 = _jl_and_sampling(facs, facs, gts, eps_jl, config, True, seeds, s, ready, (b, b_raw, gst))
+    _, _, _, _, _, g2 = _jl_and_sampling(facs, facs, gts, eps_jl, config, True, seeds, s, ready, (b, b_raw, gst),
+                                         pre_g)
     sd_idx, sd_val, seg, lrow, rrow, cdev, first_raw = g2
     main.wait_stream(gst)
     b_at = D.empty(s)  # b at the sparse-diagonal rows = b_raw at each entry's first draw
@@ -610,7 +635,7 @@ def _solve_graph_body(facs, b, config: RegressionConfig, s: int, factor1_stream=
               float(config.residual_tol), D.p(x), D.p(hist), D.p(rhs), D.p(state), D.p(plan_ws), D.stream())
     ev1.record()
     return dict(x=x, hist=hist, state=state, loop_events=(ev0, ev1),
-                keep=(gts, b_at, b_raw, first_raw, sd_idx, sd_val, seg, lrow, rrow, cdev, rhs, plan_ws))
+                keep=(gts, b_at, b_raw, first_raw, sd_idx, sd_val, seg, lrow, rrow, cdev, rhs, plan_ws, pre_g))
 
 
 def _fast_solve_graph(facs, b, config: RegressionConfig):
@@ -762,6 +787,8 @@ def _fast_solve_host_graph(factors, b, config: RegressionConfig, with_loss: bool
         try:
             with torch.cuda.graph(g):
                 main = torch.cuda.current_stream()
+                # the JL sketches need no input data: drawn while the factors upload
+                pre_g = None if _NO_PREDRAW[0] else _predraw_jl_sketches(entry.dev, config, _spawned_seeds(config.seed, 5))
                 side = _side_stream(9)
                 entry.dev[0].copy_(factors[0], non_blocking=True)
                 side.wait_stream(main)  # after factor 0's upload: the PCIe link serves one copy at a time
@@ -771,7 +798,7 @@ def _fast_solve_host_graph(factors, b, config: RegressionConfig, with_loss: bool
                               D.p(entry.flags[1]), D.stream())
                 _lib.call("ks_check_finite_nonzero", D.p(entry.dev[0]), entry.dev[0].numel(), D.p(entry.flags[0]),
                           D.stream())
-                entry.out = _solve_graph_body(entry.dev, b.reshape(-1), config, s, factor1_stream=side)
+                entry.out = _solve_graph_body(entry.dev, b.reshape(-1), config, s, factor1_stream=side, pre_g=pre_g)
                 main.wait_stream(side)
         except Exception:
             _HOST_GRAPHS.pop(key, None)
@@ -866,7 +893,7 @@ def _spawned_seeds(seed, count: int):
 
 
 def _jl_and_sampling(facs, tildes, gts, eps_jl: float, config: RegressionConfig, use_chol: bool, seeds, s: int,
-                     ready=None, raw_b=None):
+                     ready=None, raw_b=None, pre_g=None):
     """JL leverage estimates of every factor (leverage.py:85-130), the product sampler's tables
     and the s draws with their weights (solvers.py:430-452).  Launch-only: no host round trips,
     so the whole stage can be captured in a CUDA graph."""
@@ -899,7 +926,8 @@ def _jl_and_sampling(facs, tildes, gts, eps_jl: float, config: RegressionConfig,
         with torch.cuda.stream(st):
             scores.append(_jl_scores_chol(a, tildes[n], gts[n], eps_jl, seeds[2 * n + 1], config.jl_log_factor,
                                           use_chol, factors[n] if use_chol else None,
-                                          chol_st[n] if use_chol else None))
+                                          chol_st[n] if use_chol else None,
+                                          pre_g[n] if pre_g is not None else None))
         afs.append(1.0 + eps_jl / 2.0)
     for n in range(1, nf):
         main.wait_stream(_side_stream(n))
