@@ -519,13 +519,6 @@ def _solve_graph_key(facs, b, config: RegressionConfig):
         return None
     if not (b.is_cuda or b.is_pinned()):
         return None
-    n_factors = 2
-    eps_one = math.log1p(config.eps / 4.0) / n_factors
-    eps_two = eps_one / (2.0 + eps_one)
-    delta_n = config.delta / (2.0 * n_factors)
-    for a in facs:  # the spectral row-sampling branch (data-dependent shapes) stays eager
-        if math.ceil(config.effective_alpha * spectral_sample_count(int(a.shape[1]), eps_two, delta_n)) < int(a.shape[0]):
-            return None
     try:
         key = (torch.cuda.current_device(), torch.cuda.current_stream().cuda_stream,
                tuple((a.data_ptr(), tuple(a.shape), tuple(a.stride())) for a in facs),
@@ -551,19 +544,34 @@ def _eig_on(stream, g):
 _NO_PREDRAW = [bool(__import__("os").environ.get("KS_NO_PREDRAW"))]
 
 
+def _tilde_rows(facs, config: RegressionConfig):
+    """Rows of each factor's JL input: s_n spectral rows when row sampling applies (solvers.py:421-436),
+    else all n rows."""
+    nf = len(facs)
+    eps_one = math.log1p(config.eps / 4.0) / nf
+    eps_two = eps_one / (2.0 + eps_one)
+    delta_n = config.delta / (2.0 * nf)
+    out = []
+    for a in facs:
+        s_n = math.ceil(config.effective_alpha * spectral_sample_count(int(a.shape[1]), eps_two, delta_n))
+        out.append(s_n if s_n < int(a.shape[0]) else int(a.shape[0]))
+    return out, eps_two, delta_n
+
+
 def _predraw_jl_sketches(facs, config: RegressionConfig, seeds):
     """The JL Gaussian sketches (leverage.py:124-126) depend only on the seeds and the shapes: draw
     them first, each on its own stream (off the Gram / upload critical path).  Returns per factor
     (g, event)."""
     from .leverage import device_standard_normal, jl_projection_rows
     main = torch.cuda.current_stream()
+    nts, _, _ = _tilde_rows(facs, config)
     out = []
     for n, a in enumerate(facs):
         r = jl_projection_rows(int(a.shape[0]), config.jl_log_factor)
         st = _side_stream(12 + n)
         st.wait_stream(main)
         with torch.cuda.stream(st):
-            g = device_standard_normal(seeds[2 * n + 1], r * int(a.shape[0]), divisor=math.sqrt(r))
+            g = device_standard_normal(seeds[2 * n + 1], r * nts[n], divisor=math.sqrt(r))
         ev = torch.cuda.Event()
         ev.record(st)
         out.append((g, ev))
@@ -583,34 +591,36 @@ def _solve_graph_body(facs, b, config: RegressionConfig, s: int, factor1_stream=
     main = torch.cuda.current_stream()
     if pre_g is None and not _NO_PREDRAW[0]:
         pre_g = _predraw_jl_sketches(facs, config, seeds)
-    ready = None
+    # per factor, on its own stream as soon as the factor exists: the spectral row sample when it
+    # applies (leverage.py:235-252), the Gram of the JL input, then its eigendecomposition
+    nts, eps_two, delta_n = _tilde_rows(facs, config)
+    f1s = factor1_stream if factor1_stream is not None else _side_stream(8)
     if factor1_stream is None:
-        gside = _side_stream(8)
-        gside.wait_stream(main)
-        g0 = _gram_dev(facs[0])
-        with torch.cuda.stream(gside):  # the two Grams concurrently
-            g1 = _gram_dev(facs[1])
-        main.wait_stream(gside)
-        gts = [g0, g1]
-        grams_h = _factor_grams_async(gts)
-    else:
-        g0 = _gram_dev(facs[0])
-        with torch.cuda.stream(factor1_stream):
-            g1 = _gram_dev(facs[1])
-        ev1 = torch.cuda.Event()
-        ev1.record(factor1_stream)
-        gts = [g0, g1]
-        e0s, e1s = _side_stream(0), _side_stream(10)
-        e0s.wait_stream(main)
-        e1s.wait_event(ev1)
-        r0, ev_e0 = _eig_on(e0s, g0)
-        r1, ev_e1 = _eig_on(e1s, g1)
-        grams_h = ("per-factor", [r0, r1], [ev_e0, ev_e1])
-        ready = [None, ev1]
+        f1s.wait_stream(main)
+    tildes, gts, evs = [], [], []
+    for n, a in enumerate(facs):
+        with torch.cuda.stream(main if n == 0 else f1s):
+            if nts[n] < int(a.shape[0]):
+                at = (_spectral_rows_dev(a, eps_two, delta_n, seeds[2 * n], config.effective_alpha)
+                      / math.sqrt(1.0 - eps_two)).contiguous()
+            else:
+                at = a
+            gts.append(_gram_dev(at))
+            tildes.append(at)
+            ev = torch.cuda.Event()
+            ev.record()
+            evs.append(ev)
+    e0s, e1s = _side_stream(0), _side_stream(10)
+    e0s.wait_event(evs[0])
+    e1s.wait_event(evs[1])
+    r0, ev_e0 = _eig_on(e0s, gts[0])
+    r1, ev_e1 = _eig_on(e1s, gts[1])
+    grams_h = ("per-factor", [r0, r1], [ev_e0, ev_e1])
+    ready = [None, evs[1]]
     b_raw = D.empty(max(s, 1))
     gst = _side_stream(11)
-    _, _, _, _, _, g2 = _jl_and_sampling(facs, facs, gts, eps_jl, config, True, seeds, s, ready, (b, b_raw, gst),
-                                         pre_g)
+    _, _, _, _, _, g2 = _jl_and_sampling(facs, tildes, gts, eps_jl, config, True, seeds, s, ready,
+                                         (b, b_raw, gst), pre_g)
     sd_idx, sd_val, seg, lrow, rrow, cdev, first_raw = g2
     main.wait_stream(gst)
     b_at = D.empty(s)  # b at the sparse-diagonal rows = b_raw at each entry's first draw
@@ -635,7 +645,8 @@ def _solve_graph_body(facs, b, config: RegressionConfig, s: int, factor1_stream=
               float(config.residual_tol), D.p(x), D.p(hist), D.p(rhs), D.p(state), D.p(plan_ws), D.stream())
     ev1.record()
     return dict(x=x, hist=hist, state=state, loop_events=(ev0, ev1),
-                keep=(gts, b_at, b_raw, first_raw, sd_idx, sd_val, seg, lrow, rrow, cdev, rhs, plan_ws, pre_g))
+                keep=(gts, tildes, b_at, b_raw, first_raw, sd_idx, sd_val, seg, lrow, rrow, cdev, rhs, plan_ws,
+                      pre_g))
 
 
 def _fast_solve_graph(facs, b, config: RegressionConfig):
@@ -687,8 +698,8 @@ def _fast_solve_graph(facs, b, config: RegressionConfig):
     _mark("richardson")
     try:
         deferred.run(synced=True)
-    except _CholeskyFailed:
-        return None  # the eager path retries with LU inverses
+    except (_CholeskyFailed, _lev.ScoresFallback):
+        return None  # the eager path retries (LU inverses / compact-SVD scores)
     status, iters, hlen = (int(v) for v in st_h[:3].tolist())
     history = hist_h[:hlen].tolist()
     if status == 2:
@@ -725,13 +736,9 @@ def _host_graph_key(factors, b, config: RegressionConfig):
     rows = math.prod(int(a.shape[0]) for a in factors)
     if int(b.numel()) != rows:
         return None  # the regular path raises the reference's error
-    eps_one = math.log1p(config.eps / 4.0) / 2
-    eps_two = eps_one / (2.0 + eps_one)
-    delta_n = config.delta / 4.0
     for a in factors:
         n, d = int(a.shape[0]), int(a.shape[1])
-        if d not in (16, 32, 64) or n < 16 or \
-                math.ceil(config.effective_alpha * spectral_sample_count(d, eps_two, delta_n)) < n:
+        if d not in (16, 32, 64) or n < 16:
             return None
     if config.effective_max_iters > 1024:
         return None
@@ -822,8 +829,8 @@ def _fast_solve_host_graph(factors, b, config: RegressionConfig, with_loss: bool
     _mark("richardson")
     try:
         deferred.run(synced=True)
-    except _CholeskyFailed:
-        return None  # the regular path retries with LU inverses
+    except (_CholeskyFailed, _lev.ScoresFallback):
+        return None  # the regular path retries (LU inverses / compact-SVD scores)
     status, iters, hlen = (int(v) for v in st_h[:3].tolist())
     if status == 2:
         raise NumericalFailureError("Richardson iteration diverged", iterations=iters,

@@ -313,3 +313,30 @@ def test_host_pinned_factor_graph_matches_device_path():
     facs_pin[1][5, 3] = 1.0
     r = K.fast_kronecker_regression(facs_pin, b_pin, cfg)  # the graph is still usable afterwards
     assert np.all(np.isfinite(np.asarray(r.solution)))
+
+
+def test_spectral_branch_graph_matches_eager_and_oracle():
+    """n = 16384, d = 16: per-factor spectral row sampling is active (s_n < n).  The whole-solve graph
+    (spectral rows, Grams, eigensolves and JL chains per factor on their own streams) equals the
+    eager pipeline bit for bit, and its sketch equals the oracle's."""
+    import paper_2209_04876_b200 as K
+    from paper_2209_04876_b200 import solvers as S
+    from paper_2209_04876_b200.solvers import FastSolveTrace
+    n, d = 16384, 16
+    facs, _ = O.synth_regression(n, d, 2, 0)
+    b = np.random.default_rng(5).standard_normal(n * n)
+    fd = [torch.tensor(a, device="cuda") for a in facs]
+    bd = torch.tensor(b, device="cuda")
+    tr = FastSolveTrace()
+    ref = K.fast_kronecker_regression(fd, bd, cfg(), _trace=tr)  # eager
+    assert all(r < n for r in tr.a_tilde_rows)  # spectral branch
+    oref = O.fast_kronecker_regression(facs, b, with_loss=False, eps=0.1, delta=0.01, lam=1e-3, alpha=1e-5, seed=0)
+    np.testing.assert_array_equal(tr.sdiag.indices.cpu().numpy(), oref.trace["sd_indices"])
+    assert ref.iterations == oref.iterations
+    S._SOLVE_GRAPHS.clear()
+    before = dict(S._SOLVE_STATS)
+    outs = [K.fast_kronecker_regression(fd, bd, cfg()) for _ in range(4)]
+    assert S._SOLVE_STATS["capture"] == before["capture"] + 1
+    for rep in outs:
+        assert rep.iterations == ref.iterations
+        assert torch.equal(rep.solution, ref.solution)
