@@ -208,3 +208,43 @@ def sharded_kronmatmul_svd_solve(factors, b_rows, lam: float, plan: ShardPlan, d
     X = x.reshape(int(facs[0].shape[1]), int(facs[1].shape[1]))
     r2 = sk.residual_sumsq(facs[0], X, facs[1], b_rows)
     return x, r2 + lam * float((x * x).sum().item())
+
+
+def sharded_fast_kronecker_regression(factors, b_rows, config, plan: ShardPlan, caches=None):
+    """fast_kronecker_regression (solvers.py:372-462) with b row-sharded over the ranks.
+
+    Every rank holds both factors and its rows [lo, hi) of the n0 x n1 reshape of b (``b_rows``,
+    device, (hi - lo) x n1).  The sketch and the preconditioner are computed replicated (identical
+    NumPy-exact streams, so every rank draws the same sketch); each rank keeps the sampled rows
+    whose factor-0 index it owns, gathers their b entries locally, and the Richardson loop
+    all-reduces the d^2 normal-operator partial once per iteration (sharded_richardson).  Returns
+    (x, iterations, history).  With one rank it is the single-GPU algorithm through the
+    per-iteration kernels."""
+    import math
+
+    import torch
+
+    from . import _device as D
+    from .kron import SparseDiagonal, sketched_kron_apply, sketched_kron_transpose_apply
+    from .solvers import FactorGram, _fast_sketch_dev, _validated_problem, build_kron_preconditioner
+
+    if len(factors) != 2:
+        raise ValueError("the row-sharded fast solve covers the two-factor problem")
+    n0, n1 = int(factors[0].shape[0]), int(factors[1].shape[0])
+    facs = [D.to_dev(a) for a in factors]
+    sdiag, grams, s = _fast_sketch_dev(facs, config, caches)
+    lo, hi = plan.rows
+    keys = sdiag.indices
+    own = (keys >= lo * n1) & (keys < hi * n1)
+    li, lv = keys[own].contiguous(), sdiag.values[own].contiguous()
+    local = SparseDiagonal._trusted(li, lv)
+    b_at = b_rows.reshape(-1)[li - lo * n1].contiguous()
+    rhs_local = sketched_kron_transpose_apply(facs, local, (lv * b_at).contiguous())
+    pre = build_kron_preconditioner([FactorGram(v=v, eigenvalues=w, matrix=None) for v, w in grams], config.lam)
+
+    def normal_local(x):
+        return sketched_kron_transpose_apply(facs, local, sketched_kron_apply(facs, local, x))
+
+    x, iters, hist = sharded_richardson(normal_local, pre.apply, rhs_local, config.effective_damping,
+                                        config.effective_max_iters, config.residual_tol, torch, config.lam)
+    return x, iters, hist

@@ -845,6 +845,27 @@ def _fast_solve_host_graph(factors, b, config: RegressionConfig, with_loss: bool
     return SolveReport(solution=x_h.numpy().copy(), loss=loss, iterations=iters, sample_count=s, wall_time=wall)
 
 
+def _fast_sketch_dev(facs, config: RegressionConfig, caches=None):
+    """The sketch and the preconditioner's factor eigendecompositions of fast_kronecker_regression
+    (solvers.py:404-452) without the solve: (sparse diagonal, [(V_n, w_n)], s).  Deterministic: every
+    rank of a row-sharded solve computes the same sketch."""
+    from . import leverage as _lev
+    use_chol, fast_scores = True, True
+    for _attempt in range(3):
+        deferred = _lev.DeferredChecks()
+        _lev._DEFERRED[0] = deferred
+        try:
+            return _fast_solve_pass(facs, None, config, caches, None, use_chol, deferred, fast_scores,
+                                    sketch_only=True)
+        except _CholeskyFailed:
+            use_chol = False
+        except _lev.ScoresFallback:
+            fast_scores = False
+        finally:
+            _lev._DEFERRED[0] = None
+    raise AssertionError("unreachable")
+
+
 def _fast_solve_dev(facs, b, config: RegressionConfig, caches, trace: FastSolveTrace | None = None):
     """The device pipeline of solvers.py:404-459; returns (x natural order, iterations, s)."""
     from . import leverage as _lev
@@ -1037,7 +1058,7 @@ def _mark(name: str):
 
 
 def _fast_solve_pass(facs, b, config: RegressionConfig, caches, trace, use_chol: bool, deferred,
-                     fast_scores: bool = True):
+                     fast_scores: bool = True, sketch_only: bool = False):
     from . import leverage as _lev
     _mark("start")
     n_factors = len(facs)
@@ -1113,6 +1134,11 @@ def _fast_solve_pass(facs, b, config: RegressionConfig, caches, trace, use_chol:
     else:
         sdiag = sparse_diagonal_from_sketch(RowSketch(draws, w), rows)
     _mark("sparse diagonal")
+    if sketch_only:  # the replicated front half of a row-sharded solve (distributed.py)
+        grams = _join_grams(grams)
+        _lev._DEFERRED[0] = None
+        deferred.run()
+        return sdiag, grams, s
     idx = sdiag.indices
     if isinstance(b, torch.Tensor) and b.is_cuda:
         b_at = D.empty(sdiag.nnz)

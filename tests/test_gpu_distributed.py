@@ -60,3 +60,30 @@ def test_sharded_row_blocks_sum_to_full_contraction():
     full = ops.contract(L, B, R)
     np.testing.assert_allclose((parts[0] + parts[1]).cpu().numpy(), full.cpu().numpy(), rtol=1e-11, atol=1e-9)
     np.testing.assert_allclose(full.cpu().numpy(), facs[0].T @ b @ facs[1], rtol=1e-10, atol=1e-8)
+
+
+def test_sharded_fast_solve_nccl_world1():
+    """The row-sharded fast solve (replicated sketch, rank-local samples, one d^2 all-reduce per
+    Richardson iteration) over an NCCL world of one equals the single-GPU solve (same sketch, same
+    iterations; the loop runs through the per-iteration kernels, so x agrees to the floor)."""
+    import torch
+    import torch.distributed as dist
+    import paper_2209_04876_b200 as K
+    from paper_2209_04876_b200.distributed import ShardPlan, sharded_fast_kronecker_regression
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(_port())
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        n, d = 4096, 32
+        facs, _ = O.synth_regression(n, d, 2, 0)
+        b = np.random.default_rng(4).standard_normal(n * n)
+        cfg = K.RegressionConfig(eps=0.1, delta=0.01, lam=1e-3, alpha=1e-5, seed=0)
+        plan = ShardPlan(1, 0, n)
+        lo, hi = plan.rows
+        b_rows = torch.tensor(b.reshape(n, n)[lo:hi], device="cuda")
+        x, iters, hist = sharded_fast_kronecker_regression(facs, b_rows, cfg, plan)
+        ref = K.fast_kronecker_regression(facs, b, cfg)
+        assert iters == ref.iterations
+        assert rel(x, ref.solution) <= 1e-8
+    finally:
+        dist.destroy_process_group()
