@@ -16,6 +16,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 import time
 from dataclasses import dataclass, replace
 from functools import reduce
@@ -541,7 +542,7 @@ def _eig_on(stream, g):
     return (v[0], w[0]), ev
 
 
-_NO_PREDRAW = [bool(__import__("os").environ.get("KS_NO_PREDRAW"))]
+_NO_PREDRAW = [bool(os.environ.get("KS_NO_PREDRAW"))]
 
 
 def _tilde_rows(facs, config: RegressionConfig):
