@@ -393,10 +393,19 @@ def _factor_grams_async(gts: list[torch.Tensor]):
             outs = [(v[i], w[i]) for i in range(len(gts))]
             keep = [w, v]
         else:
-            for g in gts:
-                vv, ww, gs = _factor_gram_dev(g)
-                outs.append((vv, ww))
             keep = []
+            for g in gts:
+                d = int(g.shape[0])
+                if d <= 128:  # the same symmetric eigensolver as the batched / graph paths
+                    w = D.empty(1, d)
+                    v = D.empty(1, d, d)
+                    _lib.call("ks_sym_eig_batched", 1, _lib.ptr_array(ctypes.c_void_p, [g.data_ptr()]), d, D.p(w),
+                              D.p(v), D.stream())
+                    outs.append((v[0], w[0]))
+                    keep += [w, v]
+                else:
+                    vv, ww, gs = _factor_gram_dev(g)
+                    outs.append((vv, ww))
     if not torch.cuda.is_current_stream_capturing():
         for g in gts:
             g.record_stream(side)

@@ -340,3 +340,24 @@ def test_spectral_branch_graph_matches_eager_and_oracle():
     for rep in outs:
         assert rep.iterations == ref.iterations
         assert torch.equal(rep.solution, ref.solution)
+
+
+@pytest.mark.parametrize("n1,n2,d1,d2", [(3000, 2500, 16, 32), (2048, 2048, 64, 16), (2500, 2100, 24, 40),
+                                         (1800, 1500, 48, 8)])
+def test_fast_regression_mixed_widths_vs_oracle(n1, n2, d1, d2):
+    """Unequal factor shapes: graph + persistent-loop paths (widths 16/32/64, any pairing) and the
+    per-iteration path (other widths), against the oracle; later calls (graph replays) repeat the
+    first call's result bit for bit."""
+    import paper_2209_04876_b200 as K
+    rs = np.random.default_rng(n1 + d1)
+    facs = [rs.normal(1.0, math.sqrt(1e-3), (n1, d1)), rs.normal(1.0, math.sqrt(1e-3), (n2, d2))]
+    b = rs.standard_normal(n1 * n2)
+    c = K.RegressionConfig(eps=0.1, delta=0.01, lam=1e-3, alpha=1e-5, seed=3)
+    fd = [torch.tensor(a, device="cuda") for a in facs]
+    bd = torch.tensor(b, device="cuda")
+    reps = [K.fast_kronecker_regression(fd, bd, c) for _ in range(3)]
+    o = O.fast_kronecker_regression(facs, b, eps=0.1, delta=0.01, lam=1e-3, alpha=1e-5, seed=3, with_loss=False)
+    for r in reps:
+        assert r.sample_count == o.sample_count and r.iterations == o.iterations
+        assert torch.equal(r.solution, reps[0].solution)
+    assert rel(reps[0].solution, o.solution) <= 1e-7
