@@ -539,19 +539,29 @@ def _solve_graph_key(facs, b, config: RegressionConfig):
     return key
 
 
-def _eig_on(stream, g):
+def _eig_on(stream, g, tl=None, name=""):
     d = int(g.shape[0])
     w = D.empty(1, d)
     v = D.empty(1, d, d)
     with torch.cuda.stream(stream):
         _lib.call("ks_sym_eig_batched", 1, _lib.ptr_array(ctypes.c_void_p, [g.data_ptr()]), d, D.p(w), D.p(v),
                   D.stream())
+    _tl_event(tl, name, stream)
     ev = torch.cuda.Event()
     ev.record(stream)
     return (v[0], w[0]), ev
 
 
 _NO_PREDRAW = [bool(os.environ.get("KS_NO_PREDRAW"))]
+_TIMELINE = [bool(os.environ.get("KS_GRAPH_TIMELINE"))]  # external events at the solve graph's joins
+
+
+def _tl_event(tl, name, stream=None):
+    if tl is None:
+        return
+    ev = torch.cuda.Event(enable_timing=True, external=True)
+    ev.record(stream if stream is not None else torch.cuda.current_stream())
+    tl.append((name, ev))
 
 
 def _tilde_rows(facs, config: RegressionConfig):
@@ -599,6 +609,8 @@ def _solve_graph_body(facs, b, config: RegressionConfig, s: int, factor1_stream=
     eps_jl = 4.0 * math.log1p(config.eps / 4.0) / 2
     d0, d1 = int(facs[0].shape[1]), int(facs[1].shape[1])
     main = torch.cuda.current_stream()
+    tl = [] if _TIMELINE[0] else None
+    _tl_event(tl, "start")
     if pre_g is None and not _NO_PREDRAW[0]:
         pre_g = _predraw_jl_sketches(facs, config, seeds)
     # per factor, on its own stream as soon as the factor exists: the spectral row sample when it
@@ -623,8 +635,10 @@ def _solve_graph_body(facs, b, config: RegressionConfig, s: int, factor1_stream=
     e0s, e1s = _side_stream(0), _side_stream(10)
     e0s.wait_event(evs[0])
     e1s.wait_event(evs[1])
-    r0, ev_e0 = _eig_on(e0s, gts[0])
-    r1, ev_e1 = _eig_on(e1s, gts[1])
+    _tl_event(tl, "gram0", e0s)
+    _tl_event(tl, "gram1", e1s)
+    r0, ev_e0 = _eig_on(e0s, gts[0], tl, "eig0")
+    r1, ev_e1 = _eig_on(e1s, gts[1], tl, "eig1")
     grams_h = ("per-factor", [r0, r1], [ev_e0, ev_e1])
     ready = [None, evs[1]]
     b_raw = D.empty(max(s, 1))
@@ -632,7 +646,9 @@ def _solve_graph_body(facs, b, config: RegressionConfig, s: int, factor1_stream=
     _, _, _, _, _, g2 = _jl_and_sampling(facs, tildes, gts, eps_jl, config, True, seeds, s, ready,
                                          (b, b_raw, gst), pre_g)
     sd_idx, sd_val, seg, lrow, rrow, cdev, first_raw = g2
+    _tl_event(tl, "sketch")
     main.wait_stream(gst)
+    _tl_event(tl, "b gathered")
     b_at = D.empty(s)  # b at the sparse-diagonal rows = b_raw at each entry's first draw
     _lib.call("ks_gather_count", D.p(b_raw), D.p(first_raw), D.p(cdev), s, D.p(b_at), D.stream())
     struct = _lib.SketchView(facs[0].data_ptr(), d0, d0, facs[1].data_ptr(), d1, d1, s, s, seg.data_ptr(),
@@ -640,6 +656,7 @@ def _solve_graph_body(facs, b, config: RegressionConfig, s: int, factor1_stream=
     # the loop's work plan needs only the sketch: built while the eigensolves still run
     plan_ws = torch.empty(int(_lib.load().ks_richardson_plan_bytes(s, s)), dtype=torch.uint8, device=D.dev())
     _lib.call("ks_richardson_plan_async", ctypes.byref(struct), D.p(cdev), D.p(plan_ws), D.stream())
+    _tl_event(tl, "plan")
     (VL, wL), (VR, wR) = _join_grams(grams_h)
     max_iters = config.effective_max_iters
     x = D.empty(d0, d1)
@@ -654,9 +671,43 @@ def _solve_graph_body(facs, b, config: RegressionConfig, s: int, factor1_stream=
               D.p(VR), D.p(wR), None, float(config.lam), float(config.effective_damping), int(max_iters),
               float(config.residual_tol), D.p(x), D.p(hist), D.p(rhs), D.p(state), D.p(plan_ws), D.stream())
     ev1.record()
-    return dict(x=x, hist=hist, state=state, loop_events=(ev0, ev1),
+    _tl_event(tl, "loop end")
+    return dict(x=x, hist=hist, state=state, loop_events=(ev0, ev1), timeline=tl,
                 keep=(gts, tildes, b_at, b_raw, first_raw, sd_idx, sd_val, seg, lrow, rrow, cdev, rhs, plan_ws,
                       pre_g))
+
+
+class _PackedChecks:
+    """Every deferred flag word and the loop state of a solve graph, packed inside the graph into one
+    int32 buffer: one device-to-host copy per replay (into a page-locked buffer allocated once)
+    instead of one copy per flag.  Handlers run in registration order, as DeferredChecks does."""
+
+    def __init__(self, checks, state, hist):
+        self.slices = []
+        parts, off = [], 0
+        for f, h in checks:
+            n = int(f.numel())
+            parts.append(f.reshape(-1).to(torch.int32))
+            self.slices.append((off, n, h))
+            off += n
+        self.state_off = off
+        parts.append(state.reshape(-1).to(torch.int32))
+        self.buf = torch.cat(parts)  # a graph node: refreshed by every replay
+        self.host = torch.empty(int(self.buf.numel()), dtype=torch.int32).pin_memory()
+        self.hist = hist
+        self.hist_host = torch.empty(int(hist.numel()), dtype=torch.float64).pin_memory()
+
+    def fetch(self):
+        self.host.copy_(self.buf, non_blocking=True)
+        self.hist_host.copy_(self.hist, non_blocking=True)
+
+    def run(self):
+        """After a synchronisation: run the handlers; returns (status, iterations, hist_len, history)."""
+        v = self.host.tolist()
+        for off, n, h in self.slices:
+            h(v[off:off + n])
+        status, iters, hlen = v[self.state_off:self.state_off + 3]
+        return status, iters, hlen, self.hist_host[:hlen].tolist()
 
 
 def _fast_solve_graph(facs, b, config: RegressionConfig):
@@ -683,6 +734,7 @@ def _fast_solve_graph(facs, b, config: RegressionConfig):
         try:
             with torch.cuda.graph(g):
                 entry.out = _solve_graph_body(facs, b.reshape(-1), config, s)
+                entry.packed = _PackedChecks(cap.items, entry.out["state"], entry.out["hist"])
         except Exception:
             _SOLVE_GRAPHS.pop(key, None)
             raise
@@ -697,21 +749,14 @@ def _fast_solve_graph(facs, b, config: RegressionConfig):
     _LAST_LOOP_EVENTS[0] = entry.out["loop_events"]
     entry.graph.replay()
     out = entry.out
-    deferred = _lev.DeferredChecks()
-    for flags, handler in entry.checks:
-        deferred.add(flags, handler)
-    deferred.stage()
-    st_h = out["state"].to("cpu", non_blocking=True)
-    hist_h = out["hist"].to("cpu", non_blocking=True)
+    entry.packed.fetch()
     x = out["x"].reshape(-1).clone()
     torch.cuda.current_stream().synchronize()
     _mark("richardson")
     try:
-        deferred.run(synced=True)
+        status, iters, hlen, history = entry.packed.run()
     except (_CholeskyFailed, _lev.ScoresFallback):
         return None  # the eager path retries (LU inverses / compact-SVD scores)
-    status, iters, hlen = (int(v) for v in st_h[:3].tolist())
-    history = hist_h[:hlen].tolist()
     if status == 2:
         raise NumericalFailureError("Richardson iteration diverged", iterations=iters,
                                     diagnostics={"residual_history": history})
@@ -817,6 +862,10 @@ def _fast_solve_host_graph(factors, b, config: RegressionConfig, with_loss: bool
                           D.stream())
                 entry.out = _solve_graph_body(entry.dev, b.reshape(-1), config, s, factor1_stream=side, pre_g=pre_g)
                 main.wait_stream(side)
+                # the factor validation flags first: the reference validates before solving
+                entry.packed = _PackedChecks([(entry.flags.reshape(-1), _validation_handler(len(factors)))]
+                                             + cap.items, entry.out["state"], entry.out["hist"])
+                entry.x_host = torch.empty(int(entry.out["x"].numel()), dtype=torch.float64).pin_memory()
         except Exception:
             _HOST_GRAPHS.pop(key, None)
             raise
@@ -827,24 +876,18 @@ def _fast_solve_host_graph(factors, b, config: RegressionConfig, with_loss: bool
     _LAST_LOOP_EVENTS[0] = entry.out["loop_events"]
     entry.graph.replay()
     out = entry.out
-    deferred = _lev.DeferredChecks()
-    deferred.add(entry.flags.reshape(-1), _validation_handler(len(factors)))  # the reference validates first
-    for flags, handler in entry.checks:
-        deferred.add(flags, handler)
-    deferred.stage()
-    st_h = out["state"].to("cpu", non_blocking=True)
-    hist_h = out["hist"].to("cpu", non_blocking=True)
-    x_h = out["x"].reshape(-1).to("cpu", non_blocking=True)
+    entry.packed.fetch()
+    entry.x_host.copy_(out["x"].reshape(-1), non_blocking=True)
     torch.cuda.current_stream().synchronize()
     _mark("richardson")
     try:
-        deferred.run(synced=True)
+        status, iters, hlen, history = entry.packed.run()
     except (_CholeskyFailed, _lev.ScoresFallback):
         return None  # the regular path retries (LU inverses / compact-SVD scores)
-    status, iters, hlen = (int(v) for v in st_h[:3].tolist())
+    x_h = entry.x_host
     if status == 2:
         raise NumericalFailureError("Richardson iteration diverged", iterations=iters,
-                                    diagnostics={"residual_history": hist_h[:hlen].tolist()})
+                                    diagnostics={"residual_history": history})
     _mark("solve_end")
     wall = time.perf_counter() - t0
     if with_loss:
