@@ -554,6 +554,7 @@ def _eig_on(stream, g, tl=None, name=""):
 
 _NO_PREDRAW = [bool(os.environ.get("KS_NO_PREDRAW"))]
 _TIMELINE = [bool(os.environ.get("KS_GRAPH_TIMELINE"))]  # external events at the solve graph's joins
+_TL_CUR = [None]  # the timeline being captured
 
 
 def _tl_event(tl, name, stream=None):
@@ -610,6 +611,7 @@ def _solve_graph_body(facs, b, config: RegressionConfig, s: int, factor1_stream=
     d0, d1 = int(facs[0].shape[1]), int(facs[1].shape[1])
     main = torch.cuda.current_stream()
     tl = [] if _TIMELINE[0] else None
+    _TL_CUR[0] = tl
     _tl_event(tl, "start")
     if pre_g is None and not _NO_PREDRAW[0]:
         pre_g = _predraw_jl_sketches(facs, config, seeds)
@@ -672,6 +674,7 @@ def _solve_graph_body(facs, b, config: RegressionConfig, s: int, factor1_stream=
               float(config.residual_tol), D.p(x), D.p(hist), D.p(rhs), D.p(state), D.p(plan_ws), D.stream())
     ev1.record()
     _tl_event(tl, "loop end")
+    _TL_CUR[0] = None
     return dict(x=x, hist=hist, state=state, loop_events=(ev0, ev1), timeline=tl,
                 keep=(gts, tildes, b_at, b_raw, first_raw, sd_idx, sd_val, seg, lrow, rrow, cdev, rhs, plan_ws,
                       pre_g))
@@ -1016,10 +1019,13 @@ def _jl_and_sampling(facs, tildes, gts, eps_jl: float, config: RegressionConfig,
             scores[n].record_stream(main)
     for cs in chol_st:
         main.wait_stream(cs)
+    _tl_event(_TL_CUR[0], "jl scores")
     sampler = ProductSampler([LeverageScores(sc, 0.0, af) for sc, af in zip(scores, afs)])
+    _tl_event(_TL_CUR[0], "sampler tables")
     state, inc = pcg64_state(seeds[-1])
     draws = sampler._sample_dev(s, state, inc)
     w = sampler._weights_dev(draws, s)
+    _tl_event(_TL_CUR[0], "draws")
     # two factors: the sparse diagonal and its grouped view are built here too (launch-only)
     if raw_b is not None and _USE_FUSED[0] and grouped2_eligible(facs):
         # raw_b = (b, out): b read at the raw draws on a side stream while the sketch is sorted and
