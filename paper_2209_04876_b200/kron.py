@@ -208,6 +208,13 @@ def kron_rows(factors: Sequence, multi_indices) -> torch.Tensor:
     mi = D.to_dev(multi_indices, D.I64)
     if mi.ndim == 1:
         mi = mi[None, :]
+    if factors and mi.numel():
+        # NumPy fancy-indexing rules (negative indices wrap, anything else out of range raises
+        # IndexError) checked before the gather, so a bad index never becomes a device fault.
+        rows = torch.tensor([int(a.shape[0]) for a in factors], dtype=D.I64, device=mi.device)
+        cols = mi[:, :len(factors)]
+        if mi.shape[1] < len(factors) or bool(((cols < -rows) | (cols >= rows)).any()):
+            raise IndexError("multi-index out of range for the Kronecker factors")
     acc = D.zeros(mi.shape[0], 1) + 1.0
     for n, a in enumerate(factors):
         at = D.to_dev(a)

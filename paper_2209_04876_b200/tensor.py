@@ -200,3 +200,46 @@ def pseudo_inverse(a, rank_tol: float = DEFAULT_RANK_TOL):
     """Moore-Penrose inverse via the compact SVD (tensor.py:110-115)."""
     host = not D.on_device(a)
     return D.out(_pinv_dev(as_matrix(a), rank_tol), host)
+
+
+EXPLICIT_KRON_MAX_ENTRIES = 10 ** 7
+
+
+def explicit_kron(factors: Sequence, max_entries: int = EXPLICIT_KRON_MAX_ENTRIES):
+    """Dense ``A1 kron ... kron AN`` (tensor.py:186-198): the reference's test-oracle path, kept
+    size-guarded; built on the device by successive outer products."""
+    if len(factors) == 0:
+        raise InvalidInputError("need at least one factor")
+    from .errors import SizeGuardError
+    host = not any(D.on_device(a) for a in factors)
+    mats = [as_matrix(a, f"factor {n}") for n, a in enumerate(factors)]
+    rows = math.prod(int(a.shape[0]) for a in mats)
+    cols = math.prod(int(a.shape[1]) for a in mats)
+    if rows * cols > max_entries:
+        raise SizeGuardError(f"explicit Kronecker product would hold {rows}x{cols} entries "
+                             f"(guard: {max_entries})")
+    acc = mats[0]
+    for a in mats[1:]:
+        acc = (acc[:, None, :, None] * a[None, :, None, :]).reshape(acc.shape[0] * a.shape[0], -1)
+    return D.out(acc.contiguous(), host)
+
+
+def stack_columns(m):
+    """Column-major flatten for the vec-trick identities (tensor.py:201-203)."""
+    if isinstance(m, torch.Tensor):
+        return m.to(torch.float64).T.reshape(-1)
+    return np.asarray(m, dtype=np.float64).reshape(-1, order="F")
+
+
+def unstack_columns(v, shape):
+    """Inverse of :func:`stack_columns` for a (rows, cols) shape (tensor.py:206-213)."""
+    rows, cols = shape
+    if isinstance(v, torch.Tensor):
+        t = v.to(torch.float64).reshape(-1)
+        if t.numel() != rows * cols:
+            raise InvalidInputError(f"vector of length {t.numel()} cannot fill a {rows}x{cols} matrix")
+        return t.reshape(cols, rows).T
+    a = np.asarray(v, dtype=np.float64).reshape(-1)
+    if a.size != rows * cols:
+        raise InvalidInputError(f"vector of length {a.size} cannot fill a {rows}x{cols} matrix")
+    return a.reshape((rows, cols), order="F")
