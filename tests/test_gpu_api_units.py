@@ -248,3 +248,39 @@ def test_tucker_model_metrics(rng):
     m.factors = [np.zeros_like(a) for a in m.factors]
     x = rng.standard_normal((4, 3))
     assert K.regularized_loss(m, x) == pytest.approx(float(np.sum(x ** 2)), rel=1e-12)
+
+
+# ---------------------------------------------------------------------------
+# exact solve properties and the generic Richardson loop on device tensors (solvers.py:201-248)
+# ---------------------------------------------------------------------------
+
+def test_exact_solve_residual_orthogonality_and_loss(rng):
+    import paper_2209_04876_b200 as K
+    facs = [rng.standard_normal((8, 3)), rng.standard_normal((6, 2))]
+    b = rng.standard_normal(48)
+    k = dense_kron(facs)
+    rep = K.kronmatmul_svd_solve(facs, b, 0.0)
+    assert np.linalg.norm(k.T @ (k @ rep.solution - b)) <= 1e-8 * np.linalg.norm(b)
+    rep = K.kronmatmul_svd_solve(facs, b, 0.1)
+    assert rep.loss == pytest.approx(K.ridge_loss(facs, rep.solution, b, 0.1), abs=1e-10)
+    want = np.sum((k @ rep.solution - b) ** 2) + 0.1 * np.sum(rep.solution ** 2)
+    assert rep.loss == pytest.approx(want, rel=1e-12)
+
+
+def test_richardson_on_device_tensors(rng):
+    import paper_2209_04876_b200 as K
+    a = torch.tensor(rng.standard_normal((8, 3)), device="cuda")
+    b = torch.tensor(rng.standard_normal(8), device="cuda")
+    ata = a.T @ a
+    m = 2.0 * ata
+    minv = torch.linalg.inv(m)
+    xs = torch.linalg.lstsq(a.cpu(), b.cpu()[:, None]).solution[:, 0].cuda()
+    its = []
+    x, it = K.richardson_solve(lambda v: ata @ v, lambda v: minv @ v, a.T @ b, 1.0,
+                               K.RegressionConfig(eps=0.25, max_richardson_iters=10, residual_tol=1e-300),
+                               callback=lambda xk: its.append(xk.clone()))
+    assert x.is_cuda and it == 10
+    e0 = float(torch.sqrt(xs @ m @ xs))
+    for j, xk in enumerate(its, start=1):
+        d = xk - xs
+        assert float(torch.sqrt(d @ m @ d)) <= 0.5 ** j * e0 * (1 + 1e-10) + 1e-12
