@@ -546,8 +546,10 @@ def synth_regression(n, d, order=2, seed=0):
     return facs, np.ones(n ** order)
 
 
-def synth_tucker(shape, rank, noise_std, seed=0):
-    """experiments.py:118-131 consumption order, absolute noise (BASELINE.json config 5)."""
+def synth_tucker(shape, rank, noise_std, seed=0, relative=False):
+    """experiments.py:118-131 consumption order.  Absolute noise N(0, noise_std^2) by default
+    (BASELINE.json config 5); ``relative=True`` is generate_synth_tucker's own scaling,
+    noise * ||x|| / sqrt(x.size) (experiments.py:128-130)."""
     gen = np.random.default_rng(seed)
     core = gen.standard_normal(tuple(rank))
     facs = []
@@ -558,7 +560,8 @@ def synth_tucker(shape, rank, noise_std, seed=0):
     for mode, a in enumerate(facs):
         x = np.moveaxis(np.tensordot(a, x, axes=(1, mode)), 0, mode)
     if noise_std > 0:
-        x = x + gen.standard_normal(x.shape) * noise_std
+        scale = noise_std * float(np.linalg.norm(x)) / math.sqrt(x.size) if relative else noise_std
+        x = x + gen.standard_normal(x.shape) * scale
     return x
 
 

@@ -164,7 +164,7 @@ def test_tucker_monotone_and_full_rank_interpolation():
 def test_sketched_als_quality_10_seeds():
     hits = 0
     for seed in range(10):
-        x = O.synth_tucker((20, 20, 20), (4, 4, 4), 0.01, seed)
+        x = O.synth_tucker((20, 20, 20), (4, 4, 4), 0.01, seed, relative=True)
         _, exact = K().tucker_als(x, (4, 4, 4), lam=0.0, sweeps=5, solver_mode="exact",
                                   config=K().RegressionConfig(seed=seed))
         _, fast = K().tucker_als(x, (4, 4, 4), lam=0.0, sweeps=5, solver_mode="fast",

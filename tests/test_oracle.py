@@ -127,3 +127,18 @@ def test_dense_baselines_match_live_reference():
         o = O.sketch_and_solve_ridge(facs, b, eps=0.5, lam=lam, seed=4)
         np.testing.assert_array_equal(o.solution, r.solution)
         assert o.sample_count == r.sample_count
+
+
+@pytest.mark.skipif(not REFERENCE_SRC.exists(), reason="reference not mounted (GPU box)")
+def test_synth_generators_match_live_reference():
+    """The input generators the tests use follow experiments.py bit for bit."""
+    sys.path.insert(0, str(REFERENCE_SRC))
+    from kronsolve.experiments import generate_synth_regression, generate_synth_tucker
+    for seed in (0, 3):
+        np.testing.assert_array_equal(O.synth_tucker((9, 7, 5), (3, 2, 2), 0.01, seed, relative=True),
+                                      generate_synth_tucker((9, 7, 5), (3, 2, 2), 0.01, seed))
+        facs, b = O.synth_regression(64, 4, 2, seed)
+        rf, rb = generate_synth_regression(64, 4, 2, seed=seed)
+        np.testing.assert_array_equal(b, rb)
+        for a, r in zip(facs, rf):
+            np.testing.assert_array_equal(a, r)
