@@ -9,6 +9,7 @@ SparseDiagonal object."""
 from __future__ import annotations
 
 import ctypes
+import functools
 import itertools
 import math
 from dataclasses import dataclass, field
@@ -110,6 +111,11 @@ def balanced_partition(col_dims: Sequence[int]) -> FactorPartition:
             f"factors, got {len(dims)}")
     if min(dims) < 1:
         raise InvalidInputError("column dimensions must be positive")
+    return _partition_of(tuple(dims))
+
+
+@functools.lru_cache(maxsize=256)
+def _partition_of(dims: tuple) -> FactorPartition:
     total = math.prod(dims)
     key_best, left_best = None, None
     for size in range(len(dims) + 1):

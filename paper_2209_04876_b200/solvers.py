@@ -713,12 +713,13 @@ class _PackedChecks:
         return status, iters, hlen, self.hist_host[:hlen].tolist()
 
 
-def _fast_solve_graph(facs, b, config: RegressionConfig):
+def _fast_solve_graph(facs, b, config: RegressionConfig, key=None):
     """(x natural order, iterations, s) from the whole-solve graph, or None when this call has to
     run eagerly (ineligible input, or the first sight of a key: the eager pass warms every lazy
     initialisation before capture)."""
     from . import leverage as _lev
-    key = _solve_graph_key(facs, b, config)
+    if key is None:
+        key = _solve_graph_key(facs, b, config)
     if key is None:
         return None
     entry = _SOLVE_GRAPHS.get(key)
@@ -736,8 +737,21 @@ def _fast_solve_graph(facs, b, config: RegressionConfig):
         _lev._DEFERRED[0] = cap
         try:
             with torch.cuda.graph(g):
+                # the factors' finite / nonzero validation rides in the graph on a side stream (off
+                # the critical path); its flags lead the packed read-back, so a replay on new
+                # contents at the same addresses raises the reference's error before any result
+                main = torch.cuda.current_stream()
+                flags = torch.zeros(len(facs), 2, dtype=torch.int32, device=D.dev())
+                vst = _side_stream(24)
+                vst.wait_stream(main)
+                with torch.cuda.stream(vst):
+                    flags.zero_()
+                    for n, a in enumerate(facs):
+                        _lib.call("ks_check_finite_nonzero", D.p(a), a.numel(), D.p(flags[n]), D.stream())
                 entry.out = _solve_graph_body(facs, b.reshape(-1), config, s)
-                entry.packed = _PackedChecks(cap.items, entry.out["state"], entry.out["hist"])
+                main.wait_stream(vst)
+                entry.packed = _PackedChecks([(flags.reshape(-1), _validation_handler(len(facs)))] + cap.items,
+                                             entry.out["state"], entry.out["hist"])
         except Exception:
             _SOLVE_GRAPHS.pop(key, None)
             raise
@@ -1290,8 +1304,8 @@ def fast_kronecker_regression(factors: Sequence, b, config: RegressionConfig,
     exactly afterwards (``with_loss=False`` skips it: loss = nan; an extension for timing).  With host-resident ``b`` only its sampled entries are transferred
     for the solve; the loss pass then uploads it."""
     host = not D.on_device(b)
-    if caches is None and _trace is None and host:
-        got = _fast_solve_host_graph(factors, b, config, with_loss)
+    if caches is None and _trace is None:
+        got = (_fast_solve_host_graph if host else _fast_solve_dev_replay)(factors, b, config, with_loss)
         if got is not None:
             return got
     facs, rows, cols = _validated_problem(factors, b)
@@ -1324,6 +1338,41 @@ def fast_kronecker_regression(factors: Sequence, b, config: RegressionConfig,
     else:
         loss = float("nan")
     return SolveReport(solution=D.out(x, host), loss=loss, iterations=iters, sample_count=s, wall_time=wall)
+
+
+def _fast_solve_dev_replay(factors, b, config: RegressionConfig, with_loss: bool):
+    """fast_kronecker_regression for device-resident inputs whose whole-solve graph is already
+    captured: host-side shape checks only, then one replay (the factor validation is a graph node,
+    its flags read back with the results), so no synchronising validation round trip precedes the
+    solve.  None: not eligible / not captured yet (the regular path validates eagerly)."""
+    if not 0.0 < config.eps <= 0.25 or len(factors) != 2:
+        return None
+    for a in factors:
+        if not (isinstance(a, torch.Tensor) and a.is_cuda and a.dtype == torch.float64 and a.ndim == 2
+                and a.is_contiguous()):
+            return None
+    if not (isinstance(b, torch.Tensor) and b.is_cuda and b.dtype == torch.float64 and b.is_contiguous()):
+        return None
+    facs = list(factors)
+    rows, cols = kron_operator_shape(facs)
+    if int(b.numel()) != rows or _regression_sample_count(cols, config) >= rows:
+        return None
+    bsrc = b.reshape(-1)
+    key = _solve_graph_key(facs, bsrc, config)
+    entry = _SOLVE_GRAPHS.get(key) if key is not None else None
+    if entry is None or entry.graph is None:
+        return None
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    _mark("t0")
+    got = _fast_solve_graph(facs, bsrc, config, key)
+    if got is None:
+        return None
+    x, iters, s = got
+    _mark("solve_end")
+    wall = time.perf_counter() - t0
+    loss = _ridge_loss_dev(facs, x, bsrc, config.lam) if with_loss else float("nan")
+    return SolveReport(solution=x, loss=loss, iterations=iters, sample_count=s, wall_time=wall)
 
 
 def _pinv_sym_dev(m: torch.Tensor) -> torch.Tensor:

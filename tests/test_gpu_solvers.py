@@ -315,6 +315,46 @@ def test_host_pinned_factor_graph_matches_device_path():
     assert np.all(np.isfinite(np.asarray(r.solution)))
 
 
+def test_device_graph_replay_validates_in_graph():
+    """Device-resident inputs: once the whole-solve graph is captured, later calls replay it with the
+    factor validation as a graph node (no synchronising pre-check); new invalid contents at the same
+    addresses still raise the reference's errors, and valid contents give the eager result."""
+    import torch
+    import paper_2209_04876_b200 as K
+    from paper_2209_04876_b200 import solvers as S
+    from paper_2209_04876_b200.errors import InvalidInputError
+    n, d = 4096, 32
+    rng = np.random.default_rng(1)
+    facs = [torch.tensor(rng.normal(1.0, np.sqrt(1e-3), (n, d)), device="cuda") for _ in range(2)]
+    b = torch.tensor(rng.standard_normal(n * n), device="cuda")
+    c = K.RegressionConfig(eps=0.1, delta=0.01, lam=1e-3, alpha=1e-5, seed=0)
+    S._SOLVE_GRAPHS.clear()
+    outs = [K.fast_kronecker_regression(facs, b, c) for _ in range(4)]
+    key = S._solve_graph_key(facs, b, c)
+    assert key is not None and S._SOLVE_GRAPHS[key].graph is not None
+    for r in outs[1:]:
+        assert torch.equal(r.solution, outs[0].solution) and r.iterations == outs[0].iterations
+    replays = S._SOLVE_STATS["replay"]
+    facs[1][7, 2] = float("nan")
+    with pytest.raises(InvalidInputError, match="factor 1 contains non-finite"):
+        K.fast_kronecker_regression(facs, b, c)
+    facs[1][7, 2] = float("-inf")
+    with pytest.raises(InvalidInputError, match="factor 1 contains non-finite"):
+        K.fast_kronecker_regression(facs, b, c)
+    assert S._SOLVE_STATS["replay"] == replays + 2  # both rejected by the in-graph check
+    facs[1][7, 2] = 1.0
+    keep = facs[0].clone()
+    facs[0].zero_()
+    with pytest.raises(InvalidInputError, match="factor 0 is identically zero"):
+        K.fast_kronecker_regression(facs, b, c)
+    facs[0].copy_(keep)
+    facs[1][7, 2] = outs[0].solution.new_tensor(0.0) + float(np.asarray(rng.normal(1.0, 0.0316)))
+    r = K.fast_kronecker_regression(facs, b, c)
+    S._SOLVE_GRAPHS.clear()
+    e = K.fast_kronecker_regression(facs, b, c)  # eager (first sight of the key)
+    assert torch.equal(r.solution, e.solution) and r.iterations == e.iterations
+
+
 def test_spectral_branch_graph_matches_eager_and_oracle():
     """n = 16384, d = 16: per-factor spectral row sampling is active (s_n < n).  The whole-solve graph
     (spectral rows, Grams, eigensolves and JL chains per factor on their own streams) equals the
