@@ -280,6 +280,7 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
   }
 
   int status = 0, iters = 0, hlen = 0;
+  double my_rhs = 0.0, my_dv = 0.0;  // eigenbasis mode: this thread's reduce element (see P2)
   const bool prof = (b == 0 && tid == 0);
   long long p1acc[4] = {0, 0, 0, 0};
   // it == -1: the right-hand-side pass (same chunk pipeline, s_t = v_t (v_t b_t), no Y)
@@ -542,21 +543,24 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
         if (ql == 0) {
           const int i = e / DR, k = e - i * DR;
           if (a.eig_mode) {
-            // eigenbasis: step' = dinv o (G' + lam x' - rhs'), plus this CTA's share of ||step'||^2
+            // eigenbasis: step' = dinv o (G' + lam x' - rhs'), plus this CTA's share of ||step'||^2.
+            // A thread owns at most one element of the CTA's slice (epc <= PT / 8): its rhs' and
+            // dinv entries are formed in the right-hand-side pass and kept in registers.
             double r;
             if (rp) {
               r = s + cmp;
               a.rhs[e] = r;
+              if (a.dinv) {
+                my_dv = __ldg(&a.dinv[e]);
+              } else {
+                const double ev = __dadd_rn(__dmul_rn(__ldg(&a.wL[i]), __ldg(&a.wR[k])), a.lam);
+                my_dv = ev > 0.0 ? __ddiv_rn(1.0, ev) : 0.0;
+              }
+              my_rhs = r;
             } else {
-              r = __dsub_rn(__dadd_rn(s + cmp, __dmul_rn(a.lam, Xs[i * DRP + k])), __ldcg(&a.rhs[e]));
+              r = __dsub_rn(__dadd_rn(s + cmp, __dmul_rn(a.lam, Xs[i * DRP + k])), my_rhs);
             }
-            double dv;
-            if (a.dinv) {
-              dv = __ldg(&a.dinv[e]);
-            } else {
-              const double ev = __dadd_rn(__dmul_rn(__ldg(&a.wL[i]), __ldg(&a.wR[k])), a.lam);
-              dv = ev > 0.0 ? __ddiv_rn(1.0, ev) : 0.0;
-            }
+            const double dv = my_dv;
             const double st = r * dv;
             if (!rp) a.step[e] = st;
             eig_sq = fma(st, st, eig_sq);
@@ -1105,6 +1109,8 @@ int richardson_persistent(cudaStream_t st, const ks_sketch_view* sk, const doubl
   Scratch<int> state_s(state_dev ? 0 : 4, st);
   int* statep = state_dev ? state_dev : state_s.p;
   KS_REQUIRE(eig_mode <= rhs_in_kernel, KS_EINVAL, "the eigenbasis loop builds its own right-hand side");
+  KS_REQUIRE(!eig_mode || ((((int64_t)dL * dR + grid - 1) / grid + 1) & ~1) <= PT / 8, KS_ESIZE,
+             "eigenbasis loop: at most one reduce element per thread (too few SMs for d_L * d_R)");
   KS_REQUIRE(Lpack.p && Rpack.p && part.p && R.p && T.p && stepb.p && rowsq.p && VRt.p && chunks_p && range_p &&
                  (plan_ws || cpre.p) && statep && (!eig_mode || rhs_e.p),
              KS_ECUDA, "scratch allocation failed");
