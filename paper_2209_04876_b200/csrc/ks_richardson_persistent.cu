@@ -167,6 +167,7 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
   if (tid == 0) {
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
+    mbar_init(&bars[2], 1);  // the reduce operands
     fence_barrier_init();
   }
   for (int e = tid; e < DL * DRP; e += PT) Xs[e] = 0.0;
@@ -177,6 +178,7 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
 
   const int64_t c_beg = a.range[b], c_end = a.range[b + 1];
   uint32_t phase[2] = {0, 0};
+  uint32_t p2phase = 0;
   int pending[2] = {0, 0};
   const bool resident = (c_end - c_beg) == 1;
   int cur = 0;  // buffer holding the next chunk to consume
@@ -482,18 +484,25 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
     }
     // the buffer holding the next pass's first chunk (in flight); the other one is free
     if (!resident) cur = (int)((base + nch) & 1);
-    double* P = a.part + (size_t)b * NE;
+    // partials in reducer-major order: element e of CTA b's partial goes to the slice of its
+    // reducer c = e / epc at part[(c G + b) epc + e - c epc], so a reducer's G x epc operands are
+    // one contiguous block (one bulk copy); element pairs (e even) stay 16-byte stores
+    const int epc = ((NE + G - 1) / G + 1) & ~1;
 #pragma unroll
     for (int gi = 0; gi < G_PER_W; gi++) {
       const int tile = warp + gi * PW;
       if (tile < G_TILES) {
         const int m0 = (tile / GT_N) * 16, n0 = (tile % GT_N) * 8;
-        P[(m0 + g) * DR + n0 + 2 * t4] = gacc[gi][0];
-        P[(m0 + g) * DR + n0 + 2 * t4 + 1] = gacc[gi][1];
-        P[(m0 + g + 8) * DR + n0 + 2 * t4] = gacc[gi][2];
-        P[(m0 + g + 8) * DR + n0 + 2 * t4 + 1] = gacc[gi][3];
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          const int e = (m0 + g + 8 * h) * DR + n0 + 2 * t4;
+          const int c = e / epc;
+          *reinterpret_cast<double2*>(a.part + ((size_t)c * G + b) * epc + (e - c * epc)) =
+              make_double2(gacc[gi][2 * h], gacc[gi][2 * h + 1]);
+        }
       }
     }
+    asm volatile("fence.proxy.async.global;" ::: "memory");  // read back by the async (bulk-copy) proxy
     if (prof && !rp) g_prof[it * 6 + 1] = clock64();
     KS_STAMP(1)
     grid.sync();
@@ -504,18 +513,18 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
     {
       // this CTA's slice of every partial is staged in shared memory with cp.async (all copies in
       // flight at once), then 8 threads per element sum the G partials in a fixed order
-      const int epc = ((NE + G - 1) / G + 1) & ~1;
       const int e0 = b * epc, e1 = min(NE, e0 + epc);
       const int ne_cta = e1 > e0 ? e1 - e0 : 0;
       double* P2s = sm + S::R_OFF + (cur ^ 1) * CH_S * DRP;  // G x epc
-      {
-        const int npair = ne_cta / 2;
-        for (int k = tid; k < G * npair; k += PT) {
-          const int p = k / npair, j = 2 * (k - p * npair);
-          cp_async16(P2s + p * epc + j, a.part + (size_t)p * NE + e0 + j);
+      if (ne_cta > 0) {
+        if (tid == 0) {
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+          const uint32_t bytes = (uint32_t)(G * epc * 8);
+          mbar_arrive_expect_tx(&bars[2], bytes);
+          bulk_copy(P2s, a.part + (size_t)b * G * epc, bytes, &bars[2]);
         }
-        cp_async_wait_all();
-        __syncthreads();
+        mbar_wait(&bars[2], p2phase);
+        p2phase ^= 1;
       }
       const int ql = lane & 7;
       const unsigned qmask = 0xffu << (lane & 24);
@@ -1098,7 +1107,8 @@ int richardson_persistent(cudaStream_t st, const ks_sketch_view* sk, const doubl
   const int64_t nnz = sk->nnz, ul = sk->u_left;
   const int grid = num_sms();
   const int64_t cap = plan_cap(ul, nnz);  // >= chunk count
-  Scratch<double> Lpack(ul * dLp + 2, st), Rpack(nnz * dRp + 2, st), part((int64_t)grid * dL * dR, st);
+  const int64_t epc = (((int64_t)dL * dR + grid - 1) / grid + 1) & ~1;  // reduce slice per CTA
+  Scratch<double> Lpack(ul * dLp + 2, st), Rpack(nnz * dRp + 2, st), part((int64_t)grid * grid * epc, st);
   Scratch<double> R((int64_t)dL * dR, st), T((int64_t)dL * dR, st), stepb((int64_t)dL * dR, st),
       rowsq(dL > grid ? dL : grid, st), rhs_e(eig_mode ? (int64_t)dL * dR : 0, st);
   Scratch<double> VRt((int64_t)dR * dR, st);
