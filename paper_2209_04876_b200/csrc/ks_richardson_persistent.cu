@@ -571,7 +571,7 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
             }
             const double dv = my_dv;
             const double st = r * dv;
-            if (!rp) a.step[e] = st;
+            if (!rp) a.step[i * DRP + k] = st;  // padded rows: the readers fetch it with one bulk copy
             eig_sq = fma(st, st, eig_sq);
           } else if (rp) {
             a.rhs[e] = s + cmp;
@@ -585,15 +585,25 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
         if (tid == 0) a.rowsq[b] = eig_sq;
       }
     }
+    if (a.eig_mode) asm volatile("fence.proxy.async.global;" ::: "memory");
     KS_STAMP(3)
     grid.sync();
     KS_STAMP(4)
     if (a.eig_mode) {
       // every CTA: ||step'|| from the G partials (fixed order) and, past the rhs pass, the step
+      // (DL x DRP padded rows, one bulk copy into the free slab buffer)
       double* St = sm + S::R_OFF + (cur ^ 1) * CH_S * DRP;
-      if (!rp) stage(St, a.step, DL, DR, DRP, true);
+      if (!rp && tid == 0) {
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        const uint32_t bytes = (uint32_t)(DL * DRP * 8);
+        mbar_arrive_expect_tx(&bars[2], bytes);
+        bulk_copy(St, a.step, bytes, &bars[2]);
+      }
       for (int q = tid; q < G; q += PT) Ws[q] = __ldcg(&a.rowsq[q]);  // G <= 148 < 192
-      cp_async_wait_all();
+      if (!rp) {
+        mbar_wait(&bars[2], p2phase);
+        p2phase ^= 1;
+      }
       __syncthreads();
       if (warp == 0) {
         double t = 0.0;
@@ -1109,7 +1119,7 @@ int richardson_persistent(cudaStream_t st, const ks_sketch_view* sk, const doubl
   const int64_t cap = plan_cap(ul, nnz);  // >= chunk count
   const int64_t epc = (((int64_t)dL * dR + grid - 1) / grid + 1) & ~1;  // reduce slice per CTA
   Scratch<double> Lpack(ul * dLp + 2, st), Rpack(nnz * dRp + 2, st), part((int64_t)grid * grid * epc, st);
-  Scratch<double> R((int64_t)dL * dR, st), T((int64_t)dL * dR, st), stepb((int64_t)dL * dR, st),
+  Scratch<double> R((int64_t)dL * dR, st), T((int64_t)dL * dR, st), stepb((int64_t)dL * dRp, st),
       rowsq(dL > grid ? dL : grid, st), rhs_e(eig_mode ? (int64_t)dL * dR : 0, st);
   Scratch<double> VRt((int64_t)dR * dR, st);
   Scratch<Chunk> dch(plan_ws ? 0 : cap, st);
