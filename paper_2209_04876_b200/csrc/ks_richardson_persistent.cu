@@ -645,9 +645,24 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
         status = 2;
         break;
       }
-      for (int e = tid; e < NE; e += PT) {
-        const int i = e / DR, k = e - i * DR;
-        Xs[i * DRP + k] = __dsub_rn(Xs[i * DRP + k], __dmul_rn(a.damping, St[i * DRP + k]));
+      {
+        // all loads first (the compiler cannot reorder shared loads past the stores: St and Xs
+        // may alias as far as it knows), then the updates
+        constexpr int UPT = (NE + PT - 1) / PT;
+        double sv[UPT], xv[UPT];
+#pragma unroll
+        for (int q = 0; q < UPT; q++) {
+          const int e = tid + q * PT, i = e / DR, k = e - i * DR;
+          if (e < NE) {
+            sv[q] = St[i * DRP + k];
+            xv[q] = Xs[i * DRP + k];
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < UPT; q++) {
+          const int e = tid + q * PT, i = e / DR, k = e - i * DR;
+          if (e < NE) Xs[i * DRP + k] = __dsub_rn(xv[q], __dmul_rn(a.damping, sv[q]));
+        }
       }
       iters = it + 1;
       __syncthreads();
