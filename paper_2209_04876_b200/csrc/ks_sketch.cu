@@ -677,18 +677,42 @@ extern "C" int ks_sketch_diag_grouped2(const int64_t* idx, const int64_t* row_sh
 }
 
 namespace {
+// Grid-stride, GATHER_ILP independent reads in flight per thread.  With page-locked host b every
+// read is one PCIe request and the gather is request-rate bound (~3.8 ns per read on the B200
+// boxes, independent of reads in flight per thread or block size: tools/hostgather_bench.cu), so
+// a small grid reaches the same rate while leaving the other SMs' memory pipelines to the sketch
+// kernels that run beside it.
+constexpr int GATHER_ILP = 8;
 __global__ void gather_draws2_kernel(const double* __restrict__ b, const int64_t* __restrict__ draws, int64_t n1,
                                      int64_t s, double* __restrict__ out) {
-  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= s) return;
-  out[q] = b[draws[2 * q] * n1 + draws[2 * q + 1]];
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t q0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q0 < s; q0 += stride * GATHER_ILP) {
+    double v[GATHER_ILP];
+#pragma unroll
+    for (int k = 0; k < GATHER_ILP; k++) {
+      const int64_t q = q0 + k * stride;
+      v[k] = q < s ? b[draws[2 * q] * n1 + draws[2 * q + 1]] : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < GATHER_ILP; k++) {
+      const int64_t q = q0 + k * stride;
+      if (q < s) out[q] = v[k];
+    }
+  }
 }
 }  // namespace
 
 extern "C" int ks_gather_draws2(const double* b, const int64_t* draws, int64_t n1, int64_t s, double* out,
                                 void* stream) {
   if (s <= 0) return KS_OK;
-  gather_draws2_kernel<<<ceil_div_u(s, 128), 128, 0, (cudaStream_t)stream>>>(b, draws, n1, s, out);
+  static const int max_blocks = [] {
+    const char* e = getenv("KS_GATHER_BLOCKS");  // diagnostic switch (A/B of the grid size)
+    return e ? atoi(e) : 0;
+  }();
+  // default: one read per thread over the whole grid (measured best beside the sketch kernels)
+  int64_t nb = max_blocks > 0 ? ceil_div_u(s, 256 * GATHER_ILP) : ceil_div_u(s, 256);
+  if (max_blocks > 0 && nb > max_blocks) nb = max_blocks;
+  gather_draws2_kernel<<<(int)nb, 256, 0, (cudaStream_t)stream>>>(b, draws, n1, s, out);
   KS_CHECK_LAUNCH();
   return KS_OK;
 }

@@ -649,16 +649,17 @@ def _solve_graph_body(facs, b, config: RegressionConfig, s: int, factor1_stream=
                                          (b, b_raw, gst), pre_g)
     sd_idx, sd_val, seg, lrow, rrow, cdev, first_raw = g2
     _tl_event(tl, "sketch")
+    struct = _lib.SketchView(facs[0].data_ptr(), d0, d0, facs[1].data_ptr(), d1, d1, s, s, seg.data_ptr(),
+                             lrow.data_ptr(), rrow.data_ptr(), sd_val.data_ptr())
+    # the loop's work plan needs only the sketch: built while the eigensolves and the b gather
+    # still run
+    plan_ws = torch.empty(int(_lib.load().ks_richardson_plan_bytes(s, s)), dtype=torch.uint8, device=D.dev())
+    _lib.call("ks_richardson_plan_async", ctypes.byref(struct), D.p(cdev), D.p(plan_ws), D.stream())
+    _tl_event(tl, "plan")
     main.wait_stream(gst)
     _tl_event(tl, "b gathered")
     b_at = D.empty(s)  # b at the sparse-diagonal rows = b_raw at each entry's first draw
     _lib.call("ks_gather_count", D.p(b_raw), D.p(first_raw), D.p(cdev), s, D.p(b_at), D.stream())
-    struct = _lib.SketchView(facs[0].data_ptr(), d0, d0, facs[1].data_ptr(), d1, d1, s, s, seg.data_ptr(),
-                             lrow.data_ptr(), rrow.data_ptr(), sd_val.data_ptr())
-    # the loop's work plan needs only the sketch: built while the eigensolves still run
-    plan_ws = torch.empty(int(_lib.load().ks_richardson_plan_bytes(s, s)), dtype=torch.uint8, device=D.dev())
-    _lib.call("ks_richardson_plan_async", ctypes.byref(struct), D.p(cdev), D.p(plan_ws), D.stream())
-    _tl_event(tl, "plan")
     (VL, wL), (VR, wR) = _join_grams(grams_h)
     max_iters = config.effective_max_iters
     x = D.empty(d0, d1)
@@ -1045,11 +1046,20 @@ def _jl_and_sampling(facs, tildes, gts, eps_jl: float, config: RegressionConfig,
         # raw_b = (b, out): b read at the raw draws on a side stream while the sketch is sorted and
         # deduplicated (the read may cross PCIe: page-locked host b); joined by the caller
         b, b_raw, gst = raw_b
-        gst.wait_stream(main)
-        with torch.cuda.stream(gst):
-            _lib.call("ks_gather_draws2", D.p(b), D.p(draws), int(facs[1].shape[0]), s, D.p(b_raw), D.stream())
+        # the gather is issued after the sketch kernels: run beside them, the scattered reads (one
+        # PCIe request each when b is page-locked host memory) slow both down, and the sum is the
+        # same (tools/graph_timeline.py --host); the loop plan then overlaps the gather
+        after = os.environ.get("KS_GATHER_BESIDE_SKETCH") != "1"
+        if not after:
+            gst.wait_stream(main)
+            with torch.cuda.stream(gst):
+                _lib.call("ks_gather_draws2", D.p(b), D.p(draws), int(facs[1].shape[0]), s, D.p(b_raw), D.stream())
         first_raw = D.empty(max(s, 1), dtype=D.I64)
         g2 = sketch_diag_grouped2_launch(facs, draws, w, first_raw) + (first_raw,)
+        if after:
+            gst.wait_stream(main)
+            with torch.cuda.stream(gst):
+                _lib.call("ks_gather_draws2", D.p(b), D.p(draws), int(facs[1].shape[0]), s, D.p(b_raw), D.stream())
         return scores, afs, sampler, draws, w, g2
     g2 = sketch_diag_grouped2_launch(facs, draws, w) if _USE_FUSED[0] and grouped2_eligible(facs) else None
     return scores, afs, sampler, draws, w, g2
