@@ -294,10 +294,6 @@ int ks_richardson_fused_async(const ks_sketch_view* sk, const int64_t* counts_de
 int64_t ks_richardson_plan_bytes(int64_t u_left_cap, int64_t nnz_cap);
 int ks_richardson_plan_async(const ks_sketch_view* sk, const int64_t* counts_dev, void* plan_ws, void* stream);
 
-/* Profiling aid: per-CTA %globaltimer stamps (ns) of iteration 5 of the last persistent
- * Richardson run, 9 per CTA (phase boundaries and grid-barrier exits). */
-int ks_debug_richardson_cta_stamps(int32_t nctas, uint64_t* out);
-
 /* Profiling aid: globaltimer stamps (ns) of CTA 0 of the last ks_jl_projection: entry,
  * operands staged, Cholesky done, exit. */
 int ks_debug_jl_projection_stamps(uint64_t* out4);
@@ -311,13 +307,19 @@ int ks_debug_jacobi_stamps(long long* out4);
 /* Profiling aid: cycles of the FP32 prelude, its FP64 transition and the FP64 rounds (CTA 0). */
 int ks_debug_jacobi_mix(long long* out3);
 
-/* Profiling aid: average SM cycles per phase of the last persistent Richardson run (CTA 0):
- * apply, sync, reduce, precond-A, precond-B, update. */
+/* Profiling aid: with on != 0, later launches of the phase-separated eigenbasis Richardson loop
+ * run its profiling instantiation (CTA 0 records clock64 at every phase boundary); the product
+ * path runs the instantiation without instrumentation.  Process-wide, default off. */
+int ks_debug_richardson_profile(int32_t on);
+
+/* Profiling aid: average SM cycles per phase of the last profiled eigenbasis loop run
+ * (CTA 0): apply, flag barrier 1, reduce, flag barrier 2, norm + stop rules + x update, loop
+ * overhead. */
 int ks_debug_richardson_phases(int32_t iters, double* out6);
 
-/* Profiling aid: CTA 0's apply phase of the last persistent run split into mbarrier wait, Y GEMM,
- * sample loop and G GEMM (average SM cycles per iteration). */
-int ks_debug_richardson_apply_split(int32_t iters, double* out4);
+/* Profiling aid: CTA 0's apply phase of the last profiled run split per iteration (SM cycles):
+ * L load wait, Y phase, sample phase, G phase (out8[4..7] unused). */
+int ks_debug_richardson_apply_split(int32_t iters, double* out8);
 
 /* Preconditioner apply y = (VL kron VR) diag(dinv) (VL kron VR)^T r (solvers.py:180-183). */
 int ks_kron_precond_apply(const double* VL, const double* VR, int32_t dL, int32_t dR,

@@ -7,11 +7,12 @@ the functions on the north-star path.  It is the *checker*: only ``tests/``,
 ``--impl reference`` arm) may import it.  The product package
 ``paper_2209_04876_b200`` never imports or calls anything in ``oracle/``.
 
-Parity pinning: ``tests/test_oracle_vs_reference.py`` checks every function
-here against the real reference (when /root/reference is present, i.e. in the
-build container) and ``tests/test_oracle_golden.py`` against the committed
-fixtures in ``tests/golden/`` that were produced by running the reference
-itself (``tests/golden/make_golden.py``).
+Parity pinning: ``tests/test_oracle.py`` checks the functions here against the
+real reference (when /root/reference is present, i.e. in the build container)
+and against the committed fixtures in ``tests/golden/`` that were produced by
+running the reference itself (``tests/golden/make_golden.py`` for c1-c3/c5,
+``tests/golden/make_golden_c4.py`` for c4); ``tests/test_rng_oracle.py`` pins
+the PCG64 / ziggurat restatement in ``rng_oracle.py`` against NumPy.
 
 Each function cites the reference file:line it restates.  The floating-point
 operation order follows the reference (same NumPy calls in the same order) so
@@ -445,14 +446,21 @@ def sample_count(cols, eps, delta, alpha):
 
 def fast_kronecker_regression(factors, b, eps=0.25, delta=0.05, lam=0.0, alpha=1.0, seed=0,
                               max_iters=None, residual_tol=1e-9, damping=None,
-                              jl_log_factor=JL_LOG_FACTOR, caches=None, with_loss=True):
+                              jl_log_factor=JL_LOG_FACTOR, caches=None, with_loss=True, b_at=None):
     """Algorithm 1 -- solvers.py:372-462.
 
     ``caches`` is a list of (svd, (v, eigenvalues, gram)) tuples (FactorCache).
+    ``b_at``: optional callable idx -> b[idx] replacing the read of b at the sparse-diagonal
+    rows (solvers.py:448), for right-hand sides too large to hold (BASELINE c4: 34 GB); then
+    ``b`` may be None and ``with_loss`` must be False.
     ``trace`` holds every intermediate the GPU path is compared on."""
     import time
     mats = [np.asarray(a, dtype=np.float64) for a in factors]
-    b = np.asarray(b, dtype=np.float64).reshape(-1)
+    if b_at is None:
+        b = np.asarray(b, dtype=np.float64).reshape(-1)
+        b_at = b.__getitem__
+    elif with_loss:
+        raise OracleError("invalid", "b_at needs with_loss=False")
     nf = len(mats)
     rows = math.prod(a.shape[0] for a in mats)
     cols = math.prod(a.shape[1] for a in mats)
@@ -500,7 +508,7 @@ def fast_kronecker_regression(factors, b, eps=0.25, delta=0.05, lam=0.0, alpha=1
     idx, w = sample_rows(sampler, s, seeds[-1])
     row_shape = tuple(a.shape[0] for a in mats)
     sd_idx, sd_val = sparse_diagonal_from_sketch(idx, w, row_shape)
-    rhs = sketched_kron_transpose_apply(mats, sd_idx, sd_val, sd_val * b[sd_idx])
+    rhs = sketched_kron_transpose_apply(mats, sd_idx, sd_val, sd_val * np.asarray(b_at(sd_idx), dtype=np.float64))
 
     def normal(x):
         return sketched_kron_transpose_apply(mats, sd_idx, sd_val,

@@ -69,7 +69,6 @@ _SIGS = {
     "ks_debug_jacobi_stamps": ([_p], ctypes.c_int),
     "ks_debug_jacobi_mix": ([_p], ctypes.c_int),
     "ks_debug_jacobi_sweeps": ([_p], ctypes.c_int),
-    "ks_debug_richardson_cta_stamps": ([_i32, _p], ctypes.c_int),
     "ks_row_weighted_sumsq": ([_p, _i64, _i32, _p, _p, _p], ctypes.c_int),
     "ks_sampler_tables": ([_p, _i64, _i32, _p, _p, _p, _p], ctypes.c_int),
     "ks_sampler_tables_batched": ([_i32, _p, _p, _i32, _p, _p, _p, _p], ctypes.c_int),
@@ -88,6 +87,7 @@ _SIGS = {
                                 POINTER(c_int32), POINTER(c_int32), _p], ctypes.c_int),
     "ks_kron_precond_apply": ([_p, _p, _i32, _i32, _p, _p, _p, _p], ctypes.c_int),
     "ks_debug_richardson_phases": ([_i32, POINTER(c_double)], ctypes.c_int),
+    "ks_debug_richardson_profile": ([_i32], ctypes.c_int),
     "ks_debug_richardson_apply_split": ([_i32, POINTER(c_double)], ctypes.c_int),
     "ks_pcg64_random_streams": ([_p, _i32, _i64, _i32, _i64, _p, _p], ctypes.c_int),
     "ks_factor_draws_rows": ([_i32, _p, _p, _p, _p, _i64, _i64, _p, _p, _p], ctypes.c_int),

@@ -29,6 +29,17 @@ int cuda_status(cudaError_t e, const char* what) {
   return KS_ECUDA;
 }
 
+static std::once_flag g_env_once;
+static const char* g_env[ENV_COUNT];
+
+const char* env(EnvSwitch id) {
+  static const char* const names[ENV_COUNT] = {"KS_TALL", "KS_KRON2", "KS_RICHARDSON", "KS_NO_EIGBASIS", "KS_GRAM_SCALAR", "KS_GATHER_BLOCKS", "KS_TSQR", "KS_JACOBI_FP32", "KS_JACOBI_GENERIC", "KS_RICH_OLD"};
+  std::call_once(g_env_once, [] {
+    for (int i = 0; i < ENV_COUNT; i++) g_env[i] = getenv(names[i]);
+  });
+  return g_env[id];
+}
+
 static std::once_flag g_pool_once;
 
 void* scratch_alloc(size_t bytes, cudaStream_t s) {
@@ -314,7 +325,7 @@ int gemm_tn_tall(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha,
     return KS_OK;
   }
   {
-    const char* e = getenv("KS_TALL");
+    const char* e = ks::env(ks::ENV_TALL);
     if (!(e && e[0] == 'g')) return gemm_tn_tall_dmma(st, M, N, K, alpha, A, a_ks, a_ms, B, b_ks, b_ns, C);
   }
   int64_t nparts = (K + 63) / 64;

@@ -23,7 +23,7 @@ int kron2_residual_dmma(cudaStream_t st, const double* L, const double* X, const
 }
 
 static bool generic_forced() {
-  const char* e = getenv("KS_KRON2");
+  const char* e = ks::env(ks::ENV_KRON2);
   return e && e[0] == 'g';
 }
 

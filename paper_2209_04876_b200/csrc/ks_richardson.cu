@@ -221,7 +221,7 @@ extern "C" int ks_richardson_sketched(const ks_sketch_view* sk, const double* VL
   cudaStream_t st = (cudaStream_t)stream;
   const int dL = sk->dL, dR = sk->dR;
   KS_REQUIRE(dL >= 1 && dR >= 1 && dL <= 128 && dR <= 128, KS_ESIZE, "group widths must be <= 128");
-  const char* mode = getenv("KS_RICHARDSON");
+  const char* mode = ks::env(ks::ENV_RICHARDSON);
   const bool force_multi = mode && mode[0] == 'm';
   if (!force_multi && sk->nnz > 0 && ks::persistent_supported(dL, dR) && max_iters <= 1024) {
     int status = 0;
@@ -299,7 +299,7 @@ extern "C" int ks_richardson_fused(const ks_sketch_view* sk, const int64_t* perm
   int status = 0, it = 0, hl = 0;
   int rc = ks::richardson_persistent(st, sk, VL, VR, dinv, wL, wR, rhs_out, true, b_at, perm, lam, damping,
                                      max_iters, residual_tol, x, hist, &it, &hl, &status, nullptr, nullptr,
-                                     !getenv("KS_NO_EIGBASIS"), nullptr);
+                                     !ks::env(ks::ENV_NO_EIGBASIS), nullptr);
   if (rc) return rc;
   *iters = it;
   *hist_len = hl;
@@ -338,5 +338,5 @@ extern "C" int ks_richardson_fused_async(const ks_sketch_view* sk, const int64_t
   int status = 0, it = 0, hl = 0;
   return ks::richardson_persistent(st, sk, VL, VR, dinv, wL, wR, rhs_out, true, b_at, perm, lam, damping, max_iters,
                                    residual_tol, x, hist, &it, &hl, &status, counts_dev, state_dev,
-                                   !getenv("KS_NO_EIGBASIS"), plan_ws);
+                                   !ks::env(ks::ENV_NO_EIGBASIS), plan_ws);
 }

@@ -15,8 +15,7 @@
 //   divergence rules and updates its shared-memory copy of x.
 // Four grid-wide barriers per iteration; no host round trips.  Chunks are assigned to CTAs
 // in contiguous ranges of equal estimated cost (static, so results are deterministic).
-#include "ks_common.cuh"
-#include "ks_tma.cuh"
+#include "ks_persistent.cuh"
 
 #include <cooperative_groups.h>
 #include <vector>
@@ -28,55 +27,7 @@ namespace {
 
 constexpr int PT = 256;      // threads per CTA
 constexpr int PW = PT / 32;  // warps
-constexpr int CH_ROWS = 16;  // distinct left rows per chunk (one half-warp each)
-constexpr int CH_S = 64;     // samples per chunk (>= DL: the free slab holds a DL x DRP matrix)
-constexpr int PAD = 4;       // row padding (doubles) of packed / staged rows
-
-struct Chunk {
-  int64_t u_b, u_e;  // left rows [u_b, u_e)
-  int64_t t_b, t_e;  // samples  [t_b, t_e)
-};
-
-struct PArgs {
-  const double* Lpack;    // u_left x (DL+PAD)
-  const double* Rpack;    // nnz x (DR+PAD); pad slot 0 carries v_t
-  const int64_t* seg;     // u_left + 1
-  const Chunk* chunks;
-  const int64_t* range;   // grid + 1: chunk range of every CTA
-  const double* VL;       // DL x DL
-  const double* VR;       // DR x DR
-  const double* VRt;      // DR x DR
-  const double* dinv;     // DL x DR, or null: dinv(i, j) = pseudo-reciprocal(wL[i] wR[j] + lam)
-  const double* wL;       // DL (eigenvalues of the left factor's Gram) when dinv is null
-  const double* wR;       // DR
-  double* rhs;            // DL x DR (input, or output when rhs_in_kernel)
-  int rhs_in_kernel;      // pass -1 builds rhs = sum_t v_t (v_t b_t) L_u R_t^T (Rpack pad slot 1 = v_t b_t)
-  int eig_mode;           // the packed rows are L VL / R VR: the loop runs in the preconditioner's
-                          // eigenbasis, where the preconditioner is the diagonal dinv (no P3/P4)
-  double* rhs_nat_out;    // eig_mode: VL rhs' VR^T (natural-order right-hand side), may be null
-  double lam, damping, residual_tol;
-  int max_iters;
-  double* part;           // grid x DL x DR
-  double* R;              // DL x DR
-  double* T;              // DL x DR
-  double* step;           // DL x DR
-  double* rowsq;          // DL
-  double* x_out;          // DL x DR
-  double* hist;           // max_iters
-  int* state;             // [status, iters, hist_len]
-};
-
-__device__ long long g_prof[6 * 1024];
-__device__ long long g_p1split[4];  // CTA 0, summed over iterations: mbarrier wait, Y, samples, G
-__device__ unsigned long long g_cta_ts[256 * 9];  // per-CTA globaltimer stamps of iteration 5
-
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-#define KS_STAMP(k) \
-  if (it == 5 && tid == 0 && b < 256) g_cta_ts[b * 9 + (k)] = gtimer();
+using namespace ks_rich;
 
 template <int DL, int DR>
 struct Smem {
@@ -95,13 +46,6 @@ struct Smem {
   static_assert(CH_S >= DL, "staging of R / T needs the free slab buffer");
 };
 
-__device__ __forceinline__ void bulk_copy(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(dst)),
-               "l"((uint64_t)src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
-
 template <int DL, int DR>
 __device__ void issue_chunk(const PArgs& a, const Chunk& ch, double* sm, uint64_t* bar, int buf) {
   using S = Smem<DL, DR>;
@@ -110,35 +54,6 @@ __device__ void issue_chunk(const PArgs& a, const Chunk& ch, double* sm, uint64_
   mbar_arrive_expect_tx(bar, lbytes + rbytes);
   bulk_copy(sm + S::L_OFF + buf * CH_ROWS * S::DLP, a.Lpack + ch.u_b * S::DLP, lbytes, bar);
   bulk_copy(sm + S::R_OFF + buf * CH_S * S::DRP, a.Rpack + ch.t_b * S::DRP, rbytes, bar);
-}
-
-// staged copy of a rows x cols global matrix into padded smem (row stride ld)
-// 16-byte global->shared copies that bypass registers and L1 (all issued back to back, so their
-// L2 latencies overlap; ptxas would otherwise interleave loads with dependent arithmetic).
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
-
-// rows x cols (cols even) row-major global matrix -> padded smem (row stride ld, 16B aligned rows)
-__device__ __forceinline__ void stage(double* dst, const double* __restrict__ src, int rows, int cols, int ld,
-                                      bool /*coherent*/) {
-  const int pairs = rows * (cols / 2);
-  for (int e = threadIdx.x; e < pairs; e += PT) {
-    const int i = e / (cols / 2), j = 2 * (e - i * (cols / 2));
-    cp_async16(dst + i * ld + j, src + (size_t)i * cols + j);
-  }
-}
-
-// out[j] = sum_k w[k] M[k][j] for j < cols; 4 threads per output, interleaved k-split.
-__device__ __forceinline__ void vecmat(const double* w, const double* M, int K, int cols, int ld, double* out) {
-  const int j = threadIdx.x >> 2, part = threadIdx.x & 3;
-  double s = 0.0;
-  if (j < cols)
-    for (int k = part; k < K; k += 4) s = fma(w[k], M[k * ld + j], s);
-  s += __shfl_xor_sync(0xffffffffu, s, 1);
-  s += __shfl_xor_sync(0xffffffffu, s, 2);
-  if (j < cols && part == 0) out[j] = s;
 }
 
 template <int DL, int DR>
@@ -188,7 +103,7 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
     double* Rs = sm + S::R_OFF + (cur ^ 1) * CH_S * DRP;
     const double* VRs = sm + S::VR_OFF;
     for (int r = b; r < DL; r += G) {
-      stage(Rs, Rin, DL, DR, DRP, true);
+      stage(Rs, Rin, DL, DR, DRP);
       for (int k = tid; k < DL; k += PT) Ws[k] = __ldg(&a.VL[k * DL + r]);
       cp_async_wait_all();
       __syncthreads();
@@ -219,7 +134,7 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
     double* Ts = sm + S::R_OFF + (cur ^ 1) * CH_S * DRP;
     const double* VRts = sm + S::VRT_OFF;
     for (int r = b; r < DL; r += G) {
-      stage(Ts, a.T, DL, DR, DRP, true);
+      stage(Ts, a.T, DL, DR, DRP);
       for (int k = tid; k < DL; k += PT) Ws[k] = __ldg(&a.VL[r * DL + k]);
       cp_async_wait_all();
       __syncthreads();
@@ -262,8 +177,8 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
   };
 
   // VR and VR^T stay resident for the whole solve
-  stage(sm + S::VR_OFF, a.VR, DR, DR, DRP, false);
-  stage(sm + S::VRT_OFF, a.VRt, DR, DR, DRP, false);
+  stage(sm + S::VR_OFF, a.VR, DR, DR, DRP);
+  stage(sm + S::VRT_OFF, a.VRt, DR, DR, DRP);
   cp_async_wait_all();
   __syncthreads();
   // tol = residual_tol * ||P rhs|| (solvers.py:212-214)
@@ -283,14 +198,10 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
 
   int status = 0, iters = 0, hlen = 0;
   double my_rhs = 0.0, my_dv = 0.0;  // eigenbasis mode: this thread's reduce element (see P2)
-  const bool prof = (b == 0 && tid == 0);
-  long long p1acc[4] = {0, 0, 0, 0};
   // it == -1: the right-hand-side pass (same chunk pipeline, s_t = v_t (v_t b_t), no Y)
   const int it0 = a.rhs_in_kernel ? -1 : 0;  // first pass: a CTA with a single (resident) chunk waits only here
   for (int it = it0; it < a.max_iters; it++) {
     const bool rp = it < 0;
-    if (prof && !rp) g_prof[it * 6 + 0] = clock64();
-    KS_STAMP(0)
     // ---------------- P1: sketched normal-operator apply ----------------
     // Software-pipelined over the CTA's chunks: phase A = samples(c) (CUDA cores), phase B =
     // G(c) and Y(c+1) together (tensor cores, independent DMMA chains interleaved); two barriers
@@ -301,12 +212,9 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
     const int64_t nch = c_end - c_beg;
     const int base = cur;
     auto wait_buf = [&](int bb) {
-      long long pc0 = 0;
-      if (prof) pc0 = clock64();
       mbar_wait(&bars[bb], phase[bb]);
       phase[bb] ^= 1;
       pending[bb] = 0;
-      if (prof && !rp) p1acc[0] += clock64() - pc0;
     };
     auto y_tile = [&](const double* Lsrc, int tile, double (&acc)[4], int k0) {
       const int m0 = (tile / YT_N) * 16, n0 = (tile % YT_N) * 8;
@@ -329,8 +237,6 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
         issue_chunk<DL, DR>(a, a.chunks[c_beg + 1], sm, &bars[base ^ 1], base ^ 1);
         pending[base ^ 1] = 1;
       }
-      long long pc0 = 0;
-      if (prof) pc0 = clock64();
       if (!rp) {
         const double* L0 = sm + S::L_OFF + base * CH_ROWS * DLP;
 #pragma unroll
@@ -345,7 +251,6 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
         }
       }
       __syncthreads();
-      if (prof && !rp) p1acc[1] += clock64() - pc0;
     }
     for (int64_t c = c_beg; c < c_end; c++) {
       const Chunk ch = a.chunks[c];
@@ -353,8 +258,6 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
       const double* Ls = sm + S::L_OFF + bc * CH_ROWS * DLP;
       const double* Rs = sm + S::R_OFF + bc * CH_S * DRP;
       const int nrows = (int)(ch.u_e - ch.u_b);
-      long long pc0 = 0;
-      if (prof) pc0 = clock64();
       // samples: half-warp per left row, entries ql, ql + 16, ... per lane (conflict-free)
       {
         const int r = tid >> 4, ql = tid & 15;
@@ -428,7 +331,6 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
         for (int j = 0; j < QE; j++) Zs[r * DRP + ql + 16 * j] = z[j];
       }
       __syncthreads();
-      if (prof && !rp) { const long long now = clock64(); p1acc[2] += now - pc0; pc0 = now; }
       // phase B: G += L_c^T Z (K = CH_ROWS; rows >= nrows have Z == 0 and finite stale L) and
       // Y(c+1) = L_{c+1} X, their DMMA chains interleaved
       const bool next = c + 1 < c_end;
@@ -470,7 +372,6 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
         }
       }
       __syncthreads();  // Y(c+1) visible; Zs and slab bc no longer read
-      if (prof && !rp) p1acc[3] += clock64() - pc0;
       // slab bc is free: fetch chunk c + 2, or this CTA's first chunk of the next pass
       if (tid == 0 && !resident) {
         int64_t cn = -1;
@@ -503,11 +404,7 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
       }
     }
     asm volatile("fence.proxy.async.global;" ::: "memory");  // read back by the async (bulk-copy) proxy
-    if (prof && !rp) g_prof[it * 6 + 1] = clock64();
-    KS_STAMP(1)
     grid.sync();
-    KS_STAMP(2)
-    if (prof && !rp) g_prof[it * 6 + 2] = clock64();
     // ---------------- P2: R = sum G + lam X - rhs ----------------
     double eig_sq = 0.0;
     {
@@ -586,9 +483,7 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
       }
     }
     if (a.eig_mode) asm volatile("fence.proxy.async.global;" ::: "memory");
-    KS_STAMP(3)
     grid.sync();
-    KS_STAMP(4)
     if (a.eig_mode) {
       // every CTA: ||step'|| from the G partials (fixed order) and, past the rhs pass, the step
       // (DL x DRP padded rows, one bulk copy into the free slab buffer)
@@ -622,9 +517,6 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
         tol = a.residual_tol * fmax(nrm, DBL_MIN);
         continue;
       }
-      if (prof) g_prof[it * 6 + 3] = clock64();
-      KS_STAMP(5)
-      KS_STAMP(6)
       if (tid == 0) Hs[it] = nrm;
       hlen = it + 1;
       if (nrm <= tol) {
@@ -666,27 +558,17 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
       }
       iters = it + 1;
       __syncthreads();
-      if (prof) g_prof[it * 6 + 4] = g_prof[it * 6 + 5] = clock64();
-      KS_STAMP(7)
-      KS_STAMP(8)
       continue;
     }
     if (rp) {
       tol = init_tol();
       continue;
     }
-    if (prof) g_prof[it * 6 + 3] = clock64();
     // ---------------- P3 / P4: preconditioner ----------------
     precond_a(a.R);
-    KS_STAMP(5)
     grid.sync();
-    KS_STAMP(6)
-    if (prof) g_prof[it * 6 + 4] = clock64();
     precond_b();
-    KS_STAMP(7)
     grid.sync();
-    KS_STAMP(8)
-    if (prof) g_prof[it * 6 + 5] = clock64();
     // ---------------- norm, stopping rules, update ----------------
     const double nrm = row_norm();
     if (tid == 0) Hs[it] = nrm;
@@ -712,7 +594,7 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
     {
       // stage the step (written by other CTAs) with asynchronous copies, then update x
       double* St = sm + S::R_OFF + (cur ^ 1) * CH_S * DRP;
-      stage(St, a.step, DL, DR, DRP, true);
+      stage(St, a.step, DL, DR, DRP);
       cp_async_wait_all();
       __syncthreads();
       for (int e = tid; e < NE; e += PT) {
@@ -740,8 +622,8 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
     for (int row = b; row < (want_rhs ? 2 * DL : DL); row += G) {
       const bool is_rhs = row >= DL;
       const int r = is_rhs ? row - DL : row;
-      stage(VRts, a.VRt, DR, DR, DRP, false);
-      if (is_rhs) stage(Ms, a.rhs, DL, DR, DRP, true);
+      stage(VRts, a.VRt, DR, DR, DRP);
+      if (is_rhs) stage(Ms, a.rhs, DL, DR, DRP);
       for (int k = tid; k < DL; k += PT) Ws[k] = __ldg(&a.VL[r * DL + k]);
       cp_async_wait_all();
       __syncthreads();
@@ -762,7 +644,6 @@ __global__ void __launch_bounds__(PT, 1) richardson_persistent_kernel(PArgs a) {
       }
     for (int i = tid; i < hlen; i += PT) a.hist[i] = Hs[i];
     if (tid == 0) {
-      for (int k = 0; k < 4; k++) g_p1split[k] = p1acc[k];
       a.state[0] = status;
       a.state[1] = iters;
       a.state[2] = hlen;
@@ -1084,18 +965,34 @@ namespace ks {
 static int64_t plan_cap(int64_t ul, int64_t nnz) { return (ul + CH_ROWS - 1) / CH_ROWS + nnz / CH_S + 2; }
 static size_t plan_range_offset(int64_t cap) { return (size_t)cap * (sizeof(Chunk) + sizeof(int64_t)); }
 
+static bool use_ws() { return !env(ENV_RICH_OLD); }
+static int g_prof_on = 0;  // ks_debug_richardson_profile: the profiling instantiation of the ws kernel
+
 static int launch_plan(cudaStream_t st, const ks_sketch_view* sk, int64_t ul, const int64_t* counts_dev, int dL,
                        int dR, int grid, Chunk* chunks, int64_t* cpre, int64_t* range) {
-  // estimated chunk cost (SM cycles), fitted to measured per-CTA apply times at c3
-  // (tools/fit_plan_costs.py: rms error 0.23 us): ~13.3 cycles per DMMA tile-step of the Y and G
-  // GEMMs (fixed per chunk), ~139 cycles per sample of the chunk's longest row (the rows' sample
-  // loops run in parallel), ~4 cycles per sample of shared-memory traffic
   const int64_t dmma = (int64_t)(CH_ROWS / 16) * (dR / 8) * (dL / 4) + (int64_t)(dL / 16) * (dR / 8) * (CH_ROWS / 4);
+  int64_t wchunk, wsamp, wlong;
+  if (use_ws() && richardson_ws_supported(dL, dR, grid)) {
+    // phase-separated loop: a chunk costs its DMMA issue time in the Y and G phases (8 SM cycles
+    // per m16n8k4 at the FP64 tensor rate); the sample phase spreads a CTA's rows over 48
+    // quarter-warps, ~10 cycles per sample of the CTA
+    wchunk = 8 * dmma;
+    wsamp = 10;
+    wlong = 0;
+  } else {
+    // single-role kernel: estimated chunk cost (SM cycles), fitted to measured per-CTA apply
+    // times at c3 (tools/fit_plan_costs.py: rms error 0.23 us): ~13.3 cycles per DMMA tile-step
+    // of the Y and G GEMMs (fixed per chunk), ~139 cycles per sample of the chunk's longest row
+    // (the rows' sample loops run in parallel), ~4 cycles per sample of shared-memory traffic
+    wchunk = (int64_t)(13.3 * dmma);
+    wsamp = dR / 16;
+    wlong = 139;
+  }
   KS_TRY_CUDA(cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)(PLAN_SM_SEG * sizeof(int64_t))));
   plan_kernel<<<1, PLAN_T, PLAN_SM_SEG * sizeof(int64_t), st>>>(sk->seg, ul, counts_dev ? counts_dev + 1 : nullptr,
-                                                                grid, (int64_t)(13.3 * dmma), (int64_t)dR / 16, 139, chunks,
-                                                                cpre, range, range + grid + 1);
+                                                                grid, wchunk, wsamp, wlong, chunks, cpre, range,
+                                                                range + grid + 1);
   KS_CHECK_LAUNCH();
   return KS_OK;
 }
@@ -1144,8 +1041,14 @@ int richardson_persistent(cudaStream_t st, const ks_sketch_view* sk, const doubl
   Scratch<int> state_s(state_dev ? 0 : 4, st);
   int* statep = state_dev ? state_dev : state_s.p;
   KS_REQUIRE(eig_mode <= rhs_in_kernel, KS_EINVAL, "the eigenbasis loop builds its own right-hand side");
-  KS_REQUIRE(!eig_mode || ((((int64_t)dL * dR + grid - 1) / grid + 1) & ~1) <= PT / 8, KS_ESIZE,
-             "eigenbasis loop: at most one reduce element per thread (too few SMs for d_L * d_R)");
+  KS_REQUIRE(grid <= 192, KS_ESIZE, "persistent loop: at most 192 CTAs (norm staging)");
+  const bool ws = eig_mode && use_ws() && richardson_ws_supported(dL, dR, grid);
+  // the single-role kernel's eigenbasis reduce keeps one element per thread: on parts with too few
+  // SMs for d_L * d_R it runs in the natural basis instead
+  if (eig_mode && !ws && epc > PT / 8) eig_mode = false;
+  KS_REQUIRE(ws || (int64_t)grid * epc <= (int64_t)CH_S * (dR + PAD), KS_ESIZE,
+             "persistent loop: partial-sum staging exceeds the slab buffer for grid %d", grid);
+  Scratch<unsigned> flags(ws ? BARRIER_WORDS : 0, st);
   KS_REQUIRE(Lpack.p && Rpack.p && part.p && R.p && T.p && stepb.p && rowsq.p && VRt.p && chunks_p && range_p &&
                  (plan_ws || cpre.p) && statep && (!eig_mode || rhs_e.p),
              KS_ECUDA, "scratch allocation failed");
@@ -1153,7 +1056,6 @@ int richardson_persistent(cudaStream_t st, const ks_sketch_view* sk, const doubl
   // (tools/fit_plan_costs.py: rms error 0.23 us): ~13.3 cycles per DMMA tile-step of the Y and G
   // GEMMs (fixed per chunk), ~139 cycles per sample of the chunk's longest row (the rows' sample
   // loops run in parallel), ~4 cycles per sample of shared-memory traffic
-  const int64_t dmma = (int64_t)(CH_ROWS / 16) * (dR / 8) * (dL / 4) + (int64_t)(dL / 16) * (dR / 8) * (CH_ROWS / 4);
   if (!plan_ws) {
     int rc0 = launch_plan(st, sk, ul, counts_dev, dL, dR, grid, dch.p, cpre.p, drange.p);
     if (rc0) return rc0;
@@ -1195,8 +1097,10 @@ int richardson_persistent(cudaStream_t st, const ks_sketch_view* sk, const doubl
   a.lam = lam; a.damping = damping; a.residual_tol = residual_tol; a.max_iters = max_iters;
   a.part = part.p; a.R = R.p; a.T = T.p; a.step = stepb.p; a.rowsq = rowsq.p; a.x_out = x; a.hist = hist;
   a.state = statep;
+  a.flags = flags.p;
   int rc;
-  if (dL == 16 && dR == 16) rc = launch<16, 16>(st, a, grid);
+  if (ws) rc = richardson_ws_launch(st, a, dL, dR, grid, g_prof_on != 0);
+  else if (dL == 16 && dR == 16) rc = launch<16, 16>(st, a, grid);
   else if (dL == 16 && dR == 32) rc = launch<16, 32>(st, a, grid);
   else if (dL == 16 && dR == 64) rc = launch<16, 64>(st, a, grid);
   else if (dL == 32 && dR == 16) rc = launch<32, 16>(st, a, grid);
@@ -1219,40 +1123,10 @@ int richardson_persistent(cudaStream_t st, const ks_sketch_view* sk, const doubl
 
 }  // namespace ks
 
-// Average cycles of CTA 0 per phase over the last persistent run:
-// apply (P1), sync wait after P1, reduce (P2 + sync), precond A (P3 + sync), precond B (P4 + sync),
-// update + loop overhead.
-extern "C" int ks_debug_richardson_apply_split(int32_t iters, double* out4) {
-  if (iters < 1) return KS_EINVAL;
-  long long h[4];
-  KS_TRY_CUDA(cudaMemcpyFromSymbol(h, g_p1split, sizeof(h)));
-  for (int k = 0; k < 4; k++) out4[k] = (double)h[k] / iters;
-  return KS_OK;
-}
 
-extern "C" int ks_debug_richardson_phases(int32_t iters, double* out6) {
-  if (iters < 2 || iters > 1024) return KS_EINVAL;
-  std::vector<long long> h(6 * iters);
-  KS_TRY_CUDA(cudaMemcpyFromSymbol(h.data(), g_prof, sizeof(long long) * 6 * iters));
-  for (int k = 0; k < 6; k++) out6[k] = 0.0;
-  for (int it = 0; it + 1 < iters; it++) {
-    const long long* p = &h[it * 6];
-    out6[0] += p[1] - p[0];
-    out6[1] += p[2] - p[1];
-    out6[2] += p[3] - p[2];
-    out6[3] += p[4] - p[3];
-    out6[4] += p[5] - p[4];
-    out6[5] += h[(it + 1) * 6] - p[5];
-  }
-  for (int k = 0; k < 6; k++) out6[k] /= (iters - 1);
-  return KS_OK;
-}
-
-// Profiling aid: per-CTA globaltimer stamps (ns) of iteration 5: out[cta*9 + k], k = apply start,
-// apply end, after sync 1, reduce end, after sync 2, precond A end, after sync 3, precond B end,
-// after sync 4.
-extern "C" int ks_debug_richardson_cta_stamps(int32_t nctas, uint64_t* out) {
-  if (nctas < 1 || nctas > 256) return KS_EINVAL;
-  KS_TRY_CUDA(cudaMemcpyFromSymbol(out, g_cta_ts, sizeof(unsigned long long) * 9 * nctas));
+// Profiling switch: later phase-separated loop launches run the instantiation that records CTA 0's
+// phase clocks (read by ks_debug_richardson_phases).  Off by default; never on the product path.
+extern "C" int ks_debug_richardson_profile(int32_t on) {
+  ks::g_prof_on = on != 0;
   return KS_OK;
 }

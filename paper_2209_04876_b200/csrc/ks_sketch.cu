@@ -472,7 +472,7 @@ int sketched_gram_partials(cudaStream_t st, const ks_sketch_view* sk, const doub
   *nparts_out = nb;
   if (nb == 0) return KS_OK;
   const size_t smem = sizeof(double) * (size_t)CH * (sk->dL + sk->dR);
-  if (mode == 1 && sk->dL == 128 && sk->dR == 128 && !getenv("KS_GRAM_SCALAR")) {
+  if (mode == 1 && sk->dL == 128 && sk->dR == 128 && !ks::env(ks::ENV_GRAM_SCALAR)) {
     const int64_t nchunks = (sk->u_left + G128_CH - 1) / G128_CH;
     const int64_t nb128 = ks_min64(nchunks, (int64_t)num_sms());
     *nparts_out = nb128;
@@ -706,7 +706,7 @@ extern "C" int ks_gather_draws2(const double* b, const int64_t* draws, int64_t n
                                 void* stream) {
   if (s <= 0) return KS_OK;
   static const int max_blocks = [] {
-    const char* e = getenv("KS_GATHER_BLOCKS");  // diagnostic switch (A/B of the grid size)
+    const char* e = ks::env(ks::ENV_GATHER_BLOCKS);  // diagnostic switch (A/B of the grid size)
     return e ? atoi(e) : 0;
   }();
   // default: one read per thread over the whole grid (measured best beside the sketch kernels)

@@ -621,7 +621,7 @@ int qr_r(cudaStream_t st, const double* A, int64_t n, int d, double* R) {
   KS_REQUIRE(d >= 1 && d <= 128, KS_ESIZE, "qr_r supports 1 <= d <= 128 (got %d)", d);
   // tall and well-conditioned: CholeskyQR2 (two Gram passes + one streaming triangular solve,
   // ks_cholqr.cu); otherwise Householder TSQR below
-  if (n >= 4 * (int64_t)d && !getenv("KS_TSQR")) {
+  if (n >= 4 * (int64_t)d && !ks::env(ks::ENV_TSQR)) {
     int ok = 0;
     int rc = chol_qr2_r(st, A, n, d, R, &ok, nullptr);
     if (rc) return rc;
@@ -671,7 +671,7 @@ static void launch_jacobi_fixed(cudaStream_t st, const MatPtrs& Ms, const double
   // symmetric (Gram) problems: FP32 prelude sweeps (KS_JACOBI_FP32=<n>, default 4; 0 = off)
   int sweeps32 = 0;
   if (SYM) {
-    const char* e = getenv("KS_JACOBI_FP32");
+    const char* e = ks::env(ks::ENV_JACOBI_FP32);
     sweeps32 = e ? atoi(e) : 4;
   }
   const int smem = (sweeps32 > 0 ? 4 : 2) * D * (D + 8) * (int)sizeof(double);
@@ -827,7 +827,7 @@ static int launch_jacobi128(cudaStream_t st, const MatPtrs& Ms, const double* M,
 template <bool SYM>
 static bool jacobi_fixed(cudaStream_t st, const MatPtrs& Ms, const double* M, int d, double* sigma, double* V,
                          int batch) {
-  if (getenv("KS_JACOBI_GENERIC")) return false;
+  if (ks::env(ks::ENV_JACOBI_GENERIC)) return false;
   switch (d) {
     case 16: launch_jacobi_fixed<16, SYM>(st, Ms, M, sigma, V, batch); return true;
     case 32: launch_jacobi_fixed<32, SYM>(st, Ms, M, sigma, V, batch); return true;

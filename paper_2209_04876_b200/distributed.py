@@ -23,6 +23,8 @@ from dataclasses import dataclass
 
 import numpy as np
 
+from . import _state
+
 
 @dataclass(frozen=True)
 class ShardPlan:
@@ -248,3 +250,7 @@ def sharded_fast_kronecker_regression(factors, b_rows, config, plan: ShardPlan, 
     x, iters, hist = sharded_richardson(normal_local, pre.apply, rhs_local, config.effective_damping,
                                         config.effective_max_iters, config.residual_tol, torch, config.lam)
     return x, iters, hist
+
+
+# Public entry points are gated (capture vs. concurrent solves, see _state.py).
+_state.gate_names(globals(), ["sharded_kronmatmul_svd_solve", "sharded_fast_kronecker_regression"])

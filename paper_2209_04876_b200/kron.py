@@ -18,6 +18,7 @@ from typing import Sequence
 import numpy as np
 import torch
 
+from . import _state
 from . import _device as D
 from . import _lib
 from .errors import InvalidInputError
@@ -446,3 +447,18 @@ def sketch_rows_of_kron(factors: Sequence, sketch):
               _lib.ptr_array(ctypes.c_int32, [int(a.shape[1]) for a in facs]), D.p(idx), int(flat), D.p(w), s,
               D.p(out), D.stream())
     return D.out(out, host)
+
+
+# Public entry points are gated (capture vs. concurrent solves, see _state.py).
+_state.gate_names(globals(), [
+    "balanced_partition",
+    "check_factors",
+    "kron_mat_mul",
+    "kron_operator_shape",
+    "kron_rows",
+    "kron_vec_square",
+    "sketch_rows_of_kron",
+    "sketched_kron_apply",
+    "sketched_kron_transpose_apply",
+    "sparse_diagonal_from_sketch",
+])

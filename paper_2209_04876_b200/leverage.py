@@ -17,6 +17,7 @@ import torch
 
 from . import _device as D
 from . import _lib
+from . import _state
 from ._numpy_rng import pcg64_state, split128, ziggurat_tables
 from .errors import InvalidInputError, NumericalFailureError
 from .tensor import CompactSvd, as_matrix, compact_svd
@@ -105,7 +106,7 @@ class DeferredChecks:
             handler(f.reshape(-1).tolist())
 
 
-_DEFERRED: list = [None]
+_DEFERRED = _state.TLSlot()  # this thread's enclosing fast solve's DeferredChecks (or None)
 
 
 def check_later(flags: torch.Tensor, handler):
@@ -448,3 +449,16 @@ def spectral_approx_rows(a, eps: float, delta: float, seed, alpha: float = 1.0):
     if not 0.0 < delta < 1.0:
         raise InvalidInputError(f"delta must be in (0, 1), got {delta}")
     return D.out(_spectral_rows_dev(at, eps, delta, seed, alpha), host)
+
+
+# Public entry points are gated (capture vs. concurrent solves, see _state.py).
+_state.gate_names(globals(), [
+    "approx_leverage_scores_jl",
+    "build_product_sampler",
+    "ridge_leverage_scores",
+    "sample_rows",
+    "spectral_approx_rows",
+    "statistical_leverage_scores",
+])
+ProductSampler.sample = _state.gated(ProductSampler.sample)
+ProductSampler.probabilities = _state.gated(ProductSampler.probabilities)

@@ -27,6 +27,8 @@ import torch
 
 from . import _device as D
 from . import _lib
+from . import _state
+from ._state import CACHE_LOCK, CAPTURE_MODE, GATE, TLSlot
 from .errors import InvalidInputError, NumericalFailureError, SizeGuardError
 from .kron import (SparseDiagonal, _kron_apply_dev, _view_for, check_factors, grouped2_eligible,
                    kron_operator_shape, sketch_diag_grouped2_finish, sketch_diag_grouped2_launch,
@@ -366,12 +368,17 @@ _SIDE = {}
 
 
 def _side_stream(k: int = 0) -> torch.cuda.Stream:
-    """k-th auxiliary stream of the current device (0: eigensolves, 1..: per-factor JL work)."""
-    key = (torch.cuda.current_device(), k)
+    """k-th auxiliary stream of the current stream (0: eigensolves, 1..: per-factor JL work).
+    Keyed by the current stream, so concurrent solves on their own streams (and a capture, which
+    runs on its own capture stream) never share a side stream."""
+    key = (torch.cuda.current_device(), torch.cuda.current_stream().cuda_stream, k)
     s = _SIDE.get(key)
     if s is None:
-        s = torch.cuda.Stream(device=key[0])
-        _SIDE[key] = s
+        with CACHE_LOCK:
+            s = _SIDE.get(key)
+            if s is None:
+                s = torch.cuda.Stream(device=key[0])
+                _SIDE[key] = s
     return s
 
 
@@ -511,8 +518,17 @@ class _SolveGraph:
 
 
 _SOLVE_GRAPHS: dict = {}
-_LAST_LOOP_EVENTS: list = [None]  # (start, end) events of the last graph-replayed loop launch
+_LAST_LOOP_EVENTS = TLSlot()  # this thread's (start, end) events of its last graph-replayed loop launch
+_LAST_HISTORY = TLSlot()  # this thread's last fast solve: the Richardson step-norm history
 _SOLVE_STATS = {"eager": 0, "capture": 0, "replay": 0}
+_GRAPH_CAP = 16  # cached whole-solve graphs (keys are per thread and per stream)
+
+
+def last_solve_history() -> list:
+    """Step norms of the calling thread's last fast solve (graph or eager path): the history the
+    reference's richardson_solve appends (solvers.py:226-230)."""
+    h = _LAST_HISTORY[0]
+    return list(h) if h is not None else []
 
 
 _USE_SOLVE_GRAPH = [True]
@@ -530,13 +546,18 @@ def _solve_graph_key(facs, b, config: RegressionConfig):
     if not (b.is_cuda or b.is_pinned()):
         return None
     try:
-        key = (torch.cuda.current_device(), torch.cuda.current_stream().cuda_stream,
+        key = (_state.thread_key(), torch.cuda.current_device(), torch.cuda.current_stream().cuda_stream,
                tuple((a.data_ptr(), tuple(a.shape), tuple(a.stride())) for a in facs),
-               (b.data_ptr(), b.numel(), b.is_cuda), config)
+               (b.data_ptr(), b.numel(), b.is_cuda), config, _switches())
         hash(key)
     except TypeError:
         return None
     return key
+
+
+def _switches():
+    """The process-wide path switches a captured graph bakes in (part of every graph key)."""
+    return (_NO_PREDRAW[0], _TIMELINE[0], _GATHER_BESIDE[0], _USE_FUSED[0])
 
 
 def _eig_on(stream, g, tl=None, name=""):
@@ -552,9 +573,11 @@ def _eig_on(stream, g, tl=None, name=""):
     return (v[0], w[0]), ev
 
 
+# diagnostic switches, read once at import and part of every graph key
 _NO_PREDRAW = [bool(os.environ.get("KS_NO_PREDRAW"))]
 _TIMELINE = [bool(os.environ.get("KS_GRAPH_TIMELINE"))]  # external events at the solve graph's joins
-_TL_CUR = [None]  # the timeline being captured
+_GATHER_BESIDE = [os.environ.get("KS_GATHER_BESIDE_SKETCH") == "1"]  # sampled-b gather beside the sketch
+_TL_CUR = TLSlot()  # the timeline this thread is capturing
 
 
 def _tl_event(tl, name, stream=None):
@@ -723,11 +746,9 @@ def _fast_solve_graph(facs, b, config: RegressionConfig, key=None):
         key = _solve_graph_key(facs, b, config)
     if key is None:
         return None
-    entry = _SOLVE_GRAPHS.get(key)
+    entry = _state.cache_get(_SOLVE_GRAPHS, key)
     if entry is None:
-        if len(_SOLVE_GRAPHS) >= 4:
-            _SOLVE_GRAPHS.pop(next(iter(_SOLVE_GRAPHS)))
-        _SOLVE_GRAPHS[key] = _SolveGraph()
+        _state.cache_put(_SOLVE_GRAPHS, key, _SolveGraph(), _GRAPH_CAP)
         _SOLVE_STATS["eager"] += 1
         return None
     s = _regression_sample_count(math.prod(int(a.shape[1]) for a in facs), config)
@@ -736,8 +757,11 @@ def _fast_solve_graph(facs, b, config: RegressionConfig, key=None):
         cap = _lev.DeferredChecks()
         outer = _lev._DEFERRED[0]
         _lev._DEFERRED[0] = cap
+        gate = GATE.capture()
         try:
-            with torch.cuda.graph(g):
+            if not gate.__enter__():
+                return None  # other solves in flight: eager this time, captured on a later call
+            with torch.cuda.graph(g, capture_error_mode=CAPTURE_MODE):
                 # the factors' finite / nonzero validation rides in the graph on a side stream (off
                 # the critical path); its flags lead the packed read-back, so a replay on new
                 # contents at the same addresses raises the reference's error before any result
@@ -754,9 +778,10 @@ def _fast_solve_graph(facs, b, config: RegressionConfig, key=None):
                 entry.packed = _PackedChecks([(flags.reshape(-1), _validation_handler(len(facs)))] + cap.items,
                                              entry.out["state"], entry.out["hist"])
         except Exception:
-            _SOLVE_GRAPHS.pop(key, None)
+            _state.cache_drop(_SOLVE_GRAPHS, key)
             raise
         finally:
+            gate.__exit__(None, None, None)
             _lev._DEFERRED[0] = outer
         entry.graph, entry.checks = g, cap.items
         _SOLVE_STATS["capture"] += 1
@@ -775,6 +800,7 @@ def _fast_solve_graph(facs, b, config: RegressionConfig, key=None):
         status, iters, hlen, history = entry.packed.run()
     except (_CholeskyFailed, _lev.ScoresFallback):
         return None  # the eager path retries (LU inverses / compact-SVD scores)
+    _LAST_HISTORY[0] = history
     if status == 2:
         raise NumericalFailureError("Richardson iteration diverged", iterations=iters,
                                     diagnostics={"residual_history": history})
@@ -819,8 +845,9 @@ def _host_graph_key(factors, b, config: RegressionConfig):
     if s >= rows:
         return None
     try:
-        key = ("host", torch.cuda.current_device(), torch.cuda.current_stream().cuda_stream,
-               tuple((a.data_ptr(), tuple(a.shape)) for a in factors), (b.data_ptr(), b.numel(), b.is_cuda), config)
+        key = ("host", _state.thread_key(), torch.cuda.current_device(), torch.cuda.current_stream().cuda_stream,
+               tuple((a.data_ptr(), tuple(a.shape)) for a in factors), (b.data_ptr(), b.numel(), b.is_cuda), config,
+               _switches())
         hash(key)
     except TypeError:
         return None
@@ -847,11 +874,9 @@ def _fast_solve_host_graph(factors, b, config: RegressionConfig, with_loss: bool
     key = _host_graph_key(factors, b, config)
     if key is None:
         return None
-    entry = _HOST_GRAPHS.get(key)
+    entry = _state.cache_get(_HOST_GRAPHS, key)
     if entry is None:
-        if len(_HOST_GRAPHS) >= 4:
-            _HOST_GRAPHS.pop(next(iter(_HOST_GRAPHS)))
-        _HOST_GRAPHS[key] = _HostFacsGraph()
+        _state.cache_put(_HOST_GRAPHS, key, _HostFacsGraph(), _GRAPH_CAP)
         return None
     s = _regression_sample_count(math.prod(int(a.shape[1]) for a in factors), config)
     torch.cuda.synchronize()
@@ -864,8 +889,12 @@ def _fast_solve_host_graph(factors, b, config: RegressionConfig, with_loss: bool
         cap = _lev.DeferredChecks()
         outer = _lev._DEFERRED[0]
         _lev._DEFERRED[0] = cap
+        gate = GATE.capture()
         try:
-            with torch.cuda.graph(g):
+            if not gate.__enter__():
+                entry.dev = None
+                return None  # other solves in flight: the regular path this time
+            with torch.cuda.graph(g, capture_error_mode=CAPTURE_MODE):
                 main = torch.cuda.current_stream()
                 # the JL sketches need no input data: drawn while the factors upload
                 pre_g = None if _NO_PREDRAW[0] else _predraw_jl_sketches(entry.dev, config, _spawned_seeds(config.seed, 5))
@@ -885,9 +914,10 @@ def _fast_solve_host_graph(factors, b, config: RegressionConfig, with_loss: bool
                                              + cap.items, entry.out["state"], entry.out["hist"])
                 entry.x_host = torch.empty(int(entry.out["x"].numel()), dtype=torch.float64).pin_memory()
         except Exception:
-            _HOST_GRAPHS.pop(key, None)
+            _state.cache_drop(_HOST_GRAPHS, key)
             raise
         finally:
+            gate.__exit__(None, None, None)
             _lev._DEFERRED[0] = outer
         entry.graph, entry.checks = g, cap.items
     _mark("graph launch")
@@ -902,6 +932,7 @@ def _fast_solve_host_graph(factors, b, config: RegressionConfig, with_loss: bool
         status, iters, hlen, history = entry.packed.run()
     except (_CholeskyFailed, _lev.ScoresFallback):
         return None  # the regular path retries (LU inverses / compact-SVD scores)
+    _LAST_HISTORY[0] = history
     x_h = entry.x_host
     if status == 2:
         raise NumericalFailureError("Richardson iteration diverged", iterations=iters,
@@ -1049,7 +1080,7 @@ def _jl_and_sampling(facs, tildes, gts, eps_jl: float, config: RegressionConfig,
         # the gather is issued after the sketch kernels: run beside them, the scattered reads (one
         # PCIe request each when b is page-locked host memory) slow both down, and the sum is the
         # same (tools/graph_timeline.py --host); the loop plan then overlaps the gather
-        after = os.environ.get("KS_GATHER_BESIDE_SKETCH") != "1"
+        after = not _GATHER_BESIDE[0]
         if not after:
             gst.wait_stream(main)
             with torch.cuda.stream(gst):
@@ -1087,8 +1118,8 @@ def _prefix_key(facs, tildes, config: RegressionConfig, use_chol: bool):
     if not _USE_GRAPHS[0] or not use_chol or any(t is not a for t, a in zip(tildes, facs)):
         return None
     try:
-        key = (torch.cuda.current_device(), torch.cuda.current_stream().cuda_stream,
-               tuple((a.data_ptr(), tuple(a.shape), tuple(a.stride())) for a in facs), config)
+        key = (_state.thread_key(), torch.cuda.current_device(), torch.cuda.current_stream().cuda_stream,
+               tuple((a.data_ptr(), tuple(a.shape), tuple(a.stride())) for a in facs), config, _switches())
         hash(key)
     except TypeError:
         return None
@@ -1101,25 +1132,26 @@ def _prefix_graph_run(key, entry, gts, run, deferred):
     from . import leverage as _lev
     if entry is None:
         _PREFIX_STATS["eager"] += 1
-        if len(_PREFIX_GRAPHS) >= 8:
-            _PREFIX_GRAPHS.pop(next(iter(_PREFIX_GRAPHS)))
-        _PREFIX_GRAPHS[key] = _PrefixGraph()
+        _state.cache_put(_PREFIX_GRAPHS, key, _PrefixGraph(), _GRAPH_CAP)
         return run()
     if entry.graph is None:
-        _PREFIX_STATS["capture"] += 1
-        entry.gts = gts
-        g = torch.cuda.CUDAGraph()
-        cap = _lev.DeferredChecks()
-        outer = _lev._DEFERRED[0]
-        _lev._DEFERRED[0] = cap
-        try:
-            with torch.cuda.graph(g):
-                entry.out = run()
-        except Exception:
-            _PREFIX_GRAPHS.pop(key, None)
-            raise
-        finally:
-            _lev._DEFERRED[0] = outer
+        with GATE.capture() as ok:
+            if not ok:
+                return run()  # other solves in flight: eager this time
+            _PREFIX_STATS["capture"] += 1
+            entry.gts = gts
+            g = torch.cuda.CUDAGraph()
+            cap = _lev.DeferredChecks()
+            outer = _lev._DEFERRED[0]
+            _lev._DEFERRED[0] = cap
+            try:
+                with torch.cuda.graph(g, capture_error_mode=CAPTURE_MODE):
+                    entry.out = run()
+            except Exception:
+                _state.cache_drop(_PREFIX_GRAPHS, key)
+                raise
+            finally:
+                _lev._DEFERRED[0] = outer
         entry.graph = g
         entry.checks = cap.items
     _PREFIX_STATS["replay"] += 1
@@ -1129,15 +1161,17 @@ def _prefix_graph_run(key, entry, gts, run, deferred):
     return entry.out
 
 
-# Phase marks for tools/profile_fast.py --phases: (name, host time, CUDA event) when enabled.
-_PHASES: list | None = None
+# Phase marks for tools/profile_fast.py --phases and bench.py: (name, host time, CUDA event),
+# collected per thread while enabled (``_PHASES[0] = []``; ``_PHASES[0] = None`` disables).
+_PHASES = TLSlot()
 
 
 def _mark(name: str):
-    if _PHASES is not None:
+    ph = _PHASES[0]
+    if ph is not None:
         ev = torch.cuda.Event(enable_timing=True)
         ev.record()
-        _PHASES.append((name, time.perf_counter(), ev))
+        ph.append((name, time.perf_counter(), ev))
 
 
 def _fast_solve_pass(facs, b, config: RegressionConfig, caches, trace, use_chol: bool, deferred,
@@ -1191,7 +1225,7 @@ def _fast_solve_pass(facs, b, config: RegressionConfig, caches, trace, use_chol:
             if spectral[n]:
                 main.wait_stream(_side_stream(n))
         key = _prefix_key(facs, tildes, config, use_chol) if trace is None else None
-        entry = _PREFIX_GRAPHS.get(key) if key is not None else None
+        entry = _state.cache_get(_PREFIX_GRAPHS, key) if key is not None else None
         gts = [_gram_dev(t, out=entry.gts[n] if entry is not None and entry.gts is not None else None)
                for n, t in enumerate(tildes)]
         # The preconditioner's eigendecompositions (solvers.py:440, 446) run on a side stream,
@@ -1285,6 +1319,7 @@ def _fast_solve_pass(facs, b, config: RegressionConfig, caches, trace, use_chol:
     _lev._DEFERRED[0] = None
     deferred.run(synced=True)  # generator / Cholesky / sampler-table flags, copied with the loop launch
     history = hist[: hlen.value].cpu().tolist()
+    _LAST_HISTORY[0] = history
     if rc == _lib.KS_EDIVERGED:
         raise NumericalFailureError("Richardson iteration diverged", iterations=iters.value,
                                     diagnostics={"residual_history": history})
@@ -1369,7 +1404,7 @@ def _fast_solve_dev_replay(factors, b, config: RegressionConfig, with_loss: bool
         return None
     bsrc = b.reshape(-1)
     key = _solve_graph_key(facs, bsrc, config)
-    entry = _SOLVE_GRAPHS.get(key) if key is not None else None
+    entry = _state.cache_get(_SOLVE_GRAPHS, key) if key is not None else None
     if entry is None or entry.graph is None:
         return None
     torch.cuda.synchronize()
@@ -1476,3 +1511,20 @@ def sketch_and_solve_ridge(factors: Sequence, b, config: RegressionConfig, sketc
     wall = time.perf_counter() - t0
     return SolveReport(solution=D.out(x, host), loss=_ridge_loss_dev(facs, x, bt, config.lam), iterations=0,
                        sample_count=s, wall_time=wall)
+
+
+# Public entry points are gated (capture vs. concurrent solves, see _state.py).
+_state.gate_names(globals(), [
+    "build_factor_cache",
+    "build_kron_preconditioner",
+    "exact_factor_scores",
+    "factor_gram",
+    "fast_kronecker_regression",
+    "kronmatmul_svd_solve",
+    "naive_normal_solve",
+    "pseudo_reciprocal",
+    "richardson_solve",
+    "ridge_loss",
+    "sketch_and_solve_ridge",
+])
+KronPreconditioner.apply = _state.gated(KronPreconditioner.apply)

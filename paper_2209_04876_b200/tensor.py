@@ -15,6 +15,7 @@ from typing import Sequence
 import numpy as np
 import torch
 
+from . import _state
 from . import _device as D
 from . import _lib
 from .errors import InvalidInputError
@@ -243,3 +244,21 @@ def unstack_columns(v, shape):
     if a.size != rows * cols:
         raise InvalidInputError(f"vector of length {a.size} cannot fill a {rows}x{cols} matrix")
     return a.reshape((rows, cols), order="F")
+
+
+# Public entry points are gated (capture vs. concurrent solves, see _state.py).
+_state.gate_names(globals(), [
+    "as_matrix",
+    "as_tensor",
+    "compact_svd",
+    "devectorize",
+    "explicit_kron",
+    "fold",
+    "multi_mode_product",
+    "n_mode_product",
+    "pseudo_inverse",
+    "stack_columns",
+    "unfold",
+    "unstack_columns",
+    "vectorize",
+])

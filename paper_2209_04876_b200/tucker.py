@@ -28,6 +28,7 @@ from typing import Sequence
 import numpy as np
 import torch
 
+from . import _state
 from . import _device as D
 from . import _lib
 from ._numpy_rng import pcg64_state, seedseq_children_seed_words, split128
@@ -619,3 +620,18 @@ def tucker_als(x, core_shape: Sequence[int], lam: float = 0.0, sweeps: int = 5, 
     report.rre = (0.0 if num == 0.0 else math.inf) if x_norm_sq == 0.0 else num / x_norm_sq
     model = TuckerModel(core=D.out(core, host), factors=[D.out(a, host) for a in facs], lam=lam)
     return model, report
+
+
+# Public entry points are gated (capture vs. concurrent solves, see _state.py).
+_state.gate_names(globals(), [
+    "build_factor_workspace",
+    "core_update",
+    "fast_factor_matrix_update",
+    "initial_model",
+    "naive_factor_update",
+    "reconstruct",
+    "regularized_loss",
+    "relative_error",
+    "tucker_als",
+])
+FactorUpdateWorkspace.apply = _state.gated(FactorUpdateWorkspace.apply)

@@ -1,28 +1,34 @@
-"""BASELINE config 4 (n = 65536, d in {16, 32, 64, 128}) on one B200.
+"""BASELINE config 4 (n = 65536, d in {16, 32, 64, 128}) on one B200, pinned to the reference.
 
-c4 is the configuration where the per-factor spectral row sampling (leverage.py:235-252) is
-active (s_n < n) and, at d = 128, where the persistent loop kernel does not apply.  b has
-4.29e9 entries (34.4 GB): it lives only on the device.
+c4 is where the per-factor spectral row sampling (leverage.py:235-252) is active (s_n < n) and,
+at d = 128, where the largest sketch (s = 169767) runs.  b = default_rng(0).standard_normal(n^2)
+ has 4.29e9 entries (34.4 GB): the device regenerates NumPy's stream in HBM
+(``device_standard_normal``, bit-exact except ulp-level libm differences in the ziggurat's rare
+tail branch) and the results are compared with ``tests/golden/c4_d{d}.npz``, produced by running
+the REFERENCE itself on the same stream (tests/golden/make_golden_c4.py).
 
-* sampling parity: with b = 0 (b only enters the right-hand side) the oracle finishes in seconds
-  and the sketch -- spectral rows, JL scores, product sampling, sparse diagonal -- must match it
-  bit for bit in the indices and to rounding in the values;
-* solve quality: with b ~ N(0, 1) generated on the device from NumPy's stream
-  (default_rng(0).standard_normal(n^2)), the fast solve's loss is checked against
-  the exact optimum from the device KronMatMul solver."""
+Contract (tolerances from the reference's own noise floor at c4 measured by
+tests/golden/measure_floor.py -> floor.json): sample count and iterations equal, sampled and
+sparse-diagonal indices bit-exact, fast-path x and step-norm history within 2x the floor
+(floors ~1e-11 for x, ~1e-9 for the history at c4), losses within 1e-9 relative, exact-path x
+within 1e-9.  Both the eager pipeline (with its trace) and the path the bench times (the
+whole-solve CUDA graph, d <= 64) are checked."""
 
+import json
 import math
+from pathlib import Path
 
 import numpy as np
 import pytest
 import torch
 
-from oracle import kronsolve_oracle as O
+from conftest import rel
 
 pytestmark = pytest.mark.gpu
 
 N4 = 65536
 PARAMS = dict(eps=0.1, delta=0.01, lam=1e-3, alpha=1e-5, seed=0)
+FLOOR = json.loads((Path(__file__).resolve().parent / "golden" / "floor.json").read_text())
 
 
 def cfg():
@@ -33,60 +39,65 @@ def cfg():
 def factors(d):
     """experiments.py:106-115 at n = 65536 (A1 then A2 from one default_rng(0))."""
     gen = np.random.default_rng(0)
-    return [gen.normal(1.0, math.sqrt(0.001), (N4, d)) for _ in range(2)]
+    return [torch.tensor(gen.normal(1.0, math.sqrt(0.001), (N4, d)), device="cuda") for _ in range(2)]
 
 
-@pytest.mark.parametrize("d", [16, 64])
-def test_c4_sketch_matches_oracle(d):
+@pytest.fixture(scope="module")
+def b_c4():
+    from paper_2209_04876_b200.leverage import device_standard_normal
+    b = device_standard_normal(0, N4 * N4)  # default_rng(0).standard_normal(n^2)
+    np.testing.assert_array_equal(b[:4096].cpu().numpy(), np.random.default_rng(0).standard_normal(4096))
+    yield b
+    del b
+    torch.cuda.empty_cache()
+
+
+def _tol(d, what):
+    return max(1e-12, 2.0 * FLOOR[f"c4_d{d}"][what])
+
+
+@pytest.mark.parametrize("d", [16, 32, 64, 128])
+def test_c4_fast_solve_matches_reference(golden, b_c4, d):
     import paper_2209_04876_b200 as K
     from paper_2209_04876_b200.solvers import FastSolveTrace
+    g = golden(f"c4_d{d}")
     facs = factors(d)
-    b_dev = torch.zeros(N4 * N4, dtype=torch.float64, device="cuda")
     tr = FastSolveTrace()
-    rep = K.fast_kronecker_regression([torch.tensor(a, device="cuda") for a in facs], b_dev, cfg(), _trace=tr,
-                                      with_loss=False)
-    del b_dev
-    torch.cuda.empty_cache()
-    # the oracle with a zero-stride zero b: identical sketch, trivial Richardson (rhs = 0)
-    ref = O.fast_kronecker_regression(facs, np.broadcast_to(0.0, (N4 * N4,)), with_loss=False, **PARAMS)
-    t = ref.trace
-    assert rep.sample_count == t["s"]
-    assert tr.a_tilde_rows == t["a_tilde_rows"] and all(r < N4 for r in t["a_tilde_rows"])  # spectral branch
-    np.testing.assert_array_equal(tr.sketch.indices.cpu().numpy(), t["indices"])
-    np.testing.assert_allclose(tr.sketch.weights.cpu().numpy(), t["weights"], rtol=1e-9)
-    np.testing.assert_array_equal(tr.sdiag.indices.cpu().numpy(), t["sd_indices"])
-    np.testing.assert_allclose(tr.sdiag.values.cpu().numpy(), t["sd_values"], rtol=1e-9)
-    assert np.allclose(np.asarray(rep.solution.cpu()), 0.0)
+    rep = K.fast_kronecker_regression(facs, b_c4, cfg(), _trace=tr)  # eager pipeline
+    assert rep.sample_count == int(g["s"]) and rep.iterations == int(g["iterations"])
+    assert all(r < N4 for r in tr.a_tilde_rows)  # spectral branch active
+    np.testing.assert_array_equal(tr.sketch.indices.cpu().numpy(), g["indices"].astype(np.int64))
+    np.testing.assert_allclose(tr.sketch.weights.cpu().numpy(), g["weights"], rtol=1e-10)
+    np.testing.assert_array_equal(tr.sdiag.indices.cpu().numpy(), g["sd_indices"])
+    np.testing.assert_allclose(tr.sdiag.values.cpu().numpy(), g["sd_values"], rtol=1e-10)
+    assert rel(tr.rhs, g["rhs"]) <= 1e-10
+    assert rel(rep.solution, g["x"]) <= _tol(d, "x")
+    h = np.asarray(tr.history)
+    assert h.size == g["history"].size
+    assert np.max(np.abs(h / g["history"] - 1.0)) <= _tol(d, "history")
+    assert abs(rep.loss - float(g["loss"])) <= 1e-9 * float(g["loss"])
+    if d <= 64:
+        # the benchmarked path: whole-solve graph (first call eager, second capture, then replays)
+        from paper_2209_04876_b200 import solvers as S
+        S._SOLVE_GRAPHS.clear()
+        outs = [K.fast_kronecker_regression(facs, b_c4, cfg(), with_loss=(k == 3)) for k in range(4)]
+        assert S._SOLVE_GRAPHS and all(e.graph is not None for e in S._SOLVE_GRAPHS.values())
+        for o in outs:
+            assert o.iterations == int(g["iterations"]) and o.sample_count == int(g["s"])
+            assert rel(o.solution, g["x"]) <= _tol(d, "x")
+            assert torch.equal(o.solution, outs[0].solution)
+        assert abs(outs[-1].loss - float(g["loss"])) <= 1e-9 * float(g["loss"])
+        S._SOLVE_GRAPHS.clear()
 
 
 @pytest.mark.parametrize("d", [16, 64, 128])
-def test_c4_fast_solve_vs_exact(d):
+def test_c4_exact_solve_matches_reference(golden, b_c4, d):
+    """kronmatmul_svd_solve on the 34 GB b: x and OPT against the reference's own exact solve
+    (OPT there summed over row blocks, see make_golden_c4.py)."""
     import paper_2209_04876_b200 as K
-    from paper_2209_04876_b200.leverage import device_standard_normal
-    facs = [torch.tensor(a, device="cuda") for a in factors(d)]
-    b = device_standard_normal(0, N4 * N4)  # default_rng(0).standard_normal(n^2), bit-exact stream
-    # spot-check the device stream against NumPy on its first entries
-    np.testing.assert_array_equal(b[:4096].cpu().numpy(), np.random.default_rng(0).standard_normal(4096))
-    exact = K.kronmatmul_svd_solve(facs, b, PARAMS["lam"])
-    fast = K.fast_kronecker_regression(facs, b, cfg())
-    s = math.ceil(1e-5 * 1680 * d * d * math.log(40 * d * d) * math.log(100.0) / 0.1)
-    assert fast.sample_count == s
-    assert 0 < fast.iterations <= 24
-    x = fast.solution.cpu().numpy()
-    assert np.all(np.isfinite(x))
-    # b ~ N(0, 1) is almost pure noise for a rank-d^2 model: OPT ~ ||b||^2.  At alpha = 1e-5 the
-    # sample count is far below the (1 + eps) theorem's, so the reference itself lands ~20 % above
-    # OPT here (a quality property of the algorithm at this alpha, as SURVEY.md notes for c5)
-    assert exact.loss <= fast.loss <= 1.5 * exact.loss
-    # the separate right-hand-side + loop path (other kernels, other summation orders) agrees
-    from paper_2209_04876_b200 import solvers as S
-    S._USE_FUSED[0] = False
-    try:
-        sep = K.fast_kronecker_regression(facs, b, cfg(), with_loss=False)
-    finally:
-        S._USE_FUSED[0] = True
-    assert sep.iterations == fast.iterations
-    xs = sep.solution.cpu().numpy()
-    assert np.linalg.norm(xs - x) <= 1e-6 * np.linalg.norm(x)
-    del b
-    torch.cuda.empty_cache()
+    g = golden(f"c4_d{d}")
+    ex = K.kronmatmul_svd_solve(factors(d), b_c4, PARAMS["lam"])
+    assert rel(ex.solution, g["exact_x"]) <= 1e-9
+    assert abs(ex.loss - float(g["opt"])) <= 1e-9 * float(g["opt"])
+    # the reference's own quality at alpha = 1e-5: the fast loss lands 11-19 % above OPT
+    assert float(g["opt"]) < float(g["loss"]) <= 1.25 * float(g["opt"])

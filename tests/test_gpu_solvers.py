@@ -247,10 +247,11 @@ def test_fused_rhs_loop_matches_separate_rhs(name):
     assert rel(r1.solution, r2.solution) <= X_TOL[name]
 
 
-@pytest.mark.parametrize("name", ["c1", "c2"])
+@pytest.mark.parametrize("name", ["c1", "c2", "c3"])
 def test_whole_solve_graph_matches_eager(golden, name):
     """Two-factor solves with device-resident or page-locked host b run as one captured CUDA
-    graph from the second call on; results equal the eager (trace) pipeline bit for bit."""
+    graph from the second call on; results equal the eager (trace) pipeline bit for bit and the
+    reference golden x / step-norm history / loss (c3 is the configuration bench.py times)."""
     import paper_2209_04876_b200 as K
     from paper_2209_04876_b200 import solvers as S
     from paper_2209_04876_b200.solvers import FastSolveTrace
@@ -269,6 +270,11 @@ def test_whole_solve_graph_matches_eager(golden, name):
         assert rep.iterations == ref.iterations
         assert torch.equal(rep.solution, ref.solution)
     assert rel(outs[-1].solution, g["x"]) <= X_TOL[name]
+    assert outs[-1].iterations == int(g["iterations"]) and outs[-1].sample_count == int(g["s"])
+    h = np.asarray(S.last_solve_history())  # the replayed graph's step norms
+    assert h.size == g["history"].size
+    assert np.max(np.abs(h - g["history"]) / g["history"]) <= max(1e-9, H_TOL[name])
+    assert abs(outs[-1].loss - float(g["loss"])) <= 1e-9 * float(g["loss"])
     # page-locked host b: the graph gathers the sampled entries through mapped host memory
     bh = torch.tensor(b).pin_memory()
     hs = [K.fast_kronecker_regression(fd, bh, cfg()) for _ in range(3)]
@@ -401,3 +407,50 @@ def test_fast_regression_mixed_widths_vs_oracle(n1, n2, d1, d2):
         assert r.sample_count == o.sample_count and r.iterations == o.iterations
         assert torch.equal(r.solution, reps[0].solution)
     assert rel(reps[0].solution, o.solution) <= 1e-7
+
+
+def test_concurrent_solves_on_threads_match_serial():
+    """SPEC.md:394 / experiments.py:196-198: independent solves may run concurrently on threads.
+    Four solves (different seeds / inputs) from a thread pool, each thread on its own stream and
+    each repeated so that its whole-solve graph is captured and replayed while the other threads
+    run, reproduce the serial results bit for bit; NumPy inputs on threads as well."""
+    from concurrent.futures import ThreadPoolExecutor
+    import paper_2209_04876_b200 as K
+    from paper_2209_04876_b200 import solvers as S
+    n, d = 4096, 32
+    probs = []
+    for k in range(4):
+        rs = np.random.default_rng(100 + k)
+        facs = [rs.normal(1.0, math.sqrt(1e-3), (n, d)) for _ in range(2)]
+        probs.append((facs, rs.standard_normal(n * n), cfg(seed=k)))
+    dev = [([torch.tensor(a, device="cuda") for a in f], torch.tensor(b, device="cuda"), c) for f, b, c in probs]
+    serial = [K.fast_kronecker_regression(f, b, c, with_loss=False) for f, b, c in dev]
+    serial_hist = []
+    for f, b, c in dev:
+        K.fast_kronecker_regression(f, b, c, with_loss=False)
+        serial_hist.append(S.last_solve_history())
+
+    def work(k):
+        f, b, c = dev[k]
+        st = torch.cuda.Stream()
+        outs = []
+        with torch.cuda.stream(st):
+            for _ in range(4):  # eager, capture, replays
+                r = K.fast_kronecker_regression(f, b, c, with_loss=False)
+                outs.append((r.solution.clone(), r.iterations, S.last_solve_history()))
+        st.synchronize()
+        return outs
+
+    with ThreadPoolExecutor(4) as ex:
+        got = list(ex.map(work, range(4)))
+    for k in range(4):
+        for x, it, h in got[k]:
+            assert it == serial[k].iterations
+            assert torch.equal(x, serial[k].solution)
+            assert h == serial_hist[k]
+    # NumPy inputs (eager path with host gathers) on threads
+    with ThreadPoolExecutor(4) as ex:
+        host = list(ex.map(lambda k: K.fast_kronecker_regression(probs[k][0], probs[k][1], probs[k][2],
+                                                                  with_loss=False), range(4)))
+    for k in range(4):
+        np.testing.assert_array_equal(host[k].solution, serial[k].solution.cpu().numpy())

@@ -46,11 +46,8 @@ from paper_2209_04876_b200 import solvers as _S  # noqa: E402
 print("prefix graph stats:", _S._PREFIX_STATS, "keys:", len(_S._PREFIX_GRAPHS), "solve graph stats:", _S._SOLVE_STATS)
 ph = (ctypes.c_double * 6)()
 if _lib.load().ks_debug_richardson_phases(rep.iterations, ph) == 0:
-    names = ["apply", "sync", "reduce+sync", "precondA+sync", "precondB+sync", "update"]
-    print("richardson phases (cycles/iter):", {k: round(v) for k, v in zip(names, ph)})
-    sp = (ctypes.c_double * 4)()
-    if _lib.load().ks_debug_richardson_apply_split(rep.iterations, sp) == 0:
-        print("  apply split (cycles/iter):", {k: round(v) for k, v in zip(["wait", "Y", "samples", "G"], sp)})
+    names = ["apply", "barrier_1", "reduce", "barrier_2", "norm_update", "loop_overhead"]
+    print("richardson phases (cycles/iter, last profiled run):", {k: round(v) for k, v in zip(names, ph)})
 
 if "--loop" in sys.argv:
     li = tr.loop_inputs
@@ -99,103 +96,3 @@ if "--loop" in sys.argv:
         print("fused rhs+loop us:", statistics.median(ts), "iters", it.value)
     _lib.load().ks_debug_richardson_phases(it.value, ph)
     print("  phases:", [round(v) for v in ph])
-
-
-if "--cta" in sys.argv:
-    nct = torch.cuda.get_device_properties(0).multi_processor_count
-    buf = (ctypes.c_uint64 * (9 * nct))()
-    _lib.load().ks_debug_richardson_cta_stamps.argtypes = [ctypes.c_int32, ctypes.c_void_p]
-    assert _lib.load().ks_debug_richardson_cta_stamps(nct, buf) == 0
-    ts = np.array(list(buf), dtype=np.float64).reshape(nct, 9)
-    t0 = ts[:, 0].min()
-    ts = (ts - t0) / 1e3
-    names = ["apply_start", "apply_end", "sync1_out", "reduce_end", "sync2_out", "precA_end", "sync3_out",
-             "precB_end", "sync4_out"]
-    for k, nm in enumerate(names):
-        col = ts[:, k]
-        print(f"{nm:12s} min {col.min():8.2f} us  median {np.median(col):8.2f}  max {col.max():8.2f}  argmax {col.argmax()}")
-    dur = ts[:, 1] - ts[:, 0]
-    print("apply duration: min %.2f median %.2f max %.2f us" % (dur.min(), np.median(dur), dur.max()))
-    print("slowest CTAs:", np.argsort(-dur)[:8], dur[np.argsort(-dur)[:8]].round(2))
-
-if "--trace" in sys.argv:
-    # kernel timeline of one solve (CUPTI via torch.profiler): start offset, duration, stream
-    import json
-    import tempfile
-    from torch.profiler import ProfilerActivity, profile
-    from paper_2209_04876_b200 import solvers as S2
-    K.fast_kronecker_regression(facs, b, cfg)
-    K.fast_kronecker_regression(facs, b, cfg)
-    before = dict(S2._PREFIX_STATS)
-    with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
-        rep = K.fast_kronecker_regression(facs, b, cfg)
-        torch.cuda.synchronize()
-    print("prefix graph stats before/after the traced solve:", before, dict(S2._PREFIX_STATS))
-    with tempfile.NamedTemporaryFile(suffix=".json", delete=False) as f:
-        path = f.name
-    prof.export_chrome_trace(path)
-    allev = json.load(open(path))["traceEvents"]
-    ev = [e for e in allev if e.get("ph") == "X" and e.get("cat") in ("kernel", "gpu_memcpy", "gpu_memset")]
-    rt = [e for e in allev if e.get("ph") == "X" and e.get("cat") == "cuda_runtime" and e.get("dur", 0) > 15]
-    ev.sort(key=lambda e: e["ts"])
-    t0 = ev[0]["ts"]
-    print(f"{'start_us':>9} {'dur_us':>8} {'gap_us':>7} strm  kernel")
-    prev_end = {}
-    for e in ev:
-        s = e["args"].get("stream", -1)
-        gap = e["ts"] - prev_end.get(s, e["ts"])
-        prev_end[s] = e["ts"] + e["dur"]
-        print(f"{e['ts'] - t0:9.1f} {e['dur']:8.1f} {gap:7.1f} {s:4}  {e['name'][:80]}")
-    import collections
-    agg = collections.defaultdict(lambda: [0, 0.0])
-    for e in allev:
-        if e.get("ph") == "X" and e.get("cat") == "cuda_runtime":
-            agg[e["name"]][0] += 1
-            agg[e["name"]][1] += e.get("dur", 0)
-    print("runtime API totals:")
-    for k, v in sorted(agg.items(), key=lambda kv: -kv[1][1]):
-        print(f"  {k:40s} {v[0]:5d} calls {v[1]:9.1f} us")
-    print("slow runtime API calls (>15 us):")
-    for e in sorted(rt, key=lambda e: e["ts"]):
-        print(f"{e['ts'] - t0:9.1f} {e['dur']:8.1f}   {e['name']}")
-    end = max(e["ts"] + e["dur"] for e in ev)
-    print(f"span {end - t0:.1f} us, wall {rep.wall_time * 1e6:.1f} us")
-
-if "--host" in sys.argv:
-    # host-side profile of one warm solve (where the wall time goes that is not GPU work)
-    import cProfile
-    import pstats
-    torch.cuda.synchronize()
-    pr = cProfile.Profile()
-    for _ in range(5):
-        pr.enable()
-        rep = K.fast_kronecker_regression(facs, b, cfg)
-        pr.disable()
-        torch.cuda.synchronize()
-    st = pstats.Stats(pr)
-    st.sort_stats("tottime").print_stats(45)
-
-if "--phases" in sys.argv:
-    import collections
-    from paper_2209_04876_b200 import solvers as S
-    gpu_t, host_t, walls2 = collections.defaultdict(list), collections.defaultdict(list), []
-    order = []
-    for rep_i in range(8):
-        S._PHASES = []
-        torch.cuda.synchronize()
-        rep = K.fast_kronecker_regression(facs, b, cfg)
-        torch.cuda.synchronize()
-        ph, S._PHASES = S._PHASES, None
-        walls2.append(rep.wall_time * 1e6)
-        prev = ph[0]
-        for name, th, ev in ph[1:]:
-            if name not in order:
-                order.append(name)
-            gpu_t[name].append(prev[2].elapsed_time(ev) * 1e3)
-            host_t[name].append(1e6 * (th - prev[1]))
-            prev = (name, th, ev)
-    print(f"phases over 8 solves: wall median {statistics.median(walls2):.0f} us min {min(walls2):.0f} us",
-          "solve graph stats:", S._SOLVE_STATS)
-    for name in order:
-        print(f"  {name:20s} gpu median {statistics.median(gpu_t[name]):8.1f} us   host-issue median "
-              f"{statistics.median(host_t[name]):8.1f} us")
