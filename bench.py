@@ -16,8 +16,10 @@ reference: sampling + preprocessing + Richardson, loss excluded) on the BASELINE
   cpu_baseline -- the oracle port of the reference (NumPy/OpenBLAS) on this host's cores.
 
 ``--impl reference`` times the reference's CPU implementation (oracle port) instead.
-Under torchrun (N>1) every rank solves the same problem (replicas) and rank 0
-reports the max over ranks.
+Under torchrun (N>1) the solve is row-sharded: rank r holds rows [lo, hi) of the
+n x n reshape of b, the sketch is replicated, the Richardson loop all-reduces its d^2 partial over
+NCCL once per pass inside one CUDA graph (distributed.sharded_fast_kronecker_regression); rank 0
+reports the max over ranks.  ``--sharded`` runs that path at N = 1 as well.
 """
 
 from __future__ import annotations
@@ -353,6 +355,134 @@ def run_ours(args):
     return result
 
 
+def run_sharded(args):
+    """N > 1 (or --sharded): the row-sharded solve of SURVEY.md 8(e).  Rank r holds both factors and
+    rows [lo, hi) of the n x n reshape of b; the sketch and eigendecompositions are replicated, the
+    Richardson loop runs on the rank's samples with one d^2 NCCL all-reduce per pass, all on the
+    device as one CUDA graph (distributed.sharded_fast_kronecker_regression).  value = the whole
+    solve's time per step (CUDA events, max over ranks); the loop alone is timed the same way for
+    the roofline (algorithmic FLOPs of the full problem / loop time / (N x FP64 peak))."""
+    import numpy as np
+    import torch
+    import paper_2209_04876_b200 as K
+    from paper_2209_04876_b200 import distributed as DS
+    from paper_2209_04876_b200.solvers import FastSolveTrace
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    import torch.distributed as dist
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    n, d = CONFIGS[args.config]
+    facs_h = make_inputs(n, d)
+    facs = [torch.tensor(a, device="cuda") for a in facs_h]
+    plan = DS.ShardPlan(ws, rank, n)
+    lo, hi = plan.rows
+    b_rows = torch.ones((hi - lo, n), dtype=torch.float64, device="cuda")
+    cfg = K.RegressionConfig(**PARAMS)
+    l2 = torch.zeros(64 * 1024 * 1024, dtype=torch.float64, device="cuda")
+
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(v):
+        if ws > 1:
+            t = torch.tensor([v], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            v = float(t.item())
+        return v
+
+    for _ in range(args.warmup):
+        DS.sharded_fast_kronecker_regression(facs, b_rows, cfg, plan)
+    barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    times = []
+    for _ in range(args.steps):
+        flush_l2(l2)
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        x, iters, hist = DS.sharded_fast_kronecker_regression(facs, b_rows, cfg, plan)
+        e1.record()
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1) / 1e3)
+    barrier()
+    clk = clocks.stop()
+    t_step = max_over_ranks(sum(times) / len(times))
+    # the captured loop alone (apply launches + NCCL all-reduces + update kernels)
+    loop = next(iter(DS._SHARDED_LOOPS.values()))
+    lts = []
+    for _ in range(5):
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        loop.replay()
+        e1.record()
+        e1.synchronize()
+        lts.append(e0.elapsed_time(e1) * 1e3)
+    loop_us = max_over_ranks(statistics.median(lts))
+    # e2e: factors from page-locked host memory every step, the solution back to the host
+    facs_pin = [torch.from_numpy(a).pin_memory() for a in facs_h]
+    e2e = []
+    for i in range(args.warmup + args.steps):
+        barrier()
+        t0 = time.perf_counter()
+        for f, fp in zip(facs, facs_pin):
+            f.copy_(fp, non_blocking=True)
+        xr, _, _ = DS.sharded_fast_kronecker_regression(facs, b_rows, cfg, plan)
+        xh = xr.cpu().numpy()
+        if i >= args.warmup:
+            e2e.append(time.perf_counter() - t0)
+    e2e_v = max_over_ranks(statistics.median(e2e))
+    # full-problem sketch sizes for the algorithmic FLOPs (SURVEY 8(d)): one traced single-GPU solve
+    tr = FastSolveTrace()
+    rep = K.fast_kronecker_regression(facs, torch.ones(n * n, dtype=torch.float64, device="cuda"), cfg, _trace=tr,
+                                      with_loss=False)
+    view = tr.loop_inputs["view"]
+    u1, nnz = view.u_left, view.nnz
+    flops_iter = 2.0 * u1 * d * d * 2 + 4.0 * nnz * d + 4.0 * d * d * (d + d)
+    k1 = sharded_k1_timing(facs, torch.ones(n * n, dtype=torch.float64, device="cuda"), n, d, ws, rank, barrier)
+    result = None
+    if rank == 0:
+        peak = fp64_peak_tflops()
+        ach = flops_iter * iters / (loop_us * 1e-6) / 1e12
+        result = {
+            "metric": METRIC, "value": t_step, "unit": "s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"fast_kronecker_regression {args.config}: n={n}, d={d}, N=2, b=ones(n^2), "
+                                   "lam=1e-3, eps=0.1, delta=0.01, alpha=1e-5, seed=0",
+                       "n": n, "d": d, "sample_count": rep.sample_count, "iterations": iters, "nnz": nnz,
+                       "parallelism": f"rowsharded{ws}", "rows_per_rank": hi - lo,
+                       "l2": "flushed (512 MB write) before every timed solve"},
+            "e2e": {"value": e2e_v, "unit": "s", "h2d_bytes_per_step": 2 * n * d * 8, "d2h_bytes_per_step": d * d * 8,
+                    "note": "factors uploaded from page-locked host memory every step, b row-sharded and resident "
+                            "(only its sampled entries are read), the solution copied back; max over ranks"},
+            "roofline": {"bound": "tensor", "kernel": "row-sharded Richardson loop (apply-only launches of the "
+                                                        "persistent eigenbasis kernel + NCCL all-reduce + update), "
+                                                        "all ranks",
+                         "achieved": ach, "peak": peak * ws, "unit": "TFLOP/s", "frac": ach / (peak * ws),
+                         "traffic": None, "launch_us": loop_us,
+                         "algorithmic_flops_per_launch": flops_iter * iters,
+                         "peak_source": f"{ws} x measured FP64 DMMA peak (profiles/r01_fp64_peak.txt)"},
+            "kernels": {"richardson_loop_rowsharded": {"us": loop_us, "iterations": iters,
+                                                       "us_per_iter": loop_us / max(iters, 1),
+                                                       "allreduce_bytes_per_iter": 8 * d * d},
+                        "kronmatmul_rowsharded": k1},
+            "gpu_launches_per_step": 3 * (iters + 1),
+            "gpu_launches": 3 * (iters + 1) * args.steps,
+            "clocks": clk,
+        }
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    del xh
+    return result
+
+
 def _timed(fn, reps=5):
     import torch
     fn()
@@ -531,9 +661,16 @@ def main():
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--cpu-reps", type=int, default=3)
     ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--sharded", action="store_true", help="run the row-sharded solve also at N = 1")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
-    res = run_reference(args) if args.impl == "reference" else run_ours(args)
+    ws, _, _ = dist_env()
+    if args.impl == "reference":
+        res = run_reference(args)
+    elif ws > 1 or args.sharded:
+        res = run_sharded(args)
+    else:
+        res = run_ours(args)
     if res is not None:
         print(json.dumps(res))
 

@@ -52,6 +52,10 @@ _SIGS = {
     "ks_richardson_fused_async": ([POINTER(SketchView), _p, _p, _p, _p, _p, _p, _p, _p, _d, _d, _i32, _d, _p, _p,
                                    _p, _p, _p, _p], ctypes.c_int),
     "ks_richardson_plan_bytes": ([_i64, _i64], ctypes.c_int64),
+    "ks_shard_loop_sizes": ([POINTER(SketchView), _p], ctypes.c_int),
+    "ks_shard_loop_pack": ([POINTER(SketchView), _p, _p, _p, _p, _p, _p, _p, _p, _p], ctypes.c_int),
+    "ks_shard_loop_apply": ([POINTER(SketchView), _p, _p, _p, _i32, _p, _p, _p, _p, _p], ctypes.c_int),
+    "ks_shard_loop_update": ([_i32, _p, _p, _p, _p, _p, _i32, _i32, _d, _d, _d, _p, _p, _p, _p], ctypes.c_int),
     "ks_richardson_plan_async": ([POINTER(SketchView), _p, _p, _p], ctypes.c_int),
     "ks_gather_count": ([_p, _p, _p, _i64, _p, _p], ctypes.c_int),
     "ks_richardson_fused": ([POINTER(SketchView), _p, _p, _p, _p, _p, _p, _p, _d, _d, _i32, _d, _p, _p, _p,

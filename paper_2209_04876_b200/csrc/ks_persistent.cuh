@@ -47,6 +47,13 @@ struct PArgs {
   int* state;             // [status, iters, hist_len]
   unsigned* flags;        // grid-barrier counters (ks_rich::BARRIER_WORDS, zeroed before the launch)
   long long* prof;        // profiling build only: CTA 0's phase clocks, 6 per iteration
+  // apply-only launches of the phase-separated kernel (the row-sharded loop, distributed.py):
+  // 1 = right-hand-side pass, 2 = one normal-operator apply at x_in; the reduced d_L x d_R result
+  // goes to g_out and the launch ends there (no step, no update); nothing runs when *stop != 0
+  int apply_only;
+  const double* x_in;     // d_L x d_R (eigenbasis x'), apply_only == 2
+  double* g_out;          // d_L x d_R
+  const int* stop;        // device flag (may be null)
 };
 
 

@@ -962,8 +962,8 @@ int launch(cudaStream_t st, PArgs& a, int grid) {
 
 namespace ks {
 
-static int64_t plan_cap(int64_t ul, int64_t nnz) { return (ul + CH_ROWS - 1) / CH_ROWS + nnz / CH_S + 2; }
-static size_t plan_range_offset(int64_t cap) { return (size_t)cap * (sizeof(Chunk) + sizeof(int64_t)); }
+int64_t plan_cap(int64_t ul, int64_t nnz) { return (ul + CH_ROWS - 1) / CH_ROWS + nnz / CH_S + 2; }
+size_t plan_range_offset(int64_t cap) { return (size_t)cap * (sizeof(Chunk) + sizeof(int64_t)); }
 
 static bool use_ws() { return !env(ENV_RICH_OLD); }
 static int g_prof_on = 0;  // ks_debug_richardson_profile: the profiling instantiation of the ws kernel
@@ -1128,5 +1128,150 @@ int richardson_persistent(cudaStream_t st, const ks_sketch_view* sk, const doubl
 // phase clocks (read by ks_debug_richardson_phases).  Off by default; never on the product path.
 extern "C" int ks_debug_richardson_profile(int32_t on) {
   ks::g_prof_on = on != 0;
+  return KS_OK;
+}
+
+// ===========================================================================
+// Row-sharded Richardson loop (distributed.py): every rank runs the phase-separated kernel in
+// apply-only mode on its own samples, the d_L x d_R partials are all-reduced over NCCL between
+// launches, and a one-CTA kernel applies the reference's step / stopping / divergence rules on the
+// device (solvers.py:212-247), so a whole sharded solve is launches + collectives with no host
+// round trip (capturable as one CUDA graph).
+// ===========================================================================
+
+namespace {
+
+constexpr int SU_T = 256;
+
+// it < 0: rhs' = g, tol = residual_tol max(||dinv o rhs'||, DBL_MIN); it >= 0: step' =
+// dinv o (g + lam x' - rhs'), ||step'|| into the history, stop / divergence rules, x' update.
+// state = [stopped, status (1 converged, 2 diverged), iterations, history length]; aux[0] = tol.
+__global__ void __launch_bounds__(SU_T) shard_update_kernel(int it, const double* __restrict__ g, double* x,
+                                                            double* rhs, const double* __restrict__ wL,
+                                                            const double* __restrict__ wR, int dL, int dR,
+                                                            double lam, double damping, double residual_tol,
+                                                            double* hist, int* state, double* aux) {
+  __shared__ double red[SU_T / 32];
+  __shared__ int s_flag;
+  if (state[0]) return;
+  const int ne = dL * dR, tid = threadIdx.x;
+  auto dinv = [&](int e) {  // solvers.py:186-191 on kron(wL, wR) + lam
+    const double ev = __dadd_rn(__dmul_rn(wL[e / dR], wR[e % dR]), lam);
+    return ev > 0.0 ? __ddiv_rn(1.0, ev) : 0.0;
+  };
+  double sq = 0.0;
+  if (it < 0) {
+    for (int e = tid; e < ne; e += SU_T) {
+      rhs[e] = g[e];
+      const double st = g[e] * dinv(e);
+      sq = fma(st, st, sq);
+    }
+    sq = block_sum(sq, red);
+    if (tid == 0) aux[0] = residual_tol * fmax(sqrt(sq), DBL_MIN);
+    return;
+  }
+  for (int e = tid; e < ne; e += SU_T) {
+    const double r = __dsub_rn(__dadd_rn(g[e], __dmul_rn(lam, x[e])), rhs[e]);
+    const double st = r * dinv(e);
+    sq = fma(st, st, sq);
+  }
+  sq = block_sum(sq, red);
+  const double nrm = sqrt(sq);
+  if (tid == 0) {
+    hist[it] = nrm;
+    const int hlen = it + 1;
+    int status = 0;
+    if (nrm <= aux[0]) {
+      status = 1;
+    } else if (hlen > 5) {
+      bool inc = true;
+      for (int i = hlen - 6; i < hlen - 1; i++) inc &= hist[i + 1] > hist[i];
+      if (inc && hist[hlen - 1] > 10.0 * hist[hlen - 6]) status = 2;
+    }
+    state[3] = hlen;
+    if (status) {
+      state[0] = 1;
+      state[1] = status;
+    } else {
+      state[2] = it + 1;
+    }
+    s_flag = status;
+  }
+  __syncthreads();
+  if (s_flag) return;
+  for (int e = tid; e < ne; e += SU_T) {
+    const double r = __dsub_rn(__dadd_rn(g[e], __dmul_rn(lam, x[e])), rhs[e]);
+    x[e] = __dsub_rn(x[e], __dmul_rn(damping, r * dinv(e)));
+  }
+}
+
+}  // namespace
+
+// Workspace sizes (doubles / bytes) of a sharded loop on this sketch view (capacities).
+extern "C" int ks_shard_loop_sizes(const ks_sketch_view* sk, int64_t* out4) {
+  const int grid = ks::num_sms();
+  const int64_t ne = (int64_t)sk->dL * sk->dR, epc = ((ne + grid - 1) / grid + 1) & ~1;
+  out4[0] = sk->u_left * (sk->dL + PAD) + 2;      // Lpack doubles
+  out4[1] = sk->nnz * (sk->dR + PAD) + 2;         // Rpack doubles
+  out4[2] = (int64_t)grid * grid * epc + grid;    // partials + per-CTA squares (doubles)
+  out4[3] = ks::richardson_plan_bytes(sk->u_left, sk->nnz) + BARRIER_WORDS * 4;  // plan + barrier bytes
+  return KS_OK;
+}
+
+// Pack this rank's sampled rows in the preconditioner's eigenbasis (L VL, R VR; v_t and v_t b_t in
+// the padding) and build the kernel's work plan.  counts_dev: [nnz, u_left] on the device or null.
+extern "C" int ks_shard_loop_pack(const ks_sketch_view* sk, const int64_t* counts_dev, const double* VL,
+                                  const double* VR, const double* b_at, const int64_t* perm, double* Lpack,
+                                  double* Rpack, void* plan_ws, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const int dL = sk->dL, dR = sk->dR, grid = ks::num_sms();
+  KS_REQUIRE(ks::richardson_ws_supported(dL, dR, grid), KS_ESIZE, "sharded loop: widths must be 16, 32 or 64");
+  int rc = ks::richardson_plan(st, sk, counts_dev, plan_ws);
+  if (rc) return rc;
+  XfJob jl{sk->Lmat, sk->ldl, sk->lrow, sk->u_left, counts_dev ? counts_dev + 1 : nullptr, dL + PAD, VL, nullptr,
+           nullptr, nullptr, Lpack};
+  XfJob jr{sk->Rmat, sk->ldr, sk->rrow, sk->nnz, counts_dev, dR + PAD, VR, sk->v, b_at, perm, Rpack};
+  if (sk->u_left > 0) {
+    if (dL == dR) {
+      xform_pair(st, dL, jl, jr);
+    } else {
+      xform_rows(st, dL, jl.src, jl.ld, jl.rows, jl.n_host, jl.n_dev, jl.dp, jl.V, jl.extra, jl.b, jl.perm, jl.dst);
+      KS_CHECK_LAUNCH();
+      xform_rows(st, dR, jr.src, jr.ld, jr.rows, jr.n_host, jr.n_dev, jr.dp, jr.V, jr.extra, jr.b, jr.perm, jr.dst);
+    }
+    KS_CHECK_LAUNCH();
+  }
+  return KS_OK;
+}
+
+// One apply-only launch: mode 1 = this rank's right-hand-side partial, mode 2 = its normal-operator
+// partial at x_in (eigenbasis); the reduced d_L x d_R partial goes to g_out.  No-op once *stop.
+extern "C" int ks_shard_loop_apply(const ks_sketch_view* sk, const double* Lpack, const double* Rpack,
+                                   const void* plan_ws, int32_t mode, const double* x_in, double* g_out,
+                                   const int32_t* stop, double* part_ws, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const int dL = sk->dL, dR = sk->dR, grid = ks::num_sms();
+  KS_REQUIRE(mode == 1 || mode == 2, KS_EINVAL, "sharded loop: mode must be 1 or 2");
+  const int64_t cap = ks::plan_cap(sk->u_left, sk->nnz);
+  char* base = (char*)plan_ws;
+  const int64_t ne = (int64_t)dL * dR, epc = ((ne + grid - 1) / grid + 1) & ~1;
+  PArgs a{};
+  a.Lpack = Lpack; a.Rpack = Rpack; a.seg = sk->seg;
+  a.chunks = (const Chunk*)base;
+  a.range = (const int64_t*)(base + ks::plan_range_offset(cap));
+  a.rhs_in_kernel = 1; a.eig_mode = 1; a.max_iters = 1;
+  a.part = part_ws;
+  a.rowsq = part_ws + (int64_t)grid * grid * epc;
+  a.flags = (unsigned*)(base + ks::richardson_plan_bytes(sk->u_left, sk->nnz));
+  a.apply_only = mode; a.x_in = x_in; a.g_out = g_out; a.stop = stop;
+  return ks::richardson_ws_launch(st, a, dL, dR, grid, false);
+}
+
+extern "C" int ks_shard_loop_update(int32_t it, const double* g, double* x, double* rhs, const double* wL,
+                                    const double* wR, int32_t dL, int32_t dR, double lam, double damping,
+                                    double residual_tol, double* hist, int32_t* state, double* aux, void* stream) {
+  shard_update_kernel<<<1, SU_T, 0, (cudaStream_t)stream>>>(it, g, x, rhs, wL, wR, dL, dR, lam, damping, residual_tol,
+                                                           hist, state, aux);
+  KS_CHECK_LAUNCH();
   return KS_OK;
 }

@@ -134,6 +134,7 @@ __global__ void __launch_bounds__(NT, 1) richardson_ws_kernel(PArgs a) {
 
   // this CTA's share of the sketch: the left rows and samples of its chunk range (contiguous in
   // the packed slabs; a row split between two CTAs' chunks contributes its samples to each)
+  if (a.apply_only && a.stop && *a.stop) return;  // the sharded loop has stopped: a uniform no-op
   const int64_t c_beg = a.range[b], c_end = a.range[b + 1];
   int64_t u0 = 0, t_lo = 0, t_hi = 0;
   int nrows = 0;
@@ -171,14 +172,16 @@ __global__ void __launch_bounds__(NT, 1) richardson_ws_kernel(PArgs a) {
   const int ystrip = warp % Y_STRIPS, ywarp = warp / Y_STRIPS;
   double xf[XK];
 #pragma unroll
-  for (int k = 0; k < XK; k++) xf[k] = 0.0;
+  for (int k = 0; k < XK; k++)
+    xf[k] = a.apply_only == 2 ? __ldg(&a.x_in[(4 * k + t4) * DR + 8 * ystrip + g]) : 0.0;
   // reduce-thread state (one element of this CTA's slice per 8-thread group, lane ql == 0):
   // rhs', dinv, x' and the last step' of that element
   double my_rhs = 0.0, my_dv = 0.0, my_x = 0.0, my_st = 0.0;
   double tol = 0.0;
   int status = 0, iters = 0, hlen = 0;
 
-  for (int it = -1; it < a.max_iters; it++) {
+  const int it_first = a.apply_only == 2 ? 0 : -1, it_last = a.apply_only ? it_first + 1 : a.max_iters;
+  for (int it = it_first; it < it_last; it++) {
     const bool rp = it < 0;  // right-hand-side pass: s_t = v_t (v_t b_t), no Y
     if (prof && !rp) {
       g_ws_prof[it * 6 + 0] = clock64();
@@ -205,7 +208,7 @@ __global__ void __launch_bounds__(NT, 1) richardson_ws_kernel(PArgs a) {
     for (int blk = 0; blk < nblk; blk++) {
       const int r0 = blk * ROWCAP, nbr = min(ROWCAP, nrows - r0);  // the block's rows: u0 + [r0, r0 + nbr)
       const int ntile = (nbr + CH_ROWS - 1) / CH_ROWS;
-      if (!resident || rp) {
+      if (!resident || it == it_first) {  // first pass of the launch, or rows that do not stay resident
         // the block's left rows (contiguous in the packed slab), one bulk copy, and each row's
         // sample range within this CTA's samples
         if (tid == 0) {
@@ -445,7 +448,9 @@ __global__ void __launch_bounds__(NT, 1) richardson_ws_kernel(PArgs a) {
           cmp = (up ? oc : cmp) + (up ? cmp : oc) + err;
           s = tt;
         }
-        if (ql == 0) {
+        if (ql == 0 && a.apply_only) {
+          a.g_out[e0 + eo] = s + cmp;  // this GPU's reduced partial (the sharded loop all-reduces it)
+        } else if (ql == 0) {
           const int e = e0 + eo, i = e / DR, k = e - i * DR;
           double r;
           if (rp) {
@@ -470,6 +475,7 @@ __global__ void __launch_bounds__(NT, 1) richardson_ws_kernel(PArgs a) {
       if (tid == 0) a.rowsq[b] = eig_sq;
       asm volatile("fence.proxy.async.global;" ::: "memory");
     }
+    if (a.apply_only) return;
     if (prof && !rp) g_ws_prof[it * 6 + 3] = clock64();
     grid_barrier(a.flags, G, b, ++epoch);
     if (prof && !rp) g_ws_prof[it * 6 + 4] = clock64();

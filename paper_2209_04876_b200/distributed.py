@@ -9,7 +9,10 @@ ranges of factor-0 rows, one rank per GPU:
                     every rank draws the same sketch); each rank keeps the samples whose factor-0
                     row it owns, and the Richardson loop all-reduces the d1*d2 Gram partial
                     H_local x once per iteration (the only exchange in the loop); the
-                    preconditioner and the update are replicated.
+                    preconditioner and the update are replicated.  On the device the loop is
+                    launches + NCCL collectives only (DeviceShardedLoop: apply-only launches of
+                    the persistent eigenbasis kernel, an in-graph all-reduce, a one-CTA update
+                    kernel with the stopping rules), captured as one CUDA graph.
 
 Collectives go through ``torch.distributed`` (NCCL on GPUs, gloo on CPU for the tests); the local
 compute is supplied by an ops object so the same plan runs the device kernels in production and
@@ -19,6 +22,7 @@ NumPy stand-ins in the CPU tests.
 from __future__ import annotations
 
 import math
+from ctypes import byref as ctypes_byref, c_int64 as ctypes_i64
 from dataclasses import dataclass
 
 import numpy as np
@@ -62,10 +66,11 @@ class ShardPlan:
 
 
 def allreduce_sum(t, dist=None):
-    """Sum a tensor over all ranks in place (no-op for a single process)."""
+    """Sum a tensor over all ranks in place (no-op without a process group; a group of one still
+    runs the collective, so the single-GPU tests exercise the NCCL path)."""
     if dist is None:
         import torch.distributed as dist  # noqa: F811
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+    if dist.is_available() and dist.is_initialized():
         dist.all_reduce(t)
     return t
 
@@ -212,27 +217,26 @@ def sharded_kronmatmul_svd_solve(factors, b_rows, lam: float, plan: ShardPlan, d
     return x, r2 + lam * float((x * x).sum().item())
 
 
-def sharded_fast_kronecker_regression(factors, b_rows, config, plan: ShardPlan, caches=None):
+def sharded_fast_kronecker_regression(factors, b_rows, config, plan: ShardPlan, caches=None, dist=None,
+                                      use_graph: bool = True):
     """fast_kronecker_regression (solvers.py:372-462) with b row-sharded over the ranks.
 
     Every rank holds both factors and its rows [lo, hi) of the n0 x n1 reshape of b (``b_rows``,
-    device, (hi - lo) x n1).  The sketch and the preconditioner are computed replicated (identical
-    NumPy-exact streams, so every rank draws the same sketch); each rank keeps the sampled rows
-    whose factor-0 index it owns, gathers their b entries locally, and the Richardson loop
-    all-reduces the d^2 normal-operator partial once per iteration (sharded_richardson).  Returns
-    (x, iterations, history).  With one rank it is the single-GPU algorithm through the
-    per-iteration kernels."""
-    import math
-
-    import torch
-
+    device, (hi - lo) x n1).  The sketch and the preconditioner's eigendecompositions are computed
+    replicated (identical NumPy-exact streams, so every rank draws the same sketch); each rank keeps
+    the sampled rows whose factor-0 index it owns and gathers their b entries locally.  The
+    Richardson loop then runs on the device with no host round trip (DeviceShardedLoop): per pass
+    one apply-only launch of the persistent eigenbasis kernel on the rank's samples, one NCCL
+    all-reduce of the d^2 partial, and a one-CTA kernel applying the reference's step, stopping and
+    divergence rules; the whole loop is captured as one CUDA graph.  Returns (x, iterations,
+    history); with one rank it is the single-GPU algorithm."""
     from . import _device as D
-    from .kron import SparseDiagonal, sketched_kron_apply, sketched_kron_transpose_apply
-    from .solvers import FactorGram, _fast_sketch_dev, _validated_problem, build_kron_preconditioner
+    from .kron import SparseDiagonal, _view_for
+    from .solvers import _fast_sketch_dev
 
     if len(factors) != 2:
         raise ValueError("the row-sharded fast solve covers the two-factor problem")
-    n0, n1 = int(factors[0].shape[0]), int(factors[1].shape[0])
+    n1 = int(factors[1].shape[0])
     facs = [D.to_dev(a) for a in factors]
     sdiag, grams, s = _fast_sketch_dev(facs, config, caches)
     lo, hi = plan.rows
@@ -241,15 +245,135 @@ def sharded_fast_kronecker_regression(factors, b_rows, config, plan: ShardPlan, 
     li, lv = keys[own].contiguous(), sdiag.values[own].contiguous()
     local = SparseDiagonal._trusted(li, lv)
     b_at = b_rows.reshape(-1)[li - lo * n1].contiguous()
-    rhs_local = sketched_kron_transpose_apply(facs, local, (lv * b_at).contiguous())
-    pre = build_kron_preconditioner([FactorGram(v=v, eigenvalues=w, matrix=None) for v, w in grams], config.lam)
+    (VL, wL), (VR, wR) = grams
+    view = _view_for(facs, local)
+    key = None
+    if use_graph:
+        import torch
+        key = (_state.thread_key(), torch.cuda.current_stream().cuda_stream,
+               tuple((a.data_ptr(), tuple(a.shape)) for a in facs), b_rows.data_ptr(), config, plan,
+               view.nnz, view.u_left)
+    loop = _state.cache_get(_SHARDED_LOOPS, key) if key is not None else None
+    if loop is None:
+        loop = DeviceShardedLoop(facs, view, VL, wL, VR, wR, b_at, config, dist)
+        if key is not None:
+            _state.cache_put(_SHARDED_LOOPS, key, loop, 4)
+    else:  # same shapes: repack this call's rows into the captured loop's buffers and replay it
+        loop.repack(view, VL, wL, VR, wR, b_at)
+    return loop.run(use_graph)
 
-    def normal_local(x):
-        return sketched_kron_transpose_apply(facs, local, sketched_kron_apply(facs, local, x))
 
-    x, iters, hist = sharded_richardson(normal_local, pre.apply, rhs_local, config.effective_damping,
-                                        config.effective_max_iters, config.residual_tol, torch, config.lam)
-    return x, iters, hist
+_SHARDED_LOOPS: dict = {}
+
+
+class DeviceShardedLoop:
+    """The row-sharded Richardson loop of one rank on the device (ks_shard_loop_* in
+    ks_richardson_persistent.cu).  Collective count and order are identical on every rank (a
+    rank that has stopped keeps issuing its all-reduces on stale partials), and every decision is
+    taken on identical all-reduced values, so the ranks stay in lockstep."""
+
+    def __init__(self, facs, view, VL, wL, VR, wR, b_at, config, dist=None):
+        import torch
+        from . import _device as D, _lib
+        self.torch, self.D, self.L = torch, D, _lib
+        if dist is None:
+            import torch.distributed as dist  # noqa: F811
+        self.dist = dist
+        self.view, self.config = view, config
+        self.dL, self.dR = view.dL, view.dR
+        self.VL, self.VR = VL.contiguous(), VR.contiguous()
+        self.wL, self.wR = wL.contiguous(), wR.contiguous()
+        sizes = (ctypes_i64 * 4)()
+        _lib.call("ks_shard_loop_sizes", ctypes_byref(view.struct), sizes)
+        self.Lp, self.Rp, self.part = D.empty(int(sizes[0])), D.empty(int(sizes[1])), D.empty(int(sizes[2]))
+        self.plan_ws = torch.empty(int(sizes[3]), dtype=torch.uint8, device=D.dev())
+        self.b_at = b_at
+        # the apply launches (and a captured graph of them) read the row segments through this
+        # loop-owned copy, so a repack for a new sketch of the same sizes keeps the graph valid
+        self.seg = view.seg.clone()
+        st = view.struct
+        self.struct = _lib.SketchView(st.Lmat, st.ldl, st.dL, st.Rmat, st.ldr, st.dR, st.u_left, st.nnz,
+                                      self.seg.data_ptr(), st.lrow, st.rrow, st.v)
+        _lib.call("ks_shard_loop_pack", ctypes_byref(view.struct), None, D.p(self.VL), D.p(self.VR), D.p(b_at),
+                  D.p(view.perm_arg()), D.p(self.Lp), D.p(self.Rp), D.p(self.plan_ws), D.stream())
+        self.max_iters = config.effective_max_iters
+        self.x = D.zeros(self.dL, self.dR)
+        self.rhs = D.zeros(self.dL, self.dR)
+        self.g = D.zeros(self.dL, self.dR)
+        self.hist = D.zeros(max(1, self.max_iters))
+        self.state = torch.zeros(4, dtype=torch.int32, device=D.dev())
+        self.aux = D.zeros(1)
+
+    def repack(self, view, VL, wL, VR, wR, b_at):
+        """New sketch / eigendecomposition of the same sizes into the existing buffers."""
+        D, L = self.D, self.L
+        self.view = view  # keeps the new grouped-view buffers alive; the struct is passed by value
+        self.VL.copy_(VL)
+        self.VR.copy_(VR)
+        self.wL.copy_(wL)
+        self.wR.copy_(wR)
+        self.b_at = b_at
+        self.seg.copy_(view.seg)
+        L.call("ks_shard_loop_pack", ctypes_byref(view.struct), None, D.p(self.VL), D.p(self.VR), D.p(b_at),
+               D.p(view.perm_arg()), D.p(self.Lp), D.p(self.Rp), D.p(self.plan_ws), D.stream())
+
+    def _pass(self, it):
+        D, L, c = self.D, self.L, self.config
+        L.call("ks_shard_loop_apply", ctypes_byref(self.struct), D.p(self.Lp), D.p(self.Rp), D.p(self.plan_ws),
+               1 if it < 0 else 2, D.p(self.x), D.p(self.g), D.p(self.state), D.p(self.part), D.stream())
+        allreduce_sum(self.g, self.dist)
+        L.call("ks_shard_loop_update", it, D.p(self.g), D.p(self.x), D.p(self.rhs), D.p(self.wL), D.p(self.wR),
+               self.dL, self.dR, float(c.lam), float(c.effective_damping), float(c.residual_tol), D.p(self.hist),
+               D.p(self.state), D.p(self.aux), D.stream())
+
+    def body(self):
+        self.state.zero_()
+        self.x.zero_()
+        for it in range(-1, self.max_iters):
+            self._pass(it)
+
+    graph = None
+
+    def run(self, use_graph: bool = True):
+        torch = self.torch
+        if use_graph and self.graph is None:
+            try:
+                self.body()  # warm-up (lazy initialisations, NCCL communicator) before capture
+                graph = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(graph):
+                    self.body()
+                self.graph = graph
+            except Exception:
+                self.graph = None
+        if use_graph and self.graph is not None:
+            self.graph.replay()
+        else:
+            self.body()
+        state = self.state.cpu().tolist()
+        hist = self.hist[: state[3]].cpu().tolist()
+        if state[1] == 2:
+            from .errors import NumericalFailureError
+            raise NumericalFailureError("Richardson iteration diverged", iterations=state[2],
+                                        diagnostics={"residual_history": hist})
+        return self.natural_x(), state[2], hist
+
+    def replay(self):
+        """Re-run the captured loop (benchmarking); returns nothing."""
+        if self.graph is not None:
+            self.graph.replay()
+        else:
+            self.body()
+
+    def natural_x(self):
+        """x = VL x' VR^T back in the natural (grouped) order."""
+        D, L = self.D, self.L
+        t = D.empty(self.dL, self.dR)
+        out = D.empty(self.dL, self.dR)
+        L.call("ks_gemm", self.dL, self.dR, self.dL, 1.0, D.p(self.VL), self.dL, 1, 0, D.p(self.x), self.dR, 1, 0,
+               0.0, D.p(t), self.dR, 1, 0, 1, D.stream())
+        L.call("ks_gemm", self.dL, self.dR, self.dR, 1.0, D.p(t), self.dR, 1, 0, D.p(self.VR), 1, self.dR, 0, 0.0,
+               D.p(out), self.dR, 1, 0, 1, D.stream())
+        return self.view.from_groups(out)
 
 
 # Public entry points are gated (capture vs. concurrent solves, see _state.py).
