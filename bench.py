@@ -349,6 +349,15 @@ def run_ours(args):
         }
         if not args.skip_cpu:
             result["cpu_baseline"] = cpu_baseline(args.config, args.cpu_reps)
+        if not args.no_extra:  # the other BASELINE configurations, each with its own roofline and clocks
+            del b
+            torch.cuda.empty_cache()
+            result["configs"] = {}
+            for name, fn in (("c4_d64", extra_c4), ("c5_tucker_core", extra_c5)):
+                try:
+                    result["configs"][name] = fn(args, l2)
+                except Exception as exc:  # reported, never fatal for the headline line
+                    result["configs"][name] = {"error": repr(exc)[:300]}
     if ws > 1:
         torch.distributed.barrier()
         torch.distributed.destroy_process_group()
@@ -481,6 +490,180 @@ def run_sharded(args):
         dist.destroy_process_group()
     del xh
     return result
+
+
+def _events_median(fn, reps, flush=None):
+    """Median device time (s) of fn() over reps, CUDA events on the current stream, optional L2
+    flush before every rep (outside the events)."""
+    import torch
+    ts = []
+    for _ in range(reps):
+        if flush is not None:
+            flush()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn()
+        e1.record()
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1) / 1e3)
+    return statistics.median(ts)
+
+
+def extra_c4(args, l2):
+    """BASELINE config 4 at d = 64 (and the K1 pass at d = 16): n = 65536, b = default_rng(0).
+    standard_normal(n^2) regenerated in HBM (34.4 GB).  The fast solve through the public API
+    (whole-solve graph), the exact solve, the KronMatMul (K1) and loss (K2) passes with their
+    roofline fractions, clocks over the timed region, and the oracle port's time on the host."""
+    import numpy as np
+    import torch
+    import paper_2209_04876_b200 as K
+    from paper_2209_04876_b200 import _lib as L, _device as D, solvers as S
+    from paper_2209_04876_b200.leverage import device_standard_normal
+    n = 65536
+    peak = fp64_peak_tflops()
+    hbm, hbm_src = hbm_peak_gbs()
+    b = device_standard_normal(0, n * n)
+    cfg = K.RegressionConfig(**PARAMS)
+    out = {"workload": "fast_kronecker_regression c4: n=65536, d=64, N=2, b=default_rng(0).standard_normal(n^2) "
+                       "(34.4 GB, generated in HBM), lam=1e-3, eps=0.1, delta=0.01, alpha=1e-5, seed=0"}
+    facs = [torch.tensor(a, device="cuda") for a in make_inputs(n, 64)]
+    for _ in range(max(args.warmup, 3)):
+        rep = K.fast_kronecker_regression(facs, b, cfg, with_loss=False)
+    clocks = ClockSampler(0)
+    clocks.start()
+    loop_us = []
+
+    def solve():
+        K.fast_kronecker_regression(facs, b, cfg, with_loss=False)
+    ts = []
+    for _ in range(args.steps):
+        ts.append(_events_median(solve, 1, lambda: flush_l2(l2)))
+        if S._LAST_LOOP_EVENTS[0] is not None:
+            l0, l1 = S._LAST_LOOP_EVENTS[0]
+            loop_us.append(l0.elapsed_time(l1) * 1e3)
+    t_exact = _events_median(lambda: K.kronmatmul_svd_solve(facs, b, PARAMS["lam"]), 3, lambda: flush_l2(l2))
+    T = torch.empty(64, 64, dtype=torch.float64, device="cuda")
+    k1 = lambda: L.call("ks_kron2_contract", D.p(facs[0]), D.p(b), n, D.p(facs[1]), n, n, 64, 64, D.p(T),  # noqa: E731
+                        D.stream())
+    t_k1 = _events_median(k1, 3, lambda: flush_l2(l2))
+    X = torch.randn(64, 64, dtype=torch.float64, device="cuda")
+    o = torch.empty(1, dtype=torch.float64, device="cuda")
+    k2 = lambda: L.call("ks_kron2_residual_sumsq", D.p(facs[0]), D.p(X), D.p(facs[1]), D.p(b), n, n, n, 64, 64,  # noqa: E731
+                        D.p(o), D.stream())
+    t_k2 = _events_median(k2, 3, lambda: flush_l2(l2))
+    f16 = [torch.tensor(a, device="cuda") for a in make_inputs(n, 16)]
+    T16 = torch.empty(16, 16, dtype=torch.float64, device="cuda")
+    k1_16 = lambda: L.call("ks_kron2_contract", D.p(f16[0]), D.p(b), n, D.p(f16[1]), n, n, 16, 16, D.p(T16),  # noqa: E731
+                           D.stream())
+    t_k1_16 = _events_median(k1_16, 3, lambda: flush_l2(l2))
+    out["clocks"] = clocks.stop()
+    by = 8.0 * n * n
+    fl64 = 2.0 * n * n * 64 + 2.0 * n * 64 * 64
+    fl16 = 2.0 * n * n * 16 + 2.0 * n * 16 * 16
+    tr = S.FastSolveTrace()
+    K.fast_kronecker_regression(facs, b, cfg, _trace=tr, with_loss=False)
+    view = tr.loop_inputs["view"]
+    flops_iter = 2.0 * view.u_left * 64 * 64 * 2 + 4.0 * view.nnz * 64 + 4.0 * 64 * 64 * 128
+    lu = statistics.median(loop_us) if loop_us else None
+    out.update({
+        "metric": "FastKronReg solve time (s) at n=65536,d=64", "value": statistics.median(ts), "unit": "s",
+        "sample_count": rep.sample_count, "iterations": rep.iterations, "nnz": view.nnz,
+        "exact_solve_s": t_exact,
+        "roofline": {"bound": "tensor", "kernel": "persistent eigenbasis Richardson loop (graph-replayed launch)",
+                     "achieved": flops_iter * rep.iterations / (lu * 1e-6) / 1e12 if lu else None,
+                     "peak": peak, "unit": "TFLOP/s",
+                     "frac": flops_iter * rep.iterations / (lu * 1e-6) / 1e12 / peak if lu else None,
+                     "launch_us": lu, "traffic": None},
+        "kernels": {
+            "kronmatmul_d64": {"us": t_k1 * 1e6, "tflops": fl64 / t_k1 / 1e12, "frac_fp64": fl64 / t_k1 / 1e12 / peak,
+                               "gbs": by / t_k1 / 1e9, "frac_hbm": by / t_k1 / 1e9 / hbm, "bound": "fp64"},
+            "loss_pass_d64": {"us": t_k2 * 1e6, "frac_fp64": fl64 / t_k2 / 1e12 / peak, "frac_hbm": by / t_k2 / 1e9 / hbm},
+            "kronmatmul_d16": {"us": t_k1_16 * 1e6, "gbs": by / t_k1_16 / 1e9, "frac_hbm": by / t_k1_16 / 1e9 / hbm,
+                               "frac_fp64": fl16 / t_k1_16 / 1e12 / peak, "bound": "hbm",
+                               "note": "K1 of the exact solve at c4 d=16: 34.4 GB of b read once"}},
+        "peaks": {"fp64_tflops": peak, "hbm_gbs": hbm, "hbm_source": hbm_src},
+    })
+    del b
+    torch.cuda.empty_cache()
+    if not args.skip_cpu:
+        from oracle import kronsolve_oracle as O
+        fh = make_inputs(n, 64)
+        t0 = time.perf_counter()
+        r = O.fast_kronecker_regression(fh, None, with_loss=False, b_at=lambda idx: np.ones(len(idx)), **PARAMS)
+        out["cpu_baseline"] = {"value": r.wall_time, "unit": "s", "cores": os.cpu_count(), "kind": "port",
+                               "sample": "one oracle fast_kronecker_regression at c4 d=64 with b read as ones at "
+                                         "the sampled rows (the solve's cost does not depend on b's values; "
+                                         "streaming default_rng(0).standard_normal(n^2) on the host alone takes "
+                                         "~90 s)", "run_s": time.perf_counter() - t0}
+    return out
+
+
+def extra_c5(args, l2):
+    """BASELINE config 5: Tucker ALS core update (tucker.py:108-127) on the 512 x 512 x 64 synthetic
+    tensor, rank (16, 16, 4).  The exact core (K13: U0^T B (U1 kron U2) on the TMA + DMMA K1 kernel,
+    B = the 512 x 32768 reshape of X) and the fast core (cached factor SVDs / Grams), their ALS
+    'sweepK-core' step times, the K13 / K14 passes against the HBM roofline, and the oracle port."""
+    import numpy as np
+    import torch
+    import paper_2209_04876_b200 as K
+    from paper_2209_04876_b200 import _lib as L, _device as D, solvers as S
+    from oracle import kronsolve_oracle as O
+    peak = fp64_peak_tflops()
+    hbm, _ = hbm_peak_gbs()
+    shape, rank, lam = (512, 512, 64), (16, 16, 4), 1e-3
+    x = O.synth_tucker(shape, rank, 0.01, 0)
+    xd = torch.tensor(x, device="cuda")
+    cfg = K.RegressionConfig(eps=0.1, delta=0.01, lam=lam, alpha=1e-5, seed=0)
+    model = K.initial_model(xd, rank, lam, 0)
+    model.core = K.core_update(model, xd, mode="exact")
+    caches = [K.build_factor_cache(a) for a in model.factors]
+    clocks = ClockSampler(0)
+    clocks.start()
+    t_exact = _events_median(lambda: K.core_update(model, xd, mode="exact"), max(args.steps, 5), lambda: flush_l2(l2))
+    t_fast = _events_median(lambda: K.core_update(model, xd, mode="fast", config=cfg, caches=caches),
+                            max(args.steps, 5), lambda: flush_l2(l2))
+    U0, Ur = model.factors[0], S._kron_dev(model.factors[1:])
+    B = xd.reshape(512, -1)
+    T = torch.empty(16, 64, dtype=torch.float64, device="cuda")
+    k13 = lambda: L.call("ks_kron2_contract", D.p(U0), D.p(B), int(B.shape[1]), D.p(Ur), 512, int(B.shape[1]), 16, 64,  # noqa: E731
+                         D.p(T), D.stream())
+    t13 = _events_median(k13, 10, lambda: flush_l2(l2))
+    Xc = torch.randn(16, 64, dtype=torch.float64, device="cuda")
+    o = torch.empty(1, dtype=torch.float64, device="cuda")
+    k14 = lambda: L.call("ks_kron2_residual_sumsq", D.p(U0), D.p(Xc), D.p(Ur), D.p(B), int(B.shape[1]), 512,  # noqa: E731
+                         int(B.shape[1]), 16, 64, D.p(o), D.stream())
+    t14 = _events_median(k14, 10, lambda: flush_l2(l2))
+    als = {}
+    for mode in ("exact", "fast"):
+        _, rep = K.tucker_als(xd, rank, lam=lam, sweeps=3, solver_mode=mode, config=cfg)
+        core_steps = [s for lab, s in zip(rep.step_labels, rep.step_seconds) if lab.endswith("-core")]
+        als[mode] = {"sweep_core_s": core_steps, "mean_sweep_s": rep.mean_sweep_seconds, "rre": rep.rre}
+    clk = clocks.stop()
+    by = 8.0 * x.size
+    fl = 2.0 * x.size * 64 + 2.0 * 512 * 16 * 64
+    out = {"workload": "Tucker ALS core update c5: 512x512x64 = Tucker(core 16x16x4) + N(0, 0.01^2), rank "
+                       "(16,16,4), lam=1e-3, eps=0.1, delta=0.01, alpha=1e-5, seed 0",
+           "metric": "core_update time (s)", "unit": "s", "exact_core_s": t_exact, "fast_core_s": t_fast,
+           "als": als, "clocks": clk,
+           "roofline": {"bound": "hbm", "kernel": "K13: U0^T B (U1 kron U2) (TMA + DMMA K1 kernel, right group "
+                                                 "materialised)", "achieved": by / t13 / 1e9, "peak": hbm,
+                        "unit": "GB/s", "frac": by / t13 / 1e9 / hbm, "launch_us": t13 * 1e6, "traffic": None},
+           "kernels": {"k13_exact_core_contraction": {"us": t13 * 1e6, "frac_hbm": by / t13 / 1e9 / hbm,
+                                                      "frac_fp64": fl / t13 / 1e12 / peak},
+                       "k14_residual": {"us": t14 * 1e6, "frac_hbm": by / t14 / 1e9 / hbm}}}
+    if not args.skip_cpu:
+        facs_h = [a.cpu().numpy() for a in model.factors]
+        t0 = time.perf_counter()
+        O.core_update_exact(facs_h, x, lam)
+        te = time.perf_counter() - t0
+        oc = [O.factor_cache(a) for a in facs_h]
+        t0 = time.perf_counter()
+        O.core_update_fast(facs_h, x, lam, oc, eps=0.1, delta=0.01, alpha=1e-5, seed=0)
+        tf = time.perf_counter() - t0
+        out["cpu_baseline"] = {"value": te, "unit": "s", "cores": os.cpu_count(), "kind": "port",
+                               "sample": "one oracle exact core update (and one fast, fast_s) at c5", "fast_s": tf}
+    return out
 
 
 def _timed(fn, reps=5):
@@ -662,6 +845,7 @@ def main():
     ap.add_argument("--cpu-reps", type=int, default=3)
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--sharded", action="store_true", help="run the row-sharded solve also at N = 1")
+    ap.add_argument("--no-extra", action="store_true", help="skip the c4 d=64 / c5 Tucker sub-results")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     ws, _, _ = dist_env()

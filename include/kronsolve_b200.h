@@ -307,6 +307,32 @@ int ks_debug_jacobi_stamps(long long* out4);
 /* Profiling aid: cycles of the FP32 prelude, its FP64 transition and the FP64 rounds (CTA 0). */
 int ks_debug_jacobi_mix(long long* out3);
 
+/* Row-sharded Richardson loop (distributed.py; replaces the per-rank part of
+ * richardson_solve, solvers.py:201-248, in a row-sharded fast_kronecker_regression).  Per rank:
+ *   ks_shard_loop_sizes  workspace capacities for a sketch view: out4 = [Lpack doubles, Rpack
+ *                        doubles, partial-sum doubles, plan + barrier bytes];
+ *   ks_shard_loop_pack   the rank's sampled rows in the preconditioner's eigenbasis (L VL, R VR,
+ *                        v_t and v_t b_t in the padding) and the kernel's work plan;
+ *   ks_shard_loop_apply  one apply-only launch of the persistent eigenbasis kernel: mode 1 = the
+ *                        rank's right-hand-side partial, mode 2 = its normal-operator partial at
+ *                        x_in; the reduced d_L x d_R partial goes to g_out (to be all-reduced);
+ *                        a no-op once *stop != 0;
+ *   ks_shard_loop_update one CTA: it < 0 stores rhs' = g and tol; it >= 0 forms step' = dinv o
+ *                        (g + lam x' - rhs'), records ||step'||, applies the stopping and divergence
+ *                        rules and updates x'.  state = [stopped, status (1 converged, 2 diverged),
+ *                        iterations, history length], aux[0] = tol.
+ * All asynchronous (capturable, with the all-reduces between them, as one CUDA graph). */
+int ks_shard_loop_sizes(const ks_sketch_view* sk, int64_t* out4);
+int ks_shard_loop_pack(const ks_sketch_view* sk, const int64_t* counts_dev, const double* VL, const double* VR,
+                       const double* b_at, const int64_t* perm, double* Lpack, double* Rpack, void* plan_ws,
+                       void* stream);
+int ks_shard_loop_apply(const ks_sketch_view* sk, const double* Lpack, const double* Rpack, const void* plan_ws,
+                        int32_t mode, const double* x_in, double* g_out, const int32_t* stop, double* part_ws,
+                        void* stream);
+int ks_shard_loop_update(int32_t it, const double* g, double* x, double* rhs, const double* wL, const double* wR,
+                         int32_t dL, int32_t dR, double lam, double damping, double residual_tol, double* hist,
+                         int32_t* state, double* aux, void* stream);
+
 /* Profiling aid: with on != 0, later launches of the phase-separated eigenbasis Richardson loop
  * run its profiling instantiation (CTA 0 records clock64 at every phase boundary); the product
  * path runs the instantiation without instrumentation.  Process-wide, default off. */
@@ -401,6 +427,12 @@ int ks_pinv_compose(const double* U, int64_t n, const double* sigma, const doubl
 /* sketch_rows_of_kron (kron.py:208-222): out (s x prod cols) = w[t] * (A_0[j_0] (x) ... (x) A_{nf-1}[j_{nf-1}])
  * for draw t; idx holds s x nf multi-indices (flat == 0) or s flat row indices (flat != 0).  The
  * materialised S K of sketch_and_solve_ridge (solvers.py:334-369). */
+/* Explicit Kronecker product C = A kron B of row-major A (m x p) and B (k x q) into C (m k x p q)
+ * (tensor.py:186-198 for two factors; the materialised right group of the N >= 3 KronMatMul and
+ * loss passes, solvers.py:314 / :261).  Asynchronous. */
+int ks_kron_explicit2(const double* A, int64_t m, int32_t p, const double* B, int64_t k, int32_t q, double* C,
+                      void* stream);
+
 int ks_sketch_rows(int32_t nf, const double* const* factors, const int64_t* rows, const int32_t* cols,
                    const int64_t* idx, int32_t flat, const double* w, int64_t s, double* out, void* stream);
 

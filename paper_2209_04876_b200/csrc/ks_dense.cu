@@ -59,3 +59,42 @@ extern "C" int ks_sketch_rows(int32_t nf, const double* const* factors, const in
   KS_CHECK_LAUNCH();
   return KS_OK;
 }
+
+// Explicit Kronecker product of two row-major matrices (tensor.py:186-198 for two factors; the
+// materialised right group of the three-factor KronMatMul / loss passes, solvers.py:314, :261):
+// C[(i k_rows + j), (a q + c)] = A[i, a] B[j, c].  Two consecutive outputs per thread (16-byte
+// stores when aligned); A and B are small and stay in L1/L2.
+namespace {
+__global__ void kron_explicit2_kernel(const double* __restrict__ A, int64_t m, int32_t p, const double* __restrict__ B,
+                                      int64_t k, int32_t q, double* __restrict__ C) {
+  const int64_t ncols = (int64_t)p * q, total = m * k * ncols;
+  const int64_t e = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 2;
+  if (e >= total) return;
+  auto at = [&](int64_t f) {  // element f of C
+    const int64_t r = f / ncols, col = f - r * ncols;
+    const int64_t i = r / k, j = r - i * k;
+    const int32_t a = (int32_t)(col / q), c = (int32_t)(col - (int64_t)a * q);
+    return __ldg(&A[i * p + a]) * __ldg(&B[j * q + c]);
+  };
+  const double v0 = at(e);
+  if (e + 1 < total) {
+    const double v1 = at(e + 1);
+    if (((uintptr_t)(C + e) & 15) == 0) *reinterpret_cast<double2*>(C + e) = make_double2(v0, v1);
+    else { C[e] = v0; C[e + 1] = v1; }
+  } else {
+    C[e] = v0;
+  }
+}
+
+}  // namespace
+
+extern "C" int ks_kron_explicit2(const double* A, int64_t m, int32_t p, const double* B, int64_t k, int32_t q,
+                                 double* C, void* stream) {
+  KS_REQUIRE(m >= 0 && k >= 0 && p >= 1 && q >= 1, KS_EINVAL, "kron_explicit2: bad shapes");
+  const int64_t pairs = (m * k * (int64_t)p * q + 1) / 2;
+  if (pairs == 0) return KS_OK;
+  kron_explicit2_kernel<<<ceil_div_u(pairs, 256), 256, 0, (cudaStream_t)stream>>>(A, m, p, B, k, q, C);
+  KS_CHECK_LAUNCH();
+  return KS_OK;
+}
+

@@ -253,12 +253,27 @@ def richardson_solve(apply_normal: Callable, apply_precond: Callable, rhs, dampi
     return x, iterations
 
 
+def _kron_dev(mats):
+    """A_1 kron ... kron A_k (row-major, on the device) by successive ks_kron_explicit2 launches."""
+    acc = mats[0].contiguous()
+    for a in mats[1:]:
+        a = a.contiguous()
+        m, p = int(acc.shape[0]), int(acc.shape[1])
+        k, q = int(a.shape[0]), int(a.shape[1])
+        if m * k * p * q == 0:
+            acc = D.zeros(m * k, p * q)
+            continue
+        out = D.empty(m * k, p * q)
+        _lib.call("ks_kron_explicit2", D.p(acc), m, p, D.p(a), k, q, D.p(out), D.stream())
+        acc = out
+    return acc
+
+
 def _split_first(facs):
     """(A_0, kron(A_1..)) with the right group materialised when N > 2."""
     if len(facs) == 2:
         return facs[0], facs[1]
-    r = reduce(torch.kron, facs[1:]).contiguous()
-    return facs[0], r
+    return facs[0], _kron_dev(facs[1:])
 
 
 def _ridge_loss_dev(facs: list[torch.Tensor], x: torch.Tensor, b: torch.Tensor, lam: float) -> float:
@@ -322,11 +337,17 @@ def _exact_solve_dev(facs: list[torch.Tensor], bt: torch.Tensor, lam: float) -> 
     ranks = [int(s[1].numel()) for s in svds]
     if min(ranks) == 0:
         return D.zeros(math.prod(int(a.shape[1]) for a in facs))
-    if len(facs) == 2 and ranks[0] <= 128 and ranks[1] <= 128:
-        n1, n2 = int(facs[0].shape[0]), int(facs[1].shape[0])
-        T = D.empty(ranks[0], ranks[1])
-        _lib.call("ks_kron2_contract", D.p(us[0]), D.p(bt), n2, D.p(us[1]), n1, n2, ranks[0], ranks[1], D.p(T),
-                  D.stream())
+    rest_rows = math.prod(int(a.shape[0]) for a in facs[1:])
+    rest_rank = math.prod(ranks[1:])
+    if len(facs) >= 2 and ranks[0] <= 128 and rest_rank <= 128 and rest_rows * rest_rank <= (1 << 25):
+        # the n^2 pass on the FP64 tensor pipe (TMA + DMMA K1 kernel): t = U_0^T B U_rest with
+        # B the n_0 x prod(n_rest) reshape of b and, for N >= 3, the right group's U's
+        # materialised as one Kronecker product (the Tucker core's K13: 512 x 32768 B at c5)
+        n1 = int(facs[0].shape[0])
+        U0, Ur = _split_first(us)
+        T = D.empty(ranks[0], rest_rank)
+        _lib.call("ks_kron2_contract", D.p(U0), D.p(bt), rest_rows, D.p(Ur.contiguous()), n1, rest_rows, ranks[0],
+                  rest_rank, D.p(T), D.stream())
         t = T.reshape(-1)
     else:
         t = _kron_apply_dev([u.T.contiguous() for u in us], bt.reshape(-1, 1).contiguous())[:, 0]

@@ -219,10 +219,8 @@ def explicit_kron(factors: Sequence, max_entries: int = EXPLICIT_KRON_MAX_ENTRIE
     if rows * cols > max_entries:
         raise SizeGuardError(f"explicit Kronecker product would hold {rows}x{cols} entries "
                              f"(guard: {max_entries})")
-    acc = mats[0]
-    for a in mats[1:]:
-        acc = (acc[:, None, :, None] * a[None, :, None, :]).reshape(acc.shape[0] * a.shape[0], -1)
-    return D.out(acc.contiguous(), host)
+    from .solvers import _kron_dev
+    return D.out(_kron_dev([D.to_dev(a) for a in mats]), host)
 
 
 def stack_columns(m):
