@@ -731,6 +731,11 @@ def stage_timings(K, facs, b, cfg, tr, n, d):
         if L.load().ks_debug_richardson_apply_split(iters, sp) == 0:
             phases["apply_split"] = dict(zip(["l_load_wait", "y_phase", "sample_phase", "g_phase"],
                                              [round(v) for v in sp]))
+        nct = torch.cuda.get_device_properties(0).multi_processor_count
+        st = (ctypes.c_uint64 * (2 * nct))()
+        if iters > 5 and L.load().ks_debug_richardson_cta_apply(nct, st) == 0:
+            ends = [st[2 * i + 1] - st[2 * i] for i in range(nct)]
+            phases["apply_ns_per_cta"] = {"min": min(ends), "median": statistics.median(ends), "max": max(ends)}
     dL, dR = view.dL, view.dR
     flops_apply = 2.0 * u1 * dL * dR * 2 + 4.0 * nnz * dR  # Y and G GEMMs over distinct left rows + dots/axpys
     flops_iter = flops_apply + 4.0 * dL * dR * (dL + dR)  # + preconditioner (four d x d x d products)

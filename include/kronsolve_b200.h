@@ -347,6 +347,10 @@ int ks_debug_richardson_phases(int32_t iters, double* out6);
  * L load wait, Y phase, sample phase, G phase (out8[4..7] unused). */
 int ks_debug_richardson_apply_split(int32_t iters, double* out8);
 
+/* Profiling aid: per-CTA apply start / end (%globaltimer, ns) of iteration 5 of the last profiled
+ * run: out[2 b], out[2 b + 1] for b < nctas <= 256. */
+int ks_debug_richardson_cta_apply(int32_t nctas, uint64_t* out);
+
 /* Preconditioner apply y = (VL kron VR) diag(dinv) (VL kron VR)^T r (solvers.py:180-183). */
 int ks_kron_precond_apply(const double* VL, const double* VR, int32_t dL, int32_t dR,
                           const double* dinv, const double* r, double* y, void* stream);

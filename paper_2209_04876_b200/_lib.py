@@ -93,6 +93,7 @@ _SIGS = {
     "ks_debug_richardson_phases": ([_i32, POINTER(c_double)], ctypes.c_int),
     "ks_debug_richardson_profile": ([_i32], ctypes.c_int),
     "ks_debug_richardson_apply_split": ([_i32, POINTER(c_double)], ctypes.c_int),
+    "ks_debug_richardson_cta_apply": ([_i32, _p], ctypes.c_int),
     "ks_pcg64_random_streams": ([_p, _i32, _i64, _i32, _i64, _p, _p], ctypes.c_int),
     "ks_factor_draws_rows": ([_i32, _p, _p, _p, _p, _i64, _i64, _p, _p, _p], ctypes.c_int),
     "ks_factor_workspace": ([_i32, _p, _p, _p, _p, _i32, _p, _p, _d, _d, _p, _p, _p, _p, _p, _p, _p],

@@ -64,6 +64,13 @@ struct PhSmem {
 
 __device__ long long g_ws_prof[6 * 1025];  // profiling instantiation only (ks_debug_richardson_phases)
 __device__ long long g_ws_split[8];        // profiling: CTA 0 apply split, summed over iterations
+__device__ unsigned long long g_ws_cta[2 * 256];  // profiling: per-CTA apply start / end (globaltimer) at iteration 5
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 // Grid barrier: two-level arrival counters, polled by one thread per CTA.  CTA b arrives at
 // group counter b % BAR_GROUPS (own 128-byte line); the group's last arrival (acq_rel atomic)
@@ -112,10 +119,10 @@ __global__ void __launch_bounds__(NT, 1) richardson_ws_kernel(PArgs a) {
   constexpr int Y_STRIPS = DR / 8;     // n8 strips of a 16-row Y tile
   static_assert(MW % Y_STRIPS == 0, "strips divide the DMMA warps");
   constexpr int WPS = MW / Y_STRIPS;   // DMMA warps per strip (they split the row tiles)
-  constexpr int YB = 4;                // Y row tiles in flight per warp
+  constexpr int YB = 8;                // Y row tiles in flight per warp
   constexpr int XK = DL / 4;           // k-steps of Y = L X' (X' fragments per strip)
   constexpr int QE2 = DR / 16;         // double2 per lane of a quarter-warp row
-  constexpr int SB = 4;                // samples per step of the sample phase
+  constexpr int SB = 2;                // samples per step of the sample phase
   extern __shared__ __align__(128) double sm[];
   uint64_t* lbar = reinterpret_cast<uint64_t*>(sm + S::DOUBLES);
   uint64_t* auxbar = lbar + 1;
@@ -187,6 +194,7 @@ __global__ void __launch_bounds__(NT, 1) richardson_ws_kernel(PArgs a) {
       g_ws_prof[it * 6 + 0] = clock64();
       pt = clock64();
     }
+    if (PROF && it == 5 && tid == 0 && b < 256) g_ws_cta[2 * b] = gtimer();
     // ---------------- apply: G = sum_c L_c^T Z_c ----------------
     // element e of CTA b's partial G goes to the slice of its reducer c = e / epc at
     // part[(c G + b) epc + e - c epc]: a reducer's G x epc operands are one contiguous block.  With
@@ -306,20 +314,18 @@ __global__ void __launch_bounds__(NT, 1) richardson_ws_kernel(PArgs a) {
         for (int step = 0; step < wsteps; step++) {
           const int n = step < nsteps ? min(SB, te - t) : 0;
           // SB samples per step: their loads in flight together (the right rows come from L2),
-          // dot products and shuffle reductions interleaved; z accumulates in sample order
+          // dot products and shuffle reductions interleaved; z accumulates in sample order.
+          // Every load is of a valid row (samples past the step's count re-read the last one and
+          // get weight 0), so the step has no branches and no zero fills.
           double2 rv[SB][QE2], pv[SB];
 #pragma unroll
           for (int i = 0; i < SB; i++) {
-            const double* Rt = Rbase + (int64_t)(t + i) * DRP;
-            if (i < n) {
+            const int ti = max(0, min(t + i, te - 1));
+            const double* Rt = Rbase + ti * DRP;
 #pragma unroll
-              for (int m = 0; m < QE2; m++) rv[i][m] = __ldg(reinterpret_cast<const double2*>(&Rt[2 * ql + 16 * m]));
-              pv[i] = __ldg(reinterpret_cast<const double2*>(&Rt[DR]));  // v_t, v_t b_t (row padding)
-            } else {
-#pragma unroll
-              for (int m = 0; m < QE2; m++) rv[i][m] = make_double2(0.0, 0.0);
-              pv[i] = make_double2(0.0, 0.0);
-            }
+            for (int m = 0; m < QE2; m++) rv[i][m] = __ldg(reinterpret_cast<const double2*>(&Rt[2 * ql + 16 * m]));
+            pv[i] = __ldg(reinterpret_cast<const double2*>(&Rt[DR]));  // v_t, v_t b_t (row padding)
+            if (i >= n) pv[i].x = 0.0;
           }
           double sv[SB];
           if (rp) {
@@ -345,13 +351,11 @@ __global__ void __launch_bounds__(NT, 1) richardson_ws_kernel(PArgs a) {
             for (int i = 0; i < SB; i++) sv[i] = pv[i].x * (pv[i].x * d[i]);
           }
 #pragma unroll
-          for (int i = 0; i < SB; i++) {
-            if (i < n) {
+          for (int i = 0; i < SB; i++) {  // sv = 0 past the step's count: z unchanged
 #pragma unroll
-              for (int m = 0; m < QE2; m++) {
-                z[m].x = fma(sv[i], rv[i][m].x, z[m].x);
-                z[m].y = fma(sv[i], rv[i][m].y, z[m].y);
-              }
+            for (int m = 0; m < QE2; m++) {
+              z[m].x = fma(sv[i], rv[i][m].x, z[m].x);
+              z[m].y = fma(sv[i], rv[i][m].y, z[m].y);
             }
           }
           t += SB;
@@ -409,6 +413,7 @@ __global__ void __launch_bounds__(NT, 1) richardson_ws_kernel(PArgs a) {
     // ---------------- partials -> reducers (written by the G phase) ----------------
     if (is_mma) asm volatile("fence.proxy.async.global;" ::: "memory");  // read back by the bulk-copy proxy
     if (prof && !rp) g_ws_prof[it * 6 + 1] = clock64();
+    if (PROF && it == 5 && tid == 0 && b < 256) g_ws_cta[2 * b + 1] = gtimer();
     grid_barrier(a.flags, G, b, ++epoch);
     if (prof && !rp) g_ws_prof[it * 6 + 2] = clock64();
     // ---------------- reduce: step' = dinv o (sum_cta G + lam x' - rhs') ----------------
@@ -664,5 +669,13 @@ extern "C" int ks_debug_richardson_apply_split(int32_t iters, double* out8) {
   long long h[8];
   KS_TRY_CUDA(cudaMemcpyFromSymbol(h, g_ws_split, sizeof(h)));
   for (int k = 0; k < 8; k++) out8[k] = (double)h[k] / iters;
+  return KS_OK;
+}
+
+// Profiling aid: per-CTA apply start / end (%globaltimer ns) of iteration 5 of the last profiled run,
+// out[2 b], out[2 b + 1] (the spread of the ends is the skew the first grid barrier absorbs).
+extern "C" int ks_debug_richardson_cta_apply(int32_t nctas, uint64_t* out) {
+  if (nctas < 1 || nctas > 256) return KS_EINVAL;
+  KS_TRY_CUDA(cudaMemcpyFromSymbol(out, g_ws_cta, sizeof(unsigned long long) * 2 * nctas));
   return KS_OK;
 }
