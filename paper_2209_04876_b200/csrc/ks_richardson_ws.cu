@@ -24,7 +24,7 @@
 // slower: both share the FP64 pipe).  After the apply, the CTA partials of G are reduced in a
 // fixed order (reduce-scatter over CTAs, one bulk copy per reducer), the step' =
 // dinv o (G' + lam x' - rhs') and its norm are formed, and every CTA updates its register copy
-// of x'.  Two grid barriers per iteration (two-level arrival counters), no host round trips.
+// of x'.  Two grid barriers per iteration (one release-add arrival counter), no host round trips.
 #include "ks_persistent.cuh"
 
 #include <cfloat>
@@ -72,20 +72,12 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
-// Grid barrier: two-level arrival counters, polled by one thread per CTA.  CTA b arrives at
-// group counter b % BAR_GROUPS (own 128-byte line); the group's last arrival (acq_rel atomic)
-// releases into the top counter, which every CTA polls with an acquire load.  Counts are
-// monotonic (target = epoch x group size), so nothing is reset between barriers.
-constexpr int BAR_GROUPS = 8;
-constexpr int BAR_STRIDE = 32;  // words between counters
-constexpr int BAR_WORDS = (BAR_GROUPS + 1) * BAR_STRIDE;
-static_assert(BAR_WORDS == BARRIER_WORDS, "grid-barrier counter block");
+// Grid barrier: one arrival counter (red.release.gpu), polled by one thread per CTA with acquire
+// loads; counts are monotonic (target = epoch x grid), so nothing is reset between barriers.
+// (Measured at c3 against cooperative_groups' grid sync -- the same -- and against a two-level
+// counter tree with acq_rel group atomics -- ~1.7k cycles slower per barrier.)
+constexpr int BAR_WORDS = 32;
 
-__device__ __forceinline__ unsigned atom_add_acq_rel_gpu(unsigned* p, unsigned v) {
-  unsigned old;
-  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
-  return old;
-}
 __device__ __forceinline__ void red_add_release_gpu(unsigned* p, unsigned v) {
   asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -95,16 +87,11 @@ __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
   return v;
 }
 
-__device__ __forceinline__ void grid_barrier(unsigned* ctr, int G, int b, unsigned epoch) {
+__device__ __forceinline__ void grid_barrier(unsigned* ctr, int G, unsigned epoch) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    const int ng = G < BAR_GROUPS ? G : BAR_GROUPS;
-    const int grp = b % ng;
-    const unsigned gsize = (unsigned)(G / ng + (grp < G % ng ? 1 : 0));
-    if (atom_add_acq_rel_gpu(&ctr[grp * BAR_STRIDE], 1u) + 1u == gsize * epoch)
-      red_add_release_gpu(&ctr[BAR_GROUPS * BAR_STRIDE], 1u);
-    const unsigned target = (unsigned)ng * epoch;
-    while (ld_acquire_gpu(&ctr[BAR_GROUPS * BAR_STRIDE]) < target) {
+    red_add_release_gpu(ctr, 1u);
+    while (ld_acquire_gpu(ctr) < (unsigned)G * epoch) {
     }
   }
   __syncthreads();
@@ -414,7 +401,7 @@ __global__ void __launch_bounds__(NT, 1) richardson_ws_kernel(PArgs a) {
     if (is_mma) asm volatile("fence.proxy.async.global;" ::: "memory");  // read back by the bulk-copy proxy
     if (prof && !rp) g_ws_prof[it * 6 + 1] = clock64();
     if (PROF && it == 5 && tid == 0 && b < 256) g_ws_cta[2 * b + 1] = gtimer();
-    grid_barrier(a.flags, G, b, ++epoch);
+    grid_barrier(a.flags, G, ++epoch);
     if (prof && !rp) g_ws_prof[it * 6 + 2] = clock64();
     // ---------------- reduce: step' = dinv o (sum_cta G + lam x' - rhs') ----------------
     {
@@ -482,7 +469,7 @@ __global__ void __launch_bounds__(NT, 1) richardson_ws_kernel(PArgs a) {
     }
     if (a.apply_only) return;
     if (prof && !rp) g_ws_prof[it * 6 + 3] = clock64();
-    grid_barrier(a.flags, G, b, ++epoch);
+    grid_barrier(a.flags, G, ++epoch);
     if (prof && !rp) g_ws_prof[it * 6 + 4] = clock64();
     // ---------------- norm, stopping rules (solvers.py:226-247), update ----------------
     if (!rp && tid == 0) {
