@@ -1,5 +1,8 @@
 """Tucker-ALS core update (BASELINE config 5) vs the reference golden fixture."""
 
+import json
+from pathlib import Path
+
 import numpy as np
 import pytest
 
@@ -7,6 +10,8 @@ from conftest import rel
 from oracle import kronsolve_oracle as O
 
 pytestmark = pytest.mark.gpu
+# the reference's own noise floor of the fast core (tests/golden/measure_floor.py aux -> floor.json)
+C5_FAST_FLOOR = json.loads((Path(__file__).resolve().parent / "golden" / "floor.json").read_text())["c5_fast_core"]["core"]
 
 
 @pytest.fixture(scope="module")
@@ -28,7 +33,7 @@ def test_core_update_exact_and_fast(golden, c5):
     caches = [K.build_factor_cache(a) for a in model.factors]
     cfg = K.RegressionConfig(eps=0.1, delta=0.01, lam=1e-3, alpha=1e-5, seed=0)
     fast = K.core_update(model, x, mode="fast", config=cfg, caches=caches)
-    assert rel(fast, g["core_fast"]) <= 1e-7
+    assert rel(fast, g["core_fast"]) <= 2 * C5_FAST_FLOOR
 
 
 def test_core_update_validation(c5):
