@@ -792,7 +792,7 @@ def count_launches(K, facs, b, cfg):
 def traffic_bytes():
     """DRAM bytes (read + write) per launch of the persistent Richardson kernel from the committed
     ncu --set full capture (profiles/), or None."""
-    p = ROOT / "profiles" / "r01_richardson_ncu_full.json"
+    p = ROOT / "profiles" / "r02_richardson_ncu_full.json"
     try:
         return json.loads(p.read_text())["dram_bytes_per_launch"]
     except (OSError, ValueError, KeyError):

@@ -1,5 +1,5 @@
 // Shared definitions of the persistent Richardson loop kernels (ks_richardson_persistent.cu: the
-// single-role kernel, natural basis or eigenbasis; ks_richardson_ws.cu: the phase-separated
+// single-role kernel, natural basis or eigenbasis; ks_richardson_phased.cu: the phase-separated
 // eigenbasis kernel) and of their device work plan: chunk geometry, kernel arguments, bulk-copy /
 // staging helpers.
 #pragma once
@@ -95,8 +95,8 @@ __device__ __forceinline__ void vecmat(const double* w, const double* M, int K, 
 }  // namespace ks_rich
 
 namespace ks {
-// The phase-separated eigenbasis loop (ks_richardson_ws.cu).  Returns KS_OK or a KS_* error.
-int richardson_ws_launch(cudaStream_t st, ks_rich::PArgs& a, int dL, int dR, int grid, bool prof);
-// Geometry / device check for richardson_ws_launch (else the single-role kernel runs).
-bool richardson_ws_supported(int dL, int dR, int grid);
+// The phase-separated eigenbasis loop (ks_richardson_phased.cu).  Returns KS_OK or a KS_* error.
+int richardson_phased_launch(cudaStream_t st, ks_rich::PArgs& a, int dL, int dR, int grid, bool prof);
+// Geometry / device check for richardson_phased_launch (else the single-role kernel runs).
+bool richardson_phased_supported(int dL, int dR, int grid);
 }  // namespace ks

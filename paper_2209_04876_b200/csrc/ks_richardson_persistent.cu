@@ -965,14 +965,14 @@ namespace ks {
 int64_t plan_cap(int64_t ul, int64_t nnz) { return (ul + CH_ROWS - 1) / CH_ROWS + nnz / CH_S + 2; }
 size_t plan_range_offset(int64_t cap) { return (size_t)cap * (sizeof(Chunk) + sizeof(int64_t)); }
 
-static bool use_ws() { return !env(ENV_RICH_OLD); }
-static int g_prof_on = 0;  // ks_debug_richardson_profile: the profiling instantiation of the ws kernel
+static bool use_phased() { return !env(ENV_RICH_OLD); }
+static int g_prof_on = 0;  // ks_debug_richardson_profile: the profiling instantiation of the phase-separated kernel
 
 static int launch_plan(cudaStream_t st, const ks_sketch_view* sk, int64_t ul, const int64_t* counts_dev, int dL,
                        int dR, int grid, Chunk* chunks, int64_t* cpre, int64_t* range) {
   const int64_t dmma = (int64_t)(CH_ROWS / 16) * (dR / 8) * (dL / 4) + (int64_t)(dL / 16) * (dR / 8) * (CH_ROWS / 4);
   int64_t wchunk, wsamp, wlong;
-  if (use_ws() && richardson_ws_supported(dL, dR, grid)) {
+  if (use_phased() && richardson_phased_supported(dL, dR, grid)) {
     // phase-separated loop: a chunk costs its DMMA issue time in the Y and G phases (8 SM cycles
     // per m16n8k4 at the FP64 tensor rate); the sample phase spreads a CTA's rows over 48
     // quarter-warps, ~10 cycles per sample of the CTA
@@ -1042,13 +1042,13 @@ int richardson_persistent(cudaStream_t st, const ks_sketch_view* sk, const doubl
   int* statep = state_dev ? state_dev : state_s.p;
   KS_REQUIRE(eig_mode <= rhs_in_kernel, KS_EINVAL, "the eigenbasis loop builds its own right-hand side");
   KS_REQUIRE(grid <= 192, KS_ESIZE, "persistent loop: at most 192 CTAs (norm staging)");
-  const bool ws = eig_mode && use_ws() && richardson_ws_supported(dL, dR, grid);
+  const bool phased = eig_mode && use_phased() && richardson_phased_supported(dL, dR, grid);
   // the single-role kernel's eigenbasis reduce keeps one element per thread: on parts with too few
   // SMs for d_L * d_R it runs in the natural basis instead
-  if (eig_mode && !ws && epc > PT / 8) eig_mode = false;
-  KS_REQUIRE(ws || (int64_t)grid * epc <= (int64_t)CH_S * (dR + PAD), KS_ESIZE,
+  if (eig_mode && !phased && epc > PT / 8) eig_mode = false;
+  KS_REQUIRE(phased || (int64_t)grid * epc <= (int64_t)CH_S * (dR + PAD), KS_ESIZE,
              "persistent loop: partial-sum staging exceeds the slab buffer for grid %d", grid);
-  Scratch<unsigned> flags(ws ? BARRIER_WORDS : 0, st);
+  Scratch<unsigned> flags(phased ? BARRIER_WORDS : 0, st);
   KS_REQUIRE(Lpack.p && Rpack.p && part.p && R.p && T.p && stepb.p && rowsq.p && VRt.p && chunks_p && range_p &&
                  (plan_ws || cpre.p) && statep && (!eig_mode || rhs_e.p),
              KS_ECUDA, "scratch allocation failed");
@@ -1099,7 +1099,7 @@ int richardson_persistent(cudaStream_t st, const ks_sketch_view* sk, const doubl
   a.state = statep;
   a.flags = flags.p;
   int rc;
-  if (ws) rc = richardson_ws_launch(st, a, dL, dR, grid, g_prof_on != 0);
+  if (phased) rc = richardson_phased_launch(st, a, dL, dR, grid, g_prof_on != 0);
   else if (dL == 16 && dR == 16) rc = launch<16, 16>(st, a, grid);
   else if (dL == 16 && dR == 32) rc = launch<16, 32>(st, a, grid);
   else if (dL == 16 && dR == 64) rc = launch<16, 64>(st, a, grid);
@@ -1225,7 +1225,7 @@ extern "C" int ks_shard_loop_pack(const ks_sketch_view* sk, const int64_t* count
                                   double* Rpack, void* plan_ws, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   const int dL = sk->dL, dR = sk->dR, grid = ks::num_sms();
-  KS_REQUIRE(ks::richardson_ws_supported(dL, dR, grid), KS_ESIZE, "sharded loop: widths must be 16, 32 or 64");
+  KS_REQUIRE(ks::richardson_phased_supported(dL, dR, grid), KS_ESIZE, "sharded loop: widths must be 16, 32 or 64");
   int rc = ks::richardson_plan(st, sk, counts_dev, plan_ws);
   if (rc) return rc;
   XfJob jl{sk->Lmat, sk->ldl, sk->lrow, sk->u_left, counts_dev ? counts_dev + 1 : nullptr, dL + PAD, VL, nullptr,
@@ -1264,7 +1264,7 @@ extern "C" int ks_shard_loop_apply(const ks_sketch_view* sk, const double* Lpack
   a.rowsq = part_ws + (int64_t)grid * grid * epc;
   a.flags = (unsigned*)(base + ks::richardson_plan_bytes(sk->u_left, sk->nnz));
   a.apply_only = mode; a.x_in = x_in; a.g_out = g_out; a.stop = stop;
-  return ks::richardson_ws_launch(st, a, dL, dR, grid, false);
+  return ks::richardson_phased_launch(st, a, dL, dR, grid, false);
 }
 
 extern "C" int ks_shard_loop_update(int32_t it, const double* g, double* x, double* rhs, const double* wL,

@@ -98,7 +98,7 @@ __device__ __forceinline__ void grid_barrier(unsigned* ctr, int G, unsigned epoc
 }
 
 template <int DL, int DR, bool PROF>
-__global__ void __launch_bounds__(NT, 1) richardson_ws_kernel(PArgs a) {
+__global__ void __launch_bounds__(NT, 1) richardson_phased_kernel(PArgs a) {
   using S = PhSmem<DL, DR>;
   constexpr int DLP = S::DLP, DRP = S::DRP, NE = S::NE, ROWCAP = S::NB * CH_ROWS;
   constexpr int GT_N = DR / 8, G_TILES = (DL / 16) * GT_N;
@@ -576,7 +576,7 @@ __global__ void __launch_bounds__(NT, 1) richardson_ws_kernel(PArgs a) {
 template <int DL, int DR, bool PROF>
 int launch_one(cudaStream_t st, PArgs& a, int grid) {
   using S = PhSmem<DL, DR>;
-  auto kern = richardson_ws_kernel<DL, DR, PROF>;
+  auto kern = richardson_phased_kernel<DL, DR, PROF>;
   KS_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::BYTES));
   int per_sm = 0;
   KS_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, S::BYTES));
@@ -606,7 +606,7 @@ static int block_chunks(int dL, int dR) {  // PhSmem<dL, dR>::NB
 
 namespace ks {
 
-bool richardson_ws_supported(int dL, int dR, int grid) {
+bool richardson_phased_supported(int dL, int dR, int grid) {
   auto ok = [](int d) { return d == 16 || d == 32 || d == 64; };
   if (!ok(dL) || !ok(dR) || grid > 192) return false;
   const int ne = dL * dR, epc = ((ne + grid - 1) / grid + 1) & ~1;
@@ -615,8 +615,8 @@ bool richardson_ws_supported(int dL, int dR, int grid) {
   return epc <= NT / 8 && (int64_t)grid * epc <= stage;
 }
 
-int richardson_ws_launch(cudaStream_t st, PArgs& a, int dL, int dR, int grid, bool prof) {
-  KS_REQUIRE(richardson_ws_supported(dL, dR, grid), KS_ESIZE, "phase-separated loop: unsupported geometry");
+int richardson_phased_launch(cudaStream_t st, PArgs& a, int dL, int dR, int grid, bool prof) {
+  KS_REQUIRE(richardson_phased_supported(dL, dR, grid), KS_ESIZE, "phase-separated loop: unsupported geometry");
   KS_REQUIRE(a.eig_mode && a.rhs_in_kernel && a.flags, KS_EINVAL, "phase-separated loop runs in the eigenbasis");
   if (dL == 16 && dR == 16) return launch_pair<16, 16>(st, a, grid, prof);
   if (dL == 16 && dR == 32) return launch_pair<16, 32>(st, a, grid, prof);
