@@ -301,11 +301,6 @@ int ks_debug_jl_projection_stamps(uint64_t* out4);
 /* Profiling aid: sweeps used by the last one-sided Jacobi launch (first 8 problems, host out8). */
 int ks_debug_jacobi_sweeps(int32_t* out8);
 
-/* Profiling aid: CTA 0 / thread 0 cycles of the last fixed-size one-sided Jacobi launch, summed
- * over rounds: (load + dot products + reductions, rotation + update, barrier, rounds); reset on read. */
-int ks_debug_jacobi_stamps(long long* out4);
-/* Profiling aid: cycles of the FP32 prelude, its FP64 transition and the FP64 rounds (CTA 0). */
-int ks_debug_jacobi_mix(long long* out3);
 
 /* Row-sharded Richardson loop (distributed.py; replaces the per-rank part of
  * richardson_solve, solvers.py:201-248, in a row-sharded fast_kronecker_regression).  Per rank:

@@ -70,8 +70,6 @@ _SIGS = {
     "ks_jl_projection": ([_p, _i32, _p, _i32, _d, _p, _p, _p], ctypes.c_int),
     "ks_jl_cholesky": ([_p, _i32, _p, _p, _p], ctypes.c_int),
     "ks_jl_solve": ([_p, _i32, _p, _i32, _d, _p, _p], ctypes.c_int),
-    "ks_debug_jacobi_stamps": ([_p], ctypes.c_int),
-    "ks_debug_jacobi_mix": ([_p], ctypes.c_int),
     "ks_debug_jacobi_sweeps": ([_p], ctypes.c_int),
     "ks_row_weighted_sumsq": ([_p, _i64, _i32, _p, _p, _p], ctypes.c_int),
     "ks_sampler_tables": ([_p, _i64, _i32, _p, _p, _p, _p], ctypes.c_int),

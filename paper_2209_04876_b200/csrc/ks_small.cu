@@ -227,9 +227,6 @@ __global__ void jacobi_svd_kernel(const double* __restrict__ M, int d, double* _
 // so the two pairs sharing a half-warp hit disjoint banks.  SYM: read 0.5 (M + M^T) (the
 // reference symmetrises the Gram before eigh).  Ms: optional per-problem pointers.
 constexpr int JF_G = 8;
-__device__ long long g_jstamp[4];
-__device__ long long g_jmix[4];  // debug: CTA 0 cycles of the FP32 prelude (sweeps, transition), FP64 phase  // debug: CTA 0 thread 0 cycles in (load+dot+shuffle, rotate+update, barrier), rounds
-#define JSTAMP (blockIdx.x == 0 && threadIdx.x == 0)
 struct MatPtrs {
   const double* p[8];
 };
@@ -281,7 +278,6 @@ __device__ void jacobi_fp32_prelude(const double* __restrict__ M, double* W, dou
   __syncthreads();
   const int group = tid / JF_G, lg = tid % JF_G;
   const float tol = 2.0f * D * 1.1920929e-7f;
-  const long long c0 = clock64();
   for (int sweep = 0; sweep < sweeps32; sweep++) {
     if (tid == 0) s_rot32 = 0;
     __syncthreads();
@@ -335,7 +331,6 @@ __device__ void jacobi_fp32_prelude(const double* __restrict__ M, double* W, dou
     if (s_rot32 == 0) break;
     __syncthreads();
   }
-  const long long c1 = clock64();
   // V (FP64) = V32, then two Newton-Schulz steps and W = G V.  X (the FP32 buffers, D (D + 8)
   // doubles) and Y (D (D + 8) doubles after them) are scratch; every product below is laid out so
   // that a warp's threads read consecutive elements or one broadcast element (no bank conflicts).
@@ -375,10 +370,6 @@ __device__ void jacobi_fp32_prelude(const double* __restrict__ M, double* W, dou
   smem_gemm_rows<D>([&](int i, int k) { return Y[k * D + i]; }, [&](int k, int j) { return V[j * LD + k]; },
                     [&](int i, int j, double v) { W[j * LD + i] = v; });
   __syncthreads();
-  if (blockIdx.x == 0 && tid == 0) {
-    g_jmix[0] = c1 - c0;
-    g_jmix[1] = clock64() - c1;
-  }
 }
 
 template <int D, bool SYM>
@@ -410,7 +401,6 @@ __global__ void __launch_bounds__(D / 2 * JF_G) jacobi_fixed_kernel(MatPtrs Ms, 
   }
   const int group = tid / JF_G, lg = tid % JF_G;
   const double tol = 2.0 * D * 2.220446049250313e-16;
-  long long js0 = 0, js1 = 0, js2 = 0, js3 = 0;
   for (int sweep = 0; sweep < 40; sweep++) {
     if (tid == 0) s_rot = 0;
     __syncthreads();
@@ -421,8 +411,6 @@ __global__ void __launch_bounds__(D / 2 * JF_G) jacobi_fixed_kernel(MatPtrs Ms, 
         return pos == 0 ? 0 : 1 + x;
       };
       const int p = player(group), q = player(D - 1 - group);
-      long long jt0 = 0;
-      if (JSTAMP) jt0 = clock64();
       double x[E], y[E], u[E], v[E];
 #pragma unroll
       for (int k = 0; k < E; k++) {
@@ -448,7 +436,6 @@ __global__ void __launch_bounds__(D / 2 * JF_G) jacobi_fixed_kernel(MatPtrs Ms, 
         b += __shfl_xor_sync(0xffffffffu, b, o);
         c += __shfl_xor_sync(0xffffffffu, c, o);
       }
-      if (JSTAMP) { const long long now = clock64(); js0 += now - jt0; jt0 = now; }
       if (c != 0.0 && a != 0.0 && b != 0.0 && c * c > tol * tol * a * b) {
         // t ~ tan(theta) = sign(x) y / (|x| + sqrt(x^2 + y^2)), x = b - a, y = 2c, from hardware
         // approximations refined by one Newton step each (t only steers the rotation; cs, and so
@@ -475,16 +462,12 @@ __global__ void __launch_bounds__(D / 2 * JF_G) jacobi_fixed_kernel(MatPtrs Ms, 
         }
         if (lg == 0) s_rot = 1;
       }
-      if (JSTAMP) { const long long now = clock64(); js1 += now - jt0; jt0 = now; }
       __syncthreads();
-      if (JSTAMP) { js2 += clock64() - jt0; js3 += 1; }
     }
     if (tid == 0) g_jacobi_sweeps[blockIdx.x & 7] = sweep + 1;
     if (s_rot == 0) break;
     __syncthreads();
   }
-  if (JSTAMP) { g_jstamp[0] = js0; g_jstamp[1] = js1; g_jstamp[2] = js2; g_jstamp[3] = js3; }
-  if (JSTAMP) g_jmix[2] = js0 + js1 + js2;
   for (int j = tid; j < D; j += NT) {
     double s = 0.0;
     for (int i = 0; i < D; i++) s = fma(W[jf_off<D>(j, i)], W[jf_off<D>(j, i)], s);
@@ -958,20 +941,7 @@ extern "C" int ks_inverse_small(const double* M, int32_t d, double* X, int32_t* 
   return KS_OK;
 }
 
-// Profiling aid: cycles of the FP32 prelude sweeps, its FP64 transition and the FP64 rounds of the
-// last fixed-size symmetric Jacobi launch (CTA 0).
-extern "C" int ks_debug_jacobi_mix(long long* out3) {
-  return cudaMemcpyFromSymbol(out3, g_jmix, 3 * sizeof(long long)) == cudaSuccess ? KS_OK : KS_ECUDA;
-}
-
 // Profiling aid: sweeps used by the last one-sided Jacobi launch (first 8 problems).
-extern "C" int ks_debug_jacobi_stamps(long long* out4) {
-  KS_TRY_CUDA(cudaMemcpyFromSymbol(out4, g_jstamp, sizeof(long long) * 4));
-  long long z[4] = {0, 0, 0, 0};
-  KS_TRY_CUDA(cudaMemcpyToSymbol(g_jstamp, z, sizeof(z)));
-  return KS_OK;
-}
-
 extern "C" int ks_debug_jacobi_sweeps(int32_t* out8) {
   KS_TRY_CUDA(cudaMemcpyFromSymbol(out8, g_jacobi_sweeps, sizeof(int) * 8));
   return KS_OK;

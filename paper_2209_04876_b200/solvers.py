@@ -487,12 +487,19 @@ def _jl_scores_chol(a: torch.Tensor, a_tilde: torch.Tensor, gram: torch.Tensor, 
     ``factor``: a workspace from _jl_factor (made on ``factor_stream``)."""
     from .leverage import _jl_ga, _jl_scores_from_q, check_later
     d = int(a.shape[1])
+    tl = _TL_CUR[0]
+    if pre_g is not None and tl is not None:
+        torch.cuda.current_stream().wait_event(pre_g[1])
+        _tl_event(tl, f"jl g ready ({int(a.shape[0])})")
     ga, r = _jl_ga(a, a_tilde, seed, log_factor, pre_g)
+    _tl_event(tl, "jl ga")
     q = D.empty(r, d)
     if use_chol and factor is not None:
         if factor_stream is not None:
             torch.cuda.current_stream().wait_stream(factor_stream)
+            _tl_event(tl, "jl factor ready")
         _lib.call("ks_jl_solve", D.p(factor), d, D.p(ga), r, 1.0 + eps / 4.0, D.p(q), D.stream())
+        _tl_event(tl, "jl solve")
     elif use_chol:
         info = torch.zeros(1, dtype=torch.int32, device=a.device)
         _lib.call("ks_jl_projection", D.p(gram), d, D.p(ga), r, 1.0 + eps / 4.0, D.p(q), D.p(info), D.stream())
