@@ -43,7 +43,9 @@ constexpr int SMEM_MAX = 232448;
 template <int DL, int DR>
 struct PhSmem {
   static constexpr int DLP = DL + PAD, DRP = DR + PAD, NE = DL * DR;
-  static constexpr int FIXED = 256 + 1024 + 16 * CH_ROWS;      // W scratch, history, row table (<= 16 x 16 rows)
+  static constexpr int QR = 8;                                 // rows per quarter-warp list (<= 16 x 16 rows / 48 + 1)
+  static constexpr int QLIST = (NQ * QR * 2 + 2 * 16 * 4 + 7) / 8;  // int16 row lists + cost histogram / cursors
+  static constexpr int FIXED = 256 + 1024 + 16 * CH_ROWS + QLIST;  // W scratch, history, row table, row lists
   static constexpr int PER_NB = CH_ROWS * DLP + CH_ROWS * DRP;  // L rows + Y/Z rows per chunk
   static constexpr int NB_FIT = (SMEM_MAX / 8 - 64 - FIXED - CH_ROWS * DLP) / PER_NB;
   static constexpr int NB = NB_FIT > 16 ? 16 : NB_FIT;        // chunks per block
@@ -53,9 +55,11 @@ struct PhSmem {
   static constexpr int W_OFF = YZ_OFF + NB * CH_ROWS * DRP;
   static constexpr int H_OFF = W_OFF + 256;
   static constexpr int C_OFF = H_OFF + 1024;
-  static constexpr int DOUBLES = C_OFF + NB * CH_ROWS;  // one int2 per row of a block
-  static constexpr size_t BYTES = (size_t)DOUBLES * 8 + 2 * 8;  // + mbarriers (L load, reduce operands)
+  static constexpr int Q_OFF = C_OFF + NB * CH_ROWS;    // one int2 per row of a block
+  static constexpr int DOUBLES = Q_OFF + QLIST;
+  static constexpr size_t BYTES = (size_t)DOUBLES * 8 + 3 * 8;  // + mbarriers (L load, reduce operands, resident R)
   static_assert(NB >= 4, "at least four chunks per block");
+  static_assert(NB * CH_ROWS <= NQ * (QR - 1), "quarter row lists hold a block's rows");
   static_assert(BYTES <= SMEM_MAX, "shared memory per CTA");
   static_assert(L_ROWS * DLP + NB * CH_ROWS * DRP >= DL * DRP + DR * DRP + DL * DRP,
                 "back-transform staging lives in the L and Y/Z buffers");
@@ -113,12 +117,13 @@ __global__ void __launch_bounds__(NT, 1) richardson_phased_kernel(PArgs a) {
   extern __shared__ __align__(128) double sm[];
   uint64_t* lbar = reinterpret_cast<uint64_t*>(sm + S::DOUBLES);
   uint64_t* auxbar = lbar + 1;
+  uint64_t* rbar = lbar + 2;
   int* rtab = reinterpret_cast<int*>(sm + S::C_OFF);  // per row of the block: sample range [tb, te)
+  short* qrows = reinterpret_cast<short*>(sm + S::Q_OFF);  // per quarter-warp: its rows of the block
+  int* qhist = reinterpret_cast<int*>(qrows + NQ * S::QR);  // 16 cost buckets, then 16 cursors
   double* Ls = sm + S::L_OFF;
-  double* YZ = sm + S::YZ_OFF;
   double* Ws = sm + S::W_OFF;
   double* Hs = sm + S::H_OFF;
-  double* AUXs = YZ;  // reduce operands, then the step (the Y/Z rows are dead by then)
   __shared__ int s_flag;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t4 = lane & 3;
@@ -141,9 +146,26 @@ __global__ void __launch_bounds__(NT, 1) richardson_phased_kernel(PArgs a) {
   }
   const int nblk = (nrows + ROWCAP - 1) / ROWCAP;
   const bool resident = nblk <= 1;  // the L rows stay loaded for the whole solve
+  const int epc = ((NE + G - 1) / G + 1) & ~1;  // reduce slice per CTA
+  // Shared-memory layout.  With several row blocks: L (L_ROWS) | Y/Z (ROWCAP rows) at fixed
+  // offsets.  When the CTA's rows fit one block, Y/Z follows the rows the tiles read and the space
+  // the block leaves free holds a resident copy of part of the CTA's right rows r_t (loaded once
+  // per launch): their share of the per-iteration L2 stream of the sample phase is gone.
+  double* YZ = sm + S::YZ_OFF;
+  double* Rres = nullptr;
+  int rcap = 0;  // right rows that fit the resident region
+  if (resident && nrows > 0 && !a.apply_only) {
+    const int lrows = ((nrows + CH_ROWS - 1) / CH_ROWS) * CH_ROWS;
+    YZ = Ls + (lrows + CH_ROWS) * DLP;  // the tiles read L rows < lrows; one chunk more, as L_ROWS
+    const int yz = max(lrows * DRP, G * epc);
+    Rres = YZ + ((yz + 15) & ~15);  // 128-byte aligned
+    rcap = max(0, (int)((sm + S::W_OFF) - Rres) / DRP);
+  }
+  double* AUXs = YZ;  // reduce operands (the Y/Z rows are dead by then)
   if (tid == 0) {
     mbar_init(lbar, 1);
     mbar_init(auxbar, 1);
+    mbar_init(rbar, 1);
     fence_barrier_init();
   }
   // rows past the block are read by the Y / G tiles (multiplied into Y rows the sample phase
@@ -152,6 +174,7 @@ __global__ void __launch_bounds__(NT, 1) richardson_phased_kernel(PArgs a) {
   __syncthreads();
   unsigned epoch = 0;
   uint32_t auxphase = 0, lphase = 0;
+  int q_rows = 0, q_steps = 0, q_wsteps = 0;  // this quarter-warp's sample-phase rows / steps, its warp's steps
   long long sp[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // profiling: apply split of CTA 0
   long long pt = 0;
   auto split = [&](int k) {
@@ -187,7 +210,6 @@ __global__ void __launch_bounds__(NT, 1) richardson_phased_kernel(PArgs a) {
     // part[(c G + b) epc + e - c epc]: a reducer's G x epc operands are one contiguous block.  With
     // several row blocks the partial accumulates there between blocks (the G accumulators live
     // only in the G phase, so the sample phase has the registers for deep load batches).
-    const int epc = ((NE + G - 1) / G + 1) & ~1;
     auto part_at = [&](int tile, int h) {
       const int m0 = (tile / GT_N) * 16, n0 = (tile % GT_N) * 8;
       const int e = (m0 + g + 8 * h) * DR + n0 + 2 * t4;
@@ -216,9 +238,47 @@ __global__ void __launch_bounds__(NT, 1) richardson_phased_kernel(PArgs a) {
           rtab[2 * r] = (int)(ks_max64(__ldg(&a.seg[u]), t_lo) - t_lo);
           rtab[2 * r + 1] = (int)(ks_min64(__ldg(&a.seg[u + 1]), t_hi) - t_lo);
         }
-        mbar_wait(lbar, lphase);
-        lphase ^= 1;
+        if (tid < 32) qhist[tid] = 0;
         __syncthreads();
+        // the block's rows are dealt to the NQ quarter-warps of the sample phase by cost (steps of
+        // SB samples), in snake order over the rows sorted by decreasing cost: every quarter gets
+        // about the same number of steps.  Rows are independent (z_u depends only on row u's
+        // samples, in sample order), so the assignment does not change any result.
+        for (int r = tid; r < nbr; r += NT) atomicAdd(&qhist[min(15, (rtab[2 * r + 1] - rtab[2 * r] + SB - 1) / SB)], 1);
+        __syncthreads();
+        if (tid == 0) {  // exclusive prefix over decreasing cost
+          int acc = 0;
+          for (int c = 15; c >= 0; c--) {
+            const int h = qhist[c];
+            qhist[c] = acc;
+            acc += h;
+          }
+        }
+        __syncthreads();
+        for (int r = tid; r < nbr; r += NT) {
+          const int c = min(15, (rtab[2 * r + 1] - rtab[2 * r] + SB - 1) / SB);
+          const int rank = qhist[c] + atomicAdd(&qhist[16 + c], 1);
+          const int round = rank / NQ, pos = rank - round * NQ;
+          qrows[(round & 1 ? NQ - 1 - pos : pos) * S::QR + round] = (short)r;
+        }
+        {  // this quarter's row count and steps; the warp's step count (its quarters run in lockstep)
+          const int qid = warp * 4 + (lane >> 3);
+          q_rows = 0;
+          q_steps = 0;
+          for (int round = 0; round * NQ < nbr; round++) {
+            const int rank = round * NQ + (round & 1 ? NQ - 1 - qid : qid);
+            if (rank < nbr) q_rows++;
+          }
+          mbar_wait(lbar, lphase);
+          lphase ^= 1;
+          __syncthreads();  // row lists complete
+          for (int k = 0; k < q_rows; k++) {
+            const int r = qrows[qid * S::QR + k];
+            q_steps += (rtab[2 * r + 1] - rtab[2 * r] + SB - 1) / SB;
+          }
+          q_wsteps = max(q_steps, __shfl_xor_sync(0xffffffffu, q_steps, 8));
+          q_wsteps = max(q_wsteps, __shfl_xor_sync(0xffffffffu, q_wsteps, 16));
+        }
       }
       split(0);
       // ---- Y phase: Y = L X' over the block's rows: m16n8 tile (row tile, strip); the row tiles
@@ -251,11 +311,14 @@ __global__ void __launch_bounds__(NT, 1) richardson_phased_kernel(PArgs a) {
           }
         }
       }
+      // the resident right rows: this CTA's share, min(rcap, samples), is copied in the first pass
+      const int rres = rcap > 0 ? min(rcap, rtab[2 * (nbr - 1) + 1] - rtab[0]) : 0;
+      if (rres > 0 && it == it_first && tid == 0) mbar_arrive_expect_tx(rbar, (uint32_t)(rres * DRP * 8));
       __syncthreads();
       split(1);
-      // ---- sample phase: the block's rows are split into NQ contiguous groups of about equal
-      // sample counts (binary search over the rows' sample offsets), one group per quarter-warp;
-      // z_u is written over y_u, rows past the block (up to the row-tile boundary) are zeroed
+      // ---- sample phase: each quarter-warp runs through its list of rows (dealt by cost when the
+      // block was loaded); z_u is written over y_u, rows past the block (up to the row-tile
+      // boundary) are zeroed
       {
         const int ql = lane & 7, qid = warp * 4 + (lane >> 3);
         for (int rr = nbr + qid; rr < ntile * CH_ROWS; rr += NQ) {
@@ -263,31 +326,21 @@ __global__ void __launch_bounds__(NT, 1) richardson_phased_kernel(PArgs a) {
 #pragma unroll
           for (int m = 0; m < QE2; m++) *reinterpret_cast<double2*>(&YZr[2 * ql + 16 * m]) = make_double2(0.0, 0.0);
         }
-        const int s_first = rtab[0], s_total = rtab[2 * (nbr - 1) + 1] - s_first;
-        // first row whose samples start at or after the quarter's share boundary
-        auto group_start = [&](int q) {
-          const int target = s_first + (int)(((int64_t)s_total * q) / NQ);
-          int lo = 0, hi = nbr;
-          while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (rtab[2 * mid] < target) lo = mid + 1; else hi = mid;
-          }
-          return lo;
-        };
-        const int rbeg = nbr > 0 ? group_start(qid) : 0, rend = nbr > 0 ? (qid + 1 < NQ ? group_start(qid + 1) : nbr) : 0;
+        // this CTA's first rres samples are resident in shared memory (copied in the first pass)
+        const int s_first = rtab[0];
         const double* Rbase = a.Rpack + t_lo * DRP;
-        // the four quarter-warps of a warp run in lockstep (a warp-uniform step count, per-quarter
-        // predication), so their loads are in flight together instead of diverged quarters
-        // executing one after another
-        int nsteps = 0;
-        for (int rr = rbeg; rr < rend; rr++) nsteps += (rtab[2 * rr + 1] - rtab[2 * rr] + SB - 1) / SB;
-        int wsteps = max(nsteps, __shfl_xor_sync(0xffffffffu, nsteps, 8));
-        wsteps = max(wsteps, __shfl_xor_sync(0xffffffffu, wsteps, 16));
-        int cr = rbeg, t = 0, te = 0;
+        if (rres > 0 && it == it_first) {
+          if (tid == 0) bulk_copy(Rres, Rbase + s_first * DRP, (uint32_t)(rres * DRP * 8), rbar);
+          mbar_wait(rbar, 0);
+        }
+        const short* myrows = qrows + qid * S::QR;
+        const int nsteps = q_steps, wsteps = q_wsteps;
+        int k = 0, cr = 0, t = 0, te = 0;
         double2 y[QE2], z[QE2];
 #pragma unroll
         for (int m = 0; m < QE2; m++) z[m] = y[m] = make_double2(0.0, 0.0);
         auto start_row = [&]() {
+          cr = myrows[k];
           t = rtab[2 * cr];
           te = rtab[2 * cr + 1];
           const double* YZr = YZ + cr * DRP;
@@ -297,7 +350,7 @@ __global__ void __launch_bounds__(NT, 1) richardson_phased_kernel(PArgs a) {
             z[m] = make_double2(0.0, 0.0);
           }
         };
-        if (cr < rend) start_row();
+        if (k < q_rows) start_row();
         for (int step = 0; step < wsteps; step++) {
           const int n = step < nsteps ? min(SB, te - t) : 0;
           // SB samples per step: their loads in flight together (the right rows come from L2),
@@ -308,10 +361,10 @@ __global__ void __launch_bounds__(NT, 1) richardson_phased_kernel(PArgs a) {
 #pragma unroll
           for (int i = 0; i < SB; i++) {
             const int ti = max(0, min(t + i, te - 1));
-            const double* Rt = Rbase + ti * DRP;
+            const double* Rt = ti - s_first < rres ? Rres + (ti - s_first) * DRP : Rbase + ti * DRP;
 #pragma unroll
-            for (int m = 0; m < QE2; m++) rv[i][m] = __ldg(reinterpret_cast<const double2*>(&Rt[2 * ql + 16 * m]));
-            pv[i] = __ldg(reinterpret_cast<const double2*>(&Rt[DR]));  // v_t, v_t b_t (row padding)
+            for (int m = 0; m < QE2; m++) rv[i][m] = *reinterpret_cast<const double2*>(&Rt[2 * ql + 16 * m]);
+            pv[i] = *reinterpret_cast<const double2*>(&Rt[DR]);  // v_t, v_t b_t (row padding)
             if (i >= n) pv[i].x = 0.0;
           }
           double sv[SB];
@@ -350,7 +403,7 @@ __global__ void __launch_bounds__(NT, 1) richardson_phased_kernel(PArgs a) {
             double* YZr = YZ + cr * DRP;
 #pragma unroll
             for (int m = 0; m < QE2; m++) *reinterpret_cast<double2*>(&YZr[2 * ql + 16 * m]) = z[m];
-            if (++cr < rend) start_row();
+            if (++k < q_rows) start_row();
           }
         }
       }
