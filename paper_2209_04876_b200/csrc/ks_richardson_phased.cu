@@ -43,8 +43,10 @@ constexpr int SMEM_MAX = 232448;
 template <int DL, int DR>
 struct PhSmem {
   static constexpr int DLP = DL + PAD, DRP = DR + PAD, NE = DL * DR;
-  static constexpr int QR = 8;                                 // rows per quarter-warp list (<= 16 x 16 rows / 48 + 1)
-  static constexpr int QLIST = (NQ * QR * 2 + 2 * 16 * 4 + 7) / 8;  // int16 row lists + cost histogram / cursors
+  static constexpr int QR = 8;                                 // entries per quarter-warp list (<= 16 x 16 rows / 48 + 2)
+  // int16 row lists, cost histogram / cursors (32 ints), the block's resident-row offsets
+  // (16 x 16 ints) and three scalars
+  static constexpr int QLIST = (NQ * QR * 2 + 32 * 4 + 16 * CH_ROWS * 4 + 4 * 4 + 7) / 8;
   static constexpr int FIXED = 256 + 1024 + 16 * CH_ROWS + QLIST;  // W scratch, history, row table, row lists
   static constexpr int PER_NB = CH_ROWS * DLP + CH_ROWS * DRP;  // L rows + Y/Z rows per chunk
   static constexpr int NB_FIT = (SMEM_MAX / 8 - 64 - FIXED - CH_ROWS * DLP) / PER_NB;
@@ -59,7 +61,8 @@ struct PhSmem {
   static constexpr int DOUBLES = Q_OFF + QLIST;
   static constexpr size_t BYTES = (size_t)DOUBLES * 8 + 3 * 8;  // + mbarriers (L load, reduce operands, resident R)
   static_assert(NB >= 4, "at least four chunks per block");
-  static_assert(NB * CH_ROWS <= NQ * (QR - 1), "quarter row lists hold a block's rows");
+  static_assert(NB * CH_ROWS <= NQ * (QR - 2), "quarter row lists hold a block's rows");
+  static_assert(NB * CH_ROWS <= 256 && 2 * NB * CH_ROWS + 1 <= NB * CH_ROWS * DRP, "row ids fit 8 bits; setup scratch fits Y/Z");
   static_assert(BYTES <= SMEM_MAX, "shared memory per CTA");
   static_assert(L_ROWS * DLP + NB * CH_ROWS * DRP >= DL * DRP + DR * DRP + DL * DRP,
                 "back-transform staging lives in the L and Y/Z buffers");
@@ -114,13 +117,18 @@ __global__ void __launch_bounds__(NT, 1) richardson_phased_kernel(PArgs a) {
   constexpr int XK = DL / 4;           // k-steps of Y = L X' (X' fragments per strip)
   constexpr int QE2 = DR / 16;         // double2 per lane of a quarter-warp row
   constexpr int SB = 2;                // samples per step of the sample phase
+  constexpr int PAIR_C = 3;            // rows of >= PAIR_C steps are split over two quarter-warps
   extern __shared__ __align__(128) double sm[];
   uint64_t* lbar = reinterpret_cast<uint64_t*>(sm + S::DOUBLES);
   uint64_t* auxbar = lbar + 1;
   uint64_t* rbar = lbar + 2;
   int* rtab = reinterpret_cast<int*>(sm + S::C_OFF);  // per row of the block: sample range [tb, te)
-  short* qrows = reinterpret_cast<short*>(sm + S::Q_OFF);  // per quarter-warp: its rows of the block
+  // sample-phase work lists: per quarter-warp, its entries (row | PAIRED | PIECE_B); per row, the
+  // slot of its right rows in the resident region (or -1)
+  unsigned short* qrows = reinterpret_cast<unsigned short*>(sm + S::Q_OFF);
   int* qhist = reinterpret_cast<int*>(qrows + NQ * S::QR);  // 16 cost buckets, then 16 cursors
+  int* roff = qhist + 32;
+  int* qscal = roff + 16 * CH_ROWS;  // [0]: paired rows, [1]: resident samples of the block
   double* Ls = sm + S::L_OFF;
   double* Ws = sm + S::W_OFF;
   double* Hs = sm + S::H_OFF;
@@ -240,44 +248,103 @@ __global__ void __launch_bounds__(NT, 1) richardson_phased_kernel(PArgs a) {
         }
         if (tid < 32) qhist[tid] = 0;
         __syncthreads();
-        // the block's rows are dealt to the NQ quarter-warps of the sample phase by cost (steps of
-        // SB samples), in snake order over the rows sorted by decreasing cost: every quarter gets
-        // about the same number of steps.  Rows are independent (z_u depends only on row u's
-        // samples, in sample order), so the assignment does not change any result.
+        // Sample-phase work lists.  The block's rows are ranked by cost (steps of SB samples,
+        // decreasing).  The heaviest rows (>= PAIR_C steps, at most NQ / 2 of them) are each split
+        // in two halves run side by side by a pair of quarter-warps of one warp, their partial z
+        // summed with one shuffle; the other rows are dealt to the quarter-warps in snake order
+        // (the largest ones to the quarters without a pair).  Every quarter then has about the
+        // same number of steps.  Rows are independent and a row's samples are always summed in the
+        // same order, so the assignment (ties broken by atomics) does not change any result.
+        // In resident mode the right rows of the heaviest rows -- the critical path -- are copied
+        // to shared memory, in rank order while they fit.
+        int* sc_rank = reinterpret_cast<int*>(YZ);  // setup scratch: row of each rank, count prefix
+        int* sc_pre = sc_rank + ROWCAP;
         for (int r = tid; r < nbr; r += NT) atomicAdd(&qhist[min(15, (rtab[2 * r + 1] - rtab[2 * r] + SB - 1) / SB)], 1);
         __syncthreads();
-        if (tid == 0) {  // exclusive prefix over decreasing cost
+        if (tid == 0) {  // exclusive prefix over decreasing cost: qhist[c] = rows costing more than c
           int acc = 0;
           for (int c = 15; c >= 0; c--) {
             const int h = qhist[c];
             qhist[c] = acc;
             acc += h;
           }
+          qscal[0] = min(qhist[PAIR_C - 1], NQ / 2);
         }
         __syncthreads();
         for (int r = tid; r < nbr; r += NT) {
           const int c = min(15, (rtab[2 * r + 1] - rtab[2 * r] + SB - 1) / SB);
-          const int rank = qhist[c] + atomicAdd(&qhist[16 + c], 1);
-          const int round = rank / NQ, pos = rank - round * NQ;
-          qrows[(round & 1 ? NQ - 1 - pos : pos) * S::QR + round] = (short)r;
+          sc_rank[qhist[c] + atomicAdd(&qhist[16 + c], 1)] = r;
         }
-        {  // this quarter's row count and steps; the warp's step count (its quarters run in lockstep)
+        __syncthreads();
+        const int npair = qscal[0];
+        if (warp == 0) {  // sample counts of the ranks, exclusive prefix (nbr <= 256: 8 per lane)
+          int loc[8], sum = 0;
+#pragma unroll
+          for (int j = 0; j < 8; j++) {
+            const int k = lane * 8 + j;
+            loc[j] = k < nbr ? rtab[2 * sc_rank[k] + 1] - rtab[2 * sc_rank[k]] : 0;
+            sum += loc[j];
+          }
+          int inc = sum;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += v;
+          }
+          int run = inc - sum;
+#pragma unroll
+          for (int j = 0; j < 8; j++) {
+            if (lane * 8 + j <= nbr) sc_pre[lane * 8 + j] = run;
+            run += loc[j];
+          }
+          if (lane == 31 && nbr == 256) sc_pre[256] = run;
+        }
+        __syncthreads();
+        const int cap = (resident && it == it_first) ? rcap : 0;
+        for (int k = tid; k < nbr; k += NT) {
+          const int r = sc_rank[k];
+          const bool res = sc_pre[k + 1] <= cap;
+          roff[r] = res ? sc_pre[k] : -1;
+          if (res && (k + 1 == nbr || sc_pre[k + 2] > cap)) qscal[1] = sc_pre[k + 1];
+          if (k < npair) {
+            qrows[(2 * k) * S::QR] = (unsigned short)(r | 0x100);
+            qrows[(2 * k + 1) * S::QR] = (unsigned short)(r | 0x300);
+          } else {
+            const int kk = k - npair, round = kk / NQ, pos = kk - round * NQ;
+            const int q = (round & 1) ? pos : NQ - 1 - pos;
+            qrows[q * S::QR + round + (q < 2 * npair ? 1 : 0)] = (unsigned short)r;
+          }
+        }
+        if (tid == 0 && (cap == 0 || sc_pre[1] > cap)) qscal[1] = 0;
+        __syncthreads();
+        const int nres = qscal[1];
+        if (nres > 0) {  // resident mode, first pass: the heaviest rows' right rows
+          if (tid == 0) mbar_arrive_expect_tx(rbar, (uint32_t)(nres * DRP * 8));
+          __syncthreads();
+          for (int r = tid; r < nbr; r += NT)
+            if (roff[r] >= 0)
+              bulk_copy(Rres + roff[r] * DRP, a.Rpack + (t_lo + rtab[2 * r]) * DRP,
+                        (uint32_t)((rtab[2 * r + 1] - rtab[2 * r]) * DRP * 8), rbar);
+        }
+        {  // this quarter's entries and steps; the warp's step count (its quarters run in lockstep)
           const int qid = warp * 4 + (lane >> 3);
-          q_rows = 0;
+          q_rows = qid < 2 * npair ? 1 : 0;
           q_steps = 0;
-          for (int round = 0; round * NQ < nbr; round++) {
-            const int rank = round * NQ + (round & 1 ? NQ - 1 - qid : qid);
-            if (rank < nbr) q_rows++;
+          for (int round = 0; round * NQ < nbr - npair; round++) {
+            const int kk = round * NQ + ((round & 1) ? qid : NQ - 1 - qid);
+            if (kk < nbr - npair) q_rows++;
           }
           mbar_wait(lbar, lphase);
           lphase ^= 1;
-          __syncthreads();  // row lists complete
           for (int k = 0; k < q_rows; k++) {
-            const int r = qrows[qid * S::QR + k];
-            q_steps += (rtab[2 * r + 1] - rtab[2 * r] + SB - 1) / SB;
+            const int e = qrows[qid * S::QR + k], r = e & 0xff;
+            const int cnt = rtab[2 * r + 1] - rtab[2 * r];
+            q_steps += max(1, ((e & 0x100) ? (cnt + 1) / 2 + SB - 1 : cnt + SB - 1) / SB);
           }
           q_wsteps = max(q_steps, __shfl_xor_sync(0xffffffffu, q_steps, 8));
           q_wsteps = max(q_wsteps, __shfl_xor_sync(0xffffffffu, q_wsteps, 16));
+          if (nres > 0) mbar_wait(rbar, 0);
+          __syncthreads();  // the Y/Z scratch is free again
         }
       }
       split(0);
@@ -311,9 +378,6 @@ __global__ void __launch_bounds__(NT, 1) richardson_phased_kernel(PArgs a) {
           }
         }
       }
-      // the resident right rows: this CTA's share, min(rcap, samples), is copied in the first pass
-      const int rres = rcap > 0 ? min(rcap, rtab[2 * (nbr - 1) + 1] - rtab[0]) : 0;
-      if (rres > 0 && it == it_first && tid == 0) mbar_arrive_expect_tx(rbar, (uint32_t)(rres * DRP * 8));
       __syncthreads();
       split(1);
       // ---- sample phase: each quarter-warp runs through its list of rows (dealt by cost when the
@@ -326,23 +390,23 @@ __global__ void __launch_bounds__(NT, 1) richardson_phased_kernel(PArgs a) {
 #pragma unroll
           for (int m = 0; m < QE2; m++) *reinterpret_cast<double2*>(&YZr[2 * ql + 16 * m]) = make_double2(0.0, 0.0);
         }
-        // this CTA's first rres samples are resident in shared memory (copied in the first pass)
-        const int s_first = rtab[0];
         const double* Rbase = a.Rpack + t_lo * DRP;
-        if (rres > 0 && it == it_first) {
-          if (tid == 0) bulk_copy(Rres, Rbase + s_first * DRP, (uint32_t)(rres * DRP * 8), rbar);
-          mbar_wait(rbar, 0);
-        }
-        const short* myrows = qrows + qid * S::QR;
+        const unsigned short* myrows = qrows + qid * S::QR;
         const int nsteps = q_steps, wsteps = q_wsteps;
-        int k = 0, cr = 0, t = 0, te = 0;
+        const unsigned pmask = 0xffffu << (lane & 16);  // the 16 lanes of this quarter's pair
+        int k = 0, cr = 0, t = 0, te = 0, srem = 0, ro = -1, rtb = 0, ent = 0;
         double2 y[QE2], z[QE2];
 #pragma unroll
         for (int m = 0; m < QE2; m++) z[m] = y[m] = make_double2(0.0, 0.0);
-        auto start_row = [&]() {
-          cr = myrows[k];
-          t = rtab[2 * cr];
-          te = rtab[2 * cr + 1];
+        auto start_row = [&]() {  // entry k: a row, or one half of a paired row
+          ent = myrows[k];
+          cr = ent & 0xff;
+          rtb = rtab[2 * cr];
+          const int tend = rtab[2 * cr + 1], half = (tend - rtb + 1) / 2;
+          t = (ent & 0x200) ? rtb + half : rtb;
+          te = (ent & 0x100) ? ((ent & 0x200) ? tend : rtb + half) : tend;
+          srem = max(1, (((ent & 0x100) ? half : tend - rtb) + SB - 1) / SB);
+          ro = roff[cr];
           const double* YZr = YZ + cr * DRP;
 #pragma unroll
           for (int m = 0; m < QE2; m++) {
@@ -352,7 +416,7 @@ __global__ void __launch_bounds__(NT, 1) richardson_phased_kernel(PArgs a) {
         };
         if (k < q_rows) start_row();
         for (int step = 0; step < wsteps; step++) {
-          const int n = step < nsteps ? min(SB, te - t) : 0;
+          const int n = step < nsteps ? max(0, min(SB, te - t)) : 0;
           // SB samples per step: their loads in flight together (the right rows come from L2),
           // dot products and shuffle reductions interleaved; z accumulates in sample order.
           // Every load is of a valid row (samples past the step's count re-read the last one and
@@ -361,7 +425,7 @@ __global__ void __launch_bounds__(NT, 1) richardson_phased_kernel(PArgs a) {
 #pragma unroll
           for (int i = 0; i < SB; i++) {
             const int ti = max(0, min(t + i, te - 1));
-            const double* Rt = ti - s_first < rres ? Rres + (ti - s_first) * DRP : Rbase + ti * DRP;
+            const double* Rt = ro >= 0 ? Rres + (ro + ti - rtb) * DRP : Rbase + ti * DRP;
 #pragma unroll
             for (int m = 0; m < QE2; m++) rv[i][m] = *reinterpret_cast<const double2*>(&Rt[2 * ql + 16 * m]);
             pv[i] = *reinterpret_cast<const double2*>(&Rt[DR]);  // v_t, v_t b_t (row padding)
@@ -399,10 +463,19 @@ __global__ void __launch_bounds__(NT, 1) richardson_phased_kernel(PArgs a) {
             }
           }
           t += SB;
-          if (step < nsteps && t >= te) {  // the row is done: z_u over y_u (each lane its own elements)
-            double* YZr = YZ + cr * DRP;
+          if (step < nsteps && --srem == 0) {  // the entry is done: z_u over y_u (each lane its own elements)
+            if (ent & 0x100) {  // both halves of a paired row end on this step: z_u = z_first + z_second
 #pragma unroll
-            for (int m = 0; m < QE2; m++) *reinterpret_cast<double2*>(&YZr[2 * ql + 16 * m]) = z[m];
+              for (int m = 0; m < QE2; m++) {
+                z[m].x += __shfl_xor_sync(pmask, z[m].x, 8);
+                z[m].y += __shfl_xor_sync(pmask, z[m].y, 8);
+              }
+            }
+            if (!(ent & 0x200)) {
+              double* YZr = YZ + cr * DRP;
+#pragma unroll
+              for (int m = 0; m < QE2; m++) *reinterpret_cast<double2*>(&YZr[2 * ql + 16 * m]) = z[m];
+            }
             if (++k < q_rows) start_row();
           }
         }
