@@ -104,6 +104,30 @@ __device__ __forceinline__ void grid_barrier(unsigned* ctr, int G, unsigned epoc
   __syncthreads();
 }
 
+// N row tiles of Y = L X' (m16n8 tiles of one n8 strip, tiles t0, t0 + WPS, ...): N independent
+// m16n8k4 chains over the k-steps, X' fragments in registers, results to the Y/Z rows
+template <int N, int XK, int DLP, int DRP, int WPS>
+__device__ __forceinline__ void y_pass(const double* Ls, double* YZ, int t0, const double (&xf)[XK], int g, int t4,
+                                       int n0) {
+  double acc[N][4];
+#pragma unroll
+  for (int i = 0; i < N; i++) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.0;
+#pragma unroll
+  for (int k = 0; k < XK; k++) {
+#pragma unroll
+    for (int i = 0; i < N; i++) {
+      const double* L = Ls + (t0 + i * WPS) * CH_ROWS * DLP;
+      dmma_16x8x4(acc[i], L[g * DLP + 4 * k + t4], L[(g + 8) * DLP + 4 * k + t4], xf[k]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < N; i++) {
+    double* Y = YZ + (t0 + i * WPS) * CH_ROWS * DRP;
+    *reinterpret_cast<double2*>(&Y[g * DRP + n0]) = make_double2(acc[i][0], acc[i][1]);
+    *reinterpret_cast<double2*>(&Y[(g + 8) * DRP + n0]) = make_double2(acc[i][2], acc[i][3]);
+  }
+}
+
 template <int DL, int DR, bool PROF>
 __global__ void __launch_bounds__(NT, 1) richardson_phased_kernel(PArgs a) {
   using S = PhSmem<DL, DR>;
@@ -113,7 +137,7 @@ __global__ void __launch_bounds__(NT, 1) richardson_phased_kernel(PArgs a) {
   constexpr int Y_STRIPS = DR / 8;     // n8 strips of a 16-row Y tile
   static_assert(MW % Y_STRIPS == 0, "strips divide the DMMA warps");
   constexpr int WPS = MW / Y_STRIPS;   // DMMA warps per strip (they split the row tiles)
-  constexpr int YB = 8;                // Y row tiles in flight per warp
+  constexpr int YB = 2;                // Y row tiles in flight per warp
   constexpr int XK = DL / 4;           // k-steps of Y = L X' (X' fragments per strip)
   constexpr int QE2 = DR / 16;         // double2 per lane of a quarter-warp row
   constexpr int SB = 2;                // samples per step of the sample phase
@@ -351,32 +375,19 @@ __global__ void __launch_bounds__(NT, 1) richardson_phased_kernel(PArgs a) {
       // ---- Y phase: Y = L X' over the block's rows: m16n8 tile (row tile, strip); the row tiles
       // of a strip are split over its warps, YB of them in flight per warp
       if (!rp && is_mma) {
-        for (int t0 = ywarp; t0 < ntile; t0 += WPS * YB) {
-          double acc[YB][4];
-#pragma unroll
-          for (int i = 0; i < YB; i++) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.0;
-#pragma unroll
-          for (int k = 0; k < XK; k++) {
-#pragma unroll
-            for (int i = 0; i < YB; i++) {
-              const int rt = t0 + i * WPS;
-              if (rt < ntile) {
-                const double* L = Ls + rt * CH_ROWS * DLP;
-                dmma_16x8x4(acc[i], L[g * DLP + 4 * k + t4], L[(g + 8) * DLP + 4 * k + t4], xf[k]);
-              }
-            }
-          }
-#pragma unroll
-          for (int i = 0; i < YB; i++) {
-            const int rt = t0 + i * WPS;
-            if (rt < ntile) {
-              double* Y = YZ + rt * CH_ROWS * DRP;
-              const int n0 = 8 * ystrip + 2 * t4;
-              *reinterpret_cast<double2*>(&Y[g * DRP + n0]) = make_double2(acc[i][0], acc[i][1]);
-              *reinterpret_cast<double2*>(&Y[(g + 8) * DRP + n0]) = make_double2(acc[i][2], acc[i][3]);
-            }
-          }
-        }
+        // passes of YB row tiles, then one pass over the remaining ones: every DMMA issued is a
+        // real one (no predicated-off tiles)
+        int t0 = ywarp;
+        for (; t0 + (YB - 1) * WPS < ntile; t0 += WPS * YB)
+          y_pass<YB, XK, DLP, DRP, WPS>(Ls, YZ, t0, xf, g, t4, 8 * ystrip + 2 * t4);
+        const int rem = t0 < ntile ? (ntile - t0 + WPS - 1) / WPS : 0;
+        if constexpr (YB > 1) if (rem == 1) y_pass<1, XK, DLP, DRP, WPS>(Ls, YZ, t0, xf, g, t4, 8 * ystrip + 2 * t4);
+        if constexpr (YB > 2) if (rem == 2) y_pass<2, XK, DLP, DRP, WPS>(Ls, YZ, t0, xf, g, t4, 8 * ystrip + 2 * t4);
+        if constexpr (YB > 3) if (rem == 3) y_pass<3, XK, DLP, DRP, WPS>(Ls, YZ, t0, xf, g, t4, 8 * ystrip + 2 * t4);
+        if constexpr (YB > 4) if (rem == 4) y_pass<4, XK, DLP, DRP, WPS>(Ls, YZ, t0, xf, g, t4, 8 * ystrip + 2 * t4);
+        if constexpr (YB > 5) if (rem == 5) y_pass<5, XK, DLP, DRP, WPS>(Ls, YZ, t0, xf, g, t4, 8 * ystrip + 2 * t4);
+        if constexpr (YB > 6) if (rem == 6) y_pass<6, XK, DLP, DRP, WPS>(Ls, YZ, t0, xf, g, t4, 8 * ystrip + 2 * t4);
+        if constexpr (YB > 7) if (rem == 7) y_pass<7, XK, DLP, DRP, WPS>(Ls, YZ, t0, xf, g, t4, 8 * ystrip + 2 * t4);
       }
       __syncthreads();
       split(1);
@@ -495,22 +506,30 @@ __global__ void __launch_bounds__(NT, 1) richardson_phased_kernel(PArgs a) {
           }
         }
         const int nk = (nbr + 3) / 4;
-        for (int kk = 0; kk < nk; kk++) {
-          const double* Lr = Ls + (4 * kk + t4) * DLP;
-          const double* Zr = YZ + (4 * kk + t4) * DRP;
-          int mprev = -1;
-          double a0 = 0.0, a1 = 0.0;
+        // a warp's tiles share their rows of L^T when they lie in one m16 band (e.g. d_L = d_R = 64:
+        // 32 tiles, 4 per warp, 8 per band): then one pair of A fragments per k-step
+        constexpr bool BAND = G_TILES % MW == 0 && GT_N % G_PER_W == 0;
+        if constexpr (BAND) {
+          const int m0 = (warp * G_PER_W / GT_N) * 16, n0 = (warp * G_PER_W % GT_N) * 8;
+#pragma unroll 2
+          for (int kk = 0; kk < nk; kk++) {
+            const double* Lr = Ls + (4 * kk + t4) * DLP;
+            const double* Zr = YZ + (4 * kk + t4) * DRP + n0 + g;
+            const double a0 = Lr[m0 + g], a1 = Lr[m0 + g + 8];
 #pragma unroll
-          for (int i = 0; i < G_PER_W; i++) {
-            const int tile = warp * G_PER_W + i;
-            if (tile < G_TILES) {
-              const int m0 = (tile / GT_N) * 16, n0 = (tile % GT_N) * 8;
-              if (m0 != mprev) {  // consecutive tiles of a warp share their rows of L^T
-                a0 = Lr[m0 + g];
-                a1 = Lr[m0 + g + 8];
-                mprev = m0;
+            for (int i = 0; i < G_PER_W; i++) dmma_16x8x4(gacc[i], a0, a1, Zr[8 * i]);
+          }
+        } else {
+          for (int kk = 0; kk < nk; kk++) {
+            const double* Lr = Ls + (4 * kk + t4) * DLP;
+            const double* Zr = YZ + (4 * kk + t4) * DRP;
+#pragma unroll
+            for (int i = 0; i < G_PER_W; i++) {
+              const int tile = warp * G_PER_W + i;
+              if (tile < G_TILES) {
+                const int m0 = (tile / GT_N) * 16, n0 = (tile % GT_N) * 8;
+                dmma_16x8x4(gacc[i], Lr[m0 + g], Lr[m0 + g + 8], Zr[n0 + g]);
               }
-              dmma_16x8x4(gacc[i], a0, a1, Zr[n0 + g]);
             }
           }
         }
