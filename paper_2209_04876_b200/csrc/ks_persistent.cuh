@@ -9,6 +9,7 @@
 namespace ks_rich {
 
 constexpr int CH_ROWS = 16;  // distinct left rows per chunk 
+constexpr int PLAN_ROWS = 8;  // left rows per group of the device work plan (a chunk holds <= CH_ROWS)
 constexpr int CH_S = 64;     // samples per chunk (>= DL: the free slab holds a DL x DRP matrix)
 constexpr int PAD = 4;       // row padding (doubles) of packed / staged rows
 constexpr int BARRIER_WORDS = 32;  // grid-barrier counter (own 128-byte line) of the phase-separated loop

@@ -809,7 +809,7 @@ __global__ void transpose_sq_kernel2(const double* __restrict__ a, int d, double
   out[j * d + i] = a[e];
 }
 
-// Work plan on the device (no host round trip): left rows are cut into groups of CH_ROWS, a
+// Work plan on the device (no host round trip): left rows are cut into groups of PLAN_ROWS, a
 // group's samples into pieces of <= CH_S (one chunk each); chunks go to CTAs in contiguous
 // ranges of nearly equal estimated cost (chunk c goes to the first CTA b whose cost target
 // total * (b+1) / G exceeds the chunk's cost midpoint).  Costs are integers, so the plan is
@@ -864,7 +864,7 @@ __global__ void __launch_bounds__(PLAN_T) plan_kernel(const int64_t* __restrict_
   extern __shared__ int64_t plan_sm[];  // segment offsets, when they fit (latency of the searches)
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t ul = ul_dev ? *ul_dev : ul_host;
-  const int64_t ngroups = (ul + CH_ROWS - 1) / CH_ROWS;
+  const int64_t ngroups = (ul + PLAN_ROWS - 1) / PLAN_ROWS;
   if (tid == 0) carry_p = carry_c = 0;
   if (ul + 1 <= PLAN_SM_SEG) {
     for (int64_t i = tid; i <= ul; i += PLAN_T) ks_cp_async8(&plan_sm[i], seg + i);
@@ -876,8 +876,8 @@ __global__ void __launch_bounds__(PLAN_T) plan_kernel(const int64_t* __restrict_
     const int64_t gidx = g0 + tid;
     int64_t pieces = 0, cost = 0, sb = 0, se = 0, ub = 0, ue = 0;
     if (gidx < ngroups) {
-      ub = gidx * CH_ROWS;
-      ue = min(ul, ub + CH_ROWS);
+      ub = gidx * PLAN_ROWS;
+      ue = min(ul, ub + PLAN_ROWS);
       sb = seg[ub];
       se = seg[ue];
       pieces = max((int64_t)1, (se - sb + CH_S - 1) / CH_S);
@@ -962,7 +962,7 @@ int launch(cudaStream_t st, PArgs& a, int grid) {
 
 namespace ks {
 
-int64_t plan_cap(int64_t ul, int64_t nnz) { return (ul + CH_ROWS - 1) / CH_ROWS + nnz / CH_S + 2; }
+int64_t plan_cap(int64_t ul, int64_t nnz) { return (ul + PLAN_ROWS - 1) / PLAN_ROWS + nnz / CH_S + 2; }
 size_t plan_range_offset(int64_t cap) { return (size_t)cap * (sizeof(Chunk) + sizeof(int64_t)); }
 
 static bool use_phased() { return !env(ENV_RICH_OLD); }
@@ -970,20 +970,21 @@ static int g_prof_on = 0;  // ks_debug_richardson_profile: the profiling instant
 
 static int launch_plan(cudaStream_t st, const ks_sketch_view* sk, int64_t ul, const int64_t* counts_dev, int dL,
                        int dR, int grid, Chunk* chunks, int64_t* cpre, int64_t* range) {
+  // m16n8k4 DMMAs of a 16-row chunk in the Y and G GEMMs; a plan group holds PLAN_ROWS rows
   const int64_t dmma = (int64_t)(CH_ROWS / 16) * (dR / 8) * (dL / 4) + (int64_t)(dL / 16) * (dR / 8) * (CH_ROWS / 4);
   int64_t wchunk, wsamp, wlong;
   if (use_phased() && richardson_phased_supported(dL, dR, grid)) {
-    // phase-separated loop: a chunk costs its DMMA issue time in the Y and G phases (8 SM cycles
+    // phase-separated loop: a group costs its DMMA issue time in the Y and G phases (8 SM cycles
     // per m16n8k4 at the FP64 tensor rate); the sample phase spreads a CTA's rows over 48
     // quarter-warps, ~10 cycles per sample of the CTA
-    wchunk = 8 * dmma;
+    wchunk = 8 * dmma * PLAN_ROWS / CH_ROWS;
     wsamp = 10;
     wlong = 0;
   } else {
-    // single-role kernel: estimated chunk cost (SM cycles), fitted to measured per-CTA apply
-    // times at c3 (tools/fit_plan_costs.py: rms error 0.23 us): ~13.3 cycles per DMMA tile-step
-    // of the Y and G GEMMs (fixed per chunk), ~139 cycles per sample of the chunk's longest row
-    // (the rows' sample loops run in parallel), ~4 cycles per sample of shared-memory traffic
+    // single-role kernel: estimated chunk cost (SM cycles), fitted in round 1 to measured per-CTA
+    // apply times at c3 (rms error 0.23 us): ~13.3 cycles per DMMA tile-step of the Y and G GEMMs
+    // (fixed per chunk), ~139 cycles per sample of the chunk's longest row (the rows' sample
+    // loops run in parallel), ~4 cycles per sample of shared-memory traffic
     wchunk = (int64_t)(13.3 * dmma);
     wsamp = dR / 16;
     wlong = 139;
@@ -1052,10 +1053,7 @@ int richardson_persistent(cudaStream_t st, const ks_sketch_view* sk, const doubl
   KS_REQUIRE(Lpack.p && Rpack.p && part.p && R.p && T.p && stepb.p && rowsq.p && VRt.p && chunks_p && range_p &&
                  (plan_ws || cpre.p) && statep && (!eig_mode || rhs_e.p),
              KS_ECUDA, "scratch allocation failed");
-  // estimated chunk cost (SM cycles), fitted to measured per-CTA apply times at c3
-  // (tools/fit_plan_costs.py: rms error 0.23 us): ~13.3 cycles per DMMA tile-step of the Y and G
-  // GEMMs (fixed per chunk), ~139 cycles per sample of the chunk's longest row (the rows' sample
-  // loops run in parallel), ~4 cycles per sample of shared-memory traffic
+  // the work plan (launch_plan: chunks and per-CTA ranges of nearly equal estimated cost)
   if (!plan_ws) {
     int rc0 = launch_plan(st, sk, ul, counts_dev, dL, dR, grid, dch.p, cpre.p, drange.p);
     if (rc0) return rc0;
