@@ -730,7 +730,9 @@ def stage_timings(K, facs, b, cfg, tr, n, d):
         sp = (ctypes.c_double * 8)()
         if L.load().ks_debug_richardson_apply_split(iters, sp) == 0:
             phases["apply_split"] = dict(zip(["l_load_wait", "y_phase", "sample_phase", "g_phase"],
-                                             [round(v) for v in sp]))
+                                             [round(v) for v in sp[:4]]))
+            phases["sync_split"] = dict(zip(["reduce_fetch_wait", "norm_and_rules", "step_fetch_wait"],
+                                            [round(v) for v in sp[4:7]]))
         nct = torch.cuda.get_device_properties(0).multi_processor_count
         st = (ctypes.c_uint64 * (2 * nct))()
         if iters > 5 and L.load().ks_debug_richardson_cta_apply(nct, st) == 0:

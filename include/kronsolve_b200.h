@@ -432,6 +432,12 @@ int ks_pinv_compose(const double* U, int64_t n, const double* sigma, const doubl
 int ks_kron_explicit2(const double* A, int64_t m, int32_t p, const double* B, int64_t k, int32_t q, double* C,
                       void* stream);
 
+/* The spectral-row sample of one factor (leverage.py:235-252, scaled as solvers.py:424-427):
+ * out (m x d) row t = (w[t] * A[idx[t], :]) / divisor, for row-major A (n x d); indices are not
+ * range-checked (they come from the device sampler).  Asynchronous. */
+int ks_scaled_row_gather(const double* A, int64_t n, int32_t d, const int64_t* idx, const double* w, int64_t m,
+                         double divisor, double* out, void* stream);
+
 int ks_sketch_rows(int32_t nf, const double* const* factors, const int64_t* rows, const int32_t* cols,
                    const int64_t* idx, int32_t flat, const double* w, int64_t s, double* out, void* stream);
 

@@ -103,6 +103,7 @@ _SIGS = {
     "ks_qr_explicit": ([_p, _i64, _i32, _p, _p], ctypes.c_int),
     "ks_pinv_compose": ([_p, _i64, _p, _p, _i64, _i32, _p, _p], ctypes.c_int),
     "ks_kron_explicit2": ([_p, _i64, _i32, _p, _i64, _i32, _p, _p], ctypes.c_int),
+    "ks_scaled_row_gather": ([_p, _i64, _i32, _p, _p, _i64, _d, _p, _p], ctypes.c_int),
     "ks_sketch_rows": ([_i32, _p, _p, _p, _p, _i32, _p, _i64, _p, _p], ctypes.c_int),
     "ks_chol_qr2_r": ([_p, _i64, _i32, _p, POINTER(c_int32), _p], ctypes.c_int),
     "ks_leverage_scores_tall": ([_p, _i64, _i32, _p, POINTER(c_int32), _p], ctypes.c_int),

@@ -98,3 +98,28 @@ extern "C" int ks_kron_explicit2(const double* A, int64_t m, int32_t p, const do
   return KS_OK;
 }
 
+
+// The spectral-row sample of leverage.py:235-252 as used by fast_kronecker_regression
+// (solvers.py:424-427): out[t, :] = (w[t] * A[idx[t], :]) / divisor, two roundings in the
+// reference's order (the weighted gather, then the division by sqrt(1 - eps_two)).
+namespace {
+__global__ void scaled_row_gather_kernel(const double* __restrict__ A, int64_t n, int32_t d,
+                                         const int64_t* __restrict__ idx, const double* __restrict__ w, int64_t m,
+                                         double divisor, double* __restrict__ out) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= m * d) return;
+  const int64_t t = e / d;
+  const int32_t c = (int32_t)(e - t * d);
+  const int64_t r = __ldg(&idx[t]);
+  out[e] = __ddiv_rn(__dmul_rn(__ldg(&w[t]), __ldg(&A[r * d + c])), divisor);
+}
+}  // namespace
+
+extern "C" int ks_scaled_row_gather(const double* A, int64_t n, int32_t d, const int64_t* idx, const double* w,
+                                    int64_t m, double divisor, double* out, void* stream) {
+  KS_REQUIRE(n >= 0 && m >= 0 && d >= 1 && divisor != 0.0, KS_EINVAL, "scaled_row_gather: bad arguments");
+  if (m == 0) return KS_OK;
+  scaled_row_gather_kernel<<<ceil_div_u(m * d, 256), 256, 0, (cudaStream_t)stream>>>(A, n, d, idx, w, m, divisor, out);
+  KS_CHECK_LAUNCH();
+  return KS_OK;
+}

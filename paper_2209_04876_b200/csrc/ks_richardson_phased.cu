@@ -548,6 +548,7 @@ __global__ void __launch_bounds__(NT, 1) richardson_phased_kernel(PArgs a) {
     if (PROF && it == 5 && tid == 0 && b < 256) g_ws_cta[2 * b + 1] = gtimer();
     grid_barrier(a.flags, G, ++epoch);
     if (prof && !rp) g_ws_prof[it * 6 + 2] = clock64();
+    if (prof) pt = clock64();
     // ---------------- reduce: step' = dinv o (sum_cta G + lam x' - rhs') ----------------
     {
       const int e0 = b * epc, e1 = min(NE, e0 + epc);
@@ -562,6 +563,7 @@ __global__ void __launch_bounds__(NT, 1) richardson_phased_kernel(PArgs a) {
         mbar_wait(auxbar, auxphase);
         auxphase ^= 1;
       }
+      split(4);
       double eig_sq = 0.0;
       const int eo = tid >> 3, ql = lane & 7;
       const unsigned qmask = 0xffu << (lane & 24);
@@ -615,53 +617,56 @@ __global__ void __launch_bounds__(NT, 1) richardson_phased_kernel(PArgs a) {
     if (a.apply_only) return;
     if (prof && !rp) g_ws_prof[it * 6 + 3] = clock64();
     grid_barrier(a.flags, G, ++epoch);
+    if (prof) pt = clock64();
     if (prof && !rp) g_ws_prof[it * 6 + 4] = clock64();
     // ---------------- norm, stopping rules (solvers.py:226-247), update ----------------
+    // the step' fetch (one bulk copy) overlaps the norm: warp 0 sums the CTA partials of
+    // ||step'||^2 in a fixed order (identical in every CTA) and applies the stopping rules
     if (!rp && tid == 0) {
       asm volatile("fence.proxy.async.global;" ::: "memory");
       const uint32_t bytes = (uint32_t)(DL * DRP * 8);
       mbar_arrive_expect_tx(auxbar, bytes);
       bulk_copy(AUXs, a.step, bytes, auxbar);
     }
-    for (int p = tid; p < G; p += NT) Ws[p] = __ldcg(&a.rowsq[p]);  // G <= 192
-    if (!rp) {
-      mbar_wait(auxbar, auxphase);
-      auxphase ^= 1;
-    }
-    __syncthreads();
-    if (warp == 0) {  // identical fixed-order butterfly in every CTA
+    if (warp == 0) {
       double t = 0.0;
-      for (int p = lane; p < G; p += 32) t += Ws[p];
+      for (int p = lane; p < G; p += 32) t += __ldcg(&a.rowsq[p]);  // G <= 192
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         const double os = __shfl_xor_sync(0xffffffffu, t, o);
         t = (lane & o) ? os + t : t + os;
       }
-      if (lane == 0) Ws[250] = sqrt(t);
+      if (lane == 0) {
+        const double nrm = sqrt(t);
+        Ws[250] = nrm;
+        if (!rp) {
+          Hs[it] = nrm;
+          int div = 0;  // solvers.py:240-247: five increases in a row and a tenfold growth
+          if (it + 1 > 5) {
+            bool inc = true;
+            for (int i = it - 5; i < it; i++) inc &= Hs[i + 1] > Hs[i];
+            div = inc && (Hs[it] > 10.0 * Hs[it - 5]);
+          }
+          s_flag = div;
+        }
+      }
     }
     __syncthreads();
+    split(5);
     const double nrm = Ws[250];
     if (rp) {  // tol = residual_tol * ||P rhs|| (solvers.py:212-214)
       tol = a.residual_tol * fmax(nrm, DBL_MIN);
       __syncthreads();
       continue;
     }
-    if (tid == 0) Hs[it] = nrm;
+    mbar_wait(auxbar, auxphase);  // also before a stop: the buffers are reused after the loop
+    auxphase ^= 1;
+    split(6);
     hlen = it + 1;
     if (nrm <= tol) {
       status = 1;
       break;
     }
-    if (tid == 0) {
-      int div = 0;
-      if (hlen > 5) {
-        bool inc = true;
-        for (int i = hlen - 6; i < hlen - 1; i++) inc &= Hs[i + 1] > Hs[i];
-        div = inc && (Hs[hlen - 1] > 10.0 * Hs[hlen - 6]);
-      }
-      s_flag = div;
-    }
-    __syncthreads();
     if (s_flag) {
       status = 2;
       break;
@@ -707,7 +712,7 @@ __global__ void __launch_bounds__(NT, 1) richardson_phased_kernel(PArgs a) {
     }
   }
   if (prof)
-    for (int k = 0; k < 4; k++) g_ws_split[k] = sp[k];
+    for (int k = 0; k < 8; k++) g_ws_split[k] = sp[k];
   if (b == 0) {
     for (int i = tid; i < hlen; i += NT) a.hist[i] = Hs[i];
     if (tid == 0) {

@@ -430,14 +430,20 @@ def _statistical_scores_dev(a: torch.Tensor, fast: bool = True) -> torch.Tensor:
 
 
 def _spectral_rows_dev(a: torch.Tensor, eps: float, delta: float, seed, alpha: float,
-                       fast_scores: bool = True) -> torch.Tensor:
+                       fast_scores: bool = True, divisor: float = 1.0) -> torch.Tensor:
+    """w[:, None] * a[idx, :] of leverage.py:249-252 (divided by ``divisor`` afterwards, as the
+    caller solvers.py:424-427 does), in one gather kernel."""
     sc = _statistical_scores_dev(a, fast_scores)
     p1, _ = _tables(D.to_dev(sc), renorm=False, want_cdf=False, what="score vector")
     s = max(1, math.ceil(alpha * spectral_sample_count(int(a.shape[1]), eps, delta)))
     sk = sample_rows(p1, s, seed)
     idx = D.to_dev(sk.indices, D.I64)
     w = D.to_dev(sk.weights)
-    return w[:, None] * a[idx, :]
+    a = a.contiguous()
+    out = D.empty(int(idx.shape[0]), int(a.shape[1]))
+    _lib.call("ks_scaled_row_gather", D.p(a), int(a.shape[0]), int(a.shape[1]), D.p(idx), D.p(w),
+              int(idx.shape[0]), float(divisor), D.p(out), D.stream())
+    return out
 
 
 def spectral_approx_rows(a, eps: float, delta: float, seed, alpha: float = 1.0):

@@ -676,8 +676,8 @@ def _solve_graph_body(facs, b, config: RegressionConfig, s: int, factor1_stream=
     for n, a in enumerate(facs):
         with torch.cuda.stream(main if n == 0 else f1s):
             if nts[n] < int(a.shape[0]):
-                at = (_spectral_rows_dev(a, eps_two, delta_n, seeds[2 * n], config.effective_alpha)
-                      / math.sqrt(1.0 - eps_two)).contiguous()
+                at = _spectral_rows_dev(a, eps_two, delta_n, seeds[2 * n], config.effective_alpha,
+                                        divisor=math.sqrt(1.0 - eps_two))
             else:
                 at = a
             gts.append(_gram_dev(at))
@@ -1242,8 +1242,8 @@ def _fast_solve_pass(facs, b, config: RegressionConfig, caches, trace, use_chol:
                 a_tilde = a
             else:
                 with torch.cuda.stream(main if n == 0 else _side_stream(n)):
-                    a_tilde = (_spectral_rows_dev(a, eps_two, delta_n, seeds[2 * n], alpha, fast_scores)
-                               / math.sqrt(1.0 - eps_two)).contiguous()
+                    a_tilde = _spectral_rows_dev(a, eps_two, delta_n, seeds[2 * n], alpha, fast_scores,
+                                                 divisor=math.sqrt(1.0 - eps_two))
                 if n > 0:
                     a_tilde.record_stream(main)
             if trace is not None:
