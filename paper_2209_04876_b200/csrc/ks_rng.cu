@@ -8,12 +8,15 @@
 //   * Generator.random(): (raw >> 11) * 2^-53.
 //   * Generator.standard_normal(): NumPy's 256-layer ziggurat (Marsaglia-Tsang/Doornik).  Each
 //     normal consumes a data-dependent number of raw draws (1 in ~99% of cases), so draw i's
-//     start position is resolved in parallel: every position computes "value, consumption if
-//     a normal started here"; 128-position chunks record their exit offset for each possible
-//     entry offset (walks from different entries merge after a step or two); a one-block scan
-//     composes the chunk maps; a final pass emits the chain values.  The ziggurat tables
+//     start position is resolved in parallel: one kernel per super-chunk of 4096 positions
+//     draws the raw outputs, computes "value, consumption if a normal started here" at every
+//     position, and records for each 128-position chunk and each possible entry offset the exit
+//     offset (walks from different entries merge after a step or two), composed into the
+//     super-chunk's map; a one-block scan composes the super-chunk maps; a final pass emits the
+//     chain values.  The ziggurat tables
 //     (ki/wi/fi) are read from the installed NumPy's libnpyrandom.a by the host and passed in.
 #include "ks_common.cuh"
+#include "ks_pcg_jump.cuh"
 
 typedef unsigned __int128 u128;
 
@@ -49,20 +52,6 @@ __device__ __forceinline__ double to_unit(uint64_t r) { return (double)(r >> 11)
 
 constexpr int RAW_PER_THREAD = 16;
 
-// raw[p] = p-th 64-bit output after `skip` draws (output of the state after p+skip+1 steps)
-__global__ void pcg_raw_kernel(uint64_t sh, uint64_t sl, uint64_t ih, uint64_t il, uint64_t skip,
-                               int64_t count, uint64_t* __restrict__ raw) {
-  const int64_t p0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * RAW_PER_THREAD;
-  if (p0 >= count) return;
-  const u128 inc = mk128(ih, il);
-  u128 s = pcg_advance(mk128(sh, sl), inc, skip + (uint64_t)p0 + 1);
-  const int n = (int)ks_min64(RAW_PER_THREAD, count - p0);
-  for (int k = 0; k < n; k++) {
-    raw[p0 + k] = pcg_output(s);
-    s = s * PCG_MULT + inc;
-  }
-}
-
 __global__ void pcg_uniform_kernel(uint64_t sh, uint64_t sl, uint64_t ih, uint64_t il,
                                    uint64_t skip, int64_t count, double* __restrict__ out) {
   const int64_t p0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * RAW_PER_THREAD;
@@ -88,12 +77,12 @@ struct ZigTables {
 
 // Value and raw-draw consumption of a normal whose first draw is raw[p]; -1 if the draw would
 // read past `limit`.  Mirrors NumPy's random_standard_normal; IEEE ops without contraction.
-__device__ int zig_eval(const uint64_t* __restrict__ raw, int64_t p, int64_t limit,
-                        const ZigTables& T, double* out) {
+template <class RAW>
+__device__ __forceinline__ int zig_eval(RAW raw, int64_t p, int64_t limit, const ZigTables& T, double* out) {
   int64_t q = p;
   for (;;) {
     if (q >= limit) return -1;
-    uint64_t r = raw[q++];
+    uint64_t r = raw(q++);
     const int idx = (int)(r & 0xff);
     r >>= 8;
     const int sign = (int)(r & 1);
@@ -107,8 +96,8 @@ __device__ int zig_eval(const uint64_t* __restrict__ raw, int64_t p, int64_t lim
     if (idx == 0) {
       for (;;) {
         if (q + 1 >= limit) return -1;
-        const double u1 = to_unit(raw[q++]);
-        const double u2 = to_unit(raw[q++]);
+        const double u1 = to_unit(raw(q++));
+        const double u2 = to_unit(raw(q++));
         const double xx = __dmul_rn(-ZIG_INV_R, log1p(-u1));
         const double yy = -log1p(-u2);
         if (__dadd_rn(yy, yy) > __dmul_rn(xx, xx)) {
@@ -119,7 +108,7 @@ __device__ int zig_eval(const uint64_t* __restrict__ raw, int64_t p, int64_t lim
       }
     } else {
       if (q >= limit) return -1;
-      const double u = to_unit(raw[q++]);
+      const double u = to_unit(raw(q++));
       const double lhs = __dadd_rn(__dmul_rn(__dsub_rn(T.fi[idx - 1], T.fi[idx]), u), T.fi[idx]);
       if (lhs < exp(__dmul_rn(__dmul_rn(-0.5, x), x))) {
         *out = x;
@@ -129,25 +118,11 @@ __device__ int zig_eval(const uint64_t* __restrict__ raw, int64_t p, int64_t lim
   }
 }
 
-__global__ void zig_eval_kernel(const uint64_t* __restrict__ raw, int64_t M, int64_t limit,
-                                const uint64_t* __restrict__ ki, const double* __restrict__ wi,
-                                const double* __restrict__ fi, double* __restrict__ val,
-                                int16_t* __restrict__ cons) {
-  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= M) return;
-  ZigTables T{ki, wi, fi};
-  double v = 0.0;
-  const int c = zig_eval(raw, p, limit, T, &v);
-  val[p] = v;
-  cons[p] = (int16_t)(c > 32000 ? -1 : c);
-}
-
 constexpr int ZL = 128;  // chunk length (positions)
 constexpr int ZK = 16;   // entry offsets tracked per chunk
 constexpr int ZCB = 32;  // chunks per block of the chunk / emit kernels
 constexpr int ZS = 32;   // chunks per super-chunk (ZCB % ZS == 0)
 constexpr int ZT = 256;  // threads of the compose / emit kernels
-constexpr int ZCT = 4;   // threads per chunk in the chunk kernel (ZK / ZCT offsets each)
 
 // Stage the consumption table of positions [blk_beg, blk_beg + ZCB*ZL) into shared memory with
 // 16-byte asynchronous copies (all in flight at once); positions >= M read as 1.
@@ -167,93 +142,186 @@ __device__ __forceinline__ void zig_stage_cons(int16_t* sc, const int16_t* __res
   __syncthreads();
 }
 
-// For each chunk and entry offset o < ZK: exit offset into the next chunk and normals emitted.
-__global__ void __launch_bounds__(ZCB * ZCT) zig_chunk_kernel(const int16_t* __restrict__ cons, int64_t M,
-                                                       int64_t nchunks, uint8_t* __restrict__ exit_off,
-                                                       int32_t* __restrict__ cnt, int32_t* __restrict__ err) {
-  __shared__ __align__(16) int16_t sc[ZCB * ZL];
-  const int64_t blk_beg = (int64_t)blockIdx.x * ZCB * ZL;
-  zig_stage_cons(sc, cons, M, blk_beg);
-  // ZCT threads per chunk, ZK / ZCT entry offsets each (each walks offset 0 for the merge mask)
-  const int lc = threadIdx.x / ZCT, part = threadIdx.x % ZCT;
-  const int64_t c = (int64_t)blockIdx.x * ZCB + lc;
-  if (lc >= ZCB || c >= nchunks) return;
-  const int beg = lc * ZL;
-  const int end = (int)ks_min64(M - blk_beg, beg + ZL);
-  uint64_t m0 = 0, m1 = 0;
-  int q = beg, c0 = 0;
-  while (q < end) {
-    const int k = sc[q];
-    if (k <= 0) { atomicOr(err, 1); return; }
-    const int rel = q - beg;
-    if (rel < 64) m0 |= 1ull << rel; else m1 |= 1ull << (rel - 64);
-    c0++;
-    q += k;
-  }
-  const int e0 = q - end;
-  if (e0 >= ZK) { atomicOr(err, 2); return; }
-  for (int o = part * (ZK / ZCT); o < (part + 1) * (ZK / ZCT); o++) {
-    int qq = beg + o, steps = 0;
-    for (;;) {
-      if (qq >= end) break;
-      const int rel = qq - beg;
-      const bool on0 = rel < 64 ? ((m0 >> rel) & 1) : ((m1 >> (rel - 64)) & 1);
-      if (on0) break;
-      const int k = sc[qq];
-      if (k <= 0) { atomicOr(err, 1); return; }
-      steps++;
-      qq += k;
-    }
-    if (qq >= end) {
-      const int e = qq - end;
-      if (e >= ZK) { atomicOr(err, 2); return; }
-      exit_off[c * ZK + o] = (uint8_t)e;
-      cnt[c * ZK + o] = steps;
+// 128-bit position masks of a chunk (m0: positions 0..63, m1: 64..127).
+__device__ __forceinline__ void mask_set_range(uint64_t& m0, uint64_t& m1, int a, int b) {  // [a, b)
+  auto bits = [](int lo, int hi) -> uint64_t {  // bits [lo, hi) of a word, 0 <= lo <= hi <= 64
+    if (hi <= lo) return 0ull;
+    const uint64_t up = hi >= 64 ? ~0ull : ((1ull << hi) - 1);
+    return up & (~0ull << lo);
+  };
+  m0 |= bits(min(a, 64), min(b, 64));
+  m1 |= bits(max(a, 64) - 64, max(b, 64) - 64);
+}
+
+// The chain of a chunk entered at offset o: positions whose consumption is 1 follow each other,
+// so the walk only stops at the "special" positions (mask s0/s1: consumption != 1, typically
+// ~1.5 per chunk) instead of stepping through all 128.  len: positions of the chunk (< ZL only
+// for the last one).  Returns the exit offset into the next chunk (-1: bad consumption), the
+// chain positions in m0/m1.
+__device__ __forceinline__ int chunk_walk(const int16_t* sc, int len, uint64_t s0, uint64_t s1, int o, uint64_t& m0,
+                                          uint64_t& m1) {
+  m0 = 0;
+  m1 = 0;
+  int q = o;
+  while (q < len) {
+    int sp;
+    if (q < 64) {
+      const uint64_t t = s0 & (~0ull << q);
+      sp = t ? __ffsll((long long)t) - 1 : (s1 ? 63 + __ffsll((long long)s1) : ZL);
     } else {
-      // merged with the offset-0 walk at qq: remaining count = walk-0 positions >= qq
-      const int rel = qq - beg;
-      const int before = rel >= 64 ? __popcll(m0) + __popcll(m1 & ((1ull << (rel - 64)) - 1))
-                                   : __popcll(m0 & ((1ull << rel) - 1));
-      exit_off[c * ZK + o] = (uint8_t)e0;
-      cnt[c * ZK + o] = steps + (c0 - before);
+      const uint64_t t = s1 & (~0ull << (q - 64));
+      sp = t ? 63 + __ffsll((long long)t) : ZL;
     }
+    if (sp >= len) {  // unit steps to the end of the chunk
+      mask_set_range(m0, m1, q, len);
+      q = len;
+      break;
+    }
+    mask_set_range(m0, m1, q, sp + 1);
+    const int k = sc[sp];
+    if (k <= 0) return -1;
+    q = sp + k;
+  }
+  return q - len;
+}
+
+// Masks of the positions of chunk c (of a block's staged consumptions) whose consumption is
+// not 1; one warp, all lanes.
+__device__ __forceinline__ void chunk_special(const int16_t* sc, int c, int len, uint64_t& s0, uint64_t& s1) {
+  const int lane = threadIdx.x & 31;
+  unsigned b[4];
+#pragma unroll
+  for (int j = 0; j < 4; j++) {
+    const int rel = lane + 32 * j;
+    b[j] = __ballot_sync(0xffffffffu, rel < len && sc[c * ZL + rel] != 1);
+  }
+  s0 = (uint64_t)b[0] | ((uint64_t)b[1] << 32);
+  s1 = (uint64_t)b[2] | ((uint64_t)b[3] << 32);
+}
+
+// Fused front of the chain resolution, one block per super-chunk (ZS chunks of ZL positions):
+// the block's raw draws (each thread jumps once to its first position, then strides by ZT with
+// the 256-step affine map of the LCG, so shared-memory stores are conflict-free), the value and
+// consumption of a normal starting at every position (draws past the staged window are
+// recomputed by a jump: astronomically rare), the chunk maps (ZK entry offsets, ZFT threads per
+// chunk) and their composition into the super-chunk map.  Replaces the raw / eval / chunk /
+// compose launches with one; same outputs.
+constexpr int ZRX = 0;            // raw draws staged past the super-chunk (look-ahead; later draws are recomputed)
+constexpr int ZRS = ZS * ZL + ZRX;
+static_assert(ZRS % ZT == 0 && ZT == 256 && ZK <= 32, "front kernel shape");
+__global__ void __launch_bounds__(ZT) zig_front_kernel(uint64_t sh, uint64_t sl, uint64_t ih, uint64_t il,
+                                                       uint64_t skip, int64_t M, int64_t limit,
+                                                       const uint64_t* __restrict__ ki, const double* __restrict__ wi,
+                                                       const double* __restrict__ fi, double* __restrict__ val,
+                                                       int16_t* __restrict__ cons, int64_t nchunks,
+                                                       uint8_t* __restrict__ exit_off, int32_t* __restrict__ cnt,
+                                                       uint8_t* __restrict__ sexit, int32_t* __restrict__ scnt,
+                                                       int32_t* __restrict__ err) {
+  __shared__ uint64_t raw_s[ZRS];
+  __shared__ __align__(16) int16_t sc[ZS * ZL];
+  __shared__ uint8_t se[ZS * ZK];
+  __shared__ int32_t sn[ZS * ZK];
+  __shared__ uint64_t ki_s[256];
+  __shared__ double wi_s[256];
+  const int tid = threadIdx.x;
+  ki_s[tid] = __ldg(&ki[tid]);
+  wi_s[tid] = __ldg(&wi[tid]);
+  const int64_t blk_beg = (int64_t)blockIdx.x * ZS * ZL;
+  const u128 state0 = mk128(sh, sl), inc = mk128(ih, il);
+  // raw draws blk_beg + [0, ZRS): position q is the output of the state after skip + q + 1 steps.
+  // One jump to the block's start, then each thread's offset and its ZT-step stride from the
+  // precomputed affine maps (ks_pcg_jump.cuh): two 128-bit multiply-adds per draw at most
+  __shared__ uint64_t s_blk[2];
+  if (tid == 0) {
+    const u128 sb = pcg_advance(state0, inc, skip + (uint64_t)blk_beg + 1);
+    s_blk[0] = (uint64_t)(sb >> 64);
+    s_blk[1] = (uint64_t)sb;
+  }
+  __syncthreads();
+  {
+    const u128 sb = mk128(s_blk[0], s_blk[1]);
+    u128 st = mk128(ks_pcg::kJump[tid][0], ks_pcg::kJump[tid][1]) * sb +
+              mk128(ks_pcg::kJump[tid][2], ks_pcg::kJump[tid][3]) * inc;
+    const u128 am = mk128(ks_pcg::kJump[ZT][0], ks_pcg::kJump[ZT][1]);
+    const u128 ap = mk128(ks_pcg::kJump[ZT][2], ks_pcg::kJump[ZT][3]) * inc;
+#pragma unroll 4
+    for (int i = tid; i < ZRS; i += ZT) {
+      raw_s[i] = pcg_output(st);
+      st = am * st + ap;
+    }
+  }
+  __syncthreads();
+  const ZigTables T{ki, wi, fi};
+  auto raw = [&](int64_t q) -> uint64_t {
+    const int64_t i = q - blk_beg;
+    return i < ZRS ? raw_s[i] : pcg_output(pcg_advance(state0, inc, skip + (uint64_t)q + 1));
+  };
+#pragma unroll 4
+  for (int i = tid; i < ZS * ZL; i += ZT) {
+    const int64_t p = blk_beg + i;
+    int16_t c16 = 1;  // positions >= M read as 1 (as the staged chunk walks do)
+    if (p < M) {
+      // the ziggurat's first test (taken ~99% of the time) from the staged tables; the other
+      // branches through the full evaluation
+      uint64_t r = raw_s[i];
+      const int idx = (int)(r & 0xff);
+      r >>= 8;
+      const uint64_t rabs = (r >> 1) & 0x000fffffffffffffULL;
+      double v = __dmul_rn((double)rabs, wi_s[idx]);
+      if (r & 1) v = -v;
+      if (!(rabs < ki_s[idx]) || p >= limit) {
+        const int c = zig_eval(raw, p, limit, T, &v);
+        c16 = (int16_t)(c > 32000 ? -1 : c);
+      }
+      val[p] = v;
+      cons[p] = c16;
+    }
+    sc[i] = c16;
+  }
+  __syncthreads();
+  // chunk maps: one warp per chunk at a time (special-position masks by ballot), lanes 0..ZK-1
+  // walk one entry offset each
+  {
+    const int warp = tid >> 5, lane = tid & 31;
+    for (int lc = warp; lc < ZS; lc += ZT / 32) {
+      const int64_t c = (int64_t)blockIdx.x * ZS + lc;
+      if (c >= nchunks) break;
+      const int len = (int)ks_min64(M - blk_beg - (int64_t)lc * ZL, ZL);
+      uint64_t s0, s1;
+      chunk_special(sc, lc, len, s0, s1);
+      if (lane < ZK) {
+        uint64_t m0, m1;
+        const int e = chunk_walk(sc + lc * ZL, len, s0, s1, lane, m0, m1);
+        if (e < 0) atomicOr(err, 1);
+        else if (e >= ZK) atomicOr(err, 2);
+        const int n = __popcll(m0) + __popcll(m1);
+        exit_off[c * ZK + lane] = (uint8_t)(e < 0 ? 0 : e);
+        cnt[c * ZK + lane] = n;
+        se[lc * ZK + lane] = (uint8_t)(e < 0 || e >= ZK ? 0 : e);
+        sn[lc * ZK + lane] = n;
+      }
+    }
+  }
+  __syncthreads();
+  if (tid < ZK) {  // the super-chunk map: the block's chunk maps composed for every entry offset
+    const int nc = (int)ks_min64(nchunks - (int64_t)blockIdx.x * ZS, ZS);
+    int e = tid;
+    int32_t k = 0;
+    for (int c = 0; c < nc; c++) {
+      k += sn[c * ZK + e];
+      e = se[c * ZK + e];
+    }
+    sexit[(int64_t)blockIdx.x * ZK + tid] = (uint8_t)e;
+    scnt[(int64_t)blockIdx.x * ZK + tid] = k;
   }
 }
 
-// Compose the maps of ZS consecutive chunks into one super-chunk map.  One block covers
-// ZT / ZK super-chunks; their chunk maps are staged in shared memory first.
-__global__ void __launch_bounds__(ZT) zig_compose_kernel(const uint8_t* __restrict__ exit_off,
-                                                         const int32_t* __restrict__ cnt, int64_t nchunks,
-                                                         int64_t nsuper, uint8_t* __restrict__ sexit,
-                                                         int32_t* __restrict__ scnt) {
-  constexpr int SB = ZT / ZK;  // super-chunks per block
-  __shared__ __align__(16) uint8_t se[SB * ZS * ZK];
-  __shared__ int32_t sn[SB * ZS * ZK];
-  const int64_t cb = (int64_t)blockIdx.x * SB * ZS;  // first chunk of the block
-  const int64_t nc = ks_min64(nchunks - cb, SB * ZS);
-  for (int i = threadIdx.x; i < nc * ZK; i += ZT) ks_cp_async4(&sn[i], cnt + cb * ZK + i);
-  for (int i = threadIdx.x; i < nc * ZK / 4; i += ZT) ks_cp_async4(&se[4 * i], exit_off + cb * ZK + 4 * i);
-  ks_cp_async_wait_all();
-  __syncthreads();
-  const int ls = threadIdx.x / ZK, o = threadIdx.x % ZK;
-  const int64_t sidx = (int64_t)blockIdx.x * SB + ls;
-  if (sidx >= nsuper) return;
-  const int c_end = (int)ks_min64(nc, (ls + 1) * ZS);
-  int e = o;
-  int32_t k = 0;
-  for (int c = ls * ZS; c < c_end; c++) {
-    k += sn[c * ZK + e];
-    e = se[c * ZK + e];
-  }
-  sexit[sidx * ZK + o] = (uint8_t)e;
-  scnt[sidx * ZK + o] = k;
-}
-// Small-count variant (nsuper <= ZS2_MAX): the maps are staged in shared memory; the 32 lanes of
-// warp 0 compose contiguous blocks of super-chunks for all ZK entry offsets, lane 0 walks the 32
-// block maps from entry offset 0, and every lane then walks its block from its entry.  Only the
-// one path that matters is followed, instead of composing every map pair.
+// Small-count variant (nsuper <= ZS2_MAX): the maps are staged in shared memory; warp o composes
+// the 32 contiguous blocks of super-chunks for entry offset o (one block per lane), one thread
+// walks the 32 block maps from entry offset 0, and warp 0's lanes then walk their blocks from
+// their entries.  Only the one path that matters is followed, instead of composing every map pair.
 constexpr int ZS2_MAX = 2048;
-constexpr int ZS2_T = 256;
+constexpr int ZS2_T = 32 * ZK;  // one warp per entry offset
 __global__ void __launch_bounds__(ZS2_T) zig_scan_small_kernel(const uint8_t* __restrict__ sexit,
                                                               const int32_t* __restrict__ scnt, int64_t nsuper,
                                                               uint8_t* __restrict__ sentry,
@@ -271,12 +339,10 @@ __global__ void __launch_bounds__(ZS2_T) zig_scan_small_kernel(const uint8_t* __
   for (int i = threadIdx.x; i < nz / 4; i += ZS2_T) ks_cp_async4(&ex[4 * i], sexit + 4 * i);
   ks_cp_async_wait_all();
   __syncthreads();
-  if (threadIdx.x >= 32) return;
-  const int lane = threadIdx.x;
+  const int lane = threadIdx.x & 31, o = threadIdx.x >> 5;
   const int per = ((int)nsuper + 31) / 32;
   const int c0 = min((int)nsuper, lane * per), c1 = min((int)nsuper, c0 + per);
-#pragma unroll
-  for (int o = 0; o < ZK; o++) {
+  {  // lane's block of super-chunks composed for entry offset o (one warp per offset)
     int e = o;
     int64_t k = 0;
     for (int c = c0; c < c1; c++) {
@@ -286,8 +352,8 @@ __global__ void __launch_bounds__(ZS2_T) zig_scan_small_kernel(const uint8_t* __
     bexit[lane][o] = e;
     bcnt[lane][o] = k;
   }
-  __syncwarp();
-  if (lane == 0) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
     int e = 0;
     int64_t k = 0;
     for (int l = 0; l < 32; l++) {
@@ -298,7 +364,8 @@ __global__ void __launch_bounds__(ZS2_T) zig_scan_small_kernel(const uint8_t* __
     }
     *total = k;
   }
-  __syncwarp();
+  __syncthreads();
+  if (o != 0) return;
   int e = bentry[lane];
   int64_t k = bbase[lane];
   for (int c = c0; c < c1; c++) {
@@ -414,19 +481,19 @@ __global__ void __launch_bounds__(ZT) zig_emit_kernel(const int16_t* __restrict_
     }
   }
   __syncthreads();
-  if (threadIdx.x < nc) {
-    const int lc = threadIdx.x;
-    const int beg = lc * ZL, end = (int)ks_min64(M - blk_beg, beg + ZL);
-    uint64_t m0 = 0, m1 = 0;
-    for (int q = beg + c_entry[lc]; q < end;) {
-      const int rel = q - beg;
-      const int step = sc[q];
-      if (step <= 0) break;  // reported by zig_chunk_kernel
-      q += step;
-      if (rel < 64) m0 |= 1ull << rel; else m1 |= 1ull << (rel - 64);
+  {  // each chunk's chain positions from its entry offset (mask walk, one warp per chunk)
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int lc = warp; lc < nc; lc += ZT / 32) {
+      const int len = (int)ks_min64(M - blk_beg - (int64_t)lc * ZL, ZL);
+      uint64_t s0, s1;
+      chunk_special(sc, lc, len, s0, s1);
+      if (lane == 0) {
+        uint64_t m0, m1;
+        if (chunk_walk(sc + lc * ZL, len, s0, s1, c_entry[lc], m0, m1) < 0) m0 = m1 = 0;  // reported by the front kernel
+        c_mask[lc][0] = m0;
+        c_mask[lc][1] = m1;
+      }
     }
-    c_mask[lc][0] = m0;
-    c_mask[lc][1] = m1;
   }
   __syncthreads();
   const int npos = (int)ks_min64(M - blk_beg, (int64_t)nc * ZL);
@@ -505,7 +572,6 @@ extern "C" int ks_pcg64_standard_normal(uint64_t sh, uint64_t sl, uint64_t ih, u
     const int64_t M = n + n / 16 + 4096;            // positions evaluated
     const int64_t limit = M + 256;                  // raw draws generated (tail look-ahead)
     const int64_t nchunks = (M + ZL - 1) / ZL;
-    ks::Scratch<uint64_t> raw(limit, st);
     ks::Scratch<double> val(M, st);
     ks::Scratch<int16_t> cons(M, st);
     ks::Scratch<uint8_t> exit_off(nchunks * ZK, st);
@@ -518,20 +584,14 @@ extern "C" int ks_pcg64_standard_normal(uint64_t sh, uint64_t sl, uint64_t ih, u
     ks::Scratch<int64_t> tail(2, st);  // [0] chain length over M positions, [1] draws consumed
     ks::Scratch<int32_t> err_s(async ? 0 : 1, st);
     int32_t* err = async ? status : err_s.p;
-    KS_REQUIRE(raw.p && val.p && cons.p && exit_off.p && cnt.p && tail.p && err && sexit.p && scnt.p &&
+    KS_REQUIRE(val.p && cons.p && exit_off.p && cnt.p && tail.p && err && sexit.p && scnt.p &&
                sentry.p && sbase.p,
                KS_ECUDA, "scratch allocation failed");
     if (!async) KS_TRY_CUDA(cudaMemsetAsync(err, 0, sizeof(int32_t), st));
-    const int64_t rthreads = (limit + RAW_PER_THREAD - 1) / RAW_PER_THREAD;
-    pcg_raw_kernel<<<ceil_div_u(rthreads, 256), 256, 0, st>>>(sh, sl, ih, il, skip, limit, raw.p);
-    KS_CHECK_LAUNCH();
-    zig_eval_kernel<<<ceil_div_u(M, 256), 256, 0, st>>>(raw.p, M, limit, ki, wi, fi, val.p, cons.p);
-    KS_CHECK_LAUNCH();
     const unsigned nblk = ceil_div_u(nchunks, ZCB);
-    zig_chunk_kernel<<<nblk, ZCB * ZCT, 0, st>>>(cons.p, M, nchunks, exit_off.p, cnt.p, err);
-    KS_CHECK_LAUNCH();
-    zig_compose_kernel<<<ceil_div_u(nsuper, ZT / ZK), ZT, 0, st>>>(exit_off.p, cnt.p, nchunks, nsuper,
-                                                                   sexit.p, scnt.p);
+    // one block per super-chunk: raw draws, values / consumptions, chunk and super-chunk maps
+    zig_front_kernel<<<(unsigned)nsuper, ZT, 0, st>>>(sh, sl, ih, il, skip, M, limit, ki, wi, fi, val.p, cons.p,
+                                                      nchunks, exit_off.p, cnt.p, sexit.p, scnt.p, err);
     KS_CHECK_LAUNCH();
     if (nsuper <= ZS2_MAX) {
       const size_t smem2 = (size_t)ZS2_MAX * ZK * (sizeof(int32_t) + 1);
