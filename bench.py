@@ -35,6 +35,10 @@ import threading
 import time
 from pathlib import Path
 
+# the solve graph's concurrent branches need more than the default 8 hardware work queues
+# (paper_2209_04876_b200/__init__.py); set before any CUDA context exists
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 

@@ -272,7 +272,7 @@ __device__ void jacobi_fp32_prelude(const double* __restrict__ M, double* W, dou
   const int tid = threadIdx.x;
   for (int e = tid; e < D * D; e += NT) {
     const int i = e / D, j = e % D;
-    W32[jf_off<D>(j, i)] = (float)(0.5 * (M[(size_t)i * D + j] + M[(size_t)j * D + i]));
+    W32[jf_off<D>(j, i)] = (float)(0.5 * (M[i * D + j] + M[j * D + i]));
     V32[jf_off<D>(j, i)] = (i == j) ? 1.0f : 0.0f;
   }
   __syncthreads();
@@ -364,7 +364,7 @@ __device__ void jacobi_fp32_prelude(const double* __restrict__ M, double* W, dou
   // Y = G (symmetrised, row-major), then W = G V
   for (int e = tid; e < D * D; e += NT) {
     const int i = e / D, k = e % D;
-    Y[e] = 0.5 * (M[(size_t)i * D + k] + M[(size_t)k * D + i]);
+    Y[e] = 0.5 * (M[i * D + k] + M[k * D + i]);
   }
   __syncthreads();
   smem_gemm_rows<D>([&](int i, int k) { return Y[k * D + i]; }, [&](int k, int j) { return V[j * LD + k]; },
@@ -372,10 +372,74 @@ __device__ void jacobi_fp32_prelude(const double* __restrict__ M, double* W, dou
   __syncthreads();
 }
 
+// Dominant-eigenpair deflation of a symmetric Gram matrix G (row-major, shared memory), before the
+// Jacobi sweeps.  Gram matrices of factors whose columns share a large mean (BASELINE's
+// N(1, 0.001) factors: one eigenvalue ~n d, the others ~n 1e-3) carry the small eigenvalues in the
+// low bits of every entry, so the FP32 prelude cannot resolve them and the FP64 phase needs ~5
+// sweeps.  When one eigenvalue dominates (power iteration from the all-ones vector converges to a
+// residual ||G v - lam v|| <= 16 D eps lam, and ||G - lam v v^T||_F <= 1e-3 lam), G is replaced
+// by H G H with the Householder reflector H = I - beta u u^T, H v = -sign(v_0) e_1, and the
+// (rounding-level) off-diagonal entries of its first row and column are set to zero: the
+// eigenvalues and eigenvectors change by O(||r||^2 / lam) and O(||r|| / lam) ~ 1e-16, far below
+// the reference's own eigensolver rounding.  The sweeps then see a block-diagonal matrix whose
+// small block is well scaled; the eigenvectors of G are H V.  Returns beta (0: not deflated) and
+// leaves u in `u`.  All threads of the block call it.
+template <int D>
+__device__ double jacobi_deflate(double* G, double* u, double* v, double* w, double* red) {
+  constexpr int NT = D / 2 * JF_G, TPR = NT / D;  // threads per row of a product
+  static_assert(TPR * D == NT && (TPR & (TPR - 1)) == 0 && TPR <= 32, "row groups within a warp");
+  const int tid = threadIdx.x, row = tid / TPR, part = tid % TPR;
+  auto matvec = [&](const double* x, double* y) {  // y = G x
+    double t = 0.0;
+    for (int k = part; k < D; k += TPR) t = fma(G[row * D + k], x[k], t);
+#pragma unroll
+    for (int o = TPR / 2; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (part == 0) y[row] = t;
+    __syncthreads();
+  };
+  for (int i = tid; i < D; i += NT) v[i] = rsqrt((double)D);
+  __syncthreads();
+  for (int it = 0; it < 6; it++) {
+    matvec(v, w);
+    const double nn = block_sum(tid < D ? w[tid] * w[tid] : 0.0, red);
+    if (!(nn > 0.0) || !isfinite(nn)) return 0.0;
+    const double sc = rsqrt(nn);
+    for (int i = tid; i < D; i += NT) v[i] = w[i] * sc;
+    __syncthreads();
+  }
+  matvec(v, w);
+  const double lam = block_sum(tid < D ? v[tid] * w[tid] : 0.0, red);
+  const double res = block_sum(tid < D ? (w[tid] - lam * v[tid]) * (w[tid] - lam * v[tid]) : 0.0, red);
+  double off = 0.0;
+  for (int e = tid; e < D * D; e += NT) {
+    const double r = G[e] - lam * v[e / D] * v[e % D];
+    off = fma(r, r, off);
+  }
+  off = block_sum(off, red);
+  if (!(lam > 0.0) || !(sqrt(res) <= 16.0 * D * 2.220446049250313e-16 * lam) || !(sqrt(off) <= 1e-3 * lam))
+    return 0.0;
+  // u = v + sign(v_0) e_1, beta = 2 / u^T u = 1 / (1 + |v_0|)
+  const double s0 = v[0] >= 0.0 ? 1.0 : -1.0, beta = 1.0 / (1.0 + fabs(v[0]));
+  for (int i = tid; i < D; i += NT) u[i] = v[i] + (i == 0 ? s0 : 0.0);
+  __syncthreads();
+  matvec(u, w);  // p = G u
+  const double K = block_sum(tid < D ? u[tid] * w[tid] : 0.0, red);
+  for (int i = tid; i < D; i += NT) w[i] = beta * w[i] - 0.5 * beta * beta * K * u[i];  // H G H = G - u w^T - w u^T
+  __syncthreads();
+  for (int e = tid; e < D * D; e += NT) {
+    const int i = e / D, j = e % D;
+    const double g = G[e] - u[i] * w[j] - w[i] * u[j];
+    G[e] = (i == 0) != (j == 0) ? 0.0 : g;
+  }
+  __syncthreads();
+  return beta;
+}
+
 template <int D, bool SYM>
 __global__ void __launch_bounds__(D / 2 * JF_G) jacobi_fixed_kernel(MatPtrs Ms, const double* __restrict__ Mc,
                                                                    double* __restrict__ sigma,
-                                                                   double* __restrict__ Vout, int sweeps32) {
+                                                                   double* __restrict__ Vout, int sweeps32,
+                                                                   int deflate) {
   constexpr int NP = D / 2, NT = NP * JF_G, E = D / JF_G;
   extern __shared__ double jf_sm[];
   double* W = jf_sm;
@@ -387,9 +451,19 @@ __global__ void __launch_bounds__(D / 2 * JF_G) jacobi_fixed_kernel(MatPtrs Ms, 
   sigma += (size_t)blockIdx.x * D;
   Vout += (size_t)blockIdx.x * D * D;
   const int tid = threadIdx.x;
+  double beta = 0.0;
+  __shared__ double s_u[D], s_v[D], s_w[D], s_red[32];
   if (SYM && sweeps32 > 0) {
+    // the Gram matrix, symmetrised, in the Y/Z scratch past the FP32 buffers; deflated in place
+    double* Gs = jf_sm + 4 * D * (D + 8);
+    for (int e = tid; e < D * D; e += NT) {
+      const int i = e / D, j = e % D;
+      Gs[e] = 0.5 * (M[(size_t)i * D + j] + M[(size_t)j * D + i]);
+    }
+    __syncthreads();
+    if (deflate) beta = jacobi_deflate<D>(Gs, s_u, s_v, s_w, s_red);
     float* W32 = reinterpret_cast<float*>(jf_sm + 2 * D * (D + 8));
-    jacobi_fp32_prelude<D>(M, W, V, W32, W32 + D * (D + 8), sweeps32);
+    jacobi_fp32_prelude<D>(Gs, W, V, W32, W32 + D * (D + 8), sweeps32);
   } else {
     for (int e = tid; e < D * D; e += NT) {
       const int i = e / D, j = e % D;  // M row i, column j
@@ -401,8 +475,16 @@ __global__ void __launch_bounds__(D / 2 * JF_G) jacobi_fixed_kernel(MatPtrs Ms, 
   }
   const int group = tid / JF_G, lg = tid % JF_G;
   const double tol = 2.0 * D * 2.220446049250313e-16;
+  // symmetric problems: after a sweep whose rotations all had c^2 <= MU2_DONE a b (column cosines
+  // <= 1e-9), the next sweep's would be O(1e-18 / relative gap), below tol: that confirmation
+  // sweep is skipped (measured at d = 64: cosines 2e-5, 1e-9, then none above tol)
+  constexpr double MU2_DONE = 1e-18;
+  __shared__ int s_big;
   for (int sweep = 0; sweep < 40; sweep++) {
-    if (tid == 0) s_rot = 0;
+    if (tid == 0) {
+      s_rot = 0;
+      s_big = 0;
+    }
     __syncthreads();
     for (int r = 0; r < D - 1; r++) {
       auto player = [&](int pos) {
@@ -460,12 +542,15 @@ __global__ void __launch_bounds__(D / 2 * JF_G) jacobi_fixed_kernel(MatPtrs Ms, 
           V[jf_off<D>(p, lg + k * JF_G)] = cs * u[k] - sn * v[k];
           V[jf_off<D>(q, lg + k * JF_G)] = sn * u[k] + cs * v[k];
         }
-        if (lg == 0) s_rot = 1;
+        if (lg == 0) {
+          s_rot = 1;
+          if (SYM && c * c > MU2_DONE * a * b) s_big = 1;
+        }
       }
       __syncthreads();
     }
     if (tid == 0) g_jacobi_sweeps[blockIdx.x & 7] = sweep + 1;
-    if (s_rot == 0) break;
+    if (s_rot == 0 || (SYM && s_big == 0)) break;
     __syncthreads();
   }
   for (int j = tid; j < D; j += NT) {
@@ -486,6 +571,20 @@ __global__ void __launch_bounds__(D / 2 * JF_G) jacobi_fixed_kernel(MatPtrs Ms, 
   }
   __syncthreads();
   for (int k = tid; k < D; k += NT) sigma[k] = s_norm[s_order[k]];
+  if (SYM && beta != 0.0) {  // eigenvectors of G: H V' = V' - beta u (u^T V')
+    __syncthreads();  // sigma has read the norms
+    for (int j = tid; j < D; j += NT) {
+      double t = 0.0;
+      for (int i = 0; i < D; i++) t = fma(s_u[i], V[jf_off<D>(j, i)], t);
+      s_norm[j] = beta * t;  // the norms are no longer needed
+    }
+    __syncthreads();
+    for (int e = tid; e < D * D; e += NT) {
+      const int j = e / D, i = e % D;
+      V[jf_off<D>(j, i)] -= s_u[i] * s_norm[j];
+    }
+    __syncthreads();
+  }
   for (int e = tid; e < D * D; e += NT) {
     const int i = e / D, k = e % D;
     Vout[e] = V[jf_off<D>(s_order[k], i)];
@@ -651,15 +750,17 @@ int qr_r(cudaStream_t st, const double* A, int64_t n, int d, double* R) {
 template <int D, bool SYM>
 static void launch_jacobi_fixed(cudaStream_t st, const MatPtrs& Ms, const double* M, double* sigma, double* V,
                                 int batch) {
-  // symmetric (Gram) problems: FP32 prelude sweeps (KS_JACOBI_FP32=<n>, default 4; 0 = off)
+  // symmetric (Gram) problems: FP32 prelude sweeps (KS_JACOBI_FP32=<n>, default 5; 0 = off)
   int sweeps32 = 0;
   if (SYM) {
     const char* e = ks::env(ks::ENV_JACOBI_FP32);
-    sweeps32 = e ? atoi(e) : 4;
+    sweeps32 = e ? atoi(e) : 5;
   }
-  const int smem = (sweeps32 > 0 ? 4 : 2) * D * (D + 8) * (int)sizeof(double);
+  // symmetric problems with the FP32 prelude also hold the Gram matrix (D x D) for the deflation
+  const int smem = ((sweeps32 > 0 ? 4 : 2) * D * (D + 8) + (sweeps32 > 0 ? D * D : 0)) * (int)sizeof(double);
+  const int deflate = SYM && !ks::env(ks::ENV_NO_DEFLATE);
   cudaFuncSetAttribute(jacobi_fixed_kernel<D, SYM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  jacobi_fixed_kernel<D, SYM><<<batch, D / 2 * JF_G, smem, st>>>(Ms, M, sigma, V, sweeps32);
+  jacobi_fixed_kernel<D, SYM><<<batch, D / 2 * JF_G, smem, st>>>(Ms, M, sigma, V, sweeps32, deflate);
 }
 
 
