@@ -564,7 +564,6 @@ __global__ void __launch_bounds__(NT, 1) richardson_phased_kernel(PArgs a) {
         auxphase ^= 1;
       }
       split(4);
-      double eig_sq = 0.0;
       const int eo = tid >> 3, ql = lane & 7;
       const unsigned qmask = 0xffu << (lane & 24);
       if (eo < ne_cta) {  // 8 threads per element: fixed-order compensated sum over the CTA partials
@@ -606,12 +605,9 @@ __global__ void __launch_bounds__(NT, 1) richardson_phased_kernel(PArgs a) {
             r = __dsub_rn(__dadd_rn(s + cmp, __dmul_rn(a.lam, my_x)), my_rhs);
           }
           my_st = r * my_dv;
-          if (!rp) a.step[i * DRP + k] = my_st;  // padded rows: fetched with one bulk copy
-          eig_sq = fma(my_st, my_st, 0.0);
+          a.step[i * DRP + k] = my_st;  // padded rows: fetched with one bulk copy
         }
       }
-      eig_sq = block_sum(eig_sq, Ws + 192);  // fixed-order CTA partial of ||step'||^2
-      if (tid == 0) a.rowsq[b] = eig_sq;
       asm volatile("fence.proxy.async.global;" ::: "memory");
     }
     if (a.apply_only) return;
@@ -620,48 +616,39 @@ __global__ void __launch_bounds__(NT, 1) richardson_phased_kernel(PArgs a) {
     if (prof) pt = clock64();
     if (prof && !rp) g_ws_prof[it * 6 + 4] = clock64();
     // ---------------- norm, stopping rules (solvers.py:226-247), update ----------------
-    // the step' fetch (one bulk copy) overlaps the norm: warp 0 sums the CTA partials of
-    // ||step'||^2 in a fixed order (identical in every CTA) and applies the stopping rules
-    if (!rp && tid == 0) {
+    // every CTA fetches step' (one bulk copy) and forms ||step'|| from it in the same fixed order
+    // (identical in every CTA); tid 0 applies the stopping and divergence rules
+    if (tid == 0) {
       asm volatile("fence.proxy.async.global;" ::: "memory");
       const uint32_t bytes = (uint32_t)(DL * DRP * 8);
       mbar_arrive_expect_tx(auxbar, bytes);
       bulk_copy(AUXs, a.step, bytes, auxbar);
     }
-    if (warp == 0) {
-      double t = 0.0;
-      for (int p = lane; p < G; p += 32) t += __ldcg(&a.rowsq[p]);  // G <= 192
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double os = __shfl_xor_sync(0xffffffffu, t, o);
-        t = (lane & o) ? os + t : t + os;
-      }
-      if (lane == 0) {
-        const double nrm = sqrt(t);
-        Ws[250] = nrm;
-        if (!rp) {
-          Hs[it] = nrm;
-          int div = 0;  // solvers.py:240-247: five increases in a row and a tenfold growth
-          if (it + 1 > 5) {
-            bool inc = true;
-            for (int i = it - 5; i < it; i++) inc &= Hs[i + 1] > Hs[i];
-            div = inc && (Hs[it] > 10.0 * Hs[it - 5]);
-          }
-          s_flag = div;
-        }
-      }
-    }
-    __syncthreads();
-    split(5);
-    const double nrm = Ws[250];
-    if (rp) {  // tol = residual_tol * ||P rhs|| (solvers.py:212-214)
-      tol = a.residual_tol * fmax(nrm, DBL_MIN);
-      __syncthreads();
-      continue;
-    }
     mbar_wait(auxbar, auxphase);  // also before a stop: the buffers are reused after the loop
     auxphase ^= 1;
     split(6);
+    double sq = 0.0;
+    for (int e = tid; e < NE; e += NT) {
+      const double v = AUXs[(e / DR) * DRP + e % DR];
+      sq = fma(v, v, sq);
+    }
+    const double nrm = sqrt(block_sum(sq, Ws + 192));
+    if (rp) {  // tol = residual_tol * ||P rhs|| (solvers.py:212-214)
+      tol = a.residual_tol * fmax(nrm, DBL_MIN);
+      continue;  // block_sum ended with a barrier: the step buffer is free
+    }
+    if (tid == 0) {
+      Hs[it] = nrm;
+      int div = 0;  // solvers.py:240-247: five increases in a row and a tenfold growth
+      if (it + 1 > 5) {
+        bool inc = true;
+        for (int i = it - 5; i < it; i++) inc &= Hs[i + 1] > Hs[i];
+        div = inc && (Hs[it] > 10.0 * Hs[it - 5]);
+      }
+      s_flag = div;
+    }
+    __syncthreads();
+    split(5);
     hlen = it + 1;
     if (nrm <= tol) {
       status = 1;
