@@ -13,7 +13,7 @@ void set_error(const char* fmt, ...);
 
 // Diagnostic switches (environment variables), read ONCE per process on
 // first use: no getenv on the solve path, and a captured graph cannot disagree with later calls.
-enum EnvSwitch { ENV_TALL, ENV_KRON2, ENV_RICHARDSON, ENV_NO_EIGBASIS, ENV_GRAM_SCALAR, ENV_GATHER_BLOCKS, ENV_TSQR, ENV_JACOBI_FP32, ENV_JACOBI_GENERIC, ENV_RICH_OLD, ENV_NO_DEFLATE, ENV_COUNT };
+enum EnvSwitch { ENV_TALL, ENV_KRON2, ENV_RICHARDSON, ENV_NO_EIGBASIS, ENV_GRAM_SCALAR, ENV_GATHER_BLOCKS, ENV_TSQR, ENV_JACOBI_FP32, ENV_JACOBI_GENERIC, ENV_RICH_OLD, ENV_NO_DEFLATE, ENV_NO_OA, ENV_COUNT };
 const char* env(EnvSwitch id);
 int cuda_status(cudaError_t e, const char* what);
 
@@ -80,6 +80,27 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
   if (wid == 0) {
     t = lane < nw ? red[lane] : 0.0;
     t = warp_sum(t);
+    if (lane == 0) red[0] = t;
+  }
+  __syncthreads();
+  t = red[0];
+  __syncthreads();
+  return t;
+}
+
+// Block-wide maximum (same pattern as block_sum).
+__device__ __forceinline__ double block_max(double v, double* red) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  __syncthreads();
+  if (lane == 0) red[wid] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (wid == 0) {
+    t = lane < nw ? red[lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t = fmax(t, __shfl_xor_sync(0xffffffffu, t, o));
     if (lane == 0) red[0] = t;
   }
   __syncthreads();

@@ -258,6 +258,39 @@ __device__ __forceinline__ void smem_gemm_rows(LA a, LB b, Out out) {
   for (int q = 0; q < NJ; q++) out(i, j0 + q, c[q]);
 }
 
+// C = A B for D x D operands in shared memory, TM x TN register blocks per thread (D = 64: 4 x 4,
+// half the shared-memory instructions per FMA of smem_gemm_rows).  Thread (ib, jb) owns rows
+// ib TM + r and columns jb + c (D / TN): consecutive lanes read consecutive columns of B (b(k, j)
+// must be contiguous in j) and share their rows of A (broadcast reads).
+template <int D, class LA, class LB, class Out>
+__device__ __forceinline__ void smem_gemm_blk(LA a, LB b, Out out) {
+  constexpr int NT = D / 2 * JF_G, PER = D * D / NT;
+  constexpr int TM = D >= 64 ? 4 : 2, TN = PER / TM, NJB = D / TN;
+  static_assert(TM * TN == PER && (D / TM) * NJB == NT, "gemm blocking");
+  const int jb = threadIdx.x % NJB, ib = threadIdx.x / NJB;
+  double c[TM][TN];
+#pragma unroll
+  for (int r = 0; r < TM; r++)
+#pragma unroll
+    for (int q = 0; q < TN; q++) c[r][q] = 0.0;
+#pragma unroll 4
+  for (int k = 0; k < D; k++) {
+    double av[TM], bv[TN];
+#pragma unroll
+    for (int r = 0; r < TM; r++) av[r] = a(ib * TM + r, k);
+#pragma unroll
+    for (int q = 0; q < TN; q++) bv[q] = b(k, jb + q * NJB);
+#pragma unroll
+    for (int r = 0; r < TM; r++)
+#pragma unroll
+      for (int q = 0; q < TN; q++) c[r][q] = fma(av[r], bv[q], c[r][q]);
+  }
+#pragma unroll
+  for (int r = 0; r < TM; r++)
+#pragma unroll
+    for (int q = 0; q < TN; q++) out(ib * TM + r, jb + q * NJB, c[r][q]);
+}
+
 // FP32 prelude of the symmetric (Gram) eigensolve: `sweeps32` one-sided Jacobi sweeps in single
 // precision (cheaper rounds: 32-bit shuffles, 4-cycle FMAs, MUFU rsqrt), then the accumulated
 // rotations are re-orthonormalised in FP64 by two Newton-Schulz steps V <- V (3I - V^T V) / 2 and
@@ -266,7 +299,7 @@ __device__ __forceinline__ void smem_gemm_rows(LA a, LB b, Out out) {
 // same FP64 accuracy (the FP64 phase alone decides convergence).
 template <int D>
 __device__ void jacobi_fp32_prelude(const double* __restrict__ M, double* W, double* V, float* W32, float* V32,
-                                    int sweeps32) {
+                                    int sweeps32, bool want_w) {
   constexpr int NP = D / 2, NT = NP * JF_G, E = D / JF_G;
   __shared__ int s_rot32;
   const int tid = threadIdx.x;
@@ -351,16 +384,17 @@ __device__ void jacobi_fp32_prelude(const double* __restrict__ M, double* W, dou
     }
     __syncthreads();
     // Y = C = 1.5 I - 0.5 V^T V: (V^T V)(i, j) = sum_k V(k, i) V(k, j) = sum_k X[k LT + i] X[k LT + j]
-    smem_gemm_rows<D>([&](int i, int k) { return X[k * LT + i]; }, [&](int k, int j) { return X[k * LT + j]; },
-                      [&](int i, int j, double v) { Y[i * D + j] = (i == j ? 1.5 : 0.0) - 0.5 * v; });
+    smem_gemm_blk<D>([&](int i, int k) { return X[k * LT + i]; }, [&](int k, int j) { return X[k * LT + j]; },
+                     [&](int i, int j, double v) { Y[i * D + j] = (i == j ? 1.5 : 0.0) - 0.5 * v; });
     __syncthreads();
     // X = V C (jf layout), then V = X
-    smem_gemm_rows<D>([&](int i, int k) { return V[k * LD + i]; }, [&](int k, int j) { return Y[k * D + j]; },
-                      [&](int i, int j, double v) { X[j * LD + i] = v; });
+    smem_gemm_blk<D>([&](int i, int k) { return V[k * LD + i]; }, [&](int k, int j) { return Y[k * D + j]; },
+                     [&](int i, int j, double v) { X[j * LD + i] = v; });
     __syncthreads();
     for (int e = tid; e < D * LD; e += NT) V[e] = X[e];
     __syncthreads();
   }
+  if (!want_w) return;  // the refinement forms G V itself
   // Y = G (symmetrised, row-major), then W = G V
   for (int e = tid; e < D * D; e += NT) {
     const int i = e / D, k = e % D;
@@ -435,11 +469,95 @@ __device__ double jacobi_deflate(double* G, double* u, double* v, double* w, dou
   return beta;
 }
 
+// Iterative refinement of an approximate eigenbasis of a symmetric G (Ogita & Aishima 2018,
+// "Iterative refinement for symmetric eigenvalue decomposition"), replacing the FP64 Jacobi
+// sweeps after the FP32 prelude.  With R = I - V^T V and S = V^T G V, the Rayleigh quotients
+// lam_i = S_ii / (1 - R_ii) and the correction E_ij = (S_ij + lam_j R_ij) / (lam_j - lam_i)
+// (i != j), E_ii = R_ii / 2 give V <- V + V E; the error (departure from orthonormality and from
+// the eigenbasis) squares every iteration, so an FP32-accurate start converges in 2-3 steps of
+// four D x D products, against three FP64 sweeps of 63 shared-memory-bound rounds.  Pairs whose
+// Rayleigh quotients are too close to be separated at the current accuracy (|E_ij| would exceed
+// 0.25) get only the orthogonality correction E_ij = R_ij / 2, as in the paper's clustered case.
+// Returns the iterations used; on exit W = G V.  Shared memory: G (row-major D x D, symmetric),
+// W / V (jf layout), scratch X, Y, S (D x (D + 8) doubles each), lam (D).
+template <int D>
+__device__ int jacobi_oa_refine(const double* G, double* W, double* V, double* X, double* Y, double* S,
+                                double* lam, double* red) {
+  constexpr int NT = D / 2 * JF_G, LD = D + 8, LT = D + 2;
+  const int tid = threadIdx.x;
+  double* Wr = W;  // G V row-major during the iterations (jf layout again on exit)
+  // X = V row-major; Wr = G V (G symmetric: G(i, k) read as G[k D + i])
+  for (int e = tid; e < D * D; e += NT) {
+    const int i = e / D, k = e % D;
+    X[k * LT + i] = V[i * LD + k];
+  }
+  __syncthreads();
+  smem_gemm_blk<D>([&](int i, int k) { return G[k * D + i]; }, [&](int k, int j) { return X[k * LT + j]; },
+                   [&](int i, int j, double v) { Wr[i * LT + j] = v; });
+  __syncthreads();
+  int it = 0;
+  for (; it < 8; it++) {
+    // Y = R = I - V^T V; S = V^T W; lam_i = S_ii / (1 - R_ii)
+    smem_gemm_blk<D>([&](int i, int k) { return X[k * LT + i]; }, [&](int k, int j) { return X[k * LT + j]; },
+                     [&](int i, int j, double v) { Y[i * LT + j] = (i == j ? 1.0 : 0.0) - v; });
+    smem_gemm_blk<D>([&](int i, int k) { return X[k * LT + i]; }, [&](int k, int j) { return Wr[k * LT + j]; },
+                     [&](int i, int j, double v) { S[i * LT + j] = v; });
+    __syncthreads();
+    for (int i = tid; i < D; i += NT) lam[i] = S[i * LT + i] / (1.0 - Y[i * LT + i]);
+    __syncthreads();
+    // E in place of R; S symmetrised (its rounding is not: an asymmetric S would leave
+    // E + E^T != R and stall the orthogonality at ~eps ||G|| / gap)
+    double emax = 0.0;
+    for (int e = tid; e < D * D; e += NT) {
+      const int i = e / D, j = e % D;
+      const double rij = Y[i * LT + j];
+      double ev;
+      if (i == j) {
+        ev = 0.5 * rij;
+      } else {
+        const double sij = 0.5 * (S[i * LT + j] + S[j * LT + i]);
+        const double num = fma(lam[j], rij, sij), gap = lam[j] - lam[i];
+        ev = fabs(num) < 0.25 * fabs(gap) ? num / gap : 0.5 * rij;
+        emax = fmax(emax, fabs(ev));
+      }
+      Y[i * LT + j] = ev;
+    }
+    __syncthreads();
+    // X = V + V E (row-major), then V (jf) from it, then Wr = G V
+    smem_gemm_blk<D>([&](int i, int k) { return V[k * LD + i]; }, [&](int k, int j) { return Y[k * LT + j]; },
+                     [&](int i, int j, double v) { X[i * LT + j] = V[j * LD + i] + v; });
+    __syncthreads();
+    for (int e = tid; e < D * D; e += NT) {
+      const int j = e / D, i = e % D;
+      V[j * LD + i] = X[i * LT + j];
+    }
+    smem_gemm_blk<D>([&](int i, int k) { return G[k * D + i]; }, [&](int k, int j) { return X[k * LT + j]; },
+                     [&](int i, int j, double v) { Wr[i * LT + j] = v; });
+    emax = block_max(emax, red);  // ends with a barrier
+    if (emax <= 1e-8) {  // the update just applied was <= 1e-8: the remaining error is ~1e-16 / gap
+      it++;
+      break;
+    }
+  }
+  // W back to the jf layout
+  for (int e = tid; e < D * D; e += NT) {
+    const int i = e / D, j = e % D;
+    Y[i * LT + j] = Wr[i * LT + j];
+  }
+  __syncthreads();
+  for (int e = tid; e < D * D; e += NT) {
+    const int j = e / D, i = e % D;
+    W[j * LD + i] = Y[i * LT + j];
+  }
+  __syncthreads();
+  return it;
+}
+
 template <int D, bool SYM>
 __global__ void __launch_bounds__(D / 2 * JF_G) jacobi_fixed_kernel(MatPtrs Ms, const double* __restrict__ Mc,
                                                                    double* __restrict__ sigma,
                                                                    double* __restrict__ Vout, int sweeps32,
-                                                                   int deflate) {
+                                                                   int deflate, int refine) {
   constexpr int NP = D / 2, NT = NP * JF_G, E = D / JF_G;
   extern __shared__ double jf_sm[];
   double* W = jf_sm;
@@ -463,7 +581,12 @@ __global__ void __launch_bounds__(D / 2 * JF_G) jacobi_fixed_kernel(MatPtrs Ms, 
     __syncthreads();
     if (deflate) beta = jacobi_deflate<D>(Gs, s_u, s_v, s_w, s_red);
     float* W32 = reinterpret_cast<float*>(jf_sm + 2 * D * (D + 8));
-    jacobi_fp32_prelude<D>(Gs, W, V, W32, W32 + D * (D + 8), sweeps32);
+    jacobi_fp32_prelude<D>(Gs, W, V, W32, W32 + D * (D + 8), sweeps32, !refine);
+    if (refine) {
+      double* X = jf_sm + 2 * D * (D + 8);
+      const int its = jacobi_oa_refine<D>(Gs, W, V, X, X + D * (D + 8), Gs + D * D, s_w, s_red);
+      if (tid == 0) g_jacobi_sweeps[blockIdx.x & 7] = 100 + its;
+    }
   } else {
     for (int e = tid; e < D * D; e += NT) {
       const int i = e / D, j = e % D;  // M row i, column j
@@ -480,7 +603,8 @@ __global__ void __launch_bounds__(D / 2 * JF_G) jacobi_fixed_kernel(MatPtrs Ms, 
   // sweep is skipped (measured at d = 64: cosines 2e-5, 1e-9, then none above tol)
   constexpr double MU2_DONE = 1e-18;
   __shared__ int s_big;
-  for (int sweep = 0; sweep < 40; sweep++) {
+  const int fp64_sweeps = (SYM && sweeps32 > 0 && refine) ? 0 : 40;
+  for (int sweep = 0; sweep < fp64_sweeps; sweep++) {
     if (tid == 0) {
       s_rot = 0;
       s_big = 0;
@@ -750,17 +874,19 @@ int qr_r(cudaStream_t st, const double* A, int64_t n, int d, double* R) {
 template <int D, bool SYM>
 static void launch_jacobi_fixed(cudaStream_t st, const MatPtrs& Ms, const double* M, double* sigma, double* V,
                                 int batch) {
-  // symmetric (Gram) problems: FP32 prelude sweeps (KS_JACOBI_FP32=<n>, default 5; 0 = off)
+  // symmetric (Gram) problems: FP32 prelude sweeps (KS_JACOBI_FP32=<n>, default 6; 0 = off)
   int sweeps32 = 0;
   if (SYM) {
     const char* e = ks::env(ks::ENV_JACOBI_FP32);
-    sweeps32 = e ? atoi(e) : 5;
+    sweeps32 = e ? atoi(e) : 6;
   }
   // symmetric problems with the FP32 prelude also hold the Gram matrix (D x D) for the deflation
-  const int smem = ((sweeps32 > 0 ? 4 : 2) * D * (D + 8) + (sweeps32 > 0 ? D * D : 0)) * (int)sizeof(double);
+  // plus S (D x (D + 8)) for the refinement
+  const int smem = ((sweeps32 > 0 ? 5 : 2) * D * (D + 8) + (sweeps32 > 0 ? D * D : 0)) * (int)sizeof(double);
   const int deflate = SYM && !ks::env(ks::ENV_NO_DEFLATE);
+  const int refine = SYM && !ks::env(ks::ENV_NO_OA);
   cudaFuncSetAttribute(jacobi_fixed_kernel<D, SYM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  jacobi_fixed_kernel<D, SYM><<<batch, D / 2 * JF_G, smem, st>>>(Ms, M, sigma, V, sweeps32, deflate);
+  jacobi_fixed_kernel<D, SYM><<<batch, D / 2 * JF_G, smem, st>>>(Ms, M, sigma, V, sweeps32, deflate, refine);
 }
 
 
