@@ -460,6 +460,241 @@ __global__ void reduce_cols_kernel(const double* __restrict__ part, int64_t npar
   out[e] = s + c;
 }
 
+
+// ---- two-factor sketch by left-row buckets --------------------------------------------------
+// The same outputs as the sort path (ravel, stable radix sort of the flat indices, run heads,
+// scans, seg_sqrt_group2) from a counting sort on the left row: draws are counted and scattered
+// into left-row buckets (atomics: arbitrary order inside a bucket), each bucket is sorted by
+// (right row, draw index) -- i.e. into the stable order of the flat sort -- and reduced into its
+// unique entries by one warp, and two block scans place the entries.  Six small launches instead
+// of ~20 (c3: 86 -> 44 us in a graph, tools/bench_sketch.py).
+constexpr int BK_T = 1024;  // threads of the single-block scans
+
+__global__ void bk_count_kernel(const int64_t* __restrict__ idx, int64_t s, int32_t* __restrict__ cnt) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < s) atomicAdd(&cnt[idx[2 * t]], 1);
+}
+
+// exclusive scans (one block) of NS int32 arrays of n counts: out_k[0..n]; cur (optional) gets a
+// copy of out_0[0..n).  Tiles of BK_T x 8 counts: every thread loads 8 consecutive counts (two
+// 16-byte loads, all in flight), a block scan of the thread totals, the tile total carried over.
+template <int NS>
+__global__ void __launch_bounds__(BK_T) bk_scan_kernel(const int32_t* __restrict__ in0, const int32_t* __restrict__ in1,
+                                                       int64_t n, int32_t* __restrict__ out0,
+                                                       int32_t* __restrict__ out1, int32_t* __restrict__ cur) {
+  constexpr int PT = 8, TILE = BK_T * PT;
+  __shared__ int32_t wsum[NS][BK_T / 32];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  int32_t carry[NS];
+#pragma unroll
+  for (int q = 0; q < NS; q++) carry[q] = 0;
+  for (int64_t t0 = 0; t0 < n; t0 += TILE) {
+    const int64_t b = t0 + (int64_t)tid * PT;
+    int32_t v[NS][PT], inc[NS], loc[NS];
+#pragma unroll
+    for (int q = 0; q < NS; q++) {
+      const int32_t* src = q ? in1 : in0;
+      if (b + PT <= n && (((uintptr_t)(src + b)) & 15) == 0) {
+        const int4 x0 = *reinterpret_cast<const int4*>(src + b), x1 = *reinterpret_cast<const int4*>(src + b + 4);
+        v[q][0] = x0.x; v[q][1] = x0.y; v[q][2] = x0.z; v[q][3] = x0.w;
+        v[q][4] = x1.x; v[q][5] = x1.y; v[q][6] = x1.z; v[q][7] = x1.w;
+      } else {
+#pragma unroll
+        for (int k = 0; k < PT; k++) v[q][k] = b + k < n ? src[b + k] : 0;
+      }
+      loc[q] = 0;
+#pragma unroll
+      for (int k = 0; k < PT; k++) loc[q] += v[q][k];
+      inc[q] = loc[q];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t u = __shfl_up_sync(0xffffffffu, inc[q], o);
+        if (lane >= o) inc[q] += u;
+      }
+      if (lane == 31) wsum[q][wid] = inc[q];
+    }
+    __syncthreads();
+    if (wid == 0) {
+#pragma unroll
+      for (int q = 0; q < NS; q++) {
+        int32_t x = wsum[q][lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int32_t u = __shfl_up_sync(0xffffffffu, x, o);
+          if (lane >= o) x += u;
+        }
+        wsum[q][lane] = x;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < NS; q++) {
+      int32_t* out = q ? out1 : out0;
+      int32_t run = carry[q] + inc[q] - loc[q] + (wid ? wsum[q][wid - 1] : 0);
+      int32_t o[PT];
+#pragma unroll
+      for (int k = 0; k < PT; k++) {
+        o[k] = run;
+        run += v[q][k];
+      }
+      // 16-byte stores (scalar 4-byte stores from one SM throttle on the L1 store queue)
+      if (b + PT <= n && (((uintptr_t)(out + b)) & 15) == 0 && (q || !cur || (((uintptr_t)(cur + b)) & 15) == 0)) {
+        *reinterpret_cast<int4*>(out + b) = make_int4(o[0], o[1], o[2], o[3]);
+        *reinterpret_cast<int4*>(out + b + 4) = make_int4(o[4], o[5], o[6], o[7]);
+        if (q == 0 && cur) {
+          *reinterpret_cast<int4*>(cur + b) = make_int4(o[0], o[1], o[2], o[3]);
+          *reinterpret_cast<int4*>(cur + b + 4) = make_int4(o[4], o[5], o[6], o[7]);
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < PT; k++)
+          if (b + k < n) {
+            out[b + k] = o[k];
+            if (q == 0 && cur) cur[b + k] = o[k];
+          }
+      }
+      carry[q] += wsum[q][BK_T / 32 - 1];
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    out0[n] = carry[0];
+    if (NS > 1) out1[n] = carry[NS - 1];
+  }
+}
+
+__global__ void bk_scatter_kernel(const int64_t* __restrict__ idx, int64_t s, int32_t* __restrict__ cur,
+                                  int32_t* __restrict__ slot) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < s) slot[atomicAdd(&cur[idx[2 * t]], 1)] = (int32_t)t;
+}
+
+// One warp per left-row bucket: sort its draws by key (right row << 32 | draw index) -- a warp
+// bitonic sort up to 32 draws, ranks by counting beyond -- then reduce the runs of equal right
+// rows into entries (values as seg_sqrt_group2_kernel: w0^2 + pairwise sum of the others'
+// squares, in draw order), staged at the bucket's draw offset; ucnt = entries of the bucket.
+__global__ void bk_bucket_kernel(const int64_t* __restrict__ idx, const double* __restrict__ w,
+                                 const int32_t* __restrict__ off, int64_t n0, int32_t* __restrict__ slot,
+                                 int32_t* __restrict__ tmp, double* __restrict__ st_val,
+                                 int32_t* __restrict__ st_r, int32_t* __restrict__ st_first,
+                                 int32_t* __restrict__ ucnt, int32_t* __restrict__ nonempty) {
+  const int64_t l = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (l >= n0) return;
+  const int32_t b = off[l], m = off[l + 1] - b;
+  if (lane == 0) nonempty[l] = m > 0 ? 1 : 0;
+  if (m == 0) {
+    if (lane == 0) ucnt[l] = 0;
+    return;
+  }
+  auto key_of = [&](int32_t t) { return ((uint64_t)(uint32_t)idx[2 * (int64_t)t + 1] << 32) | (uint32_t)t; };
+  if (m <= 32) {
+    uint64_t k = lane < m ? key_of(slot[b + lane]) : ~0ull;
+#pragma unroll
+    for (int sz = 2; sz <= 32; sz <<= 1) {
+#pragma unroll
+      for (int j = sz >> 1; j > 0; j >>= 1) {
+        const uint64_t o = __shfl_xor_sync(0xffffffffu, k, j);
+        const bool up = (lane & sz) == 0, lower = (lane & j) == 0;
+        k = (lower == up) ? (k < o ? k : o) : (k < o ? o : k);
+      }
+    }
+    if (lane < m) slot[b + lane] = (int32_t)(uint32_t)k;
+  } else {  // rank by counting (keys are unique): O(m^2 / 32) per warp, for rare large buckets
+    for (int32_t i = lane; i < m; i += 32) {
+      const uint64_t ki = key_of(slot[b + i]);
+      int32_t r = 0;
+      for (int32_t j = 0; j < m; j++) r += key_of(slot[b + j]) < ki;
+      tmp[b + r] = (int32_t)(uint32_t)ki;
+    }
+    __syncwarp();
+    for (int32_t i = lane; i < m; i += 32) slot[b + i] = tmp[b + i];
+  }
+  __syncwarp();
+  if (m <= 32) {  // runs of equal right rows, one lane per draw: heads, entry ranks by ballot
+    const int32_t t = lane < m ? slot[b + lane] : 0;
+    const int64_t r = lane < m ? idx[2 * (int64_t)t + 1] : -1;
+    const int64_t rp = __shfl_up_sync(0xffffffffu, r, 1);
+    const bool head = lane < m && (lane == 0 || rp != r);
+    const unsigned hm = __ballot_sync(0xffffffffu, head);
+    if (head) {
+      const int32_t u = __popc(hm & ((1u << lane) - 1));
+      const unsigned later = hm & ~((2u << lane) - 1);  // heads after this one
+      const int32_t e = later ? __ffs(later) - 1 : m;
+      const double w0 = w[t];
+      double acc = __dmul_rn(w0, w0);
+      if (e - lane > 1) {
+        auto get = [&](int64_t j) {
+          const double x = w[slot[b + j]];
+          return __dmul_rn(x, x);
+        };
+        acc = acc + pw_sum_seq(get, lane + 1, e - lane - 1);
+      }
+      st_val[b + u] = __dsqrt_rn(acc);
+      st_r[b + u] = (int32_t)r;
+      st_first[b + u] = t;
+    }
+    if (lane == 0) ucnt[l] = __popc(hm);
+    return;
+  }
+  if (lane != 0) return;
+  int32_t u = 0;
+  for (int32_t i = 0; i < m;) {
+    const int32_t t0 = slot[b + i];
+    const int64_t r = idx[2 * (int64_t)t0 + 1];
+    int32_t e = i + 1;
+    while (e < m && idx[2 * (int64_t)slot[b + e] + 1] == r) e++;
+    const double w0 = w[t0];
+    double acc = __dmul_rn(w0, w0);
+    if (e - i > 1) {
+      auto get = [&](int64_t j) {
+        const double x = w[slot[b + j]];
+        return __dmul_rn(x, x);
+      };
+      acc = acc + pw_sum_seq(get, i + 1, e - i - 1);
+    }
+    st_val[b + u] = __dsqrt_rn(acc);
+    st_r[b + u] = (int32_t)r;
+    st_first[b + u] = t0;
+    u++;
+    i = e;
+  }
+  ucnt[l] = u;
+}
+
+// Final placement: entry g = uoff[l] + k of bucket l; left group u = goff[l] (non-empty buckets)
+__global__ void bk_place_kernel(const int32_t* __restrict__ off, const int32_t* __restrict__ ucnt,
+                                const int32_t* __restrict__ uoff, const int32_t* __restrict__ goff, int64_t n0,
+                                uint64_t n1, const double* __restrict__ st_val, const int32_t* __restrict__ st_r,
+                                const int32_t* __restrict__ st_first, int64_t* __restrict__ sd_idx,
+                                double* __restrict__ sd_val, int64_t* __restrict__ seg, int64_t* __restrict__ lrow,
+                                int64_t* __restrict__ rrow, int64_t* __restrict__ counts,
+                                int64_t* __restrict__ first_raw) {
+  const int64_t l = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 3;
+  const int sub = threadIdx.x & 7;
+  if (l >= n0) return;
+  const int32_t u = ucnt[l], b = off[l], g0 = uoff[l];
+  if (l == n0 - 1 && sub == 0) {
+    counts[0] = uoff[n0];
+    counts[1] = goff[n0];
+    seg[goff[n0]] = uoff[n0];
+  }
+  if (u == 0) return;
+  if (sub == 0) {
+    seg[goff[l]] = g0;
+    lrow[goff[l]] = l;
+  }
+  for (int32_t k = sub; k < u; k += 8) {
+    const int64_t g = g0 + k;
+    const int64_t r = st_r[b + k];
+    sd_idx[g] = (int64_t)((uint64_t)l * n1 + (uint64_t)r);
+    sd_val[g] = st_val[b + k];
+    rrow[g] = r;
+    if (first_raw) first_raw[g] = st_first[b + k];
+  }
+}
+
+
 }  // namespace
 
 namespace ks {
@@ -561,6 +796,35 @@ extern "C" int ks_sketch_diag_grouped2_ex(const int64_t* idx, const int64_t* row
   rs.v[1] = row_shape[1];
   const uint64_t n1 = (uint64_t)row_shape[1];
   const uint64_t rows = (uint64_t)row_shape[0] * n1;
+  const int64_t n0 = row_shape[0];
+  if (!ks::env(ks::ENV_SKETCH_SORT) && n0 >= 1 && n0 <= (1 << 24) && n1 <= (1ull << 31) && s < (1ll << 31) &&
+      s <= 64 * n0) {
+    // left-row buckets (at most 64 draws per left row on average: the warps' sorts stay short)
+    int64_t* dcounts_b = counts_dev;
+    ks::Scratch<int64_t> dcb(counts_dev ? 0 : 2, st);
+    if (!dcounts_b) dcounts_b = dcb.p;
+    ks::Scratch<int32_t> cnt(n0 + 1, st), off(n0 + 1, st), cur(n0 + 1, st), slot(s, st), tmp(s, st), sr(s, st),
+        sf(s, st), ucnt(n0 + 1, st), uoff(n0 + 1, st), ne(n0 + 1, st), goff(n0 + 1, st);
+    ks::Scratch<double> sv(s, st);
+    KS_REQUIRE(dcounts_b && cnt.p && off.p && cur.p && slot.p && tmp.p && sr.p && sf.p && ucnt.p && uoff.p && ne.p &&
+                   goff.p && sv.p,
+               KS_ECUDA, "scratch allocation failed");
+    KS_TRY_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int32_t) * (size_t)n0, st));
+    bk_count_kernel<<<ceil_div_u(s, 256), 256, 0, st>>>(idx, s, cnt.p);
+    bk_scan_kernel<1><<<1, BK_T, 0, st>>>(cnt.p, nullptr, n0, off.p, nullptr, cur.p);
+    bk_scatter_kernel<<<ceil_div_u(s, 256), 256, 0, st>>>(idx, s, cur.p, slot.p);
+    bk_bucket_kernel<<<ceil_div_u(n0 * 32, 256), 256, 0, st>>>(idx, w, off.p, n0, slot.p, tmp.p, sv.p, sr.p, sf.p,
+                                                               ucnt.p, ne.p);
+    bk_scan_kernel<2><<<1, BK_T, 0, st>>>(ucnt.p, ne.p, n0, uoff.p, goff.p, nullptr);
+    bk_place_kernel<<<ceil_div_u(n0 * 8, 256), 256, 0, st>>>(off.p, ucnt.p, uoff.p, goff.p, n0, n1, sv.p, sr.p, sf.p,
+                                                             sd_idx, sd_val, seg, lrow, rrow, dcounts_b, first_raw);
+    KS_CHECK_LAUNCH();
+    if (counts) {
+      KS_TRY_CUDA(cudaMemcpyAsync(counts, dcounts_b, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+      KS_TRY_CUDA(cudaStreamSynchronize(st));
+    }
+    return KS_OK;
+  }
   int bits = 0;
   while (bits < 64 && ((rows - 1) >> bits) != 0) bits++;
   ks::Scratch<uint64_t> keys(s, st);
