@@ -142,7 +142,7 @@ int gemm_tn_tall_dmma(cudaStream_t st, int64_t M, int64_t N, int64_t K, double a
 namespace {
 
 constexpr int JP_CPW = 2;  // right-hand-side columns per warp and pass
-constexpr int JP_COLS = 16 * JP_CPW;  // columns per CTA (512 threads)
+constexpr int JP_COLS = 16 * JP_CPW;  // columns per CTA with 512 threads (factor + solve launches)
 
 __device__ unsigned long long g_jlp_ts[4];  // globaltimer stamps of CTA 0 (debug)
 __device__ __forceinline__ unsigned long long jlp_now() {
@@ -174,7 +174,13 @@ __global__ void __launch_bounds__(512) jl_projection_kernel(const double* __rest
     if (d <= 64)
       for (int e = tid; e < d; e += nt) ks_cp_async8(&s_rdiag[e], Lg + (size_t)d * ld + e);
   }
-  if (mode != 1) {
+  if (mode == 2 && d <= 64) {  // this CTA's right-hand-side columns only
+    const int cpc = nty * JP_CPW, c_lo = blockIdx.x * cpc, nc = min(r, c_lo + cpc) - c_lo;
+    for (int e = tid; e < d * nc; e += nt) {
+      const int c = c_lo + e / d, k = e % d;
+      ks_cp_async8(&Y[k * r + c], GA + (size_t)c * d + k);
+    }
+  } else if (mode != 1) {
     for (int e = tid; e < d * r; e += nt) {
       const int k = e / r, c = e - k * r;
       ks_cp_async8(&Y[e], GA + (size_t)c * d + k);
@@ -278,9 +284,10 @@ __global__ void __launch_bounds__(512) jl_projection_kernel(const double* __rest
   // L Z = Y, then L^T X = Z.  Right-hand-side columns are independent: for d <= 64 a warp solves
   // JP_CPW columns at once with the column in registers (lane l owns rows l and l + 32); the
   // per-element operation order is the textbook one (divide by the pivot, then fma updates).
-  if (d <= 64 && nt == 512) {
+  if (d <= 64 && (nt == 512 || mode == 2)) {
     const int lane = tx, warp = ty;
-    const int c_lo = blockIdx.x * JP_COLS, c_hi = min(r, c_lo + JP_COLS);
+    const int cpc = nty * JP_CPW;  // columns per CTA
+    const int c_lo = blockIdx.x * cpc, c_hi = min(r, c_lo + cpc);
     for (int c0 = c_lo + warp; c0 < c_hi; c0 += nty * JP_CPW) {
       double y0[JP_CPW], y1[JP_CPW];
 #pragma unroll
@@ -375,9 +382,12 @@ extern "C" int ks_jl_solve(const double* Lws, int32_t d, const double* GA, int32
   const size_t smem = sizeof(double) * ((size_t)d * (d + 1) + (size_t)d * r);
   KS_REQUIRE(d >= 1 && r >= 1 && smem <= 220 * 1024, KS_ESIZE, "jl_solve: d=%d r=%d too large", d, r);
   KS_TRY_CUDA(cudaFuncSetAttribute(jl_projection_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-  const unsigned grid = d <= 64 ? ceil_div_u(r, JP_COLS) : 1;
-  jl_projection_kernel<<<grid, 512, smem, (cudaStream_t)stream>>>(nullptr, d, GA, r, scale, Q, nullptr, (double*)Lws,
-                                                                   2);
+  // solve only: 4 warps per CTA, JP_CPW columns per warp, ~r / 8 CTAs (the triangular solves are
+  // sequential in d per column: spread the columns over SMs)
+  const int nthr = d <= 64 ? 128 : 512;
+  const unsigned grid = d <= 64 ? ceil_div_u(r, (nthr / 32) * JP_CPW) : 1;
+  jl_projection_kernel<<<grid, nthr, smem, (cudaStream_t)stream>>>(nullptr, d, GA, r, scale, Q, nullptr, (double*)Lws,
+                                                                    2);
   KS_CHECK_LAUNCH();
   return KS_OK;
 }
