@@ -592,6 +592,7 @@ def _eig_on(stream, g, tl=None, name=""):
     d = int(g.shape[0])
     w = D.empty(1, d)
     v = D.empty(1, d, d)
+    _tl_event(tl, name + " start", stream)
     with torch.cuda.stream(stream):
         _lib.call("ks_sym_eig_batched", 1, _lib.ptr_array(ctypes.c_void_p, [g.data_ptr()]), d, D.p(w), D.p(v),
                   D.stream())
