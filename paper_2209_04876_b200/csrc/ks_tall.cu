@@ -90,6 +90,113 @@ __global__ void reduce_parts_warp_kernel(const double* __restrict__ part, int64_
   if (lane == 0) out[e] = alpha * s;
 }
 
+// Second version for the aligned shapes of the solve (Grams of d = 16..128 factors, the JL
+// product G A~ with r <= 80): 16-byte cp.async staging (k-fast A stored [m][k], m-fast A stored
+// [k][m], n-fast B stored [k][n]), two-slab double buffering (the next slab's loads in flight
+// while the current one's DMMAs run), TK2 = 16 k-rows per slab so that all SMs get a K-range.
+constexpr int TK2 = 16;
+__device__ __forceinline__ void cp16(void* dst, const void* src, bool valid) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  const int n = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(n) : "memory");
+}
+
+template <int MP, int NP, bool AK>
+__global__ void __launch_bounds__(TT) tall_tn2_kernel(int M, int N, int64_t K, int64_t chunk,
+                                                      const double* __restrict__ A, int64_t a_ld,
+                                                      const double* __restrict__ B, int64_t b_ld,
+                                                      double* __restrict__ part) {
+  constexpr int LDK = TK2 + 4;               // A stored [m][k] (AK)
+  constexpr int LDA = MP + 4, LDB = NP + 4;  // A stored [k][m]; B stored [k][n]
+  constexpr int ASZ = AK ? MP * LDK : TK2 * LDA, BSZ = TK2 * LDB;
+  constexpr int TILES = (MP / 16) * (NP / 8);
+  constexpr int PER_W = (TILES + TW - 1) / TW;
+  extern __shared__ __align__(16) double tsm2[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t4 = lane & 3;
+  const int64_t kbeg = (int64_t)blockIdx.x * chunk;
+  const int64_t kend = ks_min64(K, kbeg + chunk);
+  const int nslab = (int)((kend - kbeg + TK2 - 1) / TK2);
+  auto stage = [&](int sl, int buf) {
+    double* As = tsm2 + buf * (ASZ + BSZ);
+    double* Bs = As + ASZ;
+    const int64_t k0 = kbeg + (int64_t)sl * TK2;
+    if (AK) {  // A(m, k) = A[m a_ld + k]: pairs along k
+      for (int e = tid; e < MP * (TK2 / 2); e += TT) {
+        const int mm = e / (TK2 / 2), kk = 2 * (e % (TK2 / 2));
+        const int64_t gk = k0 + kk;
+        const bool ok = gk < kend && mm < M;  // K-ranges end on even k (host: K even)
+        cp16(&As[mm * LDK + kk], ok ? A + (int64_t)mm * a_ld + gk : A, ok);
+      }
+    } else {  // A(m, k) = A[k a_ld + m]: pairs along m
+      for (int e = tid; e < TK2 * (MP / 2); e += TT) {
+        const int kk = e / (MP / 2), mm = 2 * (e % (MP / 2));
+        const int64_t gk = k0 + kk;
+        const bool ok = gk < kend && mm < M;  // M even (host)
+        cp16(&As[kk * LDA + mm], ok ? A + gk * a_ld + mm : A, ok);
+      }
+    }
+    for (int e = tid; e < TK2 * (NP / 2); e += TT) {  // B(k, n) = B[k b_ld + n]: pairs along n
+      const int kk = e / (NP / 2), nn = 2 * (e % (NP / 2));
+      const int64_t gk = k0 + kk;
+      const bool ok = gk < kend && nn < N;  // N even (host)
+      cp16(&Bs[kk * LDB + nn], ok ? B + gk * b_ld + nn : B, ok);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  double acc[PER_W][4];
+#pragma unroll
+  for (int i = 0; i < PER_W; i++) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.0;
+  if (nslab > 0) stage(0, 0);
+  for (int sl = 0; sl < nslab; sl++) {
+    if (sl + 1 < nslab) {
+      stage(sl + 1, (sl + 1) & 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    const double* As = tsm2 + (sl & 1) * (ASZ + BSZ);
+    const double* Bs = As + ASZ;
+#pragma unroll
+    for (int i = 0; i < PER_W; i++) {
+      const int tile = warp + i * TW;
+      if (tile < TILES) {
+        const int m0 = (tile / (NP / 8)) * 16, n0 = (tile % (NP / 8)) * 8;
+#pragma unroll
+        for (int kk = 0; kk < TK2; kk += 4) {
+          const double a0 = AK ? As[(m0 + g) * LDK + kk + t4] : As[(kk + t4) * LDA + m0 + g];
+          const double a1 = AK ? As[(m0 + g + 8) * LDK + kk + t4] : As[(kk + t4) * LDA + m0 + g + 8];
+          const double b0 = Bs[(kk + t4) * LDB + n0 + g];
+          dmma_16x8x4(acc[i], a0, a1, b0);
+        }
+      }
+    }
+    __syncthreads();  // the buffer is restaged two slabs later
+  }
+  double* out = part + (int64_t)blockIdx.x * M * N;
+#pragma unroll
+  for (int i = 0; i < PER_W; i++) {
+    const int tile = warp + i * TW;
+    if (tile < TILES) {
+      const int m0 = (tile / (NP / 8)) * 16, n0 = (tile % (NP / 8)) * 8;
+      const int r0 = m0 + g, c0 = n0 + 2 * t4;
+      if (r0 < M && c0 < N) out[r0 * N + c0] = acc[i][0];
+      if (r0 < M && c0 + 1 < N) out[r0 * N + c0 + 1] = acc[i][1];
+      if (r0 + 8 < M && c0 < N) out[(r0 + 8) * N + c0] = acc[i][2];
+      if (r0 + 8 < M && c0 + 1 < N) out[(r0 + 8) * N + c0 + 1] = acc[i][3];
+    }
+  }
+}
+
+template <int MP, int NP, bool AK>
+void launch_tall2(cudaStream_t st, int nparts, int M, int N, int64_t K, int64_t chunk, const double* A, int64_t a_ld,
+                  const double* B, int64_t b_ld, double* part) {
+  constexpr int ASZ = AK ? MP * (TK2 + 4) : TK2 * (MP + 4), BSZ = TK2 * (NP + 4);
+  const size_t smem = sizeof(double) * 2 * (ASZ + BSZ);
+  cudaFuncSetAttribute(tall_tn2_kernel<MP, NP, AK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  tall_tn2_kernel<MP, NP, AK><<<nparts, TT, smem, st>>>(M, N, K, chunk, A, a_ld, B, b_ld, part);
+}
+
 template <int MP, int NP>
 void launch_tall(cudaStream_t st, int nparts, int M, int N, int64_t K, int64_t chunk, const double* A, int64_t a_ks,
                  int64_t a_ms, const double* B, int64_t b_ks, int64_t b_ns, double* part) {
@@ -104,6 +211,41 @@ namespace ks {
 
 int gemm_tn_tall_dmma(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
                       int64_t a_ks, int64_t a_ms, const double* B, int64_t b_ks, int64_t b_ns, double* C) {
+  // the 16-byte / double-buffered kernel for aligned shapes: B n-fast, A k-fast or m-fast, even
+  // M / N / K and leading dimensions, 16-byte aligned operands
+  const bool akf = a_ks == 1, amf = a_ms == 1;
+  const int64_t a_ld = akf ? a_ms : a_ks;
+  const bool aligned = (((uintptr_t)A | (uintptr_t)B) & 15) == 0;
+  if (!ks::env(ks::ENV_TALL_OLD) && aligned && b_ns == 1 && (b_ks & 1) == 0 && (akf || amf) && (a_ld & 1) == 0 &&
+      (M & 1) == 0 && (N & 1) == 0 && (K & 1) == 0 && M <= 128 && N <= 128 && K >= 2 * TK2) {
+    const int mp2 = M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : M <= 80 ? 80 : 128;
+    const int np2 = N <= 16 ? 16 : N <= 32 ? 32 : N <= 64 ? 64 : 128;
+    const int64_t cap2 = num_sms();
+    int64_t chunk2 = (K + cap2 - 1) / cap2;
+    chunk2 = (chunk2 + TK2 - 1) / TK2 * TK2;
+    const int64_t nparts2 = (K + chunk2 - 1) / chunk2;
+    Scratch<double> part2(nparts2 * M * N, st);
+    KS_REQUIRE(part2.p, KS_ECUDA, "scratch allocation failed");
+    const int np2_i = (int)nparts2;
+    bool done = false;
+#define KS_TALL2(MM, NN)                                                                                         \
+  if (!done && mp2 == MM && np2 == NN) {                                                                         \
+    if (akf) launch_tall2<MM, NN, true>(st, np2_i, (int)M, (int)N, K, chunk2, A, a_ld, B, b_ks, part2.p);        \
+    else launch_tall2<MM, NN, false>(st, np2_i, (int)M, (int)N, K, chunk2, A, a_ld, B, b_ks, part2.p);           \
+    done = true;                                                                                                 \
+  }
+    KS_TALL2(16, 16) KS_TALL2(16, 32) KS_TALL2(16, 64) KS_TALL2(16, 128)
+    KS_TALL2(32, 16) KS_TALL2(32, 32) KS_TALL2(32, 64) KS_TALL2(32, 128)
+    KS_TALL2(64, 16) KS_TALL2(64, 32) KS_TALL2(64, 64) KS_TALL2(64, 128)
+    KS_TALL2(80, 16) KS_TALL2(80, 32) KS_TALL2(80, 64) KS_TALL2(80, 128)
+    KS_TALL2(128, 16) KS_TALL2(128, 32) KS_TALL2(128, 64) KS_TALL2(128, 128)
+#undef KS_TALL2
+    KS_CHECK_LAUNCH();
+    const int64_t count2 = M * N;
+    reduce_parts_warp_kernel<<<ceil_div_u(count2 * 32, 256), 256, 0, st>>>(part2.p, nparts2, count2, alpha, C);
+    KS_CHECK_LAUNCH();
+    return KS_OK;
+  }
   const int mp = M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : 128;
   const int np = N <= 16 ? 16 : N <= 32 ? 32 : N <= 64 ? 64 : 128;
   int64_t nparts = (K + 63) / 64;
