@@ -13,6 +13,7 @@
 // numerically full-rank A are the squared row norms of A R^-1; ks_leverage_scores_tall fuses the
 // product and the row norms in one pass.
 #include "ks_common.cuh"
+#include "ks_tma.cuh"
 
 namespace ks {
 int gemm_tn_tall(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t a_ks,
@@ -141,6 +142,88 @@ __global__ void __launch_bounds__(CT) tallmm_kernel(const double* __restrict__ A
   }
 }
 
+// X = A B (A n x D row-major, B D x D) on the FP64 tensor pipe: 64-row blocks of A and all of B
+// staged with 16-byte cp.async, m16n8k4 tiles (each warp one m-tile and D / 16 n-tiles), X
+// written from the fragments and / or the squared row norms (per-row partials summed in a fixed
+// order: lanes, then the two warps sharing the m-tile).
+template <int D>
+__global__ void __launch_bounds__(CT) tallmm_dmma_kernel(const double* __restrict__ A, int64_t n,
+                                                        const double* __restrict__ B, double* __restrict__ X,
+                                                        double* __restrict__ sq) {
+  constexpr int TMR = 64, LD = D + 4, NTW = D / 16;  // rows per block, smem stride, n-tiles per warp
+  extern __shared__ __align__(16) double tsmm[];
+  double* Bs = tsmm;          // D x LD
+  double* As = Bs + D * LD;   // TMR x LD
+  __shared__ double rsq[2][TMR];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t4 = lane & 3;
+  const int64_t r0 = (int64_t)blockIdx.x * TMR;
+  auto cp16 = [](void* dst, const void* src, bool ok) {
+    const unsigned dd = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dd), "l"(src), "r"(ok ? 16 : 0) : "memory");
+  };
+  for (int e = tid; e < D * (D / 2); e += CT) {
+    const int k = e / (D / 2), c = 2 * (e % (D / 2));
+    cp16(&Bs[k * LD + c], B + k * D + c, true);
+  }
+  for (int e = tid; e < TMR * (D / 2); e += CT) {
+    const int i = e / (D / 2), c = 2 * (e % (D / 2));
+    const bool ok = r0 + i < n;
+    cp16(&As[i * LD + c], ok ? A + (r0 + i) * D + c : A, ok);
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
+  const int mt = warp & 3, half = warp >> 2, m0 = mt * 16;
+  double acc[NTW][4];
+#pragma unroll
+  for (int t = 0; t < NTW; t++) acc[t][0] = acc[t][1] = acc[t][2] = acc[t][3] = 0.0;
+#pragma unroll 4
+  for (int k = 0; k < D / 4; k++) {
+    const double a0 = As[(m0 + g) * LD + 4 * k + t4], a1 = As[(m0 + g + 8) * LD + 4 * k + t4];
+#pragma unroll
+    for (int t = 0; t < NTW; t++) {
+      const int n0 = (half * NTW + t) * 8;
+      dmma_16x8x4(acc[t], a0, a1, Bs[(4 * k + t4) * LD + n0 + g]);
+    }
+  }
+  const int64_t ra = r0 + m0 + g, rb = ra + 8;
+  if (X) {
+#pragma unroll
+    for (int t = 0; t < NTW; t++) {
+      const int c = (half * NTW + t) * 8 + 2 * t4;
+      if (ra < n) *reinterpret_cast<double2*>(&X[ra * D + c]) = make_double2(acc[t][0], acc[t][1]);
+      if (rb < n) *reinterpret_cast<double2*>(&X[rb * D + c]) = make_double2(acc[t][2], acc[t][3]);
+    }
+  }
+  if (!sq) return;
+  double sa = 0.0, sb = 0.0;
+#pragma unroll
+  for (int t = 0; t < NTW; t++) {
+    sa = fma(acc[t][1], acc[t][1], fma(acc[t][0], acc[t][0], sa));
+    sb = fma(acc[t][3], acc[t][3], fma(acc[t][2], acc[t][2], sb));
+  }
+#pragma unroll
+  for (int o = 1; o < 4; o <<= 1) {
+    sa += __shfl_xor_sync(0xffffffffu, sa, o);
+    sb += __shfl_xor_sync(0xffffffffu, sb, o);
+  }
+  if (t4 == 0) {
+    rsq[half][m0 + g] = sa;
+    rsq[half][m0 + g + 8] = sb;
+  }
+  __syncthreads();
+  for (int i = tid; i < TMR; i += CT)
+    if (r0 + i < n) sq[r0 + i] = rsq[0][i] + rsq[1][i];
+}
+
+template <int D>
+int launch_tallmm_dmma(cudaStream_t st, const double* A, int64_t n, const double* B, double* X, double* sq) {
+  const size_t smem = sizeof(double) * (size_t)(D + 64) * (D + 4);
+  KS_TRY_CUDA(cudaFuncSetAttribute(tallmm_dmma_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  tallmm_dmma_kernel<D><<<ceil_div_u(n, 64), CT, smem, st>>>(A, n, B, X, sq);
+  KS_CHECK_LAUNCH();
+  return KS_OK;
+}
+
 int chol_upper(cudaStream_t st, const double* G, int d, double* R, double* Rinv, int32_t* info, int slot) {
   const size_t smem = ((size_t)d * d + (size_t)d * (d + 1) / 2 + d) * sizeof(double);
   KS_TRY_CUDA(cudaFuncSetAttribute(chol_upper_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -150,6 +233,12 @@ int chol_upper(cudaStream_t st, const double* G, int d, double* R, double* Rinv,
 }
 
 int tallmm(cudaStream_t st, const double* A, int64_t n, int d, const double* B, double* X, double* sq) {
+  if (!ks::env(ks::ENV_TALL_OLD) && (((uintptr_t)A | (uintptr_t)B | (uintptr_t)X) & 15) == 0) {
+    if (d == 16) return launch_tallmm_dmma<16>(st, A, n, B, X, sq);
+    if (d == 32) return launch_tallmm_dmma<32>(st, A, n, B, X, sq);
+    if (d == 64) return launch_tallmm_dmma<64>(st, A, n, B, X, sq);
+    if (d == 128) return launch_tallmm_dmma<128>(st, A, n, B, X, sq);
+  }
   const int tm = d > 64 ? 32 : 64;
   const size_t smem = sizeof(double) * ((size_t)d * d + 2 * (size_t)tm * (d + 1));
   KS_REQUIRE(smem <= 227 * 1024, KS_ESIZE, "tallmm: d = %d too large", d);
