@@ -142,6 +142,121 @@ __global__ void __launch_bounds__(CT) tallmm_kernel(const double* __restrict__ A
   }
 }
 
+// Upper Cholesky factor R of a d x d Gram (d = 16 TBS) and optionally R^-1, register-resident:
+// thread (bi, bj) of a 16 x 16 grid owns the TBS x TBS block (rows bi TBS.., columns bj TBS..).
+// Right-looking, one barrier per step: at step k every thread reads the published column k
+// (updated through step k-1), forms r = sqrt(a_kk) and l_ik = a_ik / r for its rows and columns,
+// applies a_ij -= l_ik l_jk to its lower-triangle entries and, if it owns column k + 1, publishes it
+// for the next step.  R^-1 by the row-oriented right-looking back substitution (one barrier per
+// row).  The same pivot test as chol_upper_kernel (info = k + 1 if pivot k <= 1e-12 max diag).
+template <int TBS>
+__global__ void __launch_bounds__(CT) chol_reg_kernel(const double* __restrict__ G, double* __restrict__ R,
+                                                     double* __restrict__ Rinv, int32_t* __restrict__ info,
+                                                     int slot) {
+  constexpr int d = 16 * TBS, LDR = d + 1;
+  extern __shared__ double rsm[];
+  double* Rs = rsm;                // d x LDR: R (upper)
+  double* colb = Rs + d * LDR;     // 2 x d: published column / X row
+  __shared__ int s_bad;
+  __shared__ double s_dmax;
+  const int tid = threadIdx.x, bi = tid >> 4, bj = tid & 15;
+  const int i0 = bi * TBS, j0 = bj * TBS;
+  double a[TBS][TBS];
+#pragma unroll
+  for (int r = 0; r < TBS; r++)
+#pragma unroll
+    for (int c = 0; c < TBS; c++) {
+      const int i = i0 + r, j = j0 + c;
+      a[r][c] = i >= j ? 0.5 * (G[i * d + j] + G[j * d + i]) : 0.0;
+    }
+  if (tid == 0) {
+    s_bad = 0;
+    double m = 0.0;
+    for (int i = 0; i < d; i++) m = fmax(m, G[i * d + i]);
+    s_dmax = m;
+  }
+  for (int e = tid; e < d * LDR; e += CT) Rs[e] = 0.0;
+  if (j0 == 0)  // column 0 published by its owners
+#pragma unroll
+    for (int r = 0; r < TBS; r++) colb[i0 + r] = a[r][0];
+  __syncthreads();
+  const double tol = 1e-12 * s_dmax;
+  for (int k = 0; k < d; k++) {
+    const double* pc = colb + (k & 1) * d;
+    const double p = pc[k];
+    if (!(p > tol) || !isfinite(p)) {
+      if (tid == 0) s_bad = k + 1;
+      break;
+    }
+    const double rr = sqrt(p), ri = 1.0 / rr;
+    double lr[TBS], lc[TBS];
+#pragma unroll
+    for (int r = 0; r < TBS; r++) lr[r] = i0 + r > k ? pc[i0 + r] * ri : 0.0;
+#pragma unroll
+    for (int c = 0; c < TBS; c++) lc[c] = j0 + c > k ? pc[j0 + c] * ri : 0.0;
+    if (bi == (k / TBS) ) {  // one row of threads writes row k of R: R[k][j] = l_jk (j > k), R[k][k] = r
+#pragma unroll
+      for (int c = 0; c < TBS; c++) {
+        const int j = j0 + c;
+        if (j > k) Rs[k * LDR + j] = lc[c];
+      }
+      if (bj == 0) Rs[k * LDR + k] = rr;
+    }
+#pragma unroll
+    for (int r = 0; r < TBS; r++)
+#pragma unroll
+      for (int c = 0; c < TBS; c++)
+        if (i0 + r >= j0 + c) a[r][c] = fma(-lr[r], lc[c], a[r][c]);
+    if (k + 1 < d && k + 1 >= j0 && k + 1 < j0 + TBS) {  // publish column k + 1 (rows >= k + 1)
+#pragma unroll
+      for (int c = 0; c < TBS; c++)
+        if (c == k + 1 - j0)
+#pragma unroll
+          for (int r = 0; r < TBS; r++)
+            if (i0 + r >= k + 1) colb[((k + 1) & 1) * d + i0 + r] = a[r][c];
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  const int bad = s_bad;
+  if (tid == 0 && info) info[slot] = bad;
+  for (int e = tid; e < d * d; e += CT) R[e] = Rs[(e / d) * LDR + (e % d)];
+  if (!Rinv || bad) return;
+  // X = R^-1 (upper), rows from the bottom: X_i = (e_i - acc_i) / R_ii, then acc_m += R_mi X_i
+  double acc[TBS][TBS];
+#pragma unroll
+  for (int r = 0; r < TBS; r++)
+#pragma unroll
+    for (int c = 0; c < TBS; c++) acc[r][c] = 0.0;
+  for (int i = d - 1; i >= 0; i--) {
+    double* xr = colb + (i & 1) * d;
+    if (bi == i / TBS) {  // the owners of row i form it
+      const int r = i - i0;
+      const double rii = Rs[i * LDR + i];
+#pragma unroll
+      for (int rr2 = 0; rr2 < TBS; rr2++)
+        if (rr2 == r)
+#pragma unroll
+          for (int c = 0; c < TBS; c++) {
+            const int j = j0 + c;
+            const double v = j >= i ? ((j == i ? 1.0 : 0.0) - acc[rr2][c]) / rii : 0.0;
+            xr[j] = v;
+            Rinv[(size_t)i * d + j] = v;
+          }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < TBS; r++) {
+      const int m = i0 + r;
+      if (m < i) {
+        const double rmi = Rs[m * LDR + i];
+#pragma unroll
+        for (int c = 0; c < TBS; c++) acc[r][c] = fma(rmi, xr[j0 + c], acc[r][c]);
+      }
+    }
+  }
+}
+
 // X = A B (A n x D row-major, B D x D) on the FP64 tensor pipe: 64-row blocks of A and all of B
 // staged with 16-byte cp.async, m16n8k4 tiles (each warp one m-tile and D / 16 n-tiles), X
 // written from the fragments and / or the squared row norms (per-row partials summed in a fixed
@@ -225,6 +340,20 @@ int launch_tallmm_dmma(cudaStream_t st, const double* A, int64_t n, const double
 }
 
 int chol_upper(cudaStream_t st, const double* G, int d, double* R, double* Rinv, int32_t* info, int slot) {
+  // register-resident factor for d = 32 / 64 (at d = 128 the 8 x 8 blocks per thread run slower
+  // than the shared-memory kernel)
+  if (!ks::env(ks::ENV_TALL_OLD) && (d == 32 || d == 64)) {
+    const size_t smem = sizeof(double) * ((size_t)d * (d + 1) + 2 * d);
+#define KS_CHOL(TB)                                                                                            \
+    if (d == 16 * TB) {                                                                                        \
+      KS_TRY_CUDA(cudaFuncSetAttribute(chol_reg_kernel<TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+      chol_reg_kernel<TB><<<1, CT, smem, st>>>(G, R, Rinv, info, slot);                                        \
+      KS_CHECK_LAUNCH();                                                                                       \
+      return KS_OK;                                                                                            \
+    }
+    KS_CHOL(2) KS_CHOL(4)
+#undef KS_CHOL
+  }
   const size_t smem = ((size_t)d * d + (size_t)d * (d + 1) / 2 + d) * sizeof(double);
   KS_TRY_CUDA(cudaFuncSetAttribute(chol_upper_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   chol_upper_kernel<<<1, CT, smem, st>>>(G, d, R, Rinv, info, slot);
