@@ -77,15 +77,24 @@ __global__ void __launch_bounds__(K1_THREADS, 1)
     if (lane == 0) {
       tma_prefetch(&tmB);
       tma_prefetch(&tmR);
-      for (int64_t i = 0, s = s0; s < s1; i++, s++) {
-        const int st = (int)(i % KS_STAGES);
-        const uint32_t ph = (uint32_t)((i / KS_STAGES) & 1) ^ 1u;
+      // ring slot, phase and (row block, k-step) advanced incrementally (no 64-bit divisions)
+      int st = 0;
+      uint32_t ph = 1u;
+      int64_t rb = s0 / nKS, kk = s0 - rb * nKS;
+      for (int64_t s = s0; s < s1; s++) {
         mbar_wait(&empty[st], ph);
         double* stage = sm + st * C::STAGE;
         mbar_arrive_expect_tx(&full[st], (uint32_t)(C::STAGE * 8));
-        const int64_t rb = s / nKS, kk = s - rb * nKS;
         tma_load_2d(stage, &tmB, (int)(kk * 16), (int)(rb * BM), &full[st]);
         tma_load_2d(stage + C::B_TILE, &tmR, (int)(kk * 16), 0, &full[st]);
+        if (++kk == nKS) {
+          kk = 0;
+          rb++;
+        }
+        if (++st == KS_STAGES) {
+          st = 0;
+          ph ^= 1u;
+        }
       }
     }
     return;
@@ -101,9 +110,11 @@ __global__ void __launch_bounds__(K1_THREADS, 1)
       for (int c = 0; c < 4; c++) acc[a][b][c] = 0.0;
 
   const int row_w = (warp & 3) * WM, col_w = (warp >> 2) * (Q / 2);
-  for (int64_t i = 0, s = s0; s < s1; i++, s++) {
-    const int st = (int)(i % KS_STAGES);
-    mbar_wait(&full[st], (uint32_t)((i / KS_STAGES) & 1));
+  int st = 0;
+  uint32_t ph = 0u;
+  int64_t rb = s0 / nKS, kk = s0 - rb * nKS;  // advanced incrementally below
+  for (int64_t s = s0; s < s1; s++) {
+    mbar_wait(&full[st], ph);
     const double* Bs = sm + st * C::STAGE;
     const double* Rs = Bs + C::B_TILE;
 #pragma unroll
@@ -123,11 +134,15 @@ __global__ void __launch_bounds__(K1_THREADS, 1)
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
-
-    const int64_t rb = s / nKS;
-    const bool seg_end = ((s + 1) % nKS == 0) || (s + 1 == s1);
+    if (++st == KS_STAGES) {
+      st = 0;
+      ph ^= 1u;
+    }
+    const bool row_end = ++kk == nKS;
+    const bool seg_end = row_end || (s + 1 == s1);
+    if (row_end) kk = 0;
     if (seg_end) {
-      // ---- epilogue: T_part = L[I]^T P_I ----
+      // ---- epilogue: T_part = L[I]^T P_I (row block rb) ----
 #pragma unroll
       for (int a = 0; a < MT; a++)
 #pragma unroll
@@ -174,6 +189,7 @@ __global__ void __launch_bounds__(K1_THREADS, 1)
       }
       named_bar_sync(1, K1_CW * 32);
     }
+    if (row_end) rb++;
   }
 }
 
@@ -314,8 +330,10 @@ __global__ void __launch_bounds__(THREADS, 1)
         tma_prefetch(&tmL);
         int64_t cur_rb = -1;
         uint32_t lphase = 0;
-        for (int64_t i = 0, s = s0; s < s1; i++, s++) {
-          const int64_t rb = s / nCB, cb = s - rb * nCB;
+        int64_t rb = s0 / nCB, cb = s0 - rb * nCB;  // advanced incrementally (no 64-bit divisions)
+        int st = 0;
+        uint32_t sph = 1u;
+        for (int64_t s = s0; s < s1; s++) {
           if (rb != cur_rb) {
             mbar_wait(lempty, lphase ^ 1u);
             lphase ^= 1u;
@@ -324,8 +342,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             for (int j = 0; j < P / 16; j++) tma_load_2d(Ls + j * BM * 16, &tmL, j * 16, (int)(rb * BM), lfull);
             cur_rb = rb;
           }
-          const int st = (int)(i % K2_STAGES);
-          mbar_wait(&empty[st], (uint32_t)((i / K2_STAGES) & 1) ^ 1u);
+          mbar_wait(&empty[st], sph);
           double* stage = sm + st * C::STAGE;
           mbar_arrive_expect_tx(&full[st], (uint32_t)(C::STAGE * 8));
 #pragma unroll
@@ -334,14 +351,24 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
           for (int j = 0; j < P / 16; j++)
             tma_load_2d(stage + C::B_TILE + j * K2_BN * 16, &tmZ, j * 16, (int)(cb * K2_BN), &full[st]);
+          if (++cb == nCB) {
+            cb = 0;
+            rb++;
+          }
+          if (++st == K2_STAGES) {
+            st = 0;
+            sph ^= 1u;
+          }
         }
       }
     } else {
       int64_t cur_rb = -1;
       uint32_t lphase = 0;
       const int row_w = warp * WM;
-      for (int64_t i = 0, s = s0; s < s1; i++, s++) {
-        const int64_t rb = s / nCB;
+      int64_t rb = s0 / nCB, cb = s0 - rb * nCB;
+      int st = 0;
+      uint32_t sph = 0u;
+      for (int64_t s = s0; s < s1; s++) {
         if (rb != cur_rb) {
           if (cur_rb >= 0) {
             __syncwarp();
@@ -351,8 +378,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           lphase ^= 1u;
           cur_rb = rb;
         }
-        const int st = (int)(i % K2_STAGES);
-        mbar_wait(&full[st], (uint32_t)((i / K2_STAGES) & 1));
+        mbar_wait(&full[st], sph);
         const double* Bs = sm + st * C::STAGE;
         const double* Zs = Bs + C::B_TILE;
         double acc[MT][NT][4];
@@ -395,6 +421,14 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[st]);
+        if (++st == K2_STAGES) {
+          st = 0;
+          sph ^= 1u;
+        }
+        if (++cb == nCB) {
+          cb = 0;
+          rb++;
+        }
       }
     }
   }
