@@ -208,6 +208,7 @@ __device__ __forceinline__ void chunk_special(const int16_t* sc, int c, int len,
 // compose launches with one; same outputs.
 constexpr int ZRX = 0;            // raw draws staged past the super-chunk (look-ahead; later draws are recomputed)
 constexpr int ZRS = ZS * ZL + ZRX;
+constexpr int ZSLOW = 256;        // listed slow-path positions per super-chunk (~1.2 % of 4096 expected)
 static_assert(ZRS % ZT == 0 && ZT == 256 && ZK <= 32, "front kernel shape");
 __global__ void __launch_bounds__(ZT) zig_front_kernel(uint64_t sh, uint64_t sl, uint64_t ih, uint64_t il,
                                                        uint64_t skip, int64_t M, int64_t limit,
@@ -256,13 +257,18 @@ __global__ void __launch_bounds__(ZT) zig_front_kernel(uint64_t sh, uint64_t sl,
     const int64_t i = q - blk_beg;
     return i < ZRS ? raw_s[i] : pcg_output(pcg_advance(state0, inc, skip + (uint64_t)q + 1));
   };
+  // the ziggurat's first test (taken ~99% of the time) for every position from the staged tables;
+  // the positions that fail it are listed and evaluated afterwards by whole warps (inline, ~27 %
+  // of the warps would carry one lane through the long branch)
+  __shared__ int s_nslow;
+  __shared__ int s_slow[ZSLOW];
+  if (tid == 0) s_nslow = 0;
+  __syncthreads();
 #pragma unroll 4
   for (int i = tid; i < ZS * ZL; i += ZT) {
     const int64_t p = blk_beg + i;
     int16_t c16 = 1;  // positions >= M read as 1 (as the staged chunk walks do)
     if (p < M) {
-      // the ziggurat's first test (taken ~99% of the time) from the staged tables; the other
-      // branches through the full evaluation
       uint64_t r = raw_s[i];
       const int idx = (int)(r & 0xff);
       r >>= 8;
@@ -270,12 +276,32 @@ __global__ void __launch_bounds__(ZT) zig_front_kernel(uint64_t sh, uint64_t sl,
       double v = __dmul_rn((double)rabs, wi_s[idx]);
       if (r & 1) v = -v;
       if (!(rabs < ki_s[idx]) || p >= limit) {
-        const int c = zig_eval(raw, p, limit, T, &v);
-        c16 = (int16_t)(c > 32000 ? -1 : c);
+        const int slot = atomicAdd(&s_nslow, 1);
+        if (slot < ZSLOW) {
+          s_slow[slot] = i;
+          c16 = 0;  // filled in by the slow pass
+        } else {  // (list full: evaluate here)
+          const int c = zig_eval(raw, p, limit, T, &v);
+          c16 = (int16_t)(c > 32000 ? -1 : c);
+          val[p] = v;
+          cons[p] = c16;
+        }
+      } else {
+        val[p] = v;
+        cons[p] = c16;
       }
-      val[p] = v;
-      cons[p] = c16;
     }
+    sc[i] = c16;
+  }
+  __syncthreads();
+  for (int k = tid; k < min(s_nslow, ZSLOW); k += ZT) {
+    const int i = s_slow[k];
+    const int64_t p = blk_beg + i;
+    double v = 0.0;
+    const int c = zig_eval(raw, p, limit, T, &v);
+    const int16_t c16 = (int16_t)(c > 32000 ? -1 : c);
+    val[p] = v;
+    cons[p] = c16;
     sc[i] = c16;
   }
   __syncthreads();

@@ -433,10 +433,15 @@ def _spectral_rows_dev(a: torch.Tensor, eps: float, delta: float, seed, alpha: f
                        fast_scores: bool = True, divisor: float = 1.0) -> torch.Tensor:
     """w[:, None] * a[idx, :] of leverage.py:249-252 (divided by ``divisor`` afterwards, as the
     caller solvers.py:424-427 does), in one gather kernel."""
+    from .solvers import _TL_CUR, _tl_event
+    tl = _TL_CUR[0]
     sc = _statistical_scores_dev(a, fast_scores)
+    _tl_event(tl, f"spectral scores ({int(a.shape[0])})")
     p1, _ = _tables(D.to_dev(sc), renorm=False, want_cdf=False, what="score vector")
+    _tl_event(tl, "spectral tables")
     s = max(1, math.ceil(alpha * spectral_sample_count(int(a.shape[1]), eps, delta)))
     sk = sample_rows(p1, s, seed)
+    _tl_event(tl, "spectral draws")
     idx = D.to_dev(sk.indices, D.I64)
     w = D.to_dev(sk.weights)
     a = a.contiguous()
