@@ -973,7 +973,9 @@ extern "C" int ks_gather_draws2(const double* b, const int64_t* draws, int64_t n
     const char* e = ks::env(ks::ENV_GATHER_BLOCKS);  // diagnostic switch (A/B of the grid size)
     return e ? atoi(e) : 0;
   }();
-  // default: one read per thread over the whole grid (measured best beside the sketch kernels)
+  // default: one read per thread over the whole grid, all ~s reads in flight at once (measured
+  // fastest for page-locked host b, where every read is one PCIe request; KS_GATHER_BLOCKS caps
+  // the grid for A/B runs, each thread then reading GATHER_ILP entries per pass)
   int64_t nb = max_blocks > 0 ? ceil_div_u(s, 256 * GATHER_ILP) : ceil_div_u(s, 256);
   if (max_blocks > 0 && nb > max_blocks) nb = max_blocks;
   gather_draws2_kernel<<<(int)nb, 256, 0, (cudaStream_t)stream>>>(b, draws, n1, s, out);
