@@ -25,30 +25,6 @@ struct TabArgs {
   int renorm;
 };
 
-__device__ __forceinline__ int64_t block_incl_scan_i64(int64_t v, int64_t* wsum) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int64_t t = __shfl_up_sync(0xffffffffu, v, o);
-    if (lane >= o) v += t;
-  }
-  if (lane == 31) wsum[wid] = v;
-  __syncthreads();
-  if (wid == 0) {
-    int64_t t = lane < nw ? wsum[lane] : 0;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int64_t u = __shfl_up_sync(0xffffffffu, t, o);
-      if (lane >= o) t += u;
-    }
-    if (lane < nw) wsum[lane] = t;
-  }
-  __syncthreads();
-  if (wid > 0) v += wsum[wid - 1];
-  __syncthreads();
-  return v;
-}
-
 __device__ __forceinline__ double ulp_of(double x) {
   int e;
   frexp(x, &e);  // x = m 2^e, m in [0.5, 1)
@@ -58,9 +34,7 @@ __device__ __forceinline__ double ulp_of(double x) {
 __global__ void __launch_bounds__(ST_T) sampler_tables_kernel(TabArgs A) {
   __shared__ double slot[ST_T];
   __shared__ int8_t stopd[ST_T];
-  __shared__ int64_t wsum[32];
-  __shared__ double s_spec[ST_T];
-  __shared__ int s_bad, s_first;
+  __shared__ int s_bad;
   const int f = blockIdx.x, tid = threadIdx.x;
   const double* __restrict__ scores = A.scores[f];
   const int64_t n = A.n[f];
@@ -119,44 +93,68 @@ __global__ void __launch_bounds__(ST_T) sampler_tables_kernel(TabArgs A) {
   for (int64_t i = tid; i < n; i += ST_T) probs[i] = scores[i] / total;
   __syncthreads();
   if (cdf == nullptr) return;
-  // ---- exact cumsum by verified block speculation
+  // ---- exact cumsum by verified block speculation.  Three block barriers per window: the
+  // per-window shared arrays are double-buffered (window parity), every warp forms the prefix
+  // of the warp totals itself, and the verified restart value is published beside the first
+  // failure's index, so nothing is re-synchronised at the end of a window.
+  __shared__ int64_t c_wsum[2][ST_T / 32];
+  __shared__ double c_spec[2][ST_T], c_real[2][ST_T];
+  __shared__ int c_first[2];
+  const int lane = tid & 31, wid = tid >> 5;
   double prev = 0.0;
   int64_t pos = 0;
-  while (pos < n) {
+  for (int it = 0; pos < n; it++) {
+    const int buf = it & 1;
     const int64_t i = pos + tid;
     const bool valid = i < n;
     const double x = valid ? probs[i] : 0.0;
     double ref = prev;
     if (ref == 0.0) ref = probs[pos];
-    const double u = (ref > 0.0) ? ulp_of(ref) : 0x1.0p-1074;
+    // u = ulp(ref) and 1/u as exact powers of two from the exponent bits (a division by u is a
+    // multiplication by 1/u); tiny references keep the library path
+    const long long eb = (__double_as_longlong(ref) >> 52) & 0x7ff;
+    const bool fastu = ref > 0.0 && eb > 53 && eb < 2045;
+    const double u = fastu ? __longlong_as_double((eb - 52) << 52) : (ref > 0.0 ? ulp_of(ref) : 0x1.0p-1074);
+    const double iu = fastu ? __longlong_as_double((2098 - eb) << 52) : 0.0;
     long long qi = 0;
     if (valid) {
-      const double qd = x / u;
+      const double qd = fastu ? x * iu : x / u;
       qi = (qd < 0x1.0p52) ? __double2ll_rn(qd) : (1ll << 52);
     }
-    const int64_t Q = block_incl_scan_i64(qi, wsum);
-    const double base = prev / u;
-    const double spec = (double)((long long)base + Q) * u;
-    s_spec[tid] = spec;
-    if (tid == 0) s_first = ST_T;
-    __syncthreads();
-    const double sprev = (tid == 0) ? prev : s_spec[tid - 1];
-    const double real = __dadd_rn(sprev, x);
-    if (valid && real != spec) atomicMin(&s_first, tid);
-    __syncthreads();
-    const int fst = s_first;
-    if (valid && tid < fst) cdf[i] = spec;
-    if (valid && tid == fst) {
-      cdf[i] = real;
-      s_spec[tid] = real;
+    // inclusive block scan of qi: warp scan, warp totals published, each warp adds the prefix
+    long long v = qi;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long t = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += t;
     }
+    if (lane == 31) c_wsum[buf][wid] = v;
+    if (tid == 0) c_first[buf] = ST_T;
+    __syncthreads();
+    long long wt = lane < wid ? c_wsum[buf][lane] : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) wt += __shfl_xor_sync(0xffffffffu, wt, o);
+    const long long Q = v + wt;
+    const double base = fastu ? prev * iu : prev / u;
+    const double spec = (double)((long long)base + Q) * u;
+    c_spec[buf][tid] = spec;
+    __syncthreads();
+    const double sprev = (tid == 0) ? prev : c_spec[buf][tid - 1];
+    const double real = __dadd_rn(sprev, x);
+    if (valid && real != spec) {
+      c_real[buf][tid] = real;
+      atomicMin(&c_first[buf], tid);
+    }
+    __syncthreads();
+    const int fst = c_first[buf];
+    if (valid && tid < fst) cdf[i] = spec;
+    if (valid && tid == fst) cdf[i] = real;
     int64_t adv = (fst < ST_T) ? (int64_t)fst + 1 : (int64_t)ST_T;
     if (pos + adv > n) adv = n - pos;
-    __syncthreads();
-    prev = s_spec[adv - 1];
+    prev = ((int)adv - 1 == fst) ? c_real[buf][fst] : c_spec[buf][adv - 1];
     pos += adv;
-    __syncthreads();
   }
+  __syncthreads();
   if (A.renorm) {
     const double last = cdf[n - 1];
     __syncthreads();
