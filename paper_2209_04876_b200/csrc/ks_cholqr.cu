@@ -203,17 +203,18 @@ __global__ void __launch_bounds__(CT) chol_reg_kernel(const double* __restrict__
       if (bj == 0) Rs[k * LDR + k] = rr;
     }
 #pragma unroll
-    for (int r = 0; r < TBS; r++)
+    for (int r = 0; r < TBS; r++)  // (entries above the diagonal are updated too: never published)
 #pragma unroll
-      for (int c = 0; c < TBS; c++)
-        if (i0 + r >= j0 + c) a[r][c] = fma(-lr[r], lc[c], a[r][c]);
+      for (int c = 0; c < TBS; c++) a[r][c] = fma(-lr[r], lc[c], a[r][c]);
     if (k + 1 < d && k + 1 >= j0 && k + 1 < j0 + TBS) {  // publish column k + 1 (rows >= k + 1)
+      const int cc = k + 1 - j0;
 #pragma unroll
-      for (int c = 0; c < TBS; c++)
-        if (c == k + 1 - j0)
+      for (int r = 0; r < TBS; r++) {
+        double v = a[r][0];  // select column cc without indexing the register block dynamically
 #pragma unroll
-          for (int r = 0; r < TBS; r++)
-            if (i0 + r >= k + 1) colb[((k + 1) & 1) * d + i0 + r] = a[r][c];
+        for (int c = 1; c < TBS; c++) v = cc == c ? a[r][c] : v;
+        if (i0 + r >= k + 1) colb[((k + 1) & 1) * d + i0 + r] = v;
+      }
     }
     __syncthreads();
   }
@@ -234,15 +235,15 @@ __global__ void __launch_bounds__(CT) chol_reg_kernel(const double* __restrict__
       const int r = i - i0;
       const double rii = Rs[i * LDR + i];
 #pragma unroll
-      for (int rr2 = 0; rr2 < TBS; rr2++)
-        if (rr2 == r)
+      for (int c = 0; c < TBS; c++) {
+        double av = acc[0][c];  // row r of the block, selected without dynamic indexing
 #pragma unroll
-          for (int c = 0; c < TBS; c++) {
-            const int j = j0 + c;
-            const double v = j >= i ? ((j == i ? 1.0 : 0.0) - acc[rr2][c]) / rii : 0.0;
-            xr[j] = v;
-            Rinv[(size_t)i * d + j] = v;
-          }
+        for (int rr2 = 1; rr2 < TBS; rr2++) av = r == rr2 ? acc[rr2][c] : av;
+        const int j = j0 + c;
+        const double v = j >= i ? ((j == i ? 1.0 : 0.0) - av) / rii : 0.0;
+        xr[j] = v;
+        Rinv[(size_t)i * d + j] = v;
+      }
     }
     __syncthreads();
 #pragma unroll
@@ -465,3 +466,4 @@ extern "C" int ks_chol_qr2_r(const double* A, int64_t n, int32_t d, double* R, i
   *ok = good;
   return rc;
 }
+
