@@ -152,15 +152,43 @@ __global__ void __launch_bounds__(CT) tallmm_kernel(const double* __restrict__ A
 template <int TBS>
 __global__ void __launch_bounds__(CT) chol_reg_kernel(const double* __restrict__ G, double* __restrict__ R,
                                                      double* __restrict__ Rinv, int32_t* __restrict__ info,
-                                                     int slot) {
+                                                     int slot, int near_identity) {
   constexpr int d = 16 * TBS, LDR = d + 1;
   extern __shared__ double rsm[];
   double* Rs = rsm;                // d x LDR: R (upper)
   double* colb = Rs + d * LDR;     // 2 x d: published column / X row
   __shared__ int s_bad;
   __shared__ double s_dmax;
+  __shared__ double s_emax[CT / 32];
   const int tid = threadIdx.x, bi = tid >> 4, bj = tid & 15;
   const int i0 = bi * TBS, j0 = bj * TBS;
+  if (near_identity) {
+    // CholeskyQR2's second Gram Q1^T Q1 = I + E with E ~ kappa(A)^2 eps: chol(I + E) =
+    // I + strict_upper(E) + diag(E) / 2 + O(|E|^2) and its inverse I - strict_upper(E) - diag(E) / 2
+    // + O(|E|^2), exact to rounding once |E| <= 1e-8; otherwise the factorisation below
+    double em = 0.0;
+    for (int e = tid; e < d * d; e += CT) {
+      const int i = e / d, j = e % d;
+      em = fmax(em, fabs(0.5 * (G[i * d + j] + G[j * d + i]) - (i == j ? 1.0 : 0.0)));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) em = fmax(em, __shfl_xor_sync(0xffffffffu, em, o));
+    if ((tid & 31) == 0) s_emax[tid >> 5] = em;
+    __syncthreads();
+    em = 0.0;
+    for (int w = 0; w < CT / 32; w++) em = fmax(em, s_emax[w]);
+    if (em <= 1e-8) {
+      for (int e = tid; e < d * d; e += CT) {
+        const int i = e / d, j = e % d;
+        const double ev = 0.5 * (G[i * d + j] + G[j * d + i]) - (i == j ? 1.0 : 0.0);
+        const double up = i < j ? ev : (i == j ? 0.5 * ev : 0.0);
+        R[e] = (i == j ? 1.0 : 0.0) + up;
+        if (Rinv) Rinv[e] = (i == j ? 1.0 : 0.0) - up;
+      }
+      if (tid == 0 && info) info[slot] = 0;
+      return;
+    }
+  }
   double a[TBS][TBS];
 #pragma unroll
   for (int r = 0; r < TBS; r++)
@@ -340,7 +368,8 @@ int launch_tallmm_dmma(cudaStream_t st, const double* A, int64_t n, const double
   return KS_OK;
 }
 
-int chol_upper(cudaStream_t st, const double* G, int d, double* R, double* Rinv, int32_t* info, int slot) {
+int chol_upper(cudaStream_t st, const double* G, int d, double* R, double* Rinv, int32_t* info, int slot,
+               int near_identity = 0) {
   // register-resident factor for d = 32 / 64 (at d = 128 the 8 x 8 blocks per thread run slower
   // than the shared-memory kernel)
   if (!ks::env(ks::ENV_TALL_OLD) && (d == 32 || d == 64)) {
@@ -348,7 +377,7 @@ int chol_upper(cudaStream_t st, const double* G, int d, double* R, double* Rinv,
 #define KS_CHOL(TB)                                                                                            \
     if (d == 16 * TB) {                                                                                        \
       KS_TRY_CUDA(cudaFuncSetAttribute(chol_reg_kernel<TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-      chol_reg_kernel<TB><<<1, CT, smem, st>>>(G, R, Rinv, info, slot);                                        \
+      chol_reg_kernel<TB><<<1, CT, smem, st>>>(G, R, Rinv, info, slot, near_identity);                         \
       KS_CHECK_LAUNCH();                                                                                       \
       return KS_OK;                                                                                            \
     }
@@ -397,7 +426,7 @@ int chol_qr2_r_async(cudaStream_t st, const double* A, int64_t n, int d, double*
   if ((rc = chol_upper(st, G.p, d, R1.p, R1i.p, info_dev, 0))) return rc;
   if ((rc = tallmm(st, A, n, d, R1i.p, Q.p, nullptr))) return rc;  // Q1 = A R1^-1
   if ((rc = gemm_tn_tall(st, d, d, n, 1.0, Q.p, d, 1, Q.p, d, 1, G.p))) return rc;
-  if ((rc = chol_upper(st, G.p, d, R2.p, Rinv ? R2i.p : nullptr, info_dev, 1))) return rc;
+  if ((rc = chol_upper(st, G.p, d, R2.p, Rinv ? R2i.p : nullptr, info_dev, 1, 1))) return rc;
   if ((rc = gemm(st, d, d, d, 1.0, R2.p, d, 1, 0, R1.p, d, 1, 0, 0.0, R, d, 1, 0, 1))) return rc;
   if (Rinv && (rc = gemm(st, d, d, d, 1.0, R1i.p, d, 1, 0, R2i.p, d, 1, 0, 0.0, Rinv, d, 1, 0, 1))) return rc;
   return KS_OK;
@@ -414,7 +443,7 @@ int chol_qr2_r(cudaStream_t st, const double* A, int64_t n, int d, double* R, in
   if ((rc = chol_upper(st, G.p, d, R1.p, R1i.p, info.p, 0))) return rc;
   if ((rc = tallmm(st, A, n, d, R1i.p, Q.p, nullptr))) return rc;  // Q1 = A R1^-1
   if ((rc = gemm_tn_tall(st, d, d, n, 1.0, Q.p, d, 1, Q.p, d, 1, G.p))) return rc;
-  if ((rc = chol_upper(st, G.p, d, R2.p, Rinv ? R2i.p : nullptr, info.p, 1))) return rc;
+  if ((rc = chol_upper(st, G.p, d, R2.p, Rinv ? R2i.p : nullptr, info.p, 1, 1))) return rc;
   // R = R2 R1 and R^-1 = R1^-1 R2^-1 (all upper triangular)
   if ((rc = gemm(st, d, d, d, 1.0, R2.p, d, 1, 0, R1.p, d, 1, 0, 0.0, R, d, 1, 0, 1))) return rc;
   if (Rinv && (rc = gemm(st, d, d, d, 1.0, R1i.p, d, 1, 0, R2i.p, d, 1, 0, 0.0, Rinv, d, 1, 0, 1))) return rc;
