@@ -32,11 +32,36 @@ constexpr int CT = 256;
 // info[slot] = k + 1 if pivot k is below tol * max diag (not comfortably positive definite).
 __global__ void __launch_bounds__(CT) chol_upper_kernel(const double* __restrict__ G, int d, double* __restrict__ R,
                                                        double* __restrict__ Rinv, int32_t* __restrict__ info,
-                                                       int slot) {
+                                                       int slot, int near_identity) {
   extern __shared__ double S[];      // d x d (row-major, upper triangle used), then row k / packed R^-1
   double* W = S + (size_t)d * d;
   __shared__ int s_bad;
   __shared__ double s_dmax;
+  __shared__ double s_emax[CT / 32];
+  if (near_identity) {  // the closed form of chol_reg_kernel for G = I + E, |E| <= 1e-8
+    double em = 0.0;
+    for (int e = threadIdx.x; e < d * d; e += CT) {
+      const int i = e / d, j = e % d;
+      em = fmax(em, fabs(0.5 * (G[i * d + j] + G[j * d + i]) - (i == j ? 1.0 : 0.0)));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) em = fmax(em, __shfl_xor_sync(0xffffffffu, em, o));
+    if ((threadIdx.x & 31) == 0) s_emax[threadIdx.x >> 5] = em;
+    __syncthreads();
+    em = 0.0;
+    for (int w = 0; w < CT / 32; w++) em = fmax(em, s_emax[w]);
+    if (em <= 1e-8) {
+      for (int e = threadIdx.x; e < d * d; e += CT) {
+        const int i = e / d, j = e % d;
+        const double ev = 0.5 * (G[i * d + j] + G[j * d + i]) - (i == j ? 1.0 : 0.0);
+        const double up = i < j ? ev : (i == j ? 0.5 * ev : 0.0);
+        R[e] = (i == j ? 1.0 : 0.0) + up;
+        if (Rinv) Rinv[e] = (i == j ? 1.0 : 0.0) - up;
+      }
+      if (threadIdx.x == 0 && info) info[slot] = 0;
+      return;
+    }
+  }
   for (int e = threadIdx.x; e < d * d; e += CT) {
     const int i = e / d, j = e - i * d;
     S[e] = i <= j ? 0.5 * (G[i * d + j] + G[j * d + i]) : 0.0;
@@ -386,7 +411,7 @@ int chol_upper(cudaStream_t st, const double* G, int d, double* R, double* Rinv,
   }
   const size_t smem = ((size_t)d * d + (size_t)d * (d + 1) / 2 + d) * sizeof(double);
   KS_TRY_CUDA(cudaFuncSetAttribute(chol_upper_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  chol_upper_kernel<<<1, CT, smem, st>>>(G, d, R, Rinv, info, slot);
+  chol_upper_kernel<<<1, CT, smem, st>>>(G, d, R, Rinv, info, slot, near_identity);
   KS_CHECK_LAUNCH();
   return KS_OK;
 }
