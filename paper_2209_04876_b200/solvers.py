@@ -1305,14 +1305,23 @@ def _fast_solve_pass(facs, b, config: RegressionConfig, caches, trace, use_chol:
     iters = ctypes.c_int32(0)
     hlen = ctypes.c_int32(0)
     lib = _lib.load()
-    fused = (_USE_FUSED[0] and len(left) == 1 and len(right) == 1 and view.dL in (16, 32, 64)
+    fused = (_USE_FUSED[0] and len(left) >= 1 and len(right) >= 1 and view.dL in (16, 32, 64)
              and view.dR in (16, 32, 64) and view.nnz > 0 and max_iters <= 1024)
     dg = VL = VR = None
     if fused:
-        # right-hand side, preconditioner diagonal and the loop in one persistent launch
+        # right-hand side, preconditioner diagonal and the loop in one persistent launch; a group
+        # of several factors (the Tucker core's right group) has the Kronecker products of their
+        # eigenbases and eigenvalues, in the group's column order (as the preconditioner below)
         grams = _join_grams(grams)
-        VL, wL = grams[left[0]]
-        VR, wR = grams[right[0]]
+        def group(idx):
+            if len(idx) == 1:
+                return grams[idx[0]]
+            V = _kron_dev([grams[i][0] for i in idx])
+            w = _kron_dev([grams[i][1].reshape(-1, 1) for i in idx]).reshape(-1)
+            return V, w
+        VL, wL = group(left)
+        VR, wR = group(right)
+        VL, wL, VR, wR = (t.contiguous() for t in (VL, wL, VR, wR))
         _mark("precond")
         deferred.stage()  # flag copies complete with the loop launch's own synchronisation
         _LAST_LOOP_EVENTS[0] = None
