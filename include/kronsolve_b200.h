@@ -70,6 +70,18 @@ int ks_kron_mat_mul(int32_t nf, const double* const* factors, const int64_t* row
 int ks_kron2_contract(const double* L, const double* B, int64_t ldb, const double* R,
                       int64_t m, int64_t k, int32_t p, int32_t q, double* T, void* stream);
 
+/* K13: T (R0 x R1 R2) = (U0 kron U1 kron U2)^T b for the n0 x n1 x n2 tensor b, one streaming pass
+ * over b in the reference's rightmost-first order (kron.py:66-77 at N = 3, reached from the Tucker
+ * exact core update tucker.py:120 -> solvers.py:314).  U_k: n_k x R_k row-major.
+ * ks_kron3_supported returns 1 for the geometries the kernel handles (n2 % 8 == 0, n2 <= 128,
+ * R1 <= 32, R2 <= 8, R0 R1 R2 <= 2048), else 0; ks_kron3_contract returns KS_ESIZE for the others. */
+int ks_kron3_supported(int64_t n0, int64_t n1, int64_t n2, int32_t R0, int32_t R1, int32_t R2);
+int ks_kron3_contract(const double* U0, const double* U1, const double* U2, const double* B,
+                      int64_t n0, int64_t n1, int64_t n2, int32_t R0, int32_t R1, int32_t R2,
+                      double* T, void* stream);
+/* Profiling aid: later K13 launches only stream b through their ring (no arithmetic). */
+int ks_debug_kron3_stream_only(int32_t on);
+
 /* K2: out[0] = sum_{i,j} ((L X R^T)[i,j] - B[i,j])^2 without materialising K x.
  * L: m x p, X: p x q, R: k x q, B: m x k.  The n^2 pass of ridge_loss (solvers.py:251-262). */
 int ks_kron2_residual_sumsq(const double* L, const double* X, const double* R,

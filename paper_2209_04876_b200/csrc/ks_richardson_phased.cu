@@ -189,7 +189,7 @@ __global__ void __launch_bounds__(NT, 1) richardson_phased_kernel(PArgs a) {
   if (resident && nrows > 0 && !a.apply_only) {
     const int lrows = ((nrows + CH_ROWS - 1) / CH_ROWS) * CH_ROWS;
     YZ = Ls + (lrows + CH_ROWS) * DLP;  // the tiles read L rows < lrows; one chunk more, as L_ROWS
-    const int yz = max(lrows * DRP, G * epc);
+    const int yz = max(lrows * DRP, max(G * epc, DL * DRP));  // also the reduce operands and the step
     Rres = YZ + ((yz + 15) & ~15);  // 128-byte aligned
     rcap = max(0, (int)((sm + S::W_OFF) - Rres) / DRP);
   }

@@ -339,7 +339,15 @@ def _exact_solve_dev(facs: list[torch.Tensor], bt: torch.Tensor, lam: float) -> 
         return D.zeros(math.prod(int(a.shape[1]) for a in facs))
     rest_rows = math.prod(int(a.shape[0]) for a in facs[1:])
     rest_rank = math.prod(ranks[1:])
-    if len(facs) >= 2 and ranks[0] <= 128 and rest_rank <= 128 and rest_rows * rest_rank <= (1 << 25):
+    nk = [int(a.shape[0]) for a in facs]
+    if len(facs) == 3 and _lib.load().ks_kron3_supported(nk[0], nk[1], nk[2], *ranks) == 1:
+        # K13: one streaming pass over b in the reference's rightmost-first order (ks_kron3.cu)
+        T = D.empty(ranks[0], ranks[1] * ranks[2])
+        us3 = [u.contiguous() for u in us]
+        _lib.call("ks_kron3_contract", D.p(us3[0]), D.p(us3[1]), D.p(us3[2]), D.p(bt), nk[0], nk[1], nk[2],
+                  *ranks, D.p(T), D.stream())
+        t = T.reshape(-1)
+    elif len(facs) >= 2 and ranks[0] <= 128 and rest_rank <= 128 and rest_rows * rest_rank <= (1 << 25):
         # the n^2 pass on the FP64 tensor pipe (TMA + DMMA K1 kernel): t = U_0^T B U_rest with
         # B the n_0 x prod(n_rest) reshape of b and, for N >= 3, the right group's U's
         # materialised as one Kronecker product (the Tucker core's K13: 512 x 32768 B at c5)

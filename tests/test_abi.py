@@ -59,3 +59,16 @@ def test_error_mapping():
         with pytest.raises(exc):
             _lib.check(rc, "x")
     assert issubclass(InvalidInputError, ValueError)
+
+
+def test_kron3_supported_geometry():
+    """Host-side geometry check of the K13 streaming kernel (no device work)."""
+    from paper_2209_04876_b200 import _lib
+    L = _lib.load()
+    assert L.ks_kron3_supported(512, 512, 64, 16, 16, 4) == 1
+    assert L.ks_kron3_supported(512, 512, 60, 16, 16, 4) == 0    # n2 % 8
+    assert L.ks_kron3_supported(512, 512, 64, 15, 16, 4) == 1    # odd ranks are fine
+    assert L.ks_kron3_supported(512, 512, 64, 2, 33, 4) == 0     # R1 > 32 (two m16 tiles of S)
+    assert L.ks_kron3_supported(512, 512, 64, 64, 16, 4) == 0    # R0 R1 R2 > 2048 core entries
+    assert L.ks_kron3_supported(512, 512, 256, 16, 16, 4) == 0   # n2 > 128
+    assert L.ks_kron3_supported(64, 64, 64, 16, 16, 16) == 0     # R2 > 8

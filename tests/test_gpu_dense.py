@@ -170,3 +170,32 @@ def test_cholqr2_and_leverage_scores_tall(n, d):
     _lib.call("ks_leverage_scores_tall", D.p(torch.tensor(a, device="cuda")), n, d, D.p(sc), ctypes.byref(ok),
               D.stream())
     assert ok.value == 0
+
+
+@pytest.mark.parametrize("shape,rank", [((512, 512, 64), (16, 16, 4)),   # BASELINE c5 (K13)
+                                        ((37, 203, 8), (2, 4, 1)),      # partial unit, n2 = 8
+                                        ((9, 70, 128), (6, 8, 8)),      # n2 = 128 (32-row units)
+                                        ((5, 131, 24), (4, 2, 3)),      # odd R2, n1 not a unit multiple
+                                        ((300, 1, 16), (2, 2, 5)),      # n1 = 1: one row per unit
+                                        ((40, 300, 40), (3, 27, 7))])   # odd ranks, R1 > 16 (two S tiles)
+def test_kron3_contract_matches_oracle(rng, shape, rank):
+    """K13 (ks_kron3.cu): T = (U0 kron U1 kron U2)^T b against the oracle's rightmost-first
+    kron_mat_mul (kron.py:44-77) with the transposed factors."""
+    from oracle import kronsolve_oracle as O
+    from paper_2209_04876_b200 import _lib, _device as D
+    us = [rng.standard_normal((n, r)) for n, r in zip(shape, rank)]
+    b = rng.standard_normal(math.prod(shape))
+    assert _lib.load().ks_kron3_supported(*shape, *rank) == 1
+    T = D.empty(rank[0], rank[1] * rank[2])
+    U = [D.to_dev(u) for u in us]
+    _lib.call("ks_kron3_contract", D.p(U[0]), D.p(U[1]), D.p(U[2]), D.p(D.to_dev(b)), *shape, *rank, D.p(T),
+              D.stream())
+    want = O.kron_mat_mul([u.T for u in us], b)
+    got = T.cpu().numpy().reshape(-1)
+    assert rel(got, want) < 1e-13, rel(got, want)
+    # deterministic: a second pass gives the same bits
+    T2 = D.empty(rank[0], rank[1] * rank[2])
+    _lib.call("ks_kron3_contract", D.p(U[0]), D.p(U[1]), D.p(U[2]), D.p(D.to_dev(b)), *shape, *rank, D.p(T2),
+              D.stream())
+    assert torch.equal(T, T2)
+
