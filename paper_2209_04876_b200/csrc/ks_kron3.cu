@@ -228,6 +228,161 @@ __global__ void kron3_reduce_kernel(const double* __restrict__ part, int grid, i
   if (lane == 0) T[e] = s;
 }
 
+// ---- register-streaming variant (n2 <= 64): every warp streams its own 16-row tiles of b with 16-byte
+// loads straight into DMMA A fragments (two tiles in flight per warp: the next tile's loads are issued
+// before the current one is multiplied), no shared-memory ring and no CTA barrier until the end.
+// Lane (g, t4) loads row g and g + 8 of the tile, 16-byte chunks t4, t4 + 4, ... (each load
+// instruction covers 64 contiguous bytes of 8 rows); its k-step ks then multiplies column
+// 8 (ks / 2) + 2 t4 + ks % 2 -- the same permutation of the k index for every row and for the U2
+// fragments, so the DMMA contraction is unchanged.
+template <int NCH, int MT1>
+__global__ void __launch_bounds__(K3_T, 1) kron3_stream_kernel(K3Args a) {
+  constexpr int KS = 2 * NCH;  // k-steps (n2 = 8 NCH columns)
+  constexpr int CPL = 8;       // core columns (r1, r2) per lane: R1 R2 <= 256
+  extern __shared__ __align__(16) double k3s[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
+  const int R0 = a.R0, R1 = a.R1, R2 = a.R2, R12 = R1 * R2, NP = R0 * R12;
+  const int64_t n1 = a.n1, n2 = a.n2;
+  const int nt1 = (int)((n1 + 15) / 16);  // tiles per i0 slab
+  const int64_t tiles = a.n0 * nt1;
+  const int64_t t_beg = tiles * blockIdx.x / gridDim.x, t_end = tiles * (blockIdx.x + 1) / gridDim.x;
+  const int PWS = ((NP + 1) & ~1) + MT1 * 128;  // per warp: its core partial, then its S tile(s)
+  double* Pw = k3s + (size_t)warp * PWS;
+  double* Sw = Pw + ((NP + 1) & ~1);
+  for (int e = lane; e < NP; e += 32) Pw[e] = 0.0;
+  int sidx[CPL];  // core column c = lane + 32 j -> its S element (r1 = c / R2, r2 = c % R2)
+#pragma unroll
+  for (int j = 0; j < CPL; j++) {
+    const int c = lane + 32 * j, r1 = c / R2;
+    sidx[j] = c < R12 ? r1 * 8 + c - r1 * R2 : 0;
+  }
+
+  double u2f[KS];  // b0 = U2[column of (ks, t4)][g]
+#pragma unroll
+  for (int ks = 0; ks < KS; ks++) {
+    const int col = 8 * (ks >> 1) + 2 * t4 + (ks & 1);
+    u2f[ks] = (col < n2 && g < R2) ? __ldg(&a.U2[(size_t)col * R2 + g]) : 0.0;
+  }
+  double sacc[MT1][4];
+#pragma unroll
+  for (int m = 0; m < MT1; m++) sacc[m][0] = sacc[m][1] = sacc[m][2] = sacc[m][3] = 0.0;
+
+  // this warp's tiles t_beg + warp + 8 k, tracked as (slab i0, tile of the slab) without divisions
+  struct Pos {
+    int64_t i0;
+    int ts;  // tile within the slab
+  };
+  auto advance = [&](Pos p) {
+    p.ts += K3_CW;
+    while (p.ts >= nt1) {
+      p.ts -= nt1;
+      p.i0++;
+    }
+    return p;
+  };
+  auto load_tile = [&](Pos p, double2 (&v)[2][NCH]) {
+    const int64_t i1b = (int64_t)p.ts * 16;
+    const int nr = (int)min((int64_t)16, n1 - i1b);
+    const double* base = a.B + (p.i0 * n1 + i1b) * n2;
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      const int r = g + 8 * h;
+#pragma unroll
+      for (int j = 0; j < NCH; j++)
+        v[h][j] = r < nr ? __ldg(reinterpret_cast<const double2*>(base + r * n2) + 4 * j + t4)
+                         : make_double2(0.0, 0.0);
+    }
+  };
+  int64_t cur_i0 = -1;
+  auto flush = [&]() {  // Pw += U0[cur_i0, :] outer S_w (this warp's S over the slab's tiles it ran)
+#pragma unroll
+    for (int m = 0; m < MT1; m++) {
+      double* so = Sw + (m * 16 + g) * 8 + 2 * t4;
+      *reinterpret_cast<double2*>(so) = make_double2(sacc[m][0], sacc[m][1]);
+      *reinterpret_cast<double2*>(so + 64) = make_double2(sacc[m][2], sacc[m][3]);
+      sacc[m][0] = sacc[m][1] = sacc[m][2] = sacc[m][3] = 0.0;
+    }
+    __syncwarp();
+    double sv[CPL];
+#pragma unroll
+    for (int j = 0; j < CPL; j++) sv[j] = Sw[sidx[j]];
+    const double* u0 = a.U0 + cur_i0 * R0;
+    for (int r0 = 0; r0 < R0; r0++) {
+      const double w = __ldg(&u0[r0]);
+#pragma unroll
+      for (int j = 0; j < CPL; j++)
+        if (lane + 32 * j < R12) Pw[r0 * R12 + lane + 32 * j] = fma(w, sv[j], Pw[r0 * R12 + lane + 32 * j]);
+    }
+    __syncwarp();
+  };
+  // one tile: step 1 (M = B_tile U2, DMMA, two independent accumulator chains), step 2
+  // (S_w += U1_tile^T M through shuffles)
+  auto run_tile = [&](Pos p, const double2 (&v)[2][NCH]) {
+    const int64_t i1b = (int64_t)p.ts * 16;
+    const int nr = (int)min((int64_t)16, n1 - i1b);
+    if (p.i0 != cur_i0) {
+      if (cur_i0 >= 0) flush();
+      cur_i0 = p.i0;
+    }
+    double ua[4][MT1][2];
+#pragma unroll
+    for (int ks = 0; ks < 4; ks++) {
+      const int row = 4 * ks + t4;
+      const bool ok = row < nr;
+#pragma unroll
+      for (int m = 0; m < MT1; m++) {
+        const int r1 = 16 * m + g;
+        ua[ks][m][0] = ok && r1 < R1 ? __ldg(&a.U1[(i1b + row) * R1 + r1]) : 0.0;
+        ua[ks][m][1] = ok && r1 + 8 < R1 ? __ldg(&a.U1[(i1b + row) * R1 + r1 + 8]) : 0.0;
+      }
+    }
+    double c[4] = {0.0, 0.0, 0.0, 0.0}, d[4] = {0.0, 0.0, 0.0, 0.0};
+    if (!a.stream_only) {
+#pragma unroll
+      for (int j = 0; j < NCH; j++) {
+        dmma_16x8x4(c, v[0][j].x, v[1][j].x, u2f[2 * j]);
+        dmma_16x8x4(d, v[0][j].y, v[1][j].y, u2f[2 * j + 1]);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < NCH; j++) c[0] += v[0][j].x + v[1][j].y;  // consume the loads
+    }
+#pragma unroll
+    for (int e = 0; e < 4; e++) c[e] += d[e];
+#pragma unroll
+    for (int ks = 0; ks < 4; ks++) {
+      const int src = ((4 * ks + t4) & 7) * 4 + (g >> 1);
+      const double lo = __shfl_sync(0xffffffffu, c[ks >= 2 ? 2 : 0], src);
+      const double hi = __shfl_sync(0xffffffffu, c[ks >= 2 ? 3 : 1], src);
+      const double b0 = (g & 1) ? hi : lo;
+#pragma unroll
+      for (int m = 0; m < MT1; m++) dmma_16x8x4(sacc[m], ua[ks][m][0], ua[ks][m][1], b0);
+    }
+  };
+  double2 va[2][NCH], vb[2][NCH];
+  int64_t t = t_beg + warp;
+  Pos pa{t_beg / nt1, (int)(t_beg % nt1)};
+  pa = advance(Pos{pa.i0, pa.ts + warp - K3_CW});
+  if (t < t_end) load_tile(pa, va);
+  for (; t < t_end; t += 2 * K3_CW) {
+    const Pos pb = advance(pa);
+    if (t + K3_CW < t_end) load_tile(pb, vb);
+    run_tile(pa, va);
+    if (t + K3_CW >= t_end) break;
+    pa = advance(pb);
+    if (t + 2 * K3_CW < t_end) load_tile(pa, va);
+    run_tile(pb, vb);
+  }
+  if (cur_i0 >= 0) flush();
+  __syncthreads();
+  for (int e = tid; e < NP; e += K3_T) {  // the warps' partials in order
+    double v = 0.0;
+#pragma unroll
+    for (int w = 0; w < K3_CW; w++) v += k3s[(size_t)w * PWS + e];
+    a.part[(size_t)blockIdx.x * NP + e] = v;
+  }
+}
+
 }  // namespace
 
 static int g_k3_stream_only = 0;
@@ -240,8 +395,8 @@ extern "C" int ks_debug_kron3_stream_only(int32_t on) {
 
 // Geometry the streaming kernel handles (else the caller contracts on the materialised right group)
 extern "C" int ks_kron3_supported(int64_t n0, int64_t n1, int64_t n2, int32_t R0, int32_t R1, int32_t R2) {
-  return n0 >= 1 && n1 >= 1 && n2 >= 8 && n2 <= 128 && n2 % 8 == 0 && R0 >= 1 && R1 >= 1 && R2 >= 1 &&
-         R1 <= 32 && R2 <= 8 && R0 * R1 * R2 <= K3_PMAX * K3_CW * 32;
+  return n0 >= 1 && n1 >= 1 && n0 * n1 < (int64_t(1) << 31) && n2 >= 8 && n2 <= 128 && n2 % 8 == 0 && R0 >= 1 && R1 >= 1 && R2 >= 1 &&
+         R1 <= 32 && R2 <= 8 && R1 * R2 <= 256 && R0 * R1 * R2 <= K3_PMAX * K3_CW * 32;
 }
 
 // T (R0 x R1 R2, row-major) = (U0 kron U1 kron U2)^T b; U_k: n_k x R_k row-major, b: n0 n1 n2.
@@ -255,11 +410,32 @@ extern "C" int ks_kron3_contract(const double* U0, const double* U1, const doubl
   a.U0 = U0; a.U1 = U1; a.U2 = U2; a.B = B;
   a.stream_only = g_k3_stream_only;
   a.n0 = n0; a.n1 = n1; a.n2 = n2; a.R0 = R0; a.R1 = R1; a.R2 = R2;
+  const int np = R0 * R1 * R2;
+  const int mt1 = (R1 + 15) / 16;
+  if (n2 <= 64 && (size_t)K3_CW * (((np + 1) & ~1) + mt1 * 128) * 8 <= (size_t)K3_SMEM) {
+    // register-streaming kernel: 16-row tiles over every warp of the grid
+    const int64_t tiles = n0 * ((n1 + 15) / 16);
+    const int grid = (int)std::min<int64_t>(ks::num_sms(), (tiles + K3_CW - 1) / K3_CW);
+    ks::Scratch<double> part((size_t)grid * np, st);
+    KS_REQUIRE(part.p, KS_ECUDA, "scratch allocation failed");
+    a.part = part.p;
+    const size_t smem = (size_t)K3_CW * (((np + 1) & ~1) + mt1 * 128) * 8;
+    int rc = KS_EINVAL;
+#define KS_K3S(NCH, MT)                                                                                        if ((int)(n2 / 8) == NCH && mt1 == MT) {                                                                       KS_TRY_CUDA(cudaFuncSetAttribute(kron3_stream_kernel<NCH, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize,                                      (int)smem));                                                                kron3_stream_kernel<NCH, MT><<<grid, K3_T, smem, st>>>(a);                                                   rc = KS_OK;                                                                                                }
+    KS_K3S(1, 1) KS_K3S(2, 1) KS_K3S(3, 1) KS_K3S(4, 1) KS_K3S(5, 1) KS_K3S(6, 1) KS_K3S(7, 1) KS_K3S(8, 1)
+    KS_K3S(1, 2) KS_K3S(2, 2) KS_K3S(3, 2) KS_K3S(4, 2) KS_K3S(5, 2) KS_K3S(6, 2) KS_K3S(7, 2) KS_K3S(8, 2)
+#undef KS_K3S
+    if (rc) return rc;
+    KS_CHECK_LAUNCH();
+    kron3_reduce_kernel<<<(np + 7) / 8, 256, 0, st>>>(part.p, grid, np, T);
+    KS_CHECK_LAUNCH();
+    return KS_OK;
+  }
+  // TMA-ring kernel (64 < n2 <= 128)
   a.rows = (int)std::min<int64_t>(K3_ROWS, (n1 + 15) / 16 * 16);  // m16 row tiles, one per compute warp
   a.nb1 = (int)((n1 + a.rows - 1) / a.rows);
   const int nbox = (int)((n2 + 15) / 16);
   a.stage_doubles = (a.rows * 16 + 127) & ~127;  // one 16-column box per stage, 1 KB aligned
-  const int mt1 = (R1 + 15) / 16;
   const int fixed = K3_CW * mt1 * 128 + mt1 * 128 + 64;  // doubles (+ mbarriers)
   a.stages = std::min(16, (K3_SMEM / 8 - 128 - fixed) / a.stage_doubles);
   KS_REQUIRE(a.stages >= 2, KS_ESIZE, "kron3 contraction: stages do not fit shared memory");
@@ -269,7 +445,6 @@ extern "C" int ks_kron3_contract(const double* U0, const double* U1, const doubl
              KS_EINVAL, "kron3 contraction: tensor map");
   const int64_t units = n0 * a.nb1;
   const int grid = (int)std::min<int64_t>(ks::num_sms(), units);
-  const int np = R0 * R1 * R2;
   ks::Scratch<double> part((size_t)grid * np, st);
   KS_REQUIRE(part.p, KS_ECUDA, "scratch allocation failed");
   a.part = part.p;

@@ -47,11 +47,13 @@ def main():
         k13 = lambda: L.call("ks_kron3_contract", D.p(us[0]), D.p(us[1]), D.p(us[2]), D.p(x), *shape, *rank,  # noqa: E731
                              D.p(T), D.stream())
         out = []
-        for mode in (0, 1, 2):
+        for mode in (0, 1):
             L.call("ks_debug_kron3_stream_only", mode)
             t = ev_median(graph_of(k13).replay, 11, clean)
             out.append(f"mode{mode} {t:.1f} us {8.0 * x.numel() / t / 1e3:.0f} GB/s")
         L.call("ks_debug_kron3_stream_only", 0)
+        t = ev_median(graph_of(lambda: x.sum()).replay, 11, clean)
+        out.append(f"torch sum {t:.1f} us {8.0 * x.numel() / t / 1e3:.0f} GB/s")
         print(f"n0={n0} ({8.0 * x.numel() / 1e6:.0f} MB):", " | ".join(out), flush=True)
         del x
 
