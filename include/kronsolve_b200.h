@@ -122,7 +122,8 @@ int ks_sym_eig_batched(int32_t nb, const double* const* mats, int32_t d, double*
 
 /* Thin SVD of A (n x d): U (n x d), sigma (d, descending), V (d x d).  Columns past the
  * numerical rank (sigma <= rank_tol*sigma_max) are zeroed and *rank (host) reports it.
- * Replaces tensor.compact_svd (tensor.py:76-107).  Synchronises the stream. */
+ * Replaces tensor.compact_svd (tensor.py:76-107).  Synchronises the stream, unless rank is NULL
+ * (the caller then counts sigma_j > rank_tol * sigma_0 itself, e.g. for several factors at once). */
 int ks_compact_svd(const double* A, int64_t n, int32_t d, double rank_tol, double* U,
                    double* sigma, double* V, int32_t* rank, void* stream);
 

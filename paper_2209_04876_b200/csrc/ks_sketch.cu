@@ -941,11 +941,12 @@ extern "C" int ks_sketch_diag_grouped2(const int64_t* idx, const int64_t* row_sh
 }
 
 namespace {
-// Grid-stride, GATHER_ILP independent reads in flight per thread.  With page-locked host b every
-// read is one PCIe request and the gather is request-rate bound (~3.8 ns per read on the B200
-// boxes, independent of reads in flight per thread or block size: tools/hostgather_bench.cu), so
-// a small grid reaches the same rate while leaving the other SMs' memory pipelines to the sketch
-// kernels that run beside it.
+// Gather of the sampled b entries.  Default launch: ceil(s / 256) blocks, one read per thread (the
+// loop below runs once).  With page-locked host b every read is one PCIe request and the gather is
+// request-rate bound (~3.8 ns per read on the B200 boxes, tools/hostgather_bench.cu).  The gather
+// runs after the sketch in the solve graph (KS_GATHER_BESIDE_SKETCH=1, part of the graph key through
+// solvers._switches, moves it beside the sketch: measured slower).  KS_GATHER_BLOCKS=<n> (A/B only)
+// caps the grid, each thread then keeping GATHER_ILP independent reads in flight per pass.
 constexpr int GATHER_ILP = 8;
 __global__ void gather_draws2_kernel(const double* __restrict__ b, const int64_t* __restrict__ draws, int64_t n1,
                                      int64_t s, double* __restrict__ out) {

@@ -1171,6 +1171,7 @@ extern "C" int ks_compact_svd(const double* A, int64_t n, int32_t d, double rank
     if (rc) return rc;
     // U holds V' (n x n) already normalised; zero columns past the rank for consistency
   }
+  if (!rank) return KS_OK;  // the caller counts the rank from sigma itself (no synchronisation here)
   std::vector<double> hs(k);
   KS_TRY_CUDA(cudaMemcpyAsync(hs.data(), sigma, sizeof(double) * k, cudaMemcpyDeviceToHost, st));
   KS_TRY_CUDA(cudaStreamSynchronize(st));

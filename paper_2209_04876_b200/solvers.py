@@ -37,7 +37,7 @@ from .leverage import (JL_LOG_FACTOR, REGRESSION_SAMPLE_CONSTANT, LeverageScores
                        RowSketch, _inverse_small, _jl_scores_dev, _spectral_rows_dev,
                        ridge_leverage_scores, spectral_sample_count)
 from ._numpy_rng import pcg64_state
-from .tensor import CompactSvd, _compact_svd_dev, as_matrix, compact_svd
+from .tensor import CompactSvd, _compact_svd_dev, _compact_svds_dev, as_matrix, compact_svd
 
 DEFAULT_DENSE_GUARD = 10 ** 8
 _DIVERGENCE_WINDOW = 5
@@ -332,7 +332,7 @@ def _validated_problem(factors, b):
 
 
 def _exact_solve_dev(facs: list[torch.Tensor], bt: torch.Tensor, lam: float) -> torch.Tensor:
-    svds = [_compact_svd_dev(a, 1e-10) for a in facs]
+    svds = _compact_svds_dev(facs, 1e-10)
     us = [s[0] for s in svds]
     ranks = [int(s[1].numel()) for s in svds]
     if min(ranks) == 0:

@@ -62,21 +62,39 @@ class CompactSvd:
 
 
 def _compact_svd_dev(t: torch.Tensor, rank_tol: float):
-    n, d = t.shape
-    k = min(n, d)
-    if k == 0:
-        return t.new_zeros((n, 0)), t.new_zeros((0,)), t.new_zeros((d, 0))
-    if k > 128:
-        from .errors import SizeGuardError
-        raise SizeGuardError(f"compact_svd on the device supports min(n, d) <= 128, got {k}")
-    u = D.empty(n, k)
-    s = D.empty(k)
-    v = D.empty(d, k)
-    rank = ctypes.c_int32(0)
-    _lib.call("ks_compact_svd", D.p(t), n, d, float(rank_tol), D.p(u), D.p(s), D.p(v),
-              ctypes.byref(rank), D.stream())
-    r = rank.value
-    return u[:, :r].contiguous(), s[:r].contiguous(), v[:, :r].contiguous()
+    return _compact_svds_dev([t], rank_tol)[0]
+
+
+def _compact_svds_dev(ts, rank_tol: float):
+    """Thin SVDs of several matrices with ONE synchronisation: every ks_compact_svd runs without
+    its own rank read-back, then all singular values come back in one copy and the ranks
+    (sigma_j > rank_tol * sigma_0, tensor.py:76-107) are counted here."""
+    outs, sig = [], []
+    for t in ts:
+        n, d = t.shape
+        k = min(n, d)
+        if k == 0:
+            outs.append((t.new_zeros((n, 0)), t.new_zeros((0,)), t.new_zeros((d, 0))))
+            continue
+        if k > 128:
+            from .errors import SizeGuardError
+            raise SizeGuardError(f"compact_svd on the device supports min(n, d) <= 128, got {k}")
+        u, s, v = D.empty(n, k), D.empty(k), D.empty(d, k)
+        _lib.call("ks_compact_svd", D.p(t), n, d, float(rank_tol), D.p(u), D.p(s), D.p(v), None, D.stream())
+        outs.append((u, s, v))
+        sig.append(s)
+    hs = torch.cat(sig).cpu().tolist() if sig else []
+    res, off = [], 0
+    for u, s, v in outs:
+        k = int(s.numel())
+        if k == 0:
+            res.append((u, s, v))
+            continue
+        h = hs[off:off + k]
+        off += k
+        r = sum(1 for x in h if x > rank_tol * h[0]) if h[0] > 0.0 else 0
+        res.append((u[:, :r].contiguous(), s[:r].contiguous(), v[:, :r].contiguous()))
+    return res
 
 
 def compact_svd(a, rank_tol: float = DEFAULT_RANK_TOL) -> CompactSvd:
