@@ -744,7 +744,9 @@ def stage_timings(K, facs, b, cfg, tr, n, d):
         sp = (ctypes.c_double * 8)()
         if L.load().ks_debug_richardson_apply_split(iters, sp) == 0:
             phases["apply_split"] = dict(zip(["l_load_wait", "y_phase", "sample_phase", "g_phase"],
-                                             [round(v) for v in sp[:4]]))
+                                             [round(v) for v in (sp[0], sp[1], sp[2], sp[3] + sp[7])]))
+            phases["apply_split"]["g_dmma_loop"] = round(sp[7])
+            phases["apply_split"]["g_partial_stores"] = round(sp[3])
             phases["sync_split"] = dict(zip(["reduce_fetch_wait", "norm_and_rules", "step_fetch_wait"],
                                             [round(v) for v in sp[4:7]]))
         nct = torch.cuda.get_device_properties(0).multi_processor_count

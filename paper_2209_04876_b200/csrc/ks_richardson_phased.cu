@@ -533,6 +533,7 @@ __global__ void __launch_bounds__(NT, 1) richardson_phased_kernel(PArgs a) {
             }
           }
         }
+        split(7);  // profiling: the G DMMA loop (split 3 is then the partial stores)
 #pragma unroll
         for (int i = 0; i < G_PER_W; i++)
           if (warp * G_PER_W + i < G_TILES)
