@@ -514,6 +514,22 @@ def _events_median(fn, reps, flush=None):
     return statistics.median(ts)
 
 
+def _graph_events_median(fn, reps, flush=None):
+    """As _events_median, for fn captured once into a CUDA graph and replayed: the device time of
+    its launches without the host-side launch latency (for kernels of tens of microseconds)."""
+    import torch
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(side):
+        fn()
+        with torch.cuda.graph(g, stream=side):
+            fn()
+    torch.cuda.current_stream().wait_stream(side)
+    torch.cuda.synchronize()
+    return _events_median(g.replay, reps, flush)
+
+
 def extra_c4(args, l2):
     """BASELINE config 4 at d = 64 (and the K1 pass at d = 16): n = 65536, b = default_rng(0).
     standard_normal(n^2) regenerated in HBM (34.4 GB).  The fast solve through the public API
@@ -561,6 +577,10 @@ def extra_c4(args, l2):
     k1_16 = lambda: L.call("ks_kron2_contract", D.p(f16[0]), D.p(b), n, D.p(f16[1]), n, n, 16, 16, D.p(T16),  # noqa: E731
                            D.stream())
     t_k1_16 = _events_median(k1_16, 3, lambda: flush_l2(l2))
+    X16 = torch.randn(16, 16, dtype=torch.float64, device="cuda")
+    k2_16 = lambda: L.call("ks_kron2_residual_sumsq", D.p(f16[0]), D.p(X16), D.p(f16[1]), D.p(b), n, n, n, 16, 16,  # noqa: E731
+                           D.p(o), D.stream())
+    t_k2_16 = _events_median(k2_16, 3, lambda: flush_l2(l2))
     out["clocks"] = clocks.stop()
     by = 8.0 * n * n
     fl64 = 2.0 * n * n * 64 + 2.0 * n * 64 * 64
@@ -585,7 +605,10 @@ def extra_c4(args, l2):
             "loss_pass_d64": {"us": t_k2 * 1e6, "frac_fp64": fl64 / t_k2 / 1e12 / peak, "frac_hbm": by / t_k2 / 1e9 / hbm},
             "kronmatmul_d16": {"us": t_k1_16 * 1e6, "gbs": by / t_k1_16 / 1e9, "frac_hbm": by / t_k1_16 / 1e9 / hbm,
                                "frac_fp64": fl16 / t_k1_16 / 1e12 / peak, "bound": "hbm",
-                               "note": "K1 of the exact solve at c4 d=16: 34.4 GB of b read once"}},
+                               "note": "K1 of the exact solve at c4 d=16: 34.4 GB of b read once"},
+            "loss_pass_d16": {"us": t_k2_16 * 1e6, "gbs": by / t_k2_16 / 1e9, "frac_hbm": by / t_k2_16 / 1e9 / hbm,
+                              "frac_fp64": fl16 / t_k2_16 / 1e12 / peak, "bound": "hbm",
+                              "note": "K2 (ridge_loss pass) at c4 d=16: 34.4 GB of b read once"}},
         "peaks": {"fp64_tflops": peak, "hbm_gbs": hbm, "hbm_source": hbm_src},
     })
     del b
@@ -633,15 +656,15 @@ def extra_c5(args, l2):
     T = torch.empty(16, 64, dtype=torch.float64, device="cuda")
     k13 = lambda: L.call("ks_kron3_contract", D.p(U0), D.p(U1), D.p(U2), D.p(xd), 512, 512, 64, 16, 16, 4,  # noqa: E731
                          D.p(T), D.stream())
-    t13 = _events_median(k13, 10, lambda: flush_l2(l2))
+    t13 = _graph_events_median(k13, 10, lambda: flush_l2(l2))
     k13_k1 = lambda: L.call("ks_kron2_contract", D.p(U0), D.p(B), int(B.shape[1]), D.p(Ur), 512, int(B.shape[1]),  # noqa: E731
                             16, 64, D.p(T), D.stream())
-    t13_k1 = _events_median(k13_k1, 10, lambda: flush_l2(l2))
+    t13_k1 = _graph_events_median(k13_k1, 10, lambda: flush_l2(l2))
     Xc = torch.randn(16, 64, dtype=torch.float64, device="cuda")
     o = torch.empty(1, dtype=torch.float64, device="cuda")
     k14 = lambda: L.call("ks_kron2_residual_sumsq", D.p(U0), D.p(Xc), D.p(Ur), D.p(B), int(B.shape[1]), 512,  # noqa: E731
                          int(B.shape[1]), 16, 64, D.p(o), D.stream())
-    t14 = _events_median(k14, 10, lambda: flush_l2(l2))
+    t14 = _graph_events_median(k14, 10, lambda: flush_l2(l2))
     als = {}
     for mode in ("exact", "fast"):
         _, rep = K.tucker_als(xd, rank, lam=lam, sweeps=3, solver_mode=mode, config=cfg)
@@ -658,10 +681,11 @@ def extra_c5(args, l2):
            "roofline": {"bound": "hbm", "kernel": "K13: (U0 kron U1 kron U2)^T b, one streaming pass in the "
                                                  "reference's rightmost-first order (ks_kron3_contract)",
                         "achieved": by / t13 / 1e9, "peak": hbm,
-                        "unit": "GB/s", "frac": by / t13 / 1e9 / hbm, "launch_us": t13 * 1e6, "traffic": None},
+                        "unit": "GB/s", "frac": by / t13 / 1e9 / hbm, "launch_us": t13 * 1e6,
+                        "traffic": traffic_bytes("r02_k13_ncu_full.json")},
            "kernels": {"k13_exact_core_contraction": {"us": t13 * 1e6, "frac_hbm": by / t13 / 1e9 / hbm,
                                                       "frac_fp64": fl / t13 / 1e12 / peak,
-                                                      "note": "both partial-sum launches included"},
+                                                      "note": "both launches (streaming pass + CTA-slot sum), graph replay"},
                        "k13_via_k1_right_group": {"us": t13_k1 * 1e6, "frac_hbm": by / t13_k1 / 1e9 / hbm,
                                                   "frac_fp64": fl_k1 / t13_k1 / 1e12 / peak,
                                                   "note": "round-2 start: TMA + DMMA K1 on B (U1 kron U2)"},
@@ -807,10 +831,10 @@ def count_launches(K, facs, b, cfg):
     return ours
 
 
-def traffic_bytes():
-    """DRAM bytes (read + write) per launch of the persistent Richardson kernel from the committed
-    ncu --set full capture (profiles/), or None."""
-    p = ROOT / "profiles" / "r02_richardson_ncu_full.json"
+def traffic_bytes(name="r02_richardson_ncu_full.json"):
+    """DRAM bytes (read + write) per launch of a kernel from its committed ncu --set full capture
+    (profiles/; default: the persistent Richardson kernel), or None."""
+    p = ROOT / "profiles" / name
     try:
         return json.loads(p.read_text())["dram_bytes_per_launch"]
     except (OSError, ValueError, KeyError):

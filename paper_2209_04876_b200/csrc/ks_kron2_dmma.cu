@@ -26,8 +26,6 @@ int gemm(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha, const d
 namespace {
 
 constexpr int KS_STAGES = 6;
-constexpr int CONSUMERS = 4;
-constexpr int THREADS = (CONSUMERS + 1) * 32;
 // KronMatMul: 8 consumer warps (4 row groups x 2 column halves) = 2 per SM sub-partition
 constexpr int K1_CW = 8;
 constexpr int K1_THREADS = (K1_CW + 1) * 32;
@@ -278,22 +276,26 @@ int kron2_contract_dmma(cudaStream_t st, const double* L, const double* B, int64
 // =============================================================================================
 namespace {
 
-constexpr int K2_STAGES = 3;
 constexpr int K2_BN = 32;
 
 template <int P, int BM>
 struct K2Cfg {
-  static constexpr int WM = BM / CONSUMERS;               // rows per consumer warp (32 or 16)
+  // ring depth: the narrow widths are HBM-bound and need more of b in flight per SM
+  static constexpr int STAGES = P == 16 ? 5 : P == 32 ? 4 : 3;
+  static constexpr int CW = BM / 16;                      // consumer warps: one m16 row tile each
+  static constexpr int THREADS = (CW + 1) * 32;           // + the producer warp
+  static constexpr int WM = 16;                           // rows per consumer warp
   static constexpr int B_TILE = BM * K2_BN;               // doubles: BN/16 boxes of (16 x BM)
   static constexpr int Z_TILE = K2_BN * P;                // doubles: P/16 boxes of (16 x BN)
   static constexpr int STAGE = B_TILE + Z_TILE;
-  static constexpr int L_OFF = K2_STAGES * STAGE;         // BM x P: P/16 boxes of (16 x BM)
+  static constexpr int L_OFF = STAGES * STAGE;         // BM x P: P/16 boxes of (16 x BM)
   static constexpr int BAR_OFF = L_OFF + BM * P;
-  static constexpr size_t BYTES = (size_t)BAR_OFF * 8 + 2 * (K2_STAGES + 1) * 8 + 1024 + 64;
+  static constexpr size_t BYTES = (size_t)BAR_OFF * 8 + 2 * (STAGES + 1) * 8 + 1024 + 64;
+  static_assert(BYTES <= 232448, "K2 ring fits shared memory");
 };
 
 template <int P, int BM>
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __launch_bounds__(K2Cfg<P, BM>::THREADS, 1)
     kron2_resid_kernel(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmZ,
                        const __grid_constant__ CUtensorMap tmL, int64_t nCB, int64_t total_tiles,
                        int64_t per_cta, double* __restrict__ part) {
@@ -302,8 +304,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   extern __shared__ unsigned char dyn_raw[];
   double* sm = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(dyn_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + C::BAR_OFF);
-  uint64_t* empty = full + K2_STAGES;
-  uint64_t* lfull = empty + K2_STAGES;
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* lfull = empty + C::STAGES;
   uint64_t* lempty = lfull + 1;
   __shared__ double red[8];
   double* Ls = sm + C::L_OFF;
@@ -312,18 +314,18 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int64_t s0 = (int64_t)blockIdx.x * per_cta;
   const int64_t s1 = (s0 + per_cta < total_tiles) ? s0 + per_cta : total_tiles;
   if (tid == 0) {
-    for (int s = 0; s < K2_STAGES; s++) {
+    for (int s = 0; s < C::STAGES; s++) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], CONSUMERS);
+      mbar_init(&empty[s], C::CW);
     }
     mbar_init(lfull, 1);
-    mbar_init(lempty, CONSUMERS);
+    mbar_init(lempty, C::CW);
     fence_barrier_init();
   }
   __syncthreads();
   double ssum = 0.0, scomp = 0.0;
   if (s0 < s1) {
-    if (warp == CONSUMERS) {
+    if (warp == C::CW) {
       if (lane == 0) {
         tma_prefetch(&tmB);
         tma_prefetch(&tmZ);
@@ -355,7 +357,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             cb = 0;
             rb++;
           }
-          if (++st == K2_STAGES) {
+          if (++st == C::STAGES) {
             st = 0;
             sph ^= 1u;
           }
@@ -421,7 +423,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[st]);
-        if (++st == K2_STAGES) {
+        if (++st == C::STAGES) {
           st = 0;
           sph ^= 1u;
         }
@@ -438,7 +440,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   __syncthreads();
   if (tid == 0) {
     double s = 0.0;
-    for (int w = 0; w < CONSUMERS; w++) s += red[w];
+    for (int w = 0; w < C::CW; w++) s += red[w];
     part[blockIdx.x] = s;
   }
 }
@@ -457,7 +459,7 @@ int launch_k2(cudaStream_t st, const CUtensorMap& tmB, const CUtensorMap& tmZ, c
   KS_REQUIRE(part.p, KS_ECUDA, "scratch allocation failed");
   auto kern = kron2_resid_kernel<P, BM>;
   KS_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::BYTES));
-  kern<<<grid, THREADS, C::BYTES, st>>>(tmB, tmZ, tmL, nCB, total, per, part.p);
+  kern<<<grid, C::THREADS, C::BYTES, st>>>(tmB, tmZ, tmL, nCB, total, per, part.p);
   KS_CHECK_LAUNCH();
   reduce_slots_kernel<<<1, 32, 0, st>>>(part.p, grid, 1, out);
   KS_CHECK_LAUNCH();
