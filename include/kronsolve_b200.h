@@ -126,6 +126,11 @@ int ks_sym_eig_batched(int32_t nb, const double* const* mats, int32_t d, double*
  * (the caller then counts sigma_j > rank_tol * sigma_0 itself, e.g. for several factors at once). */
 int ks_compact_svd(const double* A, int64_t n, int32_t d, double rank_tol, double* U,
                    double* sigma, double* V, int32_t* rank, void* stream);
+/* The same without any host synchronisation (CUDA-graph capturable): no rank, and the QR's
+ * CholeskyQR2 status words go to info_dev (2 x int32, device; nonzero = declined, the result is
+ * undefined and the caller redoes it with ks_compact_svd). */
+int ks_compact_svd_async(const double* A, int64_t n, int32_t d, double rank_tol, double* U,
+                         double* sigma, double* V, int32_t* info_dev, void* stream);
 
 /* ---------------------------------------------------------------- NumPy-exact random streams */
 

@@ -65,6 +65,7 @@ _SIGS = {
                              POINTER(c_int32), POINTER(c_int32), _p], ctypes.c_int),
     "ks_sym_eig_batched": ([_i32, _p, _i32, _p, _p, _p], ctypes.c_int),
     "ks_compact_svd": ([_p, _i64, _i32, _d, _p, _p, _p, POINTER(c_int32), _p], ctypes.c_int),
+    "ks_compact_svd_async": ([_p, _i64, _i32, _d, _p, _p, _p, _p, _p], ctypes.c_int),
     "ks_inverse_small": ([_p, _i32, _p, _p, _p], ctypes.c_int),
     "ks_pcg64_random": ([c_uint64, c_uint64, c_uint64, c_uint64, c_uint64, _i64, _p, _p], ctypes.c_int),
     "ks_pcg64_standard_normal": ([c_uint64, c_uint64, c_uint64, c_uint64, _i64, _d, _p, _p, _p, _p,

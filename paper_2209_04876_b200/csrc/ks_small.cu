@@ -844,12 +844,20 @@ __global__ void inverse_small_kernel(const double* __restrict__ M, int d, double
 namespace ks {
 
 int chol_qr2_r(cudaStream_t st, const double* A, int64_t n, int d, double* R, int* ok, double* Rinv);
+int chol_qr2_r_async(cudaStream_t st, const double* A, int64_t n, int d, double* R, double* Rinv,
+                     int32_t* info_dev);
 
-int qr_r(cudaStream_t st, const double* A, int64_t n, int d, double* R) {
+// info_dev (device, 2 x int32, may be null): the CholeskyQR2 path runs without its host check and
+// leaves its status words there (nonzero: R undefined, the caller redoes the factorisation); the
+// Householder path zeroes them.  Null: the check synchronises and falls back to Householder itself.
+int qr_r(cudaStream_t st, const double* A, int64_t n, int d, double* R, int32_t* info_dev = nullptr) {
   KS_REQUIRE(d >= 1 && d <= 128, KS_ESIZE, "qr_r supports 1 <= d <= 128 (got %d)", d);
   // tall and well-conditioned: CholeskyQR2 (two Gram passes + one streaming triangular solve,
   // ks_cholqr.cu); otherwise Householder TSQR below
-  if (n >= 4 * (int64_t)d && !ks::env(ks::ENV_TSQR)) {
+  const bool cq = n >= 4 * (int64_t)d && !ks::env(ks::ENV_TSQR);
+  if (info_dev && cq) return chol_qr2_r_async(st, A, n, d, R, nullptr, info_dev);
+  if (info_dev) KS_TRY_CUDA(cudaMemsetAsync(info_dev, 0, 2 * sizeof(int32_t), st));
+  if (cq) {
     int ok = 0;
     int rc = chol_qr2_r(st, A, n, d, R, &ok, nullptr);
     if (rc) return rc;
@@ -1097,10 +1105,10 @@ int svd_small(cudaStream_t st, const double* M, int d, double* sigma, double* V,
 
 // Thin SVD of A (n x d) with n >= d: R = qr(A); (sigma, V) = svd(R); U = A V Sigma^-1.
 static int thin_svd_tall(cudaStream_t st, const double* A, int64_t n, int d, double rank_tol,
-                         double* U, double* sigma, double* V) {
+                         double* U, double* sigma, double* V, int32_t* info_dev = nullptr) {
   Scratch<double> R((int64_t)d * d, st);
   KS_REQUIRE(R.p, KS_ECUDA, "scratch allocation failed");
-  int rc = qr_r(st, A, n, d, R.p);
+  int rc = qr_r(st, A, n, d, R.p, info_dev);
   if (rc) return rc;
   rc = svd_small(st, R.p, d, sigma, V, 1);
   if (rc) return rc;
@@ -1149,17 +1157,33 @@ extern "C" int ks_svd_small_batched(const double* M, int32_t batch, int32_t d, d
   return ks::svd_small((cudaStream_t)stream, M, d, sigma, V, batch);
 }
 
+static int compact_svd_impl(const double* A, int64_t n, int32_t d, double rank_tol, double* U, double* sigma,
+                            double* V, int32_t* rank, int32_t* info_dev, cudaStream_t st);
+
 // U: n x min(n,d)... to keep the ABI simple the caller provides U (n x k), sigma (k), V (d x k)
 // with k = min(n, d); columns past the rank are zero.
 extern "C" int ks_compact_svd(const double* A, int64_t n, int32_t d, double rank_tol, double* U,
                               double* sigma, double* V, int32_t* rank, void* stream) {
-  cudaStream_t st = (cudaStream_t)stream;
+  return compact_svd_impl(A, n, d, rank_tol, U, sigma, V, rank, nullptr, (cudaStream_t)stream);
+}
+
+// Fully asynchronous form (CUDA-graph capturable): no rank read-back, and the QR's CholeskyQR2
+// status words go to info_dev (2 x int32 on the device; nonzero = that factorisation declined and
+// the result is undefined -- the caller redoes it with ks_compact_svd).
+extern "C" int ks_compact_svd_async(const double* A, int64_t n, int32_t d, double rank_tol, double* U,
+                                    double* sigma, double* V, int32_t* info_dev, void* stream) {
+  KS_REQUIRE(info_dev, KS_EINVAL, "compact_svd_async needs a device status buffer");
+  return compact_svd_impl(A, n, d, rank_tol, U, sigma, V, nullptr, info_dev, (cudaStream_t)stream);
+}
+
+static int compact_svd_impl(const double* A, int64_t n, int32_t d, double rank_tol, double* U, double* sigma,
+                            double* V, int32_t* rank, int32_t* info_dev, cudaStream_t st) {
   KS_REQUIRE(n >= 1 && d >= 1, KS_EINVAL, "compact_svd needs a non-empty matrix");
   KS_REQUIRE(rank_tol >= 0.0 && rank_tol < 1.0, KS_EINVAL, "rank_tol must be in [0, 1)");
   int rc;
   const int k = (int)ks_min64(n, d);
   if (n >= d) {
-    rc = ks::thin_svd_tall(st, A, n, d, rank_tol, U, sigma, V);
+    rc = ks::thin_svd_tall(st, A, n, d, rank_tol, U, sigma, V, info_dev);
     if (rc) return rc;
   } else {
     // A^T (d x n) = U' S V'^T  =>  A = V' S U'^T: U = V' (n x n), V = U' (d x n)
@@ -1167,7 +1191,7 @@ extern "C" int ks_compact_svd(const double* A, int64_t n, int32_t d, double rank
     KS_REQUIRE(At.p, KS_ECUDA, "scratch allocation failed");
     transpose_kernel<<<ceil_div_u(n * d, 256), 256, 0, st>>>(A, n, d, At.p);
     KS_CHECK_LAUNCH();
-    rc = ks::thin_svd_tall(st, At.p, d, (int)n, rank_tol, V, sigma, U);
+    rc = ks::thin_svd_tall(st, At.p, d, (int)n, rank_tol, V, sigma, U, info_dev);
     if (rc) return rc;
     // U holds V' (n x n) already normalised; zero columns past the rank for consistency
   }

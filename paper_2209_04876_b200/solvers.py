@@ -277,6 +277,12 @@ def _split_first(facs):
 
 
 def _ridge_loss_dev(facs: list[torch.Tensor], x: torch.Tensor, b: torch.Tensor, lam: float) -> float:
+    r2, x2 = _ridge_loss_parts(facs, x, b).cpu().tolist()
+    return float(r2 + lam * x2)
+
+
+def _ridge_loss_parts(facs: list[torch.Tensor], x: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
+    """[||K x - b||^2, ||x||^2] on the device (no host round trip)."""
     out = D.empty(2)
     rows = [int(a.shape[0]) for a in facs]
     cols = [int(a.shape[1]) for a in facs]
@@ -291,8 +297,7 @@ def _ridge_loss_dev(facs: list[torch.Tensor], x: torch.Tensor, b: torch.Tensor, 
         kx = _kron_apply_dev(facs, x.reshape(-1, 1).contiguous())[:, 0]
         _lib.call("ks_sumsq_diff", D.p(kx), D.p(b), kx.numel(), D.p(out[0:1]), D.stream())
     _lib.call("ks_sumsq_diff", D.p(x), D.p(None), x.numel(), D.p(out[1:2]), D.stream())
-    r2, x2 = out.cpu().tolist()
-    return float(r2 + lam * x2)
+    return out
 
 
 def ridge_loss(factors: Sequence, x, b, lam: float) -> float:
@@ -332,7 +337,11 @@ def _validated_problem(factors, b):
 
 
 def _exact_solve_dev(facs: list[torch.Tensor], bt: torch.Tensor, lam: float) -> torch.Tensor:
-    svds = _compact_svds_dev(facs, 1e-10)
+    return _exact_solve_svds(facs, bt, lam, _compact_svds_dev(facs, 1e-10))
+
+
+def _exact_solve_svds(facs: list[torch.Tensor], bt: torch.Tensor, lam: float, svds) -> torch.Tensor:
+    """The exact solve after the factors' compact SVDs (solvers.py:312-318): no host round trip."""
     us = [s[0] for s in svds]
     ranks = [int(s[1].numel()) for s in svds]
     if min(ranks) == 0:
@@ -367,6 +376,11 @@ def _exact_solve_dev(facs: list[torch.Tensor], bt: torch.Tensor, lam: float) -> 
 def kronmatmul_svd_solve(factors: Sequence, b, lam: float) -> SolveReport:
     """Exact ridge solution from factor SVDs and implicit Kronecker products (solvers.py:302-320)."""
     host = not D.on_device(b)
+    if not host and lam >= 0:
+        got = _exact_solve_graph(factors, b, lam)
+        if got is not None:
+            x, loss, wall = got
+            return SolveReport(solution=x, loss=loss, iterations=0, sample_count=0, wall_time=wall)
     facs, rows, cols = _validated_problem(factors, b)
     if lam < 0:
         raise InvalidInputError(f"lambda must be >= 0, got {lam}")
@@ -378,6 +392,117 @@ def kronmatmul_svd_solve(factors: Sequence, b, lam: float) -> SolveReport:
     wall = time.perf_counter() - t0
     loss = _ridge_loss_dev(facs, x, bt, lam)
     return SolveReport(solution=D.out(x, host), loss=loss, iterations=0, sample_count=0, wall_time=wall)
+
+
+class _ExactGraph:
+    """Captured exact solve (compact SVDs, the n-pass, scaling, back-transform, loss) for one key:
+    the factors are copied into the entry's own buffers before every replay (the Tucker ALS passes
+    new factor tensors on every sweep), b is read in place (keyed by its address)."""
+
+    def __init__(self, ranks):
+        self.ranks = ranks
+        self.graph = None
+        self.facs = None
+        self.out = None
+
+
+_EXACT_GRAPHS: dict = {}
+
+
+def _exact_graph_key(facs, bt, lam):
+    if not (_USE_GRAPHS[0] and bt.is_cuda and bt.dtype == torch.float64 and bt.is_contiguous()):
+        return None
+    if any(a.dtype != torch.float64 for a in facs) or min(min(int(x) for x in a.shape) for a in facs) == 0:
+        return None
+    return (_state.thread_key(), torch.cuda.current_device(), torch.cuda.current_stream().cuda_stream,
+            tuple(tuple(a.shape) for a in facs), (bt.data_ptr(), bt.numel()), float(lam))
+
+
+def _exact_solve_graph(factors, b, lam):
+    """(x, loss, wall) of the exact solve from a replayed graph, or None: the eager path then runs
+    (first sight of the key -- it records the factors' ranks --, a rank that moved, a declined
+    CholeskyQR2, or any input the eager validation has to reject in the reference's order).  The
+    factors' finite / nonzero validation is a graph node; its flags lead the one read-back and raise
+    the reference's errors (solvers.py:265-274) before any result is returned."""
+    if not all(isinstance(a, torch.Tensor) and a.is_cuda for a in factors) or len(factors) == 0:
+        return None
+    facs = list(factors)
+    if any(a.ndim != 2 for a in facs):
+        return None
+    rows, _ = kron_operator_shape(facs)
+    if int(b.numel()) != rows:
+        return None
+    bt = b.reshape(-1)
+    key = _exact_graph_key(facs, bt, lam)
+    if key is None:
+        return None
+    entry = _state.cache_get(_EXACT_GRAPHS, key)
+    if entry is None:
+        svds = _compact_svds_dev(facs, 1e-10)
+        _state.cache_put(_EXACT_GRAPHS, key, _ExactGraph([int(sv[1].numel()) for sv in svds]), _GRAPH_CAP)
+        return None
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    if entry.graph is None:
+        entry.facs = [torch.empty_like(a) for a in facs]
+        for dst, a in zip(entry.facs, facs):
+            dst.copy_(a)
+        g = torch.cuda.CUDAGraph()
+        with GATE.capture() as ok:
+            if not ok:
+                return None
+            try:
+                with torch.cuda.graph(g, capture_error_mode=CAPTURE_MODE):
+                    flags = torch.zeros(len(facs), 2, dtype=torch.int32, device=D.dev())
+                    for n, a in enumerate(entry.facs):
+                        _lib.call("ks_check_finite_nonzero", D.p(a), a.numel(), D.p(flags[n]), D.stream())
+                    svds = []
+                    info = torch.zeros(2 * len(facs), dtype=torch.int32, device=D.dev())
+                    for i, (a, r) in enumerate(zip(entry.facs, entry.ranks)):
+                        n, d = int(a.shape[0]), int(a.shape[1])
+                        k = min(n, d)
+                        u, sg, v = D.empty(n, k), D.empty(k), D.empty(d, k)
+                        _lib.call("ks_compact_svd_async", D.p(a), n, d, 1e-10, D.p(u), D.p(sg), D.p(v),
+                                  D.p(info[2 * i:2 * i + 2]), D.stream())
+                        svds.append((u[:, :r].contiguous(), sg[:r].contiguous(), v[:, :r].contiguous(), sg))
+                    x = _exact_solve_svds(entry.facs, bt, lam, svds)
+                    parts = _ridge_loss_parts(entry.facs, x, bt)
+                    # one read-back: the loss parts, the QR status words, every factor's singular
+                    # values (the ranks check)
+                    entry.out = {"x": x, "back": torch.cat([flags.reshape(-1).to(torch.float64), parts,
+                                                            info.to(torch.float64)] + [sv[3] for sv in svds])}
+            except Exception:
+                _state.cache_drop(_EXACT_GRAPHS, key)
+                raise
+        entry.graph = g
+    else:
+        for dst, a in zip(entry.facs, facs):
+            dst.copy_(a)
+    entry.graph.replay()
+    x = entry.out["x"].clone()
+    back = entry.out["back"].cpu().tolist()
+    wall = time.perf_counter() - t0
+    nf = len(facs)
+    fl = back[:2 * nf]
+    for n in range(nf):
+        if fl[2 * n]:
+            raise InvalidInputError(f"factor {n} contains non-finite entries")
+    for n in range(nf):
+        if not fl[2 * n + 1]:
+            raise InvalidInputError(f"factor {n} is identically zero")
+    back = back[2 * nf:]
+    if any(v != 0.0 for v in back[2:2 + 2 * nf]):  # a CholeskyQR2 declined: Householder, eagerly
+        _state.cache_drop(_EXACT_GRAPHS, key)
+        return None
+    off = 2 + 2 * nf
+    for a, r in zip(facs, entry.ranks):
+        k = min(int(a.shape[0]), int(a.shape[1]))
+        h = back[off:off + k]
+        off += k
+        if (sum(1 for v in h if v > 1e-10 * h[0]) if h[0] > 0.0 else 0) != r:
+            _state.cache_drop(_EXACT_GRAPHS, key)  # the numerical rank moved: recompute eagerly
+            return None
+    return x, float(back[0] + lam * back[1]), wall
 
 
 def exact_factor_scores(factors: Sequence, caches: Sequence[FactorCache] | None = None) -> list[LeverageScores]:

@@ -458,3 +458,49 @@ def test_concurrent_solves_on_threads_match_serial():
                                                                   with_loss=False), range(4)))
     for k in range(4):
         np.testing.assert_array_equal(host[k].solution, serial[k].solution.cpu().numpy())
+
+
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_exact_solve_graph_matches_eager(golden, name):
+    """kronmatmul_svd_solve with device-resident inputs: first call eager (records the factors'
+    numerical ranks), then one captured graph replayed with the factors copied into its own buffers
+    -- bit-identical to the eager solve, equal to the reference's exact x / loss, and a replay on NEW
+    factor tensors of the same shapes (the Tucker ALS pattern) equals the eager solve on them."""
+    import paper_2209_04876_b200 as K
+    from paper_2209_04876_b200 import solvers as S
+    n, d = CASES[name]
+    g = golden(name)
+    facs, b = O.synth_regression(n, d, 2, 0)
+    fd = [torch.tensor(a, device="cuda") for a in facs]
+    bd = torch.tensor(b, device="cuda")
+    S._EXACT_GRAPHS.clear()
+    S._USE_GRAPHS[0] = False
+    try:
+        ref = K.kronmatmul_svd_solve(fd, bd, 1e-3)  # eager
+    finally:
+        S._USE_GRAPHS[0] = True
+    outs = [K.kronmatmul_svd_solve(fd, bd, 1e-3) for _ in range(3)]  # eager (ranks), capture, replay
+    assert len(S._EXACT_GRAPHS) == 1 and next(iter(S._EXACT_GRAPHS.values())).graph is not None
+    for rep in outs:
+        assert torch.equal(rep.solution, ref.solution)
+        assert rep.loss == ref.loss
+    assert rel(outs[-1].solution, g["exact_x"]) <= 1e-9
+    assert abs(outs[-1].loss - float(g["opt"])) <= 1e-9 * float(g["opt"])
+    # new factor tensors, same shapes: the replay copies them in
+    f2 = [a * 1.5 + 0.01 for a in fd]
+    got = K.kronmatmul_svd_solve(f2, bd, 1e-3)
+    S._USE_GRAPHS[0] = False
+    try:
+        want = K.kronmatmul_svd_solve(f2, bd, 1e-3)
+    finally:
+        S._USE_GRAPHS[0] = True
+    assert torch.equal(got.solution, want.solution) and got.loss == want.loss
+    # the validation rides in the graph: a replay on non-finite / all-zero factors raises the
+    # reference's errors (solvers.py:265-274)
+    from paper_2209_04876_b200.errors import InvalidInputError
+    bad = fd[0].clone()
+    bad[3, 1] = float("nan")
+    with pytest.raises(InvalidInputError, match="factor 0 contains non-finite entries"):
+        K.kronmatmul_svd_solve([bad, fd[1]], bd, 1e-3)
+    with pytest.raises(InvalidInputError, match="factor 1 is identically zero"):
+        K.kronmatmul_svd_solve([fd[0], torch.zeros_like(fd[1])], bd, 1e-3)
