@@ -629,9 +629,17 @@ __global__ void __launch_bounds__(NT, 1) richardson_phased_kernel(PArgs a) {
     auxphase ^= 1;
     split(6);
     double sq = 0.0;
-    for (int e = tid; e < NE; e += NT) {
-      const double v = AUXs[(e / DR) * DRP + e % DR];
-      sq = fma(v, v, sq);
+    {  // the same order as a strided loop, loads issued together
+      constexpr int NPT = (NE + NT - 1) / NT;
+      double sv[NPT];
+#pragma unroll
+      for (int i = 0; i < NPT; i++) {
+        const int e = tid + i * NT;
+        sv[i] = e < NE ? AUXs[(e / DR) * DRP + e % DR] : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < NPT; i++)
+        if (tid + i * NT < NE) sq = fma(sv[i], sv[i], sq);
     }
     const double nrm = sqrt(block_sum(sq, Ws + 192));
     if (rp) {  // tol = residual_tol * ||P rhs|| (solvers.py:212-214)
