@@ -562,6 +562,8 @@ def extra_c4(args, l2):
         if S._LAST_LOOP_EVENTS[0] is not None:
             l0, l1 = S._LAST_LOOP_EVENTS[0]
             loop_us.append(l0.elapsed_time(l1) * 1e3)
+    for _ in range(2):  # first sight of the key (eager, records the ranks), then the graph capture
+        K.kronmatmul_svd_solve(facs, b, PARAMS["lam"])
     t_exact = _events_median(lambda: K.kronmatmul_svd_solve(facs, b, PARAMS["lam"]), 3, lambda: flush_l2(l2))
     T = torch.empty(64, 64, dtype=torch.float64, device="cuda")
     k1 = lambda: L.call("ks_kron2_contract", D.p(facs[0]), D.p(b), n, D.p(facs[1]), n, n, 64, 64, D.p(T),  # noqa: E731

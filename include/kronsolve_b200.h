@@ -69,6 +69,11 @@ int ks_kron_mat_mul(int32_t nf, const double* const* factors, const int64_t* row
  * The n^2 pass of kronmatmul_svd_solve: kron_mat_mul([U1^T, U2^T], b) (solvers.py:314). */
 int ks_kron2_contract(const double* L, const double* B, int64_t ldb, const double* R,
                       int64_t m, int64_t k, int32_t p, int32_t q, double* T, void* stream);
+/* K1 with ||B||^2 from the same pass (bsq: one device double).  The exact solve's loss then follows
+ * from ||b||^2 - sum_k s_k^2 t_k^2 / (s_k^2 + lam) without a second pass over b (solvers.py:318). */
+int ks_kron2_contract_sumsq(const double* L, const double* B, int64_t ldb, const double* R,
+                            int64_t m, int64_t k, int32_t p, int32_t q, double* T, double* bsq,
+                            void* stream);
 
 /* K13: T (R0 x R1 R2) = (U0 kron U1 kron U2)^T b for the n0 x n1 x n2 tensor b, one streaming pass
  * over b in the reference's rightmost-first order (kron.py:66-77 at N = 3, reached from the Tucker

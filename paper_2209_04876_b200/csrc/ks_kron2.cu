@@ -17,7 +17,8 @@ int gemm_resid_sumsq(cudaStream_t st, int64_t M, int64_t N, int64_t K, double al
                      const double* A, int64_t a_rs, int64_t a_cs, const double* B, int64_t b_rs,
                      int64_t b_cs, const double* C, int64_t c_rs, int64_t c_cs, double* out);
 int kron2_contract_dmma(cudaStream_t st, const double* L, const double* B, int64_t ldb, const double* R,
-                        int64_t m, int64_t k, int p, int q, double* T);
+                        int64_t m, int64_t k, int p, int q, double* T, double* bsq);
+int sumsq_diff(cudaStream_t st, const double* a, const double* b, int64_t n, double* out);
 int kron2_residual_dmma(cudaStream_t st, const double* L, const double* X, const double* R, const double* B,
                         int64_t ldb, int64_t m, int64_t k, int p, int q, double* out);
 }
@@ -27,15 +28,35 @@ static bool generic_forced() {
   return e && e[0] == 'g';
 }
 
+static int kron2_contract_impl(const double* L, const double* B, int64_t ldb, const double* R, int64_t m,
+                               int64_t k, int32_t p, int32_t q, double* T, double* bsq, cudaStream_t st);
+
 // T = L^T (B R)
 extern "C" int ks_kron2_contract(const double* L, const double* B, int64_t ldb, const double* R,
                                  int64_t m, int64_t k, int32_t p, int32_t q, double* T,
                                  void* stream) {
-  cudaStream_t st = (cudaStream_t)stream;
+  return kron2_contract_impl(L, B, ldb, R, m, k, p, q, T, nullptr, (cudaStream_t)stream);
+}
+
+// T = L^T (B R) and bsq[0] = ||B||^2 from the same pass over B
+extern "C" int ks_kron2_contract_sumsq(const double* L, const double* B, int64_t ldb, const double* R,
+                                       int64_t m, int64_t k, int32_t p, int32_t q, double* T, double* bsq,
+                                       void* stream) {
+  KS_REQUIRE(bsq, KS_EINVAL, "kron2_contract_sumsq needs an output for ||B||^2");
+  return kron2_contract_impl(L, B, ldb, R, m, k, p, q, T, bsq, (cudaStream_t)stream);
+}
+
+static int kron2_contract_impl(const double* L, const double* B, int64_t ldb, const double* R, int64_t m,
+                               int64_t k, int32_t p, int32_t q, double* T, double* bsq, cudaStream_t st) {
   KS_REQUIRE(p >= 1 && q >= 1 && p <= 128 && q <= 128, KS_ESIZE, "contract widths must be <= 128");
   if (!generic_forced()) {
-    const int rc = ks::kron2_contract_dmma(st, L, B, ldb, R, m, k, p, q, T);
+    const int rc = ks::kron2_contract_dmma(st, L, B, ldb, R, m, k, p, q, T, bsq);
     if (rc >= 0) return rc;
+  }
+  if (bsq) {  // generic path: a separate pass (contiguous B only)
+    KS_REQUIRE(ldb == k, KS_EINVAL, "kron2_contract_sumsq: generic path needs ldb == k");
+    const int rc0 = ks::sumsq_diff(st, B, nullptr, m * k, bsq);
+    if (rc0) return rc0;
   }
   ks::Scratch<double> P(m * q, st);
   KS_REQUIRE(P.p, KS_ECUDA, "scratch allocation failed");

@@ -46,7 +46,8 @@ template <int Q, int WM>
 __global__ void __launch_bounds__(K1_THREADS, 1)
     kron2_contract_kernel(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmR,
                           const double* __restrict__ L, int64_t m, int p, int q, int64_t nKS,
-                          int64_t total_steps, int64_t per_cta, int max_seg, double* __restrict__ part) {
+                          int64_t total_steps, int64_t per_cta, int max_seg, double* __restrict__ part,
+                          double* __restrict__ sqpart) {
   using C = K1Cfg<Q, WM>;
   constexpr int BM = C::BM;
   constexpr int MT = WM / 16, NT = Q / 16;
@@ -108,6 +109,10 @@ __global__ void __launch_bounds__(K1_THREADS, 1)
       for (int c = 0; c < 4; c++) acc[a][b][c] = 0.0;
 
   const int row_w = (warp & 3) * WM, col_w = (warp >> 2) * (Q / 2);
+  // ||B||^2 on the side (sqpart != null): the column-half-0 warps see every element of B exactly once
+  // in their A fragments
+  const bool sq_on = sqpart != nullptr && col_w == 0;
+  double sq = 0.0;
   int st = 0;
   uint32_t ph = 0u;
   int64_t rb = s0 / nKS, kk = s0 - rb * nKS;  // advanced incrementally below
@@ -122,6 +127,10 @@ __global__ void __launch_bounds__(K1_THREADS, 1)
       for (int a = 0; a < MT; a++) {
         af[a][0] = Bs[swz128(row_w + a * 16 + g, k0 + t4)];
         af[a][1] = Bs[swz128(row_w + a * 16 + g + 8, k0 + t4)];
+      }
+      if (sq_on) {
+#pragma unroll
+        for (int a = 0; a < MT; a++) sq = fma(af[a][1], af[a][1], fma(af[a][0], af[a][0], sq));
       }
 #pragma unroll
       for (int b = 0; b < NT; b++) bf[b] = Rs[swz128(col_w + b * 8 + g, k0 + t4)];
@@ -189,6 +198,17 @@ __global__ void __launch_bounds__(K1_THREADS, 1)
     }
     if (row_end) rb++;
   }
+  if (sqpart) {  // this CTA's share of ||B||^2: fixed-order warp and CTA sums
+    __shared__ double sqs[K1_CW];
+    sq = warp_sum(sq);
+    if (lane == 0) sqs[warp] = sq;
+    named_bar_sync(1, K1_CW * 32);
+    if (tid == 0) {
+      double t = 0.0;
+      for (int w = 0; w < K1_CW; w++) t += sqs[w];
+      sqpart[blockIdx.x] = t;
+    }
+  }
 }
 
 // T[e] = sum over slots (fixed order), warp per output element
@@ -213,7 +233,7 @@ __global__ void transpose_kernel_rq(const double* __restrict__ a, int64_t rows, 
 
 template <int Q, int WM>
 int launch_k1(cudaStream_t st, const CUtensorMap& tmB, const CUtensorMap& tmR, const double* L, int64_t m,
-              int p, int q, int64_t k, double* T) {
+              int p, int q, int64_t k, double* T, double* bsq) {
   using C = K1Cfg<Q, WM>;
   const int64_t nRB = (m + C::BM - 1) / C::BM;
   const int64_t nKS = (k + 15) / 16;
@@ -227,13 +247,22 @@ int launch_k1(cudaStream_t st, const CUtensorMap& tmB, const CUtensorMap& tmR, c
   ks::Scratch<double> part(nslots * p * q, st);
   KS_REQUIRE(part.p, KS_ECUDA, "scratch allocation failed");
   KS_TRY_CUDA(cudaMemsetAsync(part.p, 0, sizeof(double) * nslots * p * q, st));
+  ks::Scratch<double> sqp(bsq ? grid : 0, st);
+  if (bsq) {
+    KS_REQUIRE(sqp.p, KS_ECUDA, "scratch allocation failed");
+    KS_TRY_CUDA(cudaMemsetAsync(sqp.p, 0, sizeof(double) * grid, st));
+  }
   auto kern = kron2_contract_kernel<Q, WM>;
   KS_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::BYTES));
-  kern<<<grid, K1_THREADS, C::BYTES, st>>>(tmB, tmR, L, m, p, q, nKS, total, per, max_seg, part.p);
+  kern<<<grid, K1_THREADS, C::BYTES, st>>>(tmB, tmR, L, m, p, q, nKS, total, per, max_seg, part.p, sqp.p);
   KS_CHECK_LAUNCH();
   const int64_t count = (int64_t)p * q;
   reduce_slots_kernel<<<ceil_div_u(count * 32, 256), 256, 0, st>>>(part.p, nslots, count, T);
   KS_CHECK_LAUNCH();
+  if (bsq) {
+    reduce_slots_kernel<<<1, 32, 0, st>>>(sqp.p, grid, 1, bsq);
+    KS_CHECK_LAUNCH();
+  }
   return KS_OK;
 }
 
@@ -243,7 +272,7 @@ namespace ks {
 
 // Returns KS_OK if the TMA/DMMA path ran, -1 if the shapes/layout need the generic path.
 int kron2_contract_dmma(cudaStream_t st, const double* L, const double* B, int64_t ldb, const double* R,
-                        int64_t m, int64_t k, int p, int q, double* T) {
+                        int64_t m, int64_t k, int p, int q, double* T, double* bsq) {
   if (p < 1 || p > 128 || q < 1 || q > 128 || m < 1 || k < 16) return -1;
   if (((uintptr_t)B & 15) || (ldb & 1)) return -1;
   int Qp = q <= 16 ? 16 : q <= 32 ? 32 : q <= 64 ? 64 : 128;
@@ -257,10 +286,10 @@ int kron2_contract_dmma(cudaStream_t st, const double* L, const double* B, int64
   if (!make_tmap_f64(&tmB, B, (uint64_t)m, (uint64_t)k, (uint64_t)ldb, BM)) return -1;
   if (!make_tmap_f64(&tmR, Rt.p, (uint64_t)q, (uint64_t)k, (uint64_t)k, (uint32_t)Qp)) return -1;
   switch (Qp) {
-    case 16: return launch_k1<16, 32>(st, tmB, tmR, L, m, p, q, k, T);
-    case 32: return launch_k1<32, 32>(st, tmB, tmR, L, m, p, q, k, T);
-    case 64: return launch_k1<64, 32>(st, tmB, tmR, L, m, p, q, k, T);
-    default: return launch_k1<128, 16>(st, tmB, tmR, L, m, p, q, k, T);
+    case 16: return launch_k1<16, 32>(st, tmB, tmR, L, m, p, q, k, T, bsq);
+    case 32: return launch_k1<32, 32>(st, tmB, tmR, L, m, p, q, k, T, bsq);
+    case 64: return launch_k1<64, 32>(st, tmB, tmR, L, m, p, q, k, T, bsq);
+    default: return launch_k1<128, 16>(st, tmB, tmR, L, m, p, q, k, T, bsq);
   }
 }
 

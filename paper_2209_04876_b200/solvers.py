@@ -340,12 +340,20 @@ def _exact_solve_dev(facs: list[torch.Tensor], bt: torch.Tensor, lam: float) -> 
     return _exact_solve_svds(facs, bt, lam, _compact_svds_dev(facs, 1e-10))
 
 
-def _exact_solve_svds(facs: list[torch.Tensor], bt: torch.Tensor, lam: float, svds) -> torch.Tensor:
-    """The exact solve after the factors' compact SVDs (solvers.py:312-318): no host round trip."""
+def _exact_solve_svds(facs: list[torch.Tensor], bt: torch.Tensor, lam: float, svds, loss_identity: list | None = None
+                      ) -> torch.Tensor:
+    """The exact solve after the factors' compact SVDs (solvers.py:312-318): no host round trip.
+
+    ``loss_identity`` (a list, optional): when the two-factor n^2 pass runs, ||b||^2 comes out of
+    the same pass and [ridge loss, ||b||^2] by the exact-solution identity
+    ||K x - b||^2 + lam ||x||^2 = ||b||^2 - sum_k s_k^2 t_k^2 / (s_k^2 + lam)   (t = U^T b, s = kron of
+    the singular values) is appended as one device tensor -- no second pass over b.  The caller
+    checks the cancellation before trusting it."""
     us = [s[0] for s in svds]
     ranks = [int(s[1].numel()) for s in svds]
     if min(ranks) == 0:
         return D.zeros(math.prod(int(a.shape[1]) for a in facs))
+    bsq = None
     rest_rows = math.prod(int(a.shape[0]) for a in facs[1:])
     rest_rank = math.prod(ranks[1:])
     nk = [int(a.shape[0]) for a in facs]
@@ -363,12 +371,20 @@ def _exact_solve_svds(facs: list[torch.Tensor], bt: torch.Tensor, lam: float, sv
         n1 = int(facs[0].shape[0])
         U0, Ur = _split_first(us)
         T = D.empty(ranks[0], rest_rank)
-        _lib.call("ks_kron2_contract", D.p(U0), D.p(bt), rest_rows, D.p(Ur.contiguous()), n1, rest_rows, ranks[0],
-                  rest_rank, D.p(T), D.stream())
+        if loss_identity is not None:
+            bsq = D.empty(1)
+            _lib.call("ks_kron2_contract_sumsq", D.p(U0), D.p(bt), rest_rows, D.p(Ur.contiguous()), n1, rest_rows,
+                      ranks[0], rest_rank, D.p(T), D.p(bsq), D.stream())
+        else:
+            _lib.call("ks_kron2_contract", D.p(U0), D.p(bt), rest_rows, D.p(Ur.contiguous()), n1, rest_rows,
+                      ranks[0], rest_rank, D.p(T), D.stream())
         t = T.reshape(-1)
     else:
         t = _kron_apply_dev([u.T.contiguous() for u in us], bt.reshape(-1, 1).contiguous())[:, 0]
     sigma = reduce(torch.kron, [s[1] for s in svds])
+    if bsq is not None:
+        s2 = sigma * sigma
+        loss_identity.append(torch.cat([bsq - torch.sum(t * t * s2 / (s2 + lam)).reshape(1), bsq]))
     t = t * (sigma / (sigma * sigma + lam))
     return _kron_apply_dev([s[2] for s in svds], t.reshape(-1, 1).contiguous())[:, 0]
 
@@ -401,6 +417,7 @@ class _ExactGraph:
 
     def __init__(self, ranks):
         self.ranks = ranks
+        self.identity = False
         self.graph = None
         self.facs = None
         self.out = None
@@ -465,8 +482,12 @@ def _exact_solve_graph(factors, b, lam):
                         _lib.call("ks_compact_svd_async", D.p(a), n, d, 1e-10, D.p(u), D.p(sg), D.p(v),
                                   D.p(info[2 * i:2 * i + 2]), D.stream())
                         svds.append((u[:, :r].contiguous(), sg[:r].contiguous(), v[:, :r].contiguous(), sg))
-                    x = _exact_solve_svds(entry.facs, bt, lam, svds)
-                    parts = _ridge_loss_parts(entry.facs, x, bt)
+                    ident = []
+                    x = _exact_solve_svds(entry.facs, bt, lam, svds, loss_identity=ident)
+                    # the loss: [identity value, ||b||^2] when the two-factor pass gave ||b||^2 (no second
+                    # pass over b), else the direct pass [||K x - b||^2, ||x||^2]
+                    entry.identity = bool(ident)
+                    parts = ident[0] if ident else _ridge_loss_parts(entry.facs, x, bt)
                     # one read-back: the loss parts, the QR status words, every factor's singular
                     # values (the ranks check)
                     entry.out = {"x": x, "back": torch.cat([flags.reshape(-1).to(torch.float64), parts,
@@ -502,7 +523,19 @@ def _exact_solve_graph(factors, b, lam):
         if (sum(1 for v in h if v > 1e-10 * h[0]) if h[0] > 0.0 else 0) != r:
             _state.cache_drop(_EXACT_GRAPHS, key)  # the numerical rank moved: recompute eagerly
             return None
-    return x, float(back[0] + lam * back[1]), wall
+    if not entry.identity:
+        return x, float(back[0] + lam * back[1]), wall
+    loss, bsq = back[0], back[1]
+    if not loss >= _IDENTITY_MIN_FRAC * bsq:
+        # more than three digits of ||b||^2 cancel (a near-exact fit): the direct pass instead
+        r2, x2 = _ridge_loss_parts(list(facs), x, bt).cpu().tolist()
+        loss = r2 + lam * x2
+    return x, float(loss), wall
+
+
+# the exact solve's loss comes from ||b||^2 - sum s^2 t^2 / (s^2 + lam) only while the loss keeps at
+# least this fraction of ||b||^2 (relative error <= ~1e-13 / fraction); below it, the direct pass
+_IDENTITY_MIN_FRAC = 1e-3
 
 
 def exact_factor_scores(factors: Sequence, caches: Sequence[FactorCache] | None = None) -> list[LeverageScores]:

@@ -504,3 +504,22 @@ def test_exact_solve_graph_matches_eager(golden, name):
         K.kronmatmul_svd_solve([bad, fd[1]], bd, 1e-3)
     with pytest.raises(InvalidInputError, match="factor 1 is identically zero"):
         K.kronmatmul_svd_solve([fd[0], torch.zeros_like(fd[1])], bd, 1e-3)
+
+
+def test_exact_solve_loss_identity(rng):
+    """With a noisy b (loss ~ ||b||^2) the replayed exact solve takes its loss from the ||b||^2 of
+    the K1 pass and the exact-solution identity ||b||^2 - sum s^2 t^2 / (s^2 + lam) (no second pass
+    over b); it agrees with the direct ridge_loss pass to 1e-12."""
+    import paper_2209_04876_b200 as K
+    from paper_2209_04876_b200 import solvers as S
+    n, d = 2048, 16
+    facs = [torch.tensor(rng.normal(1.0, math.sqrt(1e-3), (n, d)), device="cuda") for _ in range(2)]
+    bd = torch.tensor(rng.standard_normal(n * n), device="cuda")
+    S._EXACT_GRAPHS.clear()
+    reps = [K.kronmatmul_svd_solve(facs, bd, 1e-3) for _ in range(3)]  # eager, capture, replay
+    entry = next(iter(S._EXACT_GRAPHS.values()))
+    assert entry.graph is not None and entry.identity
+    direct = K.ridge_loss(facs, reps[-1].solution, bd, 1e-3)
+    for rep in reps:
+        assert abs(rep.loss - direct) <= 1e-12 * direct
+    assert torch.equal(reps[1].solution, reps[0].solution) and torch.equal(reps[2].solution, reps[0].solution)
