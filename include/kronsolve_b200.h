@@ -84,6 +84,10 @@ int ks_kron3_supported(int64_t n0, int64_t n1, int64_t n2, int32_t R0, int32_t R
 int ks_kron3_contract(const double* U0, const double* U1, const double* U2, const double* B,
                       int64_t n0, int64_t n1, int64_t n2, int32_t R0, int32_t R1, int32_t R2,
                       double* T, void* stream);
+/* K13 with ||b||^2 (bsq: one device double) from the same pass when n2 <= 64 (else a second pass). */
+int ks_kron3_contract_sumsq(const double* U0, const double* U1, const double* U2, const double* B,
+                            int64_t n0, int64_t n1, int64_t n2, int32_t R0, int32_t R1, int32_t R2,
+                            double* T, double* bsq, void* stream);
 /* Profiling aid: later K13 launches only stream b through their ring (no arithmetic). */
 int ks_debug_kron3_stream_only(int32_t on);
 

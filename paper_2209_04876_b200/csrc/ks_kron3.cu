@@ -34,6 +34,7 @@ struct K3Args {
   const double* U2;
   const double* B;
   double* part;  // grid x (R0 R1 R2)
+  double* sqpart;  // register-streaming kernel, may be null: per-CTA ||b||^2
   int64_t n0, n1, n2;
   int R0, R1, R2;
   int rows;      // (i0, i1) rows per unit (the TMA box height, a multiple of 16)
@@ -293,6 +294,7 @@ __global__ void __launch_bounds__(K3_T, 1) kron3_stream_kernel(K3Args a) {
                          : make_double2(0.0, 0.0);
     }
   };
+  double sqa = 0.0;  // this lane's share of ||b||^2 (a.sqpart)
   int64_t cur_i0 = -1;
   auto flush = [&]() {  // Pw += U0[cur_i0, :] outer S_w (this warp's S over the slab's tiles it ran)
 #pragma unroll
@@ -336,6 +338,11 @@ __global__ void __launch_bounds__(K3_T, 1) kron3_stream_kernel(K3Args a) {
         ua[ks][m][1] = ok && r1 + 8 < R1 ? __ldg(&a.U1[(i1b + row) * R1 + r1 + 8]) : 0.0;
       }
     }
+    if (a.sqpart) {  // ||b||^2 on the side: every element of b is in exactly one lane's tile loads
+#pragma unroll
+      for (int j = 0; j < NCH; j++)
+        sqa = fma(v[1][j].y, v[1][j].y, fma(v[1][j].x, v[1][j].x, fma(v[0][j].y, v[0][j].y, fma(v[0][j].x, v[0][j].x, sqa))));
+    }
     double c[4] = {0.0, 0.0, 0.0, 0.0}, d[4] = {0.0, 0.0, 0.0, 0.0};
     if (!a.stream_only) {
 #pragma unroll
@@ -374,12 +381,22 @@ __global__ void __launch_bounds__(K3_T, 1) kron3_stream_kernel(K3Args a) {
     run_tile(pb, vb);
   }
   if (cur_i0 >= 0) flush();
+  __shared__ double sqw[K3_CW];
+  if (a.sqpart) {
+    sqa = warp_sum(sqa);
+    if (lane == 0) sqw[warp] = sqa;
+  }
   __syncthreads();
   for (int e = tid; e < NP; e += K3_T) {  // the warps' partials in order
     double v = 0.0;
 #pragma unroll
     for (int w = 0; w < K3_CW; w++) v += k3s[(size_t)w * PWS + e];
     a.part[(size_t)blockIdx.x * NP + e] = v;
+  }
+  if (a.sqpart && tid == 0) {
+    double v = 0.0;
+    for (int w = 0; w < K3_CW; w++) v += sqw[w];
+    a.sqpart[blockIdx.x] = v;
   }
 }
 
@@ -399,11 +416,32 @@ extern "C" int ks_kron3_supported(int64_t n0, int64_t n1, int64_t n2, int32_t R0
          R1 <= 32 && R2 <= 8 && R1 * R2 <= 256 && R0 * R1 * R2 <= K3_PMAX * K3_CW * 32;
 }
 
+namespace ks {
+int sumsq_diff(cudaStream_t st, const double* a, const double* b, int64_t n, double* out);
+}
+
+static int kron3_contract_impl(const double* U0, const double* U1, const double* U2, const double* B, int64_t n0,
+                               int64_t n1, int64_t n2, int32_t R0, int32_t R1, int32_t R2, double* T, double* bsq,
+                               cudaStream_t st);
+
 // T (R0 x R1 R2, row-major) = (U0 kron U1 kron U2)^T b; U_k: n_k x R_k row-major, b: n0 n1 n2.
 extern "C" int ks_kron3_contract(const double* U0, const double* U1, const double* U2, const double* B,
                                  int64_t n0, int64_t n1, int64_t n2, int32_t R0, int32_t R1, int32_t R2,
                                  double* T, void* stream) {
-  cudaStream_t st = (cudaStream_t)stream;
+  return kron3_contract_impl(U0, U1, U2, B, n0, n1, n2, R0, R1, R2, T, nullptr, (cudaStream_t)stream);
+}
+
+// The same and bsq[0] = ||b||^2 (from the same pass when n2 <= 64)
+extern "C" int ks_kron3_contract_sumsq(const double* U0, const double* U1, const double* U2, const double* B,
+                                       int64_t n0, int64_t n1, int64_t n2, int32_t R0, int32_t R1, int32_t R2,
+                                       double* T, double* bsq, void* stream) {
+  KS_REQUIRE(bsq, KS_EINVAL, "kron3_contract_sumsq needs an output for ||b||^2");
+  return kron3_contract_impl(U0, U1, U2, B, n0, n1, n2, R0, R1, R2, T, bsq, (cudaStream_t)stream);
+}
+
+static int kron3_contract_impl(const double* U0, const double* U1, const double* U2, const double* B, int64_t n0,
+                               int64_t n1, int64_t n2, int32_t R0, int32_t R1, int32_t R2, double* T, double* bsq,
+                               cudaStream_t st) {
   KS_REQUIRE(ks_kron3_supported(n0, n1, n2, R0, R1, R2), KS_ESIZE, "kron3 contraction: unsupported geometry");
   KS_REQUIRE(((uintptr_t)B & 15) == 0, KS_EINVAL, "kron3 contraction: 16-byte aligned b");
   K3Args a{};
@@ -416,9 +454,10 @@ extern "C" int ks_kron3_contract(const double* U0, const double* U1, const doubl
     // register-streaming kernel: 16-row tiles over every warp of the grid
     const int64_t tiles = n0 * ((n1 + 15) / 16);
     const int grid = (int)std::min<int64_t>(ks::num_sms(), (tiles + K3_CW - 1) / K3_CW);
-    ks::Scratch<double> part((size_t)grid * np, st);
-    KS_REQUIRE(part.p, KS_ECUDA, "scratch allocation failed");
+    ks::Scratch<double> part((size_t)grid * np, st), sqp(bsq ? grid : 0, st);
+    KS_REQUIRE(part.p && (!bsq || sqp.p), KS_ECUDA, "scratch allocation failed");
     a.part = part.p;
+    a.sqpart = sqp.p;
     const size_t smem = (size_t)K3_CW * (((np + 1) & ~1) + mt1 * 128) * 8;
     int rc = KS_EINVAL;
 #define KS_K3S(NCH, MT)                                                                                        if ((int)(n2 / 8) == NCH && mt1 == MT) {                                                                       KS_TRY_CUDA(cudaFuncSetAttribute(kron3_stream_kernel<NCH, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize,                                      (int)smem));                                                                kron3_stream_kernel<NCH, MT><<<grid, K3_T, smem, st>>>(a);                                                   rc = KS_OK;                                                                                                }
@@ -429,7 +468,15 @@ extern "C" int ks_kron3_contract(const double* U0, const double* U1, const doubl
     KS_CHECK_LAUNCH();
     kron3_reduce_kernel<<<(np + 7) / 8, 256, 0, st>>>(part.p, grid, np, T);
     KS_CHECK_LAUNCH();
+    if (bsq) {
+      kron3_reduce_kernel<<<1, 256, 0, st>>>(sqp.p, grid, 1, bsq);
+      KS_CHECK_LAUNCH();
+    }
     return KS_OK;
+  }
+  if (bsq) {  // the TMA-ring kernel has no side sum: a separate pass
+    const int rc0 = ks::sumsq_diff(st, B, nullptr, n0 * n1 * n2, bsq);
+    if (rc0) return rc0;
   }
   // TMA-ring kernel (64 < n2 <= 128)
   a.rows = (int)std::min<int64_t>(K3_ROWS, (n1 + 15) / 16 * 16);  // m16 row tiles, one per compute warp

@@ -344,7 +344,7 @@ def _exact_solve_svds(facs: list[torch.Tensor], bt: torch.Tensor, lam: float, sv
                       ) -> torch.Tensor:
     """The exact solve after the factors' compact SVDs (solvers.py:312-318): no host round trip.
 
-    ``loss_identity`` (a list, optional): when the two-factor n^2 pass runs, ||b||^2 comes out of
+    ``loss_identity`` (a list, optional): when the K1 / K13 pass runs, ||b||^2 comes out of
     the same pass and [ridge loss, ||b||^2] by the exact-solution identity
     ||K x - b||^2 + lam ||x||^2 = ||b||^2 - sum_k s_k^2 t_k^2 / (s_k^2 + lam)   (t = U^T b, s = kron of
     the singular values) is appended as one device tensor -- no second pass over b.  The caller
@@ -361,8 +361,13 @@ def _exact_solve_svds(facs: list[torch.Tensor], bt: torch.Tensor, lam: float, sv
         # K13: one streaming pass over b in the reference's rightmost-first order (ks_kron3.cu)
         T = D.empty(ranks[0], ranks[1] * ranks[2])
         us3 = [u.contiguous() for u in us]
-        _lib.call("ks_kron3_contract", D.p(us3[0]), D.p(us3[1]), D.p(us3[2]), D.p(bt), nk[0], nk[1], nk[2],
-                  *ranks, D.p(T), D.stream())
+        if loss_identity is not None:
+            bsq = D.empty(1)
+            _lib.call("ks_kron3_contract_sumsq", D.p(us3[0]), D.p(us3[1]), D.p(us3[2]), D.p(bt), nk[0], nk[1],
+                      nk[2], *ranks, D.p(T), D.p(bsq), D.stream())
+        else:
+            _lib.call("ks_kron3_contract", D.p(us3[0]), D.p(us3[1]), D.p(us3[2]), D.p(bt), nk[0], nk[1], nk[2],
+                      *ranks, D.p(T), D.stream())
         t = T.reshape(-1)
     elif len(facs) >= 2 and ranks[0] <= 128 and rest_rank <= 128 and rest_rows * rest_rank <= (1 << 25):
         # the n^2 pass on the FP64 tensor pipe (TMA + DMMA K1 kernel): t = U_0^T B U_rest with

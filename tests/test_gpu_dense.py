@@ -193,6 +193,12 @@ def test_kron3_contract_matches_oracle(rng, shape, rank):
     want = O.kron_mat_mul([u.T for u in us], b)
     got = T.cpu().numpy().reshape(-1)
     assert rel(got, want) < 1e-13, rel(got, want)
+    # with ||b||^2 from the same pass (register-streaming kernel) or a second one (TMA ring)
+    T3, bsq = D.empty(rank[0], rank[1] * rank[2]), D.empty(1)
+    _lib.call("ks_kron3_contract_sumsq", D.p(U[0]), D.p(U[1]), D.p(U[2]), D.p(D.to_dev(b)), *shape, *rank, D.p(T3),
+              D.p(bsq), D.stream())
+    assert torch.equal(T3, T)
+    assert abs(float(bsq) - float(np.dot(b, b))) <= 1e-13 * float(np.dot(b, b))
     # deterministic: a second pass gives the same bits
     T2 = D.empty(rank[0], rank[1] * rank[2])
     _lib.call("ks_kron3_contract", D.p(U[0]), D.p(U[1]), D.p(U[2]), D.p(D.to_dev(b)), *shape, *rank, D.p(T2),
