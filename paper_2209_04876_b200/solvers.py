@@ -394,11 +394,12 @@ def _exact_solve_svds(facs: list[torch.Tensor], bt: torch.Tensor, lam: float, sv
     return _kron_apply_dev([s[2] for s in svds], t.reshape(-1, 1).contiguous())[:, 0]
 
 
-def kronmatmul_svd_solve(factors: Sequence, b, lam: float) -> SolveReport:
-    """Exact ridge solution from factor SVDs and implicit Kronecker products (solvers.py:302-320)."""
+def kronmatmul_svd_solve(factors: Sequence, b, lam: float, *, with_loss: bool = True) -> SolveReport:
+    """Exact ridge solution from factor SVDs and implicit Kronecker products (solvers.py:302-320).
+    ``with_loss=False`` (an extension, as for fast_kronecker_regression) skips the loss: nan."""
     host = not D.on_device(b)
     if not host and lam >= 0:
-        got = _exact_solve_graph(factors, b, lam)
+        got = _exact_solve_graph(factors, b, lam, with_loss)
         if got is not None:
             x, loss, wall = got
             return SolveReport(solution=x, loss=loss, iterations=0, sample_count=0, wall_time=wall)
@@ -411,7 +412,7 @@ def kronmatmul_svd_solve(factors: Sequence, b, lam: float) -> SolveReport:
     x = _exact_solve_dev(facs, bt, lam)
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
-    loss = _ridge_loss_dev(facs, x, bt, lam)
+    loss = _ridge_loss_dev(facs, x, bt, lam) if with_loss else float("nan")
     return SolveReport(solution=D.out(x, host), loss=loss, iterations=0, sample_count=0, wall_time=wall)
 
 
@@ -431,16 +432,16 @@ class _ExactGraph:
 _EXACT_GRAPHS: dict = {}
 
 
-def _exact_graph_key(facs, bt, lam):
+def _exact_graph_key(facs, bt, lam, with_loss=True):
     if not (_USE_GRAPHS[0] and bt.is_cuda and bt.dtype == torch.float64 and bt.is_contiguous()):
         return None
     if any(a.dtype != torch.float64 for a in facs) or min(min(int(x) for x in a.shape) for a in facs) == 0:
         return None
     return (_state.thread_key(), torch.cuda.current_device(), torch.cuda.current_stream().cuda_stream,
-            tuple(tuple(a.shape) for a in facs), (bt.data_ptr(), bt.numel()), float(lam))
+            tuple(tuple(a.shape) for a in facs), (bt.data_ptr(), bt.numel()), float(lam), bool(with_loss))
 
 
-def _exact_solve_graph(factors, b, lam):
+def _exact_solve_graph(factors, b, lam, with_loss=True):
     """(x, loss, wall) of the exact solve from a replayed graph, or None: the eager path then runs
     (first sight of the key -- it records the factors' ranks --, a rank that moved, a declined
     CholeskyQR2, or any input the eager validation has to reject in the reference's order).  The
@@ -455,7 +456,7 @@ def _exact_solve_graph(factors, b, lam):
     if int(b.numel()) != rows:
         return None
     bt = b.reshape(-1)
-    key = _exact_graph_key(facs, bt, lam)
+    key = _exact_graph_key(facs, bt, lam, with_loss)
     if key is None:
         return None
     entry = _state.cache_get(_EXACT_GRAPHS, key)
@@ -487,12 +488,15 @@ def _exact_solve_graph(factors, b, lam):
                         _lib.call("ks_compact_svd_async", D.p(a), n, d, 1e-10, D.p(u), D.p(sg), D.p(v),
                                   D.p(info[2 * i:2 * i + 2]), D.stream())
                         svds.append((u[:, :r].contiguous(), sg[:r].contiguous(), v[:, :r].contiguous(), sg))
-                    ident = []
+                    ident = [] if with_loss else None
                     x = _exact_solve_svds(entry.facs, bt, lam, svds, loss_identity=ident)
-                    # the loss: [identity value, ||b||^2] when the two-factor pass gave ||b||^2 (no second
+                    # the loss: [identity value, ||b||^2] when the K1 / K13 pass gave ||b||^2 (no second
                     # pass over b), else the direct pass [||K x - b||^2, ||x||^2]
                     entry.identity = bool(ident)
-                    parts = ident[0] if ident else _ridge_loss_parts(entry.facs, x, bt)
+                    if not with_loss:
+                        parts = torch.zeros(2, dtype=torch.float64, device=D.dev())
+                    else:
+                        parts = ident[0] if ident else _ridge_loss_parts(entry.facs, x, bt)
                     # one read-back: the loss parts, the QR status words, every factor's singular
                     # values (the ranks check)
                     entry.out = {"x": x, "back": torch.cat([flags.reshape(-1).to(torch.float64), parts,
@@ -528,6 +532,8 @@ def _exact_solve_graph(factors, b, lam):
         if (sum(1 for v in h if v > 1e-10 * h[0]) if h[0] > 0.0 else 0) != r:
             _state.cache_drop(_EXACT_GRAPHS, key)  # the numerical rank moved: recompute eagerly
             return None
+    if not with_loss:
+        return x, float("nan"), wall
     if not entry.identity:
         return x, float(back[0] + lam * back[1]), wall
     loss, bsq = back[0], back[1]

@@ -142,11 +142,12 @@ def core_update(model: TuckerModel, x, mode: str = "exact", config: RegressionCo
     xs = tuple(int(s) for s in x.shape) if hasattr(x, "shape") else np.asarray(x).shape
     if tuple(xs) != model.shape:
         raise InvalidInputError(f"tensor shape {tuple(xs)} != model shape {model.shape}")
+    # the reference's SolveReport.loss is discarded here (only the core is returned): not computed
     if mode == "exact":
-        report = kronmatmul_svd_solve(model.factors, vectorize(x), model.lam)
+        report = kronmatmul_svd_solve(model.factors, vectorize(x), model.lam, with_loss=False)
     elif mode == "fast":
         cfg = (config or RegressionConfig()).with_lam(model.lam)
-        report = fast_kronecker_regression(model.factors, vectorize(x), cfg, caches=caches)
+        report = fast_kronecker_regression(model.factors, vectorize(x), cfg, caches=caches, with_loss=False)
     else:
         raise InvalidInputError(f"unknown core update mode {mode!r}")
     return devectorize(report.solution, model.core_shape)
