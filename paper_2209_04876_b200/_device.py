@@ -19,11 +19,17 @@ F64 = torch.float64
 I64 = torch.int64
 
 
+_READY = [False]
+
+
 def require_cuda():
+    if _READY[0]:
+        return
     if not torch.cuda.is_available():
         raise RuntimeError("paper_2209_04876_b200 needs a CUDA device (B200, sm_100a); "
                            "there is no CPU fallback")
     _lib.load()
+    _READY[0] = True
 
 
 def dev() -> torch.device:
@@ -42,6 +48,8 @@ def to_dev(x, dtype=F64) -> torch.Tensor:
     """Contiguous CUDA tensor of ``dtype`` (copies host data; no-op for matching CUDA input)."""
     require_cuda()
     if isinstance(x, torch.Tensor):
+        if x.is_cuda and x.dtype == dtype and x.is_contiguous() and x.device.index == torch.cuda.current_device():
+            return x  # already where and what it needs to be (the common device-resident case)
         return x.to(device=dev(), dtype=dtype).contiguous()
     npdt = np.float64 if dtype == F64 else np.int64
     a = np.ascontiguousarray(np.asarray(x, dtype=npdt))
