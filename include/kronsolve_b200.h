@@ -88,6 +88,9 @@ int ks_kron3_contract(const double* U0, const double* U1, const double* U2, cons
 int ks_kron3_contract_sumsq(const double* U0, const double* U1, const double* U2, const double* B,
                             int64_t n0, int64_t n1, int64_t n2, int32_t R0, int32_t R1, int32_t R2,
                             double* T, double* bsq, void* stream);
+/* Profiling aid: while set (a cudaEvent_t; NULL clears it), the fused Richardson loop records this
+ * event (external) right before its persistent kernel's launch. */
+int ks_debug_loop_kernel_event(void* event);
 /* Profiling aid: later K13 launches only stream b through their ring (no arithmetic). */
 int ks_debug_kron3_stream_only(int32_t on);
 

@@ -47,6 +47,7 @@ _SIGS = {
     "ks_kron3_contract_sumsq": ([_p, _p, _p, _p, _i64, _i64, _i64, _i32, _i32, _i32, _p, _p, _p], ctypes.c_int),
     "ks_kron3_supported": ([_i64, _i64, _i64, _i32, _i32, _i32], ctypes.c_int),
     "ks_debug_kron3_stream_only": ([_i32], ctypes.c_int),
+    "ks_debug_loop_kernel_event": ([_p], ctypes.c_int),
     "ks_kron2_residual_sumsq": ([_p, _p, _p, _p, _i64, _i64, _i64, _i32, _i32, _p, _p], ctypes.c_int),
     "ks_sumsq_diff": ([_p, _p, _i64, _p, _p], ctypes.c_int),
     "ks_check_finite_nonzero": ([_p, _i64, _p, _p], ctypes.c_int),

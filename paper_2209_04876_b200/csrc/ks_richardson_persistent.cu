@@ -967,6 +967,7 @@ size_t plan_range_offset(int64_t cap) { return (size_t)cap * (sizeof(Chunk) + si
 
 static bool use_phased() { return !env(ENV_RICH_OLD); }
 static int g_prof_on = 0;  // ks_debug_richardson_profile: the profiling instantiation of the phase-separated kernel
+thread_local void* g_kernel_event = nullptr;  // ks_debug_loop_kernel_event
 
 static int launch_plan(cudaStream_t st, const ks_sketch_view* sk, int64_t ul, const int64_t* counts_dev, int dL,
                        int dR, int grid, Chunk* chunks, int64_t* cpre, int64_t* range) {
@@ -1097,6 +1098,8 @@ int richardson_persistent(cudaStream_t st, const ks_sketch_view* sk, const doubl
   a.state = statep;
   a.flags = flags.p;
   int rc;
+  if (g_kernel_event)  // profiling aid: an external event right before the persistent launch
+    KS_TRY_CUDA(cudaEventRecordWithFlags((cudaEvent_t)g_kernel_event, st, cudaEventRecordExternal));
   if (phased) rc = richardson_phased_launch(st, a, dL, dR, grid, g_prof_on != 0);
   else if (dL == 16 && dR == 16) rc = launch<16, 16>(st, a, grid);
   else if (dL == 16 && dR == 32) rc = launch<16, 32>(st, a, grid);
@@ -1121,6 +1124,14 @@ int richardson_persistent(cudaStream_t st, const ks_sketch_view* sk, const doubl
 
 }  // namespace ks
 
+
+// Profiling aid: while set, every fused loop records this (external) event on its stream right
+// before the persistent kernel's launch, after the packing launches (bench.py times the kernel alone
+// from it, the whole stage from an event before the call).  0 clears it.
+extern "C" int ks_debug_loop_kernel_event(void* ev) {
+  ks::g_kernel_event = ev;
+  return KS_OK;
+}
 
 // Profiling switch: later phase-separated loop launches run the instantiation that records CTA 0's
 // phase clocks (read by ks_debug_richardson_phases).  Off by default; never on the product path.

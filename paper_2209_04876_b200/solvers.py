@@ -723,7 +723,7 @@ class _SolveGraph:
 
 
 _SOLVE_GRAPHS: dict = {}
-_LAST_LOOP_EVENTS = TLSlot()  # this thread's (start, end) events of its last graph-replayed loop launch
+_LAST_LOOP_EVENTS = TLSlot()  # this thread's (stage start, end, kernel start) events of its last replayed loop
 _LAST_HISTORY = TLSlot()  # this thread's last fast solve: the Richardson step-norm history
 _SOLVE_STATS = {"eager": 0, "capture": 0, "replay": 0}
 _GRAPH_CAP = 16  # cached whole-solve graphs (keys are per thread and per stream)
@@ -897,15 +897,21 @@ def _solve_graph_body(facs, b, config: RegressionConfig, s: int, factor1_stream=
     state = torch.zeros(4, dtype=torch.int32, device=D.dev())
     # external events around the loop launch: readable after every replay (bench.py's roofline)
     ev0 = torch.cuda.Event(enable_timing=True, external=True)
+    evk = torch.cuda.Event(enable_timing=True, external=True)  # recorded by the C entry before the kernel
     ev1 = torch.cuda.Event(enable_timing=True, external=True)
     ev0.record()
-    _lib.call("ks_richardson_fused_async", ctypes.byref(struct), D.p(cdev), None, D.p(b_at), D.p(VL), D.p(wL),
-              D.p(VR), D.p(wR), None, float(config.lam), float(config.effective_damping), int(max_iters),
-              float(config.residual_tol), D.p(x), D.p(hist), D.p(rhs), D.p(state), D.p(plan_ws), D.stream())
+    evk.record()  # creates the event; the C entry records it again right before the persistent launch
+    _lib.load().ks_debug_loop_kernel_event(ctypes.c_void_p(evk.cuda_event))
+    try:
+        _lib.call("ks_richardson_fused_async", ctypes.byref(struct), D.p(cdev), None, D.p(b_at), D.p(VL), D.p(wL),
+                  D.p(VR), D.p(wR), None, float(config.lam), float(config.effective_damping), int(max_iters),
+                  float(config.residual_tol), D.p(x), D.p(hist), D.p(rhs), D.p(state), D.p(plan_ws), D.stream())
+    finally:
+        _lib.load().ks_debug_loop_kernel_event(None)
     ev1.record()
     _tl_event(tl, "loop end")
     _TL_CUR[0] = None
-    return dict(x=x, hist=hist, state=state, loop_events=(ev0, ev1), timeline=tl,
+    return dict(x=x, hist=hist, state=state, loop_events=(ev0, ev1, evk), timeline=tl,
                 keep=(gts, tildes, b_at, b_raw, first_raw, sd_idx, sd_val, seg, lrow, rrow, cdev, rhs, plan_ws,
                       pre_g))
 
