@@ -687,16 +687,29 @@ __device__ __forceinline__ void pack_rows_xform_body(
   const int64_t i0 = (int64_t)blockIdx.x * XF_ROWS;
   if (i0 >= n) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t4 = lane & 3;
-  for (int e = tid; e < D * D / 2; e += 256) {
-    const int r = (2 * e) / D, c = (2 * e) % D;
-    ks_cp_async8(&Vs[r * LDV + c], V + r * D + c);
-    ks_cp_async8(&Vs[r * LDV + c + 1], V + r * D + c + 1);
-  }
-  for (int e = tid; e < XF_ROWS * D; e += 256) {
-    const int r = e / D, k = e % D;
-    const int64_t i = i0 + r;
-    const bool ok = i < n;
-    ks_cp_async8(&As[r * LDA + k], ok ? src + rows[i] * ld + k : src, ok);
+  if ((((uintptr_t)src | (uintptr_t)V | (uintptr_t)(ld * 8)) & 15) == 0) {  // 16-byte copies
+    for (int e = tid; e < D * D / 2; e += 256) {
+      const int r = (2 * e) / D, c = (2 * e) % D;
+      ks_cp_async16z(&Vs[r * LDV + c], V + r * D + c, true);
+    }
+    for (int e = tid; e < XF_ROWS * D / 2; e += 256) {
+      const int r = (2 * e) / D, k = (2 * e) % D;
+      const int64_t i = i0 + r;
+      const bool ok = i < n;
+      ks_cp_async16z(&As[r * LDA + k], ok ? src + rows[i] * ld + k : src, ok);
+    }
+  } else {
+    for (int e = tid; e < D * D / 2; e += 256) {
+      const int r = (2 * e) / D, c = (2 * e) % D;
+      ks_cp_async8(&Vs[r * LDV + c], V + r * D + c);
+      ks_cp_async8(&Vs[r * LDV + c + 1], V + r * D + c + 1);
+    }
+    for (int e = tid; e < XF_ROWS * D; e += 256) {
+      const int r = e / D, k = e % D;
+      const int64_t i = i0 + r;
+      const bool ok = i < n;
+      ks_cp_async8(&As[r * LDA + k], ok ? src + rows[i] * ld + k : src, ok);
+    }
   }
   ks_cp_async_wait_all();
   __syncthreads();
@@ -721,14 +734,8 @@ __device__ __forceinline__ void pack_rows_xform_body(
     if (tile < TILES) {
       const int m0 = (tile / (D / 8)) * 16, n0 = (tile % (D / 8)) * 8;
       const int64_t r0 = i0 + m0 + g, r1 = r0 + 8;
-      if (r0 < n) {
-        dst[r0 * dp + n0 + 2 * t4] = acc[q][0];
-        dst[r0 * dp + n0 + 2 * t4 + 1] = acc[q][1];
-      }
-      if (r1 < n) {
-        dst[r1 * dp + n0 + 2 * t4] = acc[q][2];
-        dst[r1 * dp + n0 + 2 * t4 + 1] = acc[q][3];
-      }
+      if (r0 < n) *reinterpret_cast<double2*>(&dst[r0 * dp + n0 + 2 * t4]) = make_double2(acc[q][0], acc[q][1]);
+      if (r1 < n) *reinterpret_cast<double2*>(&dst[r1 * dp + n0 + 2 * t4]) = make_double2(acc[q][2], acc[q][3]);
     }
   }
   // padding: v_t, v_t b_t, zeros
