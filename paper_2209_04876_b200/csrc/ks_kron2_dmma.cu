@@ -42,7 +42,7 @@ struct K1Cfg {
   static constexpr size_t BYTES = (size_t)BAR_OFF * 8 + 2 * KS_STAGES * 8 + 1024;
 };
 
-template <int Q, int WM>
+template <int Q, int WM, bool SQ>
 __global__ void __launch_bounds__(K1_THREADS, 1)
     kron2_contract_kernel(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmR,
                           const double* __restrict__ L, int64_t m, int p, int q, int64_t nKS,
@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(K1_THREADS, 1)
   const int row_w = (warp & 3) * WM, col_w = (warp >> 2) * (Q / 2);
   // ||B||^2 on the side (sqpart != null): the column-half-0 warps see every element of B exactly once
   // in their A fragments
-  const bool sq_on = sqpart != nullptr && col_w == 0;
+  const bool sq_on = SQ && col_w == 0;
   double sq = 0.0;
   int st = 0;
   uint32_t ph = 0u;
@@ -128,9 +128,11 @@ __global__ void __launch_bounds__(K1_THREADS, 1)
         af[a][0] = Bs[swz128(row_w + a * 16 + g, k0 + t4)];
         af[a][1] = Bs[swz128(row_w + a * 16 + g + 8, k0 + t4)];
       }
-      if (sq_on) {
+      if constexpr (SQ) {
+        if (sq_on) {
 #pragma unroll
-        for (int a = 0; a < MT; a++) sq = fma(af[a][1], af[a][1], fma(af[a][0], af[a][0], sq));
+          for (int a = 0; a < MT; a++) sq = fma(af[a][1], af[a][1], fma(af[a][0], af[a][0], sq));
+        }
       }
 #pragma unroll
       for (int b = 0; b < NT; b++) bf[b] = Rs[swz128(col_w + b * 8 + g, k0 + t4)];
@@ -198,7 +200,7 @@ __global__ void __launch_bounds__(K1_THREADS, 1)
     }
     if (row_end) rb++;
   }
-  if (sqpart) {  // this CTA's share of ||B||^2: fixed-order warp and CTA sums
+  if constexpr (SQ) {  // this CTA's share of ||B||^2: fixed-order warp and CTA sums
     __shared__ double sqs[K1_CW];
     sq = warp_sum(sq);
     if (lane == 0) sqs[warp] = sq;
@@ -252,7 +254,8 @@ int launch_k1(cudaStream_t st, const CUtensorMap& tmB, const CUtensorMap& tmR, c
     KS_REQUIRE(sqp.p, KS_ECUDA, "scratch allocation failed");
     KS_TRY_CUDA(cudaMemsetAsync(sqp.p, 0, sizeof(double) * grid, st));
   }
-  auto kern = kron2_contract_kernel<Q, WM>;
+  // the ||B||^2 side sum is its own instantiation: the plain contraction's kernel is untouched by it
+  auto kern = bsq ? kron2_contract_kernel<Q, WM, true> : kron2_contract_kernel<Q, WM, false>;
   KS_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::BYTES));
   kern<<<grid, K1_THREADS, C::BYTES, st>>>(tmB, tmR, L, m, p, q, nKS, total, per, max_seg, part.p, sqp.p);
   KS_CHECK_LAUNCH();
