@@ -447,11 +447,9 @@ __global__ void __launch_bounds__(K2Cfg<P, BM>::THREADS, 1)
             const double e1 = acc[a][b][1] - Bs[box * BM * 16 + swz128(r0, cc + 1)];
             const double e2 = acc[a][b][2] - Bs[box * BM * 16 + swz128(r0 + 8, cc)];
             const double e3 = acc[a][b][3] - Bs[box * BM * 16 + swz128(r0 + 8, cc + 1)];
-            const double v = fma(e0, e0, fma(e1, e1, fma(e2, e2, e3 * e3)));
-            const double y = v - scomp;
-            const double t = ssum + y;
-            scomp = (t - ssum) - y;
-            ssum = t;
+            // squares only (no cancellation): plain fixed-order sums, two chains per lane
+            if (b & 1) scomp = fma(e0, e0, fma(e1, e1, fma(e2, e2, fma(e3, e3, scomp))));
+            else ssum = fma(e0, e0, fma(e1, e1, fma(e2, e2, fma(e3, e3, ssum))));
           }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[st]);
@@ -467,7 +465,7 @@ __global__ void __launch_bounds__(K2Cfg<P, BM>::THREADS, 1)
     }
   }
   // CTA partial (consumers only contribute)
-  ssum = warp_sum(ssum);
+  ssum = warp_sum(ssum + scomp);
   if (lane == 0) red[warp] = ssum;
   __syncthreads();
   if (tid == 0) {

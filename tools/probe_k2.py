@@ -31,7 +31,8 @@ def main():
     flush = lambda: l2.fill_(1.0)  # noqa: E731
     o = torch.empty(1, dtype=torch.float64, device="cuda")
     by = 8.0 * n * n
-    for d in (16, 32, 64):
+    ds = [int(a) for a in sys.argv[1:]] or [16, 32, 64]
+    for d in ds:
         f = [1.0 + 0.03 * torch.randn(n, d, dtype=torch.float64, device="cuda", generator=g) for _ in range(2)]
         T = torch.empty(d, d, dtype=torch.float64, device="cuda")
         X = torch.randn(d, d, dtype=torch.float64, device="cuda", generator=g)
