@@ -24,14 +24,14 @@ def ev_median(fn, reps, flush):
 
 
 def main():
-    n = 32768
+    n = int(next((a[2:] for a in sys.argv[1:] if a.startswith("n=")), 32768))
     g = torch.Generator(device="cuda").manual_seed(0)
     b = torch.randn(n * n, dtype=torch.float64, device="cuda", generator=g)
     l2 = torch.empty(64 << 20, dtype=torch.float64, device="cuda")
     flush = lambda: l2.fill_(1.0)  # noqa: E731
     o = torch.empty(1, dtype=torch.float64, device="cuda")
     by = 8.0 * n * n
-    ds = [int(a) for a in sys.argv[1:]] or [16, 32, 64]
+    ds = [int(a) for a in sys.argv[1:] if not a.startswith("n=")] or [16, 32, 64]
     for d in ds:
         f = [1.0 + 0.03 * torch.randn(n, d, dtype=torch.float64, device="cuda", generator=g) for _ in range(2)]
         T = torch.empty(d, d, dtype=torch.float64, device="cuda")
