@@ -8,7 +8,7 @@ import sys
 LIB = sys.argv[1] if len(sys.argv) > 1 else "paper_2209_04876_b200/libkronsolve_b200.so"
 WANT = ["richardson_phased_kernel", "richardson_persistent_kernel", "kron2_contract_kernel", "kron2_resid_kernel",
         "jacobi_fixed_kernel", "tall_tn_kernel", "pack_rows_xform", "jl_projection_kernel", "sampler_tables_kernel",
-        "kron_explicit2_kernel", "shard_update_kernel", "gemm_kernel"]
+        "kron_explicit2_kernel", "shard_update_kernel", "gemm_kernel", "kron3_stream_kernel", "kron3_contract_kernel"]
 MN = ["DMMA", "DFMA", "UTMALDG", "UBLKCP", "LDGSTS", "SYNCS", "BAR", "LDS", "STS", "LDG", "STG", "SHFL", "RED", "ATOM"]
 
 sass = subprocess.run(["cuobjdump", "-sass", LIB], capture_output=True, text=True).stdout
