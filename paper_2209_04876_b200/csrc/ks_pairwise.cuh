@@ -20,7 +20,8 @@ __device__ double pw_leaf(const Get& get, int64_t s, int64_t len) {
 #pragma unroll
   for (int j = 0; j < 8; j++) r[j] = get(s + j);
   int64_t i = 8;
-  for (; i < len - (len % 8); i += 8) {
+#pragma unroll 4
+  for (; i < len - (len % 8); i += 8) {  // unrolled: several blocks' loads in flight
 #pragma unroll
     for (int j = 0; j < 8; j++) r[j] += get(s + i + j);
   }

@@ -41,15 +41,10 @@ __global__ void __launch_bounds__(ST_T) sampler_tables_kernel(TabArgs A) {
   double* __restrict__ probs = A.probs[f];
   double* __restrict__ cdf = A.cdf[f];
   if (tid == 0) s_bad = 0;
-  __syncthreads();
-  {
-    bool bad = false;
-    for (int64_t i = tid; i < n; i += ST_T) {
-      const double v = scores[i];
-      bad |= !(v >= 0.0) || !isfinite(v);
-    }
-    if (__syncthreads_or(bad) && tid == 0) s_bad = 1;
-  }
+  // the nonnegative / finite check rides in the pairwise pass: every element is read there exactly
+  // once by its subtree's owner (a separate strided pass would be one dependent L2 round trip per
+  // 1024 elements on this single SM)
+  bool bad = false;
   // ---- pairwise total: subtree of this thread at depth ST_D (or the leaf it falls into)
   {
     int64_t s = 0, len = n;
@@ -71,10 +66,15 @@ __global__ void __launch_bounds__(ST_T) sampler_tables_kernel(TabArgs A) {
     }
     stopd[tid] = owner ? (int8_t)depth : (int8_t)-1;
     if (owner) {
-      auto get = [&](int64_t i) { return scores[i]; };
+      auto get = [&](int64_t i) {
+        const double v = scores[i];
+        bad |= !(v >= 0.0) || !isfinite(v);
+        return v;
+      };
       slot[tid] = pw_sum_seq(get, s, len);
     }
   }
+  if (__syncthreads_or(bad) && tid == 0) s_bad = 1;
   __syncthreads();
   // combine the top ST_D levels: node (l, i) is internal iff its left-most slot descended past l
   for (int l = ST_D - 1; l >= 0; l--) {
@@ -90,7 +90,22 @@ __global__ void __launch_bounds__(ST_T) sampler_tables_kernel(TabArgs A) {
     if (!(total > 0.0)) fl |= 2;
     A.flags[f] = fl;
   }
-  for (int64_t i = tid; i < n; i += ST_T) probs[i] = scores[i] / total;
+  {  // probs = scores / total, 8 loads in flight per thread (one SM streams the whole vector)
+    constexpr int U = 8;
+    for (int64_t i0 = tid; i0 < n; i0 += (int64_t)ST_T * U) {
+      double v[U];
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const int64_t i = i0 + (int64_t)u * ST_T;
+        v[u] = i < n ? scores[i] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const int64_t i = i0 + (int64_t)u * ST_T;
+        if (i < n) probs[i] = v[u] / total;
+      }
+    }
+  }
   __syncthreads();
   if (cdf == nullptr) return;
   // ---- exact cumsum by verified block speculation.  Three block barriers per window: the
