@@ -32,11 +32,24 @@ def require_cuda():
     _READY[0] = True
 
 
+# the raw current device / stream without building torch Stream objects (every C-ABI call passes
+# the current stream; the Python wrappers cost microseconds per call on the host-bound small paths)
+_GET_DEVICE = getattr(torch._C, "_cuda_getDevice", None)
+_RAW_STREAM = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+_DEVICES: dict = {}
+
+
 def dev() -> torch.device:
-    return torch.device("cuda", torch.cuda.current_device())
+    i = _GET_DEVICE() if (_GET_DEVICE is not None and _READY[0]) else torch.cuda.current_device()
+    d = _DEVICES.get(i)
+    if d is None:
+        d = _DEVICES.setdefault(i, torch.device("cuda", i))
+    return d
 
 
 def stream() -> ctypes.c_void_p:
+    if _GET_DEVICE is not None and _RAW_STREAM is not None and _READY[0]:
+        return ctypes.c_void_p(_RAW_STREAM(_GET_DEVICE()))
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
