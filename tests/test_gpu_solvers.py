@@ -523,3 +523,27 @@ def test_exact_solve_loss_identity(rng):
     for rep in reps:
         assert abs(rep.loss - direct) <= 1e-12 * direct
     assert torch.equal(reps[1].solution, reps[0].solution) and torch.equal(reps[2].solution, reps[0].solution)
+
+
+def test_exact_solve_graph_declined_cholqr_and_no_loss(rng):
+    """An ill-conditioned factor (kappa^2 > 1e12: CholeskyQR2 declines) makes the captured exact solve
+    fall back to the eager Householder path -- results equal the eager solve bit for bit; with
+    with_loss=False (core_update's case) the solution is the same and the loss is nan."""
+    import paper_2209_04876_b200 as K
+    from paper_2209_04876_b200 import solvers as S
+    n, d = 2048, 16
+    a0 = rng.standard_normal((n, d))
+    a0[:, 3] = a0[:, 2] + 1e-9 * rng.standard_normal(n)  # nearly dependent columns
+    facs = [torch.tensor(a0, device="cuda"), torch.tensor(rng.normal(1.0, 0.03, (n, d)), device="cuda")]
+    bd = torch.tensor(rng.standard_normal(n * n), device="cuda")
+    S._USE_GRAPHS[0] = False
+    try:
+        ref = K.kronmatmul_svd_solve(facs, bd, 1e-3)
+    finally:
+        S._USE_GRAPHS[0] = True
+    S._EXACT_GRAPHS.clear()
+    outs = [K.kronmatmul_svd_solve(facs, bd, 1e-3) for _ in range(3)]
+    for rep in outs:
+        assert torch.equal(rep.solution, ref.solution) and rep.loss == ref.loss
+    nl = K.kronmatmul_svd_solve(facs, bd, 1e-3, with_loss=False)
+    assert torch.equal(nl.solution, ref.solution) and math.isnan(nl.loss)
