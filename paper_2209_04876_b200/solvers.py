@@ -424,6 +424,7 @@ class _ExactGraph:
     def __init__(self, ranks):
         self.ranks = ranks
         self.identity = False
+        self.disabled = False
         self.graph = None
         self.facs = None
         self.out = None
@@ -460,6 +461,8 @@ def _exact_solve_graph(factors, b, lam, with_loss=True):
     if key is None:
         return None
     entry = _state.cache_get(_EXACT_GRAPHS, key)
+    if entry is not None and entry.disabled:
+        return None
     if entry is None:
         svds = _compact_svds_dev(facs, 1e-10)
         _state.cache_put(_EXACT_GRAPHS, key, _ExactGraph([int(sv[1].numel()) for sv in svds]), _GRAPH_CAP)
@@ -522,7 +525,7 @@ def _exact_solve_graph(factors, b, lam, with_loss=True):
             raise InvalidInputError(f"factor {n} is identically zero")
     back = back[2 * nf:]
     if any(v != 0.0 for v in back[2:2 + 2 * nf]):  # a CholeskyQR2 declined: Householder, eagerly
-        _state.cache_drop(_EXACT_GRAPHS, key)
+        entry.disabled = True  # and from now on for this key (the factorisation would decline again)
         return None
     off = 2 + 2 * nf
     for a, r in zip(facs, entry.ranks):
