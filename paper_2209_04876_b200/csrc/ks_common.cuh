@@ -13,7 +13,7 @@ void set_error(const char* fmt, ...);
 
 // Diagnostic switches (environment variables), read ONCE per process on
 // first use: no getenv on the solve path, and a captured graph cannot disagree with later calls.
-enum EnvSwitch { ENV_TALL, ENV_KRON2, ENV_RICHARDSON, ENV_NO_EIGBASIS, ENV_GRAM_SCALAR, ENV_GATHER_BLOCKS, ENV_TSQR, ENV_JACOBI_FP32, ENV_JACOBI_GENERIC, ENV_RICH_OLD, ENV_NO_DEFLATE, ENV_NO_OA, ENV_SKETCH_SORT, ENV_TALL_OLD, ENV_COUNT };
+enum EnvSwitch { ENV_TALL, ENV_KRON2, ENV_RICHARDSON, ENV_NO_EIGBASIS, ENV_GRAM_SCALAR, ENV_GATHER_BLOCKS, ENV_TSQR, ENV_JACOBI_FP32, ENV_JACOBI_GENERIC, ENV_RICH_OLD, ENV_NO_DEFLATE, ENV_NO_OA, ENV_SKETCH_SORT, ENV_TALL_OLD, ENV_TABLES_ONE_CTA, ENV_COUNT };
 const char* env(EnvSwitch id);
 int cuda_status(cudaError_t e, const char* what);
 

@@ -33,7 +33,7 @@ static std::once_flag g_env_once;
 static const char* g_env[ENV_COUNT];
 
 const char* env(EnvSwitch id) {
-  static const char* const names[ENV_COUNT] = {"KS_TALL", "KS_KRON2", "KS_RICHARDSON", "KS_NO_EIGBASIS", "KS_GRAM_SCALAR", "KS_GATHER_BLOCKS", "KS_TSQR", "KS_JACOBI_FP32", "KS_JACOBI_GENERIC", "KS_RICH_OLD", "KS_NO_DEFLATE", "KS_NO_OA", "KS_SKETCH_SORT", "KS_TALL_OLD"};
+  static const char* const names[ENV_COUNT] = {"KS_TALL", "KS_KRON2", "KS_RICHARDSON", "KS_NO_EIGBASIS", "KS_GRAM_SCALAR", "KS_GATHER_BLOCKS", "KS_TSQR", "KS_JACOBI_FP32", "KS_JACOBI_GENERIC", "KS_RICH_OLD", "KS_NO_DEFLATE", "KS_NO_OA", "KS_SKETCH_SORT", "KS_TALL_OLD", "KS_TABLES_ONE_CTA"};
   std::call_once(g_env_once, [] {
     for (int i = 0; i < ENV_COUNT; i++) g_env[i] = getenv(names[i]);
   });

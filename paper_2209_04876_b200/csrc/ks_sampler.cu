@@ -23,6 +23,7 @@ struct TabArgs {
   double* cdf[MAXF];
   int32_t* flags;
   int renorm;
+  int cdf_only;  // probs (and flags) already formed by the multi-CTA path: only the cumsum runs
 };
 
 __device__ __forceinline__ double ulp_of(double x) {
@@ -40,6 +41,7 @@ __global__ void __launch_bounds__(ST_T) sampler_tables_kernel(TabArgs A) {
   const int64_t n = A.n[f];
   double* __restrict__ probs = A.probs[f];
   double* __restrict__ cdf = A.cdf[f];
+  if (!A.cdf_only) {  // (else probs and flags were formed by the multi-CTA path)
   if (tid == 0) s_bad = 0;
   // the nonnegative / finite check rides in the pairwise pass: every element is read there exactly
   // once by its subtree's owner (a separate strided pass would be one dependent L2 round trip per
@@ -106,6 +108,7 @@ __global__ void __launch_bounds__(ST_T) sampler_tables_kernel(TabArgs A) {
       }
     }
   }
+  }  // !cdf_only
   __syncthreads();
   if (cdf == nullptr) return;
   // ---- exact cumsum by verified block speculation.  Three block barriers per window: the
@@ -177,6 +180,99 @@ __global__ void __launch_bounds__(ST_T) sampler_tables_kernel(TabArgs A) {
   }
 }
 
+// ---- multi-CTA total and probabilities (n >= TAB_MULTI_N): the same NumPy pairwise tree, its top
+// TAB_KB levels over CTAs (leaf gl = CTA x 1024 + thread at depth TAB_KB + ST_D), so the sum is
+// bit-identical to the one-CTA kernel's; then the elementwise division over every CTA and the
+// exact cumsum by the one-CTA kernel (cdf_only).
+constexpr int TAB_KB = 6, TAB_NB = 1 << TAB_KB, TAB_DT = TAB_KB + ST_D;
+constexpr int64_t TAB_MULTI_N = 32768;
+
+__global__ void __launch_bounds__(ST_T) tables_partial_kernel(TabArgs A, double* __restrict__ cpart,
+                                                              int8_t* __restrict__ cstop, int* __restrict__ cbad) {
+  __shared__ double slot[ST_T];
+  __shared__ int8_t stopd[ST_T];
+  const int f = blockIdx.y, c = blockIdx.x, tid = threadIdx.x;
+  const double* __restrict__ scores = A.scores[f];
+  const int64_t n = A.n[f];
+  const int64_t gl = (int64_t)c * ST_T + tid;
+  bool bad = false;
+  {
+    int64_t s = 0, len = n;
+    int depth = 0;
+    bool owner = true;
+    for (; depth < TAB_DT; depth++) {
+      if (len <= PW_BLOCK) {
+        owner = (gl & ((1ll << (TAB_DT - depth)) - 1)) == 0;
+        break;
+      }
+      int64_t n2;
+      pw_split(len, &n2);
+      if ((gl >> (TAB_DT - 1 - depth)) & 1) {
+        s += n2;
+        len -= n2;
+      } else {
+        len = n2;
+      }
+    }
+    stopd[tid] = owner ? (int8_t)depth : (int8_t)-1;
+    if (owner) {
+      auto get = [&](int64_t i) {
+        const double v = scores[i];
+        bad |= !(v >= 0.0) || !isfinite(v);
+        return v;
+      };
+      slot[tid] = pw_sum_seq(get, s, len);
+    }
+  }
+  if (__syncthreads_or(bad) && tid == 0) atomicOr(&cbad[f], 1);
+  // the CTA's part of the tree: global levels TAB_DT - 1 .. TAB_KB
+  for (int l = ST_D - 1; l >= 0; l--) {
+    if (tid < (1 << l)) {
+      const int s0 = tid << (ST_D - l);
+      if (stopd[s0] > l + TAB_KB) slot[s0] = slot[s0] + slot[s0 + (1 << (ST_D - l - 1))];
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    cpart[f * TAB_NB + c] = stopd[0] >= 0 ? slot[0] : 0.0;
+    cstop[f * TAB_NB + c] = stopd[0];
+  }
+}
+
+__global__ void tables_total_kernel(TabArgs A, const double* __restrict__ cpart, const int8_t* __restrict__ cstop,
+                                    const int* __restrict__ cbad, double* __restrict__ totals) {
+  __shared__ double sl[TAB_NB];
+  __shared__ int8_t sd[TAB_NB];
+  const int f = blockIdx.x, tid = threadIdx.x;
+  sl[tid] = cpart[f * TAB_NB + tid];
+  sd[tid] = cstop[f * TAB_NB + tid];
+  __syncthreads();
+  for (int l = TAB_KB - 1; l >= 0; l--) {  // the top levels, same rule as inside a CTA
+    if (tid < (1 << l)) {
+      const int s0 = tid << (TAB_KB - l);
+      if (sd[s0] > l) sl[s0] = sl[s0] + sl[s0 + (1 << (TAB_KB - l - 1))];
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    const double total = sl[0];
+    totals[f] = total;
+    int fl = cbad[f] ? 1 : 0;
+    if (!(total > 0.0)) fl |= 2;
+    A.flags[f] = fl;
+  }
+}
+
+__global__ void tables_probs_kernel(TabArgs A, const double* __restrict__ totals) {
+  const int f = blockIdx.y;
+  const int64_t n = A.n[f];
+  const double total = totals[f];
+  const double* __restrict__ scores = A.scores[f];
+  double* __restrict__ probs = A.probs[f];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    probs[i] = scores[i] / total;
+}
+
 }  // namespace
 
 extern "C" int ks_sampler_tables_batched(int32_t nf, const double* const* scores, const int64_t* n,
@@ -193,7 +289,30 @@ extern "C" int ks_sampler_tables_batched(int32_t nf, const double* const* scores
   }
   a.flags = flags;
   a.renorm = renormalise;
-  sampler_tables_kernel<<<nf, ST_T, 0, (cudaStream_t)stream>>>(a);
+  cudaStream_t st = (cudaStream_t)stream;
+  int64_t nmax = 0;
+  for (int f = 0; f < nf; f++) nmax = n[f] > nmax ? n[f] : nmax;
+  if (nmax >= TAB_MULTI_N && !ks::env(ks::ENV_TABLES_ONE_CTA)) {  // KS_TABLES_ONE_CTA: A/B
+    // large vectors: the total and the probabilities over TAB_NB CTAs per vector, then the cumsum
+    ks::Scratch<double> cpart((size_t)nf * TAB_NB, st), totals(nf, st);
+    ks::Scratch<int8_t> cstop((size_t)nf * TAB_NB, st);
+    ks::Scratch<int> cbad(nf, st);
+    KS_REQUIRE(cpart.p && totals.p && cstop.p && cbad.p, KS_ECUDA, "scratch allocation failed");
+    KS_TRY_CUDA(cudaMemsetAsync(cbad.p, 0, sizeof(int) * nf, st));
+    tables_partial_kernel<<<dim3(TAB_NB, nf), ST_T, 0, st>>>(a, cpart.p, cstop.p, cbad.p);
+    KS_CHECK_LAUNCH();
+    tables_total_kernel<<<nf, TAB_NB, 0, st>>>(a, cpart.p, cstop.p, cbad.p, totals.p);
+    KS_CHECK_LAUNCH();
+    tables_probs_kernel<<<dim3(64, nf), 512, 0, st>>>(a, totals.p);
+    KS_CHECK_LAUNCH();
+    if (cdf) {
+      a.cdf_only = 1;
+      sampler_tables_kernel<<<nf, ST_T, 0, st>>>(a);
+      KS_CHECK_LAUNCH();
+    }
+    return KS_OK;
+  }
+  sampler_tables_kernel<<<nf, ST_T, 0, st>>>(a);
   KS_CHECK_LAUNCH();
   return KS_OK;
 }
