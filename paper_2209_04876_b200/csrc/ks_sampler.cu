@@ -32,6 +32,72 @@ __device__ __forceinline__ double ulp_of(double x) {
   return ldexp(1.0, e - 53);
 }
 
+// Exact cumsum from position pos (prev = the exact value before it) by verified block speculation.
+// Three block barriers per window: the per-window shared arrays are double-buffered (window
+// parity), every warp forms the prefix of the warp totals itself, and the verified restart value is
+// published beside the first failure's index, so nothing is re-synchronised at the end of a window.
+struct CumsumSmem {
+  int64_t c_wsum[2][ST_T / 32];
+  double c_spec[2][ST_T], c_real[2][ST_T];
+  int c_first[2];
+};
+
+__device__ void cumsum_windows(const double* __restrict__ probs, double* __restrict__ cdf, int64_t n, int64_t pos,
+                               double prev, CumsumSmem& S) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  for (int it = 0; pos < n; it++) {
+    const int buf = it & 1;
+    const int64_t i = pos + tid;
+    const bool valid = i < n;
+    const double x = valid ? probs[i] : 0.0;
+    double ref = prev;
+    if (ref == 0.0) ref = probs[pos];
+    // u = ulp(ref) and 1/u as exact powers of two from the exponent bits (a division by u is a
+    // multiplication by 1/u); tiny references keep the library path
+    const long long eb = (__double_as_longlong(ref) >> 52) & 0x7ff;
+    const bool fastu = ref > 0.0 && eb > 53 && eb < 2045;
+    const double u = fastu ? __longlong_as_double((eb - 52) << 52) : (ref > 0.0 ? ulp_of(ref) : 0x1.0p-1074);
+    const double iu = fastu ? __longlong_as_double((2098 - eb) << 52) : 0.0;
+    long long qi = 0;
+    if (valid) {
+      const double qd = fastu ? x * iu : x / u;
+      qi = (qd < 0x1.0p52) ? __double2ll_rn(qd) : (1ll << 52);
+    }
+    // inclusive block scan of qi: warp scan, warp totals published, each warp adds the prefix
+    long long v = qi;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long t = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += t;
+    }
+    if (lane == 31) S.c_wsum[buf][wid] = v;
+    if (tid == 0) S.c_first[buf] = ST_T;
+    __syncthreads();
+    long long wt = lane < wid ? S.c_wsum[buf][lane] : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) wt += __shfl_xor_sync(0xffffffffu, wt, o);
+    const long long Q = v + wt;
+    const double base = fastu ? prev * iu : prev / u;
+    const double spec = (double)((long long)base + Q) * u;
+    S.c_spec[buf][tid] = spec;
+    __syncthreads();
+    const double sprev = (tid == 0) ? prev : S.c_spec[buf][tid - 1];
+    const double real = __dadd_rn(sprev, x);
+    if (valid && real != spec) {
+      S.c_real[buf][tid] = real;
+      atomicMin(&S.c_first[buf], tid);
+    }
+    __syncthreads();
+    const int fst = S.c_first[buf];
+    if (valid && tid < fst) cdf[i] = spec;
+    if (valid && tid == fst) cdf[i] = real;
+    int64_t adv = (fst < ST_T) ? (int64_t)fst + 1 : (int64_t)ST_T;
+    if (pos + adv > n) adv = n - pos;
+    prev = ((int)adv - 1 == fst) ? S.c_real[buf][fst] : S.c_spec[buf][adv - 1];
+    pos += adv;
+  }
+}
+
 __global__ void __launch_bounds__(ST_T) sampler_tables_kernel(TabArgs A) {
   __shared__ double slot[ST_T];
   __shared__ int8_t stopd[ST_T];
@@ -111,67 +177,8 @@ __global__ void __launch_bounds__(ST_T) sampler_tables_kernel(TabArgs A) {
   }  // !cdf_only
   __syncthreads();
   if (cdf == nullptr) return;
-  // ---- exact cumsum by verified block speculation.  Three block barriers per window: the
-  // per-window shared arrays are double-buffered (window parity), every warp forms the prefix
-  // of the warp totals itself, and the verified restart value is published beside the first
-  // failure's index, so nothing is re-synchronised at the end of a window.
-  __shared__ int64_t c_wsum[2][ST_T / 32];
-  __shared__ double c_spec[2][ST_T], c_real[2][ST_T];
-  __shared__ int c_first[2];
-  const int lane = tid & 31, wid = tid >> 5;
-  double prev = 0.0;
-  int64_t pos = 0;
-  for (int it = 0; pos < n; it++) {
-    const int buf = it & 1;
-    const int64_t i = pos + tid;
-    const bool valid = i < n;
-    const double x = valid ? probs[i] : 0.0;
-    double ref = prev;
-    if (ref == 0.0) ref = probs[pos];
-    // u = ulp(ref) and 1/u as exact powers of two from the exponent bits (a division by u is a
-    // multiplication by 1/u); tiny references keep the library path
-    const long long eb = (__double_as_longlong(ref) >> 52) & 0x7ff;
-    const bool fastu = ref > 0.0 && eb > 53 && eb < 2045;
-    const double u = fastu ? __longlong_as_double((eb - 52) << 52) : (ref > 0.0 ? ulp_of(ref) : 0x1.0p-1074);
-    const double iu = fastu ? __longlong_as_double((2098 - eb) << 52) : 0.0;
-    long long qi = 0;
-    if (valid) {
-      const double qd = fastu ? x * iu : x / u;
-      qi = (qd < 0x1.0p52) ? __double2ll_rn(qd) : (1ll << 52);
-    }
-    // inclusive block scan of qi: warp scan, warp totals published, each warp adds the prefix
-    long long v = qi;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const long long t = __shfl_up_sync(0xffffffffu, v, o);
-      if (lane >= o) v += t;
-    }
-    if (lane == 31) c_wsum[buf][wid] = v;
-    if (tid == 0) c_first[buf] = ST_T;
-    __syncthreads();
-    long long wt = lane < wid ? c_wsum[buf][lane] : 0;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) wt += __shfl_xor_sync(0xffffffffu, wt, o);
-    const long long Q = v + wt;
-    const double base = fastu ? prev * iu : prev / u;
-    const double spec = (double)((long long)base + Q) * u;
-    c_spec[buf][tid] = spec;
-    __syncthreads();
-    const double sprev = (tid == 0) ? prev : c_spec[buf][tid - 1];
-    const double real = __dadd_rn(sprev, x);
-    if (valid && real != spec) {
-      c_real[buf][tid] = real;
-      atomicMin(&c_first[buf], tid);
-    }
-    __syncthreads();
-    const int fst = c_first[buf];
-    if (valid && tid < fst) cdf[i] = spec;
-    if (valid && tid == fst) cdf[i] = real;
-    int64_t adv = (fst < ST_T) ? (int64_t)fst + 1 : (int64_t)ST_T;
-    if (pos + adv > n) adv = n - pos;
-    prev = ((int)adv - 1 == fst) ? c_real[buf][fst] : c_spec[buf][adv - 1];
-    pos += adv;
-  }
+  __shared__ CumsumSmem csm;
+  cumsum_windows(probs, cdf, n, 0, 0.0, csm);
   __syncthreads();
   if (A.renorm) {
     const double last = cdf[n - 1];

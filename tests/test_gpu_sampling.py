@@ -23,6 +23,30 @@ def test_sampler_tables_bit_exact(n):
     np.testing.assert_array_equal(sampler.per_factor_cdf[0], ref.cdfs[0])
 
 
+@pytest.mark.parametrize("n,kind", [(65536, "ints"), (100003, "ints"), (40000, "zeros_first"), (131072, "pow2"),
+                                    (131073, "smooth"), (200000, "smooth")])
+def test_sampler_tables_bit_exact_large(n, kind):
+    """The n >= 32768 path (multi-CTA pairwise total, segmented exact cumsum with verification and the
+    window fallback): small-integer scores (exact sums, round-half-even ties), a long zero prefix,
+    power-of-two scores, and sizes past the segmented kernel's limit -- all bit-exact."""
+    import paper_2209_04876_b200 as K
+    rng = np.random.default_rng(n + len(kind))
+    if kind == "ints":
+        sc = rng.integers(0, 4, n).astype(np.float64)
+        sc[0] = 1.0
+    elif kind == "zeros_first":
+        sc = rng.random(n)
+        sc[: n // 3] = 0.0
+    elif kind == "pow2":
+        sc = np.ldexp(1.0, rng.integers(-40, 3, n)).astype(np.float64)
+    else:
+        sc = rng.random(n) + 0.25
+    sampler = K.build_product_sampler([K.LeverageScores(sc, 0.0)])
+    ref = O.Sampler([sc])
+    np.testing.assert_array_equal(sampler.per_factor_probabilities[0], ref.probs[0])
+    np.testing.assert_array_equal(sampler.per_factor_cdf[0], ref.cdfs[0])
+
+
 def test_sampler_tables_with_zeros_and_validation():
     import paper_2209_04876_b200 as K
     from paper_2209_04876_b200.errors import InvalidInputError
