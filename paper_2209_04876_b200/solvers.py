@@ -464,13 +464,13 @@ def _exact_solve_graph(factors, b, lam, with_loss=True):
     if entry is not None and entry.disabled:
         return None
     if entry is None:
-        svds = _compact_svds_dev(facs, 1e-10)
+        svds = _compact_svds_dev([a.contiguous() for a in facs], 1e-10)
         _state.cache_put(_EXACT_GRAPHS, key, _ExactGraph([int(sv[1].numel()) for sv in svds]), _GRAPH_CAP)
         return None
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     if entry.graph is None:
-        entry.facs = [torch.empty_like(a) for a in facs]
+        entry.facs = [torch.empty(tuple(a.shape), dtype=a.dtype, device=a.device) for a in facs]  # row-major
         for dst, a in zip(entry.facs, facs):
             dst.copy_(a)
         g = torch.cuda.CUDAGraph()
@@ -542,7 +542,7 @@ def _exact_solve_graph(factors, b, lam, with_loss=True):
     loss, bsq = back[0], back[1]
     if not loss >= _IDENTITY_MIN_FRAC * bsq:
         # more than three digits of ||b||^2 cancel (a near-exact fit): the direct pass instead
-        r2, x2 = _ridge_loss_parts(list(facs), x, bt).cpu().tolist()
+        r2, x2 = _ridge_loss_parts(entry.facs, x, bt).cpu().tolist()  # the row-major copies
         loss = r2 + lam * x2
     return x, float(loss), wall
 

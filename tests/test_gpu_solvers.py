@@ -547,3 +547,24 @@ def test_exact_solve_graph_declined_cholqr_and_no_loss(rng):
         assert torch.equal(rep.solution, ref.solution) and rep.loss == ref.loss
     nl = K.kronmatmul_svd_solve(facs, bd, 1e-3, with_loss=False)
     assert torch.equal(nl.solution, ref.solution) and math.isnan(nl.loss)
+
+
+def test_exact_solve_graph_noncontiguous_factors(rng):
+    """Non-contiguous device factors (transposed views) go through the graph path's row-major copies
+    and give the eager solve's result."""
+    import paper_2209_04876_b200 as K
+    from paper_2209_04876_b200 import solvers as S
+    n, d = 1024, 16
+    facs = [torch.tensor(rng.normal(1.0, 0.03, (d, n)), device="cuda").T for _ in range(2)]
+    assert not facs[0].is_contiguous()
+    bd = torch.tensor(rng.standard_normal(n * n), device="cuda") * 1e-3 + 1.0  # a near fit: the direct loss pass
+    S._USE_GRAPHS[0] = False
+    try:
+        ref = K.kronmatmul_svd_solve(facs, bd, 1e-3)
+    finally:
+        S._USE_GRAPHS[0] = True
+    S._EXACT_GRAPHS.clear()
+    outs = [K.kronmatmul_svd_solve(facs, bd, 1e-3) for _ in range(3)]
+    for rep in outs:
+        assert torch.equal(rep.solution, ref.solution)
+        assert abs(rep.loss - ref.loss) <= 1e-12 * ref.loss
