@@ -191,17 +191,19 @@ __global__ void __launch_bounds__(ST_T) sampler_tables_kernel(TabArgs A) {
 // TAB_KB levels over CTAs (leaf gl = CTA x 1024 + thread at depth TAB_KB + ST_D), so the sum is
 // bit-identical to the one-CTA kernel's; then the elementwise division over every CTA and the
 // exact cumsum by the one-CTA kernel (cdf_only).
-constexpr int TAB_KB = 6, TAB_NB = 1 << TAB_KB, TAB_DT = TAB_KB + ST_D;
+constexpr int TAB_TD = 8, TAB_T = 1 << TAB_TD;  // threads per CTA of the partial sums (registers for
+                                               // the leaves' loads in flight)
+constexpr int TAB_KB = 8, TAB_NB = 1 << TAB_KB, TAB_DT = TAB_KB + TAB_TD;
 constexpr int64_t TAB_MULTI_N = 32768;  // below it the one-CTA kernel is as fast (its 1 launch vs 12)
 
-__global__ void __launch_bounds__(ST_T) tables_partial_kernel(TabArgs A, double* __restrict__ cpart,
-                                                              int8_t* __restrict__ cstop, int* __restrict__ cbad) {
-  __shared__ double slot[ST_T];
-  __shared__ int8_t stopd[ST_T];
+__global__ void __launch_bounds__(TAB_T) tables_partial_kernel(TabArgs A, double* __restrict__ cpart,
+                                                               int8_t* __restrict__ cstop, int* __restrict__ cbad) {
+  __shared__ double slot[TAB_T];
+  __shared__ int8_t stopd[TAB_T];
   const int f = blockIdx.y, c = blockIdx.x, tid = threadIdx.x;
   const double* __restrict__ scores = A.scores[f];
   const int64_t n = A.n[f];
-  const int64_t gl = (int64_t)c * ST_T + tid;
+  const int64_t gl = (int64_t)c * TAB_T + tid;
   bool bad = false;
   {
     int64_t s = 0, len = n;
@@ -233,10 +235,10 @@ __global__ void __launch_bounds__(ST_T) tables_partial_kernel(TabArgs A, double*
   }
   if (__syncthreads_or(bad) && tid == 0) atomicOr(&cbad[f], 1);
   // the CTA's part of the tree: global levels TAB_DT - 1 .. TAB_KB
-  for (int l = ST_D - 1; l >= 0; l--) {
+  for (int l = TAB_TD - 1; l >= 0; l--) {
     if (tid < (1 << l)) {
-      const int s0 = tid << (ST_D - l);
-      if (stopd[s0] > l + TAB_KB) slot[s0] = slot[s0] + slot[s0 + (1 << (ST_D - l - 1))];
+      const int s0 = tid << (TAB_TD - l);
+      if (stopd[s0] > l + TAB_KB) slot[s0] = slot[s0] + slot[s0 + (1 << (TAB_TD - l - 1))];
     }
     __syncthreads();
   }
@@ -508,22 +510,40 @@ __global__ void __launch_bounds__(ST_T) cs_segments_kernel(TabArgs A, CsArgs C) 
   }
 }
 
-__global__ void cs_bases_kernel(TabArgs A, CsArgs C) {
-  const int f = blockIdx.x;
-  if (threadIdx.x != 0) return;
+constexpr int CS_BT = 256;
+__global__ void __launch_bounds__(CS_BT) cs_bases_kernel(TabArgs A, CsArgs C) {
+  // the segment records staged in shared memory by every thread (chunks of CS_BT), then the
+  // sequential pass over them by one thread
+  __shared__ double sp0[CS_BT], sdq[CS_BT];
+  __shared__ double s_end;
+  const int f = blockIdx.x, tid = threadIdx.x;
   const int ns = C.nseg[f];
   if (ns > CS_SEGMAX) {
-    C.fail[f] = 0;  // too many segments: the window path from the start
+    if (tid == 0) C.fail[f] = 0;  // too many segments: the window path from the start
     return;
   }
   const int64_t b0 = (int64_t)f * CS_SEGMAX;
-  double end = 0.0;
-  for (int j = 0; j < ns; j++) {
-    const double base = __dadd_rn(end, A.probs[f][C.sk0[b0 + j]]);
-    C.sbase[b0 + j] = base;
-    end = base + (double)(C.sqend[b0 + j] - C.sq0[b0 + j]) * cs_u(C.se[b0 + j]);
+  if (tid == 0) s_end = 0.0;
+  for (int j0 = 0; j0 < ns; j0 += CS_BT) {
+    const int j = j0 + tid;
+    __syncthreads();
+    if (j < ns) {
+      sp0[tid] = A.probs[f][C.sk0[b0 + j]];
+      sdq[tid] = (double)(C.sqend[b0 + j] - C.sq0[b0 + j]) * cs_u(C.se[b0 + j]);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double end = s_end;
+      const int m = min(CS_BT, ns - j0);
+      for (int i = 0; i < m; i++) {
+        const double base = __dadd_rn(end, sp0[i]);
+        C.sbase[b0 + j0 + i] = base;
+        end = base + sdq[i];
+      }
+      s_end = end;
+    }
   }
-  C.fail[f] = (unsigned long long)A.n[f];
+  if (tid == 0) C.fail[f] = (unsigned long long)A.n[f];
 }
 
 __device__ __forceinline__ double cs_value(const CsArgs& C, int f, int64_t k) {
@@ -542,7 +562,7 @@ __global__ void __launch_bounds__(ST_T) cs_values_kernel(TabArgs A, CsArgs C) {
   if (__dadd_rn(prev, A.probs[f][k]) != s) atomicMin(&C.fail[f], (unsigned long long)k);
 }
 
-// the verified prefix is final; from the first failed step on, the one-CTA window path; renorm
+// the verified prefix is final; from the first failed step on, the one-CTA window path
 __global__ void __launch_bounds__(ST_T) cs_finish_kernel(TabArgs A, CsArgs C) {
   __shared__ CumsumSmem csm;
   const int f = blockIdx.x;
@@ -553,13 +573,24 @@ __global__ void __launch_bounds__(ST_T) cs_finish_kernel(TabArgs A, CsArgs C) {
     g_cs_dbg[2 * f + 1] = C.nseg[f];
   }
   if (k1 < n) cumsum_windows(A.probs[f], A.cdf[f], n, k1, k1 > 0 ? A.cdf[f][k1 - 1] : 0.0, csm);
-  __syncthreads();
-  if (A.renorm) {
-    double* cdf = A.cdf[f];
-    const double last = cdf[n - 1];
-    __syncthreads();
-    for (int64_t i = threadIdx.x; i < n; i += ST_T) cdf[i] = cdf[i] / last;
-  }
+}
+
+// cdf /= cdf[n - 1] over every CTA (np.cumsum(p) / its last entry, as in the one-CTA kernel)
+__global__ void cs_renorm_kernel(TabArgs A) {
+  const int f = blockIdx.y;
+  const int64_t n = A.n[f];
+  double* cdf = A.cdf[f];
+  const double last = cdf[n - 1];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    if (i != n - 1) cdf[i] = cdf[i] / last;
+  // the last entry (read by every CTA) is divided by a second launch's single thread
+}
+
+__global__ void cs_renorm_last_kernel(TabArgs A) {
+  const int f = blockIdx.x;
+  double* cdf = A.cdf[f];
+  const int64_t n = A.n[f];
+  cdf[n - 1] = cdf[n - 1] / cdf[n - 1];
 }
 
 }  // namespace
@@ -598,7 +629,7 @@ extern "C" int ks_sampler_tables_batched(int32_t nf, const double* const* scores
     ks::Scratch<int> cbad(nf, st);
     KS_REQUIRE(cpart.p && totals.p && cstop.p && cbad.p, KS_ECUDA, "scratch allocation failed");
     KS_TRY_CUDA(cudaMemsetAsync(cbad.p, 0, sizeof(int) * nf, st));
-    tables_partial_kernel<<<dim3(TAB_NB, nf), ST_T, 0, st>>>(a, cpart.p, cstop.p, cbad.p);
+    tables_partial_kernel<<<dim3(TAB_NB, nf), TAB_T, 0, st>>>(a, cpart.p, cstop.p, cbad.p);
     KS_CHECK_LAUNCH();
     tables_total_kernel<<<nf, TAB_NB, 0, st>>>(a, cpart.p, cstop.p, cbad.p, totals.p);
     KS_CHECK_LAUNCH();
@@ -629,12 +660,18 @@ extern "C" int ks_sampler_tables_batched(int32_t nf, const double* const* scores
       KS_CHECK_LAUNCH();
       cs_segments_kernel<<<dim3(nb, nf), ST_T, 0, st>>>(a, c);
       KS_CHECK_LAUNCH();
-      cs_bases_kernel<<<nf, 32, 0, st>>>(a, c);
+      cs_bases_kernel<<<nf, CS_BT, 0, st>>>(a, c);
       KS_CHECK_LAUNCH();
       cs_values_kernel<<<dim3(nb, nf), ST_T, 0, st>>>(a, c);
       KS_CHECK_LAUNCH();
       cs_finish_kernel<<<nf, ST_T, 0, st>>>(a, c);
       KS_CHECK_LAUNCH();
+      if (renormalise) {
+        cs_renorm_kernel<<<dim3(64, nf), 512, 0, st>>>(a);
+        KS_CHECK_LAUNCH();
+        cs_renorm_last_kernel<<<nf, 1, 0, st>>>(a);
+        KS_CHECK_LAUNCH();
+      }
     } else if (cdf) {
       a.cdf_only = 1;
       sampler_tables_kernel<<<nf, ST_T, 0, st>>>(a);
