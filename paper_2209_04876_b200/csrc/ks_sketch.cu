@@ -478,17 +478,26 @@ __global__ void bk_count_kernel(const int64_t* __restrict__ idx, int64_t s, int3
 // exclusive scans (one block) of NS int32 arrays of n counts: out_k[0..n]; cur (optional) gets a
 // copy of out_0[0..n).  Tiles of BK_T x 8 counts: every thread loads 8 consecutive counts (two
 // 16-byte loads, all in flight), a block scan of the thread totals, the tile total carried over.
+// (Several CTAs: CTA c scans [c chunk, (c + 1) chunk) starting from the sum of the chunks before it,
+// part[q nb + c'] from bk_partsum_kernel; chunk is a multiple of the tile.)
 template <int NS>
 __global__ void __launch_bounds__(BK_T) bk_scan_kernel(const int32_t* __restrict__ in0, const int32_t* __restrict__ in1,
                                                        int64_t n, int32_t* __restrict__ out0,
-                                                       int32_t* __restrict__ out1, int32_t* __restrict__ cur) {
+                                                       int32_t* __restrict__ out1, int32_t* __restrict__ cur,
+                                                       const int32_t* __restrict__ part = nullptr, int64_t chunk = 0) {
   constexpr int PT = 8, TILE = BK_T * PT;
   __shared__ int32_t wsum[NS][BK_T / 32];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int c = blockIdx.x, nb = gridDim.x;
+  const int64_t lo = part ? (int64_t)c * chunk : 0, hi = part ? min(n, lo + chunk) : n;
   int32_t carry[NS];
 #pragma unroll
-  for (int q = 0; q < NS; q++) carry[q] = 0;
-  for (int64_t t0 = 0; t0 < n; t0 += TILE) {
+  for (int q = 0; q < NS; q++) {
+    carry[q] = 0;
+    if (part)
+      for (int i = 0; i < c; i++) carry[q] += part[q * nb + i];
+  }
+  for (int64_t t0 = lo; t0 < hi; t0 += TILE) {
     const int64_t b = t0 + (int64_t)tid * PT;
     int32_t v[NS][PT], inc[NS], loc[NS];
 #pragma unroll
@@ -557,10 +566,58 @@ __global__ void __launch_bounds__(BK_T) bk_scan_kernel(const int32_t* __restrict
     }
     __syncthreads();
   }
-  if (tid == 0) {
+  if (tid == 0 && hi == n) {
     out0[n] = carry[0];
     if (NS > 1) out1[n] = carry[NS - 1];
   }
+}
+
+// per-chunk sums for the multi-CTA form of bk_scan_kernel
+template <int NS>
+__global__ void __launch_bounds__(BK_T) bk_partsum_kernel(const int32_t* __restrict__ in0,
+                                                          const int32_t* __restrict__ in1, int64_t n, int64_t chunk,
+                                                          int32_t* __restrict__ part) {
+  __shared__ int32_t ws[NS][BK_T / 32];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, c = blockIdx.x;
+  const int64_t lo = (int64_t)c * chunk, hi = min(n, lo + chunk);
+#pragma unroll
+  for (int q = 0; q < NS; q++) {
+    const int32_t* src = q ? in1 : in0;
+    int32_t v = 0;
+    for (int64_t i = lo + tid; i < hi; i += BK_T) v += src[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) ws[q][wid] = v;
+  }
+  __syncthreads();
+  if (tid < NS) {
+    int32_t t = 0;
+    for (int w = 0; w < BK_T / 32; w++) t += ws[tid][w];
+    part[tid * gridDim.x + c] = t;
+  }
+}
+
+// exclusive scan(s) of n counts, one block for small n, else one tile-multiple chunk per CTA
+template <int NS>
+static int bk_scan(cudaStream_t st, const int32_t* in0, const int32_t* in1, int64_t n, int32_t* out0, int32_t* out1,
+                   int32_t* cur) {
+  constexpr int64_t TILE = (int64_t)BK_T * 8;
+  const int64_t nt = (n + TILE - 1) / TILE;
+  if (nt <= 2) {
+    bk_scan_kernel<NS><<<1, BK_T, 0, st>>>(in0, in1, n, out0, out1, cur);
+    KS_CHECK_LAUNCH();
+    return KS_OK;
+  }
+  const int nb = (int)std::min<int64_t>(nt, 64);
+  const int64_t chunk = ((nt + nb - 1) / nb) * TILE;
+  const int nbu = (int)((n + chunk - 1) / chunk);
+  ks::Scratch<int32_t> part((size_t)NS * nbu, st);
+  KS_REQUIRE(part.p, KS_ECUDA, "scratch allocation failed");
+  bk_partsum_kernel<NS><<<nbu, BK_T, 0, st>>>(in0, in1, n, chunk, part.p);
+  KS_CHECK_LAUNCH();
+  bk_scan_kernel<NS><<<nbu, BK_T, 0, st>>>(in0, in1, n, out0, out1, cur, part.p, chunk);
+  KS_CHECK_LAUNCH();
+  return KS_OK;
 }
 
 __global__ void bk_scatter_kernel(const int64_t* __restrict__ idx, int64_t s, int32_t* __restrict__ cur,
@@ -811,11 +868,11 @@ extern "C" int ks_sketch_diag_grouped2_ex(const int64_t* idx, const int64_t* row
                KS_ECUDA, "scratch allocation failed");
     KS_TRY_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int32_t) * (size_t)n0, st));
     bk_count_kernel<<<ceil_div_u(s, 256), 256, 0, st>>>(idx, s, cnt.p);
-    bk_scan_kernel<1><<<1, BK_T, 0, st>>>(cnt.p, nullptr, n0, off.p, nullptr, cur.p);
+    if (int rc = bk_scan<1>(st, cnt.p, nullptr, n0, off.p, nullptr, cur.p)) return rc;
     bk_scatter_kernel<<<ceil_div_u(s, 256), 256, 0, st>>>(idx, s, cur.p, slot.p);
     bk_bucket_kernel<<<ceil_div_u(n0 * 32, 256), 256, 0, st>>>(idx, w, off.p, n0, slot.p, tmp.p, sv.p, sr.p, sf.p,
                                                                ucnt.p, ne.p);
-    bk_scan_kernel<2><<<1, BK_T, 0, st>>>(ucnt.p, ne.p, n0, uoff.p, goff.p, nullptr);
+    if (int rc = bk_scan<2>(st, ucnt.p, ne.p, n0, uoff.p, goff.p, nullptr)) return rc;
     bk_place_kernel<<<ceil_div_u(n0 * 8, 256), 256, 0, st>>>(off.p, ucnt.p, uoff.p, goff.p, n0, n1, sv.p, sr.p, sf.p,
                                                              sd_idx, sd_val, seg, lrow, rrow, dcounts_b, first_raw);
     KS_CHECK_LAUNCH();
