@@ -276,38 +276,50 @@ __global__ void __launch_bounds__(CT) chol_reg_kernel(const double* __restrict__
   if (tid == 0 && info) info[slot] = bad;
   for (int e = tid; e < d * d; e += CT) R[e] = Rs[(e / d) * LDR + (e % d)];
   if (!Rinv || bad) return;
-  // X = R^-1 (upper), rows from the bottom: X_i = (e_i - acc_i) / R_ii, then acc_m += R_mi X_i
-  double acc[TBS][TBS];
-#pragma unroll
-  for (int r = 0; r < TBS; r++)
-#pragma unroll
-    for (int c = 0; c < TBS; c++) acc[r][c] = 0.0;
-  for (int i = d - 1; i >= 0; i--) {
-    double* xr = colb + (i & 1) * d;
-    if (bi == i / TBS) {  // the owners of row i form it
-      const int r = i - i0;
-      const double rii = Rs[i * LDR + i];
-#pragma unroll
-      for (int c = 0; c < TBS; c++) {
-        double av = acc[0][c];  // row r of the block, selected without dynamic indexing
-#pragma unroll
-        for (int rr2 = 1; rr2 < TBS; rr2++) av = r == rr2 ? acc[rr2][c] : av;
-        const int j = j0 + c;
-        const double v = j >= i ? ((j == i ? 1.0 : 0.0) - av) / rii : 0.0;
-        xr[j] = v;
-        Rinv[(size_t)i * d + j] = v;
+  // X = R^-1 (upper) by 16 x 16 blocks: the diagonal blocks inverted concurrently (one lane per
+  // column, back substitution), then the off-diagonal blocks by block diagonals,
+  // X_ij = -X_ii (sum_{i<k<=j} R_ik X_kj), two small block products per diagonal with a barrier
+  // between -- log-depth in the block count instead of one barrier per row
+  constexpr int NBK = d / 16;
+  double* Xs = colb + 2 * d;            // d x LDR: X
+  double* Ts = Xs + d * LDR;            // (NBK - 1) x 256: the block sums of one diagonal
+  {
+    const int wq = tid >> 5, ln = tid & 31;
+    if (wq < NBK && ln < 16) {          // warp wq inverts diagonal block wq, lane ln = column
+      const int o = wq * 16, j = ln;
+      for (int i = 15; i >= 0; i--) {
+        double acc = i == j ? 1.0 : 0.0;
+        for (int k = i + 1; k <= j; k++) acc = fma(-Rs[(o + i) * LDR + o + k], Xs[(o + k) * LDR + o + j], acc);
+        Xs[(o + i) * LDR + o + j] = i <= j ? acc / Rs[(o + i) * LDR + o + i] : 0.0;
       }
+    }
+    // zero the blocks below the diagonal and the upper off-diagonal blocks (filled below)
+    for (int e = tid; e < d * d; e += CT) {
+      const int i = e / d, j = e % d;
+      if (i / 16 != j / 16) Xs[i * LDR + j] = 0.0;
     }
     __syncthreads();
-#pragma unroll
-    for (int r = 0; r < TBS; r++) {
-      const int m = i0 + r;
-      if (m < i) {
-        const double rmi = Rs[m * LDR + i];
-#pragma unroll
-        for (int c = 0; c < TBS; c++) acc[r][c] = fma(rmi, xr[j0 + c], acc[r][c]);
+    for (int dl = 1; dl < NBK; dl++) {
+      const int np = NBK - dl;          // block pairs (i, i + dl) on this diagonal
+      for (int e = tid; e < np * 256; e += CT) {  // T = sum_{i<k<=j} R_ik X_kj
+        const int pr = e >> 8, rr = (e >> 4) & 15, cc = e & 15;
+        const int bi_ = pr, bj_ = pr + dl;
+        double acc = 0.0;
+        for (int k = (bi_ + 1) * 16; k < (bj_ + 1) * 16; k++)
+          acc = fma(Rs[(bi_ * 16 + rr) * LDR + k], Xs[k * LDR + bj_ * 16 + cc], acc);
+        Ts[e] = acc;
       }
+      __syncthreads();
+      for (int e = tid; e < np * 256; e += CT) {  // X_ij = -X_ii T
+        const int pr = e >> 8, rr = (e >> 4) & 15, cc = e & 15;
+        const int bi_ = pr, bj_ = pr + dl;
+        double acc = 0.0;
+        for (int k = rr; k < 16; k++) acc = fma(Xs[(bi_ * 16 + rr) * LDR + bi_ * 16 + k], Ts[(pr << 8) + (k << 4) + cc], acc);
+        Xs[(bi_ * 16 + rr) * LDR + bj_ * 16 + cc] = -acc;
+      }
+      __syncthreads();
     }
+    for (int e = tid; e < d * d; e += CT) Rinv[e] = Xs[(e / d) * LDR + (e % d)];
   }
 }
 
@@ -398,7 +410,8 @@ int chol_upper(cudaStream_t st, const double* G, int d, double* R, double* Rinv,
   // register-resident factor for d = 32 / 64 (at d = 128 the 8 x 8 blocks per thread run slower
   // than the shared-memory kernel)
   if (!ks::env(ks::ENV_TALL_OLD) && (d == 32 || d == 64)) {
-    const size_t smem = sizeof(double) * ((size_t)d * (d + 1) + 2 * d);
+    // R, the published column, X = R^-1 and the block sums of one diagonal of X
+    const size_t smem = sizeof(double) * (2 * (size_t)d * (d + 1) + 2 * d + (size_t)(d / 16) * 256);
 #define KS_CHOL(TB)                                                                                            \
     if (d == 16 * TB) {                                                                                        \
       KS_TRY_CUDA(cudaFuncSetAttribute(chol_reg_kernel<TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
