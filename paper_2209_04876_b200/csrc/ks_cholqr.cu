@@ -191,10 +191,12 @@ __global__ void __launch_bounds__(CT) chol_reg_kernel(const double* __restrict__
     // CholeskyQR2's second Gram Q1^T Q1 = I + E with E ~ kappa(A)^2 eps: chol(I + E) =
     // I + strict_upper(E) + diag(E) / 2 + O(|E|^2) and its inverse I - strict_upper(E) - diag(E) / 2
     // + O(|E|^2), exact to rounding once |E| <= 1e-8; otherwise the factorisation below
+    for (int e = tid; e < d * d; e += CT) Rs[(e / d) * LDR + (e % d)] = G[e];  // coalesced, then transposed reads
+    __syncthreads();
     double em = 0.0;
     for (int e = tid; e < d * d; e += CT) {
       const int i = e / d, j = e % d;
-      em = fmax(em, fabs(0.5 * (G[i * d + j] + G[j * d + i]) - (i == j ? 1.0 : 0.0)));
+      em = fmax(em, fabs(0.5 * (Rs[i * LDR + j] + Rs[j * LDR + i]) - (i == j ? 1.0 : 0.0)));
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) em = fmax(em, __shfl_xor_sync(0xffffffffu, em, o));
@@ -205,7 +207,7 @@ __global__ void __launch_bounds__(CT) chol_reg_kernel(const double* __restrict__
     if (em <= 1e-8) {
       for (int e = tid; e < d * d; e += CT) {
         const int i = e / d, j = e % d;
-        const double ev = 0.5 * (G[i * d + j] + G[j * d + i]) - (i == j ? 1.0 : 0.0);
+        const double ev = 0.5 * (Rs[i * LDR + j] + Rs[j * LDR + i]) - (i == j ? 1.0 : 0.0);
         const double up = i < j ? ev : (i == j ? 0.5 * ev : 0.0);
         R[e] = (i == j ? 1.0 : 0.0) + up;
         if (Rinv) Rinv[e] = (i == j ? 1.0 : 0.0) - up;
