@@ -496,6 +496,31 @@ int chol_qr2_r(cudaStream_t st, const double* A, int64_t n, int d, double* R, in
 
 }  // namespace ks
 
+namespace {
+
+// scores[i] = ||(Q1 R2^-1)_i||^2 with Q1 = A R1^-1 (the CholeskyQR2 first pass, kept) and R2 the
+// second pass's factor: the same Q as A (R2 R1)^-1 without the two d x d products R2 R1 and
+// R1^-1 R2^-1 (~13 us each as small-GEMM launches at d = 64).  info (device, 2 x int32): nonzero =
+// declined, scores undefined.
+int chol_qr2_scores(cudaStream_t st, const double* A, int64_t n, int d, double* scores, int32_t* info) {
+  using ks::Scratch;
+  Scratch<double> G((int64_t)d * d, st), R1((int64_t)d * d, st), R1i((int64_t)d * d, st), R2((int64_t)d * d, st),
+      R2i((int64_t)d * d, st), Q((int64_t)n * d, st);
+  KS_REQUIRE(G.p && R1.p && R1i.p && R2.p && R2i.p && Q.p, KS_ECUDA, "scratch allocation failed");
+  // defined inputs of the last two products when a factorisation declines
+  KS_TRY_CUDA(cudaMemsetAsync(R1i.p, 0, sizeof(double) * d * d, st));
+  KS_TRY_CUDA(cudaMemsetAsync(R2i.p, 0, sizeof(double) * d * d, st));
+  int rc = ks::gemm_tn_tall(st, d, d, n, 1.0, A, d, 1, A, d, 1, G.p);
+  if (rc) return rc;
+  if ((rc = chol_upper(st, G.p, d, R1.p, R1i.p, info, 0))) return rc;
+  if ((rc = tallmm(st, A, n, d, R1i.p, Q.p, nullptr))) return rc;  // Q1 = A R1^-1
+  if ((rc = ks::gemm_tn_tall(st, d, d, n, 1.0, Q.p, d, 1, Q.p, d, 1, G.p))) return rc;
+  if ((rc = chol_upper(st, G.p, d, R2.p, R2i.p, info, 1, 1))) return rc;
+  return tallmm(st, Q.p, n, d, R2i.p, nullptr, scores);
+}
+
+}  // namespace
+
 // scores[i] = ||(A R^-1)_i||^2 = a_i^T (A^T A)^-1 a_i with R from CholeskyQR2: the statistical
 // leverage scores of a numerically full-rank tall A (ridge_leverage_scores(compact_svd(a), 0),
 // leverage.py:51-64).  *ok = 0 (scores undefined) when A is too ill-conditioned; callers then
@@ -504,14 +529,15 @@ extern "C" int ks_leverage_scores_tall(const double* A, int64_t n, int32_t d, do
                                        void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   KS_REQUIRE(d >= 1 && d <= 128 && n >= d, KS_ESIZE, "leverage_scores_tall needs n >= d, 1 <= d <= 128");
-  ks::Scratch<double> R((int64_t)d * d, st), Ri((int64_t)d * d, st);
-  KS_REQUIRE(R.p && Ri.p, KS_ECUDA, "scratch allocation failed");
-  int good = 0;
-  int rc = ks::chol_qr2_r(st, A, n, d, R.p, &good, Ri.p);
+  ks::Scratch<int32_t> info(2, st);
+  KS_REQUIRE(info.p, KS_ECUDA, "scratch allocation failed");
+  int rc = chol_qr2_scores(st, A, n, d, scores, info.p);
   if (rc) return rc;
-  *ok = good;
-  if (!good) return KS_OK;
-  return tallmm(st, A, n, d, Ri.p, nullptr, scores);
+  int32_t h[2];
+  KS_TRY_CUDA(cudaMemcpyAsync(h, info.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+  KS_TRY_CUDA(cudaStreamSynchronize(st));
+  *ok = (h[0] == 0 && h[1] == 0);
+  return KS_OK;
 }
 
 // Asynchronous ks_leverage_scores_tall: no host round trip; info_dev (device, 2 x int32, zeroed by
@@ -520,12 +546,7 @@ extern "C" int ks_leverage_scores_tall_async(const double* A, int64_t n, int32_t
                                              void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   KS_REQUIRE(d >= 1 && d <= 128 && n >= d, KS_ESIZE, "leverage_scores_tall needs n >= d, 1 <= d <= 128");
-  ks::Scratch<double> R((int64_t)d * d, st), Ri((int64_t)d * d, st);
-  KS_REQUIRE(R.p && Ri.p, KS_ECUDA, "scratch allocation failed");
-  KS_TRY_CUDA(cudaMemsetAsync(Ri.p, 0, sizeof(double) * d * d, st));  // defined input if declined
-  int rc = ks::chol_qr2_r_async(st, A, n, d, R.p, Ri.p, info_dev);
-  if (rc) return rc;
-  return tallmm(st, A, n, d, Ri.p, nullptr, scores);
+  return chol_qr2_scores(st, A, n, d, scores, info_dev);
 }
 
 // R factor by CholeskyQR2 (ok = 1) -- exported for tests; ks_qr_r uses it internally.
