@@ -992,6 +992,8 @@ def _fast_solve_graph(facs, b, config: RegressionConfig, key=None):
                 main.wait_stream(vst)
                 entry.packed = _PackedChecks([(flags.reshape(-1), _validation_handler(len(facs)))] + cap.items,
                                              entry.out["state"], entry.out["hist"])
+                if _FETCH_IN_GRAPH[0]:
+                    entry.packed.fetch()  # the read-back copies as graph nodes
         except Exception:
             _state.cache_drop(_SOLVE_GRAPHS, key)
             raise
@@ -1007,7 +1009,8 @@ def _fast_solve_graph(facs, b, config: RegressionConfig, key=None):
     _LAST_LOOP_EVENTS[0] = entry.out["loop_events"]
     entry.graph.replay()
     out = entry.out
-    entry.packed.fetch()
+    if not _FETCH_IN_GRAPH[0]:
+        entry.packed.fetch()
     x = out["x"].reshape(-1).clone()
     torch.cuda.current_stream().synchronize()
     _mark("richardson")
@@ -1035,6 +1038,8 @@ class _HostFacsGraph:
 
 
 _HOST_GRAPHS: dict = {}
+# the whole-solve graphs' read-back copies (flags, loop state, history, x) captured as graph nodes
+_FETCH_IN_GRAPH = [os.environ.get("KS_FETCH_OUTSIDE", "0") != "1"]
 
 
 def _host_graph_key(factors, b, config: RegressionConfig):
@@ -1128,6 +1133,9 @@ def _fast_solve_host_graph(factors, b, config: RegressionConfig, with_loss: bool
                 entry.packed = _PackedChecks([(entry.flags.reshape(-1), _validation_handler(len(factors)))]
                                              + cap.items, entry.out["state"], entry.out["hist"])
                 entry.x_host = torch.empty(int(entry.out["x"].numel()), dtype=torch.float64).pin_memory()
+                if _FETCH_IN_GRAPH[0]:
+                    entry.packed.fetch()
+                    entry.x_host.copy_(entry.out["x"].reshape(-1), non_blocking=True)
         except Exception:
             _state.cache_drop(_HOST_GRAPHS, key)
             raise
@@ -1139,8 +1147,9 @@ def _fast_solve_host_graph(factors, b, config: RegressionConfig, with_loss: bool
     _LAST_LOOP_EVENTS[0] = entry.out["loop_events"]
     entry.graph.replay()
     out = entry.out
-    entry.packed.fetch()
-    entry.x_host.copy_(out["x"].reshape(-1), non_blocking=True)
+    if not _FETCH_IN_GRAPH[0]:
+        entry.packed.fetch()
+        entry.x_host.copy_(out["x"].reshape(-1), non_blocking=True)
     torch.cuda.current_stream().synchronize()
     _mark("richardson")
     try:
