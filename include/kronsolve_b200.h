@@ -478,7 +478,8 @@ int ks_sketch_rows(int32_t nf, const double* const* factors, const int64_t* rows
 int ks_chol_qr2_r(const double* A, int64_t n, int32_t d, double* R, int32_t* ok, void* stream);
 
 /* Statistical leverage scores of a numerically full-rank tall A: scores[i] = ||(A R^-1)_i||^2 with
- * R from CholeskyQR2 (= ridge_leverage_scores(compact_svd(a), 0), leverage.py:51-64, for
+ * R = R2 R1 from CholeskyQR2, formed as ||(Q1 R2^-1)_i||^2 from the first pass's Q1 = A R1^-1
+ * (= ridge_leverage_scores(compact_svd(a), 0), leverage.py:51-64, for
  * kappa(A) < ~3e6).  *ok = 0 when A is too ill-conditioned (scores undefined; use the compact SVD).
  * Synchronises the stream.  spectral_approx_rows' scores (leverage.py:235-252). */
 int ks_leverage_scores_tall(const double* A, int64_t n, int32_t d, double* scores, int32_t* ok, void* stream);
