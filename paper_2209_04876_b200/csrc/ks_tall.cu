@@ -101,7 +101,9 @@ __device__ __forceinline__ void cp16(void* dst, const void* src, bool valid) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(n) : "memory");
 }
 
-template <int MP, int NP, bool AK>
+// SYM (Gram A^T A: B == A, MP == NP, A m-fast): A staged once, only the m16 x n8 tiles that reach
+// the upper triangle (n0 + 8 > m0) computed, the upper entries written with their mirrors.
+template <int MP, int NP, bool AK, bool SYM = false>
 __global__ void __launch_bounds__(TT) tall_tn2_kernel(int M, int N, int64_t K, int64_t chunk,
                                                       const double* __restrict__ A, int64_t a_ld,
                                                       const double* __restrict__ B, int64_t b_ld,
@@ -109,8 +111,26 @@ __global__ void __launch_bounds__(TT) tall_tn2_kernel(int M, int N, int64_t K, i
   constexpr int LDK = TK2 + 4;               // A stored [m][k] (AK)
   constexpr int LDA = MP + 4, LDB = NP + 4;  // A stored [k][m]; B stored [k][n]
   constexpr int ASZ = AK ? MP * LDK : TK2 * LDA, BSZ = TK2 * LDB;
-  constexpr int TILES = (MP / 16) * (NP / 8);
+  static_assert(!SYM || (MP == NP && !AK), "SYM: square, A m-fast");
+  constexpr int MB = MP / 16, NB = NP / 8;
+  // SYM: upper tiles = sum over m-blocks mb of (NB - 2 mb)
+  constexpr int TILES = SYM ? MB * NB - MB * (MB - 1) : MB * NB;
   constexpr int PER_W = (TILES + TW - 1) / TW;
+  auto tile_mn = [](int tile, int& m0, int& n0) {
+    if (!SYM) {
+      m0 = (tile / NB) * 16;
+      n0 = (tile % NB) * 8;
+      return;
+    }
+    int mb = 0;
+#pragma unroll
+    for (int q = 0; q < MB; q++) {
+      const int cnt = NB - 2 * q;
+      if (mb == q && tile >= cnt) { tile -= cnt; mb = q + 1; }
+    }
+    m0 = mb * 16;
+    n0 = (2 * mb + tile) * 8;
+  };
   extern __shared__ __align__(16) double tsm2[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t4 = lane & 3;
   const int64_t kbeg = (int64_t)blockIdx.x * chunk;
@@ -120,6 +140,7 @@ __global__ void __launch_bounds__(TT) tall_tn2_kernel(int M, int N, int64_t K, i
     double* As = tsm2 + buf * (ASZ + BSZ);
     double* Bs = As + ASZ;
     const int64_t k0 = kbeg + (int64_t)sl * TK2;
+    (void)Bs;
     if (AK) {  // A(m, k) = A[m a_ld + k]: pairs along k
       for (int e = tid; e < MP * (TK2 / 2); e += TT) {
         const int mm = e / (TK2 / 2), kk = 2 * (e % (TK2 / 2));
@@ -135,7 +156,7 @@ __global__ void __launch_bounds__(TT) tall_tn2_kernel(int M, int N, int64_t K, i
         cp16(&As[kk * LDA + mm], ok ? A + gk * a_ld + mm : A, ok);
       }
     }
-    for (int e = tid; e < TK2 * (NP / 2); e += TT) {  // B(k, n) = B[k b_ld + n]: pairs along n
+    if (!SYM) for (int e = tid; e < TK2 * (NP / 2); e += TT) {  // B(k, n) = B[k b_ld + n]: pairs along n
       const int kk = e / (NP / 2), nn = 2 * (e % (NP / 2));
       const int64_t gk = k0 + kk;
       const bool ok = gk < kend && nn < N;  // N even (host)
@@ -156,12 +177,13 @@ __global__ void __launch_bounds__(TT) tall_tn2_kernel(int M, int N, int64_t K, i
     }
     __syncthreads();
     const double* As = tsm2 + (sl & 1) * (ASZ + BSZ);
-    const double* Bs = As + ASZ;
+    const double* Bs = SYM ? As : As + ASZ;  // SYM: LDA == LDB
 #pragma unroll
     for (int i = 0; i < PER_W; i++) {
       const int tile = warp + i * TW;
       if (tile < TILES) {
-        const int m0 = (tile / (NP / 8)) * 16, n0 = (tile % (NP / 8)) * 8;
+        int m0, n0;
+        tile_mn(tile, m0, n0);
 #pragma unroll
         for (int kk = 0; kk < TK2; kk += 4) {
           const double a0 = AK ? As[(m0 + g) * LDK + kk + t4] : As[(kk + t4) * LDA + m0 + g];
@@ -178,8 +200,20 @@ __global__ void __launch_bounds__(TT) tall_tn2_kernel(int M, int N, int64_t K, i
   for (int i = 0; i < PER_W; i++) {
     const int tile = warp + i * TW;
     if (tile < TILES) {
-      const int m0 = (tile / (NP / 8)) * 16, n0 = (tile % (NP / 8)) * 8;
+      int m0, n0;
+      tile_mn(tile, m0, n0);
       const int r0 = m0 + g, c0 = n0 + 2 * t4;
+      if (SYM) {  // each upper entry (r <= c) and its mirror, from the one accumulator that owns it
+#pragma unroll
+        for (int v = 0; v < 4; v++) {
+          const int r = r0 + (v >> 1) * 8, c = c0 + (v & 1);
+          if (r <= c && c < N) {
+            out[r * N + c] = acc[i][v];
+            out[c * N + r] = acc[i][v];
+          }
+        }
+        continue;
+      }
       if (r0 < M && c0 < N) out[r0 * N + c0] = acc[i][0];
       if (r0 < M && c0 + 1 < N) out[r0 * N + c0 + 1] = acc[i][1];
       if (r0 + 8 < M && c0 < N) out[(r0 + 8) * N + c0] = acc[i][2];
@@ -188,13 +222,13 @@ __global__ void __launch_bounds__(TT) tall_tn2_kernel(int M, int N, int64_t K, i
   }
 }
 
-template <int MP, int NP, bool AK>
+template <int MP, int NP, bool AK, bool SYM = false>
 void launch_tall2(cudaStream_t st, int nparts, int M, int N, int64_t K, int64_t chunk, const double* A, int64_t a_ld,
                   const double* B, int64_t b_ld, double* part) {
   constexpr int ASZ = AK ? MP * (TK2 + 4) : TK2 * (MP + 4), BSZ = TK2 * (NP + 4);
   const size_t smem = sizeof(double) * 2 * (ASZ + BSZ);
-  cudaFuncSetAttribute(tall_tn2_kernel<MP, NP, AK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  tall_tn2_kernel<MP, NP, AK><<<nparts, TT, smem, st>>>(M, N, K, chunk, A, a_ld, B, b_ld, part);
+  cudaFuncSetAttribute(tall_tn2_kernel<MP, NP, AK, SYM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  tall_tn2_kernel<MP, NP, AK, SYM><<<nparts, TT, smem, st>>>(M, N, K, chunk, A, a_ld, B, b_ld, part);
 }
 
 template <int MP, int NP>
@@ -228,6 +262,14 @@ int gemm_tn_tall_dmma(cudaStream_t st, int64_t M, int64_t N, int64_t K, double a
     KS_REQUIRE(part2.p, KS_ECUDA, "scratch allocation failed");
     const int np2_i = (int)nparts2;
     bool done = false;
+    // Gram A^T A (same operand, A m-fast, M = N in {16, 32, 64, 128}): the symmetric kernel
+    if (!akf && A == B && a_ld == b_ks && M == N && M == mp2 && mp2 != 80 && !ks::env(ks::ENV_TALL_OLD)) {
+      if (M == 16) launch_tall2<16, 16, false, true>(st, np2_i, (int)M, (int)N, K, chunk2, A, a_ld, B, b_ks, part2.p);
+      if (M == 32) launch_tall2<32, 32, false, true>(st, np2_i, (int)M, (int)N, K, chunk2, A, a_ld, B, b_ks, part2.p);
+      if (M == 64) launch_tall2<64, 64, false, true>(st, np2_i, (int)M, (int)N, K, chunk2, A, a_ld, B, b_ks, part2.p);
+      if (M == 128) launch_tall2<128, 128, false, true>(st, np2_i, (int)M, (int)N, K, chunk2, A, a_ld, B, b_ks, part2.p);
+      done = true;
+    }
 #define KS_TALL2(MM, NN)                                                                                         \
   if (!done && mp2 == MM && np2 == NN) {                                                                         \
     if (akf) launch_tall2<MM, NN, true>(st, np2_i, (int)M, (int)N, K, chunk2, A, a_ld, B, b_ks, part2.p);        \
